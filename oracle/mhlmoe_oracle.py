@@ -282,6 +282,7 @@ def cluster_plan(I: np.ndarray, N_e: int):
 class ForwardCache:
     mode: str
     Xs: np.ndarray                    # rnd(x W_in^T)           [T, D]
+    Xs_pre: np.ndarray | None = None  # x W_in^T before the storage rounding (fp64)
     I: list = field(default_factory=list)       # per head [T,k]
     g: list = field(default_factory=list)       # per head [T,k]
     S_sel: list = field(default_factory=list)   # per head [T,k]
@@ -308,8 +309,9 @@ def layer_forward(P: dict, x: np.ndarray, k: int, mode: str = "bf16",
     """
     N_h, d_h = _heads(P)
     x = np.asarray(x, np.float64)
-    Xs = round_storage(x @ np.asarray(P["W_in"], np.float64).T, mode)          # O1
-    C = ForwardCache(mode=mode, Xs=Xs)
+    Xs_pre = x @ np.asarray(P["W_in"], np.float64).T
+    Xs = round_storage(Xs_pre, mode)                                          # O1
+    C = ForwardCache(mode=mode, Xs=Xs, Xs_pre=Xs_pre)
     ys = []
     for h in range(N_h):
         X_h = Xs[:, h * d_h:(h + 1) * d_h]                                   # O2

@@ -1,0 +1,774 @@
+// capi.cpp — the C ABI (include/mhlmoe.h): plan validation/sizing, Head Parallel
+// orchestration of the per-rank steps, cuBLAS projections and the NCCL all-to-alls.
+//
+// Per-rank data layout in HBM (R12):
+//   Xs / recv1  [T_glob][HD]   HD = H_loc*d_h.  Rows are global tokens (source rank-major);
+//                              local head hl is the column block [hl*d_h, (hl+1)*d_h).
+//   send1       [G][T_loc][HD] destination-major output of F1 (G > 1 only)
+//   send2       [T_glob][HD]   = [G(dst)][T_loc][HD]: combine output, rows in global order
+//   recv2       [G(src)][T_loc][HD] -> permuted to cat [T_loc][D] (G > 1)
+//   idx, gate   [H_loc][T_glob][k];  perm/pos [H_loc][T_glob*k];  Yrep/dXrep [H_loc][T_glob*k][d_h]
+#include "../../include/mhlmoe.h"
+
+#include <cublas_v2.h>
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "kernels.h"
+#include "nccl.h"
+
+namespace {
+
+thread_local std::string g_last_error;
+
+mhl_status fail(mhl_status s, const std::string& msg) {
+  g_last_error = msg;
+  return s;
+}
+
+#define MHL_CUDA(expr)                                                                            \
+  do {                                                                                            \
+    cudaError_t e_ = (expr);                                                                      \
+    if (e_ != cudaSuccess)                                                                        \
+      return fail(MHL_ERR_CUDA, std::string(#expr) + ": " + cudaGetErrorString(e_));             \
+  } while (0)
+
+#define MHL_CUBLAS(expr)                                                                          \
+  do {                                                                                            \
+    cublasStatus_t e_ = (expr);                                                                   \
+    if (e_ != CUBLAS_STATUS_SUCCESS)                                                              \
+      return fail(MHL_ERR_CUDA, std::string(#expr) + ": cublas status " + std::to_string((int)e_)); \
+  } while (0)
+
+#define MHL_TRY(expr)                 \
+  do {                                \
+    mhl_status s_ = (expr);           \
+    if (s_ != MHL_OK) return s_;      \
+  } while (0)
+
+// ------------------------------------------------------------------------------------------
+// NCCL, loaded at runtime (the library must load on hosts without NCCL/GPU)
+// ------------------------------------------------------------------------------------------
+struct NcclApi {
+  bool loaded = false;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*GroupStart)() = nullptr;
+  ncclResult_t (*GroupEnd)() = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+
+NcclApi& nccl() {
+  static NcclApi api;
+  static bool tried = false;
+  if (tried) return api;
+  tried = true;
+  void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+  if (!h) {
+    const char* p = getenv("MHL_NCCL_LIB");
+    if (p) h = dlopen(p, RTLD_NOW | RTLD_GLOBAL);
+  }
+  if (!h) return api;
+#define LOAD(name) api.name = reinterpret_cast<decltype(api.name)>(dlsym(h, "nccl" #name))
+  LOAD(GetUniqueId); LOAD(CommInitRank); LOAD(CommDestroy); LOAD(Send); LOAD(Recv);
+  LOAD(GroupStart); LOAD(GroupEnd); LOAD(GetErrorString);
+#undef LOAD
+  api.loaded = api.GetUniqueId && api.CommInitRank && api.Send && api.Recv && api.GroupStart && api.GroupEnd;
+  return api;
+}
+
+#define MHL_NCCL(expr)                                                                            \
+  do {                                                                                            \
+    ncclResult_t e_ = (expr);                                                                     \
+    if (e_ != ncclSuccess)                                                                        \
+      return fail(MHL_ERR_NCCL, std::string(#expr) + ": " +                                      \
+                                    (nccl().GetErrorString ? nccl().GetErrorString(e_) : "?"));  \
+  } while (0)
+
+// ------------------------------------------------------------------------------------------
+// Config validation and buffer layout (pure host)
+// ------------------------------------------------------------------------------------------
+constexpr size_t kAlign = 256;
+inline size_t align_up(size_t v) { return (v + kAlign - 1) / kAlign * kAlign; }
+
+struct Dims {
+  int64_t T_loc, T_g, R;
+  int d, N_h, d_h, N_e, k, d_e, G, H, HD, D, el, dtype, rank;
+  bool loopback, simt;
+  int n_rt, max_tiles;
+};
+
+struct Bump {
+  size_t off = 0;
+  size_t take(size_t bytes) { size_t o = off; off += align_up(bytes); return o; }
+};
+
+// offsets inside one rank's saved region
+struct SavedLayout { size_t Xs, idx, gate, perm, pos, off, tiles, ntiles, cat, total; };
+// offsets inside one rank's workspace region (forward and backward alias each other)
+struct FwdLayout { size_t send1, Yrep, send2, recv2, hist, tilepref, counts, total; };
+struct BwdLayout { size_t send3, dY, dXrep, dg, dS, dH, gA, dwr_part, W_rT, send4, recv4, dXs, total; };
+
+SavedLayout saved_layout(const Dims& m) {
+  Bump b; SavedLayout L;
+  L.Xs = b.take((size_t)m.T_g * m.HD * m.el);
+  L.idx = b.take((size_t)m.H * m.R * 4);
+  L.gate = b.take((size_t)m.H * m.R * 4);
+  L.perm = b.take((size_t)m.H * m.R * 4);
+  L.pos = b.take((size_t)m.H * m.R * 4);
+  L.off = b.take((size_t)m.H * (m.N_e + 1) * 4);
+  L.tiles = b.take((size_t)m.max_tiles * sizeof(mhl::Tile));
+  L.ntiles = b.take(16);
+  L.cat = b.take((size_t)m.T_loc * m.D * m.el);
+  L.total = b.off;
+  return L;
+}
+
+FwdLayout fwd_layout(const Dims& m) {
+  Bump b; FwdLayout L;
+  L.send1 = b.take(m.G > 1 ? (size_t)m.T_loc * m.D * m.el : 0);
+  L.Yrep = b.take((size_t)m.H * m.R * m.d_h * m.el);
+  L.send2 = b.take(m.G > 1 ? (size_t)m.T_g * m.HD * m.el : 0);
+  L.recv2 = b.take(m.G > 1 ? (size_t)m.T_loc * m.D * m.el : 0);
+  L.hist = b.take((size_t)m.H * m.n_rt * m.N_e * 4);
+  L.tilepref = b.take((size_t)m.H * m.n_rt * m.N_e * 4);
+  L.counts = b.take((size_t)m.H * m.N_e * 4);
+  L.total = b.off;
+  return L;
+}
+
+BwdLayout bwd_layout(const Dims& m) {
+  Bump b; BwdLayout L;
+  L.send3 = b.take(m.G > 1 ? (size_t)m.T_loc * m.D * m.el : 0);
+  L.dY = b.take((size_t)m.T_g * m.HD * m.el);
+  L.dXrep = b.take((size_t)m.H * m.R * m.d_h * m.el);
+  L.dg = b.take((size_t)m.H * m.R * 4);
+  L.dS = b.take((size_t)m.H * m.R * 4);
+  L.dH = b.take((size_t)m.H * m.R * m.d_e * m.el);
+  L.gA = b.take((size_t)m.H * m.R * m.d_e * m.el);
+  L.dwr_part = b.take((size_t)m.H * m.n_rt * m.N_e * m.d_h * 4);
+  L.W_rT = b.take((size_t)m.H * m.N_e * m.d_h * 4);
+  L.send4 = b.take(m.G > 1 ? (size_t)m.T_g * m.HD * m.el : 0);
+  L.recv4 = b.take(m.G > 1 ? (size_t)m.T_loc * m.D * m.el : 0);
+  L.dXs = b.take((size_t)m.T_loc * m.D * m.el);
+  L.total = b.off;
+  return L;
+}
+
+mhl_status make_dims(const mhl_config* c, Dims* m) {
+  if (!c || !m) return fail(MHL_ERR_INVALID_ARGUMENT, "NULL config");
+  if (c->tokens <= 0 || c->d_model <= 0 || c->n_heads <= 0 || c->d_head <= 0 || c->n_experts <= 0 ||
+      c->d_expert <= 0 || c->world_size <= 0)
+    return fail(MHL_ERR_CONFIG, "all dimensions and world_size must be positive");
+  if (c->top_k < 1 || c->top_k > c->n_experts) return fail(MHL_ERR_CONFIG, "need 1 <= k <= N_e (S:213)");
+  if (c->world_size > c->n_heads || c->n_heads % c->world_size != 0)
+    return fail(MHL_ERR_CONFIG, "Head Parallel needs P <= N_h and N_h % P == 0 (P:803)");
+  const bool loop = (c->flags & MHL_FLAG_LOOPBACK) != 0;
+  if (!loop && (c->rank < 0 || c->rank >= c->world_size)) return fail(MHL_ERR_CONFIG, "rank out of range");
+  if (c->dtype != MHL_F32 && c->dtype != MHL_BF16) return fail(MHL_ERR_CONFIG, "dtype must be MHL_F32 or MHL_BF16");
+  if (c->top_k > 16) return fail(MHL_ERR_UNSUPPORTED, "top_k > 16 is not supported by the router kernel");
+  if (c->d_head % 8 != 0 || c->d_expert % 8 != 0 || c->d_model % 8 != 0)
+    return fail(MHL_ERR_UNSUPPORTED, "d_model, d_head and d_expert must be multiples of 8");
+  if (c->d_head > 512 || c->d_expert > 512) return fail(MHL_ERR_UNSUPPORTED, "d_head, d_expert <= 512");
+  m->T_loc = c->tokens;
+  m->G = c->world_size;
+  m->T_g = m->T_loc * m->G;
+  m->k = c->top_k;
+  m->R = m->T_g * m->k;
+  if (m->R >= (int64_t)1 << 31) return fail(MHL_ERR_UNSUPPORTED, "T_glob * k must be < 2^31");
+  m->d = c->d_model; m->N_h = c->n_heads; m->d_h = c->d_head; m->N_e = c->n_experts; m->d_e = c->d_expert;
+  m->H = m->N_h / m->G;
+  m->HD = m->H * m->d_h;
+  m->D = m->N_h * m->d_h;
+  m->dtype = c->dtype;
+  m->el = c->dtype == MHL_BF16 ? 2 : 4;
+  m->loopback = loop;
+  m->simt = (c->flags & MHL_FLAG_SIMT) != 0 || c->dtype == MHL_F32;
+  m->rank = loop ? 0 : c->rank;
+  m->n_rt = (int)((m->T_g + mhl::kRouterTile - 1) / mhl::kRouterTile);
+  const int64_t mt = (int64_t)m->H * ((m->R + mhl::kExpertBM - 1) / mhl::kExpertBM + m->N_e);
+  if (mt >= (int64_t)1 << 31) return fail(MHL_ERR_UNSUPPORTED, "too many tiles");
+  m->max_tiles = (int)mt;
+  const size_t router_smem = (size_t)m->el * m->d_h * mhl::kRouterTile + 4ull * m->d_h * 32 + 4ull * m->N_e;
+  const size_t rbwd_smem = 4ull * m->N_e * m->d_h + 8ull * mhl::kRouterTile * m->k;
+  if (router_smem > 200 * 1024 || rbwd_smem > 200 * 1024)
+    return fail(MHL_ERR_UNSUPPORTED, "d_head * N_e too large for the router kernels' shared memory");
+  return MHL_OK;
+}
+
+void fill_info(const Dims& m, mhl_plan_info* info) {
+  const int vr = m.loopback ? m.G : 1;  // regions per process
+  info->head_begin = m.loopback ? 0 : m.rank * m.H;
+  info->head_end = m.loopback ? m.N_h : (m.rank + 1) * m.H;
+  info->tokens_global = m.T_g;
+  info->a2a_bytes_per_peer = (uint64_t)m.T_loc * m.HD * m.el;
+  info->a2a_bytes_per_rank = info->a2a_bytes_per_peer * (uint64_t)(m.G - 1);
+  info->saved_bytes = (uint64_t)saved_layout(m).total * vr;
+  info->workspace_bytes = (uint64_t)std::max(fwd_layout(m).total, bwd_layout(m).total) * vr;
+  info->io_bytes = 4ull * align_up((size_t)m.T_loc * vr * m.d * m.el);
+  info->max_tiles = m.max_tiles;
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------------------------------
+// Plan
+// ------------------------------------------------------------------------------------------
+struct mhl_plan_s {
+  mhl_config cfg;
+  Dims m;
+  mhl_plan_info info;
+  cublasHandle_t blas = nullptr;
+  void* blas_ws = nullptr;
+  size_t blas_ws_bytes = 32u << 20;
+  ncclComm_t comm = nullptr;
+  int32_t* dflag = nullptr;   // device non-finite flag
+  int num_sms = 148;
+  std::atomic<uint64_t> launches{0};
+  uint64_t a2a_bytes_posted = 0;
+  // optional per-step CUDA-event timing (mhl_set_step_timing)
+  bool timing = false;
+  struct Rec { const char* name; cudaEvent_t a, b; };
+  std::vector<Rec> recs;
+  std::vector<cudaEvent_t> pool;
+  size_t pool_used = 0;
+  cudaEvent_t next_event() {
+    if (pool_used == pool.size()) {
+      cudaEvent_t e;
+      cudaEventCreate(&e);
+      pool.push_back(e);
+    }
+    return pool[pool_used++];
+  }
+};
+
+namespace {
+
+// Records CUDA events around one named step on the launching stream when timing is on.
+struct StepSpan {
+  mhl_plan p; const char* name; cudaStream_t s; cudaEvent_t a = nullptr;
+  StepSpan(mhl_plan p_, const char* n, cudaStream_t s_) : p(p_), name(n), s(s_) {
+    if (p->timing) { a = p->next_event(); cudaEventRecord(a, s); }
+  }
+  ~StepSpan() {
+    if (a) { cudaEvent_t b = p->next_event(); cudaEventRecord(b, s); p->recs.push_back({name, a, b}); }
+  }
+};
+#define MHL_SPAN(name) StepSpan span_##__LINE__(p, name, s)
+
+struct Gemm {
+  mhl_plan p;
+  cudaStream_t s;
+  // Row-major C[M,N] = alpha * op(A) op(B) + beta C; A is [M,K] (ta: stored [K,M]),
+  // B is [K,N] (tb: stored [N,K]).  Column-major cuBLAS computes C^T = op(B)^T op(A)^T.
+  mhl_status operator()(bool ta, bool tb, int64_t M, int64_t N, int64_t K, const void* A, int64_t lda,
+                        const void* B, int64_t ldb, void* C, int64_t ldc, bool c_f32, float beta) const {
+    const float alpha = 1.0f;
+    const bool bf = p->m.dtype == MHL_BF16;
+    const cudaDataType_t ab = bf ? CUDA_R_16BF : CUDA_R_32F;
+    const cudaDataType_t ct = c_f32 ? CUDA_R_32F : ab;
+    const cublasComputeType_t comp = bf ? CUBLAS_COMPUTE_32F : CUBLAS_COMPUTE_32F_PEDANTIC;
+    MHL_CUBLAS(cublasSetStream(p->blas, s));
+    MHL_CUBLAS(cublasGemmEx(p->blas, tb ? CUBLAS_OP_T : CUBLAS_OP_N, ta ? CUBLAS_OP_T : CUBLAS_OP_N, (int)N,
+                            (int)M, (int)K, &alpha, B, ab, (int)ldb, A, ab, (int)lda, &beta, C, ct, (int)ldc, comp,
+                            CUBLAS_GEMM_DEFAULT));
+    p->launches++;
+    return MHL_OK;
+  }
+};
+
+inline char* at(void* base, size_t off) { return static_cast<char*>(base) + off; }
+inline const char* at(const void* base, size_t off) { return static_cast<const char*>(base) + off; }
+
+// Equal-split all-to-all: block p of `send` ([G][blk]) goes to rank p, block q
+// of `recv` comes from rank q.  Self block by device copy.  Bytes are k-independent.
+mhl_status all_to_all(mhl_plan p, const void* send, void* recv, size_t blk_bytes, cudaStream_t s) {
+  const Dims& m = p->m;
+  const int r = m.rank;
+  MHL_CUDA(cudaMemcpyAsync(at(recv, r * blk_bytes), at(send, r * blk_bytes), blk_bytes, cudaMemcpyDeviceToDevice, s));
+  if (m.G == 1) return MHL_OK;
+  NcclApi& api = nccl();
+  MHL_NCCL(api.GroupStart());
+  for (int q = 0; q < m.G; ++q) {
+    if (q == r) continue;
+    MHL_NCCL(api.Send(at(send, q * blk_bytes), blk_bytes, ncclUint8, q, p->comm, s));
+    MHL_NCCL(api.Recv(at(recv, q * blk_bytes), blk_bytes, ncclUint8, q, p->comm, s));
+  }
+  MHL_NCCL(api.GroupEnd());
+  p->launches++;
+  p->a2a_bytes_posted += blk_bytes * (m.G - 1);
+  return MHL_OK;
+}
+
+// loopback all-to-all among G virtual ranks: recv_q block r <- send_r block q
+mhl_status all_to_all_loop(mhl_plan p, const std::vector<const void*>& send, const std::vector<void*>& recv,
+                           size_t blk_bytes, cudaStream_t s) {
+  const int G = p->m.G;
+  for (int r = 0; r < G; ++r)
+    for (int q = 0; q < G; ++q) {
+      MHL_CUDA(cudaMemcpyAsync(at(recv[q], r * blk_bytes), at(send[r], q * blk_bytes), blk_bytes,
+                               cudaMemcpyDeviceToDevice, s));
+      if (q != r) p->a2a_bytes_posted += blk_bytes;
+    }
+  return MHL_OK;
+}
+
+struct RankPtrs {   // one (virtual) rank's view
+  char* saved;
+  char* ws;
+  const void* x;
+  void* out;        // forward: out; backward: dx
+  const void* dout;
+  const float* W_r; const float* bias; const void* W1; const void* W2;   // local heads
+  float* dW_r; float* dW1; float* dW2;
+  int32_t* topk_idx; float* gates;
+};
+
+mhl_status check_kernels(mhl_plan p) {
+  (void)p;
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(MHL_ERR_CUDA, std::string("kernel launch: ") + cudaGetErrorString(e));
+  return MHL_OK;
+}
+
+// F3-F6 for one rank's local heads; input recv1 (= saved Xs), output rows into `yout` [T_g][HD]
+mhl_status moe_forward_local(mhl_plan p, const RankPtrs& R, void* yout, cudaStream_t s) {
+  const Dims& m = p->m;
+  const SavedLayout S = saved_layout(m);
+  const FwdLayout F = fwd_layout(m);
+  const void* Xs = R.saved + S.Xs;
+  int32_t* idx = (int32_t*)(R.saved + S.idx);
+  float* gate = (float*)(R.saved + S.gate);
+  int32_t* perm = (int32_t*)(R.saved + S.perm);
+  int32_t* pos = (int32_t*)(R.saved + S.pos);
+  int32_t* off = (int32_t*)(R.saved + S.off);
+  mhl::Tile* tiles = (mhl::Tile*)(R.saved + S.tiles);
+  int32_t* ntiles = (int32_t*)(R.saved + S.ntiles);
+  int32_t* hist = (int32_t*)(R.ws + F.hist);
+  {
+    MHL_SPAN("F3_router_topk");
+    mhl::launch_router_topk(m.dtype, Xs, m.HD, R.W_r, R.bias, m.H, m.T_g, m.d_h, m.N_e, m.k, idx, gate, hist, p->dflag, s);
+  }
+  {
+  MHL_SPAN("F4_cluster");
+  mhl::launch_cluster(m.H, m.T_g, m.k, m.N_e, idx, hist, (int32_t*)(R.ws + F.tilepref), (int32_t*)(R.ws + F.counts),
+                      off, perm, pos, tiles, ntiles, m.max_tiles, s);
+  }
+  void* Yrep = R.ws + F.Yrep;
+  {
+  MHL_SPAN("F5_expert_fwd");
+  if (m.simt || !mhl::expert_fwd_sm100_supported(m.d_h, m.d_e)) {
+    mhl::launch_expert_fwd_simt(m.dtype, tiles, ntiles, m.max_tiles, Xs, m.HD, perm, gate, R.W1, R.W2, m.T_g, m.k,
+                                m.N_e, m.d_h, m.d_e, Yrep, s);
+  } else {
+    mhl::launch_expert_fwd_sm100(tiles, ntiles, m.max_tiles, Xs, m.HD, perm, gate, R.W1, R.W2, m.T_g, m.k, m.N_e,
+                                 m.d_h, m.d_e, Yrep, p->num_sms, s);
+  }
+  }
+  {
+    MHL_SPAN("F6_combine");
+    mhl::launch_combine_fwd(m.dtype, Yrep, pos, m.H, m.T_g, m.k, m.d_h, yout, m.HD, s);
+  }
+  p->launches += 7;
+  if (R.topk_idx) MHL_CUDA(cudaMemcpyAsync(R.topk_idx, idx, (size_t)m.H * m.R * 4, cudaMemcpyDeviceToDevice, s));
+  if (R.gates) MHL_CUDA(cudaMemcpyAsync(R.gates, gate, (size_t)m.H * m.R * 4, cudaMemcpyDeviceToDevice, s));
+  return check_kernels(p);
+}
+
+// B5, B3, B6 for one rank's local heads; input dY [T_g][HD], output dXs rows into `dxout` [T_g][HD]
+mhl_status moe_backward_local(mhl_plan p, const RankPtrs& R, const void* dY, void* dxout, cudaStream_t s) {
+  const Dims& m = p->m;
+  const SavedLayout S = saved_layout(m);
+  const BwdLayout B = bwd_layout(m);
+  const void* Xs = R.saved + S.Xs;
+  const int32_t* idx = (const int32_t*)(R.saved + S.idx);
+  const float* gate = (const float*)(R.saved + S.gate);
+  const int32_t* perm = (const int32_t*)(R.saved + S.perm);
+  const int32_t* pos = (const int32_t*)(R.saved + S.pos);
+  const int32_t* off = (const int32_t*)(R.saved + S.off);
+  const mhl::Tile* tiles = (const mhl::Tile*)(R.saved + S.tiles);
+  const int32_t* ntiles = (const int32_t*)(R.saved + S.ntiles);
+  void* dXrep = R.ws + B.dXrep;
+  float* dg = (float*)(R.ws + B.dg);
+  float* dS = (float*)(R.ws + B.dS);
+  void* dH = R.ws + B.dH;
+  void* gA = R.ws + B.gA;
+  {
+    MHL_SPAN("B5_expert_bwd_dx");
+    mhl::launch_expert_bwd_simt(m.dtype, tiles, ntiles, m.max_tiles, Xs, m.HD, dY, m.HD, perm, gate, R.W1, R.W2, m.T_g,
+                                m.k, m.N_e, m.d_h, m.d_e, dXrep, dg, dH, gA, s);
+  }
+  if (R.dW1 || R.dW2) {
+    MHL_SPAN("B5_expert_bwd_dw");
+    mhl::launch_expert_dw_simt(m.dtype, off, Xs, m.HD, dY, m.HD, perm, dH, gA, m.H, m.T_g, m.k, m.N_e, m.d_h, m.d_e,
+                               R.dW1, R.dW2, s);
+  }
+  float* W_rT = (float*)(R.ws + B.W_rT);
+  {
+    MHL_SPAN("B3_router_bwd");
+    mhl::launch_router_bwd(m.dtype, Xs, m.HD, idx, gate, dg, m.H, m.T_g, m.k, m.d_h, m.N_e, dS,
+                           (float*)(R.ws + B.dwr_part), R.dW_r, s);
+    mhl::launch_transpose_wr(R.W_r, W_rT, m.H, m.d_h, m.N_e, s);
+  }
+  {
+    MHL_SPAN("B6_combine_bwd");
+    mhl::launch_combine_bwd(m.dtype, dXrep, pos, idx, dS, W_rT, m.H, m.T_g, m.k, m.d_h, m.N_e, dxout, m.HD, s);
+  }
+  p->launches += 6;
+  return check_kernels(p);
+}
+
+RankPtrs rank_view(mhl_plan p, int r, void* saved, void* ws, const void* x, void* out, const void* dout,
+                   const mhl_weights* w, const mhl_grads* g, int32_t* topk_idx, float* gates) {
+  const Dims& m = p->m;
+  const size_t sv = saved_layout(m).total;
+  const size_t wsz = std::max(fwd_layout(m).total, bwd_layout(m).total);
+  const int vr = m.loopback ? r : 0;            // region index
+  const int hp = m.loopback ? r : 0;            // head-block index inside the weight tensors
+  RankPtrs R{};
+  R.saved = static_cast<char*>(saved) + (size_t)vr * sv;
+  R.ws = static_cast<char*>(ws) + (size_t)vr * wsz;
+  const size_t tok = (size_t)m.T_loc * m.d * m.el * (m.loopback ? r : 0);
+  R.x = x ? at(x, tok) : nullptr;
+  R.out = out ? at(out, tok) : nullptr;
+  R.dout = dout ? at(dout, tok) : nullptr;
+  const size_t H = m.H;
+  R.W_r = w->W_r + (size_t)hp * H * m.d_h * m.N_e;
+  R.bias = w->bias + (size_t)hp * H * m.N_e;
+  const size_t we = (size_t)hp * H * m.N_e * m.d_e * m.d_h;
+  R.W1 = at(w->W1, we * m.el);
+  R.W2 = at(w->W2, we * m.el);
+  if (g) {
+    R.dW_r = g->dW_r ? g->dW_r + (size_t)hp * H * m.d_h * m.N_e : nullptr;
+    R.dW1 = g->dW1 ? g->dW1 + we : nullptr;
+    R.dW2 = g->dW2 ? g->dW2 + we : nullptr;
+  }
+  R.topk_idx = topk_idx ? topk_idx + (size_t)hp * H * m.R : nullptr;
+  R.gates = gates ? gates + (size_t)hp * H * m.R : nullptr;
+  return R;
+}
+
+mhl_status check_ws(mhl_plan p, const void* saved, const void* ws, size_t ws_bytes) {
+  if (!p) return fail(MHL_ERR_INVALID_ARGUMENT, "NULL plan");
+  if (!saved || !ws) return fail(MHL_ERR_INVALID_ARGUMENT, "NULL saved/workspace");
+  if (ws_bytes < p->info.workspace_bytes)
+    return fail(MHL_ERR_WORKSPACE_TOO_SMALL, "workspace_bytes < hp_plan_info().workspace_bytes");
+  return MHL_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+mhl_status hp_plan_query(const mhl_config* cfg, mhl_plan_info* info) {
+  if (!cfg || !info) return fail(MHL_ERR_INVALID_ARGUMENT, "NULL argument");
+  Dims m;
+  MHL_TRY(make_dims(cfg, &m));
+  fill_info(m, info);
+  return MHL_OK;
+}
+
+mhl_status mhl_get_unique_id(uint8_t id[128]) {
+  if (!id) return fail(MHL_ERR_INVALID_ARGUMENT, "NULL id");
+  NcclApi& api = nccl();
+  if (!api.loaded) return fail(MHL_ERR_NCCL, "libnccl.so.2 could not be loaded");
+  static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
+  ncclUniqueId uid;
+  MHL_NCCL(api.GetUniqueId(&uid));
+  memcpy(id, &uid, 128);
+  return MHL_OK;
+}
+
+mhl_status hp_plan(const mhl_config* cfg, const uint8_t* nccl_id, mhl_plan* out) {
+  if (!cfg || !out) return fail(MHL_ERR_INVALID_ARGUMENT, "NULL argument");
+  *out = nullptr;
+  Dims m;
+  MHL_TRY(make_dims(cfg, &m));
+  const bool need_nccl = m.G > 1 && !m.loopback;
+  if (need_nccl != (nccl_id != nullptr))
+    return fail(MHL_ERR_INVALID_ARGUMENT, "nccl_id must be non-NULL iff world_size > 1 without LOOPBACK");
+  mhl_plan p = new mhl_plan_s();
+  p->cfg = *cfg;
+  p->m = m;
+  fill_info(m, &p->info);
+  auto cleanup = [&](mhl_status s) { hp_plan_destroy(p); return s; };
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return cleanup(fail(MHL_ERR_CUDA, "no CUDA device"));
+  cudaDeviceProp prop;
+  if (cudaGetDeviceProperties(&prop, dev) != cudaSuccess) return cleanup(fail(MHL_ERR_CUDA, "cudaGetDeviceProperties"));
+  if (prop.major != 10) return cleanup(fail(MHL_ERR_UNSUPPORTED, "this library is built for sm_100a (B200)"));
+  p->num_sms = prop.multiProcessorCount;
+  if (cublasCreate(&p->blas) != CUBLAS_STATUS_SUCCESS) return cleanup(fail(MHL_ERR_CUDA, "cublasCreate"));
+  if (cudaMalloc(&p->blas_ws, p->blas_ws_bytes) != cudaSuccess) return cleanup(fail(MHL_ERR_CUDA, "cudaMalloc"));
+  if (cublasSetWorkspace(p->blas, p->blas_ws, p->blas_ws_bytes) != CUBLAS_STATUS_SUCCESS)
+    return cleanup(fail(MHL_ERR_CUDA, "cublasSetWorkspace"));
+  if (cudaMalloc(&p->dflag, 16) != cudaSuccess || cudaMemset(p->dflag, 0, 16) != cudaSuccess)
+    return cleanup(fail(MHL_ERR_CUDA, "cudaMalloc flag"));
+  if (need_nccl) {
+    NcclApi& api = nccl();
+    if (!api.loaded) return cleanup(fail(MHL_ERR_NCCL, "libnccl.so.2 could not be loaded"));
+    ncclUniqueId uid;
+    memcpy(&uid, nccl_id, 128);
+    ncclResult_t r = api.CommInitRank(&p->comm, m.G, uid, m.rank);
+    if (r != ncclSuccess) return cleanup(fail(MHL_ERR_NCCL, "ncclCommInitRank failed"));
+  }
+  *out = p;
+  return MHL_OK;
+}
+
+mhl_status hp_plan_info(mhl_plan p, mhl_plan_info* info) {
+  if (!p || !info) return fail(MHL_ERR_INVALID_ARGUMENT, "NULL argument");
+  *info = p->info;
+  return MHL_OK;
+}
+
+mhl_status hp_plan_destroy(mhl_plan p) {
+  if (!p) return MHL_OK;
+  if (p->comm && nccl().CommDestroy) nccl().CommDestroy(p->comm);
+  if (p->blas) cublasDestroy(p->blas);
+  if (p->blas_ws) cudaFree(p->blas_ws);
+  if (p->dflag) cudaFree(p->dflag);
+  for (auto e : p->pool) cudaEventDestroy(e);
+  delete p;
+  return MHL_OK;
+}
+
+mhl_status mhlmoe_forward(mhl_plan p, const void* x, const mhl_weights* w, void* out, void* saved, void* workspace,
+                          size_t workspace_bytes, int32_t* topk_idx, float* gates, void* stream) {
+  MHL_TRY(check_ws(p, saved, workspace, workspace_bytes));
+  if (!x || !w || !out || !w->W_in || !w->W_out || !w->W_r || !w->bias || !w->W1 || !w->W2)
+    return fail(MHL_ERR_INVALID_ARGUMENT, "NULL tensor");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const Dims& m = p->m;
+  const int VR = m.loopback ? m.G : 1;
+  const SavedLayout S = saved_layout(m);
+  const FwdLayout F = fwd_layout(m);
+  Gemm gemm{p, s};
+  std::vector<RankPtrs> ranks;
+  for (int r = 0; r < VR; ++r)
+    ranks.push_back(rank_view(p, r, saved, workspace, x, out, nullptr, w, nullptr, topk_idx, gates));
+  const size_t blk = (size_t)m.T_loc * m.HD * m.el;
+  // F1: Xs = x W_in^T, written destination-major (Eq. 5)
+  for (int r = 0; r < VR; ++r) {
+    MHL_SPAN("F1_proj_in");
+    const RankPtrs& R = ranks[r];
+    if (m.G == 1) {
+      MHL_TRY(gemm(false, true, m.T_loc, m.D, m.d, R.x, m.d, w->W_in, m.d, R.saved + S.Xs, m.D, false, 0.0f));
+    } else {
+      for (int q = 0; q < m.G; ++q)
+        MHL_TRY(gemm(false, true, m.T_loc, m.HD, m.d, R.x, m.d, at(w->W_in, (size_t)q * m.HD * m.d * m.el), m.d,
+                     R.ws + F.send1 + q * blk, m.HD, false, 0.0f));
+    }
+  }
+  // F2: all-to-all #1
+  if (m.G > 1) {
+    MHL_SPAN("F2_a2a");
+    if (m.loopback) {
+      std::vector<const void*> snd; std::vector<void*> rcv;
+      for (auto& R : ranks) { snd.push_back(R.ws + F.send1); rcv.push_back(R.saved + S.Xs); }
+      MHL_TRY(all_to_all_loop(p, snd, rcv, blk, s));
+    } else {
+      MHL_TRY(all_to_all(p, ranks[0].ws + F.send1, ranks[0].saved + S.Xs, blk, s));
+    }
+  }
+  // F3-F6 per rank
+  for (int r = 0; r < VR; ++r) {
+    const RankPtrs& R = ranks[r];
+    void* yout = m.G == 1 ? (void*)(R.saved + S.cat) : (void*)(R.ws + F.send2);
+    MHL_TRY(moe_forward_local(p, R, yout, s));
+  }
+  // F7: all-to-all #2, then cat [T_loc][D]
+  if (m.G > 1) {
+    MHL_SPAN("F7_a2a_permute");
+    if (m.loopback) {
+      std::vector<const void*> snd; std::vector<void*> rcv;
+      for (auto& R : ranks) { snd.push_back(R.ws + F.send2); rcv.push_back(R.ws + F.recv2); }
+      MHL_TRY(all_to_all_loop(p, snd, rcv, blk, s));
+    } else {
+      MHL_TRY(all_to_all(p, ranks[0].ws + F.send2, ranks[0].ws + F.recv2, blk, s));
+    }
+    for (auto& R : ranks) {
+      mhl::launch_permute_blocks(m.dtype, R.ws + F.recv2, R.saved + S.cat, m.G, m.T_loc, m.HD, s);
+      p->launches++;
+    }
+  }
+  // F8: out = cat W_out^T (Eq. 6)
+  for (auto& R : ranks) {
+    MHL_SPAN("F8_proj_out");
+    MHL_TRY(gemm(false, true, m.T_loc, m.d, m.D, R.saved + S.cat, m.D, w->W_out, m.D, R.out, m.d, false, 0.0f));
+  }
+  return check_kernels(p);
+}
+
+mhl_status mhlmoe_backward(mhl_plan p, const void* x, const mhl_weights* w, const void* d_out, const void* saved,
+                           void* dx, const mhl_grads* grads, void* workspace, size_t workspace_bytes, void* stream) {
+  MHL_TRY(check_ws(p, saved, workspace, workspace_bytes));
+  if (!x || !w || !d_out || !dx || !grads) return fail(MHL_ERR_INVALID_ARGUMENT, "NULL tensor");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const Dims& m = p->m;
+  const int VR = m.loopback ? m.G : 1;
+  const SavedLayout S = saved_layout(m);
+  const BwdLayout B = bwd_layout(m);
+  Gemm gemm{p, s};
+  std::vector<RankPtrs> ranks;
+  for (int r = 0; r < VR; ++r)
+    ranks.push_back(rank_view(p, r, const_cast<void*>(saved), workspace, x, dx, d_out, w, grads, nullptr, nullptr));
+  const size_t blk = (size_t)m.T_loc * m.HD * m.el;
+  // B8: dcat = dout W_out (destination-major), dW_out = dout^T cat (rank partial; loopback: summed)
+  for (int r = 0; r < VR; ++r) {
+    MHL_SPAN("B8_proj_out_bwd");
+    const RankPtrs& R = ranks[r];
+    if (m.G == 1) {
+      MHL_TRY(gemm(false, false, m.T_loc, m.D, m.d, R.dout, m.d, w->W_out, m.D, R.ws + B.dY, m.D, false, 0.0f));
+    } else {
+      for (int q = 0; q < m.G; ++q)
+        MHL_TRY(gemm(false, false, m.T_loc, m.HD, m.d, R.dout, m.d, at(w->W_out, (size_t)q * m.HD * m.el), m.D,
+                     R.ws + B.send3 + q * blk, m.HD, false, 0.0f));
+    }
+    if (grads->dW_out)
+      MHL_TRY(gemm(true, false, m.d, m.D, m.T_loc, R.dout, m.d, R.saved + S.cat, m.D, grads->dW_out, m.D, true,
+                   r == 0 ? 0.0f : 1.0f));
+  }
+  // B7: all-to-all #3
+  if (m.G > 1) {
+    MHL_SPAN("B7_a2a");
+    if (m.loopback) {
+      std::vector<const void*> snd; std::vector<void*> rcv;
+      for (auto& R : ranks) { snd.push_back(R.ws + B.send3); rcv.push_back(R.ws + B.dY); }
+      MHL_TRY(all_to_all_loop(p, snd, rcv, blk, s));
+    } else {
+      MHL_TRY(all_to_all(p, ranks[0].ws + B.send3, ranks[0].ws + B.dY, blk, s));
+    }
+  }
+  // B5, B3, B6 per rank
+  for (int r = 0; r < VR; ++r) {
+    const RankPtrs& R = ranks[r];
+    void* dxout = m.G == 1 ? (void*)(R.ws + B.dXs) : (void*)(R.ws + B.send4);
+    MHL_TRY(moe_backward_local(p, R, R.ws + B.dY, dxout, s));
+  }
+  // B2: all-to-all #4, then dXs [T_loc][D]
+  if (m.G > 1) {
+    MHL_SPAN("B2_a2a_permute");
+    if (m.loopback) {
+      std::vector<const void*> snd; std::vector<void*> rcv;
+      for (auto& R : ranks) { snd.push_back(R.ws + B.send4); rcv.push_back(R.ws + B.recv4); }
+      MHL_TRY(all_to_all_loop(p, snd, rcv, blk, s));
+    } else {
+      MHL_TRY(all_to_all(p, ranks[0].ws + B.send4, ranks[0].ws + B.recv4, blk, s));
+    }
+    for (auto& R : ranks) {
+      mhl::launch_permute_blocks(m.dtype, R.ws + B.recv4, R.ws + B.dXs, m.G, m.T_loc, m.HD, s);
+      p->launches++;
+    }
+  }
+  // B1: dx = dXs W_in; dW_in = dXs^T x (rank partial; loopback: summed)
+  for (int r = 0; r < VR; ++r) {
+    MHL_SPAN("B1_proj_in_bwd");
+    const RankPtrs& R = ranks[r];
+    MHL_TRY(gemm(false, false, m.T_loc, m.d, m.D, R.ws + B.dXs, m.D, w->W_in, m.d, R.out, m.d, false, 0.0f));
+    if (grads->dW_in)
+      MHL_TRY(gemm(true, false, m.D, m.d, m.T_loc, R.ws + B.dXs, m.D, R.x, m.d, grads->dW_in, m.d, true,
+                   r == 0 ? 0.0f : 1.0f));
+  }
+  return check_kernels(p);
+}
+
+mhl_status mhlmoe_train_step_host(mhl_plan p, const void* x_host, const void* dout_host, const mhl_weights* w,
+                                  void* out_host, void* dx_host, const mhl_grads* grads, void* io, void* saved,
+                                  void* workspace, size_t workspace_bytes, void* stream) {
+  if (!p || !x_host || !dout_host || !out_host || !dx_host || !io)
+    return fail(MHL_ERR_INVALID_ARGUMENT, "NULL argument");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const Dims& m = p->m;
+  const size_t n = (size_t)m.T_loc * (m.loopback ? m.G : 1) * m.d * m.el;
+  const size_t a = align_up(n);
+  char* xd = static_cast<char*>(io);
+  char* dd = xd + a;
+  char* od = dd + a;
+  char* gd = od + a;
+  MHL_CUDA(cudaMemcpyAsync(xd, x_host, n, cudaMemcpyHostToDevice, s));
+  MHL_CUDA(cudaMemcpyAsync(dd, dout_host, n, cudaMemcpyHostToDevice, s));
+  MHL_TRY(mhlmoe_forward(p, xd, w, od, saved, workspace, workspace_bytes, nullptr, nullptr, stream));
+  MHL_TRY(mhlmoe_backward(p, xd, w, dd, saved, gd, grads, workspace, workspace_bytes, stream));
+  MHL_CUDA(cudaMemcpyAsync(out_host, od, n, cudaMemcpyDeviceToHost, s));
+  MHL_CUDA(cudaMemcpyAsync(dx_host, gd, n, cudaMemcpyDeviceToHost, s));
+  return MHL_OK;
+}
+
+mhl_status mhl_check_device_status(mhl_plan p) {
+  if (!p) return fail(MHL_ERR_INVALID_ARGUMENT, "NULL plan");
+  int32_t f = 0;
+  MHL_CUDA(cudaMemcpy(&f, p->dflag, 4, cudaMemcpyDeviceToHost));
+  if (f) {
+    MHL_CUDA(cudaMemset(p->dflag, 0, 4));
+    return fail(MHL_ERR_NONFINITE, "non-finite router score/key encountered (R7)");
+  }
+  return MHL_OK;
+}
+
+uint64_t mhl_launch_count(mhl_plan p) { return p ? p->launches.load() : 0; }
+
+mhl_status mhl_set_step_timing(mhl_plan p, int enable) {
+  if (!p) return fail(MHL_ERR_INVALID_ARGUMENT, "NULL plan");
+  p->timing = enable != 0;
+  p->recs.clear();
+  p->pool_used = 0;
+  return MHL_OK;
+}
+
+int32_t mhl_step_times(mhl_plan p, char* names, size_t names_cap, double* ms, int32_t* calls, int32_t max_steps) {
+  if (!p) return -1;
+  if (!p->recs.empty()) cudaEventSynchronize(p->recs.back().b);
+  std::vector<std::string> order;
+  std::vector<double> tot;
+  std::vector<int32_t> cnt;
+  for (auto& r : p->recs) {
+    float t = 0.f;
+    cudaEventElapsedTime(&t, r.a, r.b);
+    size_t i = 0;
+    while (i < order.size() && order[i] != r.name) ++i;
+    if (i == order.size()) { order.push_back(r.name); tot.push_back(0.0); cnt.push_back(0); }
+    tot[i] += t; cnt[i] += 1;
+  }
+  std::string joined;
+  for (size_t i = 0; i < order.size(); ++i) {
+    if (i) joined += ",";
+    joined += order[i];
+    if ((int)i < max_steps) { if (ms) ms[i] = tot[i]; if (calls) calls[i] = cnt[i]; }
+  }
+  if (names && names_cap) { strncpy(names, joined.c_str(), names_cap - 1); names[names_cap - 1] = 0; }
+  p->recs.clear();
+  p->pool_used = 0;
+  return (int32_t)order.size();
+}
+
+uint64_t mhl_a2a_bytes_posted(mhl_plan p) { return p ? p->a2a_bytes_posted : 0; }
+
+const char* mhl_status_string(mhl_status s) {
+  switch (s) {
+    case MHL_OK: return "MHL_OK";
+    case MHL_ERR_INVALID_ARGUMENT: return "MHL_ERR_INVALID_ARGUMENT";
+    case MHL_ERR_CONFIG: return "MHL_ERR_CONFIG";
+    case MHL_ERR_WORKSPACE_TOO_SMALL: return "MHL_ERR_WORKSPACE_TOO_SMALL";
+    case MHL_ERR_UNSUPPORTED: return "MHL_ERR_UNSUPPORTED";
+    case MHL_ERR_CUDA: return "MHL_ERR_CUDA";
+    case MHL_ERR_NCCL: return "MHL_ERR_NCCL";
+    case MHL_ERR_NONFINITE: return "MHL_ERR_NONFINITE";
+  }
+  return "MHL_ERR_UNKNOWN";
+}
+
+const char* mhl_last_error(void) { return g_last_error.c_str(); }
+
+}  // extern "C"

@@ -1,0 +1,159 @@
+// cluster.cu — F4: token clustering (Fig. 2, P:941-P:949, P:970-P:972).
+//
+// Replicas r = t*k + j of each head are stably sorted by expert (a counting sort:
+// deterministic, integer-exact, dropless P:566/P:977):
+//   pos(r) = off[e] + tilepref[tile(t)][e] + rank of r among the tile's replicas of e
+// where tilepref is the exclusive scan over router tiles of the per-tile expert
+// histogram emitted by F3.  The expert segments are then cut into tiles of
+// kExpertBM rows — the block-sparse mask of Eq. 7 as a tile list.
+#include "kernels.h"
+
+namespace mhl {
+
+namespace {
+
+// (1) per (h, e): exclusive scan over router tiles of hist[h][tile][e]; total -> counts[h][e]
+__global__ void __launch_bounds__(256)
+tile_prefix_kernel(const int32_t* __restrict__ hist, int32_t* __restrict__ tilepref, int32_t* __restrict__ counts,
+                   int n_rt, int N_e) {
+  const int e = blockIdx.x, h = blockIdx.y;
+  __shared__ int warp_sums[8];
+  __shared__ int carry;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (int base = 0; base < n_rt; base += 256) {
+    const int tt = base + threadIdx.x;
+    const size_t o = ((size_t)h * n_rt + tt) * N_e + e;
+    const int v = (tt < n_rt) ? hist[o] : 0;
+    int incl = v;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const int n = __shfl_up_sync(0xffffffffu, incl, d);
+      if (lane >= d) incl += n;
+    }
+    if (lane == 31) warp_sums[wid] = incl;
+    __syncthreads();
+    int wpre = 0;
+    for (int w = 0; w < wid; ++w) wpre += warp_sums[w];
+    const int c = carry;
+    if (tt < n_rt) tilepref[o] = c + wpre + incl - v;
+    __syncthreads();
+    if (threadIdx.x == 255) carry = c + wpre + incl;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) counts[(size_t)h * N_e + e] = carry;
+}
+
+// block-wide exclusive scan over 1024 threads; *total (shared) receives the block sum
+__device__ int block_exclusive_scan_1024(int v, int* s_warp, int* total) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  int incl = v;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const int n = __shfl_up_sync(0xffffffffu, incl, d);
+    if (lane >= d) incl += n;
+  }
+  if (lane == 31) s_warp[wid] = incl;
+  __syncthreads();
+  if (wid == 0) {
+    const int w = s_warp[lane];
+    int wi = w;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const int n = __shfl_up_sync(0xffffffffu, wi, d);
+      if (lane >= d) wi += n;
+    }
+    s_warp[32 + lane] = wi - w;        // exclusive prefix of each warp
+    if (lane == 31) *total = wi;
+  }
+  __syncthreads();
+  const int r = s_warp[32 + wid] + incl - v;
+  __syncthreads();
+  return r;
+}
+
+// (2) single CTA: off[h][e] = exclusive scan over e of counts (per head), and the tile
+// list over (h, e) in order, each expert segment cut into kExpertBM-row tiles.
+__global__ void __launch_bounds__(1024)
+offsets_tiles_kernel(const int32_t* __restrict__ counts, int32_t* __restrict__ off, Tile* __restrict__ tiles,
+                     int32_t* __restrict__ ntiles, int H, int N_e, int max_tiles) {
+  __shared__ int s_warp[64];
+  __shared__ int s_tot;
+  int carry_t = 0;
+  for (int h = 0; h < H; ++h) {
+    int carry_r = 0;
+    for (int base = 0; base < N_e; base += 1024) {
+      const int e = base + threadIdx.x;
+      const int c = (e < N_e) ? counts[(size_t)h * N_e + e] : 0;
+      const int nt = (c + kExpertBM - 1) / kExpertBM;
+      const int rx = block_exclusive_scan_1024(c, s_warp, &s_tot);
+      const int rtot = s_tot;
+      __syncthreads();
+      const int tx = block_exclusive_scan_1024(nt, s_warp, &s_tot);
+      const int ttot = s_tot;
+      __syncthreads();
+      if (e < N_e) {
+        const int row_off = carry_r + rx;
+        off[(size_t)h * (N_e + 1) + e] = row_off;
+        for (int i = 0; i < nt; ++i) {
+          const int ti = carry_t + tx + i;
+          if (ti < max_tiles) {
+            Tile tl;
+            tl.head = h; tl.expert = e; tl.row0 = row_off + i * kExpertBM;
+            tl.rows = min(kExpertBM, c - i * kExpertBM);
+            tiles[ti] = tl;
+          }
+        }
+      }
+      carry_r += rtot;
+      carry_t += ttot;
+    }
+    if (threadIdx.x == 0) off[(size_t)h * (N_e + 1) + N_e] = carry_r;
+  }
+  if (threadIdx.x == 0) *ntiles = min(carry_t, max_tiles);
+}
+
+// (3) per (h, router tile): stable ranks inside the tile via warp match, scatter perm/pos
+__global__ void __launch_bounds__(32)
+scatter_kernel(const int32_t* __restrict__ idx, const int32_t* __restrict__ off,
+               const int32_t* __restrict__ tilepref, int32_t* __restrict__ perm, int32_t* __restrict__ pos,
+               int64_t T, int k, int N_e, int n_rt) {
+  extern __shared__ int cnt[];
+  const int tt = blockIdx.x, h = blockIdx.y, lane = threadIdx.x;
+  for (int e = lane; e < N_e; e += 32) cnt[e] = 0;
+  __syncwarp();
+  const int64_t r0 = (int64_t)tt * kRouterTile * k;
+  const int64_t r1 = min((int64_t)(tt + 1) * kRouterTile, T) * k;
+  const int32_t* idx_h = idx + (size_t)h * T * k;
+  const int32_t* offh = off + (size_t)h * (N_e + 1);
+  const int32_t* pre = tilepref + ((size_t)h * n_rt + tt) * N_e;
+  for (int64_t base = r0; base < r1; base += 32) {
+    const int64_t r = base + lane;
+    const bool act = r < r1;
+    const int e = act ? idx_h[r] : -1 - lane;   // unique dummy per inactive lane
+    const unsigned mask = __match_any_sync(0xffffffffu, e);
+    const int rank = __popc(mask & ((1u << lane) - 1u));
+    if (act) {
+      const int p = offh[e] + pre[e] + cnt[e] + rank;
+      perm[(size_t)h * T * k + p] = (int32_t)r;
+      pos[(size_t)h * T * k + r] = p;
+    }
+    __syncwarp();
+    if (act && rank == 0) cnt[e] += __popc(mask);
+    __syncwarp();
+  }
+}
+
+}  // namespace
+
+void launch_cluster(int H, int64_t T, int k, int N_e, const int32_t* idx, const int32_t* hist, int32_t* tilepref,
+                    int32_t* counts, int32_t* off, int32_t* perm, int32_t* pos, Tile* tiles, int32_t* ntiles,
+                    int max_tiles, cudaStream_t s) {
+  const int n_rt = (int)((T + kRouterTile - 1) / kRouterTile);
+  tile_prefix_kernel<<<dim3(N_e, H), 256, 0, s>>>(hist, tilepref, counts, n_rt, N_e);
+  offsets_tiles_kernel<<<1, 1024, 0, s>>>(counts, off, tiles, ntiles, H, N_e, max_tiles);
+  scatter_kernel<<<dim3(n_rt, H), 32, sizeof(int) * N_e, s>>>(idx, off, tilepref, perm, pos, T, k, N_e, n_rt);
+}
+
+}  // namespace mhl

@@ -1,0 +1,68 @@
+// kernels.h — internal (non-ABI) launch interface of the kernel translation units.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include "common.cuh"
+
+namespace mhl {
+
+constexpr int kRouterTile = 128;   // tokens per router CTA (= clustering tile of F4)
+constexpr int kExpertBM = 128;     // replica rows per expert tile (tcgen05 M)
+
+// ---- F3: router + online top-k + gates (SIMT fp32-FMA path). idx/gate [H][T][k];
+// hist [H][ceil(T/128)][N_e]; flag set to 1 on a non-finite key.
+void launch_router_topk(int dtype, const void* Xs, int64_t ldx, const float* W_r, const float* bias,
+                        int H, int64_t T, int d_h, int N_e, int k, int32_t* idx, float* gate,
+                        int32_t* hist, int32_t* flag, cudaStream_t s);
+
+// ---- F4: clustering.  tilepref [H][n_rt][N_e] (scratch), counts [H][N_e] (scratch),
+// off [H][N_e+1], perm/pos [H][T*k], tiles (<= max_tiles), ntiles[1].
+void launch_cluster(int H, int64_t T, int k, int N_e, const int32_t* idx, const int32_t* hist,
+                    int32_t* tilepref, int32_t* counts, int32_t* off, int32_t* perm, int32_t* pos,
+                    Tile* tiles, int32_t* ntiles, int max_tiles, cudaStream_t s);
+
+// ---- F5 (SIMT reference): Yrep[h][row][c] = gate * gelu(X W1_e^T) W2_e for sorted rows.
+void launch_expert_fwd_simt(int dtype, const Tile* tiles, const int32_t* ntiles, int max_tiles,
+                            const void* Xs, int64_t ldx, const int32_t* perm, const float* gate,
+                            const void* W1, const void* W2, int64_t T, int k, int N_e, int d_h, int d_e,
+                            void* Yrep, cudaStream_t s);
+
+// ---- F6: y[t][h*d_h+c] = sum_j Yrep[h][pos[h][t*k+j]][c]  (fixed j order), out ld = ldo.
+void launch_combine_fwd(int dtype, const void* Yrep, const int32_t* pos, int H, int64_t T, int k, int d_h,
+                        void* out, int64_t ldo, cudaStream_t s);
+
+// ---- [G][T_loc][HD] -> [T_loc][G*HD]
+void launch_permute_blocks(int dtype, const void* src, void* dst, int G, int64_t T_loc, int64_t HD, cudaStream_t s);
+
+// ---- B5 (SIMT reference): per tile dXrep (sorted rows), dg (replica order), dH, gA (sorted rows).
+void launch_expert_bwd_simt(int dtype, const Tile* tiles, const int32_t* ntiles, int max_tiles,
+                            const void* Xs, int64_t ldx, const void* dY, int64_t ldy, const int32_t* perm,
+                            const float* gate, const void* W1, const void* W2, int64_t T, int k, int N_e,
+                            int d_h, int d_e, void* dXrep, float* dg, void* dH, void* gA, cudaStream_t s);
+
+// ---- B5 weight gradients (SIMT reference): dW1/dW2 per (h,e) in sorted-row order.
+void launch_expert_dw_simt(int dtype, const int32_t* off, const void* Xs, int64_t ldx, const void* dY,
+                           int64_t ldy, const int32_t* perm, const void* dH, const void* gA, int H, int64_t T,
+                           int k, int N_e, int d_h, int d_e, float* dW1, float* dW2, cudaStream_t s);
+
+// ---- B3: dS = g (dg - sum g dg); dW_r partials per 128-token chunk; then ordered reduce.
+void launch_router_bwd(int dtype, const void* Xs, int64_t ldx, const int32_t* idx, const float* gate,
+                       const float* dg, int H, int64_t T, int k, int d_h, int N_e, float* dS,
+                       float* dwr_partial, float* dW_r, cudaStream_t s);
+
+// ---- W_rT[h][e][i] = W_r[h][i][e]
+void launch_transpose_wr(const float* W_r, float* W_rT, int H, int d_h, int N_e, cudaStream_t s);
+
+// ---- B6: dXs[t][h*d_h+c] = sum_j dXrep[h][pos][c] + sum_j dS[h][t][j] * W_rT[h][idx][c]
+void launch_combine_bwd(int dtype, const void* dXrep, const int32_t* pos, const int32_t* idx,
+                        const float* dS, const float* W_rT, int H, int64_t T, int k, int d_h, int N_e,
+                        void* out, int64_t ldo, cudaStream_t s);
+
+// ---- tcgen05 (sm_100a) expert kernels, bf16 only.  Return false if the shape is unsupported.
+bool expert_fwd_sm100_supported(int d_h, int d_e);
+void launch_expert_fwd_sm100(const Tile* tiles, const int32_t* ntiles, int max_tiles, const void* Xs,
+                             int64_t ldx, const int32_t* perm, const float* gate, const void* W1,
+                             const void* W2, int64_t T, int k, int N_e, int d_h, int d_e, void* Yrep,
+                             int num_sms, cudaStream_t s);
+
+}  // namespace mhl

@@ -1,0 +1,422 @@
+// simt.cu — CUDA-core kernels of the path: the HBM-bound passes (combine F6/B6,
+// block permutes, router backward B3) and the SIMT reference versions of the expert
+// FFN (F5/B5) used in fp32 mode and as the bf16 cross-check path (MHL_FLAG_SIMT).
+#include <algorithm>
+#include "kernels.h"
+
+namespace mhl {
+
+namespace {
+
+constexpr int kSub = 32;    // rows per SIMT sub-tile
+
+// ---------------------------------------------------------------------------------------------
+// F5 (SIMT): for one expert tile, Yrep[row] = g * gelu(x W1_e^T) W2_e      (Eq. 1)
+// ---------------------------------------------------------------------------------------------
+template <typename E>
+__global__ void __launch_bounds__(256)
+expert_fwd_simt_kernel(const Tile* __restrict__ tiles, const int32_t* __restrict__ ntiles,
+                       const E* __restrict__ Xs, int64_t ldx, const int32_t* __restrict__ perm,
+                       const float* __restrict__ gate, const E* __restrict__ W1, const E* __restrict__ W2,
+                       int64_t T, int k, int N_e, int d_h, int d_e, E* __restrict__ Yrep) {
+  if ((int)blockIdx.x >= *ntiles) return;
+  const Tile tl = tiles[blockIdx.x];
+  extern __shared__ __align__(16) float sm[];
+  float* Xsub = sm;                                   // [kSub][d_h+1]
+  float* Asub = Xsub + kSub * (d_h + 1);              // [kSub][d_e+1]
+  float* gsub = Asub + kSub * (d_e + 1);              // [kSub]
+  const int64_t R = T * k;
+  const size_t wofs = ((size_t)tl.head * N_e + tl.expert) * d_e * d_h;
+  const E* w1 = W1 + wofs;
+  const E* w2 = W2 + wofs;
+  for (int s0 = 0; s0 < tl.rows; s0 += kSub) {
+    const int nr = min(kSub, tl.rows - s0);
+    __syncthreads();
+    for (int o = threadIdx.x; o < kSub * d_h; o += blockDim.x) {
+      const int r = o / d_h, c = o % d_h;
+      float v = 0.0f;
+      if (r < nr) {
+        const int rep = perm[(size_t)tl.head * R + tl.row0 + s0 + r];
+        v = to_f(Xs[(int64_t)(rep / k) * ldx + (int64_t)tl.head * d_h + c]);
+      }
+      Xsub[r * (d_h + 1) + c] = v;
+    }
+    for (int r = threadIdx.x; r < kSub; r += blockDim.x) {
+      float g = 0.0f;
+      if (r < nr) {
+        const int rep = perm[(size_t)tl.head * R + tl.row0 + s0 + r];
+        g = gate[(size_t)tl.head * R + rep];
+      }
+      gsub[r] = g;
+    }
+    __syncthreads();
+    for (int o = threadIdx.x; o < kSub * d_e; o += blockDim.x) {
+      const int r = o / d_e, f = o % d_e;
+      float acc = 0.0f;
+      for (int c = 0; c < d_h; ++c) acc = fmaf(Xsub[r * (d_h + 1) + c], to_f(w1[(size_t)f * d_h + c]), acc);
+      Asub[r * (d_e + 1) + f] = gelu_f(acc);
+    }
+    __syncthreads();
+    for (int o = threadIdx.x; o < kSub * d_h; o += blockDim.x) {
+      const int r = o / d_h, c = o % d_h;
+      if (r >= nr) continue;
+      float acc = 0.0f;
+      for (int f = 0; f < d_e; ++f) acc = fmaf(Asub[r * (d_e + 1) + f], to_f(w2[(size_t)f * d_h + c]), acc);
+      Yrep[((size_t)tl.head * R + tl.row0 + s0 + r) * d_h + c] = from_f<E>(gsub[r] * acc);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------------------------
+// B5 (SIMT): recompute H, A = gelu(H); dA' = dY W2_e^T; dg = <A, dA'> (= <dY, E_e(x)>);
+// dH = g dA' gelu'(H); gA = g A; dXrep = dH W1_e.
+// ---------------------------------------------------------------------------------------------
+template <typename E>
+__global__ void __launch_bounds__(256)
+expert_bwd_simt_kernel(const Tile* __restrict__ tiles, const int32_t* __restrict__ ntiles,
+                       const E* __restrict__ Xs, int64_t ldx, const E* __restrict__ dY, int64_t ldy,
+                       const int32_t* __restrict__ perm, const float* __restrict__ gate,
+                       const E* __restrict__ W1, const E* __restrict__ W2, int64_t T, int k, int N_e, int d_h,
+                       int d_e, E* __restrict__ dXrep, float* __restrict__ dg, E* __restrict__ dH,
+                       E* __restrict__ gA) {
+  if ((int)blockIdx.x >= *ntiles) return;
+  const Tile tl = tiles[blockIdx.x];
+  extern __shared__ __align__(16) float sm[];
+  float* Xsub = sm;                                   // [kSub][d_h+1]
+  float* Ysub = Xsub + kSub * (d_h + 1);              // [kSub][d_h+1]  (dY rows)
+  float* Hsub = Ysub + kSub * (d_h + 1);              // [kSub][d_e+1]
+  float* Dsub = Hsub + kSub * (d_e + 1);              // [kSub][d_e+1]
+  float* gsub = Dsub + kSub * (d_e + 1);              // [kSub]
+  int* rsub = reinterpret_cast<int*>(gsub + kSub);    // [kSub]
+  const int64_t R = T * k;
+  const size_t wofs = ((size_t)tl.head * N_e + tl.expert) * d_e * d_h;
+  const E* w1 = W1 + wofs;
+  const E* w2 = W2 + wofs;
+  for (int s0 = 0; s0 < tl.rows; s0 += kSub) {
+    const int nr = min(kSub, tl.rows - s0);
+    __syncthreads();
+    for (int r = threadIdx.x; r < kSub; r += blockDim.x) {
+      int rep = -1; float g = 0.0f;
+      if (r < nr) { rep = perm[(size_t)tl.head * R + tl.row0 + s0 + r]; g = gate[(size_t)tl.head * R + rep]; }
+      rsub[r] = rep; gsub[r] = g;
+    }
+    __syncthreads();
+    for (int o = threadIdx.x; o < kSub * d_h; o += blockDim.x) {
+      const int r = o / d_h, c = o % d_h;
+      float xv = 0.0f, yv = 0.0f;
+      if (r < nr) {
+        const int64_t t = rsub[r] / k;
+        xv = to_f(Xs[t * ldx + (int64_t)tl.head * d_h + c]);
+        yv = to_f(dY[t * ldy + (int64_t)tl.head * d_h + c]);
+      }
+      Xsub[r * (d_h + 1) + c] = xv; Ysub[r * (d_h + 1) + c] = yv;
+    }
+    __syncthreads();
+    for (int o = threadIdx.x; o < kSub * d_e; o += blockDim.x) {
+      const int r = o / d_e, f = o % d_e;
+      float h = 0.0f, da = 0.0f;
+      for (int c = 0; c < d_h; ++c) {
+        h = fmaf(Xsub[r * (d_h + 1) + c], to_f(w1[(size_t)f * d_h + c]), h);
+        da = fmaf(Ysub[r * (d_h + 1) + c], to_f(w2[(size_t)f * d_h + c]), da);
+      }
+      Hsub[r * (d_e + 1) + f] = h; Dsub[r * (d_e + 1) + f] = da;
+    }
+    __syncthreads();
+    // dg (one thread per row, fixed f order), then dH / gA in place
+    for (int r = threadIdx.x; r < kSub; r += blockDim.x) {
+      if (r >= nr) continue;
+      float acc = 0.0f;
+      for (int f = 0; f < d_e; ++f) acc = fmaf(gelu_f(Hsub[r * (d_e + 1) + f]), Dsub[r * (d_e + 1) + f], acc);
+      dg[(size_t)tl.head * R + rsub[r]] = acc;
+    }
+    __syncthreads();
+    for (int o = threadIdx.x; o < kSub * d_e; o += blockDim.x) {
+      const int r = o / d_e, f = o % d_e;
+      const float h = Hsub[r * (d_e + 1) + f];
+      const float g = gsub[r];
+      const float dh = g * Dsub[r * (d_e + 1) + f] * gelu_grad_f(h);
+      const float ga = g * gelu_f(h);
+      Dsub[r * (d_e + 1) + f] = dh;
+      if (r < nr) {
+        const size_t row = (size_t)tl.head * R + tl.row0 + s0 + r;
+        dH[row * d_e + f] = from_f<E>(dh);
+        gA[row * d_e + f] = from_f<E>(ga);
+      }
+    }
+    __syncthreads();
+    for (int o = threadIdx.x; o < kSub * d_h; o += blockDim.x) {
+      const int r = o / d_h, c = o % d_h;
+      if (r >= nr) continue;
+      float acc = 0.0f;
+      for (int f = 0; f < d_e; ++f) acc = fmaf(Dsub[r * (d_e + 1) + f], to_f(w1[(size_t)f * d_h + c]), acc);
+      dXrep[((size_t)tl.head * R + tl.row0 + s0 + r) * d_h + c] = from_f<E>(acc);
+    }
+  }
+}
+
+// B5 weight gradients (SIMT): block (f-chunk of 8, e, h); thread = feature c; rows in sorted order.
+template <typename E>
+__global__ void __launch_bounds__(256)
+expert_dw_simt_kernel(const int32_t* __restrict__ off, const E* __restrict__ Xs, int64_t ldx,
+                      const E* __restrict__ dY, int64_t ldy, const int32_t* __restrict__ perm,
+                      const E* __restrict__ dH, const E* __restrict__ gA, int64_t R, int k, int N_e, int d_h,
+                      int d_e, float* __restrict__ dW1, float* __restrict__ dW2) {
+  const int f0 = blockIdx.x * 8, e = blockIdx.y, h = blockIdx.z;
+  const int nf = min(8, d_e - f0);
+  const int32_t* offh = off + (size_t)h * (N_e + 1);
+  const int beg = offh[e], end = offh[e + 1];
+  for (int c = threadIdx.x; c < d_h; c += blockDim.x) {
+    float a1[8], a2[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) { a1[q] = 0.0f; a2[q] = 0.0f; }
+    for (int row = beg; row < end; ++row) {
+      const int64_t t = perm[(size_t)h * R + row] / k;
+      const float xv = to_f(Xs[t * ldx + (int64_t)h * d_h + c]);
+      const float yv = to_f(dY[t * ldy + (int64_t)h * d_h + c]);
+      const size_t hr = ((size_t)h * R + row) * d_e + f0;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        if (q < nf) {
+          a1[q] = fmaf(to_f(dH[hr + q]), xv, a1[q]);
+          a2[q] = fmaf(to_f(gA[hr + q]), yv, a2[q]);
+        }
+      }
+    }
+    const size_t wofs = ((size_t)h * N_e + e) * d_e * d_h;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      if (q < nf) {
+        if (dW1) dW1[wofs + (size_t)(f0 + q) * d_h + c] = a1[q];
+        if (dW2) dW2[wofs + (size_t)(f0 + q) * d_h + c] = a2[q];
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------------------------
+// F6: y[t][h*d_h + c] = sum_j Yrep[h][pos(t,j)][c]  (Eq. 1; gates already applied)
+// ---------------------------------------------------------------------------------------------
+template <typename E>
+__global__ void __launch_bounds__(256)
+combine_fwd_kernel(const E* __restrict__ Yrep, const int32_t* __restrict__ pos, int H, int64_t T, int k, int d_h,
+                   E* __restrict__ out, int64_t ldo) {
+  const int64_t t = blockIdx.x;
+  const int h = blockIdx.y;
+  const int64_t R = T * k;
+  const int32_t* ph = pos + (size_t)h * R + t * k;
+  for (int c = threadIdx.x; c < d_h; c += blockDim.x) {
+    float acc = 0.0f;
+    for (int j = 0; j < k; ++j) acc += to_f(Yrep[((size_t)h * R + ph[j]) * d_h + c]);
+    out[t * ldo + (int64_t)h * d_h + c] = from_f<E>(acc);
+  }
+}
+
+template <typename E>
+__global__ void __launch_bounds__(256)
+permute_blocks_kernel(const E* __restrict__ src, E* __restrict__ dst, int G, int64_t T_loc, int64_t HD) {
+  // src [G][T_loc][HD] -> dst [T_loc][G*HD]
+  const int64_t total = (int64_t)G * T_loc * HD;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t c = i % HD;
+    const int64_t t = (i / HD) % T_loc;
+    const int64_t g = i / (HD * T_loc);
+    dst[t * G * HD + g * HD + c] = src[i];
+  }
+}
+
+// ---------------------------------------------------------------------------------------------
+// B3: softmax Jacobian + Alg. 2 (P:846-P:866), deterministic (R21).
+// Block = (128-token chunk, head); thread = feature i.
+//   dS[t][j] = g_j (dg_j - sum_i g_i dg_i)
+//   partial[e][i] = sum_{t in chunk, j: I[t][j]=e} X[t][i] dS[t][j]    (fixed t, j order)
+// ---------------------------------------------------------------------------------------------
+template <typename E>
+__global__ void __launch_bounds__(256)
+router_bwd_partial_kernel(const E* __restrict__ Xs, int64_t ldx, const int32_t* __restrict__ idx,
+                          const float* __restrict__ gate, const float* __restrict__ dg, int64_t T, int k, int d_h,
+                          int N_e, float* __restrict__ dS, float* __restrict__ partial) {
+  extern __shared__ __align__(16) float smb[];
+  float* part = smb;                                  // [N_e][d_h]
+  float* sdS = part + (size_t)N_e * d_h;              // [128][k]
+  int* sI = reinterpret_cast<int*>(sdS + kRouterTile * k);   // [128][k]
+  const int chunk = blockIdx.x, h = blockIdx.y;
+  const int64_t t0 = (int64_t)chunk * kRouterTile;
+  const int nt = (int)min((int64_t)kRouterTile, T - t0);
+  for (int i = threadIdx.x; i < N_e * d_h; i += blockDim.x) part[i] = 0.0f;
+  for (int tt = threadIdx.x; tt < nt; tt += blockDim.x) {
+    const size_t base = ((size_t)h * T + t0 + tt) * k;
+    float s = 0.0f;
+    for (int j = 0; j < k; ++j) s = fmaf(gate[base + j], dg[base + j], s);
+    for (int j = 0; j < k; ++j) {
+      const float v = gate[base + j] * (dg[base + j] - s);
+      sdS[tt * k + j] = v;
+      sI[tt * k + j] = idx[base + j];
+      dS[base + j] = v;
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < d_h; i += blockDim.x) {
+    for (int tt = 0; tt < nt; ++tt) {
+      const float xv = to_f(Xs[(t0 + tt) * ldx + (int64_t)h * d_h + i]);
+      for (int j = 0; j < k; ++j) {
+        const int e = sI[tt * k + j];
+        part[(size_t)e * d_h + i] = fmaf(xv, sdS[tt * k + j], part[(size_t)e * d_h + i]);
+      }
+    }
+  }
+  __syncthreads();
+  float* po = partial + ((size_t)h * gridDim.x + chunk) * N_e * d_h;
+  for (int i = threadIdx.x; i < N_e * d_h; i += blockDim.x) po[i] = part[i];
+}
+
+// dW_r[h][i][e] = sum over chunks (in order) of partial[h][chunk][e][i]
+__global__ void __launch_bounds__(256)
+router_bwd_reduce_kernel(const float* __restrict__ partial, int n_chunks, int d_h, int N_e, float* __restrict__ dW_r) {
+  const int h = blockIdx.y;
+  const int64_t n = (int64_t)d_h * N_e;
+  for (int64_t o = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; o < n; o += (int64_t)gridDim.x * blockDim.x) {
+    const int e = (int)(o / d_h), i = (int)(o % d_h);
+    float acc = 0.0f;
+    for (int c = 0; c < n_chunks; ++c) acc += partial[(((size_t)h * n_chunks + c) * N_e + e) * d_h + i];
+    dW_r[((size_t)h * d_h + i) * N_e + e] = acc;
+  }
+}
+
+__global__ void transpose_wr_kernel(const float* __restrict__ W_r, float* __restrict__ W_rT, int d_h, int N_e) {
+  const int h = blockIdx.y;
+  const int n = d_h * N_e;
+  for (int o = blockIdx.x * blockDim.x + threadIdx.x; o < n; o += gridDim.x * blockDim.x) {
+    const int e = o / d_h, i = o % d_h;
+    W_rT[(size_t)h * n + o] = W_r[(size_t)h * n + (size_t)i * N_e + e];
+  }
+}
+
+// B6: dXs[t][h*d_h + c] = sum_j dXrep[h][pos(t,j)][c] + sum_j dS[t][j] W_r[h][c][e_j]  (Alg. 2 line 9)
+template <typename E>
+__global__ void __launch_bounds__(256)
+combine_bwd_kernel(const E* __restrict__ dXrep, const int32_t* __restrict__ pos, const int32_t* __restrict__ idx,
+                   const float* __restrict__ dS, const float* __restrict__ W_rT, int64_t T, int k, int d_h, int N_e,
+                   E* __restrict__ out, int64_t ldo) {
+  const int64_t t = blockIdx.x;
+  const int h = blockIdx.y;
+  const int64_t R = T * k;
+  const int32_t* ph = pos + (size_t)h * R + t * k;
+  const int32_t* ih = idx + (size_t)h * R + t * k;
+  const float* sh = dS + (size_t)h * R + t * k;
+  const float* wt = W_rT + (size_t)h * N_e * d_h;
+  for (int c = threadIdx.x; c < d_h; c += blockDim.x) {
+    float acc = 0.0f;
+    for (int j = 0; j < k; ++j) acc += to_f(dXrep[((size_t)h * R + ph[j]) * d_h + c]);
+    float racc = 0.0f;
+    for (int j = 0; j < k; ++j) racc = fmaf(sh[j], wt[(size_t)ih[j] * d_h + c], racc);
+    out[t * ldo + (int64_t)h * d_h + c] = from_f<E>(acc + racc);
+  }
+}
+
+template <typename F>
+void set_smem(F f, size_t bytes) { cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes); }
+
+}  // namespace
+
+void launch_expert_fwd_simt(int dtype, const Tile* tiles, const int32_t* ntiles, int max_tiles, const void* Xs,
+                            int64_t ldx, const int32_t* perm, const float* gate, const void* W1, const void* W2,
+                            int64_t T, int k, int N_e, int d_h, int d_e, void* Yrep, cudaStream_t s) {
+  const size_t smem = sizeof(float) * (kSub * (d_h + 1) + kSub * (d_e + 1) + kSub);
+  if (dtype == 1) {
+    auto f = expert_fwd_simt_kernel<bf16>; set_smem(f, smem);
+    f<<<max_tiles, 256, smem, s>>>(tiles, ntiles, (const bf16*)Xs, ldx, perm, gate, (const bf16*)W1, (const bf16*)W2,
+                                   T, k, N_e, d_h, d_e, (bf16*)Yrep);
+  } else {
+    auto f = expert_fwd_simt_kernel<float>; set_smem(f, smem);
+    f<<<max_tiles, 256, smem, s>>>(tiles, ntiles, (const float*)Xs, ldx, perm, gate, (const float*)W1,
+                                   (const float*)W2, T, k, N_e, d_h, d_e, (float*)Yrep);
+  }
+}
+
+void launch_expert_bwd_simt(int dtype, const Tile* tiles, const int32_t* ntiles, int max_tiles, const void* Xs,
+                            int64_t ldx, const void* dY, int64_t ldy, const int32_t* perm, const float* gate,
+                            const void* W1, const void* W2, int64_t T, int k, int N_e, int d_h, int d_e, void* dXrep,
+                            float* dg, void* dH, void* gA, cudaStream_t s) {
+  const size_t smem = sizeof(float) * (2 * kSub * (d_h + 1) + 2 * kSub * (d_e + 1) + 2 * kSub);
+  if (dtype == 1) {
+    auto f = expert_bwd_simt_kernel<bf16>; set_smem(f, smem);
+    f<<<max_tiles, 256, smem, s>>>(tiles, ntiles, (const bf16*)Xs, ldx, (const bf16*)dY, ldy, perm, gate,
+                                   (const bf16*)W1, (const bf16*)W2, T, k, N_e, d_h, d_e, (bf16*)dXrep, dg,
+                                   (bf16*)dH, (bf16*)gA);
+  } else {
+    auto f = expert_bwd_simt_kernel<float>; set_smem(f, smem);
+    f<<<max_tiles, 256, smem, s>>>(tiles, ntiles, (const float*)Xs, ldx, (const float*)dY, ldy, perm, gate,
+                                   (const float*)W1, (const float*)W2, T, k, N_e, d_h, d_e, (float*)dXrep, dg,
+                                   (float*)dH, (float*)gA);
+  }
+}
+
+void launch_expert_dw_simt(int dtype, const int32_t* off, const void* Xs, int64_t ldx, const void* dY, int64_t ldy,
+                           const int32_t* perm, const void* dH, const void* gA, int H, int64_t T, int k, int N_e,
+                           int d_h, int d_e, float* dW1, float* dW2, cudaStream_t s) {
+  dim3 grid((d_e + 7) / 8, N_e, H);
+  const int threads = d_h >= 256 ? 256 : ((d_h + 31) / 32) * 32;
+  const int64_t R = T * k;
+  if (dtype == 1)
+    expert_dw_simt_kernel<bf16><<<grid, threads, 0, s>>>(off, (const bf16*)Xs, ldx, (const bf16*)dY, ldy, perm,
+                                                         (const bf16*)dH, (const bf16*)gA, R, k, N_e, d_h, d_e, dW1, dW2);
+  else
+    expert_dw_simt_kernel<float><<<grid, threads, 0, s>>>(off, (const float*)Xs, ldx, (const float*)dY, ldy, perm,
+                                                          (const float*)dH, (const float*)gA, R, k, N_e, d_h, d_e, dW1,
+                                                          dW2);
+}
+
+void launch_combine_fwd(int dtype, const void* Yrep, const int32_t* pos, int H, int64_t T, int k, int d_h, void* out,
+                        int64_t ldo, cudaStream_t s) {
+  dim3 grid((unsigned)T, H);
+  const int threads = d_h >= 256 ? 256 : ((d_h + 31) / 32) * 32;
+  if (dtype == 1)
+    combine_fwd_kernel<bf16><<<grid, threads, 0, s>>>((const bf16*)Yrep, pos, H, T, k, d_h, (bf16*)out, ldo);
+  else
+    combine_fwd_kernel<float><<<grid, threads, 0, s>>>((const float*)Yrep, pos, H, T, k, d_h, (float*)out, ldo);
+}
+
+void launch_permute_blocks(int dtype, const void* src, void* dst, int G, int64_t T_loc, int64_t HD, cudaStream_t s) {
+  const int64_t total = (int64_t)G * T_loc * HD;
+  const int blocks = (int)std::min<int64_t>((total + 255) / 256, 148 * 16);
+  if (dtype == 1)
+    permute_blocks_kernel<bf16><<<blocks, 256, 0, s>>>((const bf16*)src, (bf16*)dst, G, T_loc, HD);
+  else
+    permute_blocks_kernel<float><<<blocks, 256, 0, s>>>((const float*)src, (float*)dst, G, T_loc, HD);
+}
+
+void launch_router_bwd(int dtype, const void* Xs, int64_t ldx, const int32_t* idx, const float* gate, const float* dg,
+                       int H, int64_t T, int k, int d_h, int N_e, float* dS, float* dwr_partial, float* dW_r,
+                       cudaStream_t s) {
+  const int n_chunks = (int)((T + kRouterTile - 1) / kRouterTile);
+  const size_t smem = sizeof(float) * ((size_t)N_e * d_h + (size_t)kRouterTile * k) + sizeof(int) * kRouterTile * k;
+  const int threads = d_h >= 256 ? 256 : ((d_h + 31) / 32) * 32;
+  dim3 grid(n_chunks, H);
+  if (dtype == 1) {
+    auto f = router_bwd_partial_kernel<bf16>; set_smem(f, smem);
+    f<<<grid, threads, smem, s>>>((const bf16*)Xs, ldx, idx, gate, dg, T, k, d_h, N_e, dS, dwr_partial);
+  } else {
+    auto f = router_bwd_partial_kernel<float>; set_smem(f, smem);
+    f<<<grid, threads, smem, s>>>((const float*)Xs, ldx, idx, gate, dg, T, k, d_h, N_e, dS, dwr_partial);
+  }
+  if (dW_r) router_bwd_reduce_kernel<<<dim3(std::max(1, d_h * N_e / 256), H), 256, 0, s>>>(dwr_partial, n_chunks, d_h, N_e, dW_r);
+}
+
+void launch_transpose_wr(const float* W_r, float* W_rT, int H, int d_h, int N_e, cudaStream_t s) {
+  transpose_wr_kernel<<<dim3(std::max(1, d_h * N_e / 256), H), 256, 0, s>>>(W_r, W_rT, d_h, N_e);
+}
+
+void launch_combine_bwd(int dtype, const void* dXrep, const int32_t* pos, const int32_t* idx, const float* dS,
+                        const float* W_rT, int H, int64_t T, int k, int d_h, int N_e, void* out, int64_t ldo,
+                        cudaStream_t s) {
+  dim3 grid((unsigned)T, H);
+  const int threads = d_h >= 256 ? 256 : ((d_h + 31) / 32) * 32;
+  if (dtype == 1)
+    combine_bwd_kernel<bf16><<<grid, threads, 0, s>>>((const bf16*)dXrep, pos, idx, dS, W_rT, T, k, d_h, N_e,
+                                                      (bf16*)out, ldo);
+  else
+    combine_bwd_kernel<float><<<grid, threads, 0, s>>>((const float*)dXrep, pos, idx, dS, W_rT, T, k, d_h, N_e,
+                                                       (float*)out, ldo);
+}
+
+}  // namespace mhl

@@ -1,0 +1,163 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the fp64 oracle on the same
+seeded inputs, element by element (R8-R11; tolerances from north_star:
+max relative error 2e-2 bf16 / 1e-4 fp32, gates 1e-5, indices bit-exact on
+sub-tokens whose oracle margin >= 1e-3)."""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import oracle as O  # noqa: E402
+from parity_util import GATE_TOL, TOL, boundary_flip_budget, check_routing, rel_err  # noqa: E402
+from workloads import PRESETS, LayerConfig, make_problem  # noqa: E402
+
+
+def _need_gpu():
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+
+
+def _run_gpu(cfg: LayerConfig, W, x, dout, G=1, simt=False, backward=True):
+    from paper_2602_04870_b200.layer import MHLatentMoE, torch_dtype, weights_to_device
+    td = torch_dtype(cfg.dtype)
+    loop = G > 1
+    L = MHLatentMoE(cfg.T // G, cfg.d, cfg.N_h, cfg.d_h, cfg.N_e, cfg.k, cfg.d_e, cfg.dtype, world_size=G,
+                    loopback=loop, simt=simt)
+    Wd = weights_to_device(W, cfg.dtype)
+    xd = torch.from_numpy(x).to("cuda", td)
+    out, idx, gates = L.forward(xd, Wd, want_routing=True)
+    res = dict(out=out, idx=idx, gates=gates)
+    if backward:
+        grads = L.alloc_grads()
+        dx = L.backward(xd, Wd, torch.from_numpy(dout).to("cuda", td), grads)
+        res.update(dx=dx, **grads)
+    torch.cuda.synchronize()
+    L.check_status()
+    res = {k: v.float().cpu().numpy() if v.dtype != torch.int32 else v.cpu().numpy() for k, v in res.items()}
+    res["launches"] = L.launches()
+    return res
+
+
+def _compare(cfg, W, x, dout, g, backward=True):
+    P = {k: v.astype(np.float64) for k, v in W.items()}
+    mode = cfg.dtype
+    C0 = O.layer_forward(P, x.astype(np.float64), cfg.k, mode=mode)
+    forced, n_clean, n_excl = check_routing(P, C0, g["idx"], cfg.k)
+    assert n_clean > 0.9 * (n_clean + n_excl)
+    C = O.layer_forward(P, x.astype(np.float64), cfg.k, mode=mode, forced_idx=forced)
+    tol = TOL[mode]
+    errs = {"out": rel_err(g["out"], C.out)}
+    for h in range(cfg.N_h):
+        # gates: fp32 softmax of fp32 scores, |dg| <= 1e-5 plus the Lipschitz bound (1/2 per
+        # unit score change) of the Xs boundary-flip budget (R22; zero in fp32 mode)
+        sl = slice(h * cfg.d_h, (h + 1) * cfg.d_h)
+        budget = boundary_flip_budget(C.Xs_pre[:, sl], P["W_r"][h], mode)
+        err = np.abs(g["gates"][h] - C.g[h])
+        assert np.all(err <= GATE_TOL + 0.5 * budget[:, None]), f"gates head {h}: {err.max():.2e}"
+    if backward:
+        gr = O.layer_backward(P, x.astype(np.float64), dout.astype(np.float64), C)
+        for key in ("dx", "dW_in", "dW_out", "dW_r", "dW1", "dW2"):
+            errs[key] = rel_err(g[key], gr[key])
+    for key, e in errs.items():
+        assert e <= tol, f"{key}: rel err {e:.3e} > {tol}"
+    return errs
+
+
+def test_tiny_fp32_fwd_bwd_matches_oracle():
+    _need_gpu()
+    cfg = PRESETS["tiny"]
+    for seed in range(3):
+        W, x, dout = make_problem(cfg, seed, "conf")
+        g = _run_gpu(cfg, W, x, dout)
+        _compare(cfg, W, x, dout, g)
+
+
+@pytest.mark.parametrize("simt", [False, True])
+def test_small_bf16_forward_matches_oracle(simt):
+    _need_gpu()
+    cfg = PRESETS["small"].replace(T=2048)
+    W, x, dout = make_problem(cfg, 1, "conf")
+    g = _run_gpu(cfg, W, x, dout, simt=simt, backward=False)
+    _compare(cfg, W, x, dout, g, backward=False)
+
+
+def test_router_strict_on_exact_subtokens():
+    """W_in = 2^-1 x permutation (d = D): Xs is exact on both sides, so only the fp32
+    (GPU) vs fp64 (oracle) score arithmetic differs (~1e-6).  Indices and slot order
+    must then match on every sub-token with margin >= 1e-5, not just >= 1e-3."""
+    _need_gpu()
+    cfg = LayerConfig("exact", T=4096, d=256, N_h=2, d_h=128, N_e=64, k=8, d_e=32, dtype="bf16")
+    W, x, dout = make_problem(cfg, 7, "conf")
+    perm = np.random.default_rng(0).permutation(256)
+    W["W_in"] = (0.5 * np.eye(256, dtype=np.float32)[perm]).astype(np.float32)
+    g = _run_gpu(cfg, W, x, dout, backward=False)
+    P = {k: v.astype(np.float64) for k, v in W.items()}
+    C0 = O.layer_forward(P, x.astype(np.float64), cfg.k, mode="bf16")
+    _f, n_clean, n_excl = check_routing(P, C0, g["idx"], cfg.k, margin_thr=1e-5)
+    assert n_excl < 0.01 * (n_clean + n_excl)
+
+
+def test_bf16_fwd_bwd_ragged_matches_oracle():
+    """bf16, several 128-row tiles with a ragged tail (T not a multiple of 128)."""
+    _need_gpu()
+    cfg = LayerConfig("rag", T=1000, d=256, N_h=4, d_h=64, N_e=16, k=4, d_e=32, dtype="bf16")
+    W, x, dout = make_problem(cfg, 2, "conf")
+    g = _run_gpu(cfg, W, x, dout)
+    _compare(cfg, W, x, dout, g)
+
+
+@pytest.mark.parametrize("k,N_e", [(1, 8), (8, 8), (16, 32)])
+def test_degenerate_k(k, N_e):
+    _need_gpu()
+    cfg = LayerConfig("k", T=384, d=64, N_h=2, d_h=32, N_e=N_e, k=k, d_e=16, dtype="fp32")
+    W, x, dout = make_problem(cfg, 3, "conf")
+    g = _run_gpu(cfg, W, x, dout)
+    _compare(cfg, W, x, dout, g)
+
+
+def test_all_tokens_to_one_expert():
+    """Extreme skew: a huge bias on expert 3 makes it every sub-token's first choice."""
+    _need_gpu()
+    cfg = LayerConfig("skew", T=512, d=64, N_h=2, d_h=32, N_e=8, k=2, d_e=16, dtype="fp32")
+    W, x, dout = make_problem(cfg, 4, "conf")
+    W["b"][:, 3] = 100.0
+    g = _run_gpu(cfg, W, x, dout)
+    assert np.all(g["idx"][:, :, 0] == 3)
+    _compare(cfg, W, x, dout, g)
+
+
+@pytest.mark.parametrize("G", [2, 4])
+def test_loopback_hp_bitwise_equals_single_rank(G):
+    """HP on G virtual ranks (NCCL replaced by device copies) gives bit-identical
+    out, dx, routing and per-head weight gradients to G = 1 (HP only moves data)."""
+    _need_gpu()
+    cfg = LayerConfig("hp", T=1024, d=128, N_h=4, d_h=32, N_e=16, k=4, d_e=32, dtype="bf16")
+    W, x, dout = make_problem(cfg, 5, "conf")
+    g1 = _run_gpu(cfg, W, x, dout, G=1)
+    gG = _run_gpu(cfg, W, x, dout, G=G)
+    for key in ("out", "dx", "idx", "gates", "dW_r", "dW1", "dW2"):
+        np.testing.assert_array_equal(gG[key], g1[key], err_msg=key)
+    for key in ("dW_in", "dW_out"):     # rank-partial sums, summed in rank order
+        assert rel_err(gG[key], g1[key]) < 1e-5
+
+
+def test_run_to_run_bitwise_deterministic():
+    _need_gpu()
+    cfg = LayerConfig("det", T=2048, d=256, N_h=4, d_h=64, N_e=32, k=4, d_e=64, dtype="bf16")
+    W, x, dout = make_problem(cfg, 6, "conf")
+    a = _run_gpu(cfg, W, x, dout)
+    b = _run_gpu(cfg, W, x, dout)
+    for key in ("out", "dx", "idx", "gates", "dW_r", "dW1", "dW2", "dW_in", "dW_out"):
+        np.testing.assert_array_equal(a[key], b[key], err_msg=key)
+
+
+def test_nonfinite_router_score_is_reported():
+    _need_gpu()
+    from paper_2602_04870_b200 import mhlmoe as C
+    cfg = PRESETS["tiny"]
+    W, x, dout = make_problem(cfg, 0, "conf")
+    W["W_r"][0, 0, 0] = np.inf
+    with pytest.raises(C.MhlError) as ei:
+        _run_gpu(cfg, W, x, dout, backward=False)
+    assert C.STATUS[ei.value.status] == "MHL_ERR_NONFINITE"
