@@ -82,6 +82,20 @@ def test_small_bf16_forward_matches_oracle(simt):
     _compare(cfg, W, x, dout, g, backward=False)
 
 
+@pytest.mark.parametrize("d_h,d_e", [(256, 128), (256, 64), (128, 128), (192, 64)])
+def test_expert_tcgen05_matches_oracle_and_simt(d_h, d_e):
+    """The tcgen05 expert kernel (default bf16 path) vs the oracle, fwd+bwd, at the
+    paper's per-head shapes, ragged T; and vs the SIMT reference kernel."""
+    _need_gpu()
+    cfg = LayerConfig("tc", T=1500, d=2 * d_h, N_h=2, d_h=d_h, N_e=16, k=4, d_e=d_e, dtype="bf16")
+    W, x, dout = make_problem(cfg, 8, "conf")
+    g = _run_gpu(cfg, W, x, dout)
+    _compare(cfg, W, x, dout, g)
+    s = _run_gpu(cfg, W, x, dout, simt=True)
+    np.testing.assert_array_equal(g["idx"], s["idx"])
+    assert rel_err(g["out"], s["out"]) < 1e-2
+
+
 def test_router_strict_on_exact_subtokens():
     """W_in = 2^-1 x permutation (d = D): Xs is exact on both sides, so only the fp32
     (GPU) vs fp64 (oracle) score arithmetic differs (~1e-6).  Indices and slot order
