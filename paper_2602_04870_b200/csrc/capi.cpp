@@ -106,7 +106,7 @@ struct Dims {
   int64_t T_loc, T_g, R;
   int d, N_h, d_h, N_e, k, d_e, G, H, HD, D, el, dtype, rank;
   bool loopback, simt;
-  int n_rt, max_tiles;
+  int n_rt, max_tiles, max_chunks;
 };
 
 struct Bump {
@@ -115,10 +115,10 @@ struct Bump {
 };
 
 // offsets inside one rank's saved region
-struct SavedLayout { size_t Xs, idx, gate, perm, pos, off, tiles, ntiles, cat, total; };
+struct SavedLayout { size_t Xs, idx, gate, perm, pos, off, tiles, ntiles, chunks, nchunks, cbase, ccount, cat, total; };
 // offsets inside one rank's workspace region (forward and backward alias each other)
 struct FwdLayout { size_t send1, Yrep, send2, recv2, hist, tilepref, counts, total; };
-struct BwdLayout { size_t send3, dY, dXrep, dg, dS, dH, gA, dwr_part, W_rT, send4, recv4, dXs, total; };
+struct BwdLayout { size_t send3, dY, dXrep, dg, dS, dH, gA, dwr_part, W_rT, send4, recv4, dXs, dw_part, total; };
 
 SavedLayout saved_layout(const Dims& m) {
   Bump b; SavedLayout L;
@@ -130,6 +130,10 @@ SavedLayout saved_layout(const Dims& m) {
   L.off = b.take((size_t)m.H * (m.N_e + 1) * 4);
   L.tiles = b.take((size_t)m.max_tiles * sizeof(mhl::Tile));
   L.ntiles = b.take(16);
+  L.chunks = b.take((size_t)m.max_chunks * sizeof(mhl::Tile));
+  L.nchunks = b.take(16);
+  L.cbase = b.take((size_t)m.H * m.N_e * 4);
+  L.ccount = b.take((size_t)m.H * m.N_e * 4);
   L.cat = b.take((size_t)m.T_loc * m.D * m.el);
   L.total = b.off;
   return L;
@@ -162,6 +166,7 @@ BwdLayout bwd_layout(const Dims& m) {
   L.send4 = b.take(m.G > 1 ? (size_t)m.T_g * m.HD * m.el : 0);
   L.recv4 = b.take(m.G > 1 ? (size_t)m.T_loc * m.D * m.el : 0);
   L.dXs = b.take((size_t)m.T_loc * m.D * m.el);
+  L.dw_part = b.take(m.simt ? 0 : (size_t)m.max_chunks * 2 * m.d_e * m.d_h * 4);
   L.total = b.off;
   return L;
 }
@@ -200,6 +205,7 @@ mhl_status make_dims(const mhl_config* c, Dims* m) {
   const int64_t mt = (int64_t)m->H * ((m->R + mhl::kExpertBM - 1) / mhl::kExpertBM + m->N_e);
   if (mt >= (int64_t)1 << 31) return fail(MHL_ERR_UNSUPPORTED, "too many tiles");
   m->max_tiles = (int)mt;
+  m->max_chunks = (int)((int64_t)m->H * ((m->R + mhl::kDwChunk - 1) / mhl::kDwChunk + m->N_e));
   const size_t router_smem = (size_t)m->el * m->d_h * mhl::kRouterTile + 4ull * m->d_h * 32 + 4ull * m->N_e;
   const size_t rbwd_smem = 4ull * m->N_e * m->d_h + 8ull * mhl::kRouterTile * m->k;
   if (router_smem > 200 * 1024 || rbwd_smem > 200 * 1024)
@@ -263,6 +269,12 @@ struct StepSpan {
   }
   ~StepSpan() {
     if (a) { cudaEvent_t b = p->next_event(); cudaEventRecord(b, s); p->recs.push_back({name, a, b}); }
+    static const bool dbg = getenv("MHL_DEBUG_SYNC") != nullptr;
+    if (dbg) {
+      cudaError_t e1 = cudaGetLastError();
+      cudaError_t e2 = cudaStreamSynchronize(s);
+      fprintf(stderr, "[mhl debug] %s: launch=%s sync=%s\n", name, cudaGetErrorString(e1), cudaGetErrorString(e2));
+    }
   }
 };
 #define MHL_SPAN(name) StepSpan span_##__LINE__(p, name, s)
@@ -363,7 +375,9 @@ mhl_status moe_forward_local(mhl_plan p, const RankPtrs& R, void* yout, cudaStre
   {
   MHL_SPAN("F4_cluster");
   mhl::launch_cluster(m.H, m.T_g, m.k, m.N_e, idx, hist, (int32_t*)(R.ws + F.tilepref), (int32_t*)(R.ws + F.counts),
-                      off, perm, pos, tiles, ntiles, m.max_tiles, s);
+                      off, perm, pos, tiles, ntiles, m.max_tiles, (mhl::Tile*)(R.saved + S.chunks),
+                      (int32_t*)(R.saved + S.nchunks), (int32_t*)(R.saved + S.cbase), (int32_t*)(R.saved + S.ccount),
+                      m.max_chunks, s);
   }
   void* Yrep = R.ws + F.Yrep;
   {
@@ -404,15 +418,30 @@ mhl_status moe_backward_local(mhl_plan p, const RankPtrs& R, const void* dY, voi
   float* dS = (float*)(R.ws + B.dS);
   void* dH = R.ws + B.dH;
   void* gA = R.ws + B.gA;
+  const bool tc = !m.simt && mhl::expert_bwd_sm100_supported(m.d_h, m.d_e);
+  const mhl::Tile* chunks = (const mhl::Tile*)(R.saved + S.chunks);
+  const int32_t* nchunks = (const int32_t*)(R.saved + S.nchunks);
+  const int32_t* cbase = (const int32_t*)(R.saved + S.cbase);
+  const int32_t* ccount = (const int32_t*)(R.saved + S.ccount);
   {
     MHL_SPAN("B5_expert_bwd_dx");
-    mhl::launch_expert_bwd_simt(m.dtype, tiles, ntiles, m.max_tiles, Xs, m.HD, dY, m.HD, perm, gate, R.W1, R.W2, m.T_g,
-                                m.k, m.N_e, m.d_h, m.d_e, dXrep, dg, dH, gA, s);
+    if (tc)
+      mhl::launch_expert_bwd_sm100(tiles, ntiles, chunks, nchunks, cbase, ccount, Xs, m.HD, dY, m.HD, perm, gate, R.W1,
+                                   R.W2, m.H, m.T_g, m.k, m.N_e, m.d_h, m.d_e, dXrep, dg, dH, gA, nullptr, nullptr,
+                                   nullptr, p->num_sms, s, true, false);
+    else
+      mhl::launch_expert_bwd_simt(m.dtype, tiles, ntiles, m.max_tiles, Xs, m.HD, dY, m.HD, perm, gate, R.W1, R.W2,
+                                  m.T_g, m.k, m.N_e, m.d_h, m.d_e, dXrep, dg, dH, gA, s);
   }
   if (R.dW1 || R.dW2) {
     MHL_SPAN("B5_expert_bwd_dw");
-    mhl::launch_expert_dw_simt(m.dtype, off, Xs, m.HD, dY, m.HD, perm, dH, gA, m.H, m.T_g, m.k, m.N_e, m.d_h, m.d_e,
-                               R.dW1, R.dW2, s);
+    if (tc)
+      mhl::launch_expert_bwd_sm100(tiles, ntiles, chunks, nchunks, cbase, ccount, Xs, m.HD, dY, m.HD, perm, gate, R.W1,
+                                   R.W2, m.H, m.T_g, m.k, m.N_e, m.d_h, m.d_e, dXrep, dg, dH, gA,
+                                   (float*)(R.ws + B.dw_part), R.dW1, R.dW2, p->num_sms, s, false, true);
+    else
+      mhl::launch_expert_dw_simt(m.dtype, off, Xs, m.HD, dY, m.HD, perm, dH, gA, m.H, m.T_g, m.k, m.N_e, m.d_h,
+                                 m.d_e, R.dW1, R.dW2, s);
   }
   float* W_rT = (float*)(R.ws + B.W_rT);
   {

@@ -77,10 +77,12 @@ __device__ int block_exclusive_scan_1024(int v, int* s_warp, int* total) {
 // list over (h, e) in order, each expert segment cut into kExpertBM-row tiles.
 __global__ void __launch_bounds__(1024)
 offsets_tiles_kernel(const int32_t* __restrict__ counts, int32_t* __restrict__ off, Tile* __restrict__ tiles,
-                     int32_t* __restrict__ ntiles, int H, int N_e, int max_tiles) {
+                     int32_t* __restrict__ ntiles, int H, int N_e, int max_tiles, Tile* __restrict__ chunks,
+                     int32_t* __restrict__ nchunks, int32_t* __restrict__ cbase, int32_t* __restrict__ ccount,
+                     int max_chunks) {
   __shared__ int s_warp[64];
   __shared__ int s_tot;
-  int carry_t = 0;
+  int carry_t = 0, carry_c = 0;
   for (int h = 0; h < H; ++h) {
     int carry_r = 0;
     for (int base = 0; base < N_e; base += 1024) {
@@ -92,6 +94,10 @@ offsets_tiles_kernel(const int32_t* __restrict__ counts, int32_t* __restrict__ o
       __syncthreads();
       const int tx = block_exclusive_scan_1024(nt, s_warp, &s_tot);
       const int ttot = s_tot;
+      __syncthreads();
+      const int nc = (c + kDwChunk - 1) / kDwChunk;
+      const int cx = block_exclusive_scan_1024(nc, s_warp, &s_tot);
+      const int ctot = s_tot;
       __syncthreads();
       if (e < N_e) {
         const int row_off = carry_r + rx;
@@ -105,13 +111,25 @@ offsets_tiles_kernel(const int32_t* __restrict__ counts, int32_t* __restrict__ o
             tiles[ti] = tl;
           }
         }
+        cbase[(size_t)h * N_e + e] = carry_c + cx;
+        ccount[(size_t)h * N_e + e] = nc;
+        for (int i = 0; i < nc; ++i) {
+          const int ci = carry_c + cx + i;
+          if (ci < max_chunks) {
+            Tile tl;
+            tl.head = h; tl.expert = e; tl.row0 = row_off + i * kDwChunk;
+            tl.rows = min(kDwChunk, c - i * kDwChunk);
+            chunks[ci] = tl;
+          }
+        }
       }
       carry_r += rtot;
       carry_t += ttot;
+      carry_c += ctot;
     }
     if (threadIdx.x == 0) off[(size_t)h * (N_e + 1) + N_e] = carry_r;
   }
-  if (threadIdx.x == 0) *ntiles = min(carry_t, max_tiles);
+  if (threadIdx.x == 0) { *ntiles = min(carry_t, max_tiles); *nchunks = min(carry_c, max_chunks); }
 }
 
 // (3) per (h, router tile): stable ranks inside the tile via warp match, scatter perm/pos
@@ -149,10 +167,12 @@ scatter_kernel(const int32_t* __restrict__ idx, const int32_t* __restrict__ off,
 
 void launch_cluster(int H, int64_t T, int k, int N_e, const int32_t* idx, const int32_t* hist, int32_t* tilepref,
                     int32_t* counts, int32_t* off, int32_t* perm, int32_t* pos, Tile* tiles, int32_t* ntiles,
-                    int max_tiles, cudaStream_t s) {
+                    int max_tiles, Tile* chunks, int32_t* nchunks, int32_t* cbase, int32_t* ccount, int max_chunks,
+                    cudaStream_t s) {
   const int n_rt = (int)((T + kRouterTile - 1) / kRouterTile);
   tile_prefix_kernel<<<dim3(N_e, H), 256, 0, s>>>(hist, tilepref, counts, n_rt, N_e);
-  offsets_tiles_kernel<<<1, 1024, 0, s>>>(counts, off, tiles, ntiles, H, N_e, max_tiles);
+  offsets_tiles_kernel<<<1, 1024, 0, s>>>(counts, off, tiles, ntiles, H, N_e, max_tiles, chunks, nchunks, cbase,
+                                          ccount, max_chunks);
   scatter_kernel<<<dim3(n_rt, H), 32, sizeof(int) * N_e, s>>>(idx, off, tilepref, perm, pos, T, k, N_e, n_rt);
 }
 

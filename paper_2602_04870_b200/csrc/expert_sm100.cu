@@ -34,7 +34,7 @@ struct FwdSmem {
   static constexpr int GATE = TOK + BM * 4;           // [BM] gates
   static constexpr int TMEM = GATE + BM * 4;          // TMEM base address
   static constexpr int TOTAL = TMEM + 16;
-  static constexpr int BYTES = TOTAL + 1024;          // + alignment slack
+  static constexpr int BYTES = TOTAL;
 };
 
 template <int DH, int DE>
@@ -44,8 +44,9 @@ expert_fwd_sm100_kernel(const Tile* __restrict__ tiles, const int32_t* __restric
                         const float* __restrict__ gate, const bf16* __restrict__ W1, const bf16* __restrict__ W2,
                         int64_t R, int k, int N_e, bf16* __restrict__ Yrep) {
   using L = FwdSmem<DH, DE>;
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = smem_raw;   // SW128 atoms need 1024-byte alignment (checked below)
+  if ((smem_u32(smem) & 1023u) != 0u) __trap();
   const uint32_t sbase = smem_u32(smem);
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + L::BAR);
   int* s_tok = reinterpret_cast<int*>(smem + L::TOK);

@@ -8,6 +8,7 @@ namespace mhl {
 
 constexpr int kRouterTile = 128;   // tokens per router CTA (= clustering tile of F4)
 constexpr int kExpertBM = 128;     // replica rows per expert tile (tcgen05 M)
+constexpr int kDwChunk = 4096;     // sorted rows per weight-gradient partial (B5 dW)
 
 // ---- F3: router + online top-k + gates (SIMT fp32-FMA path). idx/gate [H][T][k];
 // hist [H][ceil(T/128)][N_e]; flag set to 1 on a non-finite key.
@@ -16,10 +17,12 @@ void launch_router_topk(int dtype, const void* Xs, int64_t ldx, const float* W_r
                         int32_t* hist, int32_t* flag, cudaStream_t s);
 
 // ---- F4: clustering.  tilepref [H][n_rt][N_e] (scratch), counts [H][N_e] (scratch),
-// off [H][N_e+1], perm/pos [H][T*k], tiles (<= max_tiles), ntiles[1].
+// off [H][N_e+1], perm/pos [H][T*k], tiles (<= max_tiles), ntiles[1]; dW chunk list
+// (<= max_chunks, kDwChunk rows each), nchunks[1], cbase/ccount [H][N_e].
 void launch_cluster(int H, int64_t T, int k, int N_e, const int32_t* idx, const int32_t* hist,
                     int32_t* tilepref, int32_t* counts, int32_t* off, int32_t* perm, int32_t* pos,
-                    Tile* tiles, int32_t* ntiles, int max_tiles, cudaStream_t s);
+                    Tile* tiles, int32_t* ntiles, int max_tiles, Tile* chunks, int32_t* nchunks,
+                    int32_t* cbase, int32_t* ccount, int max_chunks, cudaStream_t s);
 
 // ---- F5 (SIMT reference): Yrep[h][row][c] = gate * gelu(X W1_e^T) W2_e for sorted rows.
 void launch_expert_fwd_simt(int dtype, const Tile* tiles, const int32_t* ntiles, int max_tiles,
@@ -64,5 +67,14 @@ void launch_expert_fwd_sm100(const Tile* tiles, const int32_t* ntiles, int max_t
                              int64_t ldx, const int32_t* perm, const float* gate, const void* W1,
                              const void* W2, int64_t T, int k, int N_e, int d_h, int d_e, void* Yrep,
                              int num_sms, cudaStream_t s);
+
+bool expert_bwd_sm100_supported(int d_h, int d_e);
+// B5 on tcgen05: dX kernel (dXrep, dg, dH, gA) and/or dW kernel (partials + ordered reduce).
+void launch_expert_bwd_sm100(const Tile* tiles, const int32_t* ntiles, const Tile* chunks, const int32_t* nchunks,
+                             const int32_t* cbase, const int32_t* ccount, const void* Xs, int64_t ldx, const void* dY,
+                             int64_t ldy, const int32_t* perm, const float* gate, const void* W1, const void* W2,
+                             int H, int64_t T, int k, int N_e, int d_h, int d_e, void* dXrep, float* dg, void* dH,
+                             void* gA, float* partial, float* dW1, float* dW2, int num_sms, cudaStream_t s,
+                             bool do_dx, bool do_dw);
 
 }  // namespace mhl

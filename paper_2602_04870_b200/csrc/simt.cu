@@ -193,24 +193,6 @@ expert_dw_simt_kernel(const int32_t* __restrict__ off, const E* __restrict__ Xs,
   }
 }
 
-// ---------------------------------------------------------------------------------------------
-// F6: y[t][h*d_h + c] = sum_j Yrep[h][pos(t,j)][c]  (Eq. 1; gates already applied)
-// ---------------------------------------------------------------------------------------------
-template <typename E>
-__global__ void __launch_bounds__(256)
-combine_fwd_kernel(const E* __restrict__ Yrep, const int32_t* __restrict__ pos, int H, int64_t T, int k, int d_h,
-                   E* __restrict__ out, int64_t ldo) {
-  const int64_t t = blockIdx.x;
-  const int h = blockIdx.y;
-  const int64_t R = T * k;
-  const int32_t* ph = pos + (size_t)h * R + t * k;
-  for (int c = threadIdx.x; c < d_h; c += blockDim.x) {
-    float acc = 0.0f;
-    for (int j = 0; j < k; ++j) acc += to_f(Yrep[((size_t)h * R + ph[j]) * d_h + c]);
-    out[t * ldo + (int64_t)h * d_h + c] = from_f<E>(acc);
-  }
-}
-
 template <typename E>
 __global__ void __launch_bounds__(256)
 permute_blocks_kernel(const E* __restrict__ src, E* __restrict__ dst, int G, int64_t T_loc, int64_t HD) {
@@ -291,28 +273,6 @@ __global__ void transpose_wr_kernel(const float* __restrict__ W_r, float* __rest
   }
 }
 
-// B6: dXs[t][h*d_h + c] = sum_j dXrep[h][pos(t,j)][c] + sum_j dS[t][j] W_r[h][c][e_j]  (Alg. 2 line 9)
-template <typename E>
-__global__ void __launch_bounds__(256)
-combine_bwd_kernel(const E* __restrict__ dXrep, const int32_t* __restrict__ pos, const int32_t* __restrict__ idx,
-                   const float* __restrict__ dS, const float* __restrict__ W_rT, int64_t T, int k, int d_h, int N_e,
-                   E* __restrict__ out, int64_t ldo) {
-  const int64_t t = blockIdx.x;
-  const int h = blockIdx.y;
-  const int64_t R = T * k;
-  const int32_t* ph = pos + (size_t)h * R + t * k;
-  const int32_t* ih = idx + (size_t)h * R + t * k;
-  const float* sh = dS + (size_t)h * R + t * k;
-  const float* wt = W_rT + (size_t)h * N_e * d_h;
-  for (int c = threadIdx.x; c < d_h; c += blockDim.x) {
-    float acc = 0.0f;
-    for (int j = 0; j < k; ++j) acc += to_f(dXrep[((size_t)h * R + ph[j]) * d_h + c]);
-    float racc = 0.0f;
-    for (int j = 0; j < k; ++j) racc = fmaf(sh[j], wt[(size_t)ih[j] * d_h + c], racc);
-    out[t * ldo + (int64_t)h * d_h + c] = from_f<E>(acc + racc);
-  }
-}
-
 template <typename F>
 void set_smem(F f, size_t bytes) { cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes); }
 
@@ -366,16 +326,6 @@ void launch_expert_dw_simt(int dtype, const int32_t* off, const void* Xs, int64_
                                                           dW2);
 }
 
-void launch_combine_fwd(int dtype, const void* Yrep, const int32_t* pos, int H, int64_t T, int k, int d_h, void* out,
-                        int64_t ldo, cudaStream_t s) {
-  dim3 grid((unsigned)T, H);
-  const int threads = d_h >= 256 ? 256 : ((d_h + 31) / 32) * 32;
-  if (dtype == 1)
-    combine_fwd_kernel<bf16><<<grid, threads, 0, s>>>((const bf16*)Yrep, pos, H, T, k, d_h, (bf16*)out, ldo);
-  else
-    combine_fwd_kernel<float><<<grid, threads, 0, s>>>((const float*)Yrep, pos, H, T, k, d_h, (float*)out, ldo);
-}
-
 void launch_permute_blocks(int dtype, const void* src, void* dst, int G, int64_t T_loc, int64_t HD, cudaStream_t s) {
   const int64_t total = (int64_t)G * T_loc * HD;
   const int blocks = (int)std::min<int64_t>((total + 255) / 256, 148 * 16);
@@ -404,19 +354,6 @@ void launch_router_bwd(int dtype, const void* Xs, int64_t ldx, const int32_t* id
 
 void launch_transpose_wr(const float* W_r, float* W_rT, int H, int d_h, int N_e, cudaStream_t s) {
   transpose_wr_kernel<<<dim3(std::max(1, d_h * N_e / 256), H), 256, 0, s>>>(W_r, W_rT, d_h, N_e);
-}
-
-void launch_combine_bwd(int dtype, const void* dXrep, const int32_t* pos, const int32_t* idx, const float* dS,
-                        const float* W_rT, int H, int64_t T, int k, int d_h, int N_e, void* out, int64_t ldo,
-                        cudaStream_t s) {
-  dim3 grid((unsigned)T, H);
-  const int threads = d_h >= 256 ? 256 : ((d_h + 31) / 32) * 32;
-  if (dtype == 1)
-    combine_bwd_kernel<bf16><<<grid, threads, 0, s>>>((const bf16*)dXrep, pos, idx, dS, W_rT, T, k, d_h, N_e,
-                                                      (bf16*)out, ldo);
-  else
-    combine_bwd_kernel<float><<<grid, threads, 0, s>>>((const float*)dXrep, pos, idx, dS, W_rT, T, k, d_h, N_e,
-                                                       (float*)out, ldo);
 }
 
 }  // namespace mhl
