@@ -117,12 +117,12 @@ struct Bump {
 // offsets inside one rank's saved region
 struct SavedLayout { size_t Xs, idx, gate, perm, pos, off, tiles, ntiles, chunks, nchunks, cbase, ccount, cat, total; };
 // offsets inside one rank's workspace region (forward and backward alias each other)
-struct FwdLayout { size_t send1, Yrep, send2, recv2, hist, tilepref, counts, total; };
+struct FwdLayout { size_t send1, Yrep, send2, recv2, hist, tilepref, counts, planes, total; };
 struct BwdLayout { size_t send3, dY, dXrep, dg, dS, dH, gA, dwr_part, W_rT, send4, recv4, dXs, dw_part, total; };
 
 SavedLayout saved_layout(const Dims& m) {
   Bump b; SavedLayout L;
-  L.Xs = b.take((size_t)m.T_g * m.HD * m.el);
+  L.Xs = b.take((size_t)(m.T_g + 1) * m.HD * m.el);   // + one zero row: gather target of padding rows
   L.idx = b.take((size_t)m.H * m.R * 4);
   L.gate = b.take((size_t)m.H * m.R * 4);
   L.perm = b.take((size_t)m.H * m.R * 4);
@@ -148,6 +148,7 @@ FwdLayout fwd_layout(const Dims& m) {
   L.hist = b.take((size_t)m.H * m.n_rt * m.N_e * 4);
   L.tilepref = b.take((size_t)m.H * m.n_rt * m.N_e * 4);
   L.counts = b.take((size_t)m.H * m.N_e * 4);
+  L.planes = b.take(mhl::router_sm100_planes_bytes(m.H, m.d_h, m.N_e));
   L.total = b.off;
   return L;
 }
@@ -155,7 +156,7 @@ FwdLayout fwd_layout(const Dims& m) {
 BwdLayout bwd_layout(const Dims& m) {
   Bump b; BwdLayout L;
   L.send3 = b.take(m.G > 1 ? (size_t)m.T_loc * m.D * m.el : 0);
-  L.dY = b.take((size_t)m.T_g * m.HD * m.el);
+  L.dY = b.take((size_t)(m.T_g + 1) * m.HD * m.el);   // + one zero row (padding gathers)
   L.dXrep = b.take((size_t)m.H * m.R * m.d_h * m.el);
   L.dg = b.take((size_t)m.H * m.R * 4);
   L.dS = b.take((size_t)m.H * m.R * 4);
@@ -370,7 +371,14 @@ mhl_status moe_forward_local(mhl_plan p, const RankPtrs& R, void* yout, cudaStre
   int32_t* hist = (int32_t*)(R.ws + F.hist);
   {
     MHL_SPAN("F3_router_topk");
-    mhl::launch_router_topk(m.dtype, Xs, m.HD, R.W_r, R.bias, m.H, m.T_g, m.d_h, m.N_e, m.k, idx, gate, hist, p->dflag, s);
+    if (!m.simt && mhl::router_sm100_supported(m.d_h, m.N_e)) {
+      if (!mhl::launch_router_sm100(Xs, m.HD, R.W_r, R.bias, m.H, m.T_g, m.d_h, m.N_e, m.k, R.ws + F.planes, idx, gate,
+                                    hist, p->dflag, p->num_sms, s))
+        return fail(MHL_ERR_CUDA, "router: TMA tensor-map encoding failed");
+    } else {
+      mhl::launch_router_topk(m.dtype, Xs, m.HD, R.W_r, R.bias, m.H, m.T_g, m.d_h, m.N_e, m.k, idx, gate, hist,
+                              p->dflag, s);
+    }
   }
   {
   MHL_SPAN("F4_cluster");
@@ -386,8 +394,10 @@ mhl_status moe_forward_local(mhl_plan p, const RankPtrs& R, void* yout, cudaStre
     mhl::launch_expert_fwd_simt(m.dtype, tiles, ntiles, m.max_tiles, Xs, m.HD, perm, gate, R.W1, R.W2, m.T_g, m.k,
                                 m.N_e, m.d_h, m.d_e, Yrep, s);
   } else {
-    mhl::launch_expert_fwd_sm100(tiles, ntiles, m.max_tiles, Xs, m.HD, perm, gate, R.W1, R.W2, m.T_g, m.k, m.N_e,
-                                 m.d_h, m.d_e, Yrep, p->num_sms, s);
+    MHL_CUDA(cudaMemsetAsync(R.saved + S.Xs + (size_t)m.T_g * m.HD * m.el, 0, (size_t)m.HD * m.el, s));
+    if (!mhl::launch_expert_fwd_sm100(tiles, ntiles, m.max_tiles, Xs, m.HD, perm, gate, R.W1, R.W2, m.H, m.T_g, m.k,
+                                      m.N_e, m.d_h, m.d_e, Yrep, p->num_sms, s))
+      return fail(MHL_ERR_CUDA, "expert_fwd: TMA tensor-map encoding failed");
   }
   }
   {

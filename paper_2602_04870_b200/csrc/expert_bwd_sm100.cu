@@ -89,14 +89,16 @@ expert_bwd_dx_kernel(const Tile* __restrict__ tiles, const int32_t* __restrict__
   const uint32_t tH = tmem, tD = tmem + DE, tX = tmem + 256;   // H [0,DE), dA' [DE,2DE), dX [256,256+DH)
   uint32_t phase = 0;
   const int nt = *ntiles_p;
-  const int per = (nt + gridDim.x - 1) / gridDim.x;
-  const int t_begin = min(nt, (int)blockIdx.x * per), t_end = min(nt, t_begin + per);
+  const int ngroups = (nt + kTileGroup - 1) / kTileGroup;   // see expert_sm100.cu: L2-local schedule
+  const int my_groups = ngroups > (int)blockIdx.x ? (ngroups - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
   int cur_h = -1, cur_e = -1;
   constexpr uint32_t IDESC_H = idesc_bf16(BM, DE, 0, 0);
   constexpr uint32_t IDESC_X = idesc_bf16(BM, DH, 0, 1);
   const int q = warp & 3, half = warp >> 2, row = q * 32 + lane;
 
-  for (int ti = t_begin; ti < t_end; ++ti) {
+  for (int v = 0; v < my_groups * kTileGroup; ++v) {
+    const int ti = ((int)blockIdx.x + (v / kTileGroup) * (int)gridDim.x) * kTileGroup + v % kTileGroup;
+    if (ti >= nt) break;
     const Tile tl = tiles[ti];
     if (tid < BM) {
       int tok = -1, rep = -1; float g = 0.f;

@@ -9,6 +9,7 @@ namespace mhl {
 constexpr int kRouterTile = 128;   // tokens per router CTA (= clustering tile of F4)
 constexpr int kExpertBM = 128;     // replica rows per expert tile (tcgen05 M)
 constexpr int kDwChunk = 4096;     // sorted rows per weight-gradient partial (B5 dW)
+constexpr int kTileGroup = 4;      // consecutive expert tiles a persistent CTA takes at once
 
 // ---- F3: router + online top-k + gates (SIMT fp32-FMA path). idx/gate [H][T][k];
 // hist [H][ceil(T/128)][N_e]; flag set to 1 on a non-finite key.
@@ -63,10 +64,20 @@ void launch_combine_bwd(int dtype, const void* dXrep, const int32_t* pos, const 
 
 // ---- tcgen05 (sm_100a) expert kernels, bf16 only.  Return false if the shape is unsupported.
 bool expert_fwd_sm100_supported(int d_h, int d_e);
-void launch_expert_fwd_sm100(const Tile* tiles, const int32_t* ntiles, int max_tiles, const void* Xs,
+// Xs must hold T+1 rows; row T is all-zero (padding rows of a tile gather it).
+bool launch_expert_fwd_sm100(const Tile* tiles, const int32_t* ntiles, int max_tiles, const void* Xs,
                              int64_t ldx, const int32_t* perm, const float* gate, const void* W1,
-                             const void* W2, int64_t T, int k, int N_e, int d_h, int d_e, void* Yrep,
+                             const void* W2, int H, int64_t T, int k, int N_e, int d_h, int d_e, void* Yrep,
                              int num_sms, cudaStream_t s);
+
+// ---- F3 on tcgen05 (bf16 only): splits W_r into 3 bf16 planes (scratch `planes`,
+// router_sm100_planes_bytes) then runs the TMA/tcgen05 router.  Returns false if the tensor
+// maps cannot be built.
+bool router_sm100_supported(int d_h, int N_e);
+size_t router_sm100_planes_bytes(int H, int d_h, int N_e);
+bool launch_router_sm100(const void* Xs, int64_t ldx, const float* W_r, const float* bias, int H, int64_t T, int d_h,
+                         int N_e, int k, void* planes, int32_t* idx, float* gate, int32_t* hist, int32_t* flag,
+                         int num_sms, cudaStream_t s);
 
 bool expert_bwd_sm100_supported(int d_h, int d_e);
 // B5 on tcgen05: dX kernel (dXrep, dg, dH, gA) and/or dW kernel (partials + ordered reduce).
