@@ -103,7 +103,7 @@ constexpr size_t kAlign = 256;
 inline size_t align_up(size_t v) { return (v + kAlign - 1) / kAlign * kAlign; }
 
 struct Dims {
-  int64_t T_loc, T_g, R;
+  int64_t T_loc, T_g, R, Rp;   // Rp: padded sorted-row capacity per head (R + N_e*128)
   int d, N_h, d_h, N_e, k, d_e, G, H, HD, D, el, dtype, rank;
   bool loopback, simt;
   int n_rt, max_tiles, max_chunks;
@@ -115,7 +115,7 @@ struct Bump {
 };
 
 // offsets inside one rank's saved region
-struct SavedLayout { size_t Xs, idx, gate, perm, pos, off, tiles, ntiles, chunks, nchunks, cbase, ccount, cat, total; };
+struct SavedLayout { size_t Xs, idx, gate, perm, tok_s, gate_s, pos, off, tiles, ntiles, chunks, nchunks, cbase, ccount, cat, total; };
 // offsets inside one rank's workspace region (forward and backward alias each other)
 struct FwdLayout { size_t send1, Yrep, send2, recv2, hist, tilepref, counts, planes, total; };
 struct BwdLayout { size_t send3, dY, dXrep, dg, dS, dH, gA, dwr_part, W_rT, send4, recv4, dXs, dw_part, total; };
@@ -125,7 +125,9 @@ SavedLayout saved_layout(const Dims& m) {
   L.Xs = b.take((size_t)(m.T_g + 1) * m.HD * m.el);   // + one zero row: gather target of padding rows
   L.idx = b.take((size_t)m.H * m.R * 4);
   L.gate = b.take((size_t)m.H * m.R * 4);
-  L.perm = b.take((size_t)m.H * m.R * 4);
+  L.perm = b.take((size_t)m.H * m.Rp * 4);     // padded sorted rows (cluster.cu)
+  L.tok_s = b.take((size_t)m.H * m.Rp * 4);
+  L.gate_s = b.take((size_t)m.H * m.Rp * 4);
   L.pos = b.take((size_t)m.H * m.R * 4);
   L.off = b.take((size_t)m.H * (m.N_e + 1) * 4);
   L.tiles = b.take((size_t)m.max_tiles * sizeof(mhl::Tile));
@@ -142,7 +144,7 @@ SavedLayout saved_layout(const Dims& m) {
 FwdLayout fwd_layout(const Dims& m) {
   Bump b; FwdLayout L;
   L.send1 = b.take(m.G > 1 ? (size_t)m.T_loc * m.D * m.el : 0);
-  L.Yrep = b.take((size_t)m.H * m.R * m.d_h * m.el);
+  L.Yrep = b.take((size_t)m.H * m.Rp * m.d_h * m.el);
   L.send2 = b.take(m.G > 1 ? (size_t)m.T_g * m.HD * m.el : 0);
   L.recv2 = b.take(m.G > 1 ? (size_t)m.T_loc * m.D * m.el : 0);
   L.hist = b.take((size_t)m.H * m.n_rt * m.N_e * 4);
@@ -157,11 +159,11 @@ BwdLayout bwd_layout(const Dims& m) {
   Bump b; BwdLayout L;
   L.send3 = b.take(m.G > 1 ? (size_t)m.T_loc * m.D * m.el : 0);
   L.dY = b.take((size_t)(m.T_g + 1) * m.HD * m.el);   // + one zero row (padding gathers)
-  L.dXrep = b.take((size_t)m.H * m.R * m.d_h * m.el);
+  L.dXrep = b.take((size_t)m.H * m.Rp * m.d_h * m.el);
   L.dg = b.take((size_t)m.H * m.R * 4);
   L.dS = b.take((size_t)m.H * m.R * 4);
-  L.dH = b.take((size_t)m.H * m.R * m.d_e * m.el);
-  L.gA = b.take((size_t)m.H * m.R * m.d_e * m.el);
+  L.dH = b.take((size_t)m.H * m.Rp * m.d_e * m.el);
+  L.gA = b.take((size_t)m.H * m.Rp * m.d_e * m.el);
   L.dwr_part = b.take((size_t)m.H * m.n_rt * m.N_e * m.d_h * 4);
   L.W_rT = b.take((size_t)m.H * m.N_e * m.d_h * 4);
   L.send4 = b.take(m.G > 1 ? (size_t)m.T_g * m.HD * m.el : 0);
@@ -195,6 +197,8 @@ mhl_status make_dims(const mhl_config* c, Dims* m) {
   if (m->R >= (int64_t)1 << 31) return fail(MHL_ERR_UNSUPPORTED, "T_glob * k must be < 2^31");
   m->d = c->d_model; m->N_h = c->n_heads; m->d_h = c->d_head; m->N_e = c->n_experts; m->d_e = c->d_expert;
   m->H = m->N_h / m->G;
+  m->Rp = m->R + (int64_t)m->N_e * mhl::kExpertBM;
+  if (m->Rp >= (int64_t)1 << 31) return fail(MHL_ERR_UNSUPPORTED, "T_glob * k + N_e * 128 must be < 2^31");
   m->HD = m->H * m->d_h;
   m->D = m->N_h * m->d_h;
   m->dtype = c->dtype;
@@ -206,7 +210,7 @@ mhl_status make_dims(const mhl_config* c, Dims* m) {
   const int64_t mt = (int64_t)m->H * ((m->R + mhl::kExpertBM - 1) / mhl::kExpertBM + m->N_e);
   if (mt >= (int64_t)1 << 31) return fail(MHL_ERR_UNSUPPORTED, "too many tiles");
   m->max_tiles = (int)mt;
-  m->max_chunks = (int)((int64_t)m->H * ((m->R + mhl::kDwChunk - 1) / mhl::kDwChunk + m->N_e));
+  m->max_chunks = (int)((int64_t)m->H * ((m->Rp + mhl::kDwChunk - 1) / mhl::kDwChunk + m->N_e));
   const size_t router_smem = (size_t)m->el * m->d_h * mhl::kRouterTile + 4ull * m->d_h * 32 + 4ull * m->N_e;
   const size_t rbwd_smem = 4ull * m->N_e * m->d_h + 8ull * mhl::kRouterTile * m->k;
   if (router_smem > 200 * 1024 || rbwd_smem > 200 * 1024)
@@ -348,6 +352,29 @@ struct RankPtrs {   // one (virtual) rank's view
   int32_t* topk_idx; float* gates;
 };
 
+// the clustered-routing state of one rank, as stored in its `saved` region
+mhl::Routing routing_view(const Dims& m, const char* saved) {
+  const SavedLayout S = saved_layout(m);
+  mhl::Routing rt;
+  rt.H = m.H; rt.T = m.T_g; rt.k = m.k; rt.N_e = m.N_e; rt.Rp = m.Rp;
+  rt.idx = (const int32_t*)(saved + S.idx);
+  rt.gate = (const float*)(saved + S.gate);
+  rt.perm = (const int32_t*)(saved + S.perm);
+  rt.tok_s = (const int32_t*)(saved + S.tok_s);
+  rt.gate_s = (const float*)(saved + S.gate_s);
+  rt.pos = (const int32_t*)(saved + S.pos);
+  rt.off = (const int32_t*)(saved + S.off);
+  rt.tiles = (const mhl::Tile*)(saved + S.tiles);
+  rt.ntiles = (const int32_t*)(saved + S.ntiles);
+  rt.max_tiles = m.max_tiles;
+  rt.chunks = (const mhl::Tile*)(saved + S.chunks);
+  rt.nchunks = (const int32_t*)(saved + S.nchunks);
+  rt.max_chunks = m.max_chunks;
+  rt.cbase = (const int32_t*)(saved + S.cbase);
+  rt.ccount = (const int32_t*)(saved + S.ccount);
+  return rt;
+}
+
 mhl_status check_kernels(mhl_plan p) {
   (void)p;
   cudaError_t e = cudaGetLastError();
@@ -381,28 +408,28 @@ mhl_status moe_forward_local(mhl_plan p, const RankPtrs& R, void* yout, cudaStre
     }
   }
   {
-  MHL_SPAN("F4_cluster");
-  mhl::launch_cluster(m.H, m.T_g, m.k, m.N_e, idx, hist, (int32_t*)(R.ws + F.tilepref), (int32_t*)(R.ws + F.counts),
-                      off, perm, pos, tiles, ntiles, m.max_tiles, (mhl::Tile*)(R.saved + S.chunks),
-                      (int32_t*)(R.saved + S.nchunks), (int32_t*)(R.saved + S.cbase), (int32_t*)(R.saved + S.ccount),
-                      m.max_chunks, s);
+    MHL_SPAN("F4_cluster");
+    mhl::launch_cluster(m.H, m.T_g, m.k, m.N_e, idx, gate, hist, (int32_t*)(R.ws + F.tilepref),
+                        (int32_t*)(R.ws + F.counts), off, perm, pos, (int32_t*)(R.saved + S.tok_s),
+                        (float*)(R.saved + S.gate_s), m.Rp, tiles, ntiles, m.max_tiles, (mhl::Tile*)(R.saved + S.chunks),
+                        (int32_t*)(R.saved + S.nchunks), (int32_t*)(R.saved + S.cbase), (int32_t*)(R.saved + S.ccount),
+                        m.max_chunks, s);
   }
+  const mhl::Routing rt = routing_view(m, R.saved);
   void* Yrep = R.ws + F.Yrep;
   {
-  MHL_SPAN("F5_expert_fwd");
-  if (m.simt || !mhl::expert_fwd_sm100_supported(m.d_h, m.d_e)) {
-    mhl::launch_expert_fwd_simt(m.dtype, tiles, ntiles, m.max_tiles, Xs, m.HD, perm, gate, R.W1, R.W2, m.T_g, m.k,
-                                m.N_e, m.d_h, m.d_e, Yrep, s);
-  } else {
+    MHL_SPAN("F5_expert_fwd");
+    // the all-zero sub-token row T: target of the padding rows of every expert tile
     MHL_CUDA(cudaMemsetAsync(R.saved + S.Xs + (size_t)m.T_g * m.HD * m.el, 0, (size_t)m.HD * m.el, s));
-    if (!mhl::launch_expert_fwd_sm100(tiles, ntiles, m.max_tiles, Xs, m.HD, perm, gate, R.W1, R.W2, m.H, m.T_g, m.k,
-                                      m.N_e, m.d_h, m.d_e, Yrep, p->num_sms, s))
+    if (m.simt || !mhl::expert_fwd_sm100_supported(m.d_h, m.d_e)) {
+      mhl::launch_expert_fwd_simt(m.dtype, rt, Xs, m.HD, R.W1, R.W2, m.d_h, m.d_e, Yrep, s);
+    } else if (!mhl::launch_expert_fwd_sm100(rt, Xs, m.HD, R.W1, R.W2, m.d_h, m.d_e, Yrep, p->num_sms, s)) {
       return fail(MHL_ERR_CUDA, "expert_fwd: TMA tensor-map encoding failed");
-  }
+    }
   }
   {
     MHL_SPAN("F6_combine");
-    mhl::launch_combine_fwd(m.dtype, Yrep, pos, m.H, m.T_g, m.k, m.d_h, yout, m.HD, s);
+    mhl::launch_combine_fwd(m.dtype, rt, Yrep, m.d_h, yout, m.HD, s);
   }
   p->launches += 7;
   if (R.topk_idx) MHL_CUDA(cudaMemcpyAsync(R.topk_idx, idx, (size_t)m.H * m.R * 4, cudaMemcpyDeviceToDevice, s));
@@ -418,40 +445,31 @@ mhl_status moe_backward_local(mhl_plan p, const RankPtrs& R, const void* dY, voi
   const void* Xs = R.saved + S.Xs;
   const int32_t* idx = (const int32_t*)(R.saved + S.idx);
   const float* gate = (const float*)(R.saved + S.gate);
-  const int32_t* perm = (const int32_t*)(R.saved + S.perm);
-  const int32_t* pos = (const int32_t*)(R.saved + S.pos);
-  const int32_t* off = (const int32_t*)(R.saved + S.off);
-  const mhl::Tile* tiles = (const mhl::Tile*)(R.saved + S.tiles);
-  const int32_t* ntiles = (const int32_t*)(R.saved + S.ntiles);
+  const mhl::Routing rt = routing_view(m, R.saved);
   void* dXrep = R.ws + B.dXrep;
   float* dg = (float*)(R.ws + B.dg);
   float* dS = (float*)(R.ws + B.dS);
   void* dH = R.ws + B.dH;
   void* gA = R.ws + B.gA;
   const bool tc = !m.simt && mhl::expert_bwd_sm100_supported(m.d_h, m.d_e);
-  const mhl::Tile* chunks = (const mhl::Tile*)(R.saved + S.chunks);
-  const int32_t* nchunks = (const int32_t*)(R.saved + S.nchunks);
-  const int32_t* cbase = (const int32_t*)(R.saved + S.cbase);
-  const int32_t* ccount = (const int32_t*)(R.saved + S.ccount);
+  // the all-zero row T of dY (padding rows of every expert tile gather it)
+  MHL_CUDA(cudaMemsetAsync(static_cast<char*>(const_cast<void*>(dY)) + (size_t)m.T_g * m.HD * m.el, 0,
+                           (size_t)m.HD * m.el, s));
   {
     MHL_SPAN("B5_expert_bwd_dx");
     if (tc)
-      mhl::launch_expert_bwd_sm100(tiles, ntiles, chunks, nchunks, cbase, ccount, Xs, m.HD, dY, m.HD, perm, gate, R.W1,
-                                   R.W2, m.H, m.T_g, m.k, m.N_e, m.d_h, m.d_e, dXrep, dg, dH, gA, nullptr, nullptr,
-                                   nullptr, p->num_sms, s, true, false);
+      mhl::launch_expert_bwd_sm100(rt, Xs, m.HD, dY, m.HD, R.W1, R.W2, m.d_h, m.d_e, dXrep, dg, dH, gA, nullptr,
+                                   nullptr, nullptr, p->num_sms, s, true, false);
     else
-      mhl::launch_expert_bwd_simt(m.dtype, tiles, ntiles, m.max_tiles, Xs, m.HD, dY, m.HD, perm, gate, R.W1, R.W2,
-                                  m.T_g, m.k, m.N_e, m.d_h, m.d_e, dXrep, dg, dH, gA, s);
+      mhl::launch_expert_bwd_simt(m.dtype, rt, Xs, m.HD, dY, m.HD, R.W1, R.W2, m.d_h, m.d_e, dXrep, dg, dH, gA, s);
   }
   if (R.dW1 || R.dW2) {
     MHL_SPAN("B5_expert_bwd_dw");
     if (tc)
-      mhl::launch_expert_bwd_sm100(tiles, ntiles, chunks, nchunks, cbase, ccount, Xs, m.HD, dY, m.HD, perm, gate, R.W1,
-                                   R.W2, m.H, m.T_g, m.k, m.N_e, m.d_h, m.d_e, dXrep, dg, dH, gA,
+      mhl::launch_expert_bwd_sm100(rt, Xs, m.HD, dY, m.HD, R.W1, R.W2, m.d_h, m.d_e, dXrep, dg, dH, gA,
                                    (float*)(R.ws + B.dw_part), R.dW1, R.dW2, p->num_sms, s, false, true);
     else
-      mhl::launch_expert_dw_simt(m.dtype, off, Xs, m.HD, dY, m.HD, perm, dH, gA, m.H, m.T_g, m.k, m.N_e, m.d_h,
-                                 m.d_e, R.dW1, R.dW2, s);
+      mhl::launch_expert_dw_simt(m.dtype, rt, Xs, m.HD, dY, m.HD, dH, gA, m.d_h, m.d_e, R.dW1, R.dW2, s);
   }
   float* W_rT = (float*)(R.ws + B.W_rT);
   {
@@ -462,7 +480,7 @@ mhl_status moe_backward_local(mhl_plan p, const RankPtrs& R, const void* dY, voi
   }
   {
     MHL_SPAN("B6_combine_bwd");
-    mhl::launch_combine_bwd(m.dtype, dXrep, pos, idx, dS, W_rT, m.H, m.T_g, m.k, m.d_h, m.N_e, dxout, m.HD, s);
+    mhl::launch_combine_bwd(m.dtype, rt, dXrep, dS, W_rT, m.d_h, dxout, m.HD, s);
   }
   p->launches += 6;
   return check_kernels(p);

@@ -2,10 +2,14 @@
 //
 // Replicas r = t*k + j of each head are stably sorted by expert (a counting sort:
 // deterministic, integer-exact, dropless P:566/P:977):
-//   pos(r) = off[e] + tilepref[tile(t)][e] + rank of r among the tile's replicas of e
-// where tilepref is the exclusive scan over router tiles of the per-tile expert
-// histogram emitted by F3.  The expert segments are then cut into tiles of
-// kExpertBM rows — the block-sparse mask of Eq. 7 as a tile list.
+//   pos(r) = off[e] + tilepref[tile(t)][e] + rank of r among the router tile's replicas of e
+// where tilepref is the exclusive scan over router tiles of the per-tile expert histogram
+// emitted by F3.  Each expert segment starts on a 128-row boundary (off[e] is padded), so the
+// block-sparse mask of Eq. 7 becomes a list of whole 128-row tiles; padding rows point at
+// the all-zero sub-token row (token id T) with gate 0 and contribute exactly nothing.
+// Outputs per head (Rp = padded row capacity): perm (row -> replica or -1), tok_s (row -> token
+// or T), gate_s (row -> gate or 0), pos (replica -> row), off, the tile list and the list of
+// <= kDwChunk-row chunks used by the weight-gradient kernel.
 #include "kernels.h"
 
 namespace mhl {
@@ -64,7 +68,7 @@ __device__ int block_exclusive_scan_1024(int v, int* s_warp, int* total) {
       const int n = __shfl_up_sync(0xffffffffu, wi, d);
       if (lane >= d) wi += n;
     }
-    s_warp[32 + lane] = wi - w;        // exclusive prefix of each warp
+    s_warp[32 + lane] = wi - w;
     if (lane == 31) *total = wi;
   }
   __syncthreads();
@@ -73,13 +77,14 @@ __device__ int block_exclusive_scan_1024(int v, int* s_warp, int* total) {
   return r;
 }
 
-// (2) single CTA: off[h][e] = exclusive scan over e of counts (per head), and the tile
-// list over (h, e) in order, each expert segment cut into kExpertBM-row tiles.
+// (2) single CTA: padded per-head offsets off[h][e] (exclusive scan of ceil(count/128)*128),
+// the tile list, the dW chunk list (cbase/ccount per (h, e)) and the padding-row fill.
 __global__ void __launch_bounds__(1024)
 offsets_tiles_kernel(const int32_t* __restrict__ counts, int32_t* __restrict__ off, Tile* __restrict__ tiles,
                      int32_t* __restrict__ ntiles, int H, int N_e, int max_tiles, Tile* __restrict__ chunks,
                      int32_t* __restrict__ nchunks, int32_t* __restrict__ cbase, int32_t* __restrict__ ccount,
-                     int max_chunks) {
+                     int max_chunks, int64_t Rp, int32_t* __restrict__ perm, int32_t* __restrict__ tok_s,
+                     float* __restrict__ gate_s, int tok_zero) {
   __shared__ int s_warp[64];
   __shared__ int s_tot;
   int carry_t = 0, carry_c = 0;
@@ -89,13 +94,14 @@ offsets_tiles_kernel(const int32_t* __restrict__ counts, int32_t* __restrict__ o
       const int e = base + threadIdx.x;
       const int c = (e < N_e) ? counts[(size_t)h * N_e + e] : 0;
       const int nt = (c + kExpertBM - 1) / kExpertBM;
-      const int rx = block_exclusive_scan_1024(c, s_warp, &s_tot);
+      const int cp = nt * kExpertBM;                          // padded segment length
+      const int rx = block_exclusive_scan_1024(cp, s_warp, &s_tot);
       const int rtot = s_tot;
       __syncthreads();
       const int tx = block_exclusive_scan_1024(nt, s_warp, &s_tot);
       const int ttot = s_tot;
       __syncthreads();
-      const int nc = (c + kDwChunk - 1) / kDwChunk;
+      const int nc = (cp + kDwChunk - 1) / kDwChunk;
       const int cx = block_exclusive_scan_1024(nc, s_warp, &s_tot);
       const int ctot = s_tot;
       __syncthreads();
@@ -118,9 +124,15 @@ offsets_tiles_kernel(const int32_t* __restrict__ counts, int32_t* __restrict__ o
           if (ci < max_chunks) {
             Tile tl;
             tl.head = h; tl.expert = e; tl.row0 = row_off + i * kDwChunk;
-            tl.rows = min(kDwChunk, c - i * kDwChunk);
+            tl.rows = min(kDwChunk, cp - i * kDwChunk);
             chunks[ci] = tl;
           }
+        }
+        // padding rows of this segment: no replica, zero sub-token, gate 0
+        for (int r = row_off + c; r < row_off + cp; ++r) {
+          perm[(size_t)h * Rp + r] = -1;
+          tok_s[(size_t)h * Rp + r] = tok_zero;
+          gate_s[(size_t)h * Rp + r] = 0.f;
         }
       }
       carry_r += rtot;
@@ -132,11 +144,12 @@ offsets_tiles_kernel(const int32_t* __restrict__ counts, int32_t* __restrict__ o
   if (threadIdx.x == 0) { *ntiles = min(carry_t, max_tiles); *nchunks = min(carry_c, max_chunks); }
 }
 
-// (3) per (h, router tile): stable ranks inside the tile via warp match, scatter perm/pos
+// (3) per (h, router tile): stable ranks inside the tile via warp match, scatter perm/pos/tok/gate
 __global__ void __launch_bounds__(32)
-scatter_kernel(const int32_t* __restrict__ idx, const int32_t* __restrict__ off,
+scatter_kernel(const int32_t* __restrict__ idx, const float* __restrict__ gate, const int32_t* __restrict__ off,
                const int32_t* __restrict__ tilepref, int32_t* __restrict__ perm, int32_t* __restrict__ pos,
-               int64_t T, int k, int N_e, int n_rt) {
+               int32_t* __restrict__ tok_s, float* __restrict__ gate_s, int64_t T, int k, int N_e, int n_rt,
+               int64_t Rp) {
   extern __shared__ int cnt[];
   const int tt = blockIdx.x, h = blockIdx.y, lane = threadIdx.x;
   for (int e = lane; e < N_e; e += 32) cnt[e] = 0;
@@ -144,6 +157,7 @@ scatter_kernel(const int32_t* __restrict__ idx, const int32_t* __restrict__ off,
   const int64_t r0 = (int64_t)tt * kRouterTile * k;
   const int64_t r1 = min((int64_t)(tt + 1) * kRouterTile, T) * k;
   const int32_t* idx_h = idx + (size_t)h * T * k;
+  const float* gate_h = gate + (size_t)h * T * k;
   const int32_t* offh = off + (size_t)h * (N_e + 1);
   const int32_t* pre = tilepref + ((size_t)h * n_rt + tt) * N_e;
   for (int64_t base = r0; base < r1; base += 32) {
@@ -154,7 +168,10 @@ scatter_kernel(const int32_t* __restrict__ idx, const int32_t* __restrict__ off,
     const int rank = __popc(mask & ((1u << lane) - 1u));
     if (act) {
       const int p = offh[e] + pre[e] + cnt[e] + rank;
-      perm[(size_t)h * T * k + p] = (int32_t)r;
+      const size_t q = (size_t)h * Rp + p;
+      perm[q] = (int32_t)r;
+      tok_s[q] = (int32_t)(r / k);
+      gate_s[q] = gate_h[r];
       pos[(size_t)h * T * k + r] = p;
     }
     __syncwarp();
@@ -165,15 +182,16 @@ scatter_kernel(const int32_t* __restrict__ idx, const int32_t* __restrict__ off,
 
 }  // namespace
 
-void launch_cluster(int H, int64_t T, int k, int N_e, const int32_t* idx, const int32_t* hist, int32_t* tilepref,
-                    int32_t* counts, int32_t* off, int32_t* perm, int32_t* pos, Tile* tiles, int32_t* ntiles,
-                    int max_tiles, Tile* chunks, int32_t* nchunks, int32_t* cbase, int32_t* ccount, int max_chunks,
-                    cudaStream_t s) {
+void launch_cluster(int H, int64_t T, int k, int N_e, const int32_t* idx, const float* gate, const int32_t* hist,
+                    int32_t* tilepref, int32_t* counts, int32_t* off, int32_t* perm, int32_t* pos, int32_t* tok_s,
+                    float* gate_s, int64_t Rp, Tile* tiles, int32_t* ntiles, int max_tiles, Tile* chunks,
+                    int32_t* nchunks, int32_t* cbase, int32_t* ccount, int max_chunks, cudaStream_t s) {
   const int n_rt = (int)((T + kRouterTile - 1) / kRouterTile);
   tile_prefix_kernel<<<dim3(N_e, H), 256, 0, s>>>(hist, tilepref, counts, n_rt, N_e);
   offsets_tiles_kernel<<<1, 1024, 0, s>>>(counts, off, tiles, ntiles, H, N_e, max_tiles, chunks, nchunks, cbase,
-                                          ccount, max_chunks);
-  scatter_kernel<<<dim3(n_rt, H), 32, sizeof(int) * N_e, s>>>(idx, off, tilepref, perm, pos, T, k, N_e, n_rt);
+                                          ccount, max_chunks, Rp, perm, tok_s, gate_s, (int)T);
+  scatter_kernel<<<dim3(n_rt, H), 32, sizeof(int) * N_e, s>>>(idx, gate, off, tilepref, perm, pos, tok_s, gate_s, T, k,
+                                                              N_e, n_rt, Rp);
 }
 
 }  // namespace mhl

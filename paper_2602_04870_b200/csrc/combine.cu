@@ -32,7 +32,7 @@ template <typename E, bool BWD>
 __global__ void __launch_bounds__(256)
 combine_kernel(const E* __restrict__ rep, const int32_t* __restrict__ pos, const int32_t* __restrict__ idx,
                const float* __restrict__ dS, const float* __restrict__ W_rT, int H, int64_t T, int k, int d_h,
-               int N_e, E* __restrict__ out, int64_t ldo) {
+               int N_e, int64_t Rp, E* __restrict__ out, int64_t ldo) {
   constexpr int V = Vec<E>::N;
   const int64_t pair = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
   if (pair >= T * H) return;
@@ -45,7 +45,7 @@ combine_kernel(const E* __restrict__ rep, const int32_t* __restrict__ pos, const
   for (int ch = lane; ch < nchunk; ch += 32) {
     float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
     for (int j = 0; j < k; ++j) {
-      const E* src = rep + ((size_t)h * R + ph[j]) * d_h + ch * V;
+      const E* src = rep + ((size_t)h * Rp + ph[j]) * d_h + ch * V;
       if constexpr (V == 8) {
         float f[8];
         unpack(__ldg(reinterpret_cast<const uint4*>(src)), f);
@@ -87,27 +87,26 @@ combine_kernel(const E* __restrict__ rep, const int32_t* __restrict__ pos, const
 
 }  // namespace
 
-void launch_combine_fwd(int dtype, const void* Yrep, const int32_t* pos, int H, int64_t T, int k, int d_h, void* out,
-                        int64_t ldo, cudaStream_t s) {
-  const unsigned blocks = (unsigned)((T * H + 7) / 8);
+void launch_combine_fwd(int dtype, const Routing& rt, const void* Yrep, int d_h, void* out, int64_t ldo,
+                        cudaStream_t s) {
+  const unsigned blocks = (unsigned)((rt.T * rt.H + 7) / 8);
   if (dtype == 1)
-    combine_kernel<bf16, false><<<blocks, 256, 0, s>>>((const bf16*)Yrep, pos, nullptr, nullptr, nullptr, H, T, k, d_h,
-                                                       0, (bf16*)out, ldo);
+    combine_kernel<bf16, false><<<blocks, 256, 0, s>>>((const bf16*)Yrep, rt.pos, nullptr, nullptr, nullptr, rt.H, rt.T,
+                                                       rt.k, d_h, 0, rt.Rp, (bf16*)out, ldo);
   else
-    combine_kernel<float, false><<<blocks, 256, 0, s>>>((const float*)Yrep, pos, nullptr, nullptr, nullptr, H, T, k,
-                                                        d_h, 0, (float*)out, ldo);
+    combine_kernel<float, false><<<blocks, 256, 0, s>>>((const float*)Yrep, rt.pos, nullptr, nullptr, nullptr, rt.H,
+                                                        rt.T, rt.k, d_h, 0, rt.Rp, (float*)out, ldo);
 }
 
-void launch_combine_bwd(int dtype, const void* dXrep, const int32_t* pos, const int32_t* idx, const float* dS,
-                        const float* W_rT, int H, int64_t T, int k, int d_h, int N_e, void* out, int64_t ldo,
-                        cudaStream_t s) {
-  const unsigned blocks = (unsigned)((T * H + 7) / 8);
+void launch_combine_bwd(int dtype, const Routing& rt, const void* dXrep, const float* dS, const float* W_rT, int d_h,
+                        void* out, int64_t ldo, cudaStream_t s) {
+  const unsigned blocks = (unsigned)((rt.T * rt.H + 7) / 8);
   if (dtype == 1)
-    combine_kernel<bf16, true><<<blocks, 256, 0, s>>>((const bf16*)dXrep, pos, idx, dS, W_rT, H, T, k, d_h, N_e,
-                                                      (bf16*)out, ldo);
+    combine_kernel<bf16, true><<<blocks, 256, 0, s>>>((const bf16*)dXrep, rt.pos, rt.idx, dS, W_rT, rt.H, rt.T, rt.k,
+                                                      d_h, rt.N_e, rt.Rp, (bf16*)out, ldo);
   else
-    combine_kernel<float, true><<<blocks, 256, 0, s>>>((const float*)dXrep, pos, idx, dS, W_rT, H, T, k, d_h, N_e,
-                                                       (float*)out, ldo);
+    combine_kernel<float, true><<<blocks, 256, 0, s>>>((const float*)dXrep, rt.pos, rt.idx, dS, W_rT, rt.H, rt.T,
+                                                       rt.k, d_h, rt.N_e, rt.Rp, (float*)out, ldo);
 }
 
 }  // namespace mhl

@@ -53,20 +53,18 @@ __device__ __forceinline__ void gather_rows(uint32_t dst, const int* s_tok, cons
                                             int head, int tid) {
   for (int i = tid; i < BM * DH / 8; i += kThreads) {
     const int row = i / (DH / 8), c = (i % (DH / 8)) * 8;
-    const int tok = s_tok[row];
-    cp_async_16(dst + kmaj_off(row, c, BM), src + (size_t)(tok < 0 ? 0 : tok) * ld + (size_t)head * DH + c,
-                tok < 0 ? 0u : 16u);
+    cp_async_16(dst + kmaj_off(row, c, BM), src + (size_t)s_tok[row] * ld + (size_t)head * DH + c, 16);
   }
 }
 
 template <int DH, int DE>
 __global__ void __launch_bounds__(kThreads, 1)
-expert_bwd_dx_kernel(const Tile* __restrict__ tiles, const int32_t* __restrict__ ntiles_p,
-                     const bf16* __restrict__ Xs, int64_t ldx, const bf16* __restrict__ dY, int64_t ldy,
-                     const int32_t* __restrict__ perm, const float* __restrict__ gate,
-                     const bf16* __restrict__ W1, const bf16* __restrict__ W2, int64_t R, int k, int N_e,
-                     bf16* __restrict__ dXrep, float* __restrict__ dg, bf16* __restrict__ dHg,
-                     bf16* __restrict__ gAg) {
+expert_bwd_dx_kernel(Routing rt, const bf16* __restrict__ Xs, int64_t ldx, const bf16* __restrict__ dY, int64_t ldy,
+                     const bf16* __restrict__ W1, const bf16* __restrict__ W2, bf16* __restrict__ dXrep,
+                     float* __restrict__ dg, bf16* __restrict__ dHg, bf16* __restrict__ gAg) {
+  const Tile* tiles = rt.tiles;
+  const int N_e = rt.N_e;
+  const int64_t Rp = rt.Rp, R = rt.T * rt.k;
   using L = DxSmem<DH, DE>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw;   // SW128 atoms need 1024-byte alignment (checked below)
@@ -88,7 +86,7 @@ expert_bwd_dx_kernel(const Tile* __restrict__ tiles, const int32_t* __restrict__
   const uint32_t tmem = *s_tmem;
   const uint32_t tH = tmem, tD = tmem + DE, tX = tmem + 256;   // H [0,DE), dA' [DE,2DE), dX [256,256+DH)
   uint32_t phase = 0;
-  const int nt = *ntiles_p;
+  const int nt = *rt.ntiles;
   const int ngroups = (nt + kTileGroup - 1) / kTileGroup;   // see expert_sm100.cu: L2-local schedule
   const int my_groups = ngroups > (int)blockIdx.x ? (ngroups - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
   int cur_h = -1, cur_e = -1;
@@ -101,13 +99,8 @@ expert_bwd_dx_kernel(const Tile* __restrict__ tiles, const int32_t* __restrict__
     if (ti >= nt) break;
     const Tile tl = tiles[ti];
     if (tid < BM) {
-      int tok = -1, rep = -1; float g = 0.f;
-      if (tid < tl.rows) {
-        rep = perm[(size_t)tl.head * R + tl.row0 + tid];
-        tok = rep / k;
-        g = gate[(size_t)tl.head * R + rep];
-      }
-      s_tok[tid] = tok; s_rep[tid] = rep; s_gate[tid] = g;
+      const size_t q0 = (size_t)tl.head * Rp + tl.row0 + tid;
+      s_tok[tid] = rt.tok_s[q0]; s_rep[tid] = rt.perm[q0]; s_gate[tid] = rt.gate_s[q0];
     }
     __syncthreads();
     if (tl.head != cur_h || tl.expert != cur_e) {
@@ -157,8 +150,7 @@ expert_bwd_dx_kernel(const Tile* __restrict__ tiles, const int32_t* __restrict__
     // ---- epilogue: dg, dH, gA
     {
       const float g = s_gate[row];
-      const bool valid = row < tl.rows;
-      const size_t grow = (size_t)tl.head * R + tl.row0 + row;
+      const size_t grow = (size_t)tl.head * Rp + tl.row0 + row;
       float dgp = 0.f;
       for (int c0 = half * (DE / 2); c0 < (half + 1) * (DE / 2); c0 += 32) {
         uint32_t hv[32], dv[32];
@@ -184,10 +176,8 @@ expert_bwd_dx_kernel(const Tile* __restrict__ tiles, const int32_t* __restrict__
           p2.x = pack_bf16x2(ga[0], ga[1]); p2.y = pack_bf16x2(ga[2], ga[3]);
           p2.z = pack_bf16x2(ga[4], ga[5]); p2.w = pack_bf16x2(ga[6], ga[7]);
           *reinterpret_cast<uint4*>(smem + L::DHS + kmaj_off(row, c0 + j, BM)) = p1;
-          if (valid) {
-            *reinterpret_cast<uint4*>(dHg + grow * DE + c0 + j) = p1;
-            *reinterpret_cast<uint4*>(gAg + grow * DE + c0 + j) = p2;
-          }
+          *reinterpret_cast<uint4*>(dHg + grow * DE + c0 + j) = p1;   // padding rows: g = 0 -> zeros
+          *reinterpret_cast<uint4*>(gAg + grow * DE + c0 + j) = p2;
         }
       }
       s_dg[half * BM + row] = dgp;
@@ -195,7 +185,7 @@ expert_bwd_dx_kernel(const Tile* __restrict__ tiles, const int32_t* __restrict__
     fence_proxy_async();
     tc_fence_before();
     __syncthreads();
-    if (tid < BM && tid < tl.rows) dg[(size_t)tl.head * R + s_rep[tid]] = s_dg[tid] + s_dg[BM + tid];
+    if (tid < BM && s_rep[tid] >= 0) dg[(size_t)tl.head * R + s_rep[tid]] = s_dg[tid] + s_dg[BM + tid];
     // ---- dXrep = dH W1   (B = W1 viewed MN-major: N = DH atoms at DE*128 B, K groups at 1024 B)
     if (tid == 0) {
       tc_fence_after();
@@ -209,21 +199,19 @@ expert_bwd_dx_kernel(const Tile* __restrict__ tiles, const int32_t* __restrict__
     mbar_wait(bar, phase); phase ^= 1;
     tc_fence_after();
     {
-      bf16* dst = dXrep + ((size_t)tl.head * R + tl.row0 + row) * DH;
+      bf16* dst = dXrep + ((size_t)tl.head * Rp + tl.row0 + row) * DH;
       for (int c0 = half * (DH / 2); c0 < (half + 1) * (DH / 2); c0 += 32) {
         uint32_t v[32];
         tmem_ld32(tX + ((uint32_t)(q * 32) << 16) + c0, v);
         tmem_ld_wait();
-        if (row < tl.rows) {
 #pragma unroll
-          for (int j = 0; j < 32; j += 8) {
-            uint4 pk;
-            pk.x = pack_bf16x2(__uint_as_float(v[j + 0]), __uint_as_float(v[j + 1]));
-            pk.y = pack_bf16x2(__uint_as_float(v[j + 2]), __uint_as_float(v[j + 3]));
-            pk.z = pack_bf16x2(__uint_as_float(v[j + 4]), __uint_as_float(v[j + 5]));
-            pk.w = pack_bf16x2(__uint_as_float(v[j + 6]), __uint_as_float(v[j + 7]));
-            *reinterpret_cast<uint4*>(dst + c0 + j) = pk;
-          }
+        for (int j = 0; j < 32; j += 8) {
+          uint4 pk;
+          pk.x = pack_bf16x2(__uint_as_float(v[j + 0]), __uint_as_float(v[j + 1]));
+          pk.y = pack_bf16x2(__uint_as_float(v[j + 2]), __uint_as_float(v[j + 3]));
+          pk.z = pack_bf16x2(__uint_as_float(v[j + 4]), __uint_as_float(v[j + 5]));
+          pk.w = pack_bf16x2(__uint_as_float(v[j + 6]), __uint_as_float(v[j + 7]));
+          *reinterpret_cast<uint4*>(dst + c0 + j) = pk;
         }
       }
     }
@@ -253,10 +241,10 @@ struct DwSmem {
 
 template <int DH, int DE>
 __global__ void __launch_bounds__(kThreads, 1)
-expert_dw_kernel(const Tile* __restrict__ chunks, const int32_t* __restrict__ nchunks_p,
-                 const bf16* __restrict__ Xs, int64_t ldx, const bf16* __restrict__ dY, int64_t ldy,
-                 const int32_t* __restrict__ perm, const bf16* __restrict__ dHg, const bf16* __restrict__ gAg,
-                 int64_t R, int k, float* __restrict__ partial) {
+expert_dw_kernel(Routing rt, const bf16* __restrict__ Xs, int64_t ldx, const bf16* __restrict__ dY, int64_t ldy,
+                 const bf16* __restrict__ dHg, const bf16* __restrict__ gAg, float* __restrict__ partial) {
+  const Tile* chunks = rt.chunks;
+  const int64_t Rp = rt.Rp;
   using L = DwSmem<DH, DE>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw;   // SW128 atoms need 1024-byte alignment (checked below)
@@ -275,7 +263,7 @@ expert_dw_kernel(const Tile* __restrict__ chunks, const int32_t* __restrict__ nc
   uint32_t ph[2] = {0, 0};
   constexpr int MH = DH / 128;                          // M halves (c blocks of 128)
   constexpr uint32_t IDESC = idesc_bf16(128, DE, 1, 1);
-  const int nchunks = *nchunks_p;
+  const int nchunks = *rt.nchunks;
 
   for (int ci = blockIdx.x; ci < nchunks; ci += gridDim.x) {
     const Tile ch = chunks[ci];
@@ -287,26 +275,20 @@ expert_dw_kernel(const Tile* __restrict__ chunks, const int32_t* __restrict__ nc
       const uint32_t base = sbase + st * L::STAGE;
       for (int i = tid; i < kHalf * DH / 8; i += kThreads) {
         const int r = i / (DH / 8), c = (i % (DH / 8)) * 8;
-        const int t = tok[r];
-        const size_t so = (size_t)(t < 0 ? 0 : t);
-        const uint32_t sz = t < 0 ? 0u : 16u;
-        cp_async_16(base + L::X + kmaj_off(r, c, kHalf), Xs + so * ldx + (size_t)ch.head * DH + c, sz);
-        cp_async_16(base + L::DY + kmaj_off(r, c, kHalf), dY + so * ldy + (size_t)ch.head * DH + c, sz);
+        const size_t so = (size_t)tok[r];   // padding rows: the zero row
+        cp_async_16(base + L::X + kmaj_off(r, c, kHalf), Xs + so * ldx + (size_t)ch.head * DH + c, 16);
+        cp_async_16(base + L::DY + kmaj_off(r, c, kHalf), dY + so * ldy + (size_t)ch.head * DH + c, 16);
       }
       for (int i = tid; i < kHalf * DE / 8; i += kThreads) {
         const int r = i / (DE / 8), c = (i % (DE / 8)) * 8;
-        const bool ok = (r0 + r) < ch.rows;
-        const size_t grow = (size_t)ch.head * R + ch.row0 + (ok ? r0 + r : 0);
-        cp_async_16(base + L::DHH + kmaj_off(r, c, kHalf), dHg + grow * DE + c, ok ? 16u : 0u);
-        cp_async_16(base + L::GA + kmaj_off(r, c, kHalf), gAg + grow * DE + c, ok ? 16u : 0u);
+        const size_t grow = (size_t)ch.head * Rp + ch.row0 + r0 + r;   // chunk rows are whole tiles
+        cp_async_16(base + L::DHH + kmaj_off(r, c, kHalf), dHg + grow * DE + c, 16);
+        cp_async_16(base + L::GA + kmaj_off(r, c, kHalf), gAg + grow * DE + c, 16);
       }
       cp_async_commit();
     };
     auto load_tokens = [&](int st, int s) {
-      if (tid < kHalf) {
-        const int r = s * kHalf + tid;
-        s_tok[st * kHalf + tid] = r < ch.rows ? perm[(size_t)ch.head * R + ch.row0 + r] / k : -1;
-      }
+      if (tid < kHalf) s_tok[st * kHalf + tid] = rt.tok_s[(size_t)ch.head * Rp + ch.row0 + s * kHalf + tid];
     };
     load_tokens(0, 0);
     __syncthreads();
@@ -395,27 +377,6 @@ dw_reduce_kernel(const float* __restrict__ partial, const int32_t* __restrict__ 
 template <typename K>
 void set_smem(K k, int bytes) { cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes); }
 
-template <int DH, int DE>
-void launch_dx_t(const Tile* tiles, const int32_t* ntiles, const void* Xs, int64_t ldx, const void* dY, int64_t ldy,
-                 const int32_t* perm, const float* gate, const void* W1, const void* W2, int64_t R, int k, int N_e,
-                 void* dXrep, float* dg, void* dH, void* gA, int num_sms, cudaStream_t s) {
-  auto kern = expert_bwd_dx_kernel<DH, DE>;
-  set_smem(kern, DxSmem<DH, DE>::BYTES);
-  kern<<<num_sms, kThreads, DxSmem<DH, DE>::BYTES, s>>>(tiles, ntiles, (const bf16*)Xs, ldx, (const bf16*)dY, ldy,
-                                                         perm, gate, (const bf16*)W1, (const bf16*)W2, R, k, N_e,
-                                                         (bf16*)dXrep, dg, (bf16*)dH, (bf16*)gA);
-}
-
-template <int DH, int DE>
-void launch_dw_t(const Tile* chunks, const int32_t* nchunks, const void* Xs, int64_t ldx, const void* dY, int64_t ldy,
-                 const int32_t* perm, const void* dH, const void* gA, int64_t R, int k, float* partial, int num_sms,
-                 cudaStream_t s) {
-  auto kern = expert_dw_kernel<DH, DE>;
-  set_smem(kern, DwSmem<DH, DE>::BYTES);
-  kern<<<num_sms, kThreads, DwSmem<DH, DE>::BYTES, s>>>(chunks, nchunks, (const bf16*)Xs, ldx, (const bf16*)dY, ldy,
-                                                         perm, (const bf16*)dH, (const bf16*)gA, R, k, partial);
-}
-
 }  // namespace
 
 bool expert_bwd_sm100_supported(int d_h, int d_e) {
@@ -423,25 +384,36 @@ bool expert_bwd_sm100_supported(int d_h, int d_e) {
          (d_h == 128 && d_e == 64);
 }
 
-void launch_expert_bwd_sm100(const Tile* tiles, const int32_t* ntiles, const Tile* chunks, const int32_t* nchunks,
-                             const int32_t* cbase, const int32_t* ccount, const void* Xs, int64_t ldx, const void* dY,
-                             int64_t ldy, const int32_t* perm, const float* gate, const void* W1, const void* W2,
-                             int H, int64_t T, int k, int N_e, int d_h, int d_e, void* dXrep, float* dg, void* dH,
+bool launch_expert_bwd_sm100(const Routing& rt, const void* Xs, int64_t ldx, const void* dY, int64_t ldy,
+                             const void* W1, const void* W2, int d_h, int d_e, void* dXrep, float* dg, void* dH,
                              void* gA, float* partial, float* dW1, float* dW2, int num_sms, cudaStream_t s,
                              bool do_dx, bool do_dw) {
-  const int64_t R = T * k;
-#define MHL_BWD_CASE(A, B)                                                                                     \
-  if (d_h == A && d_e == B) {                                                                                  \
-    if (do_dx) launch_dx_t<A, B>(tiles, ntiles, Xs, ldx, dY, ldy, perm, gate, W1, W2, R, k, N_e, dXrep, dg, dH, \
-                                 gA, num_sms, s);                                                              \
-    if (do_dw) launch_dw_t<A, B>(chunks, nchunks, Xs, ldx, dY, ldy, perm, dH, gA, R, k, partial, num_sms, s);  \
+  bool ok = false;
+#define MHL_BWD_CASE(A, B)                                                                                       \
+  if (d_h == A && d_e == B) {                                                                                    \
+    ok = true;                                                                                                   \
+    if (do_dx) {                                                                                                 \
+      auto kern = expert_bwd_dx_kernel<A, B>;                                                                    \
+      set_smem(kern, DxSmem<A, B>::BYTES);                                                                       \
+      kern<<<num_sms, kThreads, DxSmem<A, B>::BYTES, s>>>(rt, (const bf16*)Xs, ldx, (const bf16*)dY, ldy,        \
+                                                          (const bf16*)W1, (const bf16*)W2, (bf16*)dXrep, dg,    \
+                                                          (bf16*)dH, (bf16*)gA);                                 \
+    }                                                                                                            \
+    if (do_dw) {                                                                                                 \
+      auto kern = expert_dw_kernel<A, B>;                                                                        \
+      set_smem(kern, DwSmem<A, B>::BYTES);                                                                       \
+      kern<<<num_sms, kThreads, DwSmem<A, B>::BYTES, s>>>(rt, (const bf16*)Xs, ldx, (const bf16*)dY, ldy,        \
+                                                          (const bf16*)dH, (const bf16*)gA, partial);            \
+    }                                                                                                            \
   }
   MHL_BWD_CASE(256, 128) else MHL_BWD_CASE(256, 64) else MHL_BWD_CASE(128, 128) else MHL_BWD_CASE(128, 64)
 #undef MHL_BWD_CASE
-  if (do_dw && (dW1 || dW2)) {
+  if (ok && do_dw && (dW1 || dW2)) {
     const int dedh = d_e * d_h;
-    dw_reduce_kernel<<<dim3((dedh + 255) / 256, N_e, H), 256, 0, s>>>(partial, cbase, ccount, N_e, dedh, dW1, dW2);
+    dw_reduce_kernel<<<dim3((dedh + 255) / 256, rt.N_e, rt.H), 256, 0, s>>>(partial, rt.cbase, rt.ccount, rt.N_e, dedh,
+                                                                            dW1, dW2);
   }
+  return ok;
 }
 
 }  // namespace mhl

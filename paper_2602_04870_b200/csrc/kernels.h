@@ -7,68 +7,32 @@
 namespace mhl {
 
 constexpr int kRouterTile = 128;   // tokens per router CTA (= clustering tile of F4)
-constexpr int kExpertBM = 128;     // replica rows per expert tile (tcgen05 M)
+constexpr int kExpertBM = 128;     // replica rows per expert tile (tcgen05 M); segments padded to it
 constexpr int kDwChunk = 4096;     // sorted rows per weight-gradient partial (B5 dW)
 constexpr int kTileGroup = 4;      // consecutive expert tiles a persistent CTA takes at once
+
+// Clustered routing of one rank's local heads (F3/F4 outputs, device pointers).
+// Sorted-row arrays have a fixed per-head capacity Rp = T*k + N_e*128 (expert segments are
+// padded to whole 128-row tiles; padding rows: perm -1, tok_s = T (the all-zero row), gate_s 0).
+struct Routing {
+  int H; int64_t T; int k; int N_e; int64_t Rp;
+  const int32_t* idx;      // [H][T][k]  expert ids, slot order = descending biased key
+  const float* gate;       // [H][T][k]
+  const int32_t* perm;     // [H][Rp]    sorted row -> replica t*k+j, or -1
+  const int32_t* tok_s;    // [H][Rp]    sorted row -> token, or T
+  const float* gate_s;     // [H][Rp]    sorted row -> gate, or 0
+  const int32_t* pos;      // [H][T*k]   replica -> sorted row
+  const int32_t* off;      // [H][N_e+1] padded segment offsets
+  const Tile* tiles; const int32_t* ntiles; int max_tiles;        // 128-row tiles, (h, e, row) order
+  const Tile* chunks; const int32_t* nchunks; int max_chunks;     // dW chunks
+  const int32_t* cbase; const int32_t* ccount;                    // [H][N_e] chunk range per expert
+};
 
 // ---- F3: router + online top-k + gates (SIMT fp32-FMA path). idx/gate [H][T][k];
 // hist [H][ceil(T/128)][N_e]; flag set to 1 on a non-finite key.
 void launch_router_topk(int dtype, const void* Xs, int64_t ldx, const float* W_r, const float* bias,
                         int H, int64_t T, int d_h, int N_e, int k, int32_t* idx, float* gate,
                         int32_t* hist, int32_t* flag, cudaStream_t s);
-
-// ---- F4: clustering.  tilepref [H][n_rt][N_e] (scratch), counts [H][N_e] (scratch),
-// off [H][N_e+1], perm/pos [H][T*k], tiles (<= max_tiles), ntiles[1]; dW chunk list
-// (<= max_chunks, kDwChunk rows each), nchunks[1], cbase/ccount [H][N_e].
-void launch_cluster(int H, int64_t T, int k, int N_e, const int32_t* idx, const int32_t* hist,
-                    int32_t* tilepref, int32_t* counts, int32_t* off, int32_t* perm, int32_t* pos,
-                    Tile* tiles, int32_t* ntiles, int max_tiles, Tile* chunks, int32_t* nchunks,
-                    int32_t* cbase, int32_t* ccount, int max_chunks, cudaStream_t s);
-
-// ---- F5 (SIMT reference): Yrep[h][row][c] = gate * gelu(X W1_e^T) W2_e for sorted rows.
-void launch_expert_fwd_simt(int dtype, const Tile* tiles, const int32_t* ntiles, int max_tiles,
-                            const void* Xs, int64_t ldx, const int32_t* perm, const float* gate,
-                            const void* W1, const void* W2, int64_t T, int k, int N_e, int d_h, int d_e,
-                            void* Yrep, cudaStream_t s);
-
-// ---- F6: y[t][h*d_h+c] = sum_j Yrep[h][pos[h][t*k+j]][c]  (fixed j order), out ld = ldo.
-void launch_combine_fwd(int dtype, const void* Yrep, const int32_t* pos, int H, int64_t T, int k, int d_h,
-                        void* out, int64_t ldo, cudaStream_t s);
-
-// ---- [G][T_loc][HD] -> [T_loc][G*HD]
-void launch_permute_blocks(int dtype, const void* src, void* dst, int G, int64_t T_loc, int64_t HD, cudaStream_t s);
-
-// ---- B5 (SIMT reference): per tile dXrep (sorted rows), dg (replica order), dH, gA (sorted rows).
-void launch_expert_bwd_simt(int dtype, const Tile* tiles, const int32_t* ntiles, int max_tiles,
-                            const void* Xs, int64_t ldx, const void* dY, int64_t ldy, const int32_t* perm,
-                            const float* gate, const void* W1, const void* W2, int64_t T, int k, int N_e,
-                            int d_h, int d_e, void* dXrep, float* dg, void* dH, void* gA, cudaStream_t s);
-
-// ---- B5 weight gradients (SIMT reference): dW1/dW2 per (h,e) in sorted-row order.
-void launch_expert_dw_simt(int dtype, const int32_t* off, const void* Xs, int64_t ldx, const void* dY,
-                           int64_t ldy, const int32_t* perm, const void* dH, const void* gA, int H, int64_t T,
-                           int k, int N_e, int d_h, int d_e, float* dW1, float* dW2, cudaStream_t s);
-
-// ---- B3: dS = g (dg - sum g dg); dW_r partials per 128-token chunk; then ordered reduce.
-void launch_router_bwd(int dtype, const void* Xs, int64_t ldx, const int32_t* idx, const float* gate,
-                       const float* dg, int H, int64_t T, int k, int d_h, int N_e, float* dS,
-                       float* dwr_partial, float* dW_r, cudaStream_t s);
-
-// ---- W_rT[h][e][i] = W_r[h][i][e]
-void launch_transpose_wr(const float* W_r, float* W_rT, int H, int d_h, int N_e, cudaStream_t s);
-
-// ---- B6: dXs[t][h*d_h+c] = sum_j dXrep[h][pos][c] + sum_j dS[h][t][j] * W_rT[h][idx][c]
-void launch_combine_bwd(int dtype, const void* dXrep, const int32_t* pos, const int32_t* idx,
-                        const float* dS, const float* W_rT, int H, int64_t T, int k, int d_h, int N_e,
-                        void* out, int64_t ldo, cudaStream_t s);
-
-// ---- tcgen05 (sm_100a) expert kernels, bf16 only.  Return false if the shape is unsupported.
-bool expert_fwd_sm100_supported(int d_h, int d_e);
-// Xs must hold T+1 rows; row T is all-zero (padding rows of a tile gather it).
-bool launch_expert_fwd_sm100(const Tile* tiles, const int32_t* ntiles, int max_tiles, const void* Xs,
-                             int64_t ldx, const int32_t* perm, const float* gate, const void* W1,
-                             const void* W2, int H, int64_t T, int k, int N_e, int d_h, int d_e, void* Yrep,
-                             int num_sms, cudaStream_t s);
 
 // ---- F3 on tcgen05 (bf16 only): splits W_r into 3 bf16 planes (scratch `planes`,
 // router_sm100_planes_bytes) then runs the TMA/tcgen05 router.  Returns false if the tensor
@@ -79,13 +43,51 @@ bool launch_router_sm100(const void* Xs, int64_t ldx, const float* W_r, const fl
                          int N_e, int k, void* planes, int32_t* idx, float* gate, int32_t* hist, int32_t* flag,
                          int num_sms, cudaStream_t s);
 
+// ---- F4: clustering.  tilepref [H][n_rt][N_e] and counts [H][N_e] are scratch.
+void launch_cluster(int H, int64_t T, int k, int N_e, const int32_t* idx, const float* gate, const int32_t* hist,
+                    int32_t* tilepref, int32_t* counts, int32_t* off, int32_t* perm, int32_t* pos, int32_t* tok_s,
+                    float* gate_s, int64_t Rp, Tile* tiles, int32_t* ntiles, int max_tiles, Tile* chunks,
+                    int32_t* nchunks, int32_t* cbase, int32_t* ccount, int max_chunks, cudaStream_t s);
+
+// ---- F5: Yrep[h][row][c] = gate_s * gelu(X[tok_s] W1_e^T) W2_e for every sorted row (padding rows
+// produce zeros).  Xs holds T+1 rows, row T all-zero.  Yrep is [H][Rp][d_h].
+void launch_expert_fwd_simt(int dtype, const Routing& rt, const void* Xs, int64_t ldx, const void* W1, const void* W2,
+                            int d_h, int d_e, void* Yrep, cudaStream_t s);
+bool expert_fwd_sm100_supported(int d_h, int d_e);
+bool launch_expert_fwd_sm100(const Routing& rt, const void* Xs, int64_t ldx, const void* W1, const void* W2, int d_h,
+                             int d_e, void* Yrep, int num_sms, cudaStream_t s);
+
+// ---- F6: y[t][h*d_h+c] = sum_j Yrep[h][pos[h][t*k+j]][c]  (fixed j order), out ld = ldo.
+void launch_combine_fwd(int dtype, const Routing& rt, const void* Yrep, int d_h, void* out, int64_t ldo,
+                        cudaStream_t s);
+
+// ---- [G][T_loc][HD] -> [T_loc][G*HD]
+void launch_permute_blocks(int dtype, const void* src, void* dst, int G, int64_t T_loc, int64_t HD, cudaStream_t s);
+
+// ---- B5: per sorted row dXrep [H][Rp][d_h], dH / gA [H][Rp][d_e] (zero on padding rows) and the
+// gate cotangent dg [H][T*k] (replica order); dY holds T+1 rows, row T all-zero.
+void launch_expert_bwd_simt(int dtype, const Routing& rt, const void* Xs, int64_t ldx, const void* dY, int64_t ldy,
+                            const void* W1, const void* W2, int d_h, int d_e, void* dXrep, float* dg, void* dH,
+                            void* gA, cudaStream_t s);
+void launch_expert_dw_simt(int dtype, const Routing& rt, const void* Xs, int64_t ldx, const void* dY, int64_t ldy,
+                           const void* dH, const void* gA, int d_h, int d_e, float* dW1, float* dW2, cudaStream_t s);
 bool expert_bwd_sm100_supported(int d_h, int d_e);
-// B5 on tcgen05: dX kernel (dXrep, dg, dH, gA) and/or dW kernel (partials + ordered reduce).
-void launch_expert_bwd_sm100(const Tile* tiles, const int32_t* ntiles, const Tile* chunks, const int32_t* nchunks,
-                             const int32_t* cbase, const int32_t* ccount, const void* Xs, int64_t ldx, const void* dY,
-                             int64_t ldy, const int32_t* perm, const float* gate, const void* W1, const void* W2,
-                             int H, int64_t T, int k, int N_e, int d_h, int d_e, void* dXrep, float* dg, void* dH,
+// tcgen05 dX kernel (dXrep, dg, dH, gA) and/or dW kernel (chunk partials + ordered reduce)
+bool launch_expert_bwd_sm100(const Routing& rt, const void* Xs, int64_t ldx, const void* dY, int64_t ldy,
+                             const void* W1, const void* W2, int d_h, int d_e, void* dXrep, float* dg, void* dH,
                              void* gA, float* partial, float* dW1, float* dW2, int num_sms, cudaStream_t s,
                              bool do_dx, bool do_dw);
+
+// ---- B3: dS = g (dg - sum g dg); dW_r partials per 128-token chunk; then ordered reduce.
+void launch_router_bwd(int dtype, const void* Xs, int64_t ldx, const int32_t* idx, const float* gate,
+                       const float* dg, int H, int64_t T, int k, int d_h, int N_e, float* dS,
+                       float* dwr_partial, float* dW_r, cudaStream_t s);
+
+// ---- W_rT[h][e][i] = W_r[h][i][e]
+void launch_transpose_wr(const float* W_r, float* W_rT, int H, int d_h, int N_e, cudaStream_t s);
+
+// ---- B6: dXs[t][h*d_h+c] = sum_j dXrep[h][pos][c] + sum_j dS[h][t][j] * W_rT[h][idx][c]
+void launch_combine_bwd(int dtype, const Routing& rt, const void* dXrep, const float* dS, const float* W_rT, int d_h,
+                        void* out, int64_t ldo, cudaStream_t s);
 
 }  // namespace mhl

@@ -1,6 +1,6 @@
-// simt.cu — CUDA-core kernels of the path: the HBM-bound passes (combine F6/B6,
-// block permutes, router backward B3) and the SIMT reference versions of the expert
-// FFN (F5/B5) used in fp32 mode and as the bf16 cross-check path (MHL_FLAG_SIMT).
+// simt.cu — CUDA-core kernels of the path: block permutes, router backward (B3), and the SIMT
+// versions of the expert FFN (F5/B5) used in fp32 mode and as the bf16 cross-check path
+// (MHL_FLAG_SIMT).  All work on the padded clustered layout of cluster.cu (Routing).
 #include <algorithm>
 #include "kernels.h"
 
@@ -11,44 +11,29 @@ namespace {
 constexpr int kSub = 32;    // rows per SIMT sub-tile
 
 // ---------------------------------------------------------------------------------------------
-// F5 (SIMT): for one expert tile, Yrep[row] = g * gelu(x W1_e^T) W2_e      (Eq. 1)
+// F5 (SIMT): for one 128-row expert tile, Yrep[row] = g * gelu(x W1_e^T) W2_e      (Eq. 1)
 // ---------------------------------------------------------------------------------------------
 template <typename E>
 __global__ void __launch_bounds__(256)
-expert_fwd_simt_kernel(const Tile* __restrict__ tiles, const int32_t* __restrict__ ntiles,
-                       const E* __restrict__ Xs, int64_t ldx, const int32_t* __restrict__ perm,
-                       const float* __restrict__ gate, const E* __restrict__ W1, const E* __restrict__ W2,
-                       int64_t T, int k, int N_e, int d_h, int d_e, E* __restrict__ Yrep) {
-  if ((int)blockIdx.x >= *ntiles) return;
-  const Tile tl = tiles[blockIdx.x];
+expert_fwd_simt_kernel(Routing rt, const E* __restrict__ Xs, int64_t ldx, const E* __restrict__ W1,
+                       const E* __restrict__ W2, int d_h, int d_e, E* __restrict__ Yrep) {
+  if ((int)blockIdx.x >= *rt.ntiles) return;
+  const Tile tl = rt.tiles[blockIdx.x];
   extern __shared__ __align__(16) float sm[];
   float* Xsub = sm;                                   // [kSub][d_h+1]
   float* Asub = Xsub + kSub * (d_h + 1);              // [kSub][d_e+1]
   float* gsub = Asub + kSub * (d_e + 1);              // [kSub]
-  const int64_t R = T * k;
-  const size_t wofs = ((size_t)tl.head * N_e + tl.expert) * d_e * d_h;
+  const size_t hrow = (size_t)tl.head * rt.Rp + tl.row0;
+  const size_t wofs = ((size_t)tl.head * rt.N_e + tl.expert) * d_e * d_h;
   const E* w1 = W1 + wofs;
   const E* w2 = W2 + wofs;
-  for (int s0 = 0; s0 < tl.rows; s0 += kSub) {
-    const int nr = min(kSub, tl.rows - s0);
+  for (int s0 = 0; s0 < kExpertBM; s0 += kSub) {
     __syncthreads();
     for (int o = threadIdx.x; o < kSub * d_h; o += blockDim.x) {
       const int r = o / d_h, c = o % d_h;
-      float v = 0.0f;
-      if (r < nr) {
-        const int rep = perm[(size_t)tl.head * R + tl.row0 + s0 + r];
-        v = to_f(Xs[(int64_t)(rep / k) * ldx + (int64_t)tl.head * d_h + c]);
-      }
-      Xsub[r * (d_h + 1) + c] = v;
+      Xsub[r * (d_h + 1) + c] = to_f(Xs[(int64_t)rt.tok_s[hrow + s0 + r] * ldx + (int64_t)tl.head * d_h + c]);
     }
-    for (int r = threadIdx.x; r < kSub; r += blockDim.x) {
-      float g = 0.0f;
-      if (r < nr) {
-        const int rep = perm[(size_t)tl.head * R + tl.row0 + s0 + r];
-        g = gate[(size_t)tl.head * R + rep];
-      }
-      gsub[r] = g;
-    }
+    for (int r = threadIdx.x; r < kSub; r += blockDim.x) gsub[r] = rt.gate_s[hrow + s0 + r];
     __syncthreads();
     for (int o = threadIdx.x; o < kSub * d_e; o += blockDim.x) {
       const int r = o / d_e, f = o % d_e;
@@ -59,10 +44,9 @@ expert_fwd_simt_kernel(const Tile* __restrict__ tiles, const int32_t* __restrict
     __syncthreads();
     for (int o = threadIdx.x; o < kSub * d_h; o += blockDim.x) {
       const int r = o / d_h, c = o % d_h;
-      if (r >= nr) continue;
       float acc = 0.0f;
       for (int f = 0; f < d_e; ++f) acc = fmaf(Asub[r * (d_e + 1) + f], to_f(w2[(size_t)f * d_h + c]), acc);
-      Yrep[((size_t)tl.head * R + tl.row0 + s0 + r) * d_h + c] = from_f<E>(gsub[r] * acc);
+      Yrep[(hrow + s0 + r) * d_h + c] = from_f<E>(gsub[r] * acc);
     }
   }
 }
@@ -73,43 +57,29 @@ expert_fwd_simt_kernel(const Tile* __restrict__ tiles, const int32_t* __restrict
 // ---------------------------------------------------------------------------------------------
 template <typename E>
 __global__ void __launch_bounds__(256)
-expert_bwd_simt_kernel(const Tile* __restrict__ tiles, const int32_t* __restrict__ ntiles,
-                       const E* __restrict__ Xs, int64_t ldx, const E* __restrict__ dY, int64_t ldy,
-                       const int32_t* __restrict__ perm, const float* __restrict__ gate,
-                       const E* __restrict__ W1, const E* __restrict__ W2, int64_t T, int k, int N_e, int d_h,
-                       int d_e, E* __restrict__ dXrep, float* __restrict__ dg, E* __restrict__ dH,
-                       E* __restrict__ gA) {
-  if ((int)blockIdx.x >= *ntiles) return;
-  const Tile tl = tiles[blockIdx.x];
+expert_bwd_simt_kernel(Routing rt, const E* __restrict__ Xs, int64_t ldx, const E* __restrict__ dY, int64_t ldy,
+                       const E* __restrict__ W1, const E* __restrict__ W2, int d_h, int d_e, E* __restrict__ dXrep,
+                       float* __restrict__ dg, E* __restrict__ dH, E* __restrict__ gA) {
+  if ((int)blockIdx.x >= *rt.ntiles) return;
+  const Tile tl = rt.tiles[blockIdx.x];
   extern __shared__ __align__(16) float sm[];
   float* Xsub = sm;                                   // [kSub][d_h+1]
   float* Ysub = Xsub + kSub * (d_h + 1);              // [kSub][d_h+1]  (dY rows)
   float* Hsub = Ysub + kSub * (d_h + 1);              // [kSub][d_e+1]
   float* Dsub = Hsub + kSub * (d_e + 1);              // [kSub][d_e+1]
   float* gsub = Dsub + kSub * (d_e + 1);              // [kSub]
-  int* rsub = reinterpret_cast<int*>(gsub + kSub);    // [kSub]
-  const int64_t R = T * k;
-  const size_t wofs = ((size_t)tl.head * N_e + tl.expert) * d_e * d_h;
+  const size_t hrow = (size_t)tl.head * rt.Rp + tl.row0;
+  const size_t wofs = ((size_t)tl.head * rt.N_e + tl.expert) * d_e * d_h;
   const E* w1 = W1 + wofs;
   const E* w2 = W2 + wofs;
-  for (int s0 = 0; s0 < tl.rows; s0 += kSub) {
-    const int nr = min(kSub, tl.rows - s0);
+  for (int s0 = 0; s0 < kExpertBM; s0 += kSub) {
     __syncthreads();
-    for (int r = threadIdx.x; r < kSub; r += blockDim.x) {
-      int rep = -1; float g = 0.0f;
-      if (r < nr) { rep = perm[(size_t)tl.head * R + tl.row0 + s0 + r]; g = gate[(size_t)tl.head * R + rep]; }
-      rsub[r] = rep; gsub[r] = g;
-    }
-    __syncthreads();
+    for (int r = threadIdx.x; r < kSub; r += blockDim.x) gsub[r] = rt.gate_s[hrow + s0 + r];
     for (int o = threadIdx.x; o < kSub * d_h; o += blockDim.x) {
       const int r = o / d_h, c = o % d_h;
-      float xv = 0.0f, yv = 0.0f;
-      if (r < nr) {
-        const int64_t t = rsub[r] / k;
-        xv = to_f(Xs[t * ldx + (int64_t)tl.head * d_h + c]);
-        yv = to_f(dY[t * ldy + (int64_t)tl.head * d_h + c]);
-      }
-      Xsub[r * (d_h + 1) + c] = xv; Ysub[r * (d_h + 1) + c] = yv;
+      const int64_t t = rt.tok_s[hrow + s0 + r];
+      Xsub[r * (d_h + 1) + c] = to_f(Xs[t * ldx + (int64_t)tl.head * d_h + c]);
+      Ysub[r * (d_h + 1) + c] = to_f(dY[t * ldy + (int64_t)tl.head * d_h + c]);
     }
     __syncthreads();
     for (int o = threadIdx.x; o < kSub * d_e; o += blockDim.x) {
@@ -124,10 +94,11 @@ expert_bwd_simt_kernel(const Tile* __restrict__ tiles, const int32_t* __restrict
     __syncthreads();
     // dg (one thread per row, fixed f order), then dH / gA in place
     for (int r = threadIdx.x; r < kSub; r += blockDim.x) {
-      if (r >= nr) continue;
+      const int rep = rt.perm[hrow + s0 + r];
+      if (rep < 0) continue;
       float acc = 0.0f;
       for (int f = 0; f < d_e; ++f) acc = fmaf(gelu_f(Hsub[r * (d_e + 1) + f]), Dsub[r * (d_e + 1) + f], acc);
-      dg[(size_t)tl.head * R + rsub[r]] = acc;
+      dg[(size_t)tl.head * rt.T * rt.k + rep] = acc;
     }
     __syncthreads();
     for (int o = threadIdx.x; o < kSub * d_e; o += blockDim.x) {
@@ -137,52 +108,49 @@ expert_bwd_simt_kernel(const Tile* __restrict__ tiles, const int32_t* __restrict
       const float dh = g * Dsub[r * (d_e + 1) + f] * gelu_grad_f(h);
       const float ga = g * gelu_f(h);
       Dsub[r * (d_e + 1) + f] = dh;
-      if (r < nr) {
-        const size_t row = (size_t)tl.head * R + tl.row0 + s0 + r;
-        dH[row * d_e + f] = from_f<E>(dh);
-        gA[row * d_e + f] = from_f<E>(ga);
-      }
+      const size_t row = hrow + s0 + r;
+      dH[row * d_e + f] = from_f<E>(dh);
+      gA[row * d_e + f] = from_f<E>(ga);
     }
     __syncthreads();
     for (int o = threadIdx.x; o < kSub * d_h; o += blockDim.x) {
       const int r = o / d_h, c = o % d_h;
-      if (r >= nr) continue;
       float acc = 0.0f;
       for (int f = 0; f < d_e; ++f) acc = fmaf(Dsub[r * (d_e + 1) + f], to_f(w1[(size_t)f * d_h + c]), acc);
-      dXrep[((size_t)tl.head * R + tl.row0 + s0 + r) * d_h + c] = from_f<E>(acc);
+      dXrep[(hrow + s0 + r) * d_h + c] = from_f<E>(acc);
     }
   }
 }
 
-// B5 weight gradients (SIMT): block (f-chunk of 8, e, h); thread = feature c; rows in sorted order.
+// B5 weight gradients (SIMT): block (f-chunk of 8, e, h); thread = feature c; padded segment rows in
+// order (padding rows have dH = gA = 0).
 template <typename E>
 __global__ void __launch_bounds__(256)
-expert_dw_simt_kernel(const int32_t* __restrict__ off, const E* __restrict__ Xs, int64_t ldx,
-                      const E* __restrict__ dY, int64_t ldy, const int32_t* __restrict__ perm,
-                      const E* __restrict__ dH, const E* __restrict__ gA, int64_t R, int k, int N_e, int d_h,
-                      int d_e, float* __restrict__ dW1, float* __restrict__ dW2) {
+expert_dw_simt_kernel(Routing rt, const E* __restrict__ Xs, int64_t ldx, const E* __restrict__ dY, int64_t ldy,
+                      const E* __restrict__ dH, const E* __restrict__ gA, int d_h, int d_e, float* __restrict__ dW1,
+                      float* __restrict__ dW2) {
   const int f0 = blockIdx.x * 8, e = blockIdx.y, h = blockIdx.z;
   const int nf = min(8, d_e - f0);
-  const int32_t* offh = off + (size_t)h * (N_e + 1);
+  const int32_t* offh = rt.off + (size_t)h * (rt.N_e + 1);
   const int beg = offh[e], end = offh[e + 1];
   for (int c = threadIdx.x; c < d_h; c += blockDim.x) {
     float a1[8], a2[8];
 #pragma unroll
     for (int q = 0; q < 8; ++q) { a1[q] = 0.0f; a2[q] = 0.0f; }
     for (int row = beg; row < end; ++row) {
-      const int64_t t = perm[(size_t)h * R + row] / k;
+      const size_t hr = (size_t)h * rt.Rp + row;
+      const int64_t t = rt.tok_s[hr];
       const float xv = to_f(Xs[t * ldx + (int64_t)h * d_h + c]);
       const float yv = to_f(dY[t * ldy + (int64_t)h * d_h + c]);
-      const size_t hr = ((size_t)h * R + row) * d_e + f0;
 #pragma unroll
       for (int q = 0; q < 8; ++q) {
         if (q < nf) {
-          a1[q] = fmaf(to_f(dH[hr + q]), xv, a1[q]);
-          a2[q] = fmaf(to_f(gA[hr + q]), yv, a2[q]);
+          a1[q] = fmaf(to_f(dH[hr * d_e + f0 + q]), xv, a1[q]);
+          a2[q] = fmaf(to_f(gA[hr * d_e + f0 + q]), yv, a2[q]);
         }
       }
     }
-    const size_t wofs = ((size_t)h * N_e + e) * d_e * d_h;
+    const size_t wofs = ((size_t)h * rt.N_e + e) * d_e * d_h;
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
       if (q < nf) {
@@ -278,52 +246,45 @@ void set_smem(F f, size_t bytes) { cudaFuncSetAttribute(f, cudaFuncAttributeMaxD
 
 }  // namespace
 
-void launch_expert_fwd_simt(int dtype, const Tile* tiles, const int32_t* ntiles, int max_tiles, const void* Xs,
-                            int64_t ldx, const int32_t* perm, const float* gate, const void* W1, const void* W2,
-                            int64_t T, int k, int N_e, int d_h, int d_e, void* Yrep, cudaStream_t s) {
+void launch_expert_fwd_simt(int dtype, const Routing& rt, const void* Xs, int64_t ldx, const void* W1, const void* W2,
+                            int d_h, int d_e, void* Yrep, cudaStream_t s) {
   const size_t smem = sizeof(float) * (kSub * (d_h + 1) + kSub * (d_e + 1) + kSub);
   if (dtype == 1) {
     auto f = expert_fwd_simt_kernel<bf16>; set_smem(f, smem);
-    f<<<max_tiles, 256, smem, s>>>(tiles, ntiles, (const bf16*)Xs, ldx, perm, gate, (const bf16*)W1, (const bf16*)W2,
-                                   T, k, N_e, d_h, d_e, (bf16*)Yrep);
+    f<<<rt.max_tiles, 256, smem, s>>>(rt, (const bf16*)Xs, ldx, (const bf16*)W1, (const bf16*)W2, d_h, d_e,
+                                      (bf16*)Yrep);
   } else {
     auto f = expert_fwd_simt_kernel<float>; set_smem(f, smem);
-    f<<<max_tiles, 256, smem, s>>>(tiles, ntiles, (const float*)Xs, ldx, perm, gate, (const float*)W1,
-                                   (const float*)W2, T, k, N_e, d_h, d_e, (float*)Yrep);
+    f<<<rt.max_tiles, 256, smem, s>>>(rt, (const float*)Xs, ldx, (const float*)W1, (const float*)W2, d_h, d_e,
+                                      (float*)Yrep);
   }
 }
 
-void launch_expert_bwd_simt(int dtype, const Tile* tiles, const int32_t* ntiles, int max_tiles, const void* Xs,
-                            int64_t ldx, const void* dY, int64_t ldy, const int32_t* perm, const float* gate,
-                            const void* W1, const void* W2, int64_t T, int k, int N_e, int d_h, int d_e, void* dXrep,
-                            float* dg, void* dH, void* gA, cudaStream_t s) {
-  const size_t smem = sizeof(float) * (2 * kSub * (d_h + 1) + 2 * kSub * (d_e + 1) + 2 * kSub);
+void launch_expert_bwd_simt(int dtype, const Routing& rt, const void* Xs, int64_t ldx, const void* dY, int64_t ldy,
+                            const void* W1, const void* W2, int d_h, int d_e, void* dXrep, float* dg, void* dH,
+                            void* gA, cudaStream_t s) {
+  const size_t smem = sizeof(float) * (2 * kSub * (d_h + 1) + 2 * kSub * (d_e + 1) + kSub);
   if (dtype == 1) {
     auto f = expert_bwd_simt_kernel<bf16>; set_smem(f, smem);
-    f<<<max_tiles, 256, smem, s>>>(tiles, ntiles, (const bf16*)Xs, ldx, (const bf16*)dY, ldy, perm, gate,
-                                   (const bf16*)W1, (const bf16*)W2, T, k, N_e, d_h, d_e, (bf16*)dXrep, dg,
-                                   (bf16*)dH, (bf16*)gA);
+    f<<<rt.max_tiles, 256, smem, s>>>(rt, (const bf16*)Xs, ldx, (const bf16*)dY, ldy, (const bf16*)W1,
+                                      (const bf16*)W2, d_h, d_e, (bf16*)dXrep, dg, (bf16*)dH, (bf16*)gA);
   } else {
     auto f = expert_bwd_simt_kernel<float>; set_smem(f, smem);
-    f<<<max_tiles, 256, smem, s>>>(tiles, ntiles, (const float*)Xs, ldx, (const float*)dY, ldy, perm, gate,
-                                   (const float*)W1, (const float*)W2, T, k, N_e, d_h, d_e, (float*)dXrep, dg,
-                                   (float*)dH, (float*)gA);
+    f<<<rt.max_tiles, 256, smem, s>>>(rt, (const float*)Xs, ldx, (const float*)dY, ldy, (const float*)W1,
+                                      (const float*)W2, d_h, d_e, (float*)dXrep, dg, (float*)dH, (float*)gA);
   }
 }
 
-void launch_expert_dw_simt(int dtype, const int32_t* off, const void* Xs, int64_t ldx, const void* dY, int64_t ldy,
-                           const int32_t* perm, const void* dH, const void* gA, int H, int64_t T, int k, int N_e,
-                           int d_h, int d_e, float* dW1, float* dW2, cudaStream_t s) {
-  dim3 grid((d_e + 7) / 8, N_e, H);
+void launch_expert_dw_simt(int dtype, const Routing& rt, const void* Xs, int64_t ldx, const void* dY, int64_t ldy,
+                           const void* dH, const void* gA, int d_h, int d_e, float* dW1, float* dW2, cudaStream_t s) {
+  dim3 grid((d_e + 7) / 8, rt.N_e, rt.H);
   const int threads = d_h >= 256 ? 256 : ((d_h + 31) / 32) * 32;
-  const int64_t R = T * k;
   if (dtype == 1)
-    expert_dw_simt_kernel<bf16><<<grid, threads, 0, s>>>(off, (const bf16*)Xs, ldx, (const bf16*)dY, ldy, perm,
-                                                         (const bf16*)dH, (const bf16*)gA, R, k, N_e, d_h, d_e, dW1, dW2);
+    expert_dw_simt_kernel<bf16><<<grid, threads, 0, s>>>(rt, (const bf16*)Xs, ldx, (const bf16*)dY, ldy,
+                                                         (const bf16*)dH, (const bf16*)gA, d_h, d_e, dW1, dW2);
   else
-    expert_dw_simt_kernel<float><<<grid, threads, 0, s>>>(off, (const float*)Xs, ldx, (const float*)dY, ldy, perm,
-                                                          (const float*)dH, (const float*)gA, R, k, N_e, d_h, d_e, dW1,
-                                                          dW2);
+    expert_dw_simt_kernel<float><<<grid, threads, 0, s>>>(rt, (const float*)Xs, ldx, (const float*)dY, ldy,
+                                                          (const float*)dH, (const float*)gA, d_h, d_e, dW1, dW2);
 }
 
 void launch_permute_blocks(int dtype, const void* src, void* dst, int G, int64_t T_loc, int64_t HD, cudaStream_t s) {
