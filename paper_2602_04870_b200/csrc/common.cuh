@@ -25,6 +25,43 @@ __device__ __forceinline__ float gelu_grad_f(float x) {
   return cdf + x * pdf;
 }
 
+// Exact-erf GELU for a pair of values with packed f32x2 math (sm_100 FFMA2/FMUL2) and one
+// ex2 + one rcp per element: Phi(x) = 1/2 (1 + sign(x) erf(|x|/sqrt 2)) with erf from
+// Abramowitz-Stegun 7.1.26 (|error| <= 1.5e-7; R1 requires the erf form, not tanh).
+// Returns gelu(x) = x Phi(x); if dgelu != nullptr also gelu'(x) = Phi(x) + x phi(x), reusing
+// exp(-x^2/2) for phi.
+__device__ __forceinline__ float fast_rcp(float x) {
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+__device__ __forceinline__ float fast_ex2(float x) {
+  float r;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+__device__ __forceinline__ float2 gelu2(float2 h, float2* dgelu) {
+  const float2 hh = __fmul2_rn(h, h);
+  const float2 z = make_float2(fabsf(h.x) * 0.70710678118654752f, fabsf(h.y) * 0.70710678118654752f);
+  const float2 d = __ffma2_rn(make_float2(0.3275911f, 0.3275911f), z, make_float2(1.f, 1.f));
+  const float2 t = make_float2(fast_rcp(d.x), fast_rcp(d.y));
+  float2 q = __ffma2_rn(make_float2(1.061405429f, 1.061405429f), t, make_float2(-1.453152027f, -1.453152027f));
+  q = __ffma2_rn(q, t, make_float2(1.421413741f, 1.421413741f));
+  q = __ffma2_rn(q, t, make_float2(-0.284496736f, -0.284496736f));
+  q = __ffma2_rn(q, t, make_float2(0.254829592f, 0.254829592f));
+  q = __fmul2_rn(q, t);
+  const float2 ea = __fmul2_rn(hh, make_float2(-0.72134752044448170f, -0.72134752044448170f));  // -x^2/2 log2 e
+  const float2 e = make_float2(fast_ex2(ea.x), fast_ex2(ea.y));                                  // exp(-x^2/2)
+  const float2 erfa = __ffma2_rn(make_float2(-q.x, -q.y), e, make_float2(1.f, 1.f));             // erf(|x|/sqrt2)
+  const float2 hp = __fmul2_rn(erfa, make_float2(0.5f, 0.5f));
+  const float2 phi = make_float2(0.5f + copysignf(hp.x, h.x), 0.5f + copysignf(hp.y, h.y));     // Phi(x)
+  if (dgelu) {
+    const float2 pdf = __fmul2_rn(e, make_float2(0.39894228040143268f, 0.39894228040143268f));
+    *dgelu = __ffma2_rn(h, pdf, phi);
+  }
+  return __fmul2_rn(h, phi);
+}
+
 // Order-preserving float -> uint32 (R6): flip sign bit of non-negatives, all bits of negatives.
 __device__ __forceinline__ uint32_t ord32(float v) {
   uint32_t u = __float_as_uint(v == 0.0f ? 0.0f : v);   // canonicalise -0.0

@@ -10,14 +10,17 @@
 //   epi 1  A = bf16(g * gelu(H)) -> TMEM          (exact-erf GELU, R1; A never touches smem)
 //   GEMM2  Y[128 x d_h] = A W2_e                 A read from TMEM; B = W2_e read MN-major
 //   epi 2  Yrep rows = bf16(Y)                   TMEM -> registers -> smem -> TMA bulk store
-// Warp roles (320 threads): warp 0 = producer (sub-token gathers through an smem ring, W1/W2 by
+// Warp roles (416 threads): warps 0-3 = producers (sub-token gathers through an smem ring, W1/W2 by
 // TMA when the expert changes, each as soon as the previous expert's last GEMM reading it has
-// completed), warp 1 = MMA issuer (+ TMEM owner), warps 2-9 = epilogue.  TMEM: H [0,128),
+// completed), warp 4 = MMA issuer (+ TMEM owner), warps 5-12 = epilogue.  TMEM: H [0,128),
 // A double buffer [128,256), Y [256,512): the MMA order G1(i), G2(i-1), G1(i+1), ... keeps the
 // tensor pipe busy while the epilogue of neighbouring tiles runs.  Persistent CTAs take groups of
 // kTileGroup consecutive tiles round-robin (weights reused within a group; the tiles in flight
 // stay inside one head, whose sub-tokens then stay L2-resident for their k gathers).
 #include <cuda.h>
+
+#include <cstdio>
+#include <cstdlib>
 
 #include "kernels.h"
 #include "sm100.cuh"
@@ -29,8 +32,13 @@ namespace {
 
 using namespace sm100;
 
+__device__ TraceBuf g_trace_fwd;     // profiling aid (MHL_TRACE_FWD=<file>), off by default
+
 constexpr int BM = kExpertBM;        // 128 rows = MMA M
-constexpr int kThreads = 320;
+constexpr int kProdWarps = 4;         // warps 0-3: producers
+constexpr int kMmaWarp = 4;           // warp 4: MMA issuer + TMEM owner
+constexpr int kEpiWarp0 = 5;          // warps 5-12: epilogue
+constexpr int kThreads = 13 * 32;
 constexpr int kEpiThreads = 256;
 constexpr int kXChunk = BM * 128;    // one 64-column K-chunk of the gathered X tile (16 KB)
 constexpr int kYStage = BM * 128;    // one 64-column block of the Y tile (16 KB)
@@ -85,7 +93,7 @@ expert_fwd_sm100_kernel(const __grid_constant__ CUtensorMap w1map, const __grid_
   const int N_e = rt.N_e;
 
   if (tid == 0) {
-    for (int i = 0; i < XS; ++i) { mbar_init(bar(L::B_XFULL + 8 * i), 32); mbar_init(bar(L::B_XEMPTY + 8 * i), 1); }
+    for (int i = 0; i < XS; ++i) { mbar_init(bar(L::B_XFULL + 8 * i), 32 * kProdWarps); mbar_init(bar(L::B_XEMPTY + 8 * i), 1); }
     mbar_init(bar(L::B_W1F), 1); mbar_init(bar(L::B_W1E), 1); mbar_init(bar(L::B_W2F), 1); mbar_init(bar(L::B_W2E), 1);
     mbar_init(bar(L::B_HFULL), 1);
     mbar_init(bar(L::B_HFREE), kEpiThreads);
@@ -94,7 +102,7 @@ expert_fwd_sm100_kernel(const __grid_constant__ CUtensorMap w1map, const __grid_
     fence_mbar_init();
     tma_prefetch_desc(&w1map); tma_prefetch_desc(&w2map); tma_prefetch_desc(&ymap);
   }
-  if (warp == 1) tmem_alloc<512>(s_tmem);
+  if (warp == kMmaWarp) tmem_alloc<512>(s_tmem);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -118,24 +126,25 @@ expert_fwd_sm100_kernel(const __grid_constant__ CUtensorMap w1map, const __grid_
     for (int kb = 0; kb < KB1; ++kb) tma_load_2d(sb + off + kb * DE * 128, map, kb * 64, (t.head * N_e + t.expert) * DE, full);
   };
 
-  if (warp == 0) {
-    // ================================================================ producer
+  if (warp < kProdWarps) {
+    // ================================================================ producers (4 warps)
+    // warp pw gathers rows [32 pw, 32 pw + 32) of every X chunk (more loads in flight per SM);
+    // warp 0 lane 0 also issues the weight TMAs.
+    const int pw = warp;
     Ph xe[12], w1e, w2e;
     int xs = 0;
-    int tok_next[BM / 32];
+    int tok_next = 0;
     {
       const int t0 = tile_at(0);
       if (t0 >= 0) {
         const Tile tl = tiles[t0];
-        const int32_t* ts = rt.tok_s + (size_t)tl.head * rt.Rp + tl.row0;
-#pragma unroll
-        for (int u = 0; u < BM / 32; ++u) tok_next[u] = ts[u * 32 + lane];
+        tok_next = rt.tok_s[(size_t)tl.head * rt.Rp + tl.row0 + pw * 32 + lane];
       }
     }
     for (int i = 0;; ++i) {
       const int ti = tile_at(i);
       if (ti < 0) {
-        if (i >= 1 && lane == 0 && !same_expert(tile_at(i - 2), tile_at(i - 1))) {
+        if (pw == 0 && i >= 1 && lane == 0 && !same_expert(tile_at(i - 2), tile_at(i - 1))) {
           mbar_wait(bar(L::B_W2E), w2e.flip() ^ 1);
           load_w(&w2map, L::W2, bar(L::B_W2F), tiles[tile_at(i - 1)]);
         }
@@ -144,17 +153,14 @@ expert_fwd_sm100_kernel(const __grid_constant__ CUtensorMap w1map, const __grid_
       const Tile tl = tiles[ti];
       // this tile's token ids (loaded one tile ahead) -> smem; prefetch the next tile's
       __syncwarp();
-#pragma unroll
-      for (int u = 0; u < BM / 32; ++u) s_tok[u * 32 + lane] = tok_next[u];
+      s_tok[pw * 32 + lane] = tok_next;
       const int tn = tile_at(i + 1);
       if (tn >= 0) {
         const Tile tnl = tiles[tn];
-        const int32_t* ts = rt.tok_s + (size_t)tnl.head * rt.Rp + tnl.row0;
-#pragma unroll
-        for (int u = 0; u < BM / 32; ++u) tok_next[u] = ts[u * 32 + lane];
+        tok_next = rt.tok_s[(size_t)tnl.head * rt.Rp + tnl.row0 + pw * 32 + lane];
       }
       __syncwarp();
-      if (lane == 0 && !same_expert(tile_at(i - 1), ti)) {
+      if (pw == 0 && lane == 0 && !same_expert(tile_at(i - 1), ti)) {
         mbar_wait(bar(L::B_W1E), w1e.flip() ^ 1);
         load_w(&w1map, L::W1, bar(L::B_W1F), tl);
       }
@@ -163,21 +169,22 @@ expert_fwd_sm100_kernel(const __grid_constant__ CUtensorMap w1map, const __grid_
         mbar_wait_warp(bar(L::B_XEMPTY + 8 * xs), xe[xs].flip() ^ 1);
         const uint32_t dst = sb + L::X + xs * kXChunk;
         const bf16* src = Xg + (size_t)tl.head * DH + kb * 64;
-#pragma unroll 8
-        for (int j = 0; j < BM * 8 / 32; ++j) {
-          const int idx = j * 32 + lane, r = idx >> 3, c = (idx & 7) * 8;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const int idx = j * 32 + lane, r = pw * 32 + (idx >> 3), c = (idx & 7) * 8;
           cp_async_16(dst + kmaj_off(r, c, BM), src + (size_t)s_tok[r] * ldx + c, 16);
         }
         cp_async_mbar_arrive(bar(L::B_XFULL + 8 * xs));
+        if (pw == 0 && lane == 0) trace_ev(g_trace_fwd, 2, i * 16 + kb);
         if (++xs == XS) xs = 0;
       }
       // W2 of the previous tile if it started a new expert run (read by G2(i-1), issued after G1(i))
-      if (lane == 0 && i >= 1 && !same_expert(tile_at(i - 2), tile_at(i - 1))) {
+      if (pw == 0 && lane == 0 && i >= 1 && !same_expert(tile_at(i - 2), tile_at(i - 1))) {
         mbar_wait(bar(L::B_W2E), w2e.flip() ^ 1);
         load_w(&w2map, L::W2, bar(L::B_W2F), tiles[tile_at(i - 1)]);
       }
     }
-  } else if (warp == 1) {
+  } else if (warp == kMmaWarp) {
     // ================================================================ MMA issuer
     if (lane == 0) {
       constexpr uint32_t ID1 = idesc_bf16(BM, DE, 0, 0);
@@ -190,12 +197,14 @@ expert_fwd_sm100_kernel(const __grid_constant__ CUtensorMap w1map, const __grid_
         if (!same_expert(tile_at(j - 1), tj)) mbar_wait(bar(L::B_W2F), w2f.flip());
         mbar_wait(bar(L::B_AFULL + 8 * b), af[b].flip());
         mbar_wait(bar(L::B_YEMPTY), ye.flip() ^ 1);
+        trace_ev(g_trace_fwd, 13, j);
         tc_fence_after();
 #pragma unroll
         for (int ks = 0; ks < DE / 16; ++ks)
           mma_bf16_ts(tmem + L::T_Y, tmem + L::T_A + b * (DE / 2) + ks * 8,
                       sdesc_sw128(sb + L::W2 + ks * 2 * 1024, DE * 128, 1024), ID2, ks > 0);
         mma_commit(bar(L::B_G2DONE + 8 * b));
+        trace_ev(g_trace_fwd, 14, j);
         if (!same_expert(tj, tile_at(j + 1))) mma_commit(bar(L::B_W2E));
       };
       int i = 0;
@@ -204,9 +213,11 @@ expert_fwd_sm100_kernel(const __grid_constant__ CUtensorMap w1map, const __grid_
         if (ti < 0) break;
         if (!same_expert(tile_at(i - 1), ti)) mbar_wait(bar(L::B_W1F), w1f.flip());
         if (i >= 1) mbar_wait(bar(L::B_HFREE), hfr.flip());   // epilogue has read H of tile i-1
+        trace_ev(g_trace_fwd, 10, i);
         tc_fence_after();
         for (int kb = 0; kb < KB1; ++kb) {
           mbar_wait(bar(L::B_XFULL + 8 * xs), xf[xs].flip());
+          trace_ev(g_trace_fwd, 11, i * 16 + kb);
           fence_proxy_async();   // the chunk was written by cp.async (generic proxy)
           tc_fence_after();
 #pragma unroll
@@ -224,9 +235,9 @@ expert_fwd_sm100_kernel(const __grid_constant__ CUtensorMap w1map, const __grid_
     }
   } else {
     // ================================================================ epilogue (8 warps)
-    const int q = warp & 3, half = (warp - 2) >> 2;   // warps 2..5 -> half 0, 6..9 -> half 1
+    const int q = warp & 3, half = (warp - kEpiWarp0) >> 2;   // lane quadrant, column half
     const int row = q * 32 + lane;
-    const int et = tid - 64;
+    const int et = tid - kEpiWarp0 * 32;
     const uint32_t lane_off = (uint32_t)(q * 32) << 16;
     Ph hf, gd[2];
     int ys = 0;   // running count of Y blocks stored (selects the smem stage)
@@ -234,18 +245,25 @@ expert_fwd_sm100_kernel(const __grid_constant__ CUtensorMap w1map, const __grid_
       const int b = j & 1;
       const Tile tl = tiles[tile_at(j)];
       mbar_wait_warp(bar(L::B_G2DONE + 8 * b), gd[b].flip());
+      if (et == 0) trace_ev(g_trace_fwd, 23, j);
       tc_fence_after();
-      // 64-column blocks: TMEM -> regs -> bf16 -> smem stage (SW128) -> one TMA bulk store per block
+      // 64-column blocks: TMEM -> regs -> bf16 -> smem stage (SW128) -> TMA bulk store.  The two
+      // warps of a lane quadrant own a 32-row slab and synchronise only with each other.
+      const bool leader = (half == 0 && lane == 0);
 #pragma unroll 1
       for (int cb = 0; cb < DH / 64; ++cb, ++ys) {
         const int st = ys & 1;
         uint32_t v[32];
         tmem_ld32(tmem + L::T_Y + lane_off + cb * 64 + half * 32, v);
         tmem_ld_wait();
-        if (cb == DH / 64 - 1) { tc_fence_before(); mbar_arrive(bar(L::B_YEMPTY)); }
-        if (et == 0) bulk_wait_read<1>();      // the store issued from this stage 2 blocks ago has read it
-        named_bar_sync(1, kEpiThreads);
-        uint8_t* sp = smem + L::YS + st * kYStage;
+        if (cb == DH / 64 - 1) {
+          tc_fence_before();
+          mbar_arrive(bar(L::B_YEMPTY));
+          if (et == 0) trace_ev(g_trace_fwd, 24, j);
+        }
+        if (leader) bulk_wait_read<1>();       // the slab store issued from this stage 2 blocks ago has read it
+        named_bar_sync(2 + q, 64);
+        uint8_t* sp = smem + L::YS + st * kYStage + q * 4096;
 #pragma unroll
         for (int u = 0; u < 32; u += 8) {
           uint4 pk;
@@ -253,12 +271,13 @@ expert_fwd_sm100_kernel(const __grid_constant__ CUtensorMap w1map, const __grid_
           pk.y = pack_bf16x2(__uint_as_float(v[u + 2]), __uint_as_float(v[u + 3]));
           pk.z = pack_bf16x2(__uint_as_float(v[u + 4]), __uint_as_float(v[u + 5]));
           pk.w = pack_bf16x2(__uint_as_float(v[u + 6]), __uint_as_float(v[u + 7]));
-          *reinterpret_cast<uint4*>(sp + kmaj_off(row, half * 32 + u, BM)) = pk;
+          *reinterpret_cast<uint4*>(sp + kmaj_off(lane, half * 32 + u, 32)) = pk;
         }
         fence_proxy_async();
-        named_bar_sync(1, kEpiThreads);
-        if (et == 0) {
-          tma_store_2d(&ymap, sb + L::YS + st * kYStage, cb * 64, (int)((size_t)tl.head * rt.Rp + tl.row0));
+        named_bar_sync(2 + q, 64);
+        if (leader) {
+          tma_store_2d(&ymap, sb + L::YS + st * kYStage + q * 4096, cb * 64,
+                       (int)((size_t)tl.head * rt.Rp + tl.row0 + q * 32));
           bulk_commit();
         }
       }
@@ -271,6 +290,7 @@ expert_fwd_sm100_kernel(const __grid_constant__ CUtensorMap w1map, const __grid_
       const int b = i & 1;
       const float g = rt.gate_s[(size_t)tl.head * rt.Rp + tl.row0 + row];
       mbar_wait_warp(bar(L::B_HFULL), hf.flip());
+      if (et == 0) trace_ev(g_trace_fwd, 20, i);
       tc_fence_after();
       // epi 1: this warp's DE/2 columns of H -> registers, release H, GELU, A -> TMEM buffer b
       constexpr int NC = DE / 2;
@@ -285,10 +305,14 @@ expert_fwd_sm100_kernel(const __grid_constant__ CUtensorMap w1map, const __grid_
       tmem_ld_wait();
       tc_fence_before();
       mbar_arrive(bar(L::B_HFREE));
+      if (et == 0) trace_ev(g_trace_fwd, 21, i);
       uint32_t pa[NC / 2];
 #pragma unroll
-      for (int u = 0; u < NC; u += 2)
-        pa[u / 2] = pack_bf16x2(g * gelu_f(__uint_as_float(hv[u])), g * gelu_f(__uint_as_float(hv[u + 1])));
+      for (int u = 0; u < NC; u += 2) {
+        const float2 a = __fmul2_rn(gelu2(make_float2(__uint_as_float(hv[u]), __uint_as_float(hv[u + 1])), nullptr),
+                                    make_float2(g, g));
+        pa[u / 2] = pack_bf16x2(a.x, a.y);
+      }
 #pragma unroll
       for (int c = 0; c < NC / 2; c += 16) {
         uint32_t w[16];
@@ -299,14 +323,15 @@ expert_fwd_sm100_kernel(const __grid_constant__ CUtensorMap w1map, const __grid_
       tmem_st_wait();
       tc_fence_before();
       mbar_arrive(bar(L::B_AFULL + 8 * b));
+      if (et == 0) trace_ev(g_trace_fwd, 22, i);
       if (i >= 1) epi2(i - 1);
     }
     if (i >= 1) epi2(i - 1);
-    if (et == 0) bulk_wait_all();
+    if (half == 0 && lane == 0) bulk_wait_all();
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 1) tmem_dealloc<512>(tmem);
+  if (warp == kMmaWarp) tmem_dealloc<512>(tmem);
 }
 
 template <int DH, int DE>
@@ -315,10 +340,33 @@ bool launch_t(const Routing& rt, const void* Xs, int64_t ldx, const void* W1, co
   CUtensorMap w1m, w2m, ym;
   if (!make_tmap_2d_bf16(&w1m, W1, (uint64_t)rt.H * rt.N_e * DE, DH, (uint64_t)DH * 2, DE, 64)) return false;
   if (!make_tmap_2d_bf16(&w2m, W2, (uint64_t)rt.H * rt.N_e * DE, DH, (uint64_t)DH * 2, DE, 64)) return false;
-  if (!make_tmap_2d_bf16(&ym, Yrep, (uint64_t)rt.H * rt.Rp, DH, (uint64_t)DH * 2, BM, 64)) return false;
+  if (!make_tmap_2d_bf16(&ym, Yrep, (uint64_t)rt.H * rt.Rp, DH, (uint64_t)DH * 2, 32, 64)) return false;
   auto kern = expert_fwd_sm100_kernel<DH, DE>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, FwdL<DH, DE>::BYTES);
+  static const char* trace_path = getenv("MHL_TRACE_FWD");
+  static unsigned long long* tbuf = nullptr;
+  const size_t nslot = 32 * 4096;
+  if (trace_path) {
+    if (!tbuf) cudaMalloc(&tbuf, nslot * sizeof(unsigned long long));
+    cudaMemsetAsync(tbuf, 0, nslot * sizeof(unsigned long long), s);
+    TraceBuf tb{tbuf, 0};
+    cudaMemcpyToSymbolAsync(g_trace_fwd, &tb, sizeof(tb), 0, cudaMemcpyHostToDevice, s);
+  }
   kern<<<num_sms, kThreads, FwdL<DH, DE>::BYTES, s>>>(w1m, w2m, ym, rt, (const bf16*)Xs, ldx);
+  if (trace_path) {
+    TraceBuf tb{nullptr, 0};
+    cudaMemcpyToSymbolAsync(g_trace_fwd, &tb, sizeof(tb), 0, cudaMemcpyHostToDevice, s);
+    cudaStreamSynchronize(s);
+    unsigned long long* h = (unsigned long long*)malloc(nslot * sizeof(unsigned long long));
+    cudaMemcpy(h, tbuf, nslot * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
+    FILE* f = fopen(trace_path, "w");
+    if (f) {
+      for (size_t u = 0; u < nslot; ++u)
+        if (h[u]) fprintf(f, "%zu %zu %llu\n", u / 4096, u % 4096, h[u]);
+      fclose(f);
+    }
+    free(h);
+  }
   return true;
 }
 

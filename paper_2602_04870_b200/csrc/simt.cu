@@ -9,6 +9,7 @@ namespace mhl {
 namespace {
 
 constexpr int kSub = 32;    // rows per SIMT sub-tile
+constexpr int kRbwdChunk = 512;   // tokens per router-backward partial (fewer, larger dW_r partials)
 
 // ---------------------------------------------------------------------------------------------
 // F5 (SIMT): for one 128-row expert tile, Yrep[row] = g * gelu(x W1_e^T) W2_e      (Eq. 1)
@@ -188,10 +189,10 @@ router_bwd_partial_kernel(const E* __restrict__ Xs, int64_t ldx, const int32_t* 
   extern __shared__ __align__(16) float smb[];
   float* part = smb;                                  // [N_e][d_h]
   float* sdS = part + (size_t)N_e * d_h;              // [128][k]
-  int* sI = reinterpret_cast<int*>(sdS + kRouterTile * k);   // [128][k]
+  int* sI = reinterpret_cast<int*>(sdS + kRbwdChunk * k);   // [128][k]
   const int chunk = blockIdx.x, h = blockIdx.y;
-  const int64_t t0 = (int64_t)chunk * kRouterTile;
-  const int nt = (int)min((int64_t)kRouterTile, T - t0);
+  const int64_t t0 = (int64_t)chunk * kRbwdChunk;
+  const int nt = (int)min((int64_t)kRbwdChunk, T - t0);
   for (int i = threadIdx.x; i < N_e * d_h; i += blockDim.x) part[i] = 0.0f;
   for (int tt = threadIdx.x; tt < nt; tt += blockDim.x) {
     const size_t base = ((size_t)h * T + t0 + tt) * k;
@@ -299,8 +300,8 @@ void launch_permute_blocks(int dtype, const void* src, void* dst, int G, int64_t
 void launch_router_bwd(int dtype, const void* Xs, int64_t ldx, const int32_t* idx, const float* gate, const float* dg,
                        int H, int64_t T, int k, int d_h, int N_e, float* dS, float* dwr_partial, float* dW_r,
                        cudaStream_t s) {
-  const int n_chunks = (int)((T + kRouterTile - 1) / kRouterTile);
-  const size_t smem = sizeof(float) * ((size_t)N_e * d_h + (size_t)kRouterTile * k) + sizeof(int) * kRouterTile * k;
+  const int n_chunks = (int)((T + kRbwdChunk - 1) / kRbwdChunk);
+  const size_t smem = sizeof(float) * ((size_t)N_e * d_h + (size_t)kRbwdChunk * k) + sizeof(int) * kRbwdChunk * k;
   const int threads = d_h >= 256 ? 256 : ((d_h + 31) / 32) * 32;
   dim3 grid(n_chunks, H);
   if (dtype == 1) {

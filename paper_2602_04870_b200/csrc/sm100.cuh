@@ -184,6 +184,15 @@ __device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
 
+// ---------------------------------------------------------------- optional event trace (profiling aid)
+// When the host installs a buffer (mhl_trace_install), block 0 of a traced kernel records
+// (event id, tile, clock64) triples; costs one predicated branch otherwise.
+// Slot (event, tile) = p[ev * 4096 + tile]: a plain store, no atomics (does not perturb timing).
+struct TraceBuf { unsigned long long* p; unsigned int cap; };
+__device__ __forceinline__ void trace_ev(TraceBuf& tb, int ev, int tile) {
+  if (tb.p != nullptr && blockIdx.x == 0 && tile >= 0 && tile < 4096) tb.p[ev * 4096 + tile] = clock64();
+}
+
 __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
   uint32_t r;
   asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
