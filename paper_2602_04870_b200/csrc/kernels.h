@@ -9,7 +9,7 @@ namespace mhl {
 constexpr int kRouterTile = 128;   // tokens per router CTA (= clustering tile of F4)
 constexpr int kExpertBM = 128;     // replica rows per expert tile (tcgen05 M); segments padded to it
 constexpr int kDwChunk = 4096;     // sorted rows per weight-gradient partial (B5 dW)
-constexpr int kTileGroup = 4;      // consecutive expert tiles a persistent CTA takes at once
+constexpr int kTileGroup = 16;     // consecutive expert tiles a persistent CTA takes at once
 
 // Clustered routing of one rank's local heads (F3/F4 outputs, device pointers).
 // Sorted-row arrays have a fixed per-head capacity Rp = T*k + N_e*128 (expert segments are
@@ -72,6 +72,10 @@ void launch_expert_bwd_simt(int dtype, const Routing& rt, const void* Xs, int64_
 void launch_expert_dw_simt(int dtype, const Routing& rt, const void* Xs, int64_t ldx, const void* dY, int64_t ldy,
                            const void* dH, const void* gA, int d_h, int d_e, float* dW1, float* dW2, cudaStream_t s);
 bool expert_bwd_sm100_supported(int d_h, int d_e);
+// the dX part alone (pipelined warp-specialized kernel, expert_bwd_dx_sm100.cu)
+bool launch_expert_bwd_dx_sm100(const Routing& rt, const void* Xs, int64_t ldx, const void* dY, int64_t ldy,
+                                const void* W1, const void* W2, int d_h, int d_e, void* dXrep, float* dg, void* dH,
+                                void* gA, int num_sms, cudaStream_t s);
 // tcgen05 dX kernel (dXrep, dg, dH, gA) and/or dW kernel (chunk partials + ordered reduce)
 bool launch_expert_bwd_sm100(const Routing& rt, const void* Xs, int64_t ldx, const void* dY, int64_t ldy,
                              const void* W1, const void* W2, int d_h, int d_e, void* dXrep, float* dg, void* dH,

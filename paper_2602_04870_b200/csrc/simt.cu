@@ -9,7 +9,7 @@ namespace mhl {
 namespace {
 
 constexpr int kSub = 32;    // rows per SIMT sub-tile
-constexpr int kRbwdChunk = 512;   // tokens per router-backward partial (fewer, larger dW_r partials)
+constexpr int kRbwdChunk = 128;   // tokens per router-backward partial
 
 // ---------------------------------------------------------------------------------------------
 // F5 (SIMT): for one 128-row expert tile, Yrep[row] = g * gelu(x W1_e^T) W2_e      (Eq. 1)

@@ -4,6 +4,9 @@
 
 #include <cudaTypedefs.h>
 
+#include <cstdio>
+#include <cstdlib>
+
 namespace mhl {
 
 bool make_tmap_2d_bf16(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols, uint64_t row_stride_bytes,
@@ -24,6 +27,27 @@ bool make_tmap_2d_bf16(CUtensorMap* map, const void* base, uint64_t rows, uint64
                             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
+}
+
+static unsigned long long* g_trace_dev = nullptr;
+
+unsigned long long* trace_buffer(cudaStream_t s) {
+  if (!g_trace_dev) cudaMalloc(&g_trace_dev, kTraceSlots * sizeof(unsigned long long));
+  cudaMemsetAsync(g_trace_dev, 0, kTraceSlots * sizeof(unsigned long long), s);
+  return g_trace_dev;
+}
+
+void trace_dump(const char* path, cudaStream_t s) {
+  cudaStreamSynchronize(s);
+  unsigned long long* h = (unsigned long long*)malloc(kTraceSlots * sizeof(unsigned long long));
+  cudaMemcpy(h, g_trace_dev, kTraceSlots * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
+  FILE* f = fopen(path, "w");
+  if (f) {
+    for (size_t u = 0; u < kTraceSlots; ++u)
+      if (h[u]) fprintf(f, "%zu %zu %llu\n", u / 4096, u % 4096, h[u]);
+    fclose(f);
+  }
+  free(h);
 }
 
 }  // namespace mhl

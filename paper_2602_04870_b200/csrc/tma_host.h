@@ -10,4 +10,10 @@ namespace mhl {
 bool make_tmap_2d_bf16(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols, uint64_t row_stride_bytes,
                        uint32_t box_rows, uint32_t box_cols);
 
+// Event-trace profiling aid (see sm100.cuh trace_ev): a zeroed device buffer of kTraceSlots
+// slots, and a dump of the non-zero slots "event tile clock" to a text file.
+constexpr size_t kTraceSlots = 64 * 4096;
+unsigned long long* trace_buffer(cudaStream_t s);
+void trace_dump(const char* path, cudaStream_t s);
+
 }  // namespace mhl

@@ -1,0 +1,73 @@
+#!/usr/bin/env python
+"""Summarise ncu artefacts for profiles/ (runs here, without a GPU).
+
+    python tools/ncu_summary.py launches gpurun_out/r1b_launches.csv      # per-kernel share of a step
+    python tools/ncu_summary.py report gpurun_out/r1b_prof_expert_fwd.ncu-rep [algorithmic_flops] [algorithmic_bytes]
+"""
+import csv
+import io
+import subprocess
+import sys
+from collections import defaultdict
+
+KEYS = [
+    "gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
+    "TPC.TriageCompute.sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed",
+    "sm__throughput.avg.pct_of_peak_sustained_elapsed", "dram__throughput.avg.pct_of_peak_sustained_elapsed",
+    "lts__t_sector_hit_rate.pct", "lts__throughput.avg.pct_of_peak_sustained_elapsed",
+    "launch__registers_per_thread", "launch__grid_size", "launch__block_size",
+    "sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active",
+    "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active",
+    "SM_A.TriageCompute.sm__inst_executed_pipe_xu_realtime.avg.pct_of_peak_sustained_elapsed",
+    "sm__warps_active.avg.pct_of_peak_sustained_active",
+]
+
+
+def launches(path):
+    rows = list(csv.reader(open(path)))
+    hdr_i = next(i for i, r in enumerate(rows) if "Kernel Name" in r)
+    hdr = rows[hdr_i]
+    ik, iv, iu = hdr.index("Kernel Name"), hdr.index("Metric Value"), hdr.index("Metric Unit")
+    tot = defaultdict(float)
+    cnt = defaultdict(int)
+    for r in rows[hdr_i + 1:]:
+        if len(r) <= iv:
+            continue
+        try:
+            v = float(r[iv].replace(",", ""))
+        except ValueError:
+            continue
+        scale = {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3}.get(r[iu], 1.0)
+        name = r[ik].split("(")[0].replace("void ", "").strip()
+        tot[name] += v * scale
+        cnt[name] += 1
+    s = sum(tot.values())
+    print(f"{'kernel':70s} {'launches':>8s} {'us':>10s} {'share':>7s}")
+    for k, v in sorted(tot.items(), key=lambda kv: -kv[1]):
+        print(f"{k[:70]:70s} {cnt[k]:8d} {v:10.1f} {100 * v / s:6.1f}%")
+    print(f"{'total':70s} {sum(cnt.values()):8d} {s:10.1f}")
+
+
+def report(path, flops=None, nbytes=None):
+    out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(io.StringIO(out)))
+    hdr, units, vals = rows[0], rows[1], rows[2]
+    d = {h: (vals[i], units[i]) for i, h in enumerate(hdr)}
+    print("kernel:", d.get("Kernel Name", ("?",))[0][:160])
+    for k in KEYS:
+        if k in d:
+            print(f"  {k} = {d[k][0]} {d[k][1]}")
+    t = float(d["gpu__time_duration.sum"][0]) * {"ms": 1e-3, "us": 1e-6, "ns": 1e-9}.get(d["gpu__time_duration.sum"][1], 1)
+    if flops:
+        print(f"  algorithmic {float(flops) / 1e9:.1f} GFLOP -> {float(flops) / t / 1e12:.1f} TFLOP/s (cold, serialised)")
+    if nbytes:
+        print(f"  algorithmic {float(nbytes) / 1e6:.1f} MB -> {float(nbytes) / t / 1e9:.1f} GB/s")
+    rb = float(d.get("dram__bytes_read.sum", ("0",))[0] or 0)
+    print(f"  dram traffic (read+write): {d.get('dram__bytes_read.sum')} + {d.get('dram__bytes_write.sum')}")
+
+
+if __name__ == "__main__":
+    if sys.argv[1] == "launches":
+        launches(sys.argv[2])
+    else:
+        report(sys.argv[2], *(sys.argv[3:5]))
