@@ -37,7 +37,7 @@ def launches(path):
             v = float(r[iv].replace(",", ""))
         except ValueError:
             continue
-        scale = {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3}.get(r[iu], 1.0)
+        scale = {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3}.get(r[iu], 1.0)
         name = r[ik].split("(")[0].replace("void ", "").strip()
         tot[name] += v * scale
         cnt[name] += 1
