@@ -474,8 +474,17 @@ mhl_status moe_backward_local(mhl_plan p, const RankPtrs& R, const void* dY, voi
   float* W_rT = (float*)(R.ws + B.W_rT);
   {
     MHL_SPAN("B3_router_bwd");
-    mhl::launch_router_bwd(m.dtype, Xs, m.HD, idx, gate, dg, m.H, m.T_g, m.k, m.d_h, m.N_e, dS,
-                           (float*)(R.ws + B.dwr_part), R.dW_r, s);
+    if (!m.simt && m.T_g > 0 && mhl::router_bwd_sm100_supported(m.d_h, m.N_e, m.k)) {
+      if (!mhl::launch_router_bwd_sm100(Xs, m.HD, idx, gate, dg, m.H, m.T_g, m.k, m.d_h, m.N_e, dS,
+                                        (float*)(R.ws + B.dwr_part),
+                                        // token chunks per head from the GLOBAL head count, so the
+                                        // partial-sum order (and dW_r bits) do not depend on G
+                                        std::min(m.n_rt, std::max(1, p->num_sms / m.N_h)), R.dW_r, s))
+        return fail(MHL_ERR_CUDA, "router backward: TMA tensor-map encoding failed");
+    } else {
+      mhl::launch_router_bwd(m.dtype, Xs, m.HD, idx, gate, dg, m.H, m.T_g, m.k, m.d_h, m.N_e, dS,
+                             (float*)(R.ws + B.dwr_part), R.dW_r, s);
+    }
     mhl::launch_transpose_wr(R.W_r, W_rT, m.H, m.d_h, m.N_e, s);
   }
   {

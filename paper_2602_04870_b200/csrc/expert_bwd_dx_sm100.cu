@@ -223,13 +223,11 @@ expert_bwd_dx_kernel(const __grid_constant__ CUtensorMap w1map, const __grid_con
         tmem_ld32(tmem + L::T_DX + lane_off + half * (DH / 2) + c0, v);
         tmem_ld_wait();
 #pragma unroll
-        for (int u = 0; u < 32; u += 8) {
-          uint4 pk;
-          pk.x = pack_bf16x2(__uint_as_float(v[u + 0]), __uint_as_float(v[u + 1]));
-          pk.y = pack_bf16x2(__uint_as_float(v[u + 2]), __uint_as_float(v[u + 3]));
-          pk.z = pack_bf16x2(__uint_as_float(v[u + 4]), __uint_as_float(v[u + 5]));
-          pk.w = pack_bf16x2(__uint_as_float(v[u + 6]), __uint_as_float(v[u + 7]));
-          *reinterpret_cast<uint4*>(dst + c0 + u) = pk;
+        for (int u = 0; u < 32; u += 16) {
+          uint32_t p[8];
+#pragma unroll
+          for (int w = 0; w < 8; ++w) p[w] = pack_bf16x2(__uint_as_float(v[u + 2 * w]), __uint_as_float(v[u + 2 * w + 1]));
+          st_global_v8(dst + c0 + u, p[0], p[1], p[2], p[3], p[4], p[5], p[6], p[7]);
         }
       }
       tc_fence_before();
@@ -288,9 +286,11 @@ expert_bwd_dx_kernel(const __grid_constant__ CUtensorMap w1map, const __grid_con
       if (tid == kEpiWarp0 * 32) trace_ev(g_trace_dx, 55, i);
       // dH, gA rows to HBM for the weight-gradient kernel; the gate cotangent per replica
 #pragma unroll
-      for (int u = 0; u < NC / 2; u += 4) {
-        *reinterpret_cast<uint4*>(dHg + grow * DE + half * NC + 2 * u) = make_uint4(dhp[u], dhp[u + 1], dhp[u + 2], dhp[u + 3]);
-        *reinterpret_cast<uint4*>(gAg + grow * DE + half * NC + 2 * u) = make_uint4(gap[u], gap[u + 1], gap[u + 2], gap[u + 3]);
+      for (int u = 0; u < NC / 2; u += 8) {
+        st_global_v8(dHg + grow * DE + half * NC + 2 * u, dhp[u], dhp[u + 1], dhp[u + 2], dhp[u + 3], dhp[u + 4],
+                     dhp[u + 5], dhp[u + 6], dhp[u + 7]);
+        st_global_v8(gAg + grow * DE + half * NC + 2 * u, gap[u], gap[u + 1], gap[u + 2], gap[u + 3], gap[u + 4],
+                     gap[u + 5], gap[u + 6], gap[u + 7]);
       }
       s_dg[half * BM + row] = dgp;
       named_bar_sync(2 + q, 64);

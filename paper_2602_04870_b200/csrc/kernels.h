@@ -87,6 +87,14 @@ void launch_router_bwd(int dtype, const void* Xs, int64_t ldx, const int32_t* id
                        const float* dg, int H, int64_t T, int k, int d_h, int N_e, float* dS,
                        float* dwr_partial, float* dW_r, cudaStream_t s);
 
+// ---- B3 on tcgen05 (bf16): same dS; dW_r = X_h^T dS_dense with dS split into two bf16 planes,
+// one fp32 partial per CTA (min(nc_target, ceil(T/64)) token chunks per head; partial holds
+// H * nc_target * d_h * N_e floats), then an ordered sum.
+bool router_bwd_sm100_supported(int d_h, int N_e, int k);
+bool launch_router_bwd_sm100(const void* Xs, int64_t ldx, const int32_t* idx, const float* gate, const float* dg,
+                             int H, int64_t T, int k, int d_h, int N_e, float* dS, float* partial, int nc_target,
+                             float* dW_r, cudaStream_t s);
+
 // ---- W_rT[h][e][i] = W_r[h][i][e]
 void launch_transpose_wr(const float* W_r, float* W_rT, int H, int d_h, int N_e, cudaStream_t s);
 

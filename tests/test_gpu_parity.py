@@ -96,6 +96,21 @@ def test_expert_tcgen05_matches_oracle_and_simt(d_h, d_e):
     assert rel_err(g["out"], s["out"]) < 1e-2
 
 
+@pytest.mark.parametrize("d_h,N_e,k", [(256, 64, 8), (128, 32, 4), (128, 128, 8), (256, 256, 16)])
+def test_router_bwd_tcgen05_matches_oracle_and_simt(d_h, N_e, k):
+    """B3 on the tensor cores (dW_r = X^T dS_dense, dS as hi+lo bf16 planes, P:846-P:866) vs the
+    oracle at the bf16 tolerance, and vs the fp32-FMA SIMT kernel within the hi/lo split's
+    2^-17 relative bound (ragged T: the last 64-token step is partial)."""
+    _need_gpu()
+    cfg = LayerConfig("rb", T=1000, d=2 * d_h, N_h=2, d_h=d_h, N_e=N_e, k=k, d_e=64, dtype="bf16")
+    W, x, dout = make_problem(cfg, 11, "conf")
+    g = _run_gpu(cfg, W, x, dout)
+    _compare(cfg, W, x, dout, g)
+    s = _run_gpu(cfg, W, x, dout, simt=True)
+    if np.array_equal(g["idx"], s["idx"]):
+        assert rel_err(g["dW_r"], s["dW_r"]) < 1e-4
+
+
 def test_router_strict_on_exact_subtokens():
     """W_in = 2^-1 x permutation (d = D): Xs is exact on both sides, so only the fp32
     (GPU) vs fp64 (oracle) score arithmetic differs (~1e-6).  Indices and slot order
@@ -141,12 +156,14 @@ def test_all_tokens_to_one_expert():
     _compare(cfg, W, x, dout, g)
 
 
-@pytest.mark.parametrize("G", [2, 4])
-def test_loopback_hp_bitwise_equals_single_rank(G):
+@pytest.mark.parametrize("G,d_h,N_e", [(2, 32, 16), (4, 32, 16), (2, 128, 64)])
+def test_loopback_hp_bitwise_equals_single_rank(G, d_h, N_e):
     """HP on G virtual ranks (NCCL replaced by device copies) gives bit-identical
-    out, dx, routing and per-head weight gradients to G = 1 (HP only moves data)."""
+    out, dx, routing and per-head weight gradients to G = 1 (P:801: HP only moves data);
+    d_h = 128 runs the tcgen05 router/expert kernels."""
     _need_gpu()
-    cfg = LayerConfig("hp", T=1024, d=128, N_h=4, d_h=32, N_e=16, k=4, d_e=32, dtype="bf16")
+    cfg = LayerConfig("hp", T=1024, d=4 * d_h, N_h=4, d_h=d_h, N_e=N_e, k=4, d_e=32 if d_h == 32 else 64,
+                      dtype="bf16")
     W, x, dout = make_problem(cfg, 5, "conf")
     g1 = _run_gpu(cfg, W, x, dout, G=1)
     gG = _run_gpu(cfg, W, x, dout, G=G)
