@@ -463,6 +463,11 @@ mhl_status moe_backward_local(mhl_plan p, const RankPtrs& R, const void* dY, voi
     else
       mhl::launch_expert_bwd_simt(m.dtype, rt, Xs, m.HD, dY, m.HD, R.W1, R.W2, m.d_h, m.d_e, dXrep, dg, dH, gA, s);
   }
+  if (tc) {
+    MHL_SPAN("B5_expert_dx_gemm");
+    if (!mhl::launch_expert_dx_gemm_sm100(rt, R.W1, m.d_h, m.d_e, dH, dXrep, p->num_sms, s))
+      return fail(MHL_ERR_CUDA, "expert dX GEMM: TMA tensor-map encoding failed");
+  }
   if (R.dW1 || R.dW2) {
     MHL_SPAN("B5_expert_bwd_dw");
     if (tc)
@@ -491,7 +496,8 @@ mhl_status moe_backward_local(mhl_plan p, const RankPtrs& R, const void* dY, voi
     MHL_SPAN("B6_combine_bwd");
     mhl::launch_combine_bwd(m.dtype, rt, dXrep, dS, W_rT, m.d_h, dxout, m.HD, s);
   }
-  p->launches += 6;
+  // K1 + K2 + dW + dW reduce + router (2) + transpose + combine on the tensor-core path
+  p->launches += tc ? 8 : (R.dW1 || R.dW2 ? 6 : 5);
   return check_kernels(p);
 }
 

@@ -1,17 +1,28 @@
 // expert_bwd_dx_sm100.cu — B5 (input side): block-sparse expert FFN backward on tcgen05/TMEM.
 //
 // Chain rule of y_r = g_r * gelu(x W1_e^T) W2_e for the clustered rows of one expert (P:936,
-// Eq. 1), H recomputed (the forward never stored it):
-//   G_H   H   = X  W1_e^T       A = gathered sub-tokens, B = W1_e (K-major)        TMEM [0,128)
-//   G_dA  dA' = dY W2_e^T       A = gathered dcat rows,  B = W2_e (K-major)        TMEM [128,256)
-//   epi   dg = <gelu(H), dA'>  (= <dY, E_e(x)>, the gate cotangent)
-//         dH = g dA' gelu'(H),  gA = g gelu(H)    (bf16; dH -> smem as the next A operand,
-//                                                   dH and gA -> HBM for the weight gradients)
-//   G_dX  dXrep = dH W1_e       A = dH (smem), B = W1_e viewed MN-major          TMEM [256,512)
-// Warp roles as in the forward kernel: warps 0-3 gather X then dY chunks through an smem ring
-// (W1/W2 by TMA when the expert changes), warp 4 issues the MMAs in the order
-// G_H(i), G_dA(i), G_dX(i-1) (G_dX(i-1) first when tile i starts a new expert), warps 5-12 run the
-// epilogue of tile i while the tensor pipe works on its neighbours.
+// Eq. 1), H recomputed (the forward never stored it).  Two persistent kernels over the 128-row
+// expert tiles of F4:
+//
+// kernel 1 (expert_bwd_h):
+//   G_H   H   = X  W1_e^T       A = gathered sub-tokens, B = W1_e (K-major)     TMEM [256b, 256b+128)
+//   G_dA  dA' = dY W2_e^T       A = gathered dcat rows,  B = W2_e (K-major)     TMEM [256b+128, 256b+256)
+//   epi   dg = <gelu(H), dA'>  (= <dY, E_e(x)>, the gate cotangent, per replica)
+//         dH = g dA' gelu'(H),  gA = g gelu(H)   (bf16 rows -> HBM, consumed by kernel 2 and the
+//                                                 weight-gradient kernel)
+//   The H/dA' accumulators are double-buffered (b = tile parity), so the MMAs and sub-token
+//   gathers of tile i+1 run while the epilogue of tile i computes: the kernel streams.
+//   Warps 0-3 gather X then dY chunks through an smem ring (W1/W2 by TMA on expert change),
+//   warp 4 issues the MMAs, warps 5-12 run the epilogue.
+//
+// kernel 2 (expert_dx_gemm):
+//   G_dX  dXrep = dH W1_e       A = dH tile (TMA, contiguous sorted rows), B = W1_e read MN-major
+//   TMEM double buffer [0,DH) / [DH,2DH); epilogue TMEM -> bf16 -> smem -> TMA bulk store.
+//   Warp 0 = TMA producer, warp 1 = MMA issuer, warps 2-9 = epilogue.
+//
+// Splitting G_dX off costs one extra read of dH (R*d_e*2 bytes) but lets both kernels keep every
+// accumulator double-buffered in the 512 TMEM columns (the fused form needed H, dA' and dX
+// resident at once: 128+128+256 columns, which serialised the gathers behind the epilogue).
 #include <cuda.h>
 
 #include <cstdlib>
@@ -29,47 +40,83 @@ using namespace sm100;
 __device__ TraceBuf g_trace_dx;     // profiling aid (MHL_TRACE_DX=<file>), off by default
 
 constexpr int BM = kExpertBM;
-constexpr int kProdWarps = 4, kMmaWarp = 4, kEpiWarp0 = 5;
-constexpr int kThreads = 13 * 32;
-constexpr int kEpiThreads = 256;
-constexpr int kChunk = BM * 128;     // one 64-column K-chunk of a gathered 128-row tile (16 KB)
-
-template <int DH, int DE>
-struct DxL {
-  static constexpr int WB = DE * DH * 2;
-  static constexpr int W1 = 0, W2 = WB, DHS = 2 * WB, RING = DHS + BM * DE * 2;
-  static constexpr int S_RAW = (225 * 1024 - RING) / kChunk;
-  static constexpr int S = S_RAW > 12 ? 12 : S_RAW;
-  static constexpr int CTRL = RING + S * kChunk;
-  static constexpr int B_FULL = CTRL, B_EMPTY = B_FULL + 8 * S;
-  static constexpr int B_W1F = B_EMPTY + 8 * S, B_W1E = B_W1F + 8, B_W2F = B_W1E + 8, B_W2E = B_W2F + 8;
-  static constexpr int B_HDFULL = B_W2E + 8, B_HDFREE = B_HDFULL + 8, B_DHFULL = B_HDFREE + 8;
-  static constexpr int B_G3DONE = B_DHFULL + 8, B_DXFREE = B_G3DONE + 8;
-  static constexpr int TOK = B_DXFREE + 8;                  // [BM] int (producers)
-  static constexpr int DG = TOK + BM * 4;                   // [2][BM] float (epilogue pairs)
-  static constexpr int TMEMP = DG + 2 * BM * 4;
-  static constexpr int BYTES = TMEMP + 16;
-  static constexpr uint32_t T_H = 0, T_DA = 128, T_DX = 256;
-};
+constexpr int kChunk = BM * 128;     // one 64-column K-chunk of a 128-row tile (16 KB)
+constexpr int kMaxSmem = 227 * 1024;
 
 struct Ph {
   uint32_t v = 0;
   __device__ uint32_t flip() { uint32_t o = v; v ^= 1u; return o; }
 };
 
+__device__ __forceinline__ void tma_store_2d(const void* tmap, uint32_t src, int c0, int c1) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(tmap), "r"(src),
+               "r"(c0), "r"(c1)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() { asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory"); }
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+
+// Persistent schedule shared by both kernels: CTA b takes groups of kTileGroup consecutive tiles
+// round-robin (weights reused within a group, the tiles in flight stay inside one head).
+struct Sched {
+  const Tile* tiles; int nt, my_groups;
+  __device__ Sched(const Tile* t, int n) : tiles(t), nt(n) {
+    const int ngroups = (nt + kTileGroup - 1) / kTileGroup;
+    my_groups = ngroups > (int)blockIdx.x ? (ngroups - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
+  }
+  __device__ int at(int i) const {
+    if (i < 0 || i >= my_groups * kTileGroup) return -1;
+    const int ti = ((int)blockIdx.x + (i / kTileGroup) * (int)gridDim.x) * kTileGroup + i % kTileGroup;
+    return ti < nt ? ti : -1;
+  }
+  __device__ bool same_expert(int ta, int tb) const {
+    if (ta < 0 || tb < 0) return false;
+    const Tile a = tiles[ta], b = tiles[tb];
+    return a.head == b.head && a.expert == b.expert;
+  }
+};
+
+// =============================================================================================
+// kernel 1: H, dA' -> dH, gA, dg
+// =============================================================================================
+constexpr int kProdWarps = 6, kMmaWarp = kProdWarps, kEpiWarp0 = kProdWarps + 1, kEpiWarps = 16;
+constexpr int kThreads1 = (kEpiWarp0 + kEpiWarps) * 32;
+constexpr int kEpiThreads = kEpiWarps * 32;
+
 template <int DH, int DE>
-__global__ void __launch_bounds__(kThreads, 1)
-expert_bwd_dx_kernel(const __grid_constant__ CUtensorMap w1map, const __grid_constant__ CUtensorMap w2map, Routing rt,
-                     const bf16* __restrict__ Xg, int64_t ldx, const bf16* __restrict__ dYg, int64_t ldy,
-                     bf16* __restrict__ dXrep, float* __restrict__ dg, bf16* __restrict__ dHg,
-                     bf16* __restrict__ gAg) {
-  using L = DxL<DH, DE>;
+struct HL {
+  static constexpr int WB = DE * DH * 2;
+  static constexpr int W1 = 0, W2 = WB, RING = 2 * WB;
+  static constexpr int CTRL_MAX = 3 * 1024;
+  static constexpr int S_RAW = (kMaxSmem - RING - CTRL_MAX) / kChunk;
+  // a multiple of kProdWarps: chunk c -> stage c % S, warp c % kProdWarps, so every stage is only
+  // ever refilled by the warp that filled it before (its phase parity can never alias)
+  static constexpr int S = (S_RAW > 12 ? 12 : S_RAW) / kProdWarps * kProdWarps;
+  static constexpr int CTRL = RING + S * kChunk;
+  static constexpr int B_FULL = CTRL, B_EMPTY = B_FULL + 8 * S;
+  static constexpr int B_W1F = B_EMPTY + 8 * S, B_W1E = B_W1F + 8, B_W2F = B_W1E + 8, B_W2E = B_W2F + 8;
+  static constexpr int B_HDFULL = B_W2E + 8, B_HDFREE = B_HDFULL + 16;
+  static constexpr int DG = B_HDFREE + 16;                  // [kEpiWarps/4][BM] float (dg partials)
+  static constexpr int TMEMP = DG + (kEpiWarps / 4) * BM * 4;
+  static constexpr int BYTES = TMEMP + 16;
+  static_assert(BYTES - CTRL <= CTRL_MAX, "control block overflow");
+  static_assert(S >= kProdWarps, "ring too small");
+};
+
+template <int DH, int DE>
+__global__ void __launch_bounds__(kThreads1, 1)
+expert_bwd_h_kernel(const __grid_constant__ CUtensorMap w1map, const __grid_constant__ CUtensorMap w2map,
+                    const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap ymap, Routing rt,
+                    float* __restrict__ dg, bf16* __restrict__ dHg, bf16* __restrict__ gAg, int dbg) {
+  using L = HL<DH, DE>;
+  TraceBuf trc = g_trace_dx;   // one load; trace_ev then costs a register test
   constexpr int S = L::S, KB = DH / 64;
   extern __shared__ __align__(1024) uint8_t smem[];
   if ((smem_u32(smem) & 1023u) != 0u) __trap();
   const uint32_t sb = smem_u32(smem);
   auto bar = [&](int off) { return reinterpret_cast<uint64_t*>(smem + off); };
-  int* s_tok = reinterpret_cast<int*>(smem + L::TOK);
   float* s_dg = reinterpret_cast<float*>(smem + L::DG);
   uint32_t* s_tmem = reinterpret_cast<uint32_t*>(smem + L::TMEMP);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -78,35 +125,19 @@ expert_bwd_dx_kernel(const __grid_constant__ CUtensorMap w1map, const __grid_con
   const int64_t Rp = rt.Rp, R = rt.T * rt.k;
 
   if (tid == 0) {
-    for (int i = 0; i < S; ++i) { mbar_init(bar(L::B_FULL + 8 * i), 32 * kProdWarps); mbar_init(bar(L::B_EMPTY + 8 * i), 1); }
+    for (int i = 0; i < S; ++i) { mbar_init(bar(L::B_FULL + 8 * i), 1); mbar_init(bar(L::B_EMPTY + 8 * i), 1); }
     mbar_init(bar(L::B_W1F), 1); mbar_init(bar(L::B_W1E), 1); mbar_init(bar(L::B_W2F), 1); mbar_init(bar(L::B_W2E), 1);
-    mbar_init(bar(L::B_HDFULL), 1);
-    mbar_init(bar(L::B_HDFREE), kEpiThreads);
-    mbar_init(bar(L::B_DHFULL), kEpiThreads);
-    mbar_init(bar(L::B_G3DONE), 1);
-    mbar_init(bar(L::B_DXFREE), kEpiThreads);
+    for (int b = 0; b < 2; ++b) { mbar_init(bar(L::B_HDFULL + 8 * b), 1); mbar_init(bar(L::B_HDFREE + 8 * b), kEpiThreads); }
     fence_mbar_init();
-    tma_prefetch_desc(&w1map); tma_prefetch_desc(&w2map);
+    tma_prefetch_desc(&w1map); tma_prefetch_desc(&w2map); tma_prefetch_desc(&xmap); tma_prefetch_desc(&ymap);
   }
   if (warp == kMmaWarp) tmem_alloc<512>(s_tmem);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *s_tmem;
+  const Sched sc(tiles, *rt.ntiles);
 
-  const int nt = *rt.ntiles;
-  const int ngroups = (nt + kTileGroup - 1) / kTileGroup;
-  const int my_groups = ngroups > (int)blockIdx.x ? (ngroups - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
-  auto tile_at = [&](int i) -> int {
-    if (i < 0 || i >= my_groups * kTileGroup) return -1;
-    const int ti = ((int)blockIdx.x + (i / kTileGroup) * (int)gridDim.x) * kTileGroup + i % kTileGroup;
-    return ti < nt ? ti : -1;
-  };
-  auto same_expert = [&](int ta, int tb2) {
-    if (ta < 0 || tb2 < 0) return false;
-    const Tile a = tiles[ta], b = tiles[tb2];
-    return a.head == b.head && a.expert == b.expert;
-  };
   auto load_w = [&](const CUtensorMap* map, int off, uint64_t* full, const Tile& t) {
     mbar_expect_tx(full, L::WB);
     for (int kb = 0; kb < KB; ++kb) tma_load_2d(sb + off + kb * DE * 128, map, kb * 64, (t.head * N_e + t.expert) * DE, full);
@@ -114,33 +145,22 @@ expert_bwd_dx_kernel(const __grid_constant__ CUtensorMap w1map, const __grid_con
 
   if (warp < kProdWarps) {
     // ================================================================ producers
+    // A tile is 2*KB chunks (X k-chunks, then dY k-chunks); chunk c of the CTA's stream goes to
+    // ring stage c % S and is brought by warp c % kProdWarps, each of its 32 lanes issuing one TMA
+    // gather4 (4 rows x 64 columns; lane l owns tile rows 4l..4l+3).  The SW128 swizzle is applied
+    // by smem address, so row r lands where the K-major MMA descriptor expects it (kmaj_off).
+    // Several warps with whole-chunk gathers in flight keep the TMA unit busy (tools/ring_probe.cu).
     const int pw = warp;
-    Ph ee[12], w1e, w2e;
-    int st = 0;
-    auto gather = [&](const bf16* base, int64_t ld, const Tile& tl) {
-      for (int kb = 0; kb < KB; ++kb) {
-        mbar_wait_warp(bar(L::B_EMPTY + 8 * st), ee[st].flip() ^ 1);
-        const uint32_t dst = sb + L::RING + st * kChunk;
-        const bf16* src = base + (size_t)tl.head * DH + kb * 64;
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          const int idx = j * 32 + lane, r = pw * 32 + (idx >> 3), c = (idx & 7) * 8;
-          cp_async_16(dst + kmaj_off(r, c, BM), src + (size_t)s_tok[r] * ld + c, 16);
-        }
-        cp_async_mbar_arrive(bar(L::B_FULL + 8 * st));
-        if (++st == S) st = 0;
-      }
-    };
+    Ph w1e, w2e;
+    int cnt = 0;                       // chunks of this CTA's stream so far
     for (int i = 0;; ++i) {
-      const int ti = tile_at(i);
+      const int ti = sc.at(i);
       if (ti < 0) break;
       const Tile tl = tiles[ti];
-      const bool fresh = !same_expert(tile_at(i - 1), ti);
-      __syncwarp();
-      s_tok[pw * 32 + lane] = rt.tok_s[(size_t)tl.head * Rp + tl.row0 + pw * 32 + lane];
-      __syncwarp();
-      gather(Xg, ldx, tl);
-      if (pw == 0 && lane == 0) trace_ev(g_trace_dx, 30, i);
+      const bool fresh = !sc.same_expert(sc.at(i - 1), ti);
+      if (pw == 0 && lane == 0) trace_ev(trc, 34, i);
+      const int32_t* tk = rt.tok_s + (size_t)tl.head * Rp + tl.row0 + 4 * lane;
+      const int r0 = tk[0], r1 = tk[1], r2 = tk[2], r3 = tk[3];
       if (pw == 0 && lane == 0 && fresh) {
         mbar_wait(bar(L::B_W1E), w1e.flip() ^ 1);
         load_w(&w1map, L::W1, bar(L::B_W1F), tl);
@@ -148,20 +168,30 @@ expert_bwd_dx_kernel(const __grid_constant__ CUtensorMap w1map, const __grid_con
         load_w(&w2map, L::W2, bar(L::B_W2F), tl);
       }
       __syncwarp();
-      gather(dYg, ldy, tl);
-      if (pw == 0 && lane == 0) trace_ev(g_trace_dx, 31, i);
+      for (int j = 0; j < 2 * KB; ++j, ++cnt) {
+        if (cnt % kProdWarps != pw) continue;
+        const int st = cnt % S;
+        uint64_t* full = bar(L::B_FULL + 8 * st);
+        if (lane == 0) {
+          mbar_wait(bar(L::B_EMPTY + 8 * st), ((cnt / S) & 1) ^ 1);
+          mbar_expect_tx(full, kChunk);
+        }
+        __syncwarp();
+        const int kb = j % KB;
+        tma_gather4(sb + L::RING + st * kChunk + lane * 4 * 128, j < KB ? &xmap : &ymap, tl.head * DH + kb * 64, r0,
+                    r1, r2, r3, full);
+      }
     }
   } else if (warp == kMmaWarp) {
     // ================================================================ MMA issuer
     if (lane == 0) {
       constexpr uint32_t ID_N_DE = idesc_bf16(BM, DE, 0, 0);
-      constexpr uint32_t ID_N_DH = idesc_bf16(BM, DH, 0, 1);
-      Ph ff[12], w1f, w2f, hdfr, dhf, dxfr, g3;
-      int st = 0;
-      auto gemm_k = [&](uint32_t d, int woff) {   // d += (ring chunks) . W^T over K = DH
-        for (int kb = 0; kb < KB; ++kb) {
+      Ph ff[12], w1f, w2f, hdfr[2];
+      int st = 0, nch = 0;
+      auto gemm_k = [&](uint32_t d, int woff) {   // d = (ring chunks) . W^T over K = DH
+        for (int kb = 0; kb < KB; ++kb, ++nch) {
           mbar_wait(bar(L::B_FULL + 8 * st), ff[st].flip());
-          fence_proxy_async();
+          if (dbg & 1) { mbar_arrive(bar(L::B_EMPTY + 8 * st)); if (++st == S) st = 0; continue; }
           tc_fence_after();
 #pragma unroll
           for (int ks = 0; ks < 4; ++ks)
@@ -171,159 +201,291 @@ expert_bwd_dx_kernel(const __grid_constant__ CUtensorMap w1map, const __grid_con
           if (++st == S) st = 0;
         }
       };
-      int ndx = 0;   // G_dX issued so far
-      auto gemm_dx = [&](int j) {
-        mbar_wait(bar(L::B_DHFULL), dhf.flip());          // dH(j) in smem
-        if (ndx >= 1) mbar_wait(bar(L::B_DXFREE), dxfr.flip());   // dX(j-1) drained
-        tc_fence_after();
-#pragma unroll
-        for (int ks = 0; ks < DE / 16; ++ks)
-          mma_bf16(tmem + L::T_DX, sdesc_sw128(sb + L::DHS + (ks >> 2) * BM * 128 + (ks & 3) * 32, 16, 1024),
-                   sdesc_sw128(sb + L::W1 + ks * 2 * 1024, DE * 128, 1024), ID_N_DH, ks > 0);
-        mma_commit(bar(L::B_G3DONE));
-        trace_ev(g_trace_dx, 43, j);
-        if (!same_expert(tile_at(j), tile_at(j + 1))) mma_commit(bar(L::B_W1E));
-        ++ndx;
-      };
-      int pending = -1;
       for (int i = 0;; ++i) {
-        const int ti = tile_at(i);
+        const int ti = sc.at(i);
         if (ti < 0) break;
-        const bool fresh = !same_expert(tile_at(i - 1), ti);
-        if (fresh && pending >= 0) { gemm_dx(pending); pending = -1; }
+        const int b = i & 1;
+        const bool fresh = !sc.same_expert(sc.at(i - 1), ti);
+        const bool last = !sc.same_expert(ti, sc.at(i + 1));
         if (fresh) mbar_wait(bar(L::B_W1F), w1f.flip());
-        if (i >= 1) mbar_wait(bar(L::B_HDFREE), hdfr.flip());   // epilogue has read H, dA' of tile i-1
+        if (i >= 2) mbar_wait(bar(L::B_HDFREE + 8 * b), hdfr[b].flip());   // epilogue read tile i-2
         tc_fence_after();
-        trace_ev(g_trace_dx, 40, i);
-        gemm_k(tmem + L::T_H, L::W1);
+        trace_ev(trc, 40, i);
+        gemm_k(tmem + 256 * b, L::W1);
+        if (last && !(dbg & 1)) mma_commit(bar(L::B_W1E));
         if (fresh) mbar_wait(bar(L::B_W2F), w2f.flip());
-        gemm_k(tmem + L::T_DA, L::W2);
-        mma_commit(bar(L::B_HDFULL));
-        trace_ev(g_trace_dx, 41, i);
-        if (!same_expert(ti, tile_at(i + 1))) mma_commit(bar(L::B_W2E));
-        if (pending >= 0) gemm_dx(pending);
-        pending = i;
+        gemm_k(tmem + 256 * b + 128, L::W2);
+        if (dbg & 1) {
+          mbar_arrive(bar(L::B_HDFULL + 8 * b));
+          if (last) { mbar_arrive(bar(L::B_W1E)); mbar_arrive(bar(L::B_W2E)); }
+        } else {
+          mma_commit(bar(L::B_HDFULL + 8 * b));
+          if (last) mma_commit(bar(L::B_W2E));
+        }
+        trace_ev(trc, 41, i);
       }
-      if (pending >= 0) gemm_dx(pending);
-      (void)g3;
     }
   } else {
-    // ================================================================ epilogue (8 warps)
-    const int q = warp & 3, half = (warp - kEpiWarp0) >> 2;
+    // ================================================================ epilogue (kEpiWarps warps)
+    // warp -> (lane quadrant q, column group cg); each thread owns one row and NC columns of H/dA',
+    // streamed through registers 16 columns at a time (TMEM -> gelu/gelu' -> bf16 -> HBM).
+    constexpr int NG = kEpiWarps / 4, NC = DE / NG;
+    const int q = warp & 3, cg = (warp - kEpiWarp0) >> 2;
     const int row = q * 32 + lane;
     const uint32_t lane_off = (uint32_t)(q * 32) << 16;
-    constexpr int NC = DE / 2;         // H / dA' columns per thread
-    Ph hd, g3;
-    auto drain_dx = [&](int j) {       // dXrep rows of tile j (G_dX(j) complete)
-      const Tile tl = tiles[tile_at(j)];
-      bf16* dst = dXrep + ((size_t)tl.head * Rp + tl.row0 + row) * DH + half * (DH / 2);
-#pragma unroll 1
-      for (int c0 = 0; c0 < DH / 2; c0 += 32) {
-        uint32_t v[32];
-        tmem_ld32(tmem + L::T_DX + lane_off + half * (DH / 2) + c0, v);
-        tmem_ld_wait();
-#pragma unroll
-        for (int u = 0; u < 32; u += 16) {
-          uint32_t p[8];
-#pragma unroll
-          for (int w = 0; w < 8; ++w) p[w] = pack_bf16x2(__uint_as_float(v[u + 2 * w]), __uint_as_float(v[u + 2 * w + 1]));
-          st_global_v8(dst + c0 + u, p[0], p[1], p[2], p[3], p[4], p[5], p[6], p[7]);
-        }
-      }
-      tc_fence_before();
-      mbar_arrive(bar(L::B_DXFREE));
-    };
-    int i = 0;
-    for (;; ++i) {
-      const int ti = tile_at(i);
+    Ph hd[2];
+    for (int i = 0;; ++i) {
+      const int ti = sc.at(i);
       if (ti < 0) break;
+      const int b = i & 1;
       const Tile tl = tiles[ti];
       const size_t grow = (size_t)tl.head * Rp + tl.row0 + row;
       const float g = rt.gate_s[grow];
       const int rep = rt.perm[grow];
-      mbar_wait_warp(bar(L::B_HDFULL), hd.flip());
-      if (tid == kEpiWarp0 * 32) trace_ev(g_trace_dx, 50, i);
+      mbar_wait_warp(bar(L::B_HDFULL + 8 * b), hd[b].flip());
+      if (tid == kEpiWarp0 * 32) trace_ev(trc, 50, i);
       tc_fence_after();
-      uint32_t hv[NC], dv[NC];
-#pragma unroll
-      for (int c = 0; c < NC; c += 32) {
-        uint32_t v[32], w[32];
-        tmem_ld32(tmem + L::T_H + lane_off + half * NC + c, v);
-        tmem_ld32(tmem + L::T_DA + lane_off + half * NC + c, w);
-#pragma unroll
-        for (int u = 0; u < 32; ++u) { hv[c + u] = v[u]; dv[c + u] = w[u]; }
-      }
-      tmem_ld_wait();
-      tc_fence_before();
-      mbar_arrive(bar(L::B_HDFREE));
       float dgp = 0.f;
-      uint32_t dhp[NC / 2], gap[NC / 2];
 #pragma unroll
-      for (int u = 0; u < NC; u += 2) {
-        const float2 h2 = make_float2(__uint_as_float(hv[u]), __uint_as_float(hv[u + 1]));
-        const float2 d2 = make_float2(__uint_as_float(dv[u]), __uint_as_float(dv[u + 1]));
-        float2 gp;
-        const float2 a = gelu2(h2, &gp);
-        dgp = fmaf(a.x, d2.x, dgp);
-        dgp = fmaf(a.y, d2.y, dgp);
-        const float2 dh = __fmul2_rn(__fmul2_rn(d2, gp), make_float2(g, g));
-        const float2 ga = __fmul2_rn(a, make_float2(g, g));
-        dhp[u / 2] = pack_bf16x2(dh.x, dh.y);
-        gap[u / 2] = pack_bf16x2(ga.x, ga.y);
-      }
-      // dH(i) -> smem once G_dX(i-1) has finished reading the previous dH (it also left dX(i-1))
-      if (tid == kEpiWarp0 * 32) trace_ev(g_trace_dx, 52, i);
-      if (i >= 1) mbar_wait_warp(bar(L::B_G3DONE), g3.flip());
-      if (tid == kEpiWarp0 * 32) trace_ev(g_trace_dx, 53, i);
+      for (int c = 0; c < NC; c += 16) {
+        uint32_t hv[16], dv[16];
+        const uint32_t col = lane_off + cg * NC + c;
+        tmem_ld16(tmem + 256 * b + col, hv);
+        tmem_ld16(tmem + 256 * b + 128 + col, dv);
+        tmem_ld_wait();
+        if (c + 16 >= NC) {                       // all of this thread's TMEM reads are done
+          tc_fence_before();
+          mbar_arrive(bar(L::B_HDFREE + 8 * b));
+        }
+        if (dbg & 2) continue;
+        uint32_t dhp[8], gap[8];
 #pragma unroll
-      for (int u = 0; u < NC / 2; u += 4) {
-        uint4 pk = make_uint4(dhp[u], dhp[u + 1], dhp[u + 2], dhp[u + 3]);
-        *reinterpret_cast<uint4*>(smem + L::DHS + kmaj_off(row, half * NC + 2 * u, BM)) = pk;
+        for (int u = 0; u < 16; u += 2) {
+          const float2 h2 = make_float2(__uint_as_float(hv[u]), __uint_as_float(hv[u + 1]));
+          const float2 d2 = make_float2(__uint_as_float(dv[u]), __uint_as_float(dv[u + 1]));
+          float2 gp;
+          const float2 a = gelu2(h2, &gp);
+          dgp = fmaf(a.x, d2.x, dgp);
+          dgp = fmaf(a.y, d2.y, dgp);
+          const float2 dh = __fmul2_rn(__fmul2_rn(d2, gp), make_float2(g, g));
+          const float2 ga = __fmul2_rn(a, make_float2(g, g));
+          dhp[u / 2] = pack_bf16x2(dh.x, dh.y);
+          gap[u / 2] = pack_bf16x2(ga.x, ga.y);
+        }
+        st_global_v8(dHg + grow * DE + cg * NC + c, dhp[0], dhp[1], dhp[2], dhp[3], dhp[4], dhp[5], dhp[6], dhp[7]);
+        st_global_v8(gAg + grow * DE + cg * NC + c, gap[0], gap[1], gap[2], gap[3], gap[4], gap[5], gap[6], gap[7]);
       }
-      fence_proxy_async();
-      mbar_arrive(bar(L::B_DHFULL));
-      if (i >= 1) { tc_fence_after(); drain_dx(i - 1); }
-      if (tid == kEpiWarp0 * 32) trace_ev(g_trace_dx, 55, i);
-      // dH, gA rows to HBM for the weight-gradient kernel; the gate cotangent per replica
+      if (tid == kEpiWarp0 * 32) trace_ev(trc, 52, i);
+      // gate cotangent: the NG column-group partial sums of this row, added in group order
+      s_dg[cg * BM + row] = dgp;
+      named_bar_sync(2 + q, 32 * NG);
+      if (cg == 0 && rep >= 0) {
+        float acc = s_dg[row];
 #pragma unroll
-      for (int u = 0; u < NC / 2; u += 8) {
-        st_global_v8(dHg + grow * DE + half * NC + 2 * u, dhp[u], dhp[u + 1], dhp[u + 2], dhp[u + 3], dhp[u + 4],
-                     dhp[u + 5], dhp[u + 6], dhp[u + 7]);
-        st_global_v8(gAg + grow * DE + half * NC + 2 * u, gap[u], gap[u + 1], gap[u + 2], gap[u + 3], gap[u + 4],
-                     gap[u + 5], gap[u + 6], gap[u + 7]);
+        for (int u = 1; u < NG; ++u) acc += s_dg[u * BM + row];
+        dg[(size_t)tl.head * R + rep] = acc;
       }
-      s_dg[half * BM + row] = dgp;
-      named_bar_sync(2 + q, 64);
-      if (half == 0 && rep >= 0) dg[(size_t)tl.head * R + rep] = s_dg[row] + s_dg[BM + row];
-      named_bar_sync(2 + q, 64);
+      named_bar_sync(2 + q, 32 * NG);
+      if (tid == kEpiWarp0 * 32) trace_ev(trc, 55, i);
     }
-    if (i >= 1) { mbar_wait_warp(bar(L::B_G3DONE), g3.flip()); tc_fence_after(); drain_dx(i - 1); }
   }
   tc_fence_before();
   __syncthreads();
   if (warp == kMmaWarp) tmem_dealloc<512>(tmem);
 }
 
+// =============================================================================================
+// kernel 2: dXrep = dH W1_e
+// =============================================================================================
+constexpr int kThreads2 = 10 * 32;
+constexpr int kEpiThreads2 = 8 * 32;
+constexpr int kYStage = BM * 128;    // one 64-column block of the dX tile (16 KB)
+
+template <int DH, int DE>
+struct GL {
+  static constexpr int WB = DE * DH * 2;
+  static constexpr int ASTAGE = DE * BM * 2;                // one dH tile: DE/64 chunks of 16 KB
+  static constexpr int W1 = 0, YS = WB, A = YS + 2 * kYStage;
+  static constexpr int CTRL_MAX = 1024;
+  static constexpr int AS_RAW = (kMaxSmem - A - CTRL_MAX) / ASTAGE;
+  static constexpr int AS = AS_RAW > 4 ? 4 : AS_RAW;
+  static constexpr int CTRL = A + AS * ASTAGE;
+  static constexpr int B_AFULL = CTRL, B_AEMPTY = B_AFULL + 8 * AS;
+  static constexpr int B_W1F = B_AEMPTY + 8 * AS, B_W1E = B_W1F + 8;
+  static constexpr int B_DXFULL = B_W1E + 8, B_DXEMPTY = B_DXFULL + 16;
+  static constexpr int TMEMP = B_DXEMPTY + 16;
+  static constexpr int BYTES = TMEMP + 16;
+  static constexpr int TMEM_COLS = 2 * DH <= 256 ? 256 : 512;
+  static_assert(BYTES - CTRL <= CTRL_MAX, "control block overflow");
+  static_assert(AS >= 2, "dH ring too small");
+};
+
+template <int DH, int DE>
+__global__ void __launch_bounds__(kThreads2, 1)
+expert_dx_gemm_kernel(const __grid_constant__ CUtensorMap w1map, const __grid_constant__ CUtensorMap hmap,
+                      const __grid_constant__ CUtensorMap xmap, Routing rt) {
+  using L = GL<DH, DE>;
+  constexpr int AS = L::AS, KB = DH / 64;
+  extern __shared__ __align__(1024) uint8_t smem[];
+  if ((smem_u32(smem) & 1023u) != 0u) __trap();
+  const uint32_t sb = smem_u32(smem);
+  auto bar = [&](int off) { return reinterpret_cast<uint64_t*>(smem + off); };
+  uint32_t* s_tmem = reinterpret_cast<uint32_t*>(smem + L::TMEMP);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const Tile* tiles = rt.tiles;
+  const int N_e = rt.N_e;
+  const int64_t Rp = rt.Rp;
+
+  if (tid == 0) {
+    for (int i = 0; i < AS; ++i) { mbar_init(bar(L::B_AFULL + 8 * i), 1); mbar_init(bar(L::B_AEMPTY + 8 * i), 1); }
+    mbar_init(bar(L::B_W1F), 1); mbar_init(bar(L::B_W1E), 1);
+    for (int b = 0; b < 2; ++b) { mbar_init(bar(L::B_DXFULL + 8 * b), 1); mbar_init(bar(L::B_DXEMPTY + 8 * b), kEpiThreads2); }
+    fence_mbar_init();
+    tma_prefetch_desc(&w1map); tma_prefetch_desc(&hmap); tma_prefetch_desc(&xmap);
+  }
+  if (warp == 1) tmem_alloc<L::TMEM_COLS>(s_tmem);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *s_tmem;
+  const Sched sc(tiles, *rt.ntiles);
+
+  if (warp == 0) {
+    // ================================================================ TMA producer
+    if (lane == 0) {
+      Ph ae[4], w1e;
+      int st = 0;
+      for (int i = 0;; ++i) {
+        const int ti = sc.at(i);
+        if (ti < 0) break;
+        const Tile tl = tiles[ti];
+        mbar_wait(bar(L::B_AEMPTY + 8 * st), ae[st].flip() ^ 1);
+        mbar_expect_tx(bar(L::B_AFULL + 8 * st), L::ASTAGE);
+        for (int kb = 0; kb < DE / 64; ++kb)
+          tma_load_2d(sb + L::A + st * L::ASTAGE + kb * kChunk, &hmap, kb * 64, (int)((size_t)tl.head * Rp + tl.row0),
+                      bar(L::B_AFULL + 8 * st));
+        if (++st == AS) st = 0;
+        if (!sc.same_expert(sc.at(i - 1), ti)) {
+          mbar_wait(bar(L::B_W1E), w1e.flip() ^ 1);
+          mbar_expect_tx(bar(L::B_W1F), L::WB);
+          for (int kb = 0; kb < KB; ++kb)
+            tma_load_2d(sb + L::W1 + kb * DE * 128, &w1map, kb * 64, (tl.head * N_e + tl.expert) * DE, bar(L::B_W1F));
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ================================================================ MMA issuer
+    if (lane == 0) {
+      constexpr uint32_t ID = idesc_bf16(BM, DH, 0, 1);     // B = W1_e viewed MN-major (N = d_h)
+      Ph af[4], w1f, dxe[2];
+      int st = 0;
+      for (int i = 0;; ++i) {
+        const int ti = sc.at(i);
+        if (ti < 0) break;
+        const int b = i & 1;
+        if (!sc.same_expert(sc.at(i - 1), ti)) mbar_wait(bar(L::B_W1F), w1f.flip());
+        mbar_wait(bar(L::B_DXEMPTY + 8 * b), dxe[b].flip() ^ 1);
+        mbar_wait(bar(L::B_AFULL + 8 * st), af[st].flip());
+        tc_fence_after();
+        const uint32_t a0 = sb + L::A + st * L::ASTAGE;
+#pragma unroll
+        for (int ks = 0; ks < DE / 16; ++ks)
+          mma_bf16(tmem + b * DH, sdesc_sw128(a0 + (ks >> 2) * kChunk + (ks & 3) * 32, 16, 1024),
+                   sdesc_sw128(sb + L::W1 + ks * 2 * 1024, DE * 128, 1024), ID, ks > 0);
+        mma_commit(bar(L::B_AEMPTY + 8 * st));
+        mma_commit(bar(L::B_DXFULL + 8 * b));
+        if (!sc.same_expert(ti, sc.at(i + 1))) mma_commit(bar(L::B_W1E));
+        if (++st == AS) st = 0;
+      }
+    }
+  } else {
+    // ================================================================ epilogue (8 warps)
+    const int q = warp & 3, half = (warp - 2) >> 2;    // lane quadrant, 32-column half of a block
+    const uint32_t lane_off = (uint32_t)(q * 32) << 16;
+    const bool leader = (half == 0 && lane == 0);
+    Ph dxf[2];
+    int ys = 0;
+    for (int i = 0;; ++i) {
+      const int ti = sc.at(i);
+      if (ti < 0) break;
+      const int b = i & 1;
+      const Tile tl = tiles[ti];
+      mbar_wait_warp(bar(L::B_DXFULL + 8 * b), dxf[b].flip());
+      tc_fence_after();
+#pragma unroll 1
+      for (int cb = 0; cb < KB; ++cb, ++ys) {
+        const int st = ys & 1;
+        uint32_t v[32];
+        tmem_ld32(tmem + b * DH + lane_off + cb * 64 + half * 32, v);
+        tmem_ld_wait();
+        if (cb == KB - 1) {
+          tc_fence_before();
+          mbar_arrive(bar(L::B_DXEMPTY + 8 * b));
+        }
+        if (leader) bulk_wait_read<1>();       // the slab store issued from this stage 2 blocks ago has read it
+        named_bar_sync(2 + q, 64);
+        uint8_t* sp = smem + L::YS + st * kYStage + q * 4096;
+#pragma unroll
+        for (int u = 0; u < 32; u += 8) {
+          uint4 pk;
+          pk.x = pack_bf16x2(__uint_as_float(v[u + 0]), __uint_as_float(v[u + 1]));
+          pk.y = pack_bf16x2(__uint_as_float(v[u + 2]), __uint_as_float(v[u + 3]));
+          pk.z = pack_bf16x2(__uint_as_float(v[u + 4]), __uint_as_float(v[u + 5]));
+          pk.w = pack_bf16x2(__uint_as_float(v[u + 6]), __uint_as_float(v[u + 7]));
+          *reinterpret_cast<uint4*>(sp + kmaj_off(lane, half * 32 + u, 32)) = pk;
+        }
+        fence_proxy_async();
+        named_bar_sync(2 + q, 64);
+        if (leader) {
+          tma_store_2d(&xmap, sb + L::YS + st * kYStage + q * 4096, cb * 64, (int)((size_t)tl.head * Rp + tl.row0 + q * 32));
+          bulk_commit();
+        }
+      }
+    }
+    if (leader) bulk_wait_all();
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tmem_dealloc<L::TMEM_COLS>(tmem);
+}
+
 template <int DH, int DE>
 bool launch_t(const Routing& rt, const void* Xs, int64_t ldx, const void* dY, int64_t ldy, const void* W1,
               const void* W2, void* dXrep, float* dg, void* dH, void* gA, int num_sms, cudaStream_t s) {
-  CUtensorMap w1m, w2m;
-  if (!make_tmap_2d_bf16(&w1m, W1, (uint64_t)rt.H * rt.N_e * DE, DH, (uint64_t)DH * 2, DE, 64)) return false;
-  if (!make_tmap_2d_bf16(&w2m, W2, (uint64_t)rt.H * rt.N_e * DE, DH, (uint64_t)DH * 2, DE, 64)) return false;
-  auto kern = expert_bwd_dx_kernel<DH, DE>;
-  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, DxL<DH, DE>::BYTES);
+  CUtensorMap w1m, w2m, gxm, gym;
+  const uint64_t wrows = (uint64_t)rt.H * rt.N_e * DE;
+  // gather maps over the sub-token / dcat rows (T+1 rows, row T all-zero), box = 64 columns x 1 row
+  if (!make_tmap_2d_bf16(&gxm, Xs, (uint64_t)rt.T + 1, (uint64_t)rt.H * DH, (uint64_t)ldx * 2, 1, 64)) return false;
+  if (!make_tmap_2d_bf16(&gym, dY, (uint64_t)rt.T + 1, (uint64_t)rt.H * DH, (uint64_t)ldy * 2, 1, 64)) return false;
+  if (!make_tmap_2d_bf16(&w1m, W1, wrows, DH, (uint64_t)DH * 2, DE, 64)) return false;
+  if (!make_tmap_2d_bf16(&w2m, W2, wrows, DH, (uint64_t)DH * 2, DE, 64)) return false;
+  auto k1 = expert_bwd_h_kernel<DH, DE>;
+  cudaFuncSetAttribute(k1, cudaFuncAttributeMaxDynamicSharedMemorySize, HL<DH, DE>::BYTES);
   static const char* trace_path = getenv("MHL_TRACE_DX");
   if (trace_path) {
     TraceBuf tb{trace_buffer(s), 0};
     cudaMemcpyToSymbolAsync(g_trace_dx, &tb, sizeof(tb), 0, cudaMemcpyHostToDevice, s);
   }
-  kern<<<num_sms, kThreads, DxL<DH, DE>::BYTES, s>>>(w1m, w2m, rt, (const bf16*)Xs, ldx, (const bf16*)dY, ldy,
-                                                     (bf16*)dXrep, dg, (bf16*)dH, (bf16*)gA);
+  static const int dbg = getenv("MHL_DX_DBG") ? atoi(getenv("MHL_DX_DBG")) : 0;
+  k1<<<num_sms, kThreads1, HL<DH, DE>::BYTES, s>>>(w1m, w2m, gxm, gym, rt, dg, (bf16*)dH, (bf16*)gA, dbg);
   if (trace_path) {
     TraceBuf tb{nullptr, 0};
     cudaMemcpyToSymbolAsync(g_trace_dx, &tb, sizeof(tb), 0, cudaMemcpyHostToDevice, s);
     trace_dump(trace_path, s);
   }
+  return true;
+}
+
+template <int DH, int DE>
+bool launch_gemm_t(const Routing& rt, const void* W1, const void* dH, void* dXrep, int num_sms, cudaStream_t s) {
+  CUtensorMap w1m, hm, xm;
+  const uint64_t wrows = (uint64_t)rt.H * rt.N_e * DE, rows = (uint64_t)rt.H * rt.Rp;
+  if (!make_tmap_2d_bf16(&w1m, W1, wrows, DH, (uint64_t)DH * 2, DE, 64)) return false;
+  if (!make_tmap_2d_bf16(&hm, dH, rows, DE, (uint64_t)DE * 2, BM, 64)) return false;
+  if (!make_tmap_2d_bf16(&xm, dXrep, rows, DH, (uint64_t)DH * 2, 32, 64)) return false;
+  auto k2 = expert_dx_gemm_kernel<DH, DE>;
+  cudaFuncSetAttribute(k2, cudaFuncAttributeMaxDynamicSharedMemorySize, GL<DH, DE>::BYTES);
+  k2<<<num_sms, kThreads2, GL<DH, DE>::BYTES, s>>>(w1m, hm, xm, rt);
   return true;
 }
 
@@ -334,6 +496,15 @@ bool launch_expert_bwd_dx_sm100(const Routing& rt, const void* Xs, int64_t ldx, 
                                 void* gA, int num_sms, cudaStream_t s) {
 #define MHL_DX(A, B) \
   if (d_h == A && d_e == B) return launch_t<A, B>(rt, Xs, ldx, dY, ldy, W1, W2, dXrep, dg, dH, gA, num_sms, s);
+  MHL_DX(256, 128) MHL_DX(256, 64) MHL_DX(128, 128) MHL_DX(128, 64)
+#undef MHL_DX
+  return false;
+}
+
+bool launch_expert_dx_gemm_sm100(const Routing& rt, const void* W1, int d_h, int d_e, const void* dH, void* dXrep,
+                                 int num_sms, cudaStream_t s) {
+#define MHL_DX(A, B) \
+  if (d_h == A && d_e == B) return launch_gemm_t<A, B>(rt, W1, dH, dXrep, num_sms, s);
   MHL_DX(256, 128) MHL_DX(256, 64) MHL_DX(128, 128) MHL_DX(128, 64)
 #undef MHL_DX
   return false;

@@ -72,10 +72,13 @@ void launch_expert_bwd_simt(int dtype, const Routing& rt, const void* Xs, int64_
 void launch_expert_dw_simt(int dtype, const Routing& rt, const void* Xs, int64_t ldx, const void* dY, int64_t ldy,
                            const void* dH, const void* gA, int d_h, int d_e, float* dW1, float* dW2, cudaStream_t s);
 bool expert_bwd_sm100_supported(int d_h, int d_e);
-// the dX part alone (pipelined warp-specialized kernel, expert_bwd_dx_sm100.cu)
+// H/dA' recompute -> dH, gA, dg (pipelined warp-specialized kernel, expert_bwd_dx_sm100.cu)
 bool launch_expert_bwd_dx_sm100(const Routing& rt, const void* Xs, int64_t ldx, const void* dY, int64_t ldy,
                                 const void* W1, const void* W2, int d_h, int d_e, void* dXrep, float* dg, void* dH,
                                 void* gA, int num_sms, cudaStream_t s);
+// dXrep = dH W1_e per expert tile (TMA-fed grouped GEMM, expert_bwd_dx_sm100.cu)
+bool launch_expert_dx_gemm_sm100(const Routing& rt, const void* W1, int d_h, int d_e, const void* dH, void* dXrep,
+                                 int num_sms, cudaStream_t s);
 // tcgen05 dX kernel (dXrep, dg, dH, gA) and/or dW kernel (chunk partials + ordered reduce)
 bool launch_expert_bwd_sm100(const Routing& rt, const void* Xs, int64_t ldx, const void* dY, int64_t ldy,
                              const void* W1, const void* W2, int d_h, int d_e, void* dXrep, float* dg, void* dH,
