@@ -1,18 +1,15 @@
 // expert_dw_sm100.cu — B5 weight gradients of the block-sparse expert FFN on tcgen05/TMEM (sm_100a).
 //
-// Chain rule of y_r = g_r * gelu(x W1_e^T) W2_e for the clustered replicas of one expert
-// (Eq. 1), with H recomputed instead of stored (the forward never wrote it):
-//   kernel dX (per 128-replica tile):
-//     H   = X W1_e^T                 (tcgen05, B = W1_e K-major)
-//     dA' = dY W2_e^T                (tcgen05, B = W2_e K-major)       dY = dcat rows of the tokens
-//     dg  = <gelu(H), dA'>  (= <dY, E_e(x)>, the gate cotangent)
-//     dH  = g dA' gelu'(H),   gA = g gelu(H)      (bf16; dH also staged in smem)
-//     dXrep = dH W1_e                (tcgen05, B = W1_e read MN-major from the same smem copy)
-//   kernel dW (per chunk of <= kDwChunk sorted rows of one expert), no atomics:
-//     dW1_e^T += X^T dH,  dW2_e^T += dY^T gA     (tcgen05, both operands MN-major)
-//   then an ordered reduction over the expert's chunks (deterministic).
+// Chain rule of y_r = g_r * gelu(x W1_e^T) W2_e over the clustered replicas of one expert
+// (Eq. 1): with dH = g dA' gelu'(H) and gA = g gelu(H) from expert_bwd_dx_sm100.cu,
+//   dW1_e^T = X^T dH,   dW2_e^T = dY^T gA        (X, dY = sub-token / dcat rows of the replicas)
+// per chunk of <= kDwChunk sorted rows (tcgen05, both operands MN-major), no atomics; then an
+// ordered reduction over the expert's chunks (deterministic, R21).
+#include <cuda.h>
+
 #include "kernels.h"
 #include "sm100.cuh"
+#include "tma_host.h"
 
 namespace mhl {
 
@@ -20,130 +17,139 @@ namespace {
 
 using namespace sm100;
 
-constexpr int BM = kExpertBM;
-constexpr int kThreads = 256;
-
-__device__ __forceinline__ void gelu_and_grad(float h, float& a, float& da) {
-  const float cdf = 0.5f * (1.0f + erff(h * 0.70710678118654752f));
-  const float pdf = 0.39894228040143268f * __expf(-0.5f * h * h);
-  a = h * cdf;
-  da = cdf + h * pdf;
-}
-
 // =============================================================================================
 // dW kernel: per chunk (<= kDwChunk rows of one (head, expert)), accumulate in TMEM
 //   dW1^T[c][f] += sum_r X[r][c] dH[r][f]   dW2^T[c][f] += sum_r dY[r][c] gA[r][f]
-// M = c (DH/128 MMAs of M=128), N = f (DE), K = rows (16 per MMA).  Two 64-row stages.
+// M = c (DH/128 MMAs of M=128), N = f (DE), K = rows (16 per MMA), both operands MN-major.
+// Warp roles: kDwProd producer warps bring X, dY (TMA gather4 for the token-indexed rows, one lane
+// per 4 rows) and dH, gA (2-D TMA tiles of the contiguous sorted rows) into a 2-stage ring of
+// 64-row steps; 8 warps flush each chunk's fp32 accumulators to its partial slot; the last warp
+// issues the MMAs (+ owns TMEM).  The ring keeps filling while a chunk is flushed.
 // =============================================================================================
-constexpr int kHalf = 64;   // rows per pipeline stage
+constexpr int kHalf = 64;   // rows per pipeline step
+constexpr int kDwProd = 8;                     // producer warps 0..kDwProd-1
+constexpr int kDwFlush0 = kDwProd;             // 8 flush warps
+constexpr int kDwMma = kDwProd + 8;
+constexpr int kDwThreads = (kDwMma + 1) * 32;
 
 template <int DH, int DE>
 struct DwSmem {
-  static constexpr int STAGE = 2 * kHalf * DH * 2 + 2 * kHalf * DE * 2;     // X, dY, dH, gA
-  static constexpr int X = 0, DY = kHalf * DH * 2, DHH = 2 * kHalf * DH * 2, GA = DHH + kHalf * DE * 2;
-  static constexpr int BAR = 2 * STAGE;            // 2 mbarriers
-  static constexpr int TOK = BAR + 16;             // [2][kHalf]
-  static constexpr int TMEM = TOK + 2 * kHalf * 4;
+  static constexpr int XB = kHalf * DH * 2, EB = kHalf * DE * 2;
+  static constexpr int STAGE = 2 * XB + 2 * EB;                      // X, dY, dH, gA
+  static constexpr int X = 0, DY = XB, DHH = 2 * XB, GA = 2 * XB + EB;
+  static constexpr int S = 2;
+  static constexpr int BAR = S * STAGE;            // full[S], empty[S], accfull, accempty
+  static constexpr int TMEM = BAR + 8 * (2 * S + 2);
   static constexpr int BYTES = TMEM + 16;
 };
 
 template <int DH, int DE>
-__global__ void __launch_bounds__(kThreads, 1)
-expert_dw_kernel(Routing rt, const bf16* __restrict__ Xs, int64_t ldx, const bf16* __restrict__ dY, int64_t ldy,
-                 const bf16* __restrict__ dHg, const bf16* __restrict__ gAg, float* __restrict__ partial) {
+__global__ void __launch_bounds__(kDwThreads, 1)
+expert_dw_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap ymap,
+                 const __grid_constant__ CUtensorMap hmap, const __grid_constant__ CUtensorMap amap, Routing rt,
+                 float* __restrict__ partial) {
   const Tile* chunks = rt.chunks;
   const int64_t Rp = rt.Rp;
   using L = DwSmem<DH, DE>;
-  extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = smem_raw;   // SW128 atoms need 1024-byte alignment (checked below)
+  constexpr int S = L::S, MH = DH / 128, XK = DH / 64, EK = DE / 64;
+  extern __shared__ __align__(1024) uint8_t smem[];
   if ((smem_u32(smem) & 1023u) != 0u) __trap();
-  const uint32_t sbase = smem_u32(smem);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::BAR);
-  int* s_tok = reinterpret_cast<int*>(smem + L::TOK);
+  const uint32_t sb = smem_u32(smem);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + L::BAR);
+  uint64_t* empty = full + S;
+  uint64_t* accfull = full + 2 * S;
+  uint64_t* accempty = accfull + 1;
   uint32_t* s_tmem = reinterpret_cast<uint32_t*>(smem + L::TMEM);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  if (warp == 0) tmem_alloc<512>(s_tmem);
-  if (tid == 0) { mbar_init(&bars[0], 1); mbar_init(&bars[1], 1); fence_mbar_init(); }
+  if (tid == 0) {
+    for (int i = 0; i < S; ++i) { mbar_init(&full[i], kDwProd); mbar_init(&empty[i], 1); }
+    mbar_init(accfull, 1); mbar_init(accempty, 256);
+    fence_mbar_init();
+    tma_prefetch_desc(&xmap); tma_prefetch_desc(&ymap); tma_prefetch_desc(&hmap); tma_prefetch_desc(&amap);
+  }
+  if (warp == kDwMma) tmem_alloc<512>(s_tmem);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *s_tmem;
-  uint32_t ph[2] = {0, 0};
-  constexpr int MH = DH / 128;                          // M halves (c blocks of 128)
-  constexpr uint32_t IDESC = idesc_bf16(128, DE, 1, 1);
   const int nchunks = *rt.nchunks;
 
-  for (int ci = blockIdx.x; ci < nchunks; ci += gridDim.x) {
-    const Tile ch = chunks[ci];
-    const int nsteps = (ch.rows + kHalf - 1) / kHalf;
-    auto load_stage = [&](int st, int s) {
-      const int r0 = s * kHalf;
-      int* tok = s_tok + st * kHalf;
-      // tokens were written before the preceding __syncthreads()
-      const uint32_t base = sbase + st * L::STAGE;
-      for (int i = tid; i < kHalf * DH / 8; i += kThreads) {
-        const int r = i / (DH / 8), c = (i % (DH / 8)) * 8;
-        const size_t so = (size_t)tok[r];   // padding rows: the zero row
-        cp_async_16(base + L::X + kmaj_off(r, c, kHalf), Xs + so * ldx + (size_t)ch.head * DH + c, 16);
-        cp_async_16(base + L::DY + kmaj_off(r, c, kHalf), dY + so * ldy + (size_t)ch.head * DH + c, 16);
-      }
-      for (int i = tid; i < kHalf * DE / 8; i += kThreads) {
-        const int r = i / (DE / 8), c = (i % (DE / 8)) * 8;
-        const size_t grow = (size_t)ch.head * Rp + ch.row0 + r0 + r;   // chunk rows are whole tiles
-        cp_async_16(base + L::DHH + kmaj_off(r, c, kHalf), dHg + grow * DE + c, 16);
-        cp_async_16(base + L::GA + kmaj_off(r, c, kHalf), gAg + grow * DE + c, 16);
-      }
-      cp_async_commit();
-    };
-    auto load_tokens = [&](int st, int s) {
-      if (tid < kHalf) s_tok[st * kHalf + tid] = rt.tok_s[(size_t)ch.head * Rp + ch.row0 + s * kHalf + tid];
-    };
-    load_tokens(0, 0);
-    __syncthreads();
-    load_stage(0, 0);
-    for (int s = 0; s < nsteps; ++s) {
-      const int st = s & 1;
-      // prefetch step s+1 into the other stage once its previous MMAs (step s-1) are done
-      if (s + 1 < nsteps) {
-        if (s >= 1) { mbar_wait(&bars[st ^ 1], ph[st ^ 1]); ph[st ^ 1] ^= 1; }
-        load_tokens(st ^ 1, s + 1);
-        __syncthreads();
-        load_stage(st ^ 1, s + 1);
-        cp_async_wait_group<1>();
-      } else {
-        cp_async_wait_group<0>();
-      }
-      fence_proxy_async();
-      __syncthreads();
-      if (tid == 0) {
-        tc_fence_after();
-        const uint32_t base = sbase + st * L::STAGE;
-#pragma unroll
-        for (int ks = 0; ks < kHalf / 16; ++ks) {
-          const uint32_t ko = ks * 2 * 1024;              // 16 rows = 2 K-groups of 8
-#pragma unroll
-          for (int m = 0; m < MH; ++m) {
-            const uint32_t acc = (s > 0 || ks > 0) ? 1u : 0u;
-            // A = X^T (MN-major: c atoms at kHalf*128 B, row groups at 1024 B); B = dH^T likewise
-            mma_bf16(tmem + m * DE, sdesc_sw128(base + L::X + m * 2 * kHalf * 128 + ko, kHalf * 128, 1024),
-                     sdesc_sw128(base + L::DHH + ko, kHalf * 128, 1024), IDESC, acc);
-            mma_bf16(tmem + 256 + m * DE, sdesc_sw128(base + L::DY + m * 2 * kHalf * 128 + ko, kHalf * 128, 1024),
-                     sdesc_sw128(base + L::GA + ko, kHalf * 128, 1024), IDESC, acc);
+  if (warp < kDwProd) {
+    // ================================================================ producers
+    // A step needs 2*XK gathered 64-column chunks (X, dY: pair p -> operand p / XK, column block
+    // p % XK) and 2*EK contiguous chunks (dH, gA).  Warp w takes pairs w, w + kDwProd, ...; in a
+    // pair, lane g (mod 16) issues one gather4 for rows 4g..4g+3.
+    constexpr int NP = 2 * XK, NT = 2 * EK;
+    const int g = lane & 15;
+    int mybytes = 0;
+    for (int p = warp; p < NP; p += kDwProd) mybytes += kHalf * 128;
+    for (int t = warp; t < NT; t += kDwProd) mybytes += kHalf * 128;
+    int n = 0;                                                // steps of this CTA so far
+    for (int ci = blockIdx.x; ci < nchunks; ci += gridDim.x) {
+      const Tile ch = chunks[ci];
+      const int nsteps = ch.rows / kHalf;
+      const int32_t* tk = rt.tok_s + (size_t)ch.head * Rp + ch.row0 + 4 * g;
+      int r0 = tk[0], r1 = tk[1], r2 = tk[2], r3 = tk[3];
+      for (int s = 0; s < nsteps; ++s, ++n) {
+        const int st = n % S;
+        const uint32_t base = sb + st * L::STAGE;
+        if (lane == 0) {
+          mbar_wait(&empty[st], ((n / S) & 1) ^ 1);
+          mbar_expect_tx(&full[st], mybytes);
+          for (int t = warp; t < NT; t += kDwProd) {
+            const int kb = t % EK;
+            tma_load_2d(base + (t < EK ? L::DHH : L::GA) + kb * kHalf * 128, t < EK ? &hmap : &amap, kb * 64,
+                        (int)((size_t)ch.head * Rp + ch.row0 + s * kHalf), &full[st]);
           }
         }
-        mma_commit(&bars[st]);
+        __syncwarp();
+        for (int u = lane; u < ((NP - warp + kDwProd - 1) / kDwProd) * 16; u += 32) {
+          const int p = warp + (u >> 4) * kDwProd, kb = p % XK;
+          tma_gather4(base + (p < XK ? L::X : L::DY) + kb * kHalf * 128 + 4 * g * 128, p < XK ? &xmap : &ymap,
+                      ch.head * DH + kb * 64, r0, r1, r2, r3, &full[st]);
+        }
+        if (s + 1 < nsteps) { tk += kHalf; r0 = tk[0]; r1 = tk[1]; r2 = tk[2]; r3 = tk[3]; }
       }
     }
-    // drain: wait for the last step's MMAs (and the one before, if not yet waited)
-    {
-      const int last = (nsteps - 1) & 1;
-      if (nsteps >= 2) { mbar_wait(&bars[last ^ 1], ph[last ^ 1]); ph[last ^ 1] ^= 1; }
-      mbar_wait(&bars[last], ph[last]); ph[last] ^= 1;
+  } else if (warp == kDwMma) {
+    // ================================================================ MMA issuer
+    if (lane == 0) {
+      constexpr uint32_t IDESC = idesc_bf16(128, DE, 1, 1);
+      int n = 0, nc = 0;
+      for (int ci = blockIdx.x; ci < nchunks; ci += gridDim.x, ++nc) {
+        const int nsteps = chunks[ci].rows / kHalf;
+        if (nc >= 1) mbar_wait(accempty, (nc - 1) & 1);      // previous chunk flushed
+        tc_fence_after();
+        for (int s = 0; s < nsteps; ++s, ++n) {
+          const int st = n % S;
+          mbar_wait(&full[st], (n / S) & 1);
+          tc_fence_after();
+          const uint32_t base = sb + st * L::STAGE;
+#pragma unroll
+          for (int ks = 0; ks < kHalf / 16; ++ks) {
+            const uint32_t ko = ks * 2 * 1024;              // 16 rows = 2 K-groups of 8
+#pragma unroll
+            for (int m = 0; m < MH; ++m) {
+              const uint32_t acc = (s > 0 || ks > 0) ? 1u : 0u;
+              // A = X^T (MN-major: c atoms at kHalf*128 B, row groups at 1024 B); B = dH^T likewise
+              mma_bf16(tmem + m * DE, sdesc_sw128(base + L::X + m * 2 * kHalf * 128 + ko, kHalf * 128, 1024),
+                       sdesc_sw128(base + L::DHH + ko, kHalf * 128, 1024), IDESC, acc);
+              mma_bf16(tmem + 256 + m * DE, sdesc_sw128(base + L::DY + m * 2 * kHalf * 128 + ko, kHalf * 128, 1024),
+                       sdesc_sw128(base + L::GA + ko, kHalf * 128, 1024), IDESC, acc);
+            }
+          }
+          mma_commit(&empty[st]);
+        }
+        mma_commit(accfull);
+      }
     }
-    tc_fence_after();
-    // ---- epilogue: partial[ci][mat][f][c]  (thread = c row of the M block, coalesced over c)
-    {
-      const int q = warp & 3, wm = warp >> 2;            // warps 0-3: dW1, 4-7: dW2
+  } else if (warp >= kDwFlush0 && warp < kDwFlush0 + 8) {
+    // ================================================================ flush: partial[ci][mat][f][c]
+    const int q = warp & 3, wm = (warp - kDwFlush0) >> 2;   // lane quadrant; 0: dW1, 1: dW2
+    int nc = 0;
+    for (int ci = blockIdx.x; ci < nchunks; ci += gridDim.x, ++nc) {
+      mbar_wait_warp(accfull, nc & 1);
+      tc_fence_after();
       float* out = partial + ((size_t)ci * 2 + wm) * DE * DH;
       for (int m = 0; m < MH; ++m) {
         const int c = m * 128 + q * 32 + lane;
@@ -155,12 +161,13 @@ expert_dw_kernel(Routing rt, const bf16* __restrict__ Xs, int64_t ldx, const bf1
           for (int j = 0; j < 32; ++j) out[(size_t)(f0 + j) * DH + c] = __uint_as_float(v[j]);
         }
       }
+      tc_fence_before();
+      mbar_arrive(accempty);
     }
-    tc_fence_before();
-    __syncthreads();
   }
+  tc_fence_before();
   __syncthreads();
-  if (warp == 0) tmem_dealloc<512>(tmem);
+  if (warp == kDwMma) tmem_dealloc<512>(tmem);
 }
 
 // dW[h][e][f][c] = sum over the expert's chunks, in chunk order (deterministic); 0 if unused
@@ -182,8 +189,20 @@ dw_reduce_kernel(const float* __restrict__ partial, const int32_t* __restrict__ 
   }
 }
 
-template <typename K>
-void set_smem(K k, int bytes) { cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes); }
+template <int DH, int DE>
+bool launch_dw_t(const Routing& rt, const void* Xs, int64_t ldx, const void* dY, int64_t ldy, const void* dH,
+                 const void* gA, float* partial, int num_sms, cudaStream_t s) {
+  CUtensorMap xm, ym, hm, am;
+  const uint64_t rows = (uint64_t)rt.H * rt.Rp;
+  if (!make_tmap_2d_bf16(&xm, Xs, (uint64_t)rt.T + 1, (uint64_t)rt.H * DH, (uint64_t)ldx * 2, 1, 64)) return false;
+  if (!make_tmap_2d_bf16(&ym, dY, (uint64_t)rt.T + 1, (uint64_t)rt.H * DH, (uint64_t)ldy * 2, 1, 64)) return false;
+  if (!make_tmap_2d_bf16(&hm, dH, rows, DE, (uint64_t)DE * 2, kHalf, 64)) return false;
+  if (!make_tmap_2d_bf16(&am, gA, rows, DE, (uint64_t)DE * 2, kHalf, 64)) return false;
+  auto kern = expert_dw_kernel<DH, DE>;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, DwSmem<DH, DE>::BYTES);
+  kern<<<num_sms, kDwThreads, DwSmem<DH, DE>::BYTES, s>>>(xm, ym, hm, am, rt, partial);
+  return true;
+}
 
 }  // namespace
 
@@ -203,12 +222,7 @@ bool launch_expert_bwd_sm100(const Routing& rt, const void* Xs, int64_t ldx, con
     if (do_dx && !launch_expert_bwd_dx_sm100(rt, Xs, ldx, dY, ldy, W1, W2, d_h, d_e, dXrep, dg, dH, gA,       \
                                              num_sms, s))                                                        \
       ok = false;                                                                                                \
-    if (do_dw) {                                                                                                 \
-      auto kern = expert_dw_kernel<A, B>;                                                                        \
-      set_smem(kern, DwSmem<A, B>::BYTES);                                                                       \
-      kern<<<num_sms, kThreads, DwSmem<A, B>::BYTES, s>>>(rt, (const bf16*)Xs, ldx, (const bf16*)dY, ldy,        \
-                                                          (const bf16*)dH, (const bf16*)gA, partial);            \
-    }                                                                                                            \
+    if (do_dw && !launch_dw_t<A, B>(rt, Xs, ldx, dY, ldy, dH, gA, partial, num_sms, s)) ok = false;             \
   }
   MHL_BWD_CASE(256, 128) else MHL_BWD_CASE(256, 64) else MHL_BWD_CASE(128, 128) else MHL_BWD_CASE(128, 64)
 #undef MHL_BWD_CASE
