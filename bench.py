@@ -35,15 +35,47 @@ def workload_desc(cfg, T_loc):
             f"k={cfg.k}, d_e={cfg.d_e}, {cfg.dtype} fwd+bwd, HP")
 
 
+def _find_number(d, want, avoid=()):
+    """First numeric value in a (nested) dict whose key path contains every substring in `want`
+    and none in `avoid` (MEASURED_PEAKS.json is driver-written; its exact keys are not fixed)."""
+    stack = [("", d)]
+    while stack:
+        path, v = stack.pop(0)
+        if isinstance(v, dict):
+            stack.extend((f"{path}/{k}".lower(), x) for k, x in v.items())
+        elif isinstance(v, (int, float)) and all(w in path for w in want) and not any(a in path for a in avoid):
+            return float(v), path
+    return None, None
+
+
 def load_peaks():
+    """(hbm GB/s, source), (bf16 dense TF/s for a kernel inside a long step, source)."""
+    d = {}
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
         try:
             d = json.load(open(p))
-            return d, "measured"
         except Exception:
-            pass
-    return dict(FALLBACK_PEAKS), "fallback"
+            d = {}
+    hbm, hp = _find_number(d, ("hbm",), ("capacity", "size", "gib", "total")) if d else (None, None)
+    if hbm is None and d:
+        hbm, hp = _find_number(d, ("copy",))
+    tf, tp = (_find_number(d, ("bf16", "sustain")) if d else (None, None))
+    if tf is None and d:
+        tf, tp = _find_number(d, ("bf16",), ("fp8", "fp4"))
+    hbm_src = f"measured ({hp})" if hbm else "fallback (B200_PROFILING.md)"
+    tf_src = f"measured ({tp})" if tf else "fallback (B200_PROFILING.md, sustained)"
+    return (hbm or FALLBACK_PEAKS["hbm_gbs"], hbm_src), (tf or FALLBACK_PEAKS["bf16_tflops_sustained"], tf_src)
+
+
+def load_traffic():
+    """Per-launch DRAM bytes (read + write) of each span's kernel from the committed ncu --set full
+    captures (profiles/ncu_traffic.json, written by tools/ncu_summary.py), or {}."""
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        return json.load(open(p))
+    except Exception:
+        return {}
 
 
 # ----------------------------------------------------------------------------- clocks
@@ -97,20 +129,30 @@ class ClockSampler:
 
 # ----------------------------------------------------------------------------- algorithmic work
 def step_work(cfg, T_loc, G):
-    """Algorithmic FLOPs / bytes per step on one GPU."""
+    """Algorithmic bytes (or FLOPs) per step on one GPU, per timed span.
+
+    Expert kernels are memory-movement bound: their bytes count every gathered sub-token / dcat
+    row once per replica (R = T*k rows per head; most of those gathers are served by L2, whose
+    reuse is what makes them cheap), plus the rows they read/write contiguously."""
     d, N_h, d_h, N_e, k, d_e = cfg.d, cfg.N_h, cfg.d_h, cfg.N_e, cfg.k, cfg.d_e
     D, el = N_h * d_h, (2 if cfg.dtype == "bf16" else 4)
     subtok = T_loc * N_h                                   # sub-tokens per GPU after the scatter
-    rep = subtok * k
+    rep = subtok * k                                       # replica rows
     return {
-        "F5_expert_fwd": dict(flops=4 * d_h * d_e * rep),
-        "B5_expert_bwd_dx": dict(flops=(2 + 2 + 2) * d_h * d_e * rep),   # H recompute, dA', dX
-        "B5_expert_bwd_dw": dict(flops=(2 + 2) * d_h * d_e * rep),       # dW1, dW2
+        # X gather + Yrep write
+        "F5_expert_fwd": dict(bytes=rep * (2 * d_h * el)),
+        # X, dY gathers + dH, gA writes + dg
+        "B5_expert_bwd_dx": dict(bytes=rep * (2 * d_h * el + 2 * d_e * el + 4)),
+        # dH read + dXrep write
+        "B5_expert_dx_gemm": dict(bytes=rep * (d_e * el + d_h * el)),
+        # X, dY gathers + dH, gA reads
+        "B5_expert_bwd_dw": dict(bytes=rep * (2 * d_h * el + 2 * d_e * el)),
         "F1_proj_in": dict(flops=2 * T_loc * d * D),
         "F8_proj_out": dict(flops=2 * T_loc * d * D),
         "B8_proj_out_bwd": dict(flops=4 * T_loc * d * D),
         "B1_proj_in_bwd": dict(flops=4 * T_loc * d * D),
         "F3_router_topk": dict(bytes=subtok * (d_h * el + k * 8) + N_h // G * d_h * N_e * 4),
+        "B3_router_bwd": dict(bytes=subtok * (d_h * el + k * 16)),
         "F6_combine": dict(bytes=rep * d_h * el + subtok * d_h * el + rep * 4),
         "B6_combine_bwd": dict(bytes=rep * d_h * el + subtok * d_h * el + rep * 12),
     }
@@ -293,7 +335,8 @@ def main():
         return
 
     # ---- roofline of the dominant kernel (largest share of the step)
-    peaks, peak_src = load_peaks()
+    (hbm_peak, hbm_src), (tf_peak, tf_src) = load_peaks()
+    traffic = load_traffic()
     work = step_work(cfg, T_loc, G)
     per_step = {k: v[0] / args.steps for k, v in steps_t.items()}
     dom = max(per_step, key=per_step.get) if per_step else None
@@ -302,17 +345,17 @@ def main():
         calls = steps_t[dom][1] / args.steps
         dur_s = per_step[dom] / 1e3
         w = work.get(dom, {})
+        tr = traffic.get(dom, {}).get("dram_bytes_per_launch") if cfg.name == traffic.get("_workload") else None
         if "flops" in w:
             achieved = w["flops"] / dur_s / 1e12
-            peak = peaks.get("bf16_tflops_sustained", FALLBACK_PEAKS["bf16_tflops_sustained"])
-            roof = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
-                    "traffic": None, "kernel": dom, "launches_per_step": calls,
-                    "peak_source": f"{peak_src} bf16 sustained (kernel timed inside a long step)"}
+            roof = {"bound": "tensor", "achieved": achieved, "peak": tf_peak, "unit": "TFLOP/s",
+                    "frac": achieved / tf_peak, "traffic": tr, "kernel": dom, "launches_per_step": calls,
+                    "peak_source": tf_src}
         elif "bytes" in w:
             achieved = w["bytes"] / dur_s / 1e9
-            peak = peaks.get("hbm_gbs", FALLBACK_PEAKS["hbm_gbs"])
-            roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                    "traffic": None, "kernel": dom, "launches_per_step": calls, "peak_source": f"{peak_src} HBM copy"}
+            roof = {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s", "frac": achieved / hbm_peak,
+                    "traffic": tr, "algorithmic_bytes_per_launch": w["bytes"] / max(calls, 1), "kernel": dom,
+                    "launches_per_step": calls, "peak_source": hbm_src}
     breakdown = {k: round(v, 4) for k, v in sorted(per_step.items(), key=lambda kv: -kv[1])}
     layer_tflops = total_flops(cfg, T_loc) / (ms_per_step / 1e3) / 1e12
 

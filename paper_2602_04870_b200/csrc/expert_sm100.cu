@@ -5,13 +5,13 @@
 // y = g * gelu(x W1_e^T) W2_e, with the T x k x d_e hidden activation never written to HBM.
 // A tile = 128 clustered rows of one (head, expert) (segments are padded to whole tiles; padding
 // rows gather the all-zero sub-token and have gate 0):
-//   GEMM1  H[128 x d_e] = X[128 x d_h] W1_e^T   A = sub-tokens gathered (16-byte cp.async) into
+//   GEMM1  H[128 x d_e] = X[128 x d_h] W1_e^T   A = sub-tokens gathered (TMA gather4) into
 //                                                 K-major SW128 smem chunks; B = W1_e (TMA)
 //   epi 1  A = bf16(g * gelu(H)) -> TMEM          (exact-erf GELU, R1; A never touches smem)
 //   GEMM2  Y[128 x d_h] = A W2_e                 A read from TMEM; B = W2_e read MN-major
 //   epi 2  Yrep rows = bf16(Y)                   TMEM -> registers -> smem -> TMA bulk store
-// Warp roles (416 threads): warps 0-3 = producers (sub-token gathers through an smem ring, W1/W2 by
-// TMA when the expert changes, each as soon as the previous expert's last GEMM reading it has
+// Warp roles (416 threads): warps 0-3 = producers (TMA gather4 of the sub-tokens through an smem
+// ring, W1/W2 by TMA when the expert changes, each as soon as the previous expert's last GEMM reading it has
 // completed), warp 4 = MMA issuer (+ TMEM owner), warps 5-12 = epilogue.  TMEM: H [0,128),
 // A double buffer [128,256), Y [256,512): the MMA order G1(i), G2(i-1), G1(i+1), ... keeps the
 // tensor pipe busy while the epilogue of neighbouring tiles runs.  Persistent CTAs take groups of
@@ -48,14 +48,14 @@ struct FwdL {
   static constexpr int WB = DE * DH * 2;
   static constexpr int W1 = 0, W2 = WB, YS = 2 * WB, X = YS + 2 * kYStage;
   static constexpr int XS_RAW = (224 * 1024 - X) / kXChunk;
-  static constexpr int XS = XS_RAW > 12 ? 12 : XS_RAW;           // X ring stages
+  static constexpr int XS = (XS_RAW > 12 ? 12 : XS_RAW) / kProdWarps * kProdWarps;   // X ring stages
+  static_assert(XS >= kProdWarps, "X ring too small");
   static constexpr int CTRL = X + XS * kXChunk;
   static constexpr int B_XFULL = CTRL, B_XEMPTY = B_XFULL + 8 * XS;
   static constexpr int B_W1F = B_XEMPTY + 8 * XS, B_W1E = B_W1F + 8, B_W2F = B_W1E + 8, B_W2E = B_W2F + 8;
   static constexpr int B_HFULL = B_W2E + 8, B_HFREE = B_HFULL + 8, B_AFULL = B_HFREE + 8, B_G2DONE = B_AFULL + 16;
   static constexpr int B_YEMPTY = B_G2DONE + 16;
-  static constexpr int TOK = B_YEMPTY + 8;                        // [BM] int (producer only)
-  static constexpr int TMEMP = TOK + BM * 4;
+  static constexpr int TMEMP = B_YEMPTY + 8;
   static constexpr int BYTES = TMEMP + 16;
   static constexpr uint32_t T_H = 0, T_A = 128, T_Y = 256;
 };
@@ -78,29 +78,28 @@ __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wa
 template <int DH, int DE>
 __global__ void __launch_bounds__(kThreads, 1)
 expert_fwd_sm100_kernel(const __grid_constant__ CUtensorMap w1map, const __grid_constant__ CUtensorMap w2map,
-                        const __grid_constant__ CUtensorMap ymap, Routing rt, const bf16* __restrict__ Xg,
-                        int64_t ldx) {
+                        const __grid_constant__ CUtensorMap ymap, const __grid_constant__ CUtensorMap xmap,
+                        Routing rt) {
   using L = FwdL<DH, DE>;
   constexpr int XS = L::XS, KB1 = DH / 64;
   extern __shared__ __align__(1024) uint8_t smem[];
   if ((smem_u32(smem) & 1023u) != 0u) __trap();
   const uint32_t sb = smem_u32(smem);
   auto bar = [&](int off) { return reinterpret_cast<uint64_t*>(smem + off); };
-  int* s_tok = reinterpret_cast<int*>(smem + L::TOK);
   uint32_t* s_tmem = reinterpret_cast<uint32_t*>(smem + L::TMEMP);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const Tile* tiles = rt.tiles;
   const int N_e = rt.N_e;
 
   if (tid == 0) {
-    for (int i = 0; i < XS; ++i) { mbar_init(bar(L::B_XFULL + 8 * i), 32 * kProdWarps); mbar_init(bar(L::B_XEMPTY + 8 * i), 1); }
+    for (int i = 0; i < XS; ++i) { mbar_init(bar(L::B_XFULL + 8 * i), 1); mbar_init(bar(L::B_XEMPTY + 8 * i), 1); }
     mbar_init(bar(L::B_W1F), 1); mbar_init(bar(L::B_W1E), 1); mbar_init(bar(L::B_W2F), 1); mbar_init(bar(L::B_W2E), 1);
     mbar_init(bar(L::B_HFULL), 1);
     mbar_init(bar(L::B_HFREE), kEpiThreads);
     for (int b = 0; b < 2; ++b) { mbar_init(bar(L::B_AFULL + 8 * b), kEpiThreads); mbar_init(bar(L::B_G2DONE + 8 * b), 1); }
     mbar_init(bar(L::B_YEMPTY), kEpiThreads);
     fence_mbar_init();
-    tma_prefetch_desc(&w1map); tma_prefetch_desc(&w2map); tma_prefetch_desc(&ymap);
+    tma_prefetch_desc(&w1map); tma_prefetch_desc(&w2map); tma_prefetch_desc(&ymap); tma_prefetch_desc(&xmap);
   }
   if (warp == kMmaWarp) tmem_alloc<512>(s_tmem);
   tc_fence_before();
@@ -128,17 +127,21 @@ expert_fwd_sm100_kernel(const __grid_constant__ CUtensorMap w1map, const __grid_
 
   if (warp < kProdWarps) {
     // ================================================================ producers (4 warps)
-    // warp pw gathers rows [32 pw, 32 pw + 32) of every X chunk (more loads in flight per SM);
-    // warp 0 lane 0 also issues the weight TMAs.
+    // Chunk c of this CTA's X stream (tile c / KB1, column block c % KB1) goes to ring stage
+    // c % XS and is brought by warp c % kProdWarps (XS is a multiple of kProdWarps, so a stage is
+    // only ever refilled by the warp that filled it before): each of its 32 lanes issues one TMA
+    // gather4 of 4 sub-token rows (lane l owns tile rows 4l..4l+3).  Warp 0 lane 0 also issues the
+    // weight TMAs.
     const int pw = warp;
-    Ph xe[12], w1e, w2e;
-    int xs = 0;
-    int tok_next = 0;
+    Ph w1e, w2e;
+    int cnt = 0;
+    int nx[4] = {0, 0, 0, 0};
     {
       const int t0 = tile_at(0);
       if (t0 >= 0) {
         const Tile tl = tiles[t0];
-        tok_next = rt.tok_s[(size_t)tl.head * rt.Rp + tl.row0 + pw * 32 + lane];
+        const int32_t* tk = rt.tok_s + (size_t)tl.head * rt.Rp + tl.row0 + 4 * lane;
+        nx[0] = tk[0]; nx[1] = tk[1]; nx[2] = tk[2]; nx[3] = tk[3];
       }
     }
     for (int i = 0;; ++i) {
@@ -151,32 +154,29 @@ expert_fwd_sm100_kernel(const __grid_constant__ CUtensorMap w1map, const __grid_
         break;
       }
       const Tile tl = tiles[ti];
-      // this tile's token ids (loaded one tile ahead) -> smem; prefetch the next tile's
-      __syncwarp();
-      s_tok[pw * 32 + lane] = tok_next;
+      const int r0 = nx[0], r1 = nx[1], r2 = nx[2], r3 = nx[3];
       const int tn = tile_at(i + 1);
-      if (tn >= 0) {
+      if (tn >= 0) {     // next tile's token ids, loaded while this tile's chunks are issued
         const Tile tnl = tiles[tn];
-        tok_next = rt.tok_s[(size_t)tnl.head * rt.Rp + tnl.row0 + pw * 32 + lane];
+        const int32_t* tk = rt.tok_s + (size_t)tnl.head * rt.Rp + tnl.row0 + 4 * lane;
+        nx[0] = tk[0]; nx[1] = tk[1]; nx[2] = tk[2]; nx[3] = tk[3];
       }
-      __syncwarp();
       if (pw == 0 && lane == 0 && !same_expert(tile_at(i - 1), ti)) {
         mbar_wait(bar(L::B_W1E), w1e.flip() ^ 1);
         load_w(&w1map, L::W1, bar(L::B_W1F), tl);
       }
       __syncwarp();
-      for (int kb = 0; kb < KB1; ++kb) {
-        mbar_wait_warp(bar(L::B_XEMPTY + 8 * xs), xe[xs].flip() ^ 1);
-        const uint32_t dst = sb + L::X + xs * kXChunk;
-        const bf16* src = Xg + (size_t)tl.head * DH + kb * 64;
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          const int idx = j * 32 + lane, r = pw * 32 + (idx >> 3), c = (idx & 7) * 8;
-          cp_async_16(dst + kmaj_off(r, c, BM), src + (size_t)s_tok[r] * ldx + c, 16);
+      for (int kb = 0; kb < KB1; ++kb, ++cnt) {
+        if (cnt % kProdWarps != pw) continue;
+        const int xs = cnt % XS;
+        uint64_t* full = bar(L::B_XFULL + 8 * xs);
+        if (lane == 0) {
+          mbar_wait(bar(L::B_XEMPTY + 8 * xs), ((cnt / XS) & 1) ^ 1);
+          mbar_expect_tx(full, kXChunk);
         }
-        cp_async_mbar_arrive(bar(L::B_XFULL + 8 * xs));
-        if (pw == 0 && lane == 0) trace_ev(g_trace_fwd, 2, i * 16 + kb);
-        if (++xs == XS) xs = 0;
+        __syncwarp();
+        tma_gather4(sb + L::X + xs * kXChunk + lane * 4 * 128, &xmap, (int)tl.head * DH + kb * 64, r0, r1, r2, r3,
+                    full);
       }
       // W2 of the previous tile if it started a new expert run (read by G2(i-1), issued after G1(i))
       if (pw == 0 && lane == 0 && i >= 1 && !same_expert(tile_at(i - 2), tile_at(i - 1))) {
@@ -218,7 +218,6 @@ expert_fwd_sm100_kernel(const __grid_constant__ CUtensorMap w1map, const __grid_
         for (int kb = 0; kb < KB1; ++kb) {
           mbar_wait(bar(L::B_XFULL + 8 * xs), xf[xs].flip());
           trace_ev(g_trace_fwd, 11, i * 16 + kb);
-          fence_proxy_async();   // the chunk was written by cp.async (generic proxy)
           tc_fence_after();
 #pragma unroll
           for (int ks = 0; ks < 4; ++ks)
@@ -337,7 +336,9 @@ expert_fwd_sm100_kernel(const __grid_constant__ CUtensorMap w1map, const __grid_
 template <int DH, int DE>
 bool launch_t(const Routing& rt, const void* Xs, int64_t ldx, const void* W1, const void* W2, void* Yrep, int num_sms,
               cudaStream_t s) {
-  CUtensorMap w1m, w2m, ym;
+  CUtensorMap w1m, w2m, ym, xm;
+  // sub-token gather map: T+1 rows (row T all-zero), box = 64 columns x 1 row (TMA gather4)
+  if (!make_tmap_2d_bf16(&xm, Xs, (uint64_t)rt.T + 1, (uint64_t)rt.H * DH, (uint64_t)ldx * 2, 1, 64)) return false;
   if (!make_tmap_2d_bf16(&w1m, W1, (uint64_t)rt.H * rt.N_e * DE, DH, (uint64_t)DH * 2, DE, 64)) return false;
   if (!make_tmap_2d_bf16(&w2m, W2, (uint64_t)rt.H * rt.N_e * DE, DH, (uint64_t)DH * 2, DE, 64)) return false;
   if (!make_tmap_2d_bf16(&ym, Yrep, (uint64_t)rt.H * rt.Rp, DH, (uint64_t)DH * 2, 32, 64)) return false;
@@ -352,7 +353,7 @@ bool launch_t(const Routing& rt, const void* Xs, int64_t ldx, const void* W1, co
     TraceBuf tb{tbuf, 0};
     cudaMemcpyToSymbolAsync(g_trace_fwd, &tb, sizeof(tb), 0, cudaMemcpyHostToDevice, s);
   }
-  kern<<<num_sms, kThreads, FwdL<DH, DE>::BYTES, s>>>(w1m, w2m, ym, rt, (const bf16*)Xs, ldx);
+  kern<<<num_sms, kThreads, FwdL<DH, DE>::BYTES, s>>>(w1m, w2m, ym, xm, rt);
   if (trace_path) {
     TraceBuf tb{nullptr, 0};
     cudaMemcpyToSymbolAsync(g_trace_fwd, &tb, sizeof(tb), 0, cudaMemcpyHostToDevice, s);

@@ -13,7 +13,7 @@ tail -1 $OUT/${TAG}_bench.json | cut -c1-400
 # launch list of one timed step (cold-cache, serialised: compare shares, not absolutes)
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/${TAG}_launches.csv \
   python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu-baseline > /dev/null 2>&1; echo "ncu launches rc=$?"
-for k in ${NCU_KERNELS:-expert_bwd_dx expert_fwd_sm100 expert_dw router_sm100}; do
+for k in ${NCU_KERNELS:-expert_bwd_h expert_dw_kernel expert_fwd_sm100 expert_dx_gemm combine_bwd}; do
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:$k -s 0 -c 1 -o $OUT/${TAG}_prof_$k \
     python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu-baseline > /dev/null 2>&1; echo "ncu $k rc=$?"
 done

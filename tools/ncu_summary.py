@@ -3,6 +3,7 @@
 
     python tools/ncu_summary.py launches gpurun_out/r1b_launches.csv      # per-kernel share of a step
     python tools/ncu_summary.py report gpurun_out/r1b_prof_expert_fwd.ncu-rep [algorithmic_flops] [algorithmic_bytes]
+    python tools/ncu_summary.py traffic <workload> gpurun_out/<tag>_prof_*.ncu-rep   # -> profiles/ncu_traffic.json
 """
 import csv
 import io
@@ -66,8 +67,38 @@ def report(path, flops=None, nbytes=None):
     print(f"  dram traffic (read+write): {d.get('dram__bytes_read.sum')} + {d.get('dram__bytes_write.sum')}")
 
 
+SPAN_OF = {"expert_bwd_h": "B5_expert_bwd_dx", "expert_dw_kernel": "B5_expert_bwd_dw",
+           "expert_fwd_sm100": "F5_expert_fwd", "expert_dx_gemm": "B5_expert_dx_gemm",
+           "combine_bwd": "B6_combine_bwd", "combine_fwd": "F6_combine", "router_sm100": "F3_router_topk"}
+
+
+def traffic(workload, paths):
+    """Per-launch DRAM bytes (dram__bytes_read.sum + dram__bytes_write.sum) of each captured kernel,
+    keyed by the bench span it is timed under -> profiles/ncu_traffic.json (read by bench.py)."""
+    import json
+    import os
+    out = {"_workload": workload, "_source": "ncu --set full --clock-control none, one launch each"}
+    for path in paths:
+        csvout = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+        rows = list(csv.reader(io.StringIO(csvout)))
+        hdr, units, vals = rows[0], rows[1], rows[2]
+        d = {h: (vals[i], units[i]) for i, h in enumerate(hdr)}
+        scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+        b = sum(float(d[k][0].replace(",", "")) * scale.get(d[k][1], 1) for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"))
+        name = d["Kernel Name"][0]
+        span = next((v for k, v in SPAN_OF.items() if k in name), None)
+        if span:
+            out[span] = {"kernel": name.split("(")[0][:120], "dram_bytes_per_launch": b,
+                         "report": os.path.basename(path)}
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    json.dump(out, open(os.path.join(root, "profiles", "ncu_traffic.json"), "w"), indent=1)
+    print(json.dumps(out, indent=1))
+
+
 if __name__ == "__main__":
-    if sys.argv[1] == "launches":
+    if sys.argv[1] == "traffic":
+        traffic(sys.argv[2], sys.argv[3:])
+    elif sys.argv[1] == "launches":
         launches(sys.argv[2])
     else:
         report(sys.argv[2], *(sys.argv[3:5]))
