@@ -148,7 +148,7 @@ FwdLayout fwd_layout(const Dims& m) {
   L.send2 = b.take(m.G > 1 ? (size_t)m.T_g * m.HD * m.el : 0);
   L.recv2 = b.take(m.G > 1 ? (size_t)m.T_loc * m.D * m.el : 0);
   L.hist = b.take((size_t)m.H * m.n_rt * m.N_e * 4);
-  L.tilepref = b.take((size_t)m.H * m.n_rt * m.N_e * 4);
+  L.tilepref = b.take(((size_t)m.H * m.n_rt * m.N_e + (size_t)m.H * mhl::kTileParts * m.N_e) * 4);   // + tile bases
   L.counts = b.take((size_t)m.H * m.N_e * 4);
   L.planes = b.take(mhl::router_sm100_planes_bytes(m.H, m.d_h, m.N_e));
   L.total = b.off;

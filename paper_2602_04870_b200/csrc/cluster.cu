@@ -8,8 +8,9 @@
 // block-sparse mask of Eq. 7 becomes a list of whole 128-row tiles; padding rows point at
 // the all-zero sub-token row (token id T) with gate 0 and contribute exactly nothing.
 // Outputs per head (Rp = padded row capacity): perm (row -> replica or -1), tok_s (row -> token
-// or T), gate_s (row -> gate or 0), pos (replica -> row), off, the tile list and the list of
-// <= kDwChunk-row chunks used by the weight-gradient kernel.
+// or T), gate_s (row -> gate or 0), pos (replica -> row), off, the tile list (L2-friendly
+// (head, part, expert) order, see offsets_kernel) and the list of <= kDwChunk-row chunks used by
+// the weight-gradient kernel.
 #include "kernels.h"
 
 namespace mhl {
@@ -77,71 +78,104 @@ __device__ int block_exclusive_scan_1024(int v, int* s_warp, int* total) {
   return r;
 }
 
-// (2) single CTA: padded per-head offsets off[h][e] (exclusive scan of ceil(count/128)*128),
-// the tile list, the dW chunk list (cbase/ccount per (h, e)) and the padding-row fill.
+// (2) single CTA: padded per-head offsets off[h][e] (exclusive scan of ceil(count/128)*128), the
+// per-(h, e) tile and dW-chunk bases.  The tile list is ordered (head, part, expert, tile): expert
+// e's nt tiles are cut into kTileParts contiguous parts (part p = tiles [p*nt/P, (p+1)*nt/P)),
+// and all experts' part-p tiles come before any part-(p+1) tile.  Within an expert the rows are in
+// token order, so the tiles in flight at any moment (consecutive list entries) cover one narrow
+// token window of the head across many experts: every sub-token row gathered for them is re-read
+// by its other top-k experts while it is still in L2.
 __global__ void __launch_bounds__(1024)
-offsets_tiles_kernel(const int32_t* __restrict__ counts, int32_t* __restrict__ off, Tile* __restrict__ tiles,
-                     int32_t* __restrict__ ntiles, int H, int N_e, int max_tiles, Tile* __restrict__ chunks,
-                     int32_t* __restrict__ nchunks, int32_t* __restrict__ cbase, int32_t* __restrict__ ccount,
-                     int max_chunks, int64_t Rp, int32_t* __restrict__ perm, int32_t* __restrict__ tok_s,
-                     float* __restrict__ gate_s, int tok_zero) {
+offsets_kernel(const int32_t* __restrict__ counts, int32_t* __restrict__ off, int32_t* __restrict__ tbase,
+               int32_t* __restrict__ ntiles, int H, int N_e, int max_tiles, int32_t* __restrict__ nchunks,
+               int32_t* __restrict__ cbase, int32_t* __restrict__ ccount, int max_chunks) {
   __shared__ int s_warp[64];
   __shared__ int s_tot;
   int carry_t = 0, carry_c = 0;
   for (int h = 0; h < H; ++h) {
     int carry_r = 0;
+    for (int p = 0; p < kTileParts; ++p) {
+      int carry_p = 0;
+      for (int base = 0; base < N_e; base += 1024) {
+        const int e = base + threadIdx.x;
+        const int c = (e < N_e) ? counts[(size_t)h * N_e + e] : 0;
+        const int nt = (c + kExpertBM - 1) / kExpertBM;
+        const int np = (p + 1) * nt / kTileParts - p * nt / kTileParts;   // tiles of e in part p
+        const int px = block_exclusive_scan_1024(np, s_warp, &s_tot);
+        const int ptot = s_tot;
+        __syncthreads();
+        if (e < N_e) tbase[((size_t)h * kTileParts + p) * N_e + e] = carry_t + carry_p + px;
+        carry_p += ptot;
+      }
+      carry_t += carry_p;
+    }
     for (int base = 0; base < N_e; base += 1024) {
       const int e = base + threadIdx.x;
       const int c = (e < N_e) ? counts[(size_t)h * N_e + e] : 0;
-      const int nt = (c + kExpertBM - 1) / kExpertBM;
-      const int cp = nt * kExpertBM;                          // padded segment length
+      const int cp = (c + kExpertBM - 1) / kExpertBM * kExpertBM;       // padded segment length
       const int rx = block_exclusive_scan_1024(cp, s_warp, &s_tot);
       const int rtot = s_tot;
-      __syncthreads();
-      const int tx = block_exclusive_scan_1024(nt, s_warp, &s_tot);
-      const int ttot = s_tot;
       __syncthreads();
       const int nc = (cp + kDwChunk - 1) / kDwChunk;
       const int cx = block_exclusive_scan_1024(nc, s_warp, &s_tot);
       const int ctot = s_tot;
       __syncthreads();
       if (e < N_e) {
-        const int row_off = carry_r + rx;
-        off[(size_t)h * (N_e + 1) + e] = row_off;
-        for (int i = 0; i < nt; ++i) {
-          const int ti = carry_t + tx + i;
-          if (ti < max_tiles) {
-            Tile tl;
-            tl.head = h; tl.expert = e; tl.row0 = row_off + i * kExpertBM;
-            tl.rows = min(kExpertBM, c - i * kExpertBM);
-            tiles[ti] = tl;
-          }
-        }
+        off[(size_t)h * (N_e + 1) + e] = carry_r + rx;
         cbase[(size_t)h * N_e + e] = carry_c + cx;
         ccount[(size_t)h * N_e + e] = nc;
-        for (int i = 0; i < nc; ++i) {
-          const int ci = carry_c + cx + i;
-          if (ci < max_chunks) {
-            Tile tl;
-            tl.head = h; tl.expert = e; tl.row0 = row_off + i * kDwChunk;
-            tl.rows = min(kDwChunk, cp - i * kDwChunk);
-            chunks[ci] = tl;
-          }
-        }
-        // padding rows of this segment: no replica, zero sub-token, gate 0
-        for (int r = row_off + c; r < row_off + cp; ++r) {
-          perm[(size_t)h * Rp + r] = -1;
-          tok_s[(size_t)h * Rp + r] = tok_zero;
-          gate_s[(size_t)h * Rp + r] = 0.f;
-        }
       }
       carry_r += rtot;
-      carry_t += ttot;
       carry_c += ctot;
     }
     if (threadIdx.x == 0) off[(size_t)h * (N_e + 1) + N_e] = carry_r;
   }
   if (threadIdx.x == 0) { *ntiles = min(carry_t, max_tiles); *nchunks = min(carry_c, max_chunks); }
+}
+
+// (2b) one thread per (h, e): its tiles (at the (h, part, e) positions), its dW chunks and the
+// padding-row fill of its segment.
+__global__ void __launch_bounds__(128)
+tiles_kernel(const int32_t* __restrict__ counts, const int32_t* __restrict__ off, const int32_t* __restrict__ tbase,
+             Tile* __restrict__ tiles, int max_tiles, Tile* __restrict__ chunks, const int32_t* __restrict__ cbase,
+             int max_chunks, int H, int N_e, int64_t Rp, int32_t* __restrict__ perm, int32_t* __restrict__ tok_s,
+             float* __restrict__ gate_s, int tok_zero) {
+  const int he = blockIdx.x * blockDim.x + threadIdx.x;
+  if (he >= H * N_e) return;
+  const int h = he / N_e, e = he % N_e;
+  const int c = counts[he];
+  const int nt = (c + kExpertBM - 1) / kExpertBM;
+  const int cp = nt * kExpertBM;
+  const int row_off = off[(size_t)h * (N_e + 1) + e];
+  for (int p = 0; p < kTileParts; ++p) {
+    const int j0 = p * nt / kTileParts, j1 = (p + 1) * nt / kTileParts;
+    const int tb = tbase[((size_t)h * kTileParts + p) * N_e + e];
+    for (int j = j0; j < j1; ++j) {
+      const int ti = tb + (j - j0);
+      if (ti < max_tiles) {
+        Tile tl;
+        tl.head = h; tl.expert = e; tl.row0 = row_off + j * kExpertBM;
+        tl.rows = min(kExpertBM, c - j * kExpertBM);
+        tiles[ti] = tl;
+      }
+    }
+  }
+  const int nc = (cp + kDwChunk - 1) / kDwChunk;
+  for (int i = 0; i < nc; ++i) {
+    const int ci = cbase[he] + i;
+    if (ci < max_chunks) {
+      Tile tl;
+      tl.head = h; tl.expert = e; tl.row0 = row_off + i * kDwChunk;
+      tl.rows = min(kDwChunk, cp - i * kDwChunk);
+      chunks[ci] = tl;
+    }
+  }
+  // padding rows of this segment: no replica, zero sub-token, gate 0
+  for (int r = row_off + c; r < row_off + cp; ++r) {
+    perm[(size_t)h * Rp + r] = -1;
+    tok_s[(size_t)h * Rp + r] = tok_zero;
+    gate_s[(size_t)h * Rp + r] = 0.f;
+  }
 }
 
 // (3) per (h, router tile): stable ranks inside the tile via warp match, scatter perm/pos/tok/gate
@@ -188,8 +222,11 @@ void launch_cluster(int H, int64_t T, int k, int N_e, const int32_t* idx, const 
                     int32_t* nchunks, int32_t* cbase, int32_t* ccount, int max_chunks, cudaStream_t s) {
   const int n_rt = (int)((T + kRouterTile - 1) / kRouterTile);
   tile_prefix_kernel<<<dim3(N_e, H), 256, 0, s>>>(hist, tilepref, counts, n_rt, N_e);
-  offsets_tiles_kernel<<<1, 1024, 0, s>>>(counts, off, tiles, ntiles, H, N_e, max_tiles, chunks, nchunks, cbase,
-                                          ccount, max_chunks, Rp, perm, tok_s, gate_s, (int)T);
+  // tile bases [H][kTileParts][N_e] live in the (otherwise unused here) tail of tilepref's scratch
+  int32_t* tbase = tilepref + (size_t)H * n_rt * N_e;
+  offsets_kernel<<<1, 1024, 0, s>>>(counts, off, tbase, ntiles, H, N_e, max_tiles, nchunks, cbase, ccount, max_chunks);
+  tiles_kernel<<<(H * N_e + 127) / 128, 128, 0, s>>>(counts, off, tbase, tiles, max_tiles, chunks, cbase, max_chunks, H,
+                                                     N_e, Rp, perm, tok_s, gate_s, (int)T);
   scatter_kernel<<<dim3(n_rt, H), 32, sizeof(int) * N_e, s>>>(idx, gate, off, tilepref, perm, pos, tok_s, gate_s, T, k,
                                                               N_e, n_rt, Rp);
 }

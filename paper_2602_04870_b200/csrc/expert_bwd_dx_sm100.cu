@@ -81,14 +81,16 @@ struct Sched {
 // =============================================================================================
 // kernel 1: H, dA' -> dH, gA, dg
 // =============================================================================================
-constexpr int kProdWarps = 6, kMmaWarp = kProdWarps, kEpiWarp0 = kProdWarps + 1, kEpiWarps = 16;
+constexpr int kProdWarps = 4, kMmaWarp = kProdWarps, kEpiWarp0 = kProdWarps + 1, kEpiWarps = 16;
 constexpr int kThreads1 = (kEpiWarp0 + kEpiWarps) * 32;
 constexpr int kEpiThreads = kEpiWarps * 32;
 
 template <int DH, int DE>
 struct HL {
   static constexpr int WB = DE * DH * 2;
-  static constexpr int W1 = 0, W2 = WB, RING = 2 * WB;
+  static constexpr int BOXES = DE / 64;                    // 64-column output boxes per row
+  static constexpr int STGB = 4 * BOXES * 4096;             // dH/gA staging: [quadrant][box] 32 x 64 bf16
+  static constexpr int W1 = 0, W2 = WB, STG = 2 * WB, RING = STG + STGB;
   static constexpr int CTRL_MAX = 3 * 1024;
   static constexpr int S_RAW = (kMaxSmem - RING - CTRL_MAX) / kChunk;
   // a multiple of kProdWarps: chunk c -> stage c % S, warp c % kProdWarps, so every stage is only
@@ -108,8 +110,9 @@ struct HL {
 template <int DH, int DE>
 __global__ void __launch_bounds__(kThreads1, 1)
 expert_bwd_h_kernel(const __grid_constant__ CUtensorMap w1map, const __grid_constant__ CUtensorMap w2map,
-                    const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap ymap, Routing rt,
-                    float* __restrict__ dg, bf16* __restrict__ dHg, bf16* __restrict__ gAg, int dbg) {
+                    const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap ymap,
+                    const __grid_constant__ CUtensorMap hsmap, const __grid_constant__ CUtensorMap asmap, Routing rt,
+                    float* __restrict__ dg, int dbg) {
   using L = HL<DH, DE>;
   TraceBuf trc = g_trace_dx;   // one load; trace_ev then costs a register test
   constexpr int S = L::S, KB = DH / 64;
@@ -130,6 +133,7 @@ expert_bwd_h_kernel(const __grid_constant__ CUtensorMap w1map, const __grid_cons
     for (int b = 0; b < 2; ++b) { mbar_init(bar(L::B_HDFULL + 8 * b), 1); mbar_init(bar(L::B_HDFREE + 8 * b), kEpiThreads); }
     fence_mbar_init();
     tma_prefetch_desc(&w1map); tma_prefetch_desc(&w2map); tma_prefetch_desc(&xmap); tma_prefetch_desc(&ymap);
+    tma_prefetch_desc(&hsmap); tma_prefetch_desc(&asmap);
   }
   if (warp == kMmaWarp) tmem_alloc<512>(s_tmem);
   tc_fence_before();
@@ -153,6 +157,7 @@ expert_bwd_h_kernel(const __grid_constant__ CUtensorMap w1map, const __grid_cons
     const int pw = warp;
     Ph w1e, w2e;
     int cnt = 0;                       // chunks of this CTA's stream so far
+    const uint64_t pol_keep = (dbg & 16) ? l2_evict_normal() : l2_evict_last();   // rows reused k times per head
     for (int i = 0;; ++i) {
       const int ti = sc.at(i);
       if (ti < 0) break;
@@ -178,8 +183,8 @@ expert_bwd_h_kernel(const __grid_constant__ CUtensorMap w1map, const __grid_cons
         }
         __syncwarp();
         const int kb = j % KB;
-        tma_gather4(sb + L::RING + st * kChunk + lane * 4 * 128, j < KB ? &xmap : &ymap, tl.head * DH + kb * 64, r0,
-                    r1, r2, r3, full);
+        tma_gather4_hint(sb + L::RING + st * kChunk + lane * 4 * 128, j < KB ? &xmap : &ymap, tl.head * DH + kb * 64,
+                         r0, r1, r2, r3, full, pol_keep);
       }
     }
   } else if (warp == kMmaWarp) {
@@ -227,25 +232,42 @@ expert_bwd_h_kernel(const __grid_constant__ CUtensorMap w1map, const __grid_cons
     }
   } else {
     // ================================================================ epilogue (kEpiWarps warps)
-    // warp -> (lane quadrant q, column group cg); each thread owns one row and NC columns of H/dA',
-    // streamed through registers 16 columns at a time (TMEM -> gelu/gelu' -> bf16 -> HBM).
-    constexpr int NG = kEpiWarps / 4, NC = DE / NG;
+    // warp -> (lane quadrant q, column group cg); each thread owns one row and NC columns of H/dA'
+    // (TMEM -> gelu/gelu' -> bf16).  dH and gA leave through smem and TMA bulk stores: the warps of
+    // one 64-column box (64/NC of them) write their 32 x NC slices into the box's SW128 staging slot
+    // and the box leader issues the store (dH, then gA through the same slot), so the rows reach
+    // HBM as whole 128-byte lines without occupying the LSU path the gathers share.
+    constexpr int NG = kEpiWarps / 4, NC = DE / NG, WPB = 64 / NC;   // warps per output box
     const int q = warp & 3, cg = (warp - kEpiWarp0) >> 2;
+    const int box = cg * NC / 64, bcol = cg * NC % 64;
+    const bool leader = (bcol == 0 && lane == 0);
+    const int bar_box = 2 + q * L::BOXES + box, bar_dg = 2 + 4 * L::BOXES + q;
+    uint8_t* slot = smem + L::STG + (q * L::BOXES + box) * 4096;
+    const uint32_t slot_s = sb + L::STG + (q * L::BOXES + box) * 4096;
     const int row = q * 32 + lane;
     const uint32_t lane_off = (uint32_t)(q * 32) << 16;
     Ph hd[2];
+    auto stage = [&](const uint32_t* w) {     // this thread's NC bf16 of its row -> the box slot
+#pragma unroll
+      for (int u = 0; u < NC; u += 8)
+        *reinterpret_cast<uint4*>(slot + kmaj_off(lane, bcol + u, 32)) =
+            make_uint4(w[u / 2], w[u / 2 + 1], w[u / 2 + 2], w[u / 2 + 3]);
+      fence_proxy_async();
+    };
     for (int i = 0;; ++i) {
       const int ti = sc.at(i);
       if (ti < 0) break;
       const int b = i & 1;
       const Tile tl = tiles[ti];
       const size_t grow = (size_t)tl.head * Rp + tl.row0 + row;
+      const int orow = (int)((size_t)tl.head * Rp + tl.row0 + q * 32);
       const float g = rt.gate_s[grow];
       const int rep = rt.perm[grow];
       mbar_wait_warp(bar(L::B_HDFULL + 8 * b), hd[b].flip());
       if (tid == kEpiWarp0 * 32) trace_ev(trc, 50, i);
       tc_fence_after();
       float dgp = 0.f;
+      uint32_t dhp[NC / 2], gap[NC / 2];
 #pragma unroll
       for (int c = 0; c < NC; c += 16) {
         uint32_t hv[16], dv[16];
@@ -257,8 +279,6 @@ expert_bwd_h_kernel(const __grid_constant__ CUtensorMap w1map, const __grid_cons
           tc_fence_before();
           mbar_arrive(bar(L::B_HDFREE + 8 * b));
         }
-        if (dbg & 2) continue;
-        uint32_t dhp[8], gap[8];
 #pragma unroll
         for (int u = 0; u < 16; u += 2) {
           const float2 h2 = make_float2(__uint_as_float(hv[u]), __uint_as_float(hv[u + 1]));
@@ -269,25 +289,35 @@ expert_bwd_h_kernel(const __grid_constant__ CUtensorMap w1map, const __grid_cons
           dgp = fmaf(a.y, d2.y, dgp);
           const float2 dh = __fmul2_rn(__fmul2_rn(d2, gp), make_float2(g, g));
           const float2 ga = __fmul2_rn(a, make_float2(g, g));
-          dhp[u / 2] = pack_bf16x2(dh.x, dh.y);
-          gap[u / 2] = pack_bf16x2(ga.x, ga.y);
+          dhp[(c + u) / 2] = pack_bf16x2(dh.x, dh.y);
+          gap[(c + u) / 2] = pack_bf16x2(ga.x, ga.y);
         }
-        st_global_v8(dHg + grow * DE + cg * NC + c, dhp[0], dhp[1], dhp[2], dhp[3], dhp[4], dhp[5], dhp[6], dhp[7]);
-        st_global_v8(gAg + grow * DE + cg * NC + c, gap[0], gap[1], gap[2], gap[3], gap[4], gap[5], gap[6], gap[7]);
       }
       if (tid == kEpiWarp0 * 32) trace_ev(trc, 52, i);
+      if (!(dbg & 4)) {
+        if (leader) bulk_wait_read<0>();          // the previous tile's gA store has read the slot
+        named_bar_sync(bar_box, 32 * WPB);
+        stage(dhp);
+        named_bar_sync(bar_box, 32 * WPB);
+        if (leader) { tma_store_2d(&hsmap, slot_s, box * 64, orow); bulk_commit(); bulk_wait_read<0>(); }
+        named_bar_sync(bar_box, 32 * WPB);
+        stage(gap);
+        named_bar_sync(bar_box, 32 * WPB);
+        if (leader) { tma_store_2d(&asmap, slot_s, box * 64, orow); bulk_commit(); }
+      }
       // gate cotangent: the NG column-group partial sums of this row, added in group order
       s_dg[cg * BM + row] = dgp;
-      named_bar_sync(2 + q, 32 * NG);
+      named_bar_sync(bar_dg, 32 * NG);
       if (cg == 0 && rep >= 0) {
         float acc = s_dg[row];
 #pragma unroll
         for (int u = 1; u < NG; ++u) acc += s_dg[u * BM + row];
         dg[(size_t)tl.head * R + rep] = acc;
       }
-      named_bar_sync(2 + q, 32 * NG);
+      named_bar_sync(bar_dg, 32 * NG);
       if (tid == kEpiWarp0 * 32) trace_ev(trc, 55, i);
     }
+    if (leader) bulk_wait_all();
   }
   tc_fence_before();
   __syncthreads();
@@ -452,7 +482,10 @@ expert_dx_gemm_kernel(const __grid_constant__ CUtensorMap w1map, const __grid_co
 template <int DH, int DE>
 bool launch_t(const Routing& rt, const void* Xs, int64_t ldx, const void* dY, int64_t ldy, const void* W1,
               const void* W2, void* dXrep, float* dg, void* dH, void* gA, int num_sms, cudaStream_t s) {
-  CUtensorMap w1m, w2m, gxm, gym;
+  CUtensorMap w1m, w2m, gxm, gym, hsm, asm_;
+  // dH / gA store maps: [H*Rp rows][d_e], box = 64 columns x 32 rows (one epilogue lane quadrant)
+  if (!make_tmap_2d_bf16(&hsm, dH, (uint64_t)rt.H * rt.Rp, DE, (uint64_t)DE * 2, 32, 64)) return false;
+  if (!make_tmap_2d_bf16(&asm_, gA, (uint64_t)rt.H * rt.Rp, DE, (uint64_t)DE * 2, 32, 64)) return false;
   const uint64_t wrows = (uint64_t)rt.H * rt.N_e * DE;
   // gather maps over the sub-token / dcat rows (T+1 rows, row T all-zero), box = 64 columns x 1 row
   if (!make_tmap_2d_bf16(&gxm, Xs, (uint64_t)rt.T + 1, (uint64_t)rt.H * DH, (uint64_t)ldx * 2, 1, 64)) return false;
@@ -467,7 +500,7 @@ bool launch_t(const Routing& rt, const void* Xs, int64_t ldx, const void* dY, in
     cudaMemcpyToSymbolAsync(g_trace_dx, &tb, sizeof(tb), 0, cudaMemcpyHostToDevice, s);
   }
   static const int dbg = getenv("MHL_DX_DBG") ? atoi(getenv("MHL_DX_DBG")) : 0;
-  k1<<<num_sms, kThreads1, HL<DH, DE>::BYTES, s>>>(w1m, w2m, gxm, gym, rt, dg, (bf16*)dH, (bf16*)gA, dbg);
+  k1<<<num_sms, kThreads1, HL<DH, DE>::BYTES, s>>>(w1m, w2m, gxm, gym, hsm, asm_, rt, dg, dbg);
   if (trace_path) {
     TraceBuf tb{nullptr, 0};
     cudaMemcpyToSymbolAsync(g_trace_dx, &tb, sizeof(tb), 0, cudaMemcpyHostToDevice, s);

@@ -9,7 +9,8 @@ namespace mhl {
 constexpr int kRouterTile = 128;   // tokens per router CTA (= clustering tile of F4)
 constexpr int kExpertBM = 128;     // replica rows per expert tile (tcgen05 M); segments padded to it
 constexpr int kDwChunk = 4096;     // sorted rows per weight-gradient partial (B5 dW)
-constexpr int kTileGroup = 16;     // consecutive expert tiles a persistent CTA takes at once
+constexpr int kTileGroup = 8;      // consecutive expert tiles a persistent CTA takes at once
+constexpr int kTileParts = 8;      // token-order parts per expert segment in the tile list (cluster.cu)
 
 // Clustered routing of one rank's local heads (F3/F4 outputs, device pointers).
 // Sorted-row arrays have a fixed per-head capacity Rp = T*k + N_e*128 (expert segments are
@@ -23,7 +24,7 @@ struct Routing {
   const float* gate_s;     // [H][Rp]    sorted row -> gate, or 0
   const int32_t* pos;      // [H][T*k]   replica -> sorted row
   const int32_t* off;      // [H][N_e+1] padded segment offsets
-  const Tile* tiles; const int32_t* ntiles; int max_tiles;        // 128-row tiles, (h, e, row) order
+  const Tile* tiles; const int32_t* ntiles; int max_tiles;        // 128-row tiles, (h, part, e, row) order
   const Tile* chunks; const int32_t* nchunks; int max_chunks;     // dW chunks
   const int32_t* cbase; const int32_t* ccount;                    // [H][N_e] chunk range per expert
 };
