@@ -2,8 +2,8 @@
 //
 // F6: y[t][h*d_h + c] = sum_{j=0..k-1} Yrep[h][pos(t,j)][c]          (gates already applied in F5)
 // B6: dXs[t][h*d_h + c] = sum_j dXrep[h][pos(t,j)][c] + sum_j dS[t][j] W_r[h][c][e_j]   (Alg. 2 l.9)
-// One warp per (token, head); lane l owns 16-byte column chunks l, l+32, ...  Sums run in fixed
-// j order in fp32 (deterministic), rounded once to the storage type.  Rows are written straight
+// Lane l owns 16-byte column chunks l, l+32, ... of a (token, head) row.  Sums run in fixed j
+// order in fp32 (deterministic), rounded once to the storage type.  Rows are written straight
 // into the all-to-all send buffer (row = global token, column block = local head).
 #include "kernels.h"
 
@@ -28,85 +28,145 @@ __device__ __forceinline__ uint4 pack(const float (&f)[8]) {
   return v;
 }
 
-template <typename E, bool BWD>
-__global__ void __launch_bounds__(256)
+constexpr int kCombTok = 128;    // tokens of one head per CTA (F6: 8 warps x 16)
+constexpr int kCombTokW = 512;   // B6 with W_r^T staged in smem: 16 warps x 32 tokens per CTA
+
+// One CTA = (head h, 128 consecutive tokens); warp w takes tokens w, w+8, ...  Per token, lanes
+// 0..k-1 fetch the k row positions (and for B6 the expert ids / dS) and broadcast them by shuffle;
+// every lane then has all k 16-byte row loads of its column chunk in flight at once (KMAX-unrolled).
+// B6 keeps W_r^T of the head in shared memory when it fits (SMEM_W), so the router term reads
+// smem instead of re-fetching k rows of W_r^T from L2 per token.
+template <typename E, bool BWD, int KMAX, bool SMEM_W>
+__global__ void __launch_bounds__(SMEM_W ? 512 : 256)
 combine_kernel(const E* __restrict__ rep, const int32_t* __restrict__ pos, const int32_t* __restrict__ idx,
                const float* __restrict__ dS, const float* __restrict__ W_rT, int H, int64_t T, int k, int d_h,
                int N_e, int64_t Rp, E* __restrict__ out, int64_t ldo) {
   constexpr int V = Vec<E>::N;
-  const int64_t pair = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
-  if (pair >= T * H) return;
-  const int lane = threadIdx.x & 31;
-  const int h = (int)(pair / T);
-  const int64_t t = pair % T;
+  extern __shared__ __align__(16) float s_w[];           // [N_e][d_h] when SMEM_W
+  constexpr int NT = SMEM_W ? 512 : 256, NW = NT / 32, TOK = SMEM_W ? kCombTokW : kCombTok;
+  const int h = blockIdx.y, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t R = T * k;
-  const int32_t* ph = pos + (size_t)h * R + t * k;
+  const float* wt_h = W_rT + (size_t)h * N_e * d_h;
+  if constexpr (BWD && SMEM_W) {
+    for (int i = threadIdx.x * 4; i < N_e * d_h; i += NT * 4)
+      *reinterpret_cast<float4*>(s_w + i) = __ldg(reinterpret_cast<const float4*>(wt_h + i));
+    __syncthreads();
+  }
   const int nchunk = d_h / V;
-  for (int ch = lane; ch < nchunk; ch += 32) {
-    float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-    for (int j = 0; j < k; ++j) {
-      const E* src = rep + ((size_t)h * Rp + ph[j]) * d_h + ch * V;
-      if constexpr (V == 8) {
-        float f[8];
-        unpack(__ldg(reinterpret_cast<const uint4*>(src)), f);
-#pragma unroll
-        for (int i = 0; i < 8; ++i) acc[i] += f[i];
-      } else {
-        const float4 f = __ldg(reinterpret_cast<const float4*>(src));
-        acc[0] += f.x; acc[1] += f.y; acc[2] += f.z; acc[3] += f.w;
-      }
-    }
+  const int64_t tb = (int64_t)blockIdx.x * TOK;
+  for (int tt = warp; tt < TOK; tt += NW) {
+    const int64_t t = tb + tt;
+    if (t >= T) break;
+    const size_t rb = (size_t)h * R + t * k;
+    const int my_pos = lane < k ? pos[rb + lane] : 0;
+    int my_e = 0;
+    float my_ds = 0.f;
     if constexpr (BWD) {
-      float racc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-      const int32_t* ih = idx + (size_t)h * R + t * k;
-      const float* sh = dS + (size_t)h * R + t * k;
-      const float* wt = W_rT + (size_t)h * N_e * d_h + ch * V;
-      for (int j = 0; j < k; ++j) {
-        const float ds = sh[j];
-        const float4* w = reinterpret_cast<const float4*>(wt + (size_t)ih[j] * d_h);
-#pragma unroll
-        for (int q = 0; q < V / 4; ++q) {
-          const float4 wv = __ldg(w + q);
-          racc[4 * q + 0] = fmaf(ds, wv.x, racc[4 * q + 0]);
-          racc[4 * q + 1] = fmaf(ds, wv.y, racc[4 * q + 1]);
-          racc[4 * q + 2] = fmaf(ds, wv.z, racc[4 * q + 2]);
-          racc[4 * q + 3] = fmaf(ds, wv.w, racc[4 * q + 3]);
-        }
-      }
-#pragma unroll
-      for (int i = 0; i < V; ++i) acc[i] += racc[i];
+      if (lane < k) { my_e = idx[rb + lane]; my_ds = dS[rb + lane]; }
     }
-    E* dst = out + t * ldo + (int64_t)h * d_h + ch * V;
-    if constexpr (V == 8) {
-      *reinterpret_cast<uint4*>(dst) = pack(acc);
-    } else {
-      *reinterpret_cast<float4*>(dst) = make_float4(acc[0], acc[1], acc[2], acc[3]);
+    // all lanes take part in the broadcasts (the column loop below may leave some lanes idle)
+    int p[KMAX], ej[KMAX];
+    float dsj[KMAX];
+#pragma unroll
+    for (int j = 0; j < KMAX; ++j) {
+      p[j] = __shfl_sync(0xffffffffu, my_pos, j);
+      if constexpr (BWD) { ej[j] = __shfl_sync(0xffffffffu, my_e, j); dsj[j] = __shfl_sync(0xffffffffu, my_ds, j); }
+    }
+    for (int ch = lane; ch < nchunk; ch += 32) {
+      float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+      if constexpr (V == 8) {
+        uint4 v[KMAX];
+#pragma unroll
+        for (int j = 0; j < KMAX; ++j)
+          if (j < k) v[j] = __ldg(reinterpret_cast<const uint4*>(rep + ((size_t)h * Rp + p[j]) * d_h + ch * V));
+#pragma unroll
+        for (int j = 0; j < KMAX; ++j) {
+          if (j < k) {
+            float f[8];
+            unpack(v[j], f);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) acc[i] += f[i];
+          }
+        }
+      } else {
+        float4 v[KMAX];
+#pragma unroll
+        for (int j = 0; j < KMAX; ++j)
+          if (j < k) v[j] = __ldg(reinterpret_cast<const float4*>(rep + ((size_t)h * Rp + p[j]) * d_h + ch * V));
+#pragma unroll
+        for (int j = 0; j < KMAX; ++j)
+          if (j < k) { acc[0] += v[j].x; acc[1] += v[j].y; acc[2] += v[j].z; acc[3] += v[j].w; }
+      }
+      if constexpr (BWD) {
+        float racc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+        for (int j = 0; j < KMAX; ++j) {
+          const float ds = dsj[j];
+          const int e = ej[j];
+          if (j < k) {
+            const float* wr = (SMEM_W ? s_w : wt_h) + (size_t)e * d_h + ch * V;
+#pragma unroll
+            for (int q = 0; q < V / 4; ++q) {
+              const float4 wv = SMEM_W ? *reinterpret_cast<const float4*>(wr + 4 * q)
+                                       : __ldg(reinterpret_cast<const float4*>(wr + 4 * q));
+              racc[4 * q + 0] = fmaf(ds, wv.x, racc[4 * q + 0]);
+              racc[4 * q + 1] = fmaf(ds, wv.y, racc[4 * q + 1]);
+              racc[4 * q + 2] = fmaf(ds, wv.z, racc[4 * q + 2]);
+              racc[4 * q + 3] = fmaf(ds, wv.w, racc[4 * q + 3]);
+            }
+          }
+        }
+#pragma unroll
+        for (int i = 0; i < V; ++i) acc[i] += racc[i];
+      }
+      E* dst = out + t * ldo + (int64_t)h * d_h + ch * V;
+      if constexpr (V == 8) {
+        *reinterpret_cast<uint4*>(dst) = pack(acc);
+      } else {
+        *reinterpret_cast<float4*>(dst) = make_float4(acc[0], acc[1], acc[2], acc[3]);
+      }
     }
   }
+}
+
+template <typename E, bool BWD, bool SMEM_W>
+void launch_kw(const Routing& rt, const E* rep, const float* dS, const float* W_rT, int d_h, E* out, int64_t ldo,
+               cudaStream_t s) {
+  const int tok = SMEM_W ? kCombTokW : kCombTok;
+  const dim3 grid((unsigned)((rt.T + tok - 1) / tok), (unsigned)rt.H);
+  const size_t smem = SMEM_W ? (size_t)rt.N_e * d_h * 4 : 0;
+#define MHL_CK(KM)                                                                                          \
+  {                                                                                                         \
+    auto f = combine_kernel<E, BWD, KM, SMEM_W>;                                                            \
+    if (smem > 48 * 1024) cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);  \
+    f<<<grid, SMEM_W ? 512 : 256, smem, s>>>(rep, rt.pos, rt.idx, dS, W_rT, rt.H, rt.T, rt.k, d_h, rt.N_e, rt.Rp, out, ldo); \
+  }
+  if (rt.k <= 2) MHL_CK(2) else if (rt.k <= 4) MHL_CK(4) else if (rt.k <= 8) MHL_CK(8) else MHL_CK(16)
+#undef MHL_CK
 }
 
 }  // namespace
 
 void launch_combine_fwd(int dtype, const Routing& rt, const void* Yrep, int d_h, void* out, int64_t ldo,
                         cudaStream_t s) {
-  const unsigned blocks = (unsigned)((rt.T * rt.H + 7) / 8);
+  if (rt.T <= 0) return;
   if (dtype == 1)
-    combine_kernel<bf16, false><<<blocks, 256, 0, s>>>((const bf16*)Yrep, rt.pos, nullptr, nullptr, nullptr, rt.H, rt.T,
-                                                       rt.k, d_h, 0, rt.Rp, (bf16*)out, ldo);
+    launch_kw<bf16, false, false>(rt, (const bf16*)Yrep, nullptr, nullptr, d_h, (bf16*)out, ldo, s);
   else
-    combine_kernel<float, false><<<blocks, 256, 0, s>>>((const float*)Yrep, rt.pos, nullptr, nullptr, nullptr, rt.H,
-                                                        rt.T, rt.k, d_h, 0, rt.Rp, (float*)out, ldo);
+    launch_kw<float, false, false>(rt, (const float*)Yrep, nullptr, nullptr, d_h, (float*)out, ldo, s);
 }
 
 void launch_combine_bwd(int dtype, const Routing& rt, const void* dXrep, const float* dS, const float* W_rT, int d_h,
                         void* out, int64_t ldo, cudaStream_t s) {
-  const unsigned blocks = (unsigned)((rt.T * rt.H + 7) / 8);
-  if (dtype == 1)
-    combine_kernel<bf16, true><<<blocks, 256, 0, s>>>((const bf16*)dXrep, rt.pos, rt.idx, dS, W_rT, rt.H, rt.T, rt.k,
-                                                      d_h, rt.N_e, rt.Rp, (bf16*)out, ldo);
-  else
-    combine_kernel<float, true><<<blocks, 256, 0, s>>>((const float*)dXrep, rt.pos, rt.idx, dS, W_rT, rt.H, rt.T,
-                                                       rt.k, d_h, rt.N_e, rt.Rp, (float*)out, ldo);
+  if (rt.T <= 0) return;
+  const bool smem_w = (size_t)rt.N_e * d_h * 4 <= 96 * 1024;
+  if (dtype == 1) {
+    if (smem_w) launch_kw<bf16, true, true>(rt, (const bf16*)dXrep, dS, W_rT, d_h, (bf16*)out, ldo, s);
+    else launch_kw<bf16, true, false>(rt, (const bf16*)dXrep, dS, W_rT, d_h, (bf16*)out, ldo, s);
+  } else {
+    if (smem_w) launch_kw<float, true, true>(rt, (const float*)dXrep, dS, W_rT, d_h, (float*)out, ldo, s);
+    else launch_kw<float, true, false>(rt, (const float*)dXrep, dS, W_rT, d_h, (float*)out, ldo, s);
+  }
 }
 
 }  // namespace mhl
