@@ -9,8 +9,9 @@
 // the raw scores (R4) and emit the per-tile expert histogram for clustering (F4).
 //
 // Warp roles: warp 0 = TMA producer (X tiles in 64-column K-chunks through an smem ring, W planes
-// once per head), warp 1 = MMA issuer (+ TMEM owner), warps 2-5 = epilogue.  The TMEM accumulator
-// is double-buffered so the epilogue of tile i overlaps the MMAs of tile i+1.
+// once per head), warp 1 = MMA issuer (+ TMEM owner), warps 2.. = epilogue.  The TMEM accumulator
+// holds kNB = 2*kEG buffers: kEG epilogue warpgroups each work on their own tile while the MMAs of
+// later tiles proceed (the top-k is ALU-bound; one warpgroup left the ALU pipe half idle).
 #include <cuda.h>
 
 #include "kernels.h"
@@ -24,23 +25,28 @@ namespace {
 using namespace sm100;
 
 constexpr int RT = kRouterTile;   // 128 tokens = MMA M
-constexpr int kThreads = 192;
+constexpr int kEG = 3;            // epilogue warpgroups (each owns every kEG-th tile of the CTA)
+constexpr int kThreads = (2 + 4 * kEG) * 32;
 constexpr int kChunkBytes = RT * 128;   // one 64-column K-chunk of the X tile
 
 template <int DH, int NE>
 struct RSmem {
+  static constexpr int kNB = (2 * kEG * NE <= 512) ? 2 * kEG : 512 / NE;   // TMEM accumulator buffers
+  static_assert(kNB >= kEG, "router: fewer TMEM buffers than epilogue warpgroups");
   static constexpr int W = 0;                                   // [3][DH/64][NE][64] SW128
   static constexpr int WBYTES = 3 * NE * DH * 2;
   static constexpr int RING = WBYTES;                           // X chunks
   static constexpr int STAGES_RAW = (225 * 1024 - WBYTES) / kChunkBytes;
   static constexpr int STAGES = STAGES_RAW > 8 ? 8 : STAGES_RAW;
-  static constexpr int BAR = RING + STAGES * kChunkBytes;       // full[S], empty[S], wfull, wfree, tfull[2], tempty[2]
-  static constexpr int NBAR = 2 * STAGES + 6;
-  static constexpr int BIAS = BAR + NBAR * 8;
-  static constexpr int HIST = BIAS + NE * 4;
-  static constexpr int TMEMP = HIST + NE * 4;
+  static constexpr int BAR = RING + STAGES * kChunkBytes;       // full[S], empty[S], wfull, wfree, tfull[NB], tempty[NB]
+  static constexpr int NBAR = 2 * STAGES + 2 + 2 * kNB;
+  static constexpr int BIAS = BAR + NBAR * 8;                   // [kEG][NE]
+  static constexpr int HIST = BIAS + kEG * NE * 4;              // [kEG][NE]
+  static constexpr int TMEMP = HIST + kEG * NE * 4;
   static constexpr int BYTES = TMEMP + 16;
-  static constexpr int TMEM_COLS = (2 * NE <= 32) ? 32 : (2 * NE <= 64) ? 64 : (2 * NE <= 128) ? 128 : (2 * NE <= 256) ? 256 : 512;
+  static constexpr int TMEM_COLS = (kNB * NE <= 32) ? 32 : (kNB * NE <= 64) ? 64 : (kNB * NE <= 128) ? 128
+                                   : (kNB * NE <= 256) ? 256 : 512;
+
 };
 
 template <int DH, int NE, int KMAX>
@@ -60,7 +66,8 @@ router_sm100_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_const
   uint64_t* wfull = bars + 2 * S;
   uint64_t* wfree = wfull + 1;
   uint64_t* tfull = wfull + 2;
-  uint64_t* tempty = wfull + 4;
+  constexpr int kNB = L::kNB;
+  uint64_t* tempty = tfull + kNB;
   float* s_bias = reinterpret_cast<float*>(smem + L::BIAS);
   int* s_hist = reinterpret_cast<int*>(smem + L::HIST);
   uint32_t* s_tmem = reinterpret_cast<uint32_t*>(smem + L::TMEMP);
@@ -74,12 +81,12 @@ router_sm100_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_const
   if (tid == 0) {
     for (int i = 0; i < S; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], 1); }
     mbar_init(wfull, 1); mbar_init(wfree, 1);
-    for (int i = 0; i < 2; ++i) { mbar_init(&tfull[i], 1); mbar_init(&tempty[i], 128); }
+    for (int i = 0; i < kNB; ++i) { mbar_init(&tfull[i], 1); mbar_init(&tempty[i], 128); }
     fence_mbar_init();
     tma_prefetch_desc(&xmap); tma_prefetch_desc(&wmap);
   }
   if (warp == 1) tmem_alloc<L::TMEM_COLS>(s_tmem);
-  for (int i = tid; i < NE; i += kThreads) s_hist[i] = 0;
+  for (int i = tid; i < kEG * NE; i += kThreads) s_hist[i] = 0;
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -113,13 +120,12 @@ router_sm100_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_const
     if (lane == 0) {
       constexpr uint32_t IDESC = idesc_bf16(128, NE, 0, 0);
       int stage = 0; uint32_t ph = 0, wph = 0;
-      uint32_t tph[2] = {0, 0};
       int cur_h = -1, n = 0;
       for (int ti = tb; ti < te; ++ti, ++n) {
         const int h = ti / n_rt;
         if (h != cur_h) { mbar_wait(wfull, wph); wph ^= 1; cur_h = h; }
-        const int acc = n & 1;
-        mbar_wait(&tempty[acc], tph[acc] ^ 1); tph[acc] ^= 1;
+        const int acc = n % kNB;
+        mbar_wait(&tempty[acc], ((n / kNB) & 1) ^ 1);
         tc_fence_after();
         const uint32_t d = tmem + acc * NE;
         for (int kb = 0; kb < KB; ++kb) {
@@ -142,23 +148,25 @@ router_sm100_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_const
       }
     }
   } else {
-    // ============================ epilogue: 4 warps, thread = token row
-    const int q = warp & 3;
+    // ============================ epilogue: kEG warpgroups of 4 warps, thread = token row;
+    // warpgroup g takes the CTA's tiles n = g, g + kEG, ... (accumulator buffer n % kNB)
+    const int q = warp & 3, g = (warp - 2) >> 2;
     const int row = q * 32 + lane;
-    const int et = tid - 64;                    // 0..127
-    uint32_t tph[2] = {0, 0};
-    int cur_h = -1, n = 0;
+    const int et = (tid - 64) & 127;            // 0..127 within the warpgroup
+    float* s_bias_g = s_bias + g * NE;
+    int* s_hist_g = s_hist + g * NE;
+    int cur_h = -1;
     bool bad = false;
-    for (int ti = tb; ti < te; ++ti, ++n) {
+    for (int ti = tb + g, n = g; ti < te; ti += kEG, n += kEG) {
       const int h = ti / n_rt, rt = ti % n_rt;
       if (h != cur_h) {
-        named_bar_sync(1, 128);
-        for (int i = et; i < NE; i += 128) s_bias[i] = bias[(size_t)h * NE + i];
-        named_bar_sync(1, 128);
+        named_bar_sync(1 + g, 128);
+        for (int i = et; i < NE; i += 128) s_bias_g[i] = bias[(size_t)h * NE + i];
+        named_bar_sync(1 + g, 128);
         cur_h = h;
       }
-      const int acc = n & 1;
-      mbar_wait(&tfull[acc], tph[acc]); tph[acc] ^= 1;
+      const int acc = n % kNB;
+      mbar_wait(&tfull[acc], (n / kNB) & 1);
       tc_fence_after();
       // Running top-k on float keys.  Experts are visited in increasing index order and a new
       // key displaces a slot only if STRICTLY greater, so equal keys keep the lower index first:
@@ -177,7 +185,7 @@ router_sm100_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_const
 #pragma unroll
         for (int j = 0; j < 32; ++j) {
           const float s = __uint_as_float(v[j]);
-          float kf = s + s_bias[c0 + j];
+          float kf = s + s_bias_g[c0 + j];
           chk = fmaf(kf, 0.f, chk);
           if (kf > key[KMAX - 1]) {
             float sv = s;
@@ -213,14 +221,14 @@ router_sm100_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_const
             const int e = kid[j];
             io[j] = e;
             go[j] = ex[j] * inv;
-            atomicAdd(&s_hist[e], 1);
+            atomicAdd(&s_hist_g[e], 1);
           }
         }
       }
-      named_bar_sync(1, 128);
+      named_bar_sync(1 + g, 128);
       int32_t* ho = hist + ((size_t)h * n_rt + rt) * NE;
-      for (int i = et; i < NE; i += 128) { ho[i] = s_hist[i]; s_hist[i] = 0; }
-      named_bar_sync(1, 128);
+      for (int i = et; i < NE; i += 128) { ho[i] = s_hist_g[i]; s_hist_g[i] = 0; }
+      named_bar_sync(1 + g, 128);
     }
     if (bad) *flag = 1;
   }
