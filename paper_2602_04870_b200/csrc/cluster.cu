@@ -178,30 +178,50 @@ tiles_kernel(const int32_t* __restrict__ counts, const int32_t* __restrict__ off
   }
 }
 
-// (3) per (h, router tile): stable ranks inside the tile via warp match, scatter perm/pos/tok/gate
-__global__ void __launch_bounds__(32)
+// (3) per (h, router tile), 8 warps: warp w owns a contiguous run of the tile's replicas.
+// Pass 1 counts each warp's replicas per expert (warp match, no atomics); a per-expert scan over
+// the warps gives every warp its stable starting rank; pass 2 recomputes the in-warp ranks and
+// scatters perm/pos/tok/gate.  Replica order is preserved within every expert (stable sort).
+constexpr int kScatterWarps = 8;
+__global__ void __launch_bounds__(kScatterWarps * 32)
 scatter_kernel(const int32_t* __restrict__ idx, const float* __restrict__ gate, const int32_t* __restrict__ off,
                const int32_t* __restrict__ tilepref, int32_t* __restrict__ perm, int32_t* __restrict__ pos,
                int32_t* __restrict__ tok_s, float* __restrict__ gate_s, int64_t T, int k, int N_e, int n_rt,
                int64_t Rp) {
-  extern __shared__ int cnt[];
-  const int tt = blockIdx.x, h = blockIdx.y, lane = threadIdx.x;
-  for (int e = lane; e < N_e; e += 32) cnt[e] = 0;
-  __syncwarp();
+  extern __shared__ int wcnt[];                       // [kScatterWarps][N_e]
+  const int tt = blockIdx.x, h = blockIdx.y, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int i = threadIdx.x; i < kScatterWarps * N_e; i += blockDim.x) wcnt[i] = 0;
+  __syncthreads();
   const int64_t r0 = (int64_t)tt * kRouterTile * k;
   const int64_t r1 = min((int64_t)(tt + 1) * kRouterTile, T) * k;
+  const int64_t per = ((r1 - r0 + kScatterWarps - 1) / kScatterWarps + 31) / 32 * 32;
+  const int64_t w0 = r0 + warp * per, w1 = min(r1, w0 + per);
   const int32_t* idx_h = idx + (size_t)h * T * k;
   const float* gate_h = gate + (size_t)h * T * k;
+  int* my = wcnt + warp * N_e;
+  for (int64_t base = w0; base < w1; base += 32) {
+    const int64_t r = base + lane;
+    const bool act = r < w1;
+    const int e = act ? idx_h[r] : -1 - lane;   // unique dummy per inactive lane
+    const unsigned mask = __match_any_sync(0xffffffffu, e);
+    if (act && __popc(mask & ((1u << lane) - 1u)) == 0) my[e] += __popc(mask);
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < N_e; e += blockDim.x) {
+    int run = 0;
+    for (int w = 0; w < kScatterWarps; ++w) { const int c = wcnt[w * N_e + e]; wcnt[w * N_e + e] = run; run += c; }
+  }
+  __syncthreads();
   const int32_t* offh = off + (size_t)h * (N_e + 1);
   const int32_t* pre = tilepref + ((size_t)h * n_rt + tt) * N_e;
-  for (int64_t base = r0; base < r1; base += 32) {
+  for (int64_t base = w0; base < w1; base += 32) {
     const int64_t r = base + lane;
-    const bool act = r < r1;
-    const int e = act ? idx_h[r] : -1 - lane;   // unique dummy per inactive lane
+    const bool act = r < w1;
+    const int e = act ? idx_h[r] : -1 - lane;
     const unsigned mask = __match_any_sync(0xffffffffu, e);
     const int rank = __popc(mask & ((1u << lane) - 1u));
     if (act) {
-      const int p = offh[e] + pre[e] + cnt[e] + rank;
+      const int p = offh[e] + pre[e] + my[e] + rank;
       const size_t q = (size_t)h * Rp + p;
       perm[q] = (int32_t)r;
       tok_s[q] = (int32_t)(r / k);
@@ -209,7 +229,7 @@ scatter_kernel(const int32_t* __restrict__ idx, const float* __restrict__ gate, 
       pos[(size_t)h * T * k + r] = p;
     }
     __syncwarp();
-    if (act && rank == 0) cnt[e] += __popc(mask);
+    if (act && rank == 0) my[e] += __popc(mask);
     __syncwarp();
   }
 }
@@ -227,8 +247,8 @@ void launch_cluster(int H, int64_t T, int k, int N_e, const int32_t* idx, const 
   offsets_kernel<<<1, 1024, 0, s>>>(counts, off, tbase, ntiles, H, N_e, max_tiles, nchunks, cbase, ccount, max_chunks);
   tiles_kernel<<<(H * N_e + 127) / 128, 128, 0, s>>>(counts, off, tbase, tiles, max_tiles, chunks, cbase, max_chunks, H,
                                                      N_e, Rp, perm, tok_s, gate_s, (int)T);
-  scatter_kernel<<<dim3(n_rt, H), 32, sizeof(int) * N_e, s>>>(idx, gate, off, tilepref, perm, pos, tok_s, gate_s, T, k,
-                                                              N_e, n_rt, Rp);
+  scatter_kernel<<<dim3(n_rt, H), kScatterWarps * 32, sizeof(int) * kScatterWarps * N_e, s>>>(
+      idx, gate, off, tilepref, perm, pos, tok_s, gate_s, T, k, N_e, n_rt, Rp);
 }
 
 }  // namespace mhl
