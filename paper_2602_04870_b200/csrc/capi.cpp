@@ -118,7 +118,7 @@ struct Bump {
 struct SavedLayout { size_t Xs, idx, gate, perm, tok_s, gate_s, pos, off, tiles, ntiles, chunks, nchunks, cbase, ccount, cat, total; };
 // offsets inside one rank's workspace region (forward and backward alias each other)
 struct FwdLayout { size_t send1, Yrep, send2, recv2, hist, tilepref, counts, planes, total; };
-struct BwdLayout { size_t send3, dY, dXrep, dg, dS, dH, gA, dwr_part, W_rT, send4, recv4, dXs, dw_part, total; };
+struct BwdLayout { size_t send3, dY, dXrep, dg, dS, dH, gA, dwr_part, W_rT, send4, recv4, dXs, dw_part, dw_done, total; };
 
 SavedLayout saved_layout(const Dims& m) {
   Bump b; SavedLayout L;
@@ -170,6 +170,7 @@ BwdLayout bwd_layout(const Dims& m) {
   L.recv4 = b.take(m.G > 1 ? (size_t)m.T_loc * m.D * m.el : 0);
   L.dXs = b.take((size_t)m.T_loc * m.D * m.el);
   L.dw_part = b.take(m.simt ? 0 : (size_t)m.max_chunks * 2 * m.d_e * m.d_h * 4);
+  L.dw_done = b.take((size_t)m.H * m.N_e * 4);
   L.total = b.off;
   return L;
 }
@@ -459,7 +460,7 @@ mhl_status moe_backward_local(mhl_plan p, const RankPtrs& R, const void* dY, voi
     MHL_SPAN("B5_expert_bwd_dx");
     if (tc)
       mhl::launch_expert_bwd_sm100(rt, Xs, m.HD, dY, m.HD, R.W1, R.W2, m.d_h, m.d_e, dXrep, dg, dH, gA, nullptr,
-                                   nullptr, nullptr, p->num_sms, s, true, false);
+                                   nullptr, nullptr, nullptr, p->num_sms, s, true, false);
     else
       mhl::launch_expert_bwd_simt(m.dtype, rt, Xs, m.HD, dY, m.HD, R.W1, R.W2, m.d_h, m.d_e, dXrep, dg, dH, gA, s);
   }
@@ -472,7 +473,8 @@ mhl_status moe_backward_local(mhl_plan p, const RankPtrs& R, const void* dY, voi
     MHL_SPAN("B5_expert_bwd_dw");
     if (tc)
       mhl::launch_expert_bwd_sm100(rt, Xs, m.HD, dY, m.HD, R.W1, R.W2, m.d_h, m.d_e, dXrep, dg, dH, gA,
-                                   (float*)(R.ws + B.dw_part), R.dW1, R.dW2, p->num_sms, s, false, true);
+                                   (float*)(R.ws + B.dw_part), (int*)(R.ws + B.dw_done), R.dW1, R.dW2,
+                                   p->num_sms, s, false, true);
     else
       mhl::launch_expert_dw_simt(m.dtype, rt, Xs, m.HD, dY, m.HD, dH, gA, m.d_h, m.d_e, R.dW1, R.dW2, s);
   }
@@ -496,8 +498,8 @@ mhl_status moe_backward_local(mhl_plan p, const RankPtrs& R, const void* dY, voi
     MHL_SPAN("B6_combine_bwd");
     mhl::launch_combine_bwd(m.dtype, rt, dXrep, dS, W_rT, m.d_h, dxout, m.HD, s);
   }
-  // K1 + K2 + dW + dW reduce + router (2) + transpose + combine on the tensor-core path
-  p->launches += tc ? 8 : (R.dW1 || R.dW2 ? 6 : 5);
+  // K1 + K2 + dW (+ its in-kernel reduce) + router (2) + transpose + combine on the tensor-core path
+  p->launches += tc ? 7 : (R.dW1 || R.dW2 ? 6 : 5);
   return check_kernels(p);
 }
 

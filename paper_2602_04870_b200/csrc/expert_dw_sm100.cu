@@ -3,8 +3,8 @@
 // Chain rule of y_r = g_r * gelu(x W1_e^T) W2_e over the clustered replicas of one expert
 // (Eq. 1): with dH = g dA' gelu'(H) and gA = g gelu(H) from expert_bwd_dx_sm100.cu,
 //   dW1_e^T = X^T dH,   dW2_e^T = dY^T gA        (X, dY = sub-token / dcat rows of the replicas)
-// per chunk of <= kDwChunk sorted rows (tcgen05, both operands MN-major), no atomics; then an
-// ordered reduction over the expert's chunks (deterministic, R21).
+// per chunk of <= kDwChunk sorted rows (tcgen05, both operands MN-major) into fp32 partials; the
+// CTA finishing an expert's last chunk sums its partials in chunk order (deterministic, R21).
 #include <cuda.h>
 
 #include "kernels.h"
@@ -39,7 +39,8 @@ struct DwSmem {
   static constexpr int X = 0, DY = XB, DHH = 2 * XB, GA = 2 * XB + EB;
   static constexpr int S = 2;
   static constexpr int BAR = S * STAGE;            // full[S], empty[S], accfull, accempty
-  static constexpr int TMEM = BAR + 8 * (2 * S + 2);
+  static constexpr int LAST = BAR + 8 * (2 * S + 2);            // int: "this CTA reduces the expert"
+  static constexpr int TMEM = LAST + 16;
   static constexpr int BYTES = TMEM + 16;
 };
 
@@ -47,7 +48,8 @@ template <int DH, int DE>
 __global__ void __launch_bounds__(kDwThreads, 1)
 expert_dw_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap ymap,
                  const __grid_constant__ CUtensorMap hmap, const __grid_constant__ CUtensorMap amap, Routing rt,
-                 float* __restrict__ partial) {
+                 float* __restrict__ partial, int* __restrict__ done, float* __restrict__ dW1,
+                 float* __restrict__ dW2) {
   const Tile* chunks = rt.chunks;
   const int64_t Rp = rt.Rp;
   using L = DwSmem<DH, DE>;
@@ -145,7 +147,22 @@ expert_dw_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant
     }
   } else if (warp >= kDwFlush0 && warp < kDwFlush0 + 8) {
     // ================================================================ flush: partial[ci][mat][f][c]
+    // Each chunk's accumulators go to its partial slot; the CTA that flushes an expert's LAST chunk
+    // (counted with one atomic per chunk) then sums that expert's partials in chunk order and
+    // writes dW1/dW2 — the same order as a separate reduction pass, without its launch and
+    // re-read, and overlapped with the next chunk's MMAs.
     const int q = warp & 3, wm = (warp - kDwFlush0) >> 2;   // lane quadrant; 0: dW1, 1: dW2
+    const int ft = tid - kDwFlush0 * 32;                    // 0..255
+    constexpr int DEDH = DE * DH;
+    int* s_last = reinterpret_cast<int*>(smem + L::LAST);
+    static_assert(DEDH % (4 * 256 * 4) == 0, "dW reduce tiling");
+    // experts without rows have no chunk: their gradients are zero
+    for (int he = blockIdx.x; he < rt.H * rt.N_e; he += gridDim.x)
+      if (rt.ccount[he] == 0)
+        for (int i = ft; i < DEDH; i += 256) {
+          if (dW1) dW1[(size_t)he * DEDH + i] = 0.f;
+          if (dW2) dW2[(size_t)he * DEDH + i] = 0.f;
+        }
     int nc = 0;
     for (int ci = blockIdx.x; ci < nchunks; ci += gridDim.x, ++nc) {
       mbar_wait_warp(accfull, nc & 1);
@@ -163,6 +180,43 @@ expert_dw_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant
       }
       tc_fence_before();
       mbar_arrive(accempty);
+      if (dW1 == nullptr && dW2 == nullptr) continue;
+      __threadfence();
+      named_bar_sync(1, 256);
+      const Tile ch = chunks[ci];
+      const int he = ch.head * rt.N_e + ch.expert;
+      if (ft == 0) *s_last = (atomicAdd(&done[he], 1) == rt.ccount[he] - 1);
+      named_bar_sync(1, 256);
+      if (*s_last) {
+        __threadfence();
+        const int b0 = rt.cbase[he], n = rt.ccount[he];
+        constexpr int U = 4;                              // float4s per thread in flight per matrix
+        const float4* p4 = reinterpret_cast<const float4*>(partial);
+        for (int i0 = ft; i0 < DEDH / 4; i0 += 256 * U) {
+          float4 a1[U], a2[U];
+#pragma unroll
+          for (int u = 0; u < U; ++u) { a1[u] = make_float4(0.f, 0.f, 0.f, 0.f); a2[u] = a1[u]; }
+          for (int c = 0; c < n; ++c) {
+            const float4* s1 = p4 + ((size_t)(b0 + c) * 2 + 0) * (DEDH / 4);
+            const float4* s2 = p4 + ((size_t)(b0 + c) * 2 + 1) * (DEDH / 4);
+            float4 v1[U], v2[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) { v1[u] = __ldcg(s1 + i0 + 256 * u); v2[u] = __ldcg(s2 + i0 + 256 * u); }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+              a1[u].x += v1[u].x; a1[u].y += v1[u].y; a1[u].z += v1[u].z; a1[u].w += v1[u].w;
+              a2[u].x += v2[u].x; a2[u].y += v2[u].y; a2[u].z += v2[u].z; a2[u].w += v2[u].w;
+            }
+          }
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            if (dW1) reinterpret_cast<float4*>(dW1 + (size_t)he * DEDH)[i0 + 256 * u] = a1[u];
+            if (dW2) reinterpret_cast<float4*>(dW2 + (size_t)he * DEDH)[i0 + 256 * u] = a2[u];
+          }
+        }
+        if (ft == 0) done[he] = 0;   // ready for the next call
+      }
+      named_bar_sync(1, 256);
     }
   }
   tc_fence_before();
@@ -170,28 +224,9 @@ expert_dw_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant
   if (warp == kDwMma) tmem_dealloc<512>(tmem);
 }
 
-// dW[h][e][f][c] = sum over the expert's chunks, in chunk order (deterministic); 0 if unused
-__global__ void __launch_bounds__(256)
-dw_reduce_kernel(const float* __restrict__ partial, const int32_t* __restrict__ cbase,
-                 const int32_t* __restrict__ ccount, int N_e, int DEDH, float* __restrict__ dW1,
-                 float* __restrict__ dW2) {
-  const int e = blockIdx.y, h = blockIdx.z;
-  const int he = h * N_e + e;
-  const int b = cbase[he], n = ccount[he];
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < DEDH; i += gridDim.x * blockDim.x) {
-    float a1 = 0.f, a2 = 0.f;
-    for (int c = 0; c < n; ++c) {
-      a1 += partial[((size_t)(b + c) * 2 + 0) * DEDH + i];
-      a2 += partial[((size_t)(b + c) * 2 + 1) * DEDH + i];
-    }
-    if (dW1) dW1[(size_t)he * DEDH + i] = a1;
-    if (dW2) dW2[(size_t)he * DEDH + i] = a2;
-  }
-}
-
 template <int DH, int DE>
 bool launch_dw_t(const Routing& rt, const void* Xs, int64_t ldx, const void* dY, int64_t ldy, const void* dH,
-                 const void* gA, float* partial, int num_sms, cudaStream_t s) {
+                 const void* gA, float* partial, int* done, float* dW1, float* dW2, int num_sms, cudaStream_t s) {
   CUtensorMap xm, ym, hm, am;
   const uint64_t rows = (uint64_t)rt.H * rt.Rp;
   if (!make_tmap_2d_bf16(&xm, Xs, (uint64_t)rt.T + 1, (uint64_t)rt.H * DH, (uint64_t)ldx * 2, 1, 64)) return false;
@@ -200,7 +235,8 @@ bool launch_dw_t(const Routing& rt, const void* Xs, int64_t ldx, const void* dY,
   if (!make_tmap_2d_bf16(&am, gA, rows, DE, (uint64_t)DE * 2, kHalf, 64)) return false;
   auto kern = expert_dw_kernel<DH, DE>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, DwSmem<DH, DE>::BYTES);
-  kern<<<num_sms, kDwThreads, DwSmem<DH, DE>::BYTES, s>>>(xm, ym, hm, am, rt, partial);
+  cudaMemsetAsync(done, 0, (size_t)rt.H * rt.N_e * sizeof(int), s);
+  kern<<<num_sms, kDwThreads, DwSmem<DH, DE>::BYTES, s>>>(xm, ym, hm, am, rt, partial, done, dW1, dW2);
   return true;
 }
 
@@ -213,8 +249,8 @@ bool expert_bwd_sm100_supported(int d_h, int d_e) {
 
 bool launch_expert_bwd_sm100(const Routing& rt, const void* Xs, int64_t ldx, const void* dY, int64_t ldy,
                              const void* W1, const void* W2, int d_h, int d_e, void* dXrep, float* dg, void* dH,
-                             void* gA, float* partial, float* dW1, float* dW2, int num_sms, cudaStream_t s,
-                             bool do_dx, bool do_dw) {
+                             void* gA, float* partial, int* done, float* dW1, float* dW2, int num_sms,
+                             cudaStream_t s, bool do_dx, bool do_dw) {
   bool ok = false;
 #define MHL_BWD_CASE(A, B)                                                                                       \
   if (d_h == A && d_e == B) {                                                                                    \
@@ -222,15 +258,10 @@ bool launch_expert_bwd_sm100(const Routing& rt, const void* Xs, int64_t ldx, con
     if (do_dx && !launch_expert_bwd_dx_sm100(rt, Xs, ldx, dY, ldy, W1, W2, d_h, d_e, dXrep, dg, dH, gA,       \
                                              num_sms, s))                                                        \
       ok = false;                                                                                                \
-    if (do_dw && !launch_dw_t<A, B>(rt, Xs, ldx, dY, ldy, dH, gA, partial, num_sms, s)) ok = false;             \
+    if (do_dw && !launch_dw_t<A, B>(rt, Xs, ldx, dY, ldy, dH, gA, partial, done, dW1, dW2, num_sms, s)) ok = false; \
   }
   MHL_BWD_CASE(256, 128) else MHL_BWD_CASE(256, 64) else MHL_BWD_CASE(128, 128) else MHL_BWD_CASE(128, 64)
 #undef MHL_BWD_CASE
-  if (ok && do_dw && (dW1 || dW2)) {
-    const int dedh = d_e * d_h;
-    dw_reduce_kernel<<<dim3((dedh + 255) / 256, rt.N_e, rt.H), 256, 0, s>>>(partial, rt.cbase, rt.ccount, rt.N_e, dedh,
-                                                                            dW1, dW2);
-  }
   return ok;
 }
 

@@ -80,11 +80,12 @@ bool launch_expert_bwd_dx_sm100(const Routing& rt, const void* Xs, int64_t ldx, 
 // dXrep = dH W1_e per expert tile (TMA-fed grouped GEMM, expert_bwd_dx_sm100.cu)
 bool launch_expert_dx_gemm_sm100(const Routing& rt, const void* W1, int d_h, int d_e, const void* dH, void* dXrep,
                                  int num_sms, cudaStream_t s);
-// tcgen05 dX kernel (dXrep, dg, dH, gA) and/or dW kernel (chunk partials + ordered reduce)
+// tcgen05 dX kernel (dXrep, dg, dH, gA) and/or dW kernel (chunk partials + in-kernel ordered
+// reduce; `done` = H*N_e int counters, zeroed by the launch)
 bool launch_expert_bwd_sm100(const Routing& rt, const void* Xs, int64_t ldx, const void* dY, int64_t ldy,
                              const void* W1, const void* W2, int d_h, int d_e, void* dXrep, float* dg, void* dH,
-                             void* gA, float* partial, float* dW1, float* dW2, int num_sms, cudaStream_t s,
-                             bool do_dx, bool do_dw);
+                             void* gA, float* partial, int* done, float* dW1, float* dW2, int num_sms,
+                             cudaStream_t s, bool do_dx, bool do_dw);
 
 // ---- B3: dS = g (dg - sum g dg); dW_r partials per 128-token chunk; then ordered reduce.
 void launch_router_bwd(int dtype, const void* Xs, int64_t ldx, const int32_t* idx, const float* gate,
