@@ -247,6 +247,10 @@ struct mhl_plan_s {
   ncclComm_t comm = nullptr;
   int32_t* dflag = nullptr;   // device non-finite flag
   int num_sms = 148;
+  // host-buffer step (mhlmoe_train_step_host): side stream for the copies that can overlap compute
+  cudaStream_t copy_stream = nullptr;
+  cudaEvent_t ev_dout = nullptr, ev_fwd = nullptr, ev_out = nullptr, ev_bwd = nullptr;
+  bool ev_bwd_live = false, ev_out_live = false;
   std::atomic<uint64_t> launches{0};
   uint64_t a2a_bytes_posted = 0;
   // optional per-step CUDA-event timing (mhl_set_step_timing)
@@ -613,6 +617,9 @@ mhl_status hp_plan_destroy(mhl_plan p) {
   if (p->blas) cublasDestroy(p->blas);
   if (p->blas_ws) cudaFree(p->blas_ws);
   if (p->dflag) cudaFree(p->dflag);
+  for (cudaEvent_t e : {p->ev_dout, p->ev_fwd, p->ev_out, p->ev_bwd})
+    if (e) cudaEventDestroy(e);
+  if (p->copy_stream) cudaStreamDestroy(p->copy_stream);
   for (auto e : p->pool) cudaEventDestroy(e);
   delete p;
   return MHL_OK;
@@ -771,12 +778,31 @@ mhl_status mhlmoe_train_step_host(mhl_plan p, const void* x_host, const void* do
   char* dd = xd + a;
   char* od = dd + a;
   char* gd = od + a;
+  // Copies that do not feed the next kernel ride a side stream: d_out's upload overlaps the
+  // forward, out's download overlaps the backward (H2D and D2H use separate link directions).
+  if (!p->copy_stream) {
+    MHL_CUDA(cudaStreamCreateWithFlags(&p->copy_stream, cudaStreamNonBlocking));
+    for (cudaEvent_t* e : {&p->ev_dout, &p->ev_fwd, &p->ev_out, &p->ev_bwd})
+      MHL_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+  }
+  cudaStream_t cs = p->copy_stream;
   MHL_CUDA(cudaMemcpyAsync(xd, x_host, n, cudaMemcpyHostToDevice, s));
-  MHL_CUDA(cudaMemcpyAsync(dd, dout_host, n, cudaMemcpyHostToDevice, s));
+  if (p->ev_bwd_live) MHL_CUDA(cudaStreamWaitEvent(cs, p->ev_bwd, 0));   // previous backward read dd
+  MHL_CUDA(cudaMemcpyAsync(dd, dout_host, n, cudaMemcpyHostToDevice, cs));
+  MHL_CUDA(cudaEventRecord(p->ev_dout, cs));
+  if (p->ev_out_live) MHL_CUDA(cudaStreamWaitEvent(s, p->ev_out, 0));    // previous download of od
   MHL_TRY(mhlmoe_forward(p, xd, w, od, saved, workspace, workspace_bytes, nullptr, nullptr, stream));
+  MHL_CUDA(cudaEventRecord(p->ev_fwd, s));
+  MHL_CUDA(cudaStreamWaitEvent(cs, p->ev_fwd, 0));
+  MHL_CUDA(cudaMemcpyAsync(out_host, od, n, cudaMemcpyDeviceToHost, cs));
+  MHL_CUDA(cudaEventRecord(p->ev_out, cs));
+  p->ev_out_live = true;
+  MHL_CUDA(cudaStreamWaitEvent(s, p->ev_dout, 0));
   MHL_TRY(mhlmoe_backward(p, xd, w, dd, saved, gd, grads, workspace, workspace_bytes, stream));
-  MHL_CUDA(cudaMemcpyAsync(out_host, od, n, cudaMemcpyDeviceToHost, s));
+  MHL_CUDA(cudaEventRecord(p->ev_bwd, s));
+  p->ev_bwd_live = true;
   MHL_CUDA(cudaMemcpyAsync(dx_host, gd, n, cudaMemcpyDeviceToHost, s));
+  MHL_CUDA(cudaStreamWaitEvent(s, p->ev_out, 0));   // every output is on the host when `stream` completes
   return MHL_OK;
 }
 

@@ -192,3 +192,40 @@ def test_nonfinite_router_score_is_reported():
     with pytest.raises(C.MhlError) as ei:
         _run_gpu(cfg, W, x, dout, backward=False)
     assert C.STATUS[ei.value.status] == "MHL_ERR_NONFINITE"
+
+
+def test_train_step_host_matches_device_path():
+    """mhlmoe_train_step_host (pinned host buffers, side-stream copies overlapping the forward /
+    backward) gives bit-identical out, dx and gradients to the device-buffer path, for two
+    back-to-back calls with different inputs (checks the cross-call event ordering)."""
+    _need_gpu()
+    from paper_2602_04870_b200 import mhlmoe as C
+    from paper_2602_04870_b200.layer import MHLatentMoE, torch_dtype, weights_to_device
+    cfg = LayerConfig("host", T=2048, d=256, N_h=2, d_h=128, N_e=64, k=8, d_e=64, dtype="bf16")
+    td = torch_dtype(cfg.dtype)
+    L = MHLatentMoE(cfg.T, cfg.d, cfg.N_h, cfg.d_h, cfg.N_e, cfg.k, cfg.d_e, cfg.dtype)
+    W, _, _ = make_problem(cfg, 9, "conf")
+    Wd = weights_to_device(W, cfg.dtype)
+    io = torch.empty(L.info["io_bytes"], dtype=torch.uint8, device="cuda")
+    hosts, refs = [], []
+    for seed in (21, 22):
+        _, x, dout = make_problem(cfg, seed, "conf")
+        xd, dd = torch.from_numpy(x).to("cuda", td), torch.from_numpy(dout).to("cuda", td)
+        g = L.alloc_grads()
+        out, _, _ = L.forward(xd, Wd)
+        dx = L.backward(xd, Wd, dd, g)
+        torch.cuda.synchronize()
+        refs.append((out.cpu(), dx.cpu(), {k: v.cpu() for k, v in g.items()}))
+        hosts.append((xd.cpu().pin_memory(), dd.cpu().pin_memory()))
+    outs = []
+    for xh, dh in hosts:   # back to back on one stream, no host sync in between
+        oh = torch.empty_like(xh).pin_memory()
+        gh = torch.empty_like(xh).pin_memory()
+        g = L.alloc_grads()
+        C.mhlmoe_train_step_host(L.plan, xh, dh, Wd, oh, gh, g, io, L.saved, L.workspace)
+        outs.append((oh, gh, g))
+    torch.cuda.synchronize()
+    for (o, d, g), (ro, rd, rg) in zip(outs, refs):
+        assert torch.equal(o, ro) and torch.equal(d, rd)
+        for k in rg:
+            assert torch.equal(g[k].cpu(), rg[k]), k
