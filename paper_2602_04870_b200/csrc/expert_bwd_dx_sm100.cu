@@ -158,14 +158,22 @@ expert_bwd_h_kernel(const __grid_constant__ CUtensorMap w1map, const __grid_cons
     Ph w1e, w2e;
     int cnt = 0;                       // chunks of this CTA's stream so far
     const uint64_t pol_keep = (dbg & 16) ? l2_evict_normal() : l2_evict_last();   // rows reused k times per head
+    int nx[4] = {0, 0, 0, 0};          // token ids of the next tile's rows 4*lane..4*lane+3
+    auto load_tok = [&](int ti) {
+      if (ti < 0) return;
+      const Tile t = tiles[ti];
+      const int32_t* tk = rt.tok_s + (size_t)t.head * Rp + t.row0 + 4 * lane;
+      nx[0] = tk[0]; nx[1] = tk[1]; nx[2] = tk[2]; nx[3] = tk[3];
+    };
+    load_tok(sc.at(0));
     for (int i = 0;; ++i) {
       const int ti = sc.at(i);
       if (ti < 0) break;
       const Tile tl = tiles[ti];
       const bool fresh = !sc.same_expert(sc.at(i - 1), ti);
       if (pw == 0 && lane == 0) trace_ev(trc, 34, i);
-      const int32_t* tk = rt.tok_s + (size_t)tl.head * Rp + tl.row0 + 4 * lane;
-      const int r0 = tk[0], r1 = tk[1], r2 = tk[2], r3 = tk[3];
+      const int r0 = nx[0], r1 = nx[1], r2 = nx[2], r3 = nx[3];
+      load_tok(sc.at(i + 1));          // in flight while this tile's chunks are issued
       if (pw == 0 && lane == 0 && fresh) {
         mbar_wait(bar(L::B_W1E), w1e.flip() ^ 1);
         load_w(&w1map, L::W1, bar(L::B_W1F), tl);

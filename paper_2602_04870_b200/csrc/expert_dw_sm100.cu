@@ -92,6 +92,8 @@ expert_dw_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant
       const int nsteps = ch.rows / kHalf;
       const int32_t* tk = rt.tok_s + (size_t)ch.head * Rp + ch.row0 + 4 * g;
       int r0 = tk[0], r1 = tk[1], r2 = tk[2], r3 = tk[3];
+      int q0 = 0, q1 = 0, q2 = 0, q3 = 0;              // the next step's ids, loaded one step ahead
+      if (nsteps > 1) { q0 = tk[kHalf]; q1 = tk[kHalf + 1]; q2 = tk[kHalf + 2]; q3 = tk[kHalf + 3]; }
       for (int s = 0; s < nsteps; ++s, ++n) {
         const int st = n % S;
         const uint32_t base = sb + st * L::STAGE;
@@ -110,7 +112,11 @@ expert_dw_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant
           tma_gather4(base + (p < XK ? L::X : L::DY) + kb * kHalf * 128 + 4 * g * 128, p < XK ? &xmap : &ymap,
                       ch.head * DH + kb * 64, r0, r1, r2, r3, &full[st]);
         }
-        if (s + 1 < nsteps) { tk += kHalf; r0 = tk[0]; r1 = tk[1]; r2 = tk[2]; r3 = tk[3]; }
+        r0 = q0; r1 = q1; r2 = q2; r3 = q3;
+        if (s + 2 < nsteps) {
+          tk += kHalf;
+          q0 = tk[kHalf]; q1 = tk[kHalf + 1]; q2 = tk[kHalf + 2]; q3 = tk[kHalf + 3];
+        }
       }
     }
   } else if (warp == kDwMma) {
