@@ -156,13 +156,13 @@ def test_all_tokens_to_one_expert():
     _compare(cfg, W, x, dout, g)
 
 
-@pytest.mark.parametrize("G,d_h,N_e", [(2, 32, 16), (4, 32, 16), (2, 128, 64)])
-def test_loopback_hp_bitwise_equals_single_rank(G, d_h, N_e):
+@pytest.mark.parametrize("G,N_h,d_h,N_e", [(2, 4, 32, 16), (4, 4, 32, 16), (2, 4, 128, 64), (8, 8, 128, 64)])
+def test_loopback_hp_bitwise_equals_single_rank(G, N_h, d_h, N_e):
     """HP on G virtual ranks (NCCL replaced by device copies) gives bit-identical
     out, dx, routing and per-head weight gradients to G = 1 (P:801: HP only moves data);
-    d_h = 128 runs the tcgen05 router/expert kernels."""
+    d_h = 128 runs the tcgen05 router/expert kernels; G = 8 leaves one head per rank."""
     _need_gpu()
-    cfg = LayerConfig("hp", T=1024, d=4 * d_h, N_h=4, d_h=d_h, N_e=N_e, k=4, d_e=32 if d_h == 32 else 64,
+    cfg = LayerConfig("hp", T=1024, d=N_h * d_h, N_h=N_h, d_h=d_h, N_e=N_e, k=4, d_e=32 if d_h == 32 else 64,
                       dtype="bf16")
     W, x, dout = make_problem(cfg, 5, "conf")
     g1 = _run_gpu(cfg, W, x, dout, G=1)
