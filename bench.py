@@ -32,7 +32,7 @@ FALLBACK_PEAKS = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustain
 
 def workload_desc(cfg, T_loc):
     return (f"{cfg.name}: T_loc={T_loc} tokens/GPU, d={cfg.d}, N_h={cfg.N_h}, d_h={cfg.d_h}, N_e={cfg.N_e}, "
-            f"k={cfg.k}, d_e={cfg.d_e}, {cfg.dtype} fwd+bwd, HP")
+            f"k={cfg.k}, d_e={cfg.d_e}, {cfg.dtype} {'fwd only' if cfg.fwd_only else 'fwd+bwd'}, HP")
 
 
 def _find_number(d, want, avoid=()):
@@ -163,7 +163,7 @@ def total_flops(cfg, T_loc):
     D = N_h * d_h
     fwd = 2 * d * D + 2 * N_h * d_h * N_e + 4 * N_h * k * d_h * d_e + 2 * D * d
     bwd = 4 * d * D + 4 * D * d + 8 * N_h * k * d_h * d_e + 4 * N_h * k * d_h
-    return T_loc * (fwd + bwd)
+    return T_loc * (fwd + (0 if cfg.fwd_only else bwd))
 
 
 # ----------------------------------------------------------------------------- CPU oracle arm
@@ -265,7 +265,8 @@ def main():
 
     def step():
         L.forward(x, Wd, out=out, stream=stream)
-        L.backward(x, Wd, dout, grads, dx=dx, stream=stream)
+        if not cfg.fwd_only:      # BASELINE's "small" config is forward only
+            L.backward(x, Wd, dout, grads, dx=dx, stream=stream)
 
     for _ in range(args.warmup):
         step()
@@ -303,7 +304,7 @@ def main():
 
     # ---- e2e: host buffers through mhlmoe_train_step_host, H2D/D2H inside the timed region
     e2e = None
-    if not args.no_e2e:
+    if not args.no_e2e and not cfg.fwd_only:
         xh = x.cpu().pin_memory(); dh = dout.cpu().pin_memory()
         oh = torch.empty_like(xh).pin_memory(); gh = torch.empty_like(xh).pin_memory()
         io = torch.empty(L.info["io_bytes"], dtype=torch.uint8, device=dev)

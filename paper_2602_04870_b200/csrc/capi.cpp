@@ -246,6 +246,8 @@ struct mhl_plan_s {
   size_t blas_ws_bytes = 32u << 20;
   ncclComm_t comm = nullptr;
   int32_t* dflag = nullptr;   // device non-finite flag
+  cudaError_t launch_err = cudaSuccess;   // first launch error harvested by a StepSpan
+  const char* launch_err_at = "";
   int num_sms = 148;
   // host-buffer step (mhlmoe_train_step_host): side stream for the copies that can overlap compute
   cudaStream_t copy_stream = nullptr;
@@ -278,6 +280,10 @@ struct StepSpan {
     if (p->timing) { a = p->next_event(); cudaEventRecord(a, s); }
   }
   ~StepSpan() {
+    // Launch-time errors are non-sticky and a later library call (cuBLAS) may reset the runtime's
+    // last-error slot, so every span harvests them immediately; check_kernels() reports the first.
+    const cudaError_t le = cudaGetLastError();
+    if (le != cudaSuccess && p->launch_err == cudaSuccess) { p->launch_err = le; p->launch_err_at = name; }
     if (a) { cudaEvent_t b = p->next_event(); cudaEventRecord(b, s); p->recs.push_back({name, a, b}); }
     static const bool dbg = getenv("MHL_DEBUG_SYNC") != nullptr;
     if (dbg) {
@@ -381,7 +387,11 @@ mhl::Routing routing_view(const Dims& m, const char* saved) {
 }
 
 mhl_status check_kernels(mhl_plan p) {
-  (void)p;
+  if (p->launch_err != cudaSuccess) {
+    const cudaError_t e = p->launch_err;
+    p->launch_err = cudaSuccess;
+    return fail(MHL_ERR_CUDA, std::string("kernel launch in ") + p->launch_err_at + ": " + cudaGetErrorString(e));
+  }
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return fail(MHL_ERR_CUDA, std::string("kernel launch: ") + cudaGetErrorString(e));
   return MHL_OK;

@@ -104,6 +104,7 @@ struct HL {
   static constexpr int TMEMP = DG + (kEpiWarps / 4) * BM * 4;
   static constexpr int BYTES = TMEMP + 16;
   static_assert(BYTES - CTRL <= CTRL_MAX, "control block overflow");
+  static_assert(BYTES <= kMaxSmem, "K1: shared memory over the per-CTA limit");
   static_assert(S >= kProdWarps, "ring too small");
 };
 
@@ -356,6 +357,7 @@ struct GL {
   static constexpr int TMEM_COLS = 2 * DH <= 256 ? 256 : 512;
   static_assert(BYTES - CTRL <= CTRL_MAX, "control block overflow");
   static_assert(AS >= 2, "dH ring too small");
+  static_assert(BYTES <= kMaxSmem, "K2: shared memory over the per-CTA limit");
 };
 
 template <int DH, int DE>

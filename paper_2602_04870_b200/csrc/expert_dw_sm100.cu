@@ -42,6 +42,7 @@ struct DwSmem {
   static constexpr int LAST = BAR + 8 * (2 * S + 2);            // int: "this CTA reduces the expert"
   static constexpr int TMEM = LAST + 16;
   static constexpr int BYTES = TMEM + 16;
+  static_assert(BYTES <= 227 * 1024, "dW: shared memory over the per-CTA limit");
 };
 
 template <int DH, int DE>

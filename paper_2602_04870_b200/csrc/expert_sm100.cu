@@ -57,6 +57,7 @@ struct FwdL {
   static constexpr int B_YEMPTY = B_G2DONE + 16;
   static constexpr int TMEMP = B_YEMPTY + 8;
   static constexpr int BYTES = TMEMP + 16;
+  static_assert(BYTES <= 227 * 1024, "expert fwd: shared memory over the per-CTA limit");
   static constexpr uint32_t T_H = 0, T_A = 128, T_Y = 256;
 };
 

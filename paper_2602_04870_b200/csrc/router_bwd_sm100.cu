@@ -43,6 +43,7 @@ struct RbL {
   static constexpr int NBAR = 2 * XS + 5;                    // xfull[XS], xempty[XS], bfull[2], bempty[2], acc
   static constexpr int TMEMP = BAR + NBAR * 8;
   static constexpr int BYTES = TMEMP + 16;
+  static_assert(BYTES <= 227 * 1024, "router bwd: shared memory over the per-CTA limit");
   static constexpr int ACC_COLS = (DH / 128) * NE;
   static constexpr int TMEM_COLS = ACC_COLS <= 32 ? 32 : ACC_COLS <= 64 ? 64 : ACC_COLS <= 128 ? 128
                                    : ACC_COLS <= 256 ? 256 : 512;

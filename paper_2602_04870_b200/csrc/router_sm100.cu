@@ -25,12 +25,13 @@ namespace {
 using namespace sm100;
 
 constexpr int RT = kRouterTile;   // 128 tokens = MMA M
-constexpr int kEG = 3;            // epilogue warpgroups (each owns every kEG-th tile of the CTA)
-constexpr int kThreads = (2 + 4 * kEG) * 32;
 constexpr int kChunkBytes = RT * 128;   // one 64-column K-chunk of the X tile
 
 template <int DH, int NE>
 struct RSmem {
+  // epilogue warpgroups (each owns every kEG-th tile of the CTA); fewer when the W planes fill smem
+  static constexpr int kEG = NE <= 64 ? 3 : 2;
+  static constexpr int THREADS = (2 + 4 * kEG) * 32;
   static constexpr int kNB = (2 * kEG * NE <= 512) ? 2 * kEG : 512 / NE;   // TMEM accumulator buffers
   static_assert(kNB >= kEG, "router: fewer TMEM buffers than epilogue warpgroups");
   static constexpr int W = 0;                                   // [3][DH/64][NE][64] SW128
@@ -44,13 +45,14 @@ struct RSmem {
   static constexpr int HIST = BIAS + kEG * NE * 4;              // [kEG][NE]
   static constexpr int TMEMP = HIST + kEG * NE * 4;
   static constexpr int BYTES = TMEMP + 16;
+  static_assert(BYTES <= 227 * 1024, "router: shared memory over the 227 KB per-CTA limit");
   static constexpr int TMEM_COLS = (kNB * NE <= 32) ? 32 : (kNB * NE <= 64) ? 64 : (kNB * NE <= 128) ? 128
                                    : (kNB * NE <= 256) ? 256 : 512;
 
 };
 
 template <int DH, int NE, int KMAX>
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(RSmem<DH, NE>::THREADS, 1)
 router_sm100_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap wmap,
                     const float* __restrict__ bias, int H, int64_t T, int k, int32_t* __restrict__ idx,
                     float* __restrict__ gate, int32_t* __restrict__ hist, int32_t* __restrict__ flag) {
@@ -66,7 +68,7 @@ router_sm100_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_const
   uint64_t* wfull = bars + 2 * S;
   uint64_t* wfree = wfull + 1;
   uint64_t* tfull = wfull + 2;
-  constexpr int kNB = L::kNB;
+  constexpr int kNB = L::kNB, kEG = L::kEG, kThreads = L::THREADS;
   uint64_t* tempty = tfull + kNB;
   float* s_bias = reinterpret_cast<float*>(smem + L::BIAS);
   int* s_hist = reinterpret_cast<int*>(smem + L::HIST);
@@ -267,7 +269,7 @@ bool launch_t(const void* Xs, int64_t ldx, const bf16* planes, const float* bias
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, RSmem<DH, NE>::BYTES);
   const int n_rt = (int)((T + RT - 1) / RT);
   const int grid = std::min(num_sms, H * n_rt);
-  kern<<<grid, kThreads, RSmem<DH, NE>::BYTES, s>>>(xm, wm, bias, H, T, k, idx, gate, hist, flag);
+  kern<<<grid, RSmem<DH, NE>::THREADS, RSmem<DH, NE>::BYTES, s>>>(xm, wm, bias, H, T, k, idx, gate, hist, flag);
   return true;
 }
 

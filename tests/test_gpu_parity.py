@@ -111,6 +111,17 @@ def test_router_bwd_tcgen05_matches_oracle_and_simt(d_h, N_e, k):
         assert rel_err(g["dW_r"], s["dW_r"]) < 1e-4
 
 
+@pytest.mark.parametrize("N_e,k,d_e", [(128, 16, 64), (64, 8, 128)])
+def test_paper_head_shapes_match_oracle(N_e, k, d_e):
+    """The paper-scale head shape (d_h = 256) at BASELINE's paper and doubled-granularity (G2x)
+    expert settings, every kernel on its tensor-core path, ragged T."""
+    _need_gpu()
+    cfg = LayerConfig("g2x", T=1000, d=512, N_h=2, d_h=256, N_e=N_e, k=k, d_e=d_e, dtype="bf16")
+    W, x, dout = make_problem(cfg, 12, "conf")
+    g = _run_gpu(cfg, W, x, dout)
+    _compare(cfg, W, x, dout, g)
+
+
 def test_router_strict_on_exact_subtokens():
     """W_in = 2^-1 x permutation (d = D): Xs is exact on both sides, so only the fp32
     (GPU) vs fp64 (oracle) score arithmetic differs (~1e-6).  Indices and slot order
