@@ -4,7 +4,8 @@
 // deterministic, integer-exact, dropless P:566/P:977):
 //   pos(r) = off[e] + tilepref[tile(t)][e] + rank of r among the router tile's replicas of e
 // where tilepref is the exclusive scan over router tiles of the per-tile expert histogram
-// emitted by F3.  Each expert segment starts on a 128-row boundary (off[e] is padded), so the
+// emitted by F3.  Each expert segment is padded to a multiple of kSegAlign rows (whole 128-row
+// tiles; kSegAlign = 256 would make them whole tile pairs for the cta_group::2 kernel), so the
 // block-sparse mask of Eq. 7 becomes a list of whole 128-row tiles; padding rows point at
 // the all-zero sub-token row (token id T) with gate 0 and contribute exactly nothing.
 // Outputs per head (Rp = padded row capacity): perm (row -> replica or -1), tok_s (row -> token
@@ -78,9 +79,9 @@ __device__ int block_exclusive_scan_1024(int v, int* s_warp, int* total) {
   return r;
 }
 
-// (2) single CTA: padded per-head offsets off[h][e] (exclusive scan of ceil(count/128)*128), the
+// (2) single CTA: padded per-head offsets off[h][e] (exclusive scan of the kSegAlign-padded counts), the
 // per-(h, e) tile and dW-chunk bases.  The tile list is ordered (head, part, expert, tile): expert
-// e's nt tiles are cut into kTileParts contiguous parts (part p = tiles [p*nt/P, (p+1)*nt/P)),
+// e's alignment units are cut into kTileParts contiguous parts (part p = units [p*n/P, (p+1)*n/P)),
 // and all experts' part-p tiles come before any part-(p+1) tile.  Within an expert the rows are in
 // token order, so the tiles in flight at any moment (consecutive list entries) cover one narrow
 // token window of the head across many experts: every sub-token row gathered for them is re-read
@@ -99,8 +100,9 @@ offsets_kernel(const int32_t* __restrict__ counts, int32_t* __restrict__ off, in
       for (int base = 0; base < N_e; base += 1024) {
         const int e = base + threadIdx.x;
         const int c = (e < N_e) ? counts[(size_t)h * N_e + e] : 0;
-        const int nt = (c + kExpertBM - 1) / kExpertBM;
-        const int np = (p + 1) * nt / kTileParts - p * nt / kTileParts;   // tiles of e in part p
+        constexpr int TPS = kSegAlign / kExpertBM;                         // tiles per alignment unit
+        const int nu = (c + kSegAlign - 1) / kSegAlign;                     // alignment units of e
+        const int np = TPS * ((p + 1) * nu / kTileParts - p * nu / kTileParts);   // tiles in part p
         const int px = block_exclusive_scan_1024(np, s_warp, &s_tot);
         const int ptot = s_tot;
         __syncthreads();
@@ -112,7 +114,7 @@ offsets_kernel(const int32_t* __restrict__ counts, int32_t* __restrict__ off, in
     for (int base = 0; base < N_e; base += 1024) {
       const int e = base + threadIdx.x;
       const int c = (e < N_e) ? counts[(size_t)h * N_e + e] : 0;
-      const int cp = (c + kExpertBM - 1) / kExpertBM * kExpertBM;       // padded segment length
+      const int cp = (c + kSegAlign - 1) / kSegAlign * kSegAlign;       // padded segment length
       const int rx = block_exclusive_scan_1024(cp, s_warp, &s_tot);
       const int rtot = s_tot;
       __syncthreads();
@@ -144,18 +146,19 @@ tiles_kernel(const int32_t* __restrict__ counts, const int32_t* __restrict__ off
   if (he >= H * N_e) return;
   const int h = he / N_e, e = he % N_e;
   const int c = counts[he];
-  const int nt = (c + kExpertBM - 1) / kExpertBM;
-  const int cp = nt * kExpertBM;
+  constexpr int TPS = kSegAlign / kExpertBM;
+  const int nu = (c + kSegAlign - 1) / kSegAlign;
+  const int cp = nu * kSegAlign;
   const int row_off = off[(size_t)h * (N_e + 1) + e];
   for (int p = 0; p < kTileParts; ++p) {
-    const int j0 = p * nt / kTileParts, j1 = (p + 1) * nt / kTileParts;
+    const int j0 = TPS * (p * nu / kTileParts), j1 = TPS * ((p + 1) * nu / kTileParts);   // unit-aligned
     const int tb = tbase[((size_t)h * kTileParts + p) * N_e + e];
     for (int j = j0; j < j1; ++j) {
       const int ti = tb + (j - j0);
       if (ti < max_tiles) {
         Tile tl;
         tl.head = h; tl.expert = e; tl.row0 = row_off + j * kExpertBM;
-        tl.rows = min(kExpertBM, c - j * kExpertBM);
+        tl.rows = max(0, min(kExpertBM, c - j * kExpertBM));
         tiles[ti] = tl;
       }
     }

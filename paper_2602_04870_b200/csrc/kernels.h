@@ -7,14 +7,18 @@
 namespace mhl {
 
 constexpr int kRouterTile = 128;   // tokens per router CTA (= clustering tile of F4)
-constexpr int kExpertBM = 128;     // replica rows per expert tile (tcgen05 M); segments padded to it
+constexpr int kExpertBM = 128;     // replica rows per expert tile (tcgen05 M)
+// Expert segments are padded to a multiple of kSegAlign rows.  2*kExpertBM makes every segment a
+// whole number of tile pairs, which the cta_group::2 forward kernel (expert_fwd_pair_sm100.cu,
+// opt-in) requires; one tile is the default (less padding, measured faster overall).
+constexpr int kSegAlign = kExpertBM;
 constexpr int kDwChunk = 4096;     // sorted rows per weight-gradient partial (B5 dW)
 constexpr int kTileGroup = 8;      // consecutive expert tiles a persistent CTA takes at once
 constexpr int kTileParts = 8;      // token-order parts per expert segment in the tile list (cluster.cu)
 
 // Clustered routing of one rank's local heads (F3/F4 outputs, device pointers).
-// Sorted-row arrays have a fixed per-head capacity Rp = T*k + N_e*128 (expert segments are
-// padded to whole 128-row tiles; padding rows: perm -1, tok_s = T (the all-zero row), gate_s 0).
+// Sorted-row arrays have a fixed per-head capacity Rp = T*k + N_e*kSegAlign (expert segments are
+// padded to whole pairs of 128-row tiles; padding rows: perm -1, tok_s = T (the all-zero row), gate_s 0).
 struct Routing {
   int H; int64_t T; int k; int N_e; int64_t Rp;
   const int32_t* idx;      // [H][T][k]  expert ids, slot order = descending biased key
@@ -57,6 +61,10 @@ void launch_expert_fwd_simt(int dtype, const Routing& rt, const void* Xs, int64_
 bool expert_fwd_sm100_supported(int d_h, int d_e);
 bool launch_expert_fwd_sm100(const Routing& rt, const void* Xs, int64_t ldx, const void* W1, const void* W2, int d_h,
                              int d_e, void* Yrep, int num_sms, cudaStream_t s);
+// the same on CTA pairs (tcgen05 cta_group::2, half of each weight matrix per CTA)
+bool expert_fwd_pair_supported(int d_h, int d_e);
+bool launch_expert_fwd_pair_sm100(const Routing& rt, const void* Xs, int64_t ldx, const void* W1, const void* W2,
+                                  int d_h, int d_e, void* Yrep, int num_sms, cudaStream_t s);
 
 // ---- F6: y[t][h*d_h+c] = sum_j Yrep[h][pos[h][t*k+j]][c]  (fixed j order), out ld = ldo.
 void launch_combine_fwd(int dtype, const Routing& rt, const void* Yrep, int d_h, void* out, int64_t ldo,
