@@ -156,10 +156,11 @@ MHL_API mhl_status mhlmoe_backward(mhl_plan plan, const void* x, const mhl_weigh
  * pinned for asynchronous copies): copies x and d_out to device staging `io`
  * (io_bytes), runs forward + backward, copies out and dx back to out_host /
  * dx_host ([T_loc, d] E).  Asynchronous on `stream`; synchronize before reading
- * the host outputs.  Weights and gradients are device pointers.  The d_out upload
- * and the out download run on a plan-owned side stream (overlapping the forward /
- * backward), ordered with `stream` by events: when `stream` completes, every output
- * of the call is on the host. */
+ * the host outputs.  Weights and gradients are device pointers.  The copies run on
+ * two plan-owned side streams (one per link direction) ordered with `stream` by
+ * events: the d_out upload overlaps the forward, the out download the backward, and
+ * a call's x upload overlaps the previous call's dx download.  When `stream`
+ * completes, every output of the call is on the host. */
 MHL_API mhl_status mhlmoe_train_step_host(mhl_plan plan, const void* x_host, const void* dout_host,
                                   const mhl_weights* w, void* out_host, void* dx_host,
                                   const mhl_grads* grads, void* io, void* saved,

@@ -250,9 +250,10 @@ struct mhl_plan_s {
   const char* launch_err_at = "";
   int num_sms = 148;
   // host-buffer step (mhlmoe_train_step_host): side stream for the copies that can overlap compute
-  cudaStream_t copy_stream = nullptr;
-  cudaEvent_t ev_dout = nullptr, ev_fwd = nullptr, ev_out = nullptr, ev_bwd = nullptr;
-  bool ev_bwd_live = false, ev_out_live = false;
+  cudaStream_t h2d_stream = nullptr, d2h_stream = nullptr;
+  cudaEvent_t ev_x = nullptr, ev_dout = nullptr, ev_fwd = nullptr, ev_out = nullptr, ev_bwd = nullptr,
+              ev_dx = nullptr;
+  bool io_live = false;   // a previous host step's events are recorded
   std::atomic<uint64_t> launches{0};
   uint64_t a2a_bytes_posted = 0;
   // optional per-step CUDA-event timing (mhl_set_step_timing)
@@ -633,9 +634,10 @@ mhl_status hp_plan_destroy(mhl_plan p) {
   if (p->blas) cublasDestroy(p->blas);
   if (p->blas_ws) cudaFree(p->blas_ws);
   if (p->dflag) cudaFree(p->dflag);
-  for (cudaEvent_t e : {p->ev_dout, p->ev_fwd, p->ev_out, p->ev_bwd})
+  for (cudaEvent_t e : {p->ev_x, p->ev_dout, p->ev_fwd, p->ev_out, p->ev_bwd, p->ev_dx})
     if (e) cudaEventDestroy(e);
-  if (p->copy_stream) cudaStreamDestroy(p->copy_stream);
+  if (p->h2d_stream) cudaStreamDestroy(p->h2d_stream);
+  if (p->d2h_stream) cudaStreamDestroy(p->d2h_stream);
   for (auto e : p->pool) cudaEventDestroy(e);
   delete p;
   return MHL_OK;
@@ -794,31 +796,41 @@ mhl_status mhlmoe_train_step_host(mhl_plan p, const void* x_host, const void* do
   char* dd = xd + a;
   char* od = dd + a;
   char* gd = od + a;
-  // Copies that do not feed the next kernel ride a side stream: d_out's upload overlaps the
-  // forward, out's download overlaps the backward (H2D and D2H use separate link directions).
-  if (!p->copy_stream) {
-    MHL_CUDA(cudaStreamCreateWithFlags(&p->copy_stream, cudaStreamNonBlocking));
-    for (cudaEvent_t* e : {&p->ev_dout, &p->ev_fwd, &p->ev_out, &p->ev_bwd})
+  // Copies run on two plan-owned side streams, one per link direction, ordered against the
+  // compute stream by events: d_out's upload overlaps the forward, out's download overlaps the
+  // backward, and (across back-to-back calls) this call's x upload overlaps the previous call's
+  // dx download.  Buffer reuse across calls is guarded: x / d_out are re-uploaded only after the
+  // previous backward (their last reader), out / dx rewritten only after their downloads.
+  if (!p->h2d_stream) {
+    MHL_CUDA(cudaStreamCreateWithFlags(&p->h2d_stream, cudaStreamNonBlocking));
+    MHL_CUDA(cudaStreamCreateWithFlags(&p->d2h_stream, cudaStreamNonBlocking));
+    for (cudaEvent_t* e : {&p->ev_x, &p->ev_dout, &p->ev_fwd, &p->ev_out, &p->ev_bwd, &p->ev_dx})
       MHL_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
   }
-  cudaStream_t cs = p->copy_stream;
-  MHL_CUDA(cudaMemcpyAsync(xd, x_host, n, cudaMemcpyHostToDevice, s));
-  if (p->ev_bwd_live) MHL_CUDA(cudaStreamWaitEvent(cs, p->ev_bwd, 0));   // previous backward read dd
-  MHL_CUDA(cudaMemcpyAsync(dd, dout_host, n, cudaMemcpyHostToDevice, cs));
-  MHL_CUDA(cudaEventRecord(p->ev_dout, cs));
-  if (p->ev_out_live) MHL_CUDA(cudaStreamWaitEvent(s, p->ev_out, 0));    // previous download of od
+  cudaStream_t up = p->h2d_stream, down = p->d2h_stream;
+  if (p->io_live) MHL_CUDA(cudaStreamWaitEvent(up, p->ev_bwd, 0));
+  MHL_CUDA(cudaMemcpyAsync(xd, x_host, n, cudaMemcpyHostToDevice, up));
+  MHL_CUDA(cudaEventRecord(p->ev_x, up));
+  MHL_CUDA(cudaMemcpyAsync(dd, dout_host, n, cudaMemcpyHostToDevice, up));
+  MHL_CUDA(cudaEventRecord(p->ev_dout, up));
+  MHL_CUDA(cudaStreamWaitEvent(s, p->ev_x, 0));
+  if (p->io_live) MHL_CUDA(cudaStreamWaitEvent(s, p->ev_out, 0));   // previous download of od
   MHL_TRY(mhlmoe_forward(p, xd, w, od, saved, workspace, workspace_bytes, nullptr, nullptr, stream));
   MHL_CUDA(cudaEventRecord(p->ev_fwd, s));
-  MHL_CUDA(cudaStreamWaitEvent(cs, p->ev_fwd, 0));
-  MHL_CUDA(cudaMemcpyAsync(out_host, od, n, cudaMemcpyDeviceToHost, cs));
-  MHL_CUDA(cudaEventRecord(p->ev_out, cs));
-  p->ev_out_live = true;
+  MHL_CUDA(cudaStreamWaitEvent(down, p->ev_fwd, 0));
+  MHL_CUDA(cudaMemcpyAsync(out_host, od, n, cudaMemcpyDeviceToHost, down));
+  MHL_CUDA(cudaEventRecord(p->ev_out, down));
   MHL_CUDA(cudaStreamWaitEvent(s, p->ev_dout, 0));
+  if (p->io_live) MHL_CUDA(cudaStreamWaitEvent(s, p->ev_dx, 0));    // previous download of gd
   MHL_TRY(mhlmoe_backward(p, xd, w, dd, saved, gd, grads, workspace, workspace_bytes, stream));
   MHL_CUDA(cudaEventRecord(p->ev_bwd, s));
-  p->ev_bwd_live = true;
-  MHL_CUDA(cudaMemcpyAsync(dx_host, gd, n, cudaMemcpyDeviceToHost, s));
-  MHL_CUDA(cudaStreamWaitEvent(s, p->ev_out, 0));   // every output is on the host when `stream` completes
+  MHL_CUDA(cudaStreamWaitEvent(down, p->ev_bwd, 0));
+  MHL_CUDA(cudaMemcpyAsync(dx_host, gd, n, cudaMemcpyDeviceToHost, down));
+  MHL_CUDA(cudaEventRecord(p->ev_dx, down));
+  p->io_live = true;
+  // every output of this call is on the host when `stream` completes
+  MHL_CUDA(cudaStreamWaitEvent(s, p->ev_out, 0));
+  MHL_CUDA(cudaStreamWaitEvent(s, p->ev_dx, 0));
   return MHL_OK;
 }
 
