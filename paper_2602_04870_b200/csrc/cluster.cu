@@ -79,70 +79,92 @@ __device__ int block_exclusive_scan_1024(int v, int* s_warp, int* total) {
   return r;
 }
 
-// (2) single CTA: padded per-head offsets off[h][e] (exclusive scan of the kSegAlign-padded counts), the
+// (2) padded per-head offsets off[h][e] (exclusive scan of the kSegAlign-padded counts), the
 // per-(h, e) tile and dW-chunk bases.  The tile list is ordered (head, part, expert, tile): expert
 // e's alignment units are cut into kTileParts contiguous parts (part p = units [p*n/P, (p+1)*n/P)),
 // and all experts' part-p tiles come before any part-(p+1) tile.  Within an expert the rows are in
 // token order, so the tiles in flight at any moment (consecutive list entries) cover one narrow
 // token window of the head across many experts: every sub-token row gathered for them is re-read
 // by its other top-k experts while it is still in L2.
+// One CTA per head: the global tile / chunk bases of head h are the totals of heads < h, which the
+// CTA recomputes itself from `counts` (H*N_e values), so the heads scan in parallel.
 __global__ void __launch_bounds__(1024)
 offsets_kernel(const int32_t* __restrict__ counts, int32_t* __restrict__ off, int32_t* __restrict__ tbase,
                int32_t* __restrict__ ntiles, int H, int N_e, int max_tiles, int32_t* __restrict__ nchunks,
                int32_t* __restrict__ cbase, int32_t* __restrict__ ccount, int max_chunks) {
   __shared__ int s_warp[64];
   __shared__ int s_tot;
-  int carry_t = 0, carry_c = 0;
-  for (int h = 0; h < H; ++h) {
-    int carry_r = 0;
-    for (int p = 0; p < kTileParts; ++p) {
-      int carry_p = 0;
-      for (int base = 0; base < N_e; base += 1024) {
-        const int e = base + threadIdx.x;
-        const int c = (e < N_e) ? counts[(size_t)h * N_e + e] : 0;
-        constexpr int TPS = kSegAlign / kExpertBM;                         // tiles per alignment unit
-        const int nu = (c + kSegAlign - 1) / kSegAlign;                     // alignment units of e
-        const int np = TPS * ((p + 1) * nu / kTileParts - p * nu / kTileParts);   // tiles in part p
-        const int px = block_exclusive_scan_1024(np, s_warp, &s_tot);
-        const int ptot = s_tot;
-        __syncthreads();
-        if (e < N_e) tbase[((size_t)h * kTileParts + p) * N_e + e] = carry_t + carry_p + px;
-        carry_p += ptot;
-      }
-      carry_t += carry_p;
-    }
+  constexpr int TPS = kSegAlign / kExpertBM;                             // tiles per alignment unit
+  const int h = blockIdx.x;
+  // tiles and dW chunks of all heads before h (and of all heads, for the totals)
+  int t_before = 0, c_before = 0, t_all = 0, c_all = 0;
+  for (int i = threadIdx.x; i < H * N_e; i += blockDim.x) {
+    const int c = counts[i];
+    const int cp = (c + kSegAlign - 1) / kSegAlign * kSegAlign;
+    const int nt = cp / kExpertBM, nc = (cp + kDwChunk - 1) / kDwChunk;
+    if (i / N_e < h) { t_before += nt; c_before += nc; }
+    t_all += nt; c_all += nc;
+  }
+  // block reductions (order-independent integer sums)
+  auto block_sum = [&](int v) {
+    const int ex = block_exclusive_scan_1024(v, s_warp, &s_tot);
+    (void)ex;
+    const int t = s_tot;
+    __syncthreads();
+    return t;
+  };
+  int carry_t = block_sum(t_before);
+  int carry_c = block_sum(c_before);
+  const int tot_t = block_sum(t_all), tot_c = block_sum(c_all);
+  int carry_r = 0;
+  for (int p = 0; p < kTileParts; ++p) {
+    int carry_p = 0;
     for (int base = 0; base < N_e; base += 1024) {
       const int e = base + threadIdx.x;
       const int c = (e < N_e) ? counts[(size_t)h * N_e + e] : 0;
-      const int cp = (c + kSegAlign - 1) / kSegAlign * kSegAlign;       // padded segment length
-      const int rx = block_exclusive_scan_1024(cp, s_warp, &s_tot);
-      const int rtot = s_tot;
+      const int nu = (c + kSegAlign - 1) / kSegAlign;                   // alignment units of e
+      const int np = TPS * ((p + 1) * nu / kTileParts - p * nu / kTileParts);   // tiles in part p
+      const int px = block_exclusive_scan_1024(np, s_warp, &s_tot);
+      const int ptot = s_tot;
       __syncthreads();
-      const int nc = (cp + kDwChunk - 1) / kDwChunk;
-      const int cx = block_exclusive_scan_1024(nc, s_warp, &s_tot);
-      const int ctot = s_tot;
-      __syncthreads();
-      if (e < N_e) {
-        off[(size_t)h * (N_e + 1) + e] = carry_r + rx;
-        cbase[(size_t)h * N_e + e] = carry_c + cx;
-        ccount[(size_t)h * N_e + e] = nc;
-      }
-      carry_r += rtot;
-      carry_c += ctot;
+      if (e < N_e) tbase[((size_t)h * kTileParts + p) * N_e + e] = carry_t + carry_p + px;
+      carry_p += ptot;
     }
-    if (threadIdx.x == 0) off[(size_t)h * (N_e + 1) + N_e] = carry_r;
+    carry_t += carry_p;
   }
-  if (threadIdx.x == 0) { *ntiles = min(carry_t, max_tiles); *nchunks = min(carry_c, max_chunks); }
+  for (int base = 0; base < N_e; base += 1024) {
+    const int e = base + threadIdx.x;
+    const int c = (e < N_e) ? counts[(size_t)h * N_e + e] : 0;
+    const int cp = (c + kSegAlign - 1) / kSegAlign * kSegAlign;         // padded segment length
+    const int rx = block_exclusive_scan_1024(cp, s_warp, &s_tot);
+    const int rtot = s_tot;
+    __syncthreads();
+    const int nc = (cp + kDwChunk - 1) / kDwChunk;
+    const int cx = block_exclusive_scan_1024(nc, s_warp, &s_tot);
+    const int ctot = s_tot;
+    __syncthreads();
+    if (e < N_e) {
+      off[(size_t)h * (N_e + 1) + e] = carry_r + rx;
+      cbase[(size_t)h * N_e + e] = carry_c + cx;
+      ccount[(size_t)h * N_e + e] = nc;
+    }
+    carry_r += rtot;
+    carry_c += ctot;
+  }
+  if (threadIdx.x == 0) {
+    off[(size_t)h * (N_e + 1) + N_e] = carry_r;
+    if (h == 0) { *ntiles = min(tot_t, max_tiles); *nchunks = min(tot_c, max_chunks); }
+  }
 }
 
-// (2b) one thread per (h, e): its tiles (at the (h, part, e) positions), its dW chunks and the
-// padding-row fill of its segment.
-__global__ void __launch_bounds__(128)
+// (2b) one warp per (h, e): its tiles (at the (h, part, e) positions), its dW chunks and the
+// padding-row fill of its segment, lanes striding over each list.
+__global__ void __launch_bounds__(256)
 tiles_kernel(const int32_t* __restrict__ counts, const int32_t* __restrict__ off, const int32_t* __restrict__ tbase,
              Tile* __restrict__ tiles, int max_tiles, Tile* __restrict__ chunks, const int32_t* __restrict__ cbase,
              int max_chunks, int H, int N_e, int64_t Rp, int32_t* __restrict__ perm, int32_t* __restrict__ tok_s,
              float* __restrict__ gate_s, int tok_zero) {
-  const int he = blockIdx.x * blockDim.x + threadIdx.x;
+  const int he = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5), lane = threadIdx.x & 31;
   if (he >= H * N_e) return;
   const int h = he / N_e, e = he % N_e;
   const int c = counts[he];
@@ -153,7 +175,7 @@ tiles_kernel(const int32_t* __restrict__ counts, const int32_t* __restrict__ off
   for (int p = 0; p < kTileParts; ++p) {
     const int j0 = TPS * (p * nu / kTileParts), j1 = TPS * ((p + 1) * nu / kTileParts);   // unit-aligned
     const int tb = tbase[((size_t)h * kTileParts + p) * N_e + e];
-    for (int j = j0; j < j1; ++j) {
+    for (int j = j0 + lane; j < j1; j += 32) {
       const int ti = tb + (j - j0);
       if (ti < max_tiles) {
         Tile tl;
@@ -164,7 +186,7 @@ tiles_kernel(const int32_t* __restrict__ counts, const int32_t* __restrict__ off
     }
   }
   const int nc = (cp + kDwChunk - 1) / kDwChunk;
-  for (int i = 0; i < nc; ++i) {
+  for (int i = lane; i < nc; i += 32) {
     const int ci = cbase[he] + i;
     if (ci < max_chunks) {
       Tile tl;
@@ -174,7 +196,7 @@ tiles_kernel(const int32_t* __restrict__ counts, const int32_t* __restrict__ off
     }
   }
   // padding rows of this segment: no replica, zero sub-token, gate 0
-  for (int r = row_off + c; r < row_off + cp; ++r) {
+  for (int r = row_off + c + lane; r < row_off + cp; r += 32) {
     perm[(size_t)h * Rp + r] = -1;
     tok_s[(size_t)h * Rp + r] = tok_zero;
     gate_s[(size_t)h * Rp + r] = 0.f;
@@ -247,9 +269,9 @@ void launch_cluster(int H, int64_t T, int k, int N_e, const int32_t* idx, const 
   tile_prefix_kernel<<<dim3(N_e, H), 256, 0, s>>>(hist, tilepref, counts, n_rt, N_e);
   // tile bases [H][kTileParts][N_e] live in the (otherwise unused here) tail of tilepref's scratch
   int32_t* tbase = tilepref + (size_t)H * n_rt * N_e;
-  offsets_kernel<<<1, 1024, 0, s>>>(counts, off, tbase, ntiles, H, N_e, max_tiles, nchunks, cbase, ccount, max_chunks);
-  tiles_kernel<<<(H * N_e + 127) / 128, 128, 0, s>>>(counts, off, tbase, tiles, max_tiles, chunks, cbase, max_chunks, H,
-                                                     N_e, Rp, perm, tok_s, gate_s, (int)T);
+  offsets_kernel<<<H, 1024, 0, s>>>(counts, off, tbase, ntiles, H, N_e, max_tiles, nchunks, cbase, ccount, max_chunks);
+  tiles_kernel<<<(H * N_e + 7) / 8, 256, 0, s>>>(counts, off, tbase, tiles, max_tiles, chunks, cbase, max_chunks, H,
+                                                 N_e, Rp, perm, tok_s, gate_s, (int)T);
   scatter_kernel<<<dim3(n_rt, H), kScatterWarps * 32, sizeof(int) * kScatterWarps * N_e, s>>>(
       idx, gate, off, tilepref, perm, pos, tok_s, gate_s, T, k, N_e, n_rt, Rp);
 }
