@@ -36,7 +36,7 @@ __all__ = [
     "experts_dense", "experts_sparse_loop", "expert_flex_form",
     "cluster_plan", "layer_forward", "layer_backward", "hp_layer_forward",
     "hp_layer_backward", "hp_a2a_bytes", "layer_flops", "moe_flops_equivalent",
-    "ep_dispatch_rows", "ForwardCache",
+    "ep_dispatch_rows", "ForwardCache", "expert_loads", "update_bias",
 ]
 
 
@@ -514,6 +514,27 @@ def _head_backward(Ph, X_h, dY, I, g):
     dW_r = X_h.T @ dS_full
     dXs_h = dXs_h + dS_full @ W_r_h.T
     return dict(dXs_h=dXs_h, dW_r=dW_r, dW1=dW1, dW2=dW2, dg=dg, dS=dS)
+
+
+# ---------------------------------------------------------------------------
+# Aux-free, global load balancing (rule per S:245-S:253, R24)
+# ---------------------------------------------------------------------------
+def expert_loads(I: np.ndarray, N_e: int) -> np.ndarray:
+    """Expert loads of one head over the step's tokens: load[e] = #{(t, j): I[t, j] = e}.
+    Under HP the head's whole token set is on one rank, so this count is already the
+    *global* load the paper balances on."""
+    return np.bincount(np.asarray(I, np.int64).reshape(-1), minlength=N_e).astype(np.int64)
+
+
+def update_bias(b_h: np.ndarray, load: np.ndarray, gamma: float) -> np.ndarray:
+    """Aux-free bias update of one head: b[e] -= gamma * sign(load[e] - mean(load)) (R24; the
+    paper cites the aux-free method and only states that the bias enters selection,
+    not the scores; the sign rule and gamma come from SPEC S:248).  The bias is
+    fp32 (P:1992 'routers compute in FP32'), so the update is evaluated in fp32."""
+    load = np.asarray(load, np.float64)
+    mean = load.sum() / load.size
+    step = np.float32(gamma) * np.sign(load - mean).astype(np.float32)
+    return (np.asarray(b_h, np.float32) - step).astype(np.float32)
 
 
 # ---------------------------------------------------------------------------

@@ -230,3 +230,50 @@ def test_cluster_plan_brute_force():
     # everything to expert 0 (degenerate)
     p0, q0, o0 = O.cluster_plan(np.zeros((5, 1), np.int64), 4)
     np.testing.assert_array_equal(p0, np.arange(5)); np.testing.assert_array_equal(o0, [0, 5, 5, 5, 5])
+
+
+def test_expert_loads_brute_force():
+    rng = np.random.default_rng(3)
+    T, k, N_e = 50, 3, 7
+    I = np.stack([rng.choice(N_e, size=k, replace=False) for _ in range(T)])
+    count = {}
+    for t in range(T):
+        for j in range(k):
+            count[int(I[t, j])] = count.get(int(I[t, j]), 0) + 1
+    load = O.expert_loads(I, N_e)
+    assert [count.get(e, 0) for e in range(N_e)] == load.tolist()
+    assert load.sum() == T * k and load.max() <= T
+
+
+def test_update_bias_sign_rule_cases():
+    """S:248-S:251 examples: balanced -> unchanged; one overloaded expert -> exactly -gamma;
+    underloaded experts move up by gamma; the update is fp32."""
+    b = np.array([0.5, -0.25, 0.125, 0.0], np.float32)
+    assert np.array_equal(O.update_bias(b, np.array([5, 5, 5, 5]), 1e-3), b)
+    nb = O.update_bias(b, np.array([8, 4, 4, 4]), 1e-3)          # mean 5
+    assert nb.dtype == np.float32
+    assert nb[0] == np.float32(b[0] - np.float32(1e-3))
+    assert np.all(nb[1:] == (b[1:] + np.float32(1e-3)).astype(np.float32))
+    # mean need not be an integer: load == mean never happens, every expert moves
+    nb = O.update_bias(b, np.array([3, 2, 2, 2]), 0.5)            # mean 2.25
+    assert np.array_equal(nb, (b + np.float32(0.5) * np.array([-1, 1, 1, 1], np.float32)).astype(np.float32))
+
+
+def test_update_bias_closed_loop_reduces_imbalance():
+    """closed loop on skewed synthetic tokens -> max/mean expert load decreases
+    (router = the oracle's full-sort top-k, bias only steers selection)."""
+    rng = np.random.default_rng(11)
+    T, d_h, N_e, k = 512, 16, 8, 2
+    X = rng.standard_normal((T, d_h))
+    W = rng.standard_normal((d_h, N_e)) * 0.1
+    W[:, 0] += 0.3                                                # expert 0 preferred
+    X[:, :] += 0.5
+    b = np.zeros(N_e, np.float32)
+    ratios = []
+    for _ in range(200):
+        I, *_ = O.route_topk(X, W, b.astype(np.float64), k)
+        load = O.expert_loads(I, N_e)
+        ratios.append(load.max() / load.mean())
+        b = O.update_bias(b, load, 2e-2)
+    assert ratios[0] > 1.5
+    assert np.mean(ratios[-20:]) < 0.75 * ratios[0]
