@@ -166,6 +166,16 @@ MHL_API mhl_status mhlmoe_train_step_host(mhl_plan plan, const void* x_host, con
                                   const mhl_grads* grads, void* io, void* saved,
                                   void* workspace, size_t workspace_bytes, void* stream);
 
+/* Aux-free, global load balancing (NEXT-2): after a forward on
+ * `saved`, updates this rank's router bias in place from the step's expert loads:
+ *   bias[h][e] -= gamma * sign(load[h][e] - mean_e load[h][e])       (rule S:248, R24)
+ * load[h][e] = replicas of local head h routed to expert e (F4's counts).  Under HP a
+ * head's whole token set lives on one rank, so the load is already global: no
+ * collective.  bias: DEVICE float32 [H_loc][N_e] (LOOPBACK: [N_h][N_e]), in/out, the
+ * same tensor the forward used (mhl_weights.bias).  gamma >= 0 (S:267 suggests 1e-3).
+ * Asynchronous on `stream`.  Errors: MHL_ERR_INVALID_ARGUMENT (NULL, gamma < 0 or NaN). */
+MHL_API mhl_status mhlmoe_update_bias(mhl_plan plan, const void* saved, float* bias, float gamma, void* stream);
+
 /* After a stream synchronize: MHL_ERR_NONFINITE if any router key seen since the
  * last call was NaN/Inf (R7), else MHL_OK.  Resets the flag. */
 MHL_API mhl_status mhl_check_device_status(mhl_plan plan);

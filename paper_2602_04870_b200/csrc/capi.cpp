@@ -115,9 +115,9 @@ struct Bump {
 };
 
 // offsets inside one rank's saved region
-struct SavedLayout { size_t Xs, idx, gate, perm, tok_s, gate_s, pos, off, tiles, ntiles, chunks, nchunks, cbase, ccount, cat, total; };
+struct SavedLayout { size_t Xs, idx, gate, perm, tok_s, gate_s, pos, off, tiles, ntiles, chunks, nchunks, cbase, ccount, load, cat, total; };
 // offsets inside one rank's workspace region (forward and backward alias each other)
-struct FwdLayout { size_t send1, Yrep, send2, recv2, hist, tilepref, counts, planes, total; };
+struct FwdLayout { size_t send1, Yrep, send2, recv2, hist, tilepref, planes, total; };
 struct BwdLayout { size_t send3, dY, dXrep, dg, dS, dH, gA, dwr_part, W_rT, send4, recv4, dXs, dw_part, dw_done, total; };
 
 SavedLayout saved_layout(const Dims& m) {
@@ -136,6 +136,7 @@ SavedLayout saved_layout(const Dims& m) {
   L.nchunks = b.take(16);
   L.cbase = b.take((size_t)m.H * m.N_e * 4);
   L.ccount = b.take((size_t)m.H * m.N_e * 4);
+  L.load = b.take((size_t)m.H * m.N_e * 4);             // per-head expert loads of the step (F4)
   L.cat = b.take((size_t)m.T_loc * m.D * m.el);
   L.total = b.off;
   return L;
@@ -149,7 +150,6 @@ FwdLayout fwd_layout(const Dims& m) {
   L.recv2 = b.take(m.G > 1 ? (size_t)m.T_loc * m.D * m.el : 0);
   L.hist = b.take((size_t)m.H * m.n_rt * m.N_e * 4);
   L.tilepref = b.take(((size_t)m.H * m.n_rt * m.N_e + (size_t)m.H * mhl::kTileParts * m.N_e) * 4);   // + tile bases
-  L.counts = b.take((size_t)m.H * m.N_e * 4);
   L.planes = b.take(mhl::router_sm100_planes_bytes(m.H, m.d_h, m.N_e));
   L.total = b.off;
   return L;
@@ -426,7 +426,7 @@ mhl_status moe_forward_local(mhl_plan p, const RankPtrs& R, void* yout, cudaStre
   {
     MHL_SPAN("F4_cluster");
     mhl::launch_cluster(m.H, m.T_g, m.k, m.N_e, idx, gate, hist, (int32_t*)(R.ws + F.tilepref),
-                        (int32_t*)(R.ws + F.counts), off, perm, pos, (int32_t*)(R.saved + S.tok_s),
+                        (int32_t*)(R.saved + S.load), off, perm, pos, (int32_t*)(R.saved + S.tok_s),
                         (float*)(R.saved + S.gate_s), m.Rp, tiles, ntiles, m.max_tiles, (mhl::Tile*)(R.saved + S.chunks),
                         (int32_t*)(R.saved + S.nchunks), (int32_t*)(R.saved + S.cbase), (int32_t*)(R.saved + S.ccount),
                         m.max_chunks, s);
@@ -832,6 +832,22 @@ mhl_status mhlmoe_train_step_host(mhl_plan p, const void* x_host, const void* do
   MHL_CUDA(cudaStreamWaitEvent(s, p->ev_out, 0));
   MHL_CUDA(cudaStreamWaitEvent(s, p->ev_dx, 0));
   return MHL_OK;
+}
+
+mhl_status mhlmoe_update_bias(mhl_plan p, const void* saved, float* bias, float gamma, void* stream) {
+  if (!p || !saved || !bias) return fail(MHL_ERR_INVALID_ARGUMENT, "NULL argument");
+  if (!(gamma >= 0.0f) || gamma != gamma) return fail(MHL_ERR_INVALID_ARGUMENT, "gamma must be a finite value >= 0");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const Dims& m = p->m;
+  const SavedLayout S = saved_layout(m);
+  const int VR = m.loopback ? m.G : 1;
+  for (int r = 0; r < VR; ++r) {
+    const char* sv = static_cast<const char*>(saved) + (size_t)r * S.total;
+    mhl::launch_update_bias((const int32_t*)(sv + S.load), m.H, m.N_e, m.T_g * m.k, gamma,
+                            bias + (size_t)r * m.H * m.N_e, s);
+    p->launches++;
+  }
+  return check_kernels(p);
 }
 
 mhl_status mhl_check_device_status(mhl_plan p) {

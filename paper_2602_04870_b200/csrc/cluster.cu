@@ -259,7 +259,23 @@ scatter_kernel(const int32_t* __restrict__ idx, const float* __restrict__ gate, 
   }
 }
 
+// aux-free bias update (R24): one thread per (h, e); sign of load - mean as an exact integer test
+__global__ void update_bias_kernel(const int32_t* __restrict__ load, int n, int N_e, int64_t total, float gamma,
+                                   float* __restrict__ bias) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int64_t d = (int64_t)load[i] * N_e - total;
+  const float sgn = d > 0 ? 1.0f : (d < 0 ? -1.0f : 0.0f);
+  bias[i] = bias[i] - gamma * sgn;
+}
+
 }  // namespace
+
+void launch_update_bias(const int32_t* load, int H, int N_e, int64_t total, float gamma, float* bias,
+                        cudaStream_t s) {
+  const int n = H * N_e;
+  if (n > 0) update_bias_kernel<<<(n + 255) / 256, 256, 0, s>>>(load, n, N_e, total, gamma, bias);
+}
 
 void launch_cluster(int H, int64_t T, int k, int N_e, const int32_t* idx, const float* gate, const int32_t* hist,
                     int32_t* tilepref, int32_t* counts, int32_t* off, int32_t* perm, int32_t* pos, int32_t* tok_s,

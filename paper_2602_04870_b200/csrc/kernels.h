@@ -48,7 +48,7 @@ bool launch_router_sm100(const void* Xs, int64_t ldx, const float* W_r, const fl
                          int N_e, int k, void* planes, int32_t* idx, float* gate, int32_t* hist, int32_t* flag,
                          int num_sms, cudaStream_t s);
 
-// ---- F4: clustering.  tilepref [H][n_rt][N_e] and counts [H][N_e] are scratch.
+// ---- F4: clustering.  tilepref [H][n_rt][N_e] is scratch; counts [H][N_e] receives the expert loads.
 void launch_cluster(int H, int64_t T, int k, int N_e, const int32_t* idx, const float* gate, const int32_t* hist,
                     int32_t* tilepref, int32_t* counts, int32_t* off, int32_t* perm, int32_t* pos, int32_t* tok_s,
                     float* gate_s, int64_t Rp, Tile* tiles, int32_t* ntiles, int max_tiles, Tile* chunks,
@@ -65,6 +65,11 @@ bool launch_expert_fwd_sm100(const Routing& rt, const void* Xs, int64_t ldx, con
 bool expert_fwd_pair_supported(int d_h, int d_e);
 bool launch_expert_fwd_pair_sm100(const Routing& rt, const void* Xs, int64_t ldx, const void* W1, const void* W2,
                                   int d_h, int d_e, void* Yrep, int num_sms, cudaStream_t s);
+
+// ---- aux-free load balancing (NEXT-2): bias[h][e] -= gamma * sign(load[h][e]*N_e - total), with
+// total = T*k the replicas per head (exact integer comparison with the mean load)
+void launch_update_bias(const int32_t* load, int H, int N_e, int64_t total, float gamma, float* bias,
+                        cudaStream_t s);
 
 // ---- F6: y[t][h*d_h+c] = sum_j Yrep[h][pos[h][t*k+j]][c]  (fixed j order), out ld = ldo.
 void launch_combine_fwd(int dtype, const Routing& rt, const void* Yrep, int d_h, void* out, int64_t ldo,

@@ -19,7 +19,8 @@ MHL_FLAG_LOOPBACK, MHL_FLAG_SIMT = 1, 2
 STATUS = {0: "MHL_OK", 1: "MHL_ERR_INVALID_ARGUMENT", 2: "MHL_ERR_CONFIG", 3: "MHL_ERR_WORKSPACE_TOO_SMALL",
           4: "MHL_ERR_UNSUPPORTED", 5: "MHL_ERR_CUDA", 6: "MHL_ERR_NCCL", 7: "MHL_ERR_NONFINITE"}
 EXPORTS = ["hp_plan_query", "mhl_get_unique_id", "hp_plan", "hp_plan_info", "hp_plan_destroy", "mhlmoe_forward",
-           "mhlmoe_backward", "mhlmoe_train_step_host", "mhl_check_device_status", "mhl_launch_count",
+           "mhlmoe_backward", "mhlmoe_train_step_host", "mhlmoe_update_bias", "mhl_check_device_status",
+           "mhl_launch_count",
            "mhl_a2a_bytes_posted", "mhl_set_step_timing", "mhl_step_times", "mhl_status_string",
            "mhl_last_error"]
 
@@ -71,6 +72,7 @@ def _load():
                                 ctypes.c_size_t, P]),
         "mhlmoe_train_step_host": (I, [P, P, P, ctypes.POINTER(mhl_weights), P, P, ctypes.POINTER(mhl_grads), P,
                                        P, P, ctypes.c_size_t, P]),
+        "mhlmoe_update_bias": (I, [P, P, P, ctypes.c_float, P]),
         "mhl_check_device_status": (I, [P]),
         "mhl_launch_count": (ctypes.c_uint64, [P]),
         "mhl_a2a_bytes_posted": (ctypes.c_uint64, [P]),
@@ -183,6 +185,12 @@ def mhlmoe_train_step_host(plan: Plan, x_host, dout_host, W, out_host, dx_host, 
                                        _ptr(dx_host), ctypes.byref(gs), _ptr(io), _ptr(saved), _ptr(workspace),
                                        workspace.numel() * workspace.element_size(), _stream(stream)),
            "mhlmoe_train_step_host")
+
+
+def mhlmoe_update_bias(plan: Plan, saved, bias, gamma: float, stream=None):
+    """Aux-free load-balancing step on the router bias (in place, device fp32 [H_loc][N_e])."""
+    _check(_lib.mhlmoe_update_bias(plan.handle, _ptr(saved), _ptr(bias), ctypes.c_float(gamma), _stream(stream)),
+           "mhlmoe_update_bias")
 
 
 def mhl_check_device_status(plan: Plan):

@@ -240,3 +240,28 @@ def test_train_step_host_matches_device_path():
         assert torch.equal(o, ro) and torch.equal(d, rd)
         for k in rg:
             assert torch.equal(g[k].cpu(), rg[k]), k
+
+
+@pytest.mark.parametrize("G", [1, 2])
+def test_update_bias_matches_oracle(G):
+    """NEXT-2 aux-free balancing: the bias after mhlmoe_update_bias equals, bit for bit, the
+    oracle's fp32 sign-rule update driven by the loads of the routing the GPU forward chose
+    (and the same under loopback HP, where each virtual rank updates its own heads)."""
+    _need_gpu()
+    from paper_2602_04870_b200 import mhlmoe as C
+    from paper_2602_04870_b200.layer import MHLatentMoE, torch_dtype, weights_to_device
+    cfg = LayerConfig("bias", T=1024, d=256, N_h=2, d_h=128, N_e=64, k=8, d_e=64, dtype="bf16")
+    W, x, _ = make_problem(cfg, 13, "conf")
+    L = MHLatentMoE(cfg.T // G, cfg.d, cfg.N_h, cfg.d_h, cfg.N_e, cfg.k, cfg.d_e, cfg.dtype, world_size=G,
+                    loopback=G > 1)
+    Wd = weights_to_device(W, cfg.dtype)
+    b0 = Wd["b"].clone()
+    _, idx, _ = L.forward(torch.from_numpy(x).to("cuda", torch_dtype(cfg.dtype)), Wd, want_routing=True)
+    C.mhlmoe_update_bias(L.plan, L.saved, Wd["b"], 1e-3)
+    torch.cuda.synchronize()
+    got = Wd["b"].cpu().numpy()
+    idx = idx.cpu().numpy()
+    for h in range(cfg.N_h):
+        load = O.expert_loads(idx[h], cfg.N_e)
+        want = O.update_bias(b0[h].cpu().numpy(), load, 1e-3)
+        np.testing.assert_array_equal(got[h], want)
