@@ -213,7 +213,7 @@ mhl_status make_dims(const mhl_config* c, Dims* m) {
   m->max_tiles = (int)mt;
   m->max_chunks = (int)((int64_t)m->H * ((m->Rp + mhl::kDwChunk - 1) / mhl::kDwChunk + m->N_e));
   const size_t router_smem = (size_t)m->el * m->d_h * mhl::kRouterTile + 4ull * m->d_h * 32 + 4ull * m->N_e;
-  const size_t rbwd_smem = 4ull * m->N_e * m->d_h + 8ull * mhl::kRouterTile * m->k;
+  const size_t rbwd_smem = 4ull * std::min<int64_t>((int64_t)m->N_e * m->d_h, 32768) + 8ull * mhl::kRouterTile * m->k;
   if (router_smem > 200 * 1024 || rbwd_smem > 200 * 1024)
     return fail(MHL_ERR_UNSUPPORTED, "d_head * N_e too large for the router kernels' shared memory");
   return MHL_OK;

@@ -10,6 +10,7 @@ namespace {
 
 constexpr int kSub = 32;    // rows per SIMT sub-tile
 constexpr int kRbwdChunk = 128;   // tokens per router-backward partial
+constexpr int kRbwdPartialFloats = 32768;   // per-block partial tile (128 KB): expert block = this / d_h
 
 // ---------------------------------------------------------------------------------------------
 // F5 (SIMT): for one 128-row expert tile, Yrep[row] = g * gelu(x W1_e^T) W2_e      (Eq. 1)
@@ -185,15 +186,18 @@ template <typename E>
 __global__ void __launch_bounds__(256)
 router_bwd_partial_kernel(const E* __restrict__ Xs, int64_t ldx, const int32_t* __restrict__ idx,
                           const float* __restrict__ gate, const float* __restrict__ dg, int64_t T, int k, int d_h,
-                          int N_e, float* __restrict__ dS, float* __restrict__ partial) {
+                          int N_e, int eblk, float* __restrict__ dS, float* __restrict__ partial) {
+  // blockIdx.z selects the expert block [e0, e0 + eblk) whose partial sums this block owns (large
+  // N_e: the paper's own 384-1536 experts per head do not fit one block's shared memory)
   extern __shared__ __align__(16) float smb[];
-  float* part = smb;                                  // [N_e][d_h]
-  float* sdS = part + (size_t)N_e * d_h;              // [128][k]
+  const int e0 = blockIdx.z * eblk, ne = min(eblk, N_e - e0);
+  float* part = smb;                                  // [ne][d_h]
+  float* sdS = part + (size_t)eblk * d_h;             // [128][k]
   int* sI = reinterpret_cast<int*>(sdS + kRbwdChunk * k);   // [128][k]
   const int chunk = blockIdx.x, h = blockIdx.y;
   const int64_t t0 = (int64_t)chunk * kRbwdChunk;
   const int nt = (int)min((int64_t)kRbwdChunk, T - t0);
-  for (int i = threadIdx.x; i < N_e * d_h; i += blockDim.x) part[i] = 0.0f;
+  for (int i = threadIdx.x; i < ne * d_h; i += blockDim.x) part[i] = 0.0f;
   for (int tt = threadIdx.x; tt < nt; tt += blockDim.x) {
     const size_t base = ((size_t)h * T + t0 + tt) * k;
     float s = 0.0f;
@@ -201,8 +205,8 @@ router_bwd_partial_kernel(const E* __restrict__ Xs, int64_t ldx, const int32_t* 
     for (int j = 0; j < k; ++j) {
       const float v = gate[base + j] * (dg[base + j] - s);
       sdS[tt * k + j] = v;
-      sI[tt * k + j] = idx[base + j];
-      dS[base + j] = v;
+      sI[tt * k + j] = idx[base + j] - e0;
+      if (blockIdx.z == 0) dS[base + j] = v;
     }
   }
   __syncthreads();
@@ -211,13 +215,13 @@ router_bwd_partial_kernel(const E* __restrict__ Xs, int64_t ldx, const int32_t* 
       const float xv = to_f(Xs[(t0 + tt) * ldx + (int64_t)h * d_h + i]);
       for (int j = 0; j < k; ++j) {
         const int e = sI[tt * k + j];
-        part[(size_t)e * d_h + i] = fmaf(xv, sdS[tt * k + j], part[(size_t)e * d_h + i]);
+        if (e >= 0 && e < ne) part[(size_t)e * d_h + i] = fmaf(xv, sdS[tt * k + j], part[(size_t)e * d_h + i]);
       }
     }
   }
   __syncthreads();
-  float* po = partial + ((size_t)h * gridDim.x + chunk) * N_e * d_h;
-  for (int i = threadIdx.x; i < N_e * d_h; i += blockDim.x) po[i] = part[i];
+  float* po = partial + (((size_t)h * gridDim.x + chunk) * N_e + e0) * d_h;
+  for (int i = threadIdx.x; i < ne * d_h; i += blockDim.x) po[i] = part[i];
 }
 
 // dW_r[h][i][e] = sum over chunks (in order) of partial[h][chunk][e][i]
@@ -301,15 +305,16 @@ void launch_router_bwd(int dtype, const void* Xs, int64_t ldx, const int32_t* id
                        int H, int64_t T, int k, int d_h, int N_e, float* dS, float* dwr_partial, float* dW_r,
                        cudaStream_t s) {
   const int n_chunks = (int)((T + kRbwdChunk - 1) / kRbwdChunk);
-  const size_t smem = sizeof(float) * ((size_t)N_e * d_h + (size_t)kRbwdChunk * k) + sizeof(int) * kRbwdChunk * k;
+  const int eblk = std::min(N_e, std::max(1, kRbwdPartialFloats / d_h));   // experts per block
+  const size_t smem = sizeof(float) * ((size_t)eblk * d_h + (size_t)kRbwdChunk * k) + sizeof(int) * kRbwdChunk * k;
   const int threads = d_h >= 256 ? 256 : ((d_h + 31) / 32) * 32;
-  dim3 grid(n_chunks, H);
+  dim3 grid(n_chunks, H, (N_e + eblk - 1) / eblk);
   if (dtype == 1) {
     auto f = router_bwd_partial_kernel<bf16>; set_smem(f, smem);
-    f<<<grid, threads, smem, s>>>((const bf16*)Xs, ldx, idx, gate, dg, T, k, d_h, N_e, dS, dwr_partial);
+    f<<<grid, threads, smem, s>>>((const bf16*)Xs, ldx, idx, gate, dg, T, k, d_h, N_e, eblk, dS, dwr_partial);
   } else {
     auto f = router_bwd_partial_kernel<float>; set_smem(f, smem);
-    f<<<grid, threads, smem, s>>>((const float*)Xs, ldx, idx, gate, dg, T, k, d_h, N_e, dS, dwr_partial);
+    f<<<grid, threads, smem, s>>>((const float*)Xs, ldx, idx, gate, dg, T, k, d_h, N_e, eblk, dS, dwr_partial);
   }
   if (dW_r) router_bwd_reduce_kernel<<<dim3(std::max(1, d_h * N_e / 256), H), 256, 0, s>>>(dwr_partial, n_chunks, d_h, N_e, dW_r);
 }

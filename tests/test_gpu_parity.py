@@ -122,6 +122,18 @@ def test_paper_head_shapes_match_oracle(N_e, k, d_e):
     _compare(cfg, W, x, dout, g)
 
 
+@pytest.mark.parametrize("N_e,k,d_e", [(384, 4, 256), (1536, 8, 128)])
+def test_paper_own_shapes_match_oracle(N_e, k, d_e):
+    """NEXT-4(a): the paper's own head shapes (d_h = 128, N_e = 384-1536 per head, Tables 4-5,
+    P:2053-P:2080): the router runs Alg. 1's online top-k over many 32-expert blocks and the
+    router backward tiles the experts; kernels outside the tcgen05 shapes take the SIMT path."""
+    _need_gpu()
+    cfg = LayerConfig("t5", T=384, d=256, N_h=2, d_h=128, N_e=N_e, k=k, d_e=d_e, dtype="bf16")
+    W, x, dout = make_problem(cfg, 14, "conf")
+    g = _run_gpu(cfg, W, x, dout)
+    _compare(cfg, W, x, dout, g)
+
+
 def test_router_strict_on_exact_subtokens():
     """W_in = 2^-1 x permutation (d = D): Xs is exact on both sides, so only the fp32
     (GPU) vs fp64 (oracle) score arithmetic differs (~1e-6).  Indices and slot order
