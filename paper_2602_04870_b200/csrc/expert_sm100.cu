@@ -58,7 +58,11 @@ struct FwdL {
   static constexpr int TMEMP = B_YEMPTY + 8;
   static constexpr int BYTES = TMEMP + 16;
   static_assert(BYTES <= 227 * 1024, "expert fwd: shared memory over the per-CTA limit");
-  static constexpr uint32_t T_H = 0, T_A = 128, T_Y = 256;
+  // TMEM columns: H [0, DE), A (bf16 pairs, DE/2 columns) x NA buffers, Y [T_Y, T_Y + DH).  At
+  // d_e = 256 (the paper's own expert width) only one A buffer fits next to H and Y.
+  static constexpr int NA = (DE + 2 * (DE / 2) + DH <= 512) ? 2 : 1;
+  static constexpr uint32_t T_H = 0, T_A = DE, T_Y = DE + NA * (DE / 2);
+  static_assert(T_Y + DH <= 512, "expert fwd: TMEM over 512 columns");
 };
 
 struct Ph {   // mbarrier phase bit
@@ -193,10 +197,10 @@ expert_fwd_sm100_kernel(const __grid_constant__ CUtensorMap w1map, const __grid_
       Ph xf[12], w1f, w2f, hfr, af[2], ye;
       int xs = 0;
       auto gemm2 = [&](int j) {
-        const int b = j & 1;
+        const int b = j % L::NA;
         const int tj = tile_at(j);
         if (!same_expert(tile_at(j - 1), tj)) mbar_wait(bar(L::B_W2F), w2f.flip());
-        mbar_wait(bar(L::B_AFULL + 8 * b), af[b].flip());
+        mbar_wait(bar(L::B_AFULL + 8 * b), af[b].flip());   // (NA = 1: b = 0 throughout)
         mbar_wait(bar(L::B_YEMPTY), ye.flip() ^ 1);
         trace_ev(g_trace_fwd, 13, j);
         tc_fence_after();
@@ -241,10 +245,10 @@ expert_fwd_sm100_kernel(const __grid_constant__ CUtensorMap w1map, const __grid_
     const uint32_t lane_off = (uint32_t)(q * 32) << 16;
     Ph hf, gd[2];
     int ys = 0;   // running count of Y blocks stored (selects the smem stage)
-    auto epi2 = [&](int j) {
-      const int b = j & 1;
+    auto epi2 = [&](int j, bool waited) {
+      const int b = j % L::NA;
       const Tile tl = tiles[tile_at(j)];
-      mbar_wait_warp(bar(L::B_G2DONE + 8 * b), gd[b].flip());
+      if (!waited) mbar_wait_warp(bar(L::B_G2DONE + 8 * b), gd[b].flip());
       if (et == 0) trace_ev(g_trace_fwd, 23, j);
       tc_fence_after();
       // 64-column blocks: TMEM -> regs -> bf16 -> smem stage (SW128) -> TMA bulk store.  The two
@@ -287,13 +291,37 @@ expert_fwd_sm100_kernel(const __grid_constant__ CUtensorMap w1map, const __grid_
       const int ti = tile_at(i);
       if (ti < 0) break;
       const Tile tl = tiles[ti];
-      const int b = i & 1;
+      const int b = i % L::NA;
       const float g = rt.gate_s[(size_t)tl.head * rt.Rp + tl.row0 + row];
       mbar_wait_warp(bar(L::B_HFULL), hf.flip());
       if (et == 0) trace_ev(g_trace_fwd, 20, i);
       tc_fence_after();
-      // epi 1: this warp's DE/2 columns of H -> registers, release H, GELU, A -> TMEM buffer b
       constexpr int NC = DE / 2;
+      if constexpr (L::NA == 1) {
+        // single A buffer: G2(i-1) must have read it; stream H 32 columns at a time (NC = 128 values
+        // would not fit in registers), release H after the last load
+        if (i >= 1) { mbar_wait_warp(bar(L::B_G2DONE), gd[0].flip()); tc_fence_after(); }
+#pragma unroll 1
+        for (int c = 0; c < NC; c += 32) {
+          uint32_t v[32], w[16];
+          tmem_ld32(tmem + L::T_H + lane_off + half * NC + c, v);
+          tmem_ld_wait();
+          if (c + 32 >= NC) { tc_fence_before(); mbar_arrive(bar(L::B_HFREE)); }
+#pragma unroll
+          for (int u = 0; u < 32; u += 2) {
+            const float2 a = __fmul2_rn(gelu2(make_float2(__uint_as_float(v[u]), __uint_as_float(v[u + 1])), nullptr),
+                                        make_float2(g, g));
+            w[u / 2] = pack_bf16x2(a.x, a.y);
+          }
+          tmem_st16(tmem + L::T_A + lane_off + half * (NC / 2) + c / 2, w);
+        }
+        tmem_st_wait();
+        tc_fence_before();
+        mbar_arrive(bar(L::B_AFULL));
+        if (i >= 1) epi2(i - 1, true);
+        continue;
+      }
+      // epi 1: this warp's DE/2 columns of H -> registers, release H, GELU, A -> TMEM buffer b
       uint32_t hv[NC];
 #pragma unroll
       for (int c = 0; c < NC; c += 32) {
@@ -324,9 +352,9 @@ expert_fwd_sm100_kernel(const __grid_constant__ CUtensorMap w1map, const __grid_
       tc_fence_before();
       mbar_arrive(bar(L::B_AFULL + 8 * b));
       if (et == 0) trace_ev(g_trace_fwd, 22, i);
-      if (i >= 1) epi2(i - 1);
+      if (i >= 1) epi2(i - 1, false);
     }
-    if (i >= 1) epi2(i - 1);
+    if (i >= 1) epi2(i - 1, false);
     if (half == 0 && lane == 0) bulk_wait_all();
   }
   tc_fence_before();
@@ -376,14 +404,15 @@ bool launch_t(const Routing& rt, const void* Xs, int64_t ldx, const void* W1, co
 
 bool expert_fwd_sm100_supported(int d_h, int d_e) {
   return (d_h == 256 && d_e == 128) || (d_h == 192 && d_e == 64) || (d_h == 256 && d_e == 64) ||
-         (d_h == 128 && d_e == 128) || (d_h == 128 && d_e == 64) || (d_h == 64 && d_e == 64);
+         (d_h == 128 && d_e == 128) || (d_h == 128 && d_e == 64) || (d_h == 64 && d_e == 64) ||
+         (d_h == 128 && d_e == 256);
 }
 
 bool launch_expert_fwd_sm100(const Routing& rt, const void* Xs, int64_t ldx, const void* W1, const void* W2, int d_h,
                              int d_e, void* Yrep, int num_sms, cudaStream_t s) {
 #define MHL_F(A, B) \
   if (d_h == A && d_e == B) return launch_t<A, B>(rt, Xs, ldx, W1, W2, Yrep, num_sms, s);
-  MHL_F(256, 128) MHL_F(256, 64) MHL_F(192, 64) MHL_F(128, 128) MHL_F(128, 64) MHL_F(64, 64)
+  MHL_F(256, 128) MHL_F(256, 64) MHL_F(192, 64) MHL_F(128, 128) MHL_F(128, 64) MHL_F(64, 64) MHL_F(128, 256)
 #undef MHL_F
   return false;
 }

@@ -82,7 +82,7 @@ def test_small_bf16_forward_matches_oracle(simt):
     _compare(cfg, W, x, dout, g, backward=False)
 
 
-@pytest.mark.parametrize("d_h,d_e", [(256, 128), (256, 64), (128, 128), (192, 64)])
+@pytest.mark.parametrize("d_h,d_e", [(256, 128), (256, 64), (128, 128), (192, 64), (128, 256)])
 def test_expert_tcgen05_matches_oracle_and_simt(d_h, d_e):
     """The tcgen05 expert kernel (default bf16 path) vs the oracle, fwd+bwd, at the
     paper's per-head shapes, ragged T; and vs the SIMT reference kernel."""
