@@ -81,8 +81,7 @@ struct Sched {
 // =============================================================================================
 // kernel 1: H, dA' -> dH, gA, dg
 // =============================================================================================
-constexpr int kProdWarps = 4, kMmaWarp = kProdWarps, kEpiWarp0 = kProdWarps + 1, kEpiWarps = 16;
-constexpr int kThreads1 = (kEpiWarp0 + kEpiWarps) * 32;
+constexpr int kEpiWarps = 16;
 constexpr int kEpiThreads = kEpiWarps * 32;
 
 template <int DH, int DE>
@@ -93,9 +92,14 @@ struct HL {
   static constexpr int W1 = 0, W2 = WB, STG = 2 * WB, RING = STG + STGB;
   static constexpr int CTRL_MAX = 3 * 1024;
   static constexpr int S_RAW = (kMaxSmem - RING - CTRL_MAX) / kChunk;
-  // a multiple of kProdWarps: chunk c -> stage c % S, warp c % kProdWarps, so every stage is only
-  // ever refilled by the warp that filled it before (its phase parity can never alias)
-  static constexpr int S = (S_RAW > 12 ? 12 : S_RAW) / kProdWarps * kProdWarps;
+  // producer warps (4, or 2 when only a 2-3 stage ring fits, at d_e = 256) and warp roles
+  static constexpr int PW = S_RAW >= 4 ? 4 : 2;
+  static constexpr int MMA_WARP = PW, EPI_WARP0 = PW + 1, THREADS = (PW + 1 + kEpiWarps) * 32;
+  // a multiple of PW: chunk c -> stage c % S, warp c % PW, so every stage is only ever refilled by
+  // the warp that filled it before (its phase parity can never alias)
+  static constexpr int S = (S_RAW > 12 ? 12 : S_RAW) / PW * PW;
+  // H and dA' accumulators (DE columns each) double-buffered when they fit twice in TMEM
+  static constexpr int NBUF = 4 * DE <= 512 ? 2 : 1;
   static constexpr int CTRL = RING + S * kChunk;
   static constexpr int B_FULL = CTRL, B_EMPTY = B_FULL + 8 * S;
   static constexpr int B_W1F = B_EMPTY + 8 * S, B_W1E = B_W1F + 8, B_W2F = B_W1E + 8, B_W2E = B_W2F + 8;
@@ -105,16 +109,17 @@ struct HL {
   static constexpr int BYTES = TMEMP + 16;
   static_assert(BYTES - CTRL <= CTRL_MAX, "control block overflow");
   static_assert(BYTES <= kMaxSmem, "K1: shared memory over the per-CTA limit");
-  static_assert(S >= kProdWarps, "ring too small");
+  static_assert(S >= PW, "ring too small");
 };
 
 template <int DH, int DE>
-__global__ void __launch_bounds__(kThreads1, 1)
+__global__ void __launch_bounds__(HL<DH, DE>::THREADS, 1)
 expert_bwd_h_kernel(const __grid_constant__ CUtensorMap w1map, const __grid_constant__ CUtensorMap w2map,
                     const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap ymap,
                     const __grid_constant__ CUtensorMap hsmap, const __grid_constant__ CUtensorMap asmap, Routing rt,
                     float* __restrict__ dg, int dbg) {
   using L = HL<DH, DE>;
+  constexpr int kProdWarps = L::PW, kMmaWarp = L::MMA_WARP, kEpiWarp0 = L::EPI_WARP0, NBUF = L::NBUF;
   TraceBuf trc = g_trace_dx;   // one load; trace_ev then costs a register test
   constexpr int S = L::S, KB = DH / 64;
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -218,17 +223,17 @@ expert_bwd_h_kernel(const __grid_constant__ CUtensorMap w1map, const __grid_cons
       for (int i = 0;; ++i) {
         const int ti = sc.at(i);
         if (ti < 0) break;
-        const int b = i & 1;
+        const int b = i % NBUF;
         const bool fresh = !sc.same_expert(sc.at(i - 1), ti);
         const bool last = !sc.same_expert(ti, sc.at(i + 1));
         if (fresh) mbar_wait(bar(L::B_W1F), w1f.flip());
-        if (i >= 2) mbar_wait(bar(L::B_HDFREE + 8 * b), hdfr[b].flip());   // epilogue read tile i-2
+        if (i >= NBUF) mbar_wait(bar(L::B_HDFREE + 8 * b), hdfr[b].flip());   // epilogue read tile i-NBUF
         tc_fence_after();
         trace_ev(trc, 40, i);
-        gemm_k(tmem + 256 * b, L::W1);
+        gemm_k(tmem + 2 * DE * b, L::W1);
         if (last && !(dbg & 1)) mma_commit(bar(L::B_W1E));
         if (fresh) mbar_wait(bar(L::B_W2F), w2f.flip());
-        gemm_k(tmem + 256 * b + 128, L::W2);
+        gemm_k(tmem + 2 * DE * b + DE, L::W2);
         if (dbg & 1) {
           mbar_arrive(bar(L::B_HDFULL + 8 * b));
           if (last) { mbar_arrive(bar(L::B_W1E)); mbar_arrive(bar(L::B_W2E)); }
@@ -250,7 +255,10 @@ expert_bwd_h_kernel(const __grid_constant__ CUtensorMap w1map, const __grid_cons
     const int q = warp & 3, cg = (warp - kEpiWarp0) >> 2;
     const int box = cg * NC / 64, bcol = cg * NC % 64;
     const bool leader = (bcol == 0 && lane == 0);
-    const int bar_box = 2 + q * L::BOXES + box, bar_dg = 2 + 4 * L::BOXES + q;
+    // named barrier ids (< 16): per (quadrant, box) only when several warps share a box
+    const int bar_box = 2 + q * L::BOXES + box, bar_dg = (WPB > 1 ? 2 + 4 * L::BOXES : 2) + q;
+    static_assert(WPB == 1 || 2 + 4 * L::BOXES + 4 <= 16, "K1: named barrier ids exhausted");
+    auto box_sync = [&]() { if constexpr (WPB > 1) named_bar_sync(bar_box, 32 * WPB); else __syncwarp(); };
     uint8_t* slot = smem + L::STG + (q * L::BOXES + box) * 4096;
     const uint32_t slot_s = sb + L::STG + (q * L::BOXES + box) * 4096;
     const int row = q * 32 + lane;
@@ -266,7 +274,7 @@ expert_bwd_h_kernel(const __grid_constant__ CUtensorMap w1map, const __grid_cons
     for (int i = 0;; ++i) {
       const int ti = sc.at(i);
       if (ti < 0) break;
-      const int b = i & 1;
+      const int b = i % NBUF;
       const Tile tl = tiles[ti];
       const size_t grow = (size_t)tl.head * Rp + tl.row0 + row;
       const int orow = (int)((size_t)tl.head * Rp + tl.row0 + q * 32);
@@ -281,8 +289,8 @@ expert_bwd_h_kernel(const __grid_constant__ CUtensorMap w1map, const __grid_cons
       for (int c = 0; c < NC; c += 16) {
         uint32_t hv[16], dv[16];
         const uint32_t col = lane_off + cg * NC + c;
-        tmem_ld16(tmem + 256 * b + col, hv);
-        tmem_ld16(tmem + 256 * b + 128 + col, dv);
+        tmem_ld16(tmem + 2 * DE * b + col, hv);
+        tmem_ld16(tmem + 2 * DE * b + DE + col, dv);
         tmem_ld_wait();
         if (c + 16 >= NC) {                       // all of this thread's TMEM reads are done
           tc_fence_before();
@@ -305,13 +313,13 @@ expert_bwd_h_kernel(const __grid_constant__ CUtensorMap w1map, const __grid_cons
       if (tid == kEpiWarp0 * 32) trace_ev(trc, 52, i);
       if (!(dbg & 4)) {
         if (leader) bulk_wait_read<0>();          // the previous tile's gA store has read the slot
-        named_bar_sync(bar_box, 32 * WPB);
+        box_sync();
         stage(dhp);
-        named_bar_sync(bar_box, 32 * WPB);
+        box_sync();
         if (leader) { tma_store_2d(&hsmap, slot_s, box * 64, orow); bulk_commit(); bulk_wait_read<0>(); }
-        named_bar_sync(bar_box, 32 * WPB);
+        box_sync();
         stage(gap);
-        named_bar_sync(bar_box, 32 * WPB);
+        box_sync();
         if (leader) { tma_store_2d(&asmap, slot_s, box * 64, orow); bulk_commit(); }
       }
       // gate cotangent: the NG column-group partial sums of this row, added in group order
@@ -510,7 +518,7 @@ bool launch_t(const Routing& rt, const void* Xs, int64_t ldx, const void* dY, in
     cudaMemcpyToSymbolAsync(g_trace_dx, &tb, sizeof(tb), 0, cudaMemcpyHostToDevice, s);
   }
   static const int dbg = getenv("MHL_DX_DBG") ? atoi(getenv("MHL_DX_DBG")) : 0;
-  k1<<<num_sms, kThreads1, HL<DH, DE>::BYTES, s>>>(w1m, w2m, gxm, gym, hsm, asm_, rt, dg, dbg);
+  k1<<<num_sms, HL<DH, DE>::THREADS, HL<DH, DE>::BYTES, s>>>(w1m, w2m, gxm, gym, hsm, asm_, rt, dg, dbg);
   if (trace_path) {
     TraceBuf tb{nullptr, 0};
     cudaMemcpyToSymbolAsync(g_trace_dx, &tb, sizeof(tb), 0, cudaMemcpyHostToDevice, s);
@@ -539,7 +547,7 @@ bool launch_expert_bwd_dx_sm100(const Routing& rt, const void* Xs, int64_t ldx, 
                                 void* gA, int num_sms, cudaStream_t s) {
 #define MHL_DX(A, B) \
   if (d_h == A && d_e == B) return launch_t<A, B>(rt, Xs, ldx, dY, ldy, W1, W2, dXrep, dg, dH, gA, num_sms, s);
-  MHL_DX(256, 128) MHL_DX(256, 64) MHL_DX(128, 128) MHL_DX(128, 64)
+  MHL_DX(256, 128) MHL_DX(256, 64) MHL_DX(128, 128) MHL_DX(128, 64) MHL_DX(128, 256)
 #undef MHL_DX
   return false;
 }
@@ -548,7 +556,7 @@ bool launch_expert_dx_gemm_sm100(const Routing& rt, const void* W1, int d_h, int
                                  int num_sms, cudaStream_t s) {
 #define MHL_DX(A, B) \
   if (d_h == A && d_e == B) return launch_gemm_t<A, B>(rt, W1, dH, dXrep, num_sms, s);
-  MHL_DX(256, 128) MHL_DX(256, 64) MHL_DX(128, 128) MHL_DX(128, 64)
+  MHL_DX(256, 128) MHL_DX(256, 64) MHL_DX(128, 128) MHL_DX(128, 64) MHL_DX(128, 256)
 #undef MHL_DX
   return false;
 }

@@ -174,7 +174,14 @@ expert_dw_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant
     for (int ci = blockIdx.x; ci < nchunks; ci += gridDim.x, ++nc) {
       mbar_wait_warp(accfull, nc & 1);
       tc_fence_after();
-      float* out = partial + ((size_t)ci * 2 + wm) * DE * DH;
+      const Tile ch = chunks[ci];
+      const int he = ch.head * rt.N_e + ch.expert;
+      // an expert with a single chunk (small segments, e.g. the paper's N_e = 384-1536 per head)
+      // is complete here: write dW directly, no partial round trip
+      const bool single = rt.ccount[he] == 1;
+      float* dWm = wm == 0 ? dW1 : dW2;
+      if (single && dWm == nullptr) { tc_fence_before(); mbar_arrive(accempty); continue; }
+      float* out = single ? dWm + (size_t)he * DE * DH : partial + ((size_t)ci * 2 + wm) * DE * DH;
       for (int m = 0; m < MH; ++m) {
         const int c = m * 128 + q * 32 + lane;
         for (int f0 = 0; f0 < DE; f0 += 32) {
@@ -187,11 +194,9 @@ expert_dw_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant
       }
       tc_fence_before();
       mbar_arrive(accempty);
-      if (dW1 == nullptr && dW2 == nullptr) continue;
+      if ((dW1 == nullptr && dW2 == nullptr) || single) continue;
       __threadfence();
       named_bar_sync(1, 256);
-      const Tile ch = chunks[ci];
-      const int he = ch.head * rt.N_e + ch.expert;
       if (ft == 0) *s_last = (atomicAdd(&done[he], 1) == rt.ccount[he] - 1);
       named_bar_sync(1, 256);
       if (*s_last) {
@@ -251,7 +256,7 @@ bool launch_dw_t(const Routing& rt, const void* Xs, int64_t ldx, const void* dY,
 
 bool expert_bwd_sm100_supported(int d_h, int d_e) {
   return (d_h == 256 && d_e == 128) || (d_h == 256 && d_e == 64) || (d_h == 128 && d_e == 128) ||
-         (d_h == 128 && d_e == 64);
+         (d_h == 128 && d_e == 64) || (d_h == 128 && d_e == 256);
 }
 
 bool launch_expert_bwd_sm100(const Routing& rt, const void* Xs, int64_t ldx, const void* dY, int64_t ldy,
@@ -268,6 +273,7 @@ bool launch_expert_bwd_sm100(const Routing& rt, const void* Xs, int64_t ldx, con
     if (do_dw && !launch_dw_t<A, B>(rt, Xs, ldx, dY, ldy, dH, gA, partial, done, dW1, dW2, num_sms, s)) ok = false; \
   }
   MHL_BWD_CASE(256, 128) else MHL_BWD_CASE(256, 64) else MHL_BWD_CASE(128, 128) else MHL_BWD_CASE(128, 64)
+  else MHL_BWD_CASE(128, 256)
 #undef MHL_BWD_CASE
   return ok;
 }

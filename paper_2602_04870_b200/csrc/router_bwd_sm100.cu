@@ -54,7 +54,9 @@ template <int DH, int NE, int KMAX>
 __global__ void __launch_bounds__(kThreads, 1)
 router_bwd_sm100_kernel(const __grid_constant__ CUtensorMap xmap, const int32_t* __restrict__ idx,
                         const float* __restrict__ gate, const float* __restrict__ dg, int64_t T, int k, int nc,
-                        float* __restrict__ dS, float* __restrict__ partial) {
+                        int N_e, float* __restrict__ dS, float* __restrict__ partial) {
+  // blockIdx.z = expert block [e0, e0 + NE) of N_e (the paper's own N_e = 384-1536 per head)
+  const int e0 = blockIdx.z * NE;
   using L = RbL<DH, NE>;
   constexpr int XS = L::XS, XB = DH / 64;
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -160,12 +162,15 @@ router_bwd_sm100_kernel(const __grid_constant__ CUtensorMap xmap, const int32_t*
         for (int j = 0; j < KMAX; ++j) {
           if (j < k) {
             const float v = gv[j] * (dv[j] - sum);
-            dso[j] = v;
-            const bf16 hi = __float2bfloat16_rn(v);
-            const bf16 lo = __float2bfloat16_rn(v - __bfloat162float(hi));
-            const uint32_t off = kmaj_off(ev[j], tt, NE);
-            *reinterpret_cast<bf16*>(bt + off) = hi;
-            *reinterpret_cast<bf16*>(bt + L::BT + off) = lo;
+            if (blockIdx.z == 0) dso[j] = v;
+            const int el = ev[j] - e0;
+            if (el >= 0 && el < NE) {
+              const bf16 hi = __float2bfloat16_rn(v);
+              const bf16 lo = __float2bfloat16_rn(v - __bfloat162float(hi));
+              const uint32_t off = kmaj_off(el, tt, NE);
+              *reinterpret_cast<bf16*>(bt + off) = hi;
+              *reinterpret_cast<bf16*>(bt + L::BT + off) = lo;
+            }
           }
         }
       }
@@ -180,7 +185,7 @@ router_bwd_sm100_kernel(const __grid_constant__ CUtensorMap xmap, const int32_t*
 #pragma unroll 1
     for (int mh = 0; mh < DH / 128; ++mh) {
       const int i = mh * 128 + q * 32 + lane;
-      float* po = partial + (((size_t)h * nc + c) * DH + i) * NE;
+      float* po = partial + (((size_t)h * nc + c) * DH + i) * N_e + e0;
 #pragma unroll 1
       for (int e0 = 0; e0 < NE; e0 += 32) {
         uint32_t v[32];
@@ -210,7 +215,7 @@ router_bwd_sum_kernel(const float* __restrict__ partial, int nc, int64_t n, floa
 
 template <int DH, int NE, int KMAX>
 bool launch_t(const void* Xs, int64_t ldx, const int32_t* idx, const float* gate, const float* dg, int H, int64_t T,
-              int k, float* dS, float* partial, int nc_target, float* dW_r, cudaStream_t s) {
+              int k, int N_e, float* dS, float* partial, int nc_target, float* dW_r, cudaStream_t s) {
   using L = RbL<DH, NE>;
   CUtensorMap xm;
   if (!make_tmap_2d_bf16(&xm, Xs, (uint64_t)T, (uint64_t)H * DH, (uint64_t)ldx * 2, kStep, 64)) return false;
@@ -218,9 +223,9 @@ bool launch_t(const void* Xs, int64_t ldx, const int32_t* idx, const float* gate
   const int nc = (int)std::max<int64_t>(1, std::min<int64_t>(nc_target, nst));
   auto kern = router_bwd_sm100_kernel<DH, NE, KMAX>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::BYTES);
-  kern<<<dim3(nc, H), kThreads, L::BYTES, s>>>(xm, idx, gate, dg, T, k, nc, dS, partial);
+  kern<<<dim3(nc, H, N_e / NE), kThreads, L::BYTES, s>>>(xm, idx, gate, dg, T, k, nc, N_e, dS, partial);
   if (dW_r) {
-    const int64_t n = (int64_t)DH * NE;
+    const int64_t n = (int64_t)DH * N_e;
     router_bwd_sum_kernel<<<dim3((unsigned)std::max<int64_t>(1, (n + 255) / 256), H), 256, 0, s>>>(partial, nc, n, dW_r);
   }
   return true;
@@ -228,27 +233,29 @@ bool launch_t(const void* Xs, int64_t ldx, const int32_t* idx, const float* gate
 
 template <int DH, int NE>
 bool launch_k(const void* Xs, int64_t ldx, const int32_t* idx, const float* gate, const float* dg, int H, int64_t T,
-              int k, float* dS, float* partial, int nc_target, float* dW_r, cudaStream_t s) {
-  if (k <= 2) return launch_t<DH, NE, 2>(Xs, ldx, idx, gate, dg, H, T, k, dS, partial, nc_target, dW_r, s);
-  if (k <= 4) return launch_t<DH, NE, 4>(Xs, ldx, idx, gate, dg, H, T, k, dS, partial, nc_target, dW_r, s);
-  if (k <= 8) return launch_t<DH, NE, 8>(Xs, ldx, idx, gate, dg, H, T, k, dS, partial, nc_target, dW_r, s);
-  return launch_t<DH, NE, 16>(Xs, ldx, idx, gate, dg, H, T, k, dS, partial, nc_target, dW_r, s);
+              int k, int N_e, float* dS, float* partial, int nc_target, float* dW_r, cudaStream_t s) {
+  if (k <= 2) return launch_t<DH, NE, 2>(Xs, ldx, idx, gate, dg, H, T, k, N_e, dS, partial, nc_target, dW_r, s);
+  if (k <= 4) return launch_t<DH, NE, 4>(Xs, ldx, idx, gate, dg, H, T, k, N_e, dS, partial, nc_target, dW_r, s);
+  if (k <= 8) return launch_t<DH, NE, 8>(Xs, ldx, idx, gate, dg, H, T, k, N_e, dS, partial, nc_target, dW_r, s);
+  return launch_t<DH, NE, 16>(Xs, ldx, idx, gate, dg, H, T, k, N_e, dS, partial, nc_target, dW_r, s);
 }
 
 }  // namespace
 
 bool router_bwd_sm100_supported(int d_h, int N_e, int k) {
-  return (d_h == 128 || d_h == 256) && (N_e == 32 || N_e == 64 || N_e == 128 || N_e == 256) && k >= 1 && k <= 16 &&
-         k <= N_e;
+  const bool blocked = N_e > 256 && N_e % 256 == 0;          // processed in blocks of 256 experts
+  return (d_h == 128 || d_h == 256) && (N_e == 32 || N_e == 64 || N_e == 128 || N_e == 256 || blocked) &&
+         k >= 1 && k <= 16 && k <= N_e;
 }
 
 bool launch_router_bwd_sm100(const void* Xs, int64_t ldx, const int32_t* idx, const float* gate, const float* dg,
                              int H, int64_t T, int k, int d_h, int N_e, float* dS, float* partial, int nc_target,
                              float* dW_r, cudaStream_t s) {
   if (T <= 0) return false;
+  const int NEB = N_e > 256 ? 256 : N_e;                      // experts per CTA block
 #define MHL_RB(A, B)        \
-  if (d_h == A && N_e == B) \
-    return launch_k<A, B>(Xs, ldx, idx, gate, dg, H, T, k, dS, partial, nc_target, dW_r, s);
+  if (d_h == A && NEB == B) \
+    return launch_k<A, B>(Xs, ldx, idx, gate, dg, H, T, k, N_e, dS, partial, nc_target, dW_r, s);
   MHL_RB(256, 32) MHL_RB(256, 64) MHL_RB(256, 128) MHL_RB(256, 256)
   MHL_RB(128, 32) MHL_RB(128, 64) MHL_RB(128, 128) MHL_RB(128, 256)
 #undef MHL_RB
