@@ -418,6 +418,11 @@ mhl_status moe_forward_local(mhl_plan p, const RankPtrs& R, void* yout, cudaStre
       if (!mhl::launch_router_sm100(Xs, m.HD, R.W_r, R.bias, m.H, m.T_g, m.d_h, m.N_e, m.k, R.ws + F.planes, idx, gate,
                                     hist, p->dflag, p->num_sms, s))
         return fail(MHL_ERR_CUDA, "router: TMA tensor-map encoding failed");
+    } else if (!m.simt && mhl::router_blk_supported(m.d_h, m.N_e, m.k)) {
+      mhl::launch_router_split(R.W_r, R.ws + F.planes, m.H, m.d_h, m.N_e, s);
+      if (!mhl::launch_router_blk_sm100(Xs, m.HD, R.ws + F.planes, R.bias, m.H, m.T_g, m.d_h, m.N_e, m.k, idx, gate,
+                                        hist, p->dflag, p->num_sms, s))
+        return fail(MHL_ERR_CUDA, "router (blocked): TMA tensor-map encoding failed");
     } else {
       mhl::launch_router_topk(m.dtype, Xs, m.HD, R.W_r, R.bias, m.H, m.T_g, m.d_h, m.N_e, m.k, idx, gate, hist,
                               p->dflag, s);

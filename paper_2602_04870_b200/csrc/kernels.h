@@ -48,6 +48,14 @@ bool launch_router_sm100(const void* Xs, int64_t ldx, const float* W_r, const fl
                          int N_e, int k, void* planes, int32_t* idx, float* gate, int32_t* hist, int32_t* flag,
                          int num_sms, cudaStream_t s);
 
+// ---- F3 for many experts (Alg. 1 over 64-expert blocks streamed through smem, d_h = 128):
+// W_r split into planes by launch_router_split first
+void launch_router_split(const float* W_r, void* planes, int H, int d_h, int N_e, cudaStream_t s);
+bool router_blk_supported(int d_h, int N_e, int k);
+bool launch_router_blk_sm100(const void* Xs, int64_t ldx, const void* planes, const float* bias, int H, int64_t T,
+                             int d_h, int N_e, int k, int32_t* idx, float* gate, int32_t* hist, int32_t* flag,
+                             int num_sms, cudaStream_t s);
+
 // ---- F4: clustering.  tilepref [H][n_rt][N_e] is scratch; counts [H][N_e] receives the expert loads.
 void launch_cluster(int H, int64_t T, int k, int N_e, const int32_t* idx, const float* gate, const int32_t* hist,
                     int32_t* tilepref, int32_t* counts, int32_t* off, int32_t* perm, int32_t* pos, int32_t* tok_s,

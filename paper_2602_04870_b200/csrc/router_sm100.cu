@@ -292,12 +292,16 @@ bool router_sm100_supported(int d_h, int N_e) {
 
 size_t router_sm100_planes_bytes(int H, int d_h, int N_e) { return (size_t)H * 3 * N_e * d_h * 2; }
 
-bool launch_router_sm100(const void* Xs, int64_t ldx, const float* W_r, const float* bias, int H, int64_t T, int d_h,
-                         int N_e, int k, void* planes, int32_t* idx, float* gate, int32_t* hist, int32_t* flag,
-                         int num_sms, cudaStream_t s) {
+void launch_router_split(const float* W_r, void* planes, int H, int d_h, int N_e, cudaStream_t s) {
   const int64_t n = (int64_t)H * d_h * N_e;
   router_split_kernel<<<(unsigned)std::min<int64_t>((n + 255) / 256, 4096), 256, 0, s>>>(W_r, (bf16*)planes, H, d_h,
                                                                                          N_e);
+}
+
+bool launch_router_sm100(const void* Xs, int64_t ldx, const float* W_r, const float* bias, int H, int64_t T, int d_h,
+                         int N_e, int k, void* planes, int32_t* idx, float* gate, int32_t* hist, int32_t* flag,
+                         int num_sms, cudaStream_t s) {
+  launch_router_split(W_r, planes, H, d_h, N_e, s);
   const bf16* pl = (const bf16*)planes;
 #define MHL_R(A, B) \
   if (d_h == A && N_e == B) return launch_k<A, B>(Xs, ldx, pl, bias, H, T, k, idx, gate, hist, flag, num_sms, s);
