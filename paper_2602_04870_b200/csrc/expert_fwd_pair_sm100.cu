@@ -75,10 +75,6 @@ __device__ __forceinline__ uint32_t map_to_rank(uint32_t saddr, uint32_t rank) {
 __device__ __forceinline__ void cluster_sync() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
-// arrive on an mbarrier given by its shared::cluster address (possibly in the peer CTA)
-__device__ __forceinline__ void mbar_arrive_cluster(uint32_t caddr) {
-  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(caddr) : "memory");
-}
 __device__ __forceinline__ void mbar_expect_tx_local(uint32_t saddr, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(saddr), "r"(bytes) : "memory");
 }
@@ -306,10 +302,17 @@ expert_fwd_pair_kernel(const __grid_constant__ CUtensorMap w1map, const __grid_c
     Ph hf, gd[2];
     int ys = 0;
     // one arrival per epilogue warp (8 per CTA) on a leader barrier once its lanes are past `fence`
+    // The leader arrives on its own barrier with a plain CTA-scope arrive; the peer with a RELAXED
+    // cluster-scope arrive: everything the leader's MMA depends on is TMEM state already settled by
+    // tcgen05.wait::ld / wait::st before the arrive, and a release.cluster arrive measured ~1-1.5 k
+    // cycles each (it made the peer's epilogue the pair's bottleneck).
     auto arrive_lead = [&](int off) {
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive_cluster(lead(off));
+      if (lane == 0) {
+        if (leader) mbar_arrive(bar(off));
+        else asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(lead(off)) : "memory");
+      }
     };
     auto epi2 = [&](int j) {
       const int b = j & 1;
