@@ -342,6 +342,269 @@ expert_bwd_h_kernel(const __grid_constant__ CUtensorMap w1map, const __grid_cons
 }
 
 // =============================================================================================
+// kernel 1 on CTA pairs (tcgen05 cta_group::2): two CTAs of a cluster take tiles 2u and 2u+1 of the
+// same expert (segments padded to tile pairs, kSegAlign = 256) and the leader issues M = 256 MMAs;
+// cta_group::2 splits each weight matrix along N (d_e), so each CTA keeps HALF of W1_e and W2_e
+// and its gather ring grows from 4 to 8 chunks.  Same epilogue as kernel 1 on each CTA's rows.
+// =============================================================================================
+template <int DH, int DE>
+struct HLP {
+  static constexpr int WH = DE * DH;                        // half of one expert matrix (bytes)
+  static constexpr int BOXES = DE / 64;
+  static constexpr int STGB = 4 * BOXES * 4096;
+  static constexpr int W1 = 0, W2 = WH, STG = 2 * WH, RING = STG + STGB;
+  static constexpr int CTRL_MAX = 3 * 1024;
+  static constexpr int S_RAW = (kMaxSmem - RING - CTRL_MAX) / kChunk;
+  static constexpr int PW = 4;
+  static constexpr int MMA_WARP = PW, EPI_WARP0 = PW + 1, THREADS = (PW + 1 + kEpiWarps) * 32;
+  static constexpr int S = (S_RAW > 12 ? 12 : S_RAW) / PW * PW;
+  static constexpr int NBUF = 4 * DE <= 512 ? 2 : 1;
+  static constexpr int CTRL = RING + S * kChunk;
+  static constexpr int B_FULL = CTRL, B_EMPTY = B_FULL + 8 * S;
+  static constexpr int B_W1F = B_EMPTY + 8 * S, B_W1E = B_W1F + 8, B_W2F = B_W1E + 8, B_W2E = B_W2F + 8;
+  static constexpr int B_HDFULL = B_W2E + 8, B_HDFREE = B_HDFULL + 16;
+  static constexpr int DG = B_HDFREE + 16;
+  static constexpr int TMEMP = DG + (kEpiWarps / 4) * BM * 4;
+  static constexpr int BYTES = TMEMP + 16;
+  static_assert(BYTES - CTRL <= CTRL_MAX, "control block overflow");
+  static_assert(BYTES <= kMaxSmem, "K1 pair: shared memory over the per-CTA limit");
+  static_assert(S >= PW, "ring too small");
+};
+
+template <int DH, int DE>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(HLP<DH, DE>::THREADS, 1)
+expert_bwd_h_pair_kernel(const __grid_constant__ CUtensorMap w1map, const __grid_constant__ CUtensorMap w2map,
+                         const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap ymap,
+                         const __grid_constant__ CUtensorMap hsmap, const __grid_constant__ CUtensorMap asmap,
+                         Routing rt, float* __restrict__ dg) {
+  using L = HLP<DH, DE>;
+  constexpr int kProdWarps = L::PW, kMmaWarp = L::MMA_WARP, kEpiWarp0 = L::EPI_WARP0, NBUF = L::NBUF;
+  constexpr int S = L::S, KB = DH / 64;
+  extern __shared__ __align__(1024) uint8_t smem[];
+  if ((smem_u32(smem) & 1023u) != 0u) __trap();
+  const uint32_t sb = smem_u32(smem);
+  auto bar = [&](int off) { return reinterpret_cast<uint64_t*>(smem + off); };
+  auto lead = [&](int off) { return map_to_rank(sb + off, 0); };
+  float* s_dg = reinterpret_cast<float*>(smem + L::DG);
+  uint32_t* s_tmem = reinterpret_cast<uint32_t*>(smem + L::TMEMP);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const uint32_t rank = cta_rank();
+  const bool leader = rank == 0;
+  const Tile* tiles = rt.tiles;
+  const int N_e = rt.N_e;
+  const int64_t Rp = rt.Rp, R = rt.T * rt.k;
+
+  if (tid == 0) {
+    for (int i = 0; i < S; ++i) { mbar_init(bar(L::B_FULL + 8 * i), 1); mbar_init(bar(L::B_EMPTY + 8 * i), 1); }
+    mbar_init(bar(L::B_W1F), 1); mbar_init(bar(L::B_W1E), 1); mbar_init(bar(L::B_W2F), 1); mbar_init(bar(L::B_W2E), 1);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(bar(L::B_HDFULL + 8 * b), 1);
+      mbar_init(bar(L::B_HDFREE + 8 * b), 2 * kEpiWarps);      // one arrival per epilogue warp of each CTA
+    }
+    fence_mbar_init();
+    tma_prefetch_desc(&w1map); tma_prefetch_desc(&w2map); tma_prefetch_desc(&xmap); tma_prefetch_desc(&ymap);
+    tma_prefetch_desc(&hsmap); tma_prefetch_desc(&asmap);
+  }
+  if (warp == kMmaWarp) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(s_tmem)) : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem = *s_tmem;
+
+  // pair-tile schedule: pair-tile u = tiles (2u, 2u+1) (same head and expert); this CTA: 2u + rank
+  const int npt = *rt.ntiles / 2;
+  constexpr int G = kTileGroup / 2 > 0 ? kTileGroup / 2 : 1;
+  const int pair = (int)blockIdx.x >> 1, npairs = (int)gridDim.x >> 1;
+  const int ngroups = (npt + G - 1) / G;
+  const int my_groups = ngroups > pair ? (ngroups - 1 - pair) / npairs + 1 : 0;
+  auto pt_at = [&](int i) -> int {
+    if (i < 0 || i >= my_groups * G) return -1;
+    const int u = (pair + (i / G) * npairs) * G + i % G;
+    return u < npt ? u : -1;
+  };
+  auto same_expert = [&](int ua, int ub) {
+    if (ua < 0 || ub < 0) return false;
+    const Tile a = tiles[2 * ua], b = tiles[2 * ub];
+    return a.head == b.head && a.expert == b.expert;
+  };
+  auto load_wh = [&](const CUtensorMap* map, int off, int foff, const Tile& t) {   // this CTA's N half
+    if (leader) mbar_expect_tx_local(sb + foff, 2 * L::WH);
+    for (int kb = 0; kb < KB; ++kb)
+      load2d_pair(sb + off + kb * (DE / 2) * 128, map, kb * 64, (t.head * N_e + t.expert) * DE + (int)rank * (DE / 2),
+                  lead(foff));
+  };
+
+  if (warp < kProdWarps) {
+    // ================================================================ producers
+    const int pw = warp;
+    Ph w1e, w2e;
+    int cnt = 0;
+    int nx[4] = {0, 0, 0, 0};
+    auto load_tok = [&](int u) {
+      if (u < 0) return;
+      const Tile t = tiles[2 * u + rank];
+      const int32_t* tk = rt.tok_s + (size_t)t.head * Rp + t.row0 + 4 * lane;
+      nx[0] = tk[0]; nx[1] = tk[1]; nx[2] = tk[2]; nx[3] = tk[3];
+    };
+    load_tok(pt_at(0));
+    for (int i = 0;; ++i) {
+      const int u = pt_at(i);
+      if (u < 0) break;
+      const Tile tl = tiles[2 * u + rank];
+      const bool fresh = !same_expert(pt_at(i - 1), u);
+      const int r0 = nx[0], r1 = nx[1], r2 = nx[2], r3 = nx[3];
+      load_tok(pt_at(i + 1));
+      if (pw == 0 && lane == 0 && fresh) {
+        mbar_wait(bar(L::B_W1E), w1e.flip() ^ 1);
+        load_wh(&w1map, L::W1, L::B_W1F, tl);
+        mbar_wait(bar(L::B_W2E), w2e.flip() ^ 1);
+        load_wh(&w2map, L::W2, L::B_W2F, tl);
+      }
+      __syncwarp();
+      for (int j = 0; j < 2 * KB; ++j, ++cnt) {
+        if (cnt % kProdWarps != pw) continue;
+        const int st = cnt % S;
+        if (lane == 0) {
+          mbar_wait(bar(L::B_EMPTY + 8 * st), ((cnt / S) & 1) ^ 1);
+          if (leader) mbar_expect_tx_local(sb + L::B_FULL + 8 * st, 2 * kChunk);
+        }
+        __syncwarp();
+        const int kb = j % KB;
+        gather4_pair(sb + L::RING + st * kChunk + lane * 4 * 128, j < KB ? &xmap : &ymap, tl.head * DH + kb * 64, r0,
+                     r1, r2, r3, lead(L::B_FULL + 8 * st));
+      }
+    }
+  } else if (warp == kMmaWarp) {
+    // ================================================================ MMA issuer (leader CTA only)
+    if (leader && lane == 0) {
+      constexpr uint32_t ID_N_DE = idesc_bf16(2 * BM, DE, 0, 0);
+      Ph w1f, w2f, hdfr[2];
+      int cnt = 0;
+      auto gemm_k = [&](uint32_t d, int woff) {
+        for (int kb = 0; kb < KB; ++kb, ++cnt) {
+          const int st = cnt % S;
+          mbar_wait(bar(L::B_FULL + 8 * st), (cnt / S) & 1);
+          tc_fence_after();
+#pragma unroll
+          for (int ks = 0; ks < 4; ++ks)
+            mma_pair(d, sdesc_sw128(sb + L::RING + st * kChunk + ks * 32, 16, 1024),
+                     sdesc_sw128(sb + woff + kb * (DE / 2) * 128 + ks * 32, 16, 1024), ID_N_DE, (kb | ks) ? 1u : 0u);
+          commit_pair(bar(L::B_EMPTY + 8 * st));
+        }
+      };
+      for (int i = 0;; ++i) {
+        const int u = pt_at(i);
+        if (u < 0) break;
+        const int b = i % NBUF;
+        const bool fresh = !same_expert(pt_at(i - 1), u);
+        const bool last = !same_expert(u, pt_at(i + 1));
+        if (fresh) mbar_wait(bar(L::B_W1F), w1f.flip());
+        if (i >= NBUF) mbar_wait(bar(L::B_HDFREE + 8 * b), hdfr[b].flip());
+        tc_fence_after();
+        gemm_k(tmem + 2 * DE * b, L::W1);
+        if (last) commit_pair(bar(L::B_W1E));
+        if (fresh) mbar_wait(bar(L::B_W2F), w2f.flip());
+        gemm_k(tmem + 2 * DE * b + DE, L::W2);
+        commit_pair(bar(L::B_HDFULL + 8 * b));
+        if (last) commit_pair(bar(L::B_W2E));
+      }
+    }
+  } else {
+    // ================================================================ epilogue (16 warps, this CTA's rows)
+    constexpr int NG = kEpiWarps / 4, NC = DE / NG, WPB = 64 / NC;
+    const int q = warp & 3, cg = (warp - kEpiWarp0) >> 2;
+    const int box = cg * NC / 64, bcol = cg * NC % 64;
+    const bool wleader = (bcol == 0 && lane == 0);
+    const int bar_box = 2 + q * L::BOXES + box, bar_dg = (WPB > 1 ? 2 + 4 * L::BOXES : 2) + q;
+    static_assert(WPB == 1 || 2 + 4 * L::BOXES + 4 <= 16, "K1 pair: named barrier ids exhausted");
+    auto box_sync = [&]() { if constexpr (WPB > 1) named_bar_sync(bar_box, 32 * WPB); else __syncwarp(); };
+    uint8_t* slot = smem + L::STG + (q * L::BOXES + box) * 4096;
+    const uint32_t slot_s = sb + L::STG + (q * L::BOXES + box) * 4096;
+    const int row = q * 32 + lane;
+    const uint32_t lane_off = (uint32_t)(q * 32) << 16;
+    Ph hd[2];
+    auto stage = [&](const uint32_t* w) {
+#pragma unroll
+      for (int c = 0; c < NC; c += 8)
+        *reinterpret_cast<uint4*>(slot + kmaj_off(lane, bcol + c, 32)) =
+            make_uint4(w[c / 2], w[c / 2 + 1], w[c / 2 + 2], w[c / 2 + 3]);
+      fence_proxy_async();
+    };
+    for (int i = 0;; ++i) {
+      const int u = pt_at(i);
+      if (u < 0) break;
+      const int b = i % NBUF;
+      const Tile tl = tiles[2 * u + rank];
+      const size_t grow = (size_t)tl.head * Rp + tl.row0 + row;
+      const int orow = (int)((size_t)tl.head * Rp + tl.row0 + q * 32);
+      const float g = rt.gate_s[grow];
+      const int rep = rt.perm[grow];
+      mbar_wait_warp(bar(L::B_HDFULL + 8 * b), hd[b].flip());
+      tc_fence_after();
+      float dgp = 0.f;
+      uint32_t dhp[NC / 2], gap[NC / 2];
+#pragma unroll
+      for (int c = 0; c < NC; c += 16) {
+        uint32_t hv[16], dv[16];
+        const uint32_t col = lane_off + cg * NC + c;
+        tmem_ld16(tmem + 2 * DE * b + col, hv);
+        tmem_ld16(tmem + 2 * DE * b + DE + col, dv);
+        tmem_ld_wait();
+        if (c + 16 >= NC) {                       // this warp's TMEM reads are done: one arrival
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) {
+            if (leader) mbar_arrive(bar(L::B_HDFREE + 8 * b));
+            else mbar_arrive_relaxed_cluster(lead(L::B_HDFREE + 8 * b));
+          }
+        }
+#pragma unroll
+        for (int x = 0; x < 16; x += 2) {
+          const float2 h2 = make_float2(__uint_as_float(hv[x]), __uint_as_float(hv[x + 1]));
+          const float2 d2 = make_float2(__uint_as_float(dv[x]), __uint_as_float(dv[x + 1]));
+          float2 gp;
+          const float2 a = gelu2(h2, &gp);
+          dgp = fmaf(a.x, d2.x, dgp);
+          dgp = fmaf(a.y, d2.y, dgp);
+          const float2 dh = __fmul2_rn(__fmul2_rn(d2, gp), make_float2(g, g));
+          const float2 ga = __fmul2_rn(a, make_float2(g, g));
+          dhp[(c + x) / 2] = pack_bf16x2(dh.x, dh.y);
+          gap[(c + x) / 2] = pack_bf16x2(ga.x, ga.y);
+        }
+      }
+      if (wleader) bulk_wait_read<0>();
+      box_sync();
+      stage(dhp);
+      box_sync();
+      if (wleader) { tma_store_2d(&hsmap, slot_s, box * 64, orow); bulk_commit(); bulk_wait_read<0>(); }
+      box_sync();
+      stage(gap);
+      box_sync();
+      if (wleader) { tma_store_2d(&asmap, slot_s, box * 64, orow); bulk_commit(); }
+      s_dg[cg * BM + row] = dgp;
+      named_bar_sync(bar_dg, 32 * NG);
+      if (cg == 0 && rep >= 0) {
+        float acc = s_dg[row];
+#pragma unroll
+        for (int x = 1; x < NG; ++x) acc += s_dg[x * BM + row];
+        dg[(size_t)tl.head * R + rep] = acc;
+      }
+      named_bar_sync(bar_dg, 32 * NG);
+    }
+    if (wleader) bulk_wait_all();
+  }
+  tc_fence_before();
+  cluster_sync();
+  if (warp == kMmaWarp) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
+  }
+}
+
+// =============================================================================================
 // kernel 2: dXrep = dH W1_e
 // =============================================================================================
 constexpr int kThreads2 = 10 * 32;
@@ -518,7 +781,19 @@ bool launch_t(const Routing& rt, const void* Xs, int64_t ldx, const void* dY, in
     cudaMemcpyToSymbolAsync(g_trace_dx, &tb, sizeof(tb), 0, cudaMemcpyHostToDevice, s);
   }
   static const int dbg = getenv("MHL_DX_DBG") ? atoi(getenv("MHL_DX_DBG")) : 0;
-  k1<<<num_sms, HL<DH, DE>::THREADS, HL<DH, DE>::BYTES, s>>>(w1m, w2m, gxm, gym, hsm, asm_, rt, dg, dbg);
+  static const bool pair = getenv("MHL_BWD_PAIR") && getenv("MHL_BWD_PAIR")[0] == '1';
+  if (pair && kSegAlign % (2 * kExpertBM) == 0 && num_sms >= 2) {
+    // CTA-pair variant: W maps with half-height boxes (each CTA loads its d_e/2 rows)
+    CUtensorMap w1h, w2h;
+    const uint64_t wr = (uint64_t)rt.H * rt.N_e * DE;
+    if (!make_tmap_2d_bf16(&w1h, W1, wr, DH, (uint64_t)DH * 2, DE / 2, 64)) return false;
+    if (!make_tmap_2d_bf16(&w2h, W2, wr, DH, (uint64_t)DH * 2, DE / 2, 64)) return false;
+    auto kp = expert_bwd_h_pair_kernel<DH, DE>;
+    cudaFuncSetAttribute(kp, cudaFuncAttributeMaxDynamicSharedMemorySize, HLP<DH, DE>::BYTES);
+    kp<<<(num_sms / 2) * 2, HLP<DH, DE>::THREADS, HLP<DH, DE>::BYTES, s>>>(w1h, w2h, gxm, gym, hsm, asm_, rt, dg);
+  } else {
+    k1<<<num_sms, HL<DH, DE>::THREADS, HL<DH, DE>::BYTES, s>>>(w1m, w2m, gxm, gym, hsm, asm_, rt, dg, dbg);
+  }
   if (trace_path) {
     TraceBuf tb{nullptr, 0};
     cudaMemcpyToSymbolAsync(g_trace_dx, &tb, sizeof(tb), 0, cudaMemcpyHostToDevice, s);
