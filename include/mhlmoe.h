@@ -54,6 +54,8 @@ typedef enum { MHL_F32 = 0, MHL_BF16 = 1 } mhl_dtype;
                                  forward/backward then take the WHOLE global problem (see below). */
 #define MHL_FLAG_SIMT     2u  /* bf16 mode: run the SIMT reference kernels instead of the
                                  tcgen05 kernels (debug/cross-check path; fp32 mode always SIMT). */
+#define MHL_FLAG_PAIR     4u  /* bf16: CTA-pair (tcgen05 cta_group::2) expert kernels; expert
+                                 segments are then padded to 256-row tile pairs   */
 
 /* Layer + HP configuration (the paper's problem statement: P:496). */
 typedef struct {

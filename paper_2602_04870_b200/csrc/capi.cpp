@@ -103,10 +103,10 @@ constexpr size_t kAlign = 256;
 inline size_t align_up(size_t v) { return (v + kAlign - 1) / kAlign * kAlign; }
 
 struct Dims {
-  int64_t T_loc, T_g, R, Rp;   // Rp: padded sorted-row capacity per head (R + N_e*kSegAlign)
+  int64_t T_loc, T_g, R, Rp;   // Rp: padded sorted-row capacity per head (R + N_e*seg_align)
   int d, N_h, d_h, N_e, k, d_e, G, H, HD, D, el, dtype, rank;
-  bool loopback, simt;
-  int n_rt, max_tiles, max_chunks;
+  bool loopback, simt, pair;
+  int n_rt, max_tiles, max_chunks, seg_align;
 };
 
 struct Bump {
@@ -198,17 +198,19 @@ mhl_status make_dims(const mhl_config* c, Dims* m) {
   if (m->R >= (int64_t)1 << 31) return fail(MHL_ERR_UNSUPPORTED, "T_glob * k must be < 2^31");
   m->d = c->d_model; m->N_h = c->n_heads; m->d_h = c->d_head; m->N_e = c->n_experts; m->d_e = c->d_expert;
   m->H = m->N_h / m->G;
-  m->Rp = m->R + (int64_t)m->N_e * mhl::kSegAlign;
-  if (m->Rp >= (int64_t)1 << 31) return fail(MHL_ERR_UNSUPPORTED, "T_glob * k + N_e * kSegAlign must be < 2^31");
+  m->Rp = m->R + (int64_t)m->N_e * 2 * mhl::kExpertBM;   // capacity for either segment alignment
+  if (m->Rp >= (int64_t)1 << 31) return fail(MHL_ERR_UNSUPPORTED, "T_glob * k + N_e * 256 must be < 2^31");
   m->HD = m->H * m->d_h;
   m->D = m->N_h * m->d_h;
   m->dtype = c->dtype;
   m->el = c->dtype == MHL_BF16 ? 2 : 4;
   m->loopback = loop;
   m->simt = (c->flags & MHL_FLAG_SIMT) != 0 || c->dtype == MHL_F32;
+  m->pair = !m->simt && (c->flags & MHL_FLAG_PAIR) != 0;
+  m->seg_align = m->pair ? 2 * mhl::kExpertBM : mhl::kExpertBM;
   m->rank = loop ? 0 : c->rank;
   m->n_rt = (int)((m->T_g + mhl::kRouterTile - 1) / mhl::kRouterTile);
-  const int64_t mt = (int64_t)m->H * ((m->R + mhl::kExpertBM - 1) / mhl::kExpertBM + (mhl::kSegAlign / mhl::kExpertBM) * m->N_e);
+  const int64_t mt = (int64_t)m->H * ((m->R + mhl::kExpertBM - 1) / mhl::kExpertBM + 2 * m->N_e);
   if (mt >= (int64_t)1 << 31) return fail(MHL_ERR_UNSUPPORTED, "too many tiles");
   m->max_tiles = (int)mt;
   m->max_chunks = (int)((int64_t)m->H * ((m->Rp + mhl::kDwChunk - 1) / mhl::kDwChunk + m->N_e));
@@ -368,7 +370,7 @@ struct RankPtrs {   // one (virtual) rank's view
 mhl::Routing routing_view(const Dims& m, const char* saved) {
   const SavedLayout S = saved_layout(m);
   mhl::Routing rt;
-  rt.H = m.H; rt.T = m.T_g; rt.k = m.k; rt.N_e = m.N_e; rt.Rp = m.Rp;
+  rt.H = m.H; rt.T = m.T_g; rt.k = m.k; rt.N_e = m.N_e; rt.Rp = m.Rp; rt.seg_align = m.seg_align;
   rt.idx = (const int32_t*)(saved + S.idx);
   rt.gate = (const float*)(saved + S.gate);
   rt.perm = (const int32_t*)(saved + S.perm);
@@ -432,7 +434,8 @@ mhl_status moe_forward_local(mhl_plan p, const RankPtrs& R, void* yout, cudaStre
     MHL_SPAN("F4_cluster");
     mhl::launch_cluster(m.H, m.T_g, m.k, m.N_e, idx, gate, hist, (int32_t*)(R.ws + F.tilepref),
                         (int32_t*)(R.saved + S.load), off, perm, pos, (int32_t*)(R.saved + S.tok_s),
-                        (float*)(R.saved + S.gate_s), m.Rp, tiles, ntiles, m.max_tiles, (mhl::Tile*)(R.saved + S.chunks),
+                        (float*)(R.saved + S.gate_s), m.Rp, m.seg_align, tiles, ntiles, m.max_tiles,
+                        (mhl::Tile*)(R.saved + S.chunks),
                         (int32_t*)(R.saved + S.nchunks), (int32_t*)(R.saved + S.cbase), (int32_t*)(R.saved + S.ccount),
                         m.max_chunks, s);
   }
@@ -442,12 +445,10 @@ mhl_status moe_forward_local(mhl_plan p, const RankPtrs& R, void* yout, cudaStre
     MHL_SPAN("F5_expert_fwd");
     // the all-zero sub-token row T: target of the padding rows of every expert tile
     MHL_CUDA(cudaMemsetAsync(R.saved + S.Xs + (size_t)m.T_g * m.HD * m.el, 0, (size_t)m.HD * m.el, s));
-    // the cta_group::2 variant is correct but measured slower at the paper shape (its epilogue's
-    // TMEM loads run ~7x slower beside pair MMAs): opt-in with MHL_FWD_PAIR=1
-    static const bool pair_off = !(getenv("MHL_FWD_PAIR") && getenv("MHL_FWD_PAIR")[0] == '1');
+    // CTA-pair (cta_group::2) kernels with MHL_FLAG_PAIR (segments padded to tile pairs)
     if (m.simt || !mhl::expert_fwd_sm100_supported(m.d_h, m.d_e)) {
       mhl::launch_expert_fwd_simt(m.dtype, rt, Xs, m.HD, R.W1, R.W2, m.d_h, m.d_e, Yrep, s);
-    } else if (!pair_off && mhl::expert_fwd_pair_supported(m.d_h, m.d_e) && p->num_sms >= 2) {
+    } else if (m.pair && mhl::expert_fwd_pair_supported(m.d_h, m.d_e) && p->num_sms >= 2) {
       if (!mhl::launch_expert_fwd_pair_sm100(rt, Xs, m.HD, R.W1, R.W2, m.d_h, m.d_e, Yrep, p->num_sms, s))
         return fail(MHL_ERR_CUDA, "expert_fwd (pair): TMA tensor-map encoding failed");
     } else if (!mhl::launch_expert_fwd_sm100(rt, Xs, m.HD, R.W1, R.W2, m.d_h, m.d_e, Yrep, p->num_sms, s)) {

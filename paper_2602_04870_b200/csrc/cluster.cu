@@ -4,8 +4,8 @@
 // deterministic, integer-exact, dropless P:566/P:977):
 //   pos(r) = off[e] + tilepref[tile(t)][e] + rank of r among the router tile's replicas of e
 // where tilepref is the exclusive scan over router tiles of the per-tile expert histogram
-// emitted by F3.  Each expert segment is padded to a multiple of kSegAlign rows (whole 128-row
-// tiles; kSegAlign = 256 would make them whole tile pairs for the cta_group::2 kernel), so the
+// emitted by F3.  Each expert segment is padded to a multiple of seg_align rows (whole 128-row
+// tiles; 256 = whole tile pairs for the cta_group::2 kernels, MHL_FLAG_PAIR), so the
 // block-sparse mask of Eq. 7 becomes a list of whole 128-row tiles; padding rows point at
 // the all-zero sub-token row (token id T) with gate 0 and contribute exactly nothing.
 // Outputs per head (Rp = padded row capacity): perm (row -> replica or -1), tok_s (row -> token
@@ -79,7 +79,7 @@ __device__ int block_exclusive_scan_1024(int v, int* s_warp, int* total) {
   return r;
 }
 
-// (2) padded per-head offsets off[h][e] (exclusive scan of the kSegAlign-padded counts), the
+// (2) padded per-head offsets off[h][e] (exclusive scan of the seg_align-padded counts), the
 // per-(h, e) tile and dW-chunk bases.  The tile list is ordered (head, part, expert, tile): expert
 // e's alignment units are cut into kTileParts contiguous parts (part p = units [p*n/P, (p+1)*n/P)),
 // and all experts' part-p tiles come before any part-(p+1) tile.  Within an expert the rows are in
@@ -91,16 +91,16 @@ __device__ int block_exclusive_scan_1024(int v, int* s_warp, int* total) {
 __global__ void __launch_bounds__(1024)
 offsets_kernel(const int32_t* __restrict__ counts, int32_t* __restrict__ off, int32_t* __restrict__ tbase,
                int32_t* __restrict__ ntiles, int H, int N_e, int max_tiles, int32_t* __restrict__ nchunks,
-               int32_t* __restrict__ cbase, int32_t* __restrict__ ccount, int max_chunks) {
+               int32_t* __restrict__ cbase, int32_t* __restrict__ ccount, int max_chunks, int seg_align) {
   __shared__ int s_warp[64];
   __shared__ int s_tot;
-  constexpr int TPS = kSegAlign / kExpertBM;                             // tiles per alignment unit
+  const int TPS = seg_align / kExpertBM;                                 // tiles per alignment unit
   const int h = blockIdx.x;
   // tiles and dW chunks of all heads before h (and of all heads, for the totals)
   int t_before = 0, c_before = 0, t_all = 0, c_all = 0;
   for (int i = threadIdx.x; i < H * N_e; i += blockDim.x) {
     const int c = counts[i];
-    const int cp = (c + kSegAlign - 1) / kSegAlign * kSegAlign;
+    const int cp = (c + seg_align - 1) / seg_align * seg_align;
     const int nt = cp / kExpertBM, nc = (cp + kDwChunk - 1) / kDwChunk;
     if (i / N_e < h) { t_before += nt; c_before += nc; }
     t_all += nt; c_all += nc;
@@ -122,7 +122,7 @@ offsets_kernel(const int32_t* __restrict__ counts, int32_t* __restrict__ off, in
     for (int base = 0; base < N_e; base += 1024) {
       const int e = base + threadIdx.x;
       const int c = (e < N_e) ? counts[(size_t)h * N_e + e] : 0;
-      const int nu = (c + kSegAlign - 1) / kSegAlign;                   // alignment units of e
+      const int nu = (c + seg_align - 1) / seg_align;                   // alignment units of e
       const int np = TPS * ((p + 1) * nu / kTileParts - p * nu / kTileParts);   // tiles in part p
       const int px = block_exclusive_scan_1024(np, s_warp, &s_tot);
       const int ptot = s_tot;
@@ -135,7 +135,7 @@ offsets_kernel(const int32_t* __restrict__ counts, int32_t* __restrict__ off, in
   for (int base = 0; base < N_e; base += 1024) {
     const int e = base + threadIdx.x;
     const int c = (e < N_e) ? counts[(size_t)h * N_e + e] : 0;
-    const int cp = (c + kSegAlign - 1) / kSegAlign * kSegAlign;         // padded segment length
+    const int cp = (c + seg_align - 1) / seg_align * seg_align;         // padded segment length
     const int rx = block_exclusive_scan_1024(cp, s_warp, &s_tot);
     const int rtot = s_tot;
     __syncthreads();
@@ -163,14 +163,14 @@ __global__ void __launch_bounds__(256)
 tiles_kernel(const int32_t* __restrict__ counts, const int32_t* __restrict__ off, const int32_t* __restrict__ tbase,
              Tile* __restrict__ tiles, int max_tiles, Tile* __restrict__ chunks, const int32_t* __restrict__ cbase,
              int max_chunks, int H, int N_e, int64_t Rp, int32_t* __restrict__ perm, int32_t* __restrict__ tok_s,
-             float* __restrict__ gate_s, int tok_zero) {
+             float* __restrict__ gate_s, int tok_zero, int seg_align) {
   const int he = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5), lane = threadIdx.x & 31;
   if (he >= H * N_e) return;
   const int h = he / N_e, e = he % N_e;
   const int c = counts[he];
-  constexpr int TPS = kSegAlign / kExpertBM;
-  const int nu = (c + kSegAlign - 1) / kSegAlign;
-  const int cp = nu * kSegAlign;
+  const int TPS = seg_align / kExpertBM;
+  const int nu = (c + seg_align - 1) / seg_align;
+  const int cp = nu * seg_align;
   const int row_off = off[(size_t)h * (N_e + 1) + e];
   for (int p = 0; p < kTileParts; ++p) {
     const int j0 = TPS * (p * nu / kTileParts), j1 = TPS * ((p + 1) * nu / kTileParts);   // unit-aligned
@@ -279,15 +279,16 @@ void launch_update_bias(const int32_t* load, int H, int N_e, int64_t total, floa
 
 void launch_cluster(int H, int64_t T, int k, int N_e, const int32_t* idx, const float* gate, const int32_t* hist,
                     int32_t* tilepref, int32_t* counts, int32_t* off, int32_t* perm, int32_t* pos, int32_t* tok_s,
-                    float* gate_s, int64_t Rp, Tile* tiles, int32_t* ntiles, int max_tiles, Tile* chunks,
-                    int32_t* nchunks, int32_t* cbase, int32_t* ccount, int max_chunks, cudaStream_t s) {
+                    float* gate_s, int64_t Rp, int seg_align, Tile* tiles, int32_t* ntiles, int max_tiles,
+                    Tile* chunks, int32_t* nchunks, int32_t* cbase, int32_t* ccount, int max_chunks, cudaStream_t s) {
   const int n_rt = (int)((T + kRouterTile - 1) / kRouterTile);
   tile_prefix_kernel<<<dim3(N_e, H), 256, 0, s>>>(hist, tilepref, counts, n_rt, N_e);
   // tile bases [H][kTileParts][N_e] live in the (otherwise unused here) tail of tilepref's scratch
   int32_t* tbase = tilepref + (size_t)H * n_rt * N_e;
-  offsets_kernel<<<H, 1024, 0, s>>>(counts, off, tbase, ntiles, H, N_e, max_tiles, nchunks, cbase, ccount, max_chunks);
+  offsets_kernel<<<H, 1024, 0, s>>>(counts, off, tbase, ntiles, H, N_e, max_tiles, nchunks, cbase, ccount, max_chunks,
+                                    seg_align);
   tiles_kernel<<<(H * N_e + 7) / 8, 256, 0, s>>>(counts, off, tbase, tiles, max_tiles, chunks, cbase, max_chunks, H,
-                                                 N_e, Rp, perm, tok_s, gate_s, (int)T);
+                                                 N_e, Rp, perm, tok_s, gate_s, (int)T, seg_align);
   scatter_kernel<<<dim3(n_rt, H), kScatterWarps * 32, sizeof(int) * kScatterWarps * N_e, s>>>(
       idx, gate, off, tilepref, perm, pos, tok_s, gate_s, T, k, N_e, n_rt, Rp);
 }

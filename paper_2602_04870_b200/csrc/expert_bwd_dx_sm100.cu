@@ -343,7 +343,7 @@ expert_bwd_h_kernel(const __grid_constant__ CUtensorMap w1map, const __grid_cons
 
 // =============================================================================================
 // kernel 1 on CTA pairs (tcgen05 cta_group::2): two CTAs of a cluster take tiles 2u and 2u+1 of the
-// same expert (segments padded to tile pairs, kSegAlign = 256) and the leader issues M = 256 MMAs;
+// same expert (segments padded to tile pairs, MHL_FLAG_PAIR) and the leader issues M = 256 MMAs;
 // cta_group::2 splits each weight matrix along N (d_e), so each CTA keeps HALF of W1_e and W2_e
 // and its gather ring grows from 4 to 8 chunks.  Same epilogue as kernel 1 on each CTA's rows.
 // =============================================================================================
@@ -781,8 +781,7 @@ bool launch_t(const Routing& rt, const void* Xs, int64_t ldx, const void* dY, in
     cudaMemcpyToSymbolAsync(g_trace_dx, &tb, sizeof(tb), 0, cudaMemcpyHostToDevice, s);
   }
   static const int dbg = getenv("MHL_DX_DBG") ? atoi(getenv("MHL_DX_DBG")) : 0;
-  static const bool pair = getenv("MHL_BWD_PAIR") && getenv("MHL_BWD_PAIR")[0] == '1';
-  if (pair && kSegAlign % (2 * kExpertBM) == 0 && num_sms >= 2) {
+  if (rt.seg_align % (2 * kExpertBM) == 0 && num_sms >= 2) {   // MHL_FLAG_PAIR: CTA-pair variant
     // CTA-pair variant: W maps with half-height boxes (each CTA loads its d_e/2 rows)
     CUtensorMap w1h, w2h;
     const uint64_t wr = (uint64_t)rt.H * rt.N_e * DE;

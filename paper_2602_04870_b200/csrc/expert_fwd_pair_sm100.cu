@@ -375,11 +375,12 @@ bool launch_t(const Routing& rt, const void* Xs, int64_t ldx, const void* W1, co
 
 bool expert_fwd_pair_supported(int d_h, int d_e) {
   // tiles 2u and 2u+1 must share an expert: segments padded to whole tile pairs
-  return kSegAlign % (2 * kExpertBM) == 0 && (d_h == 256 || d_h == 128) && (d_e == 128 || d_e == 64);
+  return (d_h == 256 || d_h == 128) && (d_e == 128 || d_e == 64);   // caller: seg_align = 256
 }
 
 bool launch_expert_fwd_pair_sm100(const Routing& rt, const void* Xs, int64_t ldx, const void* W1, const void* W2,
                                   int d_h, int d_e, void* Yrep, int num_sms, cudaStream_t s) {
+  if (rt.seg_align % (2 * kExpertBM) != 0) return false;   // tiles 2u, 2u+1 must share an expert
 #define MHL_P(A, B) \
   if (d_h == A && d_e == B) return launch_t<A, B>(rt, Xs, ldx, W1, W2, Yrep, num_sms, s);
   MHL_P(256, 128) MHL_P(256, 64) MHL_P(128, 128) MHL_P(128, 64)

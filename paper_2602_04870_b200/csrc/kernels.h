@@ -8,19 +8,18 @@ namespace mhl {
 
 constexpr int kRouterTile = 128;   // tokens per router CTA (= clustering tile of F4)
 constexpr int kExpertBM = 128;     // replica rows per expert tile (tcgen05 M)
-// Expert segments are padded to a multiple of kSegAlign rows.  2*kExpertBM makes every segment a
-// whole number of tile pairs, which the cta_group::2 forward kernel (expert_fwd_pair_sm100.cu,
-// opt-in) requires; one tile is the default (less padding, measured faster overall).
-constexpr int kSegAlign = kExpertBM;
+// Expert segments are padded to a multiple of Routing::seg_align rows: one tile (128, default) or a
+// tile pair (256, MHL_FLAG_PAIR), which the cta_group::2 kernels need (tiles 2u, 2u+1 share an expert).
 constexpr int kDwChunk = 4096;     // sorted rows per weight-gradient partial (B5 dW)
 constexpr int kTileGroup = 8;      // consecutive expert tiles a persistent CTA takes at once
 constexpr int kTileParts = 8;      // token-order parts per expert segment in the tile list (cluster.cu)
 
 // Clustered routing of one rank's local heads (F3/F4 outputs, device pointers).
-// Sorted-row arrays have a fixed per-head capacity Rp = T*k + N_e*kSegAlign (expert segments are
-// padded to whole pairs of 128-row tiles; padding rows: perm -1, tok_s = T (the all-zero row), gate_s 0).
+// Sorted-row arrays have a fixed per-head capacity Rp = T*k + N_e*seg_align (expert segments are
+// padded to whole tiles or tile pairs; padding rows: perm -1, tok_s = T (the all-zero row), gate_s 0).
 struct Routing {
   int H; int64_t T; int k; int N_e; int64_t Rp;
+  int seg_align;           // expert segments padded to a multiple of this many rows (128 or 256)
   const int32_t* idx;      // [H][T][k]  expert ids, slot order = descending biased key
   const float* gate;       // [H][T][k]
   const int32_t* perm;     // [H][Rp]    sorted row -> replica t*k+j, or -1
@@ -59,8 +58,8 @@ bool launch_router_blk_sm100(const void* Xs, int64_t ldx, const void* planes, co
 // ---- F4: clustering.  tilepref [H][n_rt][N_e] is scratch; counts [H][N_e] receives the expert loads.
 void launch_cluster(int H, int64_t T, int k, int N_e, const int32_t* idx, const float* gate, const int32_t* hist,
                     int32_t* tilepref, int32_t* counts, int32_t* off, int32_t* perm, int32_t* pos, int32_t* tok_s,
-                    float* gate_s, int64_t Rp, Tile* tiles, int32_t* ntiles, int max_tiles, Tile* chunks,
-                    int32_t* nchunks, int32_t* cbase, int32_t* ccount, int max_chunks, cudaStream_t s);
+                    float* gate_s, int64_t Rp, int seg_align, Tile* tiles, int32_t* ntiles, int max_tiles,
+                    Tile* chunks, int32_t* nchunks, int32_t* cbase, int32_t* ccount, int max_chunks, cudaStream_t s);
 
 // ---- F5: Yrep[h][row][c] = gate_s * gelu(X[tok_s] W1_e^T) W2_e for every sorted row (padding rows
 // produce zeros).  Xs holds T+1 rows, row T all-zero.  Yrep is [H][Rp][d_h].

@@ -18,12 +18,12 @@ def _need_gpu():
         pytest.skip("no GPU")
 
 
-def _run_gpu(cfg: LayerConfig, W, x, dout, G=1, simt=False, backward=True):
+def _run_gpu(cfg: LayerConfig, W, x, dout, G=1, simt=False, backward=True, pair=False):
     from paper_2602_04870_b200.layer import MHLatentMoE, torch_dtype, weights_to_device
     td = torch_dtype(cfg.dtype)
     loop = G > 1
     L = MHLatentMoE(cfg.T // G, cfg.d, cfg.N_h, cfg.d_h, cfg.N_e, cfg.k, cfg.d_e, cfg.dtype, world_size=G,
-                    loopback=loop, simt=simt)
+                    loopback=loop, simt=simt, pair=pair)
     Wd = weights_to_device(W, cfg.dtype)
     xd = torch.from_numpy(x).to("cuda", td)
     out, idx, gates = L.forward(xd, Wd, want_routing=True)
@@ -132,6 +132,23 @@ def test_paper_own_shapes_match_oracle(N_e, k, d_e):
     W, x, dout = make_problem(cfg, 14, "conf")
     g = _run_gpu(cfg, W, x, dout)
     _compare(cfg, W, x, dout, g)
+
+
+@pytest.mark.parametrize("d_h,d_e,G", [(256, 128, 1), (128, 64, 1), (256, 128, 2)])
+def test_pair_kernels_match_oracle_and_single_cta(d_h, d_e, G):
+    """MHL_FLAG_PAIR: the CTA-pair (tcgen05 cta_group::2) forward and backward expert kernels, with
+    segments padded to tile pairs, against the oracle and against the single-CTA kernels (same
+    per-row arithmetic: outputs and input gradients identical; weight gradients to 1e-6)."""
+    _need_gpu()
+    cfg = LayerConfig("pair", T=1500, d=2 * d_h, N_h=2, d_h=d_h, N_e=16, k=4, d_e=d_e, dtype="bf16")
+    W, x, dout = make_problem(cfg, 15, "conf")
+    g = _run_gpu(cfg, W, x, dout, G=G, pair=True)
+    _compare(cfg, W, x, dout, g)
+    s = _run_gpu(cfg, W, x, dout, G=G)
+    for key in ("out", "dx", "idx", "gates"):
+        np.testing.assert_array_equal(g[key], s[key], err_msg=key)
+    for key in ("dW_r", "dW1", "dW2"):
+        assert rel_err(g[key], s[key]) < 1e-6, key
 
 
 def test_router_strict_on_exact_subtokens():

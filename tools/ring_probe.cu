@@ -38,13 +38,39 @@ ring(const __grid_constant__ CUtensorMap map, const uint16_t* __restrict__ x, in
   int* stok = reinterpret_cast<int*>(empty + 16);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (tid == 0) {
-    for (int i = 0; i < S; ++i) { mbar_init(&full[i], mech == 4 ? 1 : (mech == 1 || mech == 3) ? PW : 32 * PW); mbar_init(&empty[i], 1); }
+    for (int i = 0; i < S; ++i) { mbar_init(&full[i], mech == 5 ? 32 : mech == 4 ? 1 : (mech == 1 || mech == 3) ? PW : 32 * PW); mbar_init(&empty[i], 1); }
     asm volatile("fence.mbarrier_init.release.cluster;");
   }
   __syncthreads();
   const uint32_t sb = smem_u32(smem);
   const int RPW = 128 / PW;   // rows per producer warp
-  if (mech == 4 && warp < PW) {
+  if (mech == 5 && warp < PW) {
+    // half the warps: TMA gather4 (whole chunk, 32 lanes); the other half: cp.async 16 B per lane
+    int cnt = 0;
+    for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+      const int h = t % 8;
+      const int r4[4] = {rows[(t / 8) * 128 + 4 * lane], rows[(t / 8) * 128 + 4 * lane + 1],
+                         rows[(t / 8) * 128 + 4 * lane + 2], rows[(t / 8) * 128 + 4 * lane + 3]};
+      for (int kb = 0; kb < 4; ++kb, ++cnt) {
+        if (cnt % PW != warp) continue;
+        const int st = cnt % S;
+        if (lane == 0) mbar_wait(&empty[st], ((cnt / S) & 1) ^ 1);
+        __syncwarp();
+        if (warp & 1) {
+          // cp.async: lane covers rows 4*lane..4*lane+3, 8 x 16 B each
+          for (int rr = 0; rr < 4; ++rr)
+            for (int c = 0; c < 8; ++c)
+              cp_async_16(sb + st * kChunk + kmaj(4 * lane + rr, c * 8), x + (size_t)r4[rr] * ld + h * 256 + kb * 64 + c * 8);
+          cp_async_arrive(&full[st]);
+        } else {
+          if (lane == 0) mbar_expect_tx(&full[st], kChunk);
+          __syncwarp();
+          gather4(sb + st * kChunk + 4 * lane * 128, &map, h * 256 + kb * 64, r4[0], r4[1], r4[2], r4[3], &full[st]);
+          if (lane != 0) mbar_arrive(&full[st]);   // 1 expect_tx + 31 arrivals = the 32 of a cp.async warp
+        }
+      }
+    }
+  } else if (mech == 4 && warp < PW) {
     // warp w owns every PW-th chunk; its 32 lanes each issue one gather4 (4 rows) of it
     uint32_t eph[16] = {0};
     int cnt = 0;
@@ -150,9 +176,10 @@ int main() {
   const int ntiles = (int)(n / 128) * 8;   // every head of every clustered tile: 2.1 GB gathered
   char* flush; cudaMalloc(&flush, 512 << 20);
   cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
-  for (int mech : {3, 4})
-    for (int PW : {1, 2, 4, 8})
-      for (int S : {6, 12}) {
+  for (int mech : {4})
+    for (int PW : {4, 6, 8})
+      for (int S : {4, 6, 8, 12}) {
+        if (S % PW) continue;
         const int smem = S * kChunk + 2048;
         cudaFuncSetAttribute(ring, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         float tot = 0;
