@@ -6,7 +6,7 @@
 //                              local head hl is the column block [hl*d_h, (hl+1)*d_h).
 //   send1       [G][T_loc][HD] destination-major output of F1 (G > 1 only)
 //   send2       [T_glob][HD]   = [G(dst)][T_loc][HD]: combine output, rows in global order
-//   recv2       [G(src)][T_loc][HD] -> permuted to cat [T_loc][D] (G > 1)
+//   recv2       [G(src)][T_loc][HD] -> each received block placed in its column block of cat [T_loc][D]
 //   idx, gate   [H_loc][T_glob][k];  perm/pos [H_loc][T_glob*k];  Yrep/dXrep [H_loc][T_glob*k][d_h]
 #include "../../include/mhlmoe.h"
 
@@ -118,7 +118,7 @@ struct Bump {
 struct SavedLayout { size_t Xs, idx, gate, perm, tok_s, gate_s, pos, off, tiles, ntiles, chunks, nchunks, cbase, ccount, load, cat, total; };
 // offsets inside one rank's workspace region (forward and backward alias each other)
 struct FwdLayout { size_t send1, Yrep, send2, recv2, hist, tilepref, planes, total; };
-struct BwdLayout { size_t send3, dY, dXrep, dg, dS, dH, gA, dwr_part, W_rT, send4, recv4, dXs, dw_part, dw_done, total; };
+struct BwdLayout { size_t send3, dY, dXrep, dg, dS, dS_s, dH, gA, dwr_part, W_rT, send4, recv4, dXs, dw_part, dw_done, total; };
 
 SavedLayout saved_layout(const Dims& m) {
   Bump b; SavedLayout L;
@@ -162,6 +162,7 @@ BwdLayout bwd_layout(const Dims& m) {
   L.dXrep = b.take((size_t)m.H * m.Rp * m.d_h * m.el);
   L.dg = b.take((size_t)m.H * m.R * 4);
   L.dS = b.take((size_t)m.H * m.R * 4);
+  L.dS_s = b.take((size_t)m.H * m.Rp * 4);   // dS in sorted-row order (K2's router term)
   L.dH = b.take((size_t)m.H * m.Rp * m.d_e * m.el);
   L.gA = b.take((size_t)m.H * m.Rp * m.d_e * m.el);
   L.dwr_part = b.take((size_t)m.H * m.n_rt * m.N_e * m.d_h * 4);
@@ -256,6 +257,9 @@ struct mhl_plan_s {
   cudaEvent_t ev_x = nullptr, ev_dout = nullptr, ev_fwd = nullptr, ev_out = nullptr, ev_bwd = nullptr,
               ev_dx = nullptr;
   bool io_live = false;   // a previous host step's events are recorded
+  // HP exchanges (G > 1): comm stream pipelined against the producers on the compute stream
+  cudaStream_t comm_stream = nullptr;
+  cudaEvent_t ev_prod = nullptr, ev_comm = nullptr;
   std::atomic<uint64_t> launches{0};
   uint64_t a2a_bytes_posted = 0;
   // optional per-step CUDA-event timing (mhl_set_step_timing)
@@ -322,36 +326,66 @@ struct Gemm {
 inline char* at(void* base, size_t off) { return static_cast<char*>(base) + off; }
 inline const char* at(const void* base, size_t off) { return static_cast<const char*>(base) + off; }
 
-// Equal-split all-to-all: block p of `send` ([G][blk]) goes to rank p, block q
-// of `recv` comes from rank q.  Self block by device copy.  Bytes are k-independent.
-mhl_status all_to_all(mhl_plan p, const void* send, void* recv, size_t blk_bytes, cudaStream_t s) {
-  const Dims& m = p->m;
-  const int r = m.rank;
-  MHL_CUDA(cudaMemcpyAsync(at(recv, r * blk_bytes), at(send, r * blk_bytes), blk_bytes, cudaMemcpyDeviceToDevice, s));
-  if (m.G == 1) return MHL_OK;
-  NcclApi& api = nccl();
-  MHL_NCCL(api.GroupStart());
-  for (int q = 0; q < m.G; ++q) {
-    if (q == r) continue;
-    MHL_NCCL(api.Send(at(send, q * blk_bytes), blk_bytes, ncclUint8, q, p->comm, s));
-    MHL_NCCL(api.Recv(at(recv, q * blk_bytes), blk_bytes, ncclUint8, q, p->comm, s));
-  }
-  MHL_NCCL(api.GroupEnd());
-  p->launches++;
-  p->a2a_bytes_posted += blk_bytes * (m.G - 1);
-  return MHL_OK;
-}
+// Equal-split all-to-all (P:805-P:806), pipelined with its producer.  Step
+// i = 0..G-1 sends the block rank r addresses to q = (r+i) mod G and receives the block of
+// src = (r-i) mod G, so at every step each rank's send meets its peer's receive.  produce(i)
+// enqueues on the compute stream `s` whatever writes step i's outgoing block (step 0 is the self
+// block, which its producer writes straight into place); step i's exchange waits only for that
+// producer and runs on the plan's comm stream while produce(i+1) runs on `s`.  tail() enqueues
+// more independent work on `s` (the dW_out GEMM) that overlaps the last exchanges; `s` then waits
+// for the comm stream.  Bytes are k-independent and counted per posted send.
+//   send[v]  [G][blk]   outgoing blocks of (virtual) rank v
+//   recv[v]  [G][blk]   incoming blocks (NCCL mode; loopback copies straight to their destination)
+//   place[v] optional: incoming block src is then copied into columns [src*row_bytes, ...) of the
+//            [rows][pitch] matrix place[v] (F7 -> cat, B2 -> dXs), else recv itself is the target
+struct Xfer {
+  std::vector<const char*> send;
+  std::vector<char*> recv, place;
+  size_t blk = 0;
+  int64_t rows = 0;
+  size_t row_bytes = 0, pitch = 0;
+};
 
-// loopback all-to-all among G virtual ranks: recv_q block r <- send_r block q
-mhl_status all_to_all_loop(mhl_plan p, const std::vector<const void*>& send, const std::vector<void*>& recv,
-                           size_t blk_bytes, cudaStream_t s) {
-  const int G = p->m.G;
-  for (int r = 0; r < G; ++r)
-    for (int q = 0; q < G; ++q) {
-      MHL_CUDA(cudaMemcpyAsync(at(recv[q], r * blk_bytes), at(send[r], q * blk_bytes), blk_bytes,
-                               cudaMemcpyDeviceToDevice, s));
-      if (q != r) p->a2a_bytes_posted += blk_bytes;
+template <class Produce, class Tail>
+mhl_status hp_exchange(mhl_plan p, const Xfer& X, cudaStream_t s, Produce produce, Tail tail) {
+  const Dims& m = p->m;
+  cudaStream_t cs = p->comm_stream;
+  const size_t blk = X.blk;
+  for (int i = 0; i < m.G; ++i) {
+    MHL_TRY(produce(i));
+    if (i == 0) continue;
+    MHL_CUDA(cudaEventRecord(p->ev_prod, s));
+    MHL_CUDA(cudaStreamWaitEvent(cs, p->ev_prod, 0));
+    if (m.loopback) {
+      for (int v = 0; v < m.G; ++v) {
+        const int q = (v + i) % m.G;
+        if (!X.place.empty())
+          mhl::launch_copy_rows(X.send[v] + q * blk, (int64_t)X.row_bytes, X.place[q] + v * X.row_bytes,
+                                (int64_t)X.pitch, X.rows, (int64_t)X.row_bytes, cs);
+        else
+          MHL_CUDA(cudaMemcpyAsync(X.recv[q] + v * blk, X.send[v] + q * blk, blk, cudaMemcpyDeviceToDevice, cs));
+        p->a2a_bytes_posted += blk;
+        if (!X.place.empty()) p->launches++;
+      }
+    } else {
+      const int r = m.rank, q = (r + i) % m.G, src = (r - i + m.G) % m.G;
+      NcclApi& api = nccl();
+      MHL_NCCL(api.GroupStart());
+      MHL_NCCL(api.Send(X.send[0] + q * blk, blk, ncclUint8, q, p->comm, cs));
+      MHL_NCCL(api.Recv(X.recv[0] + src * blk, blk, ncclUint8, src, p->comm, cs));
+      MHL_NCCL(api.GroupEnd());
+      p->a2a_bytes_posted += blk;
+      p->launches++;
+      if (!X.place.empty()) {
+        mhl::launch_copy_rows(X.recv[0] + src * blk, (int64_t)X.row_bytes, X.place[0] + src * X.row_bytes,
+                              (int64_t)X.pitch, X.rows, (int64_t)X.row_bytes, cs);
+        p->launches++;
+      }
     }
+  }
+  MHL_TRY(tail());
+  MHL_CUDA(cudaEventRecord(p->ev_comm, cs));
+  MHL_CUDA(cudaStreamWaitEvent(s, p->ev_comm, 0));
   return MHL_OK;
 }
 
@@ -400,7 +434,18 @@ mhl_status check_kernels(mhl_plan p) {
   return MHL_OK;
 }
 
+// B6 for tokens [t0, t0 + nT): on the tensor-core path K2 already added the router term to each
+// replica row, so B6 is the plain k-row sum (the F6 kernel); the SIMT path adds it here
+void combine_bwd(const Dims& m, const mhl::Routing& rt, const void* dXrep, const float* dS, const float* W_rT, bool tc,
+                 void* out, int64_t ldo, cudaStream_t s, int64_t t0, int64_t nT) {
+  if (tc)
+    mhl::launch_combine_fwd(m.dtype, rt, dXrep, m.d_h, out, ldo, s, t0, nT);
+  else
+    mhl::launch_combine_bwd(m.dtype, rt, dXrep, dS, W_rT, m.d_h, out, ldo, s, t0, nT);
+}
+
 // F3-F6 for one rank's local heads; input recv1 (= saved Xs), output rows into `yout` [T_g][HD]
+// (yout == nullptr: F6 is left to the caller, which runs it per HP destination block)
 mhl_status moe_forward_local(mhl_plan p, const RankPtrs& R, void* yout, cudaStream_t s) {
   const Dims& m = p->m;
   const SavedLayout S = saved_layout(m);
@@ -455,17 +500,18 @@ mhl_status moe_forward_local(mhl_plan p, const RankPtrs& R, void* yout, cudaStre
       return fail(MHL_ERR_CUDA, "expert_fwd: TMA tensor-map encoding failed");
     }
   }
-  {
+  if (yout) {
     MHL_SPAN("F6_combine");
     mhl::launch_combine_fwd(m.dtype, rt, Yrep, m.d_h, yout, m.HD, s);
   }
-  p->launches += 7;
+  p->launches += yout ? 7 : 6;
   if (R.topk_idx) MHL_CUDA(cudaMemcpyAsync(R.topk_idx, idx, (size_t)m.H * m.R * 4, cudaMemcpyDeviceToDevice, s));
   if (R.gates) MHL_CUDA(cudaMemcpyAsync(R.gates, gate, (size_t)m.H * m.R * 4, cudaMemcpyDeviceToDevice, s));
   return check_kernels(p);
 }
 
 // B5, B3, B6 for one rank's local heads; input dY [T_g][HD], output dXs rows into `dxout` [T_g][HD]
+// (dxout == nullptr: B6 is left to the caller, which runs it per HP destination block)
 mhl_status moe_backward_local(mhl_plan p, const RankPtrs& R, const void* dY, void* dxout, cudaStream_t s) {
   const Dims& m = p->m;
   const SavedLayout S = saved_layout(m);
@@ -491,20 +537,7 @@ mhl_status moe_backward_local(mhl_plan p, const RankPtrs& R, const void* dY, voi
     else
       mhl::launch_expert_bwd_simt(m.dtype, rt, Xs, m.HD, dY, m.HD, R.W1, R.W2, m.d_h, m.d_e, dXrep, dg, dH, gA, s);
   }
-  if (tc) {
-    MHL_SPAN("B5_expert_dx_gemm");
-    if (!mhl::launch_expert_dx_gemm_sm100(rt, R.W1, m.d_h, m.d_e, dH, dXrep, p->num_sms, s))
-      return fail(MHL_ERR_CUDA, "expert dX GEMM: TMA tensor-map encoding failed");
-  }
-  if (R.dW1 || R.dW2) {
-    MHL_SPAN("B5_expert_bwd_dw");
-    if (tc)
-      mhl::launch_expert_bwd_sm100(rt, Xs, m.HD, dY, m.HD, R.W1, R.W2, m.d_h, m.d_e, dXrep, dg, dH, gA,
-                                   (float*)(R.ws + B.dw_part), (int*)(R.ws + B.dw_done), R.dW1, R.dW2,
-                                   p->num_sms, s, false, true);
-    else
-      mhl::launch_expert_dw_simt(m.dtype, rt, Xs, m.HD, dY, m.HD, dH, gA, m.d_h, m.d_e, R.dW1, R.dW2, s);
-  }
+  // B3 (needs only K1's dg) runs before K2, which folds the router term dS W_r^T into dXrep
   float* W_rT = (float*)(R.ws + B.W_rT);
   {
     MHL_SPAN("B3_router_bwd");
@@ -520,13 +553,29 @@ mhl_status moe_backward_local(mhl_plan p, const RankPtrs& R, const void* dY, voi
                              (float*)(R.ws + B.dwr_part), R.dW_r, s);
     }
     mhl::launch_transpose_wr(R.W_r, W_rT, m.H, m.d_h, m.N_e, s);
+    if (tc) mhl::launch_sort_ds(rt, dS, (float*)(R.ws + B.dS_s), s);
   }
-  {
+  if (tc) {
+    MHL_SPAN("B5_expert_dx_gemm");
+    if (!mhl::launch_expert_dx_gemm_sm100(rt, R.W1, m.d_h, m.d_e, dH, dXrep, (const float*)(R.ws + B.dS_s), W_rT,
+                                          p->num_sms, s))
+      return fail(MHL_ERR_CUDA, "expert dX GEMM: TMA tensor-map encoding failed");
+  }
+  if (R.dW1 || R.dW2) {
+    MHL_SPAN("B5_expert_bwd_dw");
+    if (tc)
+      mhl::launch_expert_bwd_sm100(rt, Xs, m.HD, dY, m.HD, R.W1, R.W2, m.d_h, m.d_e, dXrep, dg, dH, gA,
+                                   (float*)(R.ws + B.dw_part), (int*)(R.ws + B.dw_done), R.dW1, R.dW2,
+                                   p->num_sms, s, false, true);
+    else
+      mhl::launch_expert_dw_simt(m.dtype, rt, Xs, m.HD, dY, m.HD, dH, gA, m.d_h, m.d_e, R.dW1, R.dW2, s);
+  }
+  if (dxout) {
     MHL_SPAN("B6_combine_bwd");
-    mhl::launch_combine_bwd(m.dtype, rt, dXrep, dS, W_rT, m.d_h, dxout, m.HD, s);
+    combine_bwd(m, rt, dXrep, dS, W_rT, tc, dxout, m.HD, s, 0, -1);
   }
-  // K1 + K2 + dW (+ its in-kernel reduce) + router (2) + transpose + combine on the tensor-core path
-  p->launches += tc ? 7 : (R.dW1 || R.dW2 ? 6 : 5);
+  // K1 + K2 + dW (+ its in-kernel reduce) + router (2) + transpose + dS sort + combine on the tensor-core path
+  p->launches += (tc ? 8 : (R.dW1 || R.dW2 ? 6 : 5)) - (dxout ? 0 : 1);
   return check_kernels(p);
 }
 
@@ -616,6 +665,12 @@ mhl_status hp_plan(const mhl_config* cfg, const uint8_t* nccl_id, mhl_plan* out)
     return cleanup(fail(MHL_ERR_CUDA, "cublasSetWorkspace"));
   if (cudaMalloc(&p->dflag, 16) != cudaSuccess || cudaMemset(p->dflag, 0, 16) != cudaSuccess)
     return cleanup(fail(MHL_ERR_CUDA, "cudaMalloc flag"));
+  if (m.G > 1) {
+    if (cudaStreamCreateWithFlags(&p->comm_stream, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&p->ev_prod, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&p->ev_comm, cudaEventDisableTiming) != cudaSuccess)
+      return cleanup(fail(MHL_ERR_CUDA, "comm stream / events"));
+  }
   if (need_nccl) {
     NcclApi& api = nccl();
     if (!api.loaded) return cleanup(fail(MHL_ERR_NCCL, "libnccl.so.2 could not be loaded"));
@@ -643,6 +698,9 @@ mhl_status hp_plan_destroy(mhl_plan p) {
   for (cudaEvent_t e : {p->ev_x, p->ev_dout, p->ev_fwd, p->ev_out, p->ev_bwd, p->ev_dx})
     if (e) cudaEventDestroy(e);
   if (p->h2d_stream) cudaStreamDestroy(p->h2d_stream);
+  if (p->comm_stream) cudaStreamDestroy(p->comm_stream);
+  for (cudaEvent_t e : {p->ev_prod, p->ev_comm})
+    if (e) cudaEventDestroy(e);
   if (p->d2h_stream) cudaStreamDestroy(p->d2h_stream);
   for (auto e : p->pool) cudaEventDestroy(e);
   delete p;
@@ -664,49 +722,61 @@ mhl_status mhlmoe_forward(mhl_plan p, const void* x, const mhl_weights* w, void*
   for (int r = 0; r < VR; ++r)
     ranks.push_back(rank_view(p, r, saved, workspace, x, out, nullptr, w, nullptr, topk_idx, gates));
   const size_t blk = (size_t)m.T_loc * m.HD * m.el;
-  // F1: Xs = x W_in^T, written destination-major (Eq. 5)
-  for (int r = 0; r < VR; ++r) {
-    MHL_SPAN("F1_proj_in");
-    const RankPtrs& R = ranks[r];
-    if (m.G == 1) {
+  if (m.G == 1) {
+    const RankPtrs& R = ranks[0];
+    {
+      MHL_SPAN("F1_proj_in");   // F1: Xs = x W_in^T (Eq. 5)
       MHL_TRY(gemm(false, true, m.T_loc, m.D, m.d, R.x, m.d, w->W_in, m.d, R.saved + S.Xs, m.D, false, 0.0f));
-    } else {
-      for (int q = 0; q < m.G; ++q)
+    }
+    MHL_TRY(moe_forward_local(p, R, R.saved + S.cat, s));   // F3-F6
+    MHL_SPAN("F8_proj_out");     // F8: out = cat W_out^T (Eq. 6)
+    MHL_TRY(gemm(false, true, m.T_loc, m.d, m.D, R.saved + S.cat, m.D, w->W_out, m.D, R.out, m.d, false, 0.0f));
+    return check_kernels(p);
+  }
+  auto rank_of = [&](int v) { return m.loopback ? v : m.rank; };
+  // F1 + F2: destination block q of Xs = x W_in[q]^T is sent as soon as its GEMM is done
+  {
+    MHL_SPAN("F1F2_proj_in_a2a");
+    Xfer X;
+    X.blk = blk;
+    for (auto& R : ranks) { X.send.push_back(R.ws + F.send1); X.recv.push_back(R.saved + S.Xs); }
+    MHL_TRY(hp_exchange(p, X, s, [&](int i) -> mhl_status {
+      for (int v = 0; v < VR; ++v) {
+        const RankPtrs& R = ranks[v];
+        const int rk = rank_of(v), q = (rk + i) % m.G;
+        char* dst = i == 0 ? R.saved + S.Xs + rk * blk : R.ws + F.send1 + q * blk;
         MHL_TRY(gemm(false, true, m.T_loc, m.HD, m.d, R.x, m.d, at(w->W_in, (size_t)q * m.HD * m.d * m.el), m.d,
-                     R.ws + F.send1 + q * blk, m.HD, false, 0.0f));
-    }
+                     dst, m.HD, false, 0.0f));
+      }
+      return MHL_OK;
+    }, [] { return MHL_OK; }));
   }
-  // F2: all-to-all #1
-  if (m.G > 1) {
-    MHL_SPAN("F2_a2a");
-    if (m.loopback) {
-      std::vector<const void*> snd; std::vector<void*> rcv;
-      for (auto& R : ranks) { snd.push_back(R.ws + F.send1); rcv.push_back(R.saved + S.Xs); }
-      MHL_TRY(all_to_all_loop(p, snd, rcv, blk, s));
-    } else {
-      MHL_TRY(all_to_all(p, ranks[0].ws + F.send1, ranks[0].saved + S.Xs, blk, s));
-    }
-  }
-  // F3-F6 per rank
-  for (int r = 0; r < VR; ++r) {
-    const RankPtrs& R = ranks[r];
-    void* yout = m.G == 1 ? (void*)(R.saved + S.cat) : (void*)(R.ws + F.send2);
-    MHL_TRY(moe_forward_local(p, R, yout, s));
-  }
-  // F7: all-to-all #2, then cat [T_loc][D]
-  if (m.G > 1) {
-    MHL_SPAN("F7_a2a_permute");
-    if (m.loopback) {
-      std::vector<const void*> snd; std::vector<void*> rcv;
-      for (auto& R : ranks) { snd.push_back(R.ws + F.send2); rcv.push_back(R.ws + F.recv2); }
-      MHL_TRY(all_to_all_loop(p, snd, rcv, blk, s));
-    } else {
-      MHL_TRY(all_to_all(p, ranks[0].ws + F.send2, ranks[0].ws + F.recv2, blk, s));
-    }
+  // F3-F5 per rank
+  for (int v = 0; v < VR; ++v) MHL_TRY(moe_forward_local(p, ranks[v], nullptr, s));
+  // F6 + F7: the combine of destination block q (its tokens' head outputs) is sent as soon as it is
+  // done; received blocks are placed in their column block of cat [T_loc][D]
+  {
+    MHL_SPAN("F6F7_combine_a2a");
+    Xfer X;
+    X.blk = blk; X.rows = m.T_loc; X.row_bytes = (size_t)m.HD * m.el; X.pitch = (size_t)m.D * m.el;
     for (auto& R : ranks) {
-      mhl::launch_permute_blocks(m.dtype, R.ws + F.recv2, R.saved + S.cat, m.G, m.T_loc, m.HD, s);
-      p->launches++;
+      X.send.push_back(R.ws + F.send2); X.recv.push_back(R.ws + F.recv2); X.place.push_back(R.saved + S.cat);
     }
+    MHL_TRY(hp_exchange(p, X, s, [&](int i) -> mhl_status {
+      for (int v = 0; v < VR; ++v) {
+        const RankPtrs& R = ranks[v];
+        const int rk = rank_of(v), q = (rk + i) % m.G;
+        const mhl::Routing rt = routing_view(m, R.saved);
+        if (i == 0)
+          mhl::launch_combine_fwd(m.dtype, rt, R.ws + F.Yrep, m.d_h, R.saved + S.cat + rk * X.row_bytes, m.D, s,
+                                  (int64_t)q * m.T_loc, m.T_loc);
+        else
+          mhl::launch_combine_fwd(m.dtype, rt, R.ws + F.Yrep, m.d_h, R.ws + F.send2 + q * blk, m.HD, s,
+                                  (int64_t)q * m.T_loc, m.T_loc);
+        p->launches++;
+      }
+      return MHL_OK;
+    }, [] { return MHL_OK; }));
   }
   // F8: out = cat W_out^T (Eq. 6)
   for (auto& R : ranks) {
@@ -730,61 +800,79 @@ mhl_status mhlmoe_backward(mhl_plan p, const void* x, const mhl_weights* w, cons
   for (int r = 0; r < VR; ++r)
     ranks.push_back(rank_view(p, r, const_cast<void*>(saved), workspace, x, dx, d_out, w, grads, nullptr, nullptr));
   const size_t blk = (size_t)m.T_loc * m.HD * m.el;
-  // B8: dcat = dout W_out (destination-major), dW_out = dout^T cat (rank partial; loopback: summed)
-  for (int r = 0; r < VR; ++r) {
-    MHL_SPAN("B8_proj_out_bwd");
-    const RankPtrs& R = ranks[r];
-    if (m.G == 1) {
+  if (m.G == 1) {
+    const RankPtrs& R = ranks[0];
+    {
+      MHL_SPAN("B8_proj_out_bwd");   // B8: dcat = dout W_out, dW_out = dout^T cat
       MHL_TRY(gemm(false, false, m.T_loc, m.D, m.d, R.dout, m.d, w->W_out, m.D, R.ws + B.dY, m.D, false, 0.0f));
-    } else {
-      for (int q = 0; q < m.G; ++q)
+      if (grads->dW_out)
+        MHL_TRY(gemm(true, false, m.d, m.D, m.T_loc, R.dout, m.d, R.saved + S.cat, m.D, grads->dW_out, m.D, true, 0.0f));
+    }
+    MHL_TRY(moe_backward_local(p, R, R.ws + B.dY, R.ws + B.dXs, s));   // B5, B3, B6
+    MHL_SPAN("B1_proj_in_bwd");      // B1: dx = dXs W_in, dW_in = dXs^T x
+    MHL_TRY(gemm(false, false, m.T_loc, m.d, m.D, R.ws + B.dXs, m.D, w->W_in, m.d, R.out, m.d, false, 0.0f));
+    if (grads->dW_in)
+      MHL_TRY(gemm(true, false, m.D, m.d, m.T_loc, R.ws + B.dXs, m.D, R.x, m.d, grads->dW_in, m.d, true, 0.0f));
+    return check_kernels(p);
+  }
+  auto rank_of = [&](int v) { return m.loopback ? v : m.rank; };
+  // B8 + B7: destination block q of dcat = dout W_out[:, q] is sent as soon as its GEMM is done; the
+  // dW_out GEMM (rank partial; loopback: summed over virtual ranks) overlaps the last exchanges
+  {
+    MHL_SPAN("B8B7_proj_out_bwd_a2a");
+    Xfer X;
+    X.blk = blk;
+    for (auto& R : ranks) { X.send.push_back(R.ws + B.send3); X.recv.push_back(R.ws + B.dY); }
+    MHL_TRY(hp_exchange(p, X, s, [&](int i) -> mhl_status {
+      for (int v = 0; v < VR; ++v) {
+        const RankPtrs& R = ranks[v];
+        const int rk = rank_of(v), q = (rk + i) % m.G;
+        char* dst = i == 0 ? R.ws + B.dY + rk * blk : R.ws + B.send3 + q * blk;
         MHL_TRY(gemm(false, false, m.T_loc, m.HD, m.d, R.dout, m.d, at(w->W_out, (size_t)q * m.HD * m.el), m.D,
-                     R.ws + B.send3 + q * blk, m.HD, false, 0.0f));
-    }
-    if (grads->dW_out)
-      MHL_TRY(gemm(true, false, m.d, m.D, m.T_loc, R.dout, m.d, R.saved + S.cat, m.D, grads->dW_out, m.D, true,
-                   r == 0 ? 0.0f : 1.0f));
+                     dst, m.HD, false, 0.0f));
+      }
+      return MHL_OK;
+    }, [&]() -> mhl_status {
+      if (grads->dW_out)
+        for (int v = 0; v < VR; ++v)
+          MHL_TRY(gemm(true, false, m.d, m.D, m.T_loc, ranks[v].dout, m.d, ranks[v].saved + S.cat, m.D,
+                       grads->dW_out, m.D, true, v == 0 ? 0.0f : 1.0f));
+      return MHL_OK;
+    }));
   }
-  // B7: all-to-all #3
-  if (m.G > 1) {
-    MHL_SPAN("B7_a2a");
-    if (m.loopback) {
-      std::vector<const void*> snd; std::vector<void*> rcv;
-      for (auto& R : ranks) { snd.push_back(R.ws + B.send3); rcv.push_back(R.ws + B.dY); }
-      MHL_TRY(all_to_all_loop(p, snd, rcv, blk, s));
-    } else {
-      MHL_TRY(all_to_all(p, ranks[0].ws + B.send3, ranks[0].ws + B.dY, blk, s));
-    }
-  }
-  // B5, B3, B6 per rank
-  for (int r = 0; r < VR; ++r) {
-    const RankPtrs& R = ranks[r];
-    void* dxout = m.G == 1 ? (void*)(R.ws + B.dXs) : (void*)(R.ws + B.send4);
-    MHL_TRY(moe_backward_local(p, R, R.ws + B.dY, dxout, s));
-  }
-  // B2: all-to-all #4, then dXs [T_loc][D]
-  if (m.G > 1) {
-    MHL_SPAN("B2_a2a_permute");
-    if (m.loopback) {
-      std::vector<const void*> snd; std::vector<void*> rcv;
-      for (auto& R : ranks) { snd.push_back(R.ws + B.send4); rcv.push_back(R.ws + B.recv4); }
-      MHL_TRY(all_to_all_loop(p, snd, rcv, blk, s));
-    } else {
-      MHL_TRY(all_to_all(p, ranks[0].ws + B.send4, ranks[0].ws + B.recv4, blk, s));
-    }
+  // B5, B3 per rank
+  for (int v = 0; v < VR; ++v) MHL_TRY(moe_backward_local(p, ranks[v], ranks[v].ws + B.dY, nullptr, s));
+  // B6 + B2: the dX combine of destination block q is sent as soon as it is done; received blocks
+  // are placed in their column block of dXs [T_loc][D]
+  {
+    MHL_SPAN("B6B2_combine_bwd_a2a");
+    Xfer X;
+    X.blk = blk; X.rows = m.T_loc; X.row_bytes = (size_t)m.HD * m.el; X.pitch = (size_t)m.D * m.el;
     for (auto& R : ranks) {
-      mhl::launch_permute_blocks(m.dtype, R.ws + B.recv4, R.ws + B.dXs, m.G, m.T_loc, m.HD, s);
-      p->launches++;
+      X.send.push_back(R.ws + B.send4); X.recv.push_back(R.ws + B.recv4); X.place.push_back(R.ws + B.dXs);
     }
+    MHL_TRY(hp_exchange(p, X, s, [&](int i) -> mhl_status {
+      for (int v = 0; v < VR; ++v) {
+        const RankPtrs& R = ranks[v];
+        const int rk = rank_of(v), q = (rk + i) % m.G;
+        const mhl::Routing rt = routing_view(m, R.saved);
+        void* dst = i == 0 ? (void*)(R.ws + B.dXs + rk * X.row_bytes) : (void*)(R.ws + B.send4 + q * blk);
+        combine_bwd(m, rt, R.ws + B.dXrep, (const float*)(R.ws + B.dS), (const float*)(R.ws + B.W_rT),
+                    !m.simt && mhl::expert_bwd_sm100_supported(m.d_h, m.d_e), dst, i == 0 ? m.D : m.HD, s,
+                    (int64_t)q * m.T_loc, m.T_loc);
+        p->launches++;
+      }
+      return MHL_OK;
+    }, [] { return MHL_OK; }));
   }
   // B1: dx = dXs W_in; dW_in = dXs^T x (rank partial; loopback: summed)
-  for (int r = 0; r < VR; ++r) {
+  for (int v = 0; v < VR; ++v) {
     MHL_SPAN("B1_proj_in_bwd");
-    const RankPtrs& R = ranks[r];
+    const RankPtrs& R = ranks[v];
     MHL_TRY(gemm(false, false, m.T_loc, m.d, m.D, R.ws + B.dXs, m.D, w->W_in, m.d, R.out, m.d, false, 0.0f));
     if (grads->dW_in)
       MHL_TRY(gemm(true, false, m.D, m.d, m.T_loc, R.ws + B.dXs, m.D, R.x, m.d, grads->dW_in, m.d, true,
-                   r == 0 ? 0.0f : 1.0f));
+                   v == 0 ? 0.0f : 1.0f));
   }
   return check_kernels(p);
 }

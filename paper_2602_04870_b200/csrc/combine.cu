@@ -40,7 +40,7 @@ template <typename E, bool BWD, int KMAX, bool SMEM_W>
 __global__ void __launch_bounds__(SMEM_W ? 512 : 256)
 combine_kernel(const E* __restrict__ rep, const int32_t* __restrict__ pos, const int32_t* __restrict__ idx,
                const float* __restrict__ dS, const float* __restrict__ W_rT, int H, int64_t T, int k, int d_h,
-               int N_e, int64_t Rp, E* __restrict__ out, int64_t ldo) {
+               int N_e, int64_t Rp, int64_t t0, int64_t nT, E* __restrict__ out, int64_t ldo) {
   constexpr int V = Vec<E>::N;
   extern __shared__ __align__(16) float s_w[];           // [N_e][d_h] when SMEM_W
   constexpr int NT = SMEM_W ? 512 : 256, NW = NT / 32, TOK = SMEM_W ? kCombTokW : kCombTok;
@@ -53,10 +53,11 @@ combine_kernel(const E* __restrict__ rep, const int32_t* __restrict__ pos, const
     __syncthreads();
   }
   const int nchunk = d_h / V;
+  // tokens [t0, t0 + nT) of the head (one HP destination block, or all T); output row = t - t0
   const int64_t tb = (int64_t)blockIdx.x * TOK;
   for (int tt = warp; tt < TOK; tt += NW) {
-    const int64_t t = tb + tt;
-    if (t >= T) break;
+    if (tb + tt >= nT) break;
+    const int64_t t = t0 + tb + tt;
     const size_t rb = (size_t)h * R + t * k;
     const int my_pos = lane < k ? pos[rb + lane] : 0;
     int my_e = 0;
@@ -119,7 +120,7 @@ combine_kernel(const E* __restrict__ rep, const int32_t* __restrict__ pos, const
 #pragma unroll
         for (int i = 0; i < V; ++i) acc[i] += racc[i];
       }
-      E* dst = out + t * ldo + (int64_t)h * d_h + ch * V;
+      E* dst = out + (t - t0) * ldo + (int64_t)h * d_h + ch * V;
       if constexpr (V == 8) {
         *reinterpret_cast<uint4*>(dst) = pack(acc);
       } else {
@@ -131,15 +132,15 @@ combine_kernel(const E* __restrict__ rep, const int32_t* __restrict__ pos, const
 
 template <typename E, bool BWD, bool SMEM_W>
 void launch_kw(const Routing& rt, const E* rep, const float* dS, const float* W_rT, int d_h, E* out, int64_t ldo,
-               cudaStream_t s) {
+               int64_t t0, int64_t nT, cudaStream_t s) {
   const int tok = SMEM_W ? kCombTokW : kCombTok;
-  const dim3 grid((unsigned)((rt.T + tok - 1) / tok), (unsigned)rt.H);
+  const dim3 grid((unsigned)((nT + tok - 1) / tok), (unsigned)rt.H);
   const size_t smem = SMEM_W ? (size_t)rt.N_e * d_h * 4 : 0;
 #define MHL_CK(KM)                                                                                          \
   {                                                                                                         \
     auto f = combine_kernel<E, BWD, KM, SMEM_W>;                                                            \
     if (smem > 48 * 1024) cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);  \
-    f<<<grid, SMEM_W ? 512 : 256, smem, s>>>(rep, rt.pos, rt.idx, dS, W_rT, rt.H, rt.T, rt.k, d_h, rt.N_e, rt.Rp, out, ldo); \
+    f<<<grid, SMEM_W ? 512 : 256, smem, s>>>(rep, rt.pos, rt.idx, dS, W_rT, rt.H, rt.T, rt.k, d_h, rt.N_e, rt.Rp, t0, nT, out, ldo); \
   }
   if (rt.k <= 2) MHL_CK(2) else if (rt.k <= 4) MHL_CK(4) else if (rt.k <= 8) MHL_CK(8) else MHL_CK(16)
 #undef MHL_CK
@@ -148,24 +149,26 @@ void launch_kw(const Routing& rt, const E* rep, const float* dS, const float* W_
 }  // namespace
 
 void launch_combine_fwd(int dtype, const Routing& rt, const void* Yrep, int d_h, void* out, int64_t ldo,
-                        cudaStream_t s) {
-  if (rt.T <= 0) return;
+                        cudaStream_t s, int64_t t0, int64_t nT) {
+  if (nT < 0) nT = rt.T - t0;
+  if (nT <= 0) return;
   if (dtype == 1)
-    launch_kw<bf16, false, false>(rt, (const bf16*)Yrep, nullptr, nullptr, d_h, (bf16*)out, ldo, s);
+    launch_kw<bf16, false, false>(rt, (const bf16*)Yrep, nullptr, nullptr, d_h, (bf16*)out, ldo, t0, nT, s);
   else
-    launch_kw<float, false, false>(rt, (const float*)Yrep, nullptr, nullptr, d_h, (float*)out, ldo, s);
+    launch_kw<float, false, false>(rt, (const float*)Yrep, nullptr, nullptr, d_h, (float*)out, ldo, t0, nT, s);
 }
 
 void launch_combine_bwd(int dtype, const Routing& rt, const void* dXrep, const float* dS, const float* W_rT, int d_h,
-                        void* out, int64_t ldo, cudaStream_t s) {
-  if (rt.T <= 0) return;
+                        void* out, int64_t ldo, cudaStream_t s, int64_t t0, int64_t nT) {
+  if (nT < 0) nT = rt.T - t0;
+  if (nT <= 0) return;
   const bool smem_w = (size_t)rt.N_e * d_h * 4 <= 96 * 1024;
   if (dtype == 1) {
-    if (smem_w) launch_kw<bf16, true, true>(rt, (const bf16*)dXrep, dS, W_rT, d_h, (bf16*)out, ldo, s);
-    else launch_kw<bf16, true, false>(rt, (const bf16*)dXrep, dS, W_rT, d_h, (bf16*)out, ldo, s);
+    if (smem_w) launch_kw<bf16, true, true>(rt, (const bf16*)dXrep, dS, W_rT, d_h, (bf16*)out, ldo, t0, nT, s);
+    else launch_kw<bf16, true, false>(rt, (const bf16*)dXrep, dS, W_rT, d_h, (bf16*)out, ldo, t0, nT, s);
   } else {
-    if (smem_w) launch_kw<float, true, true>(rt, (const float*)dXrep, dS, W_rT, d_h, (float*)out, ldo, s);
-    else launch_kw<float, true, false>(rt, (const float*)dXrep, dS, W_rT, d_h, (float*)out, ldo, s);
+    if (smem_w) launch_kw<float, true, true>(rt, (const float*)dXrep, dS, W_rT, d_h, (float*)out, ldo, t0, nT, s);
+    else launch_kw<float, true, false>(rt, (const float*)dXrep, dS, W_rT, d_h, (float*)out, ldo, t0, nT, s);
   }
 }
 

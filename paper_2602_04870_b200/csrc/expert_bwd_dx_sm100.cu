@@ -617,9 +617,11 @@ struct GL {
   static constexpr int ASTAGE = DE * BM * 2;                // one dH tile: DE/64 chunks of 16 KB
   static constexpr int W1 = 0, YS = WB, A = YS + 2 * kYStage;
   static constexpr int CTRL_MAX = 1024;
-  static constexpr int AS_RAW = (kMaxSmem - A - CTRL_MAX) / ASTAGE;
+  static constexpr int WRB = 2 * DH * 4;                     // W_r^T[h][e] rows of two tiles (router term)
+  static constexpr int AS_RAW = (kMaxSmem - A - CTRL_MAX - WRB) / ASTAGE;
   static constexpr int AS = AS_RAW > 4 ? 4 : AS_RAW;
-  static constexpr int CTRL = A + AS * ASTAGE;
+  static constexpr int WR = A + AS * ASTAGE;
+  static constexpr int CTRL = WR + WRB;
   static constexpr int B_AFULL = CTRL, B_AEMPTY = B_AFULL + 8 * AS;
   static constexpr int B_W1F = B_AEMPTY + 8 * AS, B_W1E = B_W1F + 8;
   static constexpr int B_DXFULL = B_W1E + 8, B_DXEMPTY = B_DXFULL + 16;
@@ -634,7 +636,8 @@ struct GL {
 template <int DH, int DE>
 __global__ void __launch_bounds__(kThreads2, 1)
 expert_dx_gemm_kernel(const __grid_constant__ CUtensorMap w1map, const __grid_constant__ CUtensorMap hmap,
-                      const __grid_constant__ CUtensorMap xmap, Routing rt) {
+                      const __grid_constant__ CUtensorMap xmap, Routing rt, const float* __restrict__ dS,
+                      const float* __restrict__ W_rT) {
   using L = GL<DH, DE>;
   constexpr int AS = L::AS, KB = DH / 64;
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -714,6 +717,25 @@ expert_dx_gemm_kernel(const __grid_constant__ CUtensorMap w1map, const __grid_co
     const int q = warp & 3, half = (warp - 2) >> 2;    // lane quadrant, 32-column half of a block
     const uint32_t lane_off = (uint32_t)(q * 32) << 16;
     const bool leader = (half == 0 && lane == 0);
+    const int et = tid - 64;                            // epilogue thread 0..255
+    float* s_wr = reinterpret_cast<float*>(smem + L::WR);
+    // Router term of Alg. 2 l.9, fused here so B6 is a plain k-row sum: dXrep[row] += dS_s[row] *
+    // W_r[h][:, e] (e = the tile's expert; dS_s = dS in sorted-row order, 0 on padding rows).  The
+    // next tile's W_r^T row element and dS values are fetched one tile ahead, so their L2 latency
+    // hides behind this tile's epilogue.
+    const bool rterm = dS != nullptr;
+    auto w_of = [&](int t) -> float {
+      if (!rterm || t < 0 || et >= DH) return 0.f;
+      const Tile u = tiles[t];
+      return __ldg(W_rT + ((size_t)u.head * N_e + u.expert) * DH + et);
+    };
+    auto ds_of = [&](int t) -> float {   // dS in sorted-row order (0 on padding rows)
+      if (!rterm || t < 0) return 0.f;
+      const Tile u = tiles[t];
+      return __ldg(dS + (size_t)u.head * Rp + u.row0 + q * 32 + lane);
+    };
+    float w_cur = w_of(sc.at(0));
+    float ds = ds_of(sc.at(0));
     Ph dxf[2];
     int ys = 0;
     for (int i = 0;; ++i) {
@@ -721,6 +743,14 @@ expert_dx_gemm_kernel(const __grid_constant__ CUtensorMap w1map, const __grid_co
       if (ti < 0) break;
       const int b = i & 1;
       const Tile tl = tiles[ti];
+      const int tn = sc.at(i + 1);
+      const float* wr = s_wr + b * DH;
+      if (rterm) {
+        if (et < DH) s_wr[b * DH + et] = w_cur;
+        named_bar_sync(7, kEpiThreads2);   // slot b published; slot b is rewritten only after the next barrier
+      }
+      w_cur = w_of(tn);
+      const float ds_n = ds_of(tn);
       mbar_wait_warp(bar(L::B_DXFULL + 8 * b), dxf[b].flip());
       tc_fence_after();
 #pragma unroll 1
@@ -729,6 +759,16 @@ expert_dx_gemm_kernel(const __grid_constant__ CUtensorMap w1map, const __grid_co
         uint32_t v[32];
         tmem_ld32(tmem + b * DH + lane_off + cb * 64 + half * 32, v);
         tmem_ld_wait();
+        if (rterm) {
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const float4 w4 = *reinterpret_cast<const float4*>(wr + cb * 64 + half * 32 + 4 * u);
+            v[4 * u + 0] = __float_as_uint(fmaf(ds, w4.x, __uint_as_float(v[4 * u + 0])));
+            v[4 * u + 1] = __float_as_uint(fmaf(ds, w4.y, __uint_as_float(v[4 * u + 1])));
+            v[4 * u + 2] = __float_as_uint(fmaf(ds, w4.z, __uint_as_float(v[4 * u + 2])));
+            v[4 * u + 3] = __float_as_uint(fmaf(ds, w4.w, __uint_as_float(v[4 * u + 3])));
+          }
+        }
         if (cb == KB - 1) {
           tc_fence_before();
           mbar_arrive(bar(L::B_DXEMPTY + 8 * b));
@@ -752,6 +792,7 @@ expert_dx_gemm_kernel(const __grid_constant__ CUtensorMap w1map, const __grid_co
           bulk_commit();
         }
       }
+      ds = ds_n;
     }
     if (leader) bulk_wait_all();
   }
@@ -802,7 +843,8 @@ bool launch_t(const Routing& rt, const void* Xs, int64_t ldx, const void* dY, in
 }
 
 template <int DH, int DE>
-bool launch_gemm_t(const Routing& rt, const void* W1, const void* dH, void* dXrep, int num_sms, cudaStream_t s) {
+bool launch_gemm_t(const Routing& rt, const void* W1, const void* dH, void* dXrep, const float* dS, const float* W_rT,
+                   int num_sms, cudaStream_t s) {
   CUtensorMap w1m, hm, xm;
   const uint64_t wrows = (uint64_t)rt.H * rt.N_e * DE, rows = (uint64_t)rt.H * rt.Rp;
   if (!make_tmap_2d_bf16(&w1m, W1, wrows, DH, (uint64_t)DH * 2, DE, 64)) return false;
@@ -810,7 +852,7 @@ bool launch_gemm_t(const Routing& rt, const void* W1, const void* dH, void* dXre
   if (!make_tmap_2d_bf16(&xm, dXrep, rows, DH, (uint64_t)DH * 2, 32, 64)) return false;
   auto k2 = expert_dx_gemm_kernel<DH, DE>;
   cudaFuncSetAttribute(k2, cudaFuncAttributeMaxDynamicSharedMemorySize, GL<DH, DE>::BYTES);
-  k2<<<num_sms, kThreads2, GL<DH, DE>::BYTES, s>>>(w1m, hm, xm, rt);
+  k2<<<num_sms, kThreads2, GL<DH, DE>::BYTES, s>>>(w1m, hm, xm, rt, dS, W_rT);
   return true;
 }
 
@@ -827,9 +869,9 @@ bool launch_expert_bwd_dx_sm100(const Routing& rt, const void* Xs, int64_t ldx, 
 }
 
 bool launch_expert_dx_gemm_sm100(const Routing& rt, const void* W1, int d_h, int d_e, const void* dH, void* dXrep,
-                                 int num_sms, cudaStream_t s) {
+                                 const float* dS, const float* W_rT, int num_sms, cudaStream_t s) {
 #define MHL_DX(A, B) \
-  if (d_h == A && d_e == B) return launch_gemm_t<A, B>(rt, W1, dH, dXrep, num_sms, s);
+  if (d_h == A && d_e == B) return launch_gemm_t<A, B>(rt, W1, dH, dXrep, dS, W_rT, num_sms, s);
   MHL_DX(256, 128) MHL_DX(256, 64) MHL_DX(128, 128) MHL_DX(128, 64) MHL_DX(128, 256)
 #undef MHL_DX
   return false;

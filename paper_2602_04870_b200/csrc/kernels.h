@@ -79,11 +79,14 @@ void launch_update_bias(const int32_t* load, int H, int N_e, int64_t total, floa
                         cudaStream_t s);
 
 // ---- F6: y[t][h*d_h+c] = sum_j Yrep[h][pos[h][t*k+j]][c]  (fixed j order), out ld = ldo.
+// tokens [t0, t0 + nT) (nT < 0: to the end), written to output rows 0.. (one HP destination block)
 void launch_combine_fwd(int dtype, const Routing& rt, const void* Yrep, int d_h, void* out, int64_t ldo,
-                        cudaStream_t s);
+                        cudaStream_t s, int64_t t0 = 0, int64_t nT = -1);
 
 // ---- [G][T_loc][HD] -> [T_loc][G*HD]
 void launch_permute_blocks(int dtype, const void* src, void* dst, int G, int64_t T_loc, int64_t HD, cudaStream_t s);
+// ---- rows x row_bytes from src (pitch sp) to dst (pitch dp); 16-byte aligned (HP block placement)
+void launch_copy_rows(const void* src, int64_t sp, void* dst, int64_t dp, int64_t rows, int64_t row_bytes, cudaStream_t s);
 
 // ---- B5: per sorted row dXrep [H][Rp][d_h], dH / gA [H][Rp][d_e] (zero on padding rows) and the
 // gate cotangent dg [H][T*k] (replica order); dY holds T+1 rows, row T all-zero.
@@ -97,9 +100,10 @@ bool expert_bwd_sm100_supported(int d_h, int d_e);
 bool launch_expert_bwd_dx_sm100(const Routing& rt, const void* Xs, int64_t ldx, const void* dY, int64_t ldy,
                                 const void* W1, const void* W2, int d_h, int d_e, void* dXrep, float* dg, void* dH,
                                 void* gA, int num_sms, cudaStream_t s);
-// dXrep = dH W1_e per expert tile (TMA-fed grouped GEMM, expert_bwd_dx_sm100.cu)
+// dXrep = dH W1_e (+ dS_s[h][row] W_rT[h][e] when dS_s != nullptr: the router term of Alg. 2 l.9,
+// dS_s = dS in sorted-row order [H][Rp], see launch_sort_ds) per expert tile (expert_bwd_dx_sm100.cu)
 bool launch_expert_dx_gemm_sm100(const Routing& rt, const void* W1, int d_h, int d_e, const void* dH, void* dXrep,
-                                 int num_sms, cudaStream_t s);
+                                 const float* dS, const float* W_rT, int num_sms, cudaStream_t s);
 // tcgen05 dX kernel (dXrep, dg, dH, gA) and/or dW kernel (chunk partials + in-kernel ordered
 // reduce; `done` = H*N_e int counters, zeroed by the launch)
 bool launch_expert_bwd_sm100(const Routing& rt, const void* Xs, int64_t ldx, const void* dY, int64_t ldy,
@@ -120,11 +124,14 @@ bool launch_router_bwd_sm100(const void* Xs, int64_t ldx, const int32_t* idx, co
                              int H, int64_t T, int k, int d_h, int N_e, float* dS, float* partial, int nc_target,
                              float* dW_r, cudaStream_t s);
 
+// ---- dS_s[h][pos(t,j)] = dS[h][t][j], 0 on padding rows (zeroes dS_s first)
+void launch_sort_ds(const Routing& rt, const float* dS, float* dS_s, cudaStream_t s);
+
 // ---- W_rT[h][e][i] = W_r[h][i][e]
 void launch_transpose_wr(const float* W_r, float* W_rT, int H, int d_h, int N_e, cudaStream_t s);
 
 // ---- B6: dXs[t][h*d_h+c] = sum_j dXrep[h][pos][c] + sum_j dS[h][t][j] * W_rT[h][idx][c]
 void launch_combine_bwd(int dtype, const Routing& rt, const void* dXrep, const float* dS, const float* W_rT, int d_h,
-                        void* out, int64_t ldo, cudaStream_t s);
+                        void* out, int64_t ldo, cudaStream_t s, int64_t t0 = 0, int64_t nT = -1);
 
 }  // namespace mhl

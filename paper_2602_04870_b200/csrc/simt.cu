@@ -292,6 +292,42 @@ void launch_expert_dw_simt(int dtype, const Routing& rt, const void* Xs, int64_t
                                                           (const float*)dH, (const float*)gA, d_h, d_e, dW1, dW2);
 }
 
+// HP block placement (F7 / B2 receive side): rows x row_bytes, 16 bytes per thread per step.
+__global__ void __launch_bounds__(256)
+copy_rows_kernel(const uint4* __restrict__ src, int64_t sp, uint4* __restrict__ dst, int64_t dp, int64_t rows, int64_t w) {
+  const int64_t total = rows * w;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / w, c = i - r * w;
+    dst[r * dp + c] = src[r * sp + c];
+  }
+}
+
+void launch_copy_rows(const void* src, int64_t sp, void* dst, int64_t dp, int64_t rows, int64_t row_bytes, cudaStream_t s) {
+  const int64_t w = row_bytes / 16, total = rows * w;
+  if (total <= 0) return;
+  const int blocks = (int)std::min<int64_t>((total + 255) / 256, 148 * 8);
+  copy_rows_kernel<<<blocks, 256, 0, s>>>((const uint4*)src, sp / 16, (uint4*)dst, dp / 16, rows, w);
+}
+
+// dS in sorted-row order for the router term fused into the dX GEMM (K2)
+__global__ void __launch_bounds__(256)
+sort_ds_kernel(const float* __restrict__ dS, const int32_t* __restrict__ pos, int64_t R, int64_t Rp, int H,
+               float* __restrict__ dS_s) {
+  const int64_t total = (int64_t)H * R;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t h = i / R;
+    dS_s[h * Rp + pos[i]] = dS[i];
+  }
+}
+
+void launch_sort_ds(const Routing& rt, const float* dS, float* dS_s, cudaStream_t s) {
+  cudaMemsetAsync(dS_s, 0, (size_t)rt.H * rt.Rp * 4, s);
+  const int64_t total = (int64_t)rt.H * rt.T * rt.k;
+  if (total <= 0) return;
+  const int blocks = (int)std::min<int64_t>((total + 255) / 256, 148 * 8);
+  sort_ds_kernel<<<blocks, 256, 0, s>>>(dS, rt.pos, rt.T * rt.k, rt.Rp, rt.H, dS_s);
+}
+
 void launch_permute_blocks(int dtype, const void* src, void* dst, int G, int64_t T_loc, int64_t HD, cudaStream_t s) {
   const int64_t total = (int64_t)G * T_loc * HD;
   const int blocks = (int)std::min<int64_t>((total + 255) / 256, 148 * 16);

@@ -1,0 +1,5 @@
+TAG=$1
+python -c "import __graft_entry__ as g; g.build(); g.smoke()" > gpurun_out/${TAG}_smoke.log 2>&1; echo smoke rc=$?; tail -1 gpurun_out/${TAG}_smoke.log | cut -c1-200
+timeout 900 python -m pytest tests -q -m gpu -x > gpurun_out/${TAG}_gpu_tests.log 2>&1; echo tests rc=$?; tail -15 gpurun_out/${TAG}_gpu_tests.log
+timeout 600 python bench.py --steps 10 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/${TAG}_bench.json 2> gpurun_out/${TAG}_bench.err; echo bench rc=$?
+tail -1 gpurun_out/${TAG}_bench.json | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(d['ms_per_step'], d['step_breakdown_ms'])"
