@@ -309,9 +309,11 @@ def main():
         oh = torch.empty_like(xh).pin_memory(); gh = torch.empty_like(xh).pin_memory()
         io = torch.empty(L.info["io_bytes"], dtype=torch.uint8, device=dev)
         def e2e_step():
-            C.mhlmoe_train_step_host(L.plan, xh, dh, Wd, oh, gh, grads, io, L.saved, L.workspace, stream)
-        e2e_step(); torch.cuda.synchronize(dev)
-        ne = max(2, args.steps // 2)
+            # steps pipelined through the host link: step i+1's uploads overlap step i's backward and
+            # downloads; mhl_host_drain (below, inside the timed region) waits for every download
+            C.mhlmoe_train_step_host_pipelined(L.plan, xh, dh, Wd, oh, gh, grads, io, L.saved, L.workspace, stream)
+        e2e_step(); C.mhl_host_drain(L.plan, stream); torch.cuda.synchronize(dev)
+        ne = max(3, args.steps)
         if G > 1:
             dist.barrier()
         torch.cuda.synchronize(dev)
@@ -319,6 +321,7 @@ def main():
         e0.record(stream)
         for _ in range(ne):
             e2e_step()
+        C.mhl_host_drain(L.plan, stream)
         e1.record(stream)
         torch.cuda.synchronize(dev)
         ems = e0.elapsed_time(e1)
@@ -328,7 +331,7 @@ def main():
             ems = float(t.item())
         nbytes = T_loc * cfg.d * x.element_size()
         e2e = {"value": G * T_loc * ne / (ems / 1e3), "unit": "tokens/s", "h2d_bytes_per_step": 2 * nbytes,
-               "d2h_bytes_per_step": 2 * nbytes, "api": "mhlmoe_train_step_host (pinned host x, d_out -> out, dx)"}
+               "d2h_bytes_per_step": 2 * nbytes, "api": "mhlmoe_train_step_host_pipelined x steps + mhl_host_drain (pinned host x, d_out -> out, dx)"}
 
     if rank != 0:
         if G > 1:

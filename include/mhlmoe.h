@@ -156,17 +156,31 @@ MHL_API mhl_status mhlmoe_backward(mhl_plan plan, const void* x, const mhl_weigh
 
 /* End-to-end training step from HOST buffers (x_host, dout_host: [T_loc, d] E,
  * pinned for asynchronous copies): copies x and d_out to device staging `io`
- * (io_bytes), runs forward + backward, copies out and dx back to out_host /
- * dx_host ([T_loc, d] E).  Asynchronous on `stream`; synchronize before reading
- * the host outputs.  Weights and gradients are device pointers.  The copies run on
- * two plan-owned side streams (one per link direction) ordered with `stream` by
- * events: the d_out upload overlaps the forward, the out download the backward, and
- * a call's x upload overlaps the previous call's dx download.  When `stream`
- * completes, every output of the call is on the host. */
+ * (io_bytes = two slots used by alternate calls), runs forward + backward, copies
+ * out and dx back to out_host / dx_host ([T_loc, d] E).  Asynchronous on `stream`;
+ * synchronize before reading the host outputs.  Weights and gradients are device
+ * pointers.  The copies run on two plan-owned side streams (one per link direction)
+ * ordered with `stream` by events: the d_out upload overlaps the forward, the out
+ * download the backward, and a call's uploads overlap the previous call's backward
+ * and downloads.  When `stream` completes, every output of the call is on the host.
+ * Host buffers must stay valid and unmodified until then. */
 MHL_API mhl_status mhlmoe_train_step_host(mhl_plan plan, const void* x_host, const void* dout_host,
                                   const mhl_weights* w, void* out_host, void* dx_host,
                                   const mhl_grads* grads, void* io, void* saved,
                                   void* workspace, size_t workspace_bytes, void* stream);
+
+/* As mhlmoe_train_step_host, but `stream` does NOT wait for this call's downloads:
+ * the next call's forward starts as soon as its own input is uploaded, so a loop of
+ * calls is bound by the host link rather than by upload + compute + download in
+ * series.  The host outputs (and the reuse of the host inputs) of every pipelined
+ * call issued so far are safe once `stream` completes after mhl_host_drain. */
+MHL_API mhl_status mhlmoe_train_step_host_pipelined(mhl_plan plan, const void* x_host, const void* dout_host,
+                                            const mhl_weights* w, void* out_host, void* dx_host,
+                                            const mhl_grads* grads, void* io, void* saved,
+                                            void* workspace, size_t workspace_bytes, void* stream);
+
+/* Makes `stream` wait for every host-step download issued so far (see above). */
+MHL_API mhl_status mhl_host_drain(mhl_plan plan, void* stream);
 
 /* Aux-free, global load balancing (NEXT-2): after a forward on
  * `saved`, updates this rank's router bias in place from the step's expert loads:

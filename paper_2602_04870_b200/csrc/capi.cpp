@@ -107,6 +107,7 @@ struct Dims {
   int d, N_h, d_h, N_e, k, d_e, G, H, HD, D, el, dtype, rank;
   bool loopback, simt, pair;
   int n_rt, max_tiles, max_chunks, seg_align;
+  int dw_parts = mhl::kMaxDwParts;   // dW row parts per head (= dW grid), set from the SM count by hp_plan
 };
 
 struct Bump {
@@ -115,7 +116,7 @@ struct Bump {
 };
 
 // offsets inside one rank's saved region
-struct SavedLayout { size_t Xs, idx, gate, perm, tok_s, gate_s, pos, off, tiles, ntiles, chunks, nchunks, cbase, ccount, load, cat, total; };
+struct SavedLayout { size_t Xs, idx, gate, perm, tok_s, gate_s, pos, off, tiles, ntiles, chunks, nchunks, cbase, ccount, pbase, pcount, load, cat, total; };
 // offsets inside one rank's workspace region (forward and backward alias each other)
 struct FwdLayout { size_t send1, Yrep, send2, recv2, hist, tilepref, planes, total; };
 struct BwdLayout { size_t send3, dY, dXrep, dg, dS, dS_s, dH, gA, dwr_part, W_rT, send4, recv4, dXs, dw_part, dw_done, total; };
@@ -136,6 +137,8 @@ SavedLayout saved_layout(const Dims& m) {
   L.nchunks = b.take(16);
   L.cbase = b.take((size_t)m.H * m.N_e * 4);
   L.ccount = b.take((size_t)m.H * m.N_e * 4);
+  L.pbase = b.take((size_t)m.H * mhl::kMaxDwParts * 4);
+  L.pcount = b.take((size_t)m.H * mhl::kMaxDwParts * 4);
   L.load = b.take((size_t)m.H * m.N_e * 4);             // per-head expert loads of the step (F4)
   L.cat = b.take((size_t)m.T_loc * m.D * m.el);
   L.total = b.off;
@@ -214,7 +217,7 @@ mhl_status make_dims(const mhl_config* c, Dims* m) {
   const int64_t mt = (int64_t)m->H * ((m->R + mhl::kExpertBM - 1) / mhl::kExpertBM + 2 * m->N_e);
   if (mt >= (int64_t)1 << 31) return fail(MHL_ERR_UNSUPPORTED, "too many tiles");
   m->max_tiles = (int)mt;
-  m->max_chunks = (int)((int64_t)m->H * ((m->Rp + mhl::kDwChunk - 1) / mhl::kDwChunk + m->N_e));
+  m->max_chunks = (int)((int64_t)m->H * (mhl::kMaxDwParts + m->N_e));   // <= parts + expert boundaries
   const size_t router_smem = (size_t)m->el * m->d_h * mhl::kRouterTile + 4ull * m->d_h * 32 + 4ull * m->N_e;
   const size_t rbwd_smem = 4ull * std::min<int64_t>((int64_t)m->N_e * m->d_h, 32768) + 8ull * mhl::kRouterTile * m->k;
   if (router_smem > 200 * 1024 || rbwd_smem > 200 * 1024)
@@ -231,7 +234,7 @@ void fill_info(const Dims& m, mhl_plan_info* info) {
   info->a2a_bytes_per_rank = info->a2a_bytes_per_peer * (uint64_t)(m.G - 1);
   info->saved_bytes = (uint64_t)saved_layout(m).total * vr;
   info->workspace_bytes = (uint64_t)std::max(fwd_layout(m).total, bwd_layout(m).total) * vr;
-  info->io_bytes = 4ull * align_up((size_t)m.T_loc * vr * m.d * m.el);
+  info->io_bytes = 8ull * align_up((size_t)m.T_loc * vr * m.d * m.el);   // 2 slots x {x, d_out, out, dx}
   info->max_tiles = m.max_tiles;
 }
 
@@ -254,9 +257,11 @@ struct mhl_plan_s {
   int num_sms = 148;
   // host-buffer step (mhlmoe_train_step_host): side stream for the copies that can overlap compute
   cudaStream_t h2d_stream = nullptr, d2h_stream = nullptr;
-  cudaEvent_t ev_x = nullptr, ev_dout = nullptr, ev_fwd = nullptr, ev_out = nullptr, ev_bwd = nullptr,
-              ev_dx = nullptr;
-  bool io_live = false;   // a previous host step's events are recorded
+  // per io slot (host steps alternate between two staging slots)
+  cudaEvent_t ev_x[2] = {}, ev_dout[2] = {}, ev_fwd[2] = {}, ev_out[2] = {}, ev_bwd[2] = {}, ev_dx[2] = {};
+  cudaEvent_t ev_drain = nullptr;
+  bool io_live[2] = {false, false};   // the slot's events of a previous host step are recorded
+  uint64_t host_steps = 0;
   // HP exchanges (G > 1): comm stream pipelined against the producers on the compute stream
   cudaStream_t comm_stream = nullptr;
   cudaEvent_t ev_prod = nullptr, ev_comm = nullptr;
@@ -420,6 +425,9 @@ mhl::Routing routing_view(const Dims& m, const char* saved) {
   rt.max_chunks = m.max_chunks;
   rt.cbase = (const int32_t*)(saved + S.cbase);
   rt.ccount = (const int32_t*)(saved + S.ccount);
+  rt.pbase = (const int32_t*)(saved + S.pbase);
+  rt.pcount = (const int32_t*)(saved + S.pcount);
+  rt.dw_parts = m.dw_parts;
   return rt;
 }
 
@@ -482,7 +490,7 @@ mhl_status moe_forward_local(mhl_plan p, const RankPtrs& R, void* yout, cudaStre
                         (float*)(R.saved + S.gate_s), m.Rp, m.seg_align, tiles, ntiles, m.max_tiles,
                         (mhl::Tile*)(R.saved + S.chunks),
                         (int32_t*)(R.saved + S.nchunks), (int32_t*)(R.saved + S.cbase), (int32_t*)(R.saved + S.ccount),
-                        m.max_chunks, s);
+                        m.max_chunks, m.dw_parts, (int32_t*)(R.saved + S.pbase), (int32_t*)(R.saved + S.pcount), s);
   }
   const mhl::Routing rt = routing_view(m, R.saved);
   void* Yrep = R.ws + F.Yrep;
@@ -659,6 +667,7 @@ mhl_status hp_plan(const mhl_config* cfg, const uint8_t* nccl_id, mhl_plan* out)
   if (cudaGetDeviceProperties(&prop, dev) != cudaSuccess) return cleanup(fail(MHL_ERR_CUDA, "cudaGetDeviceProperties"));
   if (prop.major != 10) return cleanup(fail(MHL_ERR_UNSUPPORTED, "this library is built for sm_100a (B200)"));
   p->num_sms = prop.multiProcessorCount;
+  p->m.dw_parts = std::max(1, std::min(p->num_sms, mhl::kMaxDwParts));
   if (cublasCreate(&p->blas) != CUBLAS_STATUS_SUCCESS) return cleanup(fail(MHL_ERR_CUDA, "cublasCreate"));
   if (cudaMalloc(&p->blas_ws, p->blas_ws_bytes) != cudaSuccess) return cleanup(fail(MHL_ERR_CUDA, "cudaMalloc"));
   if (cublasSetWorkspace(p->blas, p->blas_ws, p->blas_ws_bytes) != CUBLAS_STATUS_SUCCESS)
@@ -695,8 +704,10 @@ mhl_status hp_plan_destroy(mhl_plan p) {
   if (p->blas) cublasDestroy(p->blas);
   if (p->blas_ws) cudaFree(p->blas_ws);
   if (p->dflag) cudaFree(p->dflag);
-  for (cudaEvent_t e : {p->ev_x, p->ev_dout, p->ev_fwd, p->ev_out, p->ev_bwd, p->ev_dx})
-    if (e) cudaEventDestroy(e);
+  for (int i = 0; i < 2; ++i)
+    for (cudaEvent_t e : {p->ev_x[i], p->ev_dout[i], p->ev_fwd[i], p->ev_out[i], p->ev_bwd[i], p->ev_dx[i]})
+      if (e) cudaEventDestroy(e);
+  if (p->ev_drain) cudaEventDestroy(p->ev_drain);
   if (p->h2d_stream) cudaStreamDestroy(p->h2d_stream);
   if (p->comm_stream) cudaStreamDestroy(p->comm_stream);
   for (cudaEvent_t e : {p->ev_prod, p->ev_comm})
@@ -877,54 +888,87 @@ mhl_status mhlmoe_backward(mhl_plan p, const void* x, const mhl_weights* w, cons
   return check_kernels(p);
 }
 
-mhl_status mhlmoe_train_step_host(mhl_plan p, const void* x_host, const void* dout_host, const mhl_weights* w,
-                                  void* out_host, void* dx_host, const mhl_grads* grads, void* io, void* saved,
-                                  void* workspace, size_t workspace_bytes, void* stream) {
+namespace {
+// Host-buffer training step.  Copies run on two plan-owned side streams, one per link direction,
+// ordered against the compute stream by events; consecutive calls alternate between two device
+// staging slots, so a call's uploads need only wait for the backward of the call two steps back.
+// Within a call the d_out upload overlaps the forward and the out download the backward; across
+// calls the next call's uploads overlap this call's backward and downloads.  `sync_outputs` makes
+// `stream` wait for this call's downloads (outputs on the host when the stream completes);
+// otherwise mhl_host_drain provides that point for all calls so far.
+mhl_status host_step(mhl_plan p, const void* x_host, const void* dout_host, const mhl_weights* w, void* out_host,
+                     void* dx_host, const mhl_grads* grads, void* io, void* saved, void* workspace,
+                     size_t workspace_bytes, void* stream, bool sync_outputs) {
   if (!p || !x_host || !dout_host || !out_host || !dx_host || !io)
     return fail(MHL_ERR_INVALID_ARGUMENT, "NULL argument");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const Dims& m = p->m;
   const size_t n = (size_t)m.T_loc * (m.loopback ? m.G : 1) * m.d * m.el;
   const size_t a = align_up(n);
-  char* xd = static_cast<char*>(io);
+  const int sl = (int)(p->host_steps & 1);
+  char* xd = static_cast<char*>(io) + (size_t)sl * 4 * a;
   char* dd = xd + a;
   char* od = dd + a;
   char* gd = od + a;
-  // Copies run on two plan-owned side streams, one per link direction, ordered against the
-  // compute stream by events: d_out's upload overlaps the forward, out's download overlaps the
-  // backward, and (across back-to-back calls) this call's x upload overlaps the previous call's
-  // dx download.  Buffer reuse across calls is guarded: x / d_out are re-uploaded only after the
-  // previous backward (their last reader), out / dx rewritten only after their downloads.
   if (!p->h2d_stream) {
     MHL_CUDA(cudaStreamCreateWithFlags(&p->h2d_stream, cudaStreamNonBlocking));
     MHL_CUDA(cudaStreamCreateWithFlags(&p->d2h_stream, cudaStreamNonBlocking));
-    for (cudaEvent_t* e : {&p->ev_x, &p->ev_dout, &p->ev_fwd, &p->ev_out, &p->ev_bwd, &p->ev_dx})
-      MHL_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+    for (int i = 0; i < 2; ++i)
+      for (cudaEvent_t* e : {&p->ev_x[i], &p->ev_dout[i], &p->ev_fwd[i], &p->ev_out[i], &p->ev_bwd[i], &p->ev_dx[i]})
+        MHL_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+    MHL_CUDA(cudaEventCreateWithFlags(&p->ev_drain, cudaEventDisableTiming));
   }
   cudaStream_t up = p->h2d_stream, down = p->d2h_stream;
-  if (p->io_live) MHL_CUDA(cudaStreamWaitEvent(up, p->ev_bwd, 0));
+  const bool live = p->io_live[sl];
+  if (live) MHL_CUDA(cudaStreamWaitEvent(up, p->ev_bwd[sl], 0));     // slot's x / d_out last read there
   MHL_CUDA(cudaMemcpyAsync(xd, x_host, n, cudaMemcpyHostToDevice, up));
-  MHL_CUDA(cudaEventRecord(p->ev_x, up));
+  MHL_CUDA(cudaEventRecord(p->ev_x[sl], up));
   MHL_CUDA(cudaMemcpyAsync(dd, dout_host, n, cudaMemcpyHostToDevice, up));
-  MHL_CUDA(cudaEventRecord(p->ev_dout, up));
-  MHL_CUDA(cudaStreamWaitEvent(s, p->ev_x, 0));
-  if (p->io_live) MHL_CUDA(cudaStreamWaitEvent(s, p->ev_out, 0));   // previous download of od
+  MHL_CUDA(cudaEventRecord(p->ev_dout[sl], up));
+  MHL_CUDA(cudaStreamWaitEvent(s, p->ev_x[sl], 0));
+  if (live) MHL_CUDA(cudaStreamWaitEvent(s, p->ev_out[sl], 0));      // slot's previous out download
   MHL_TRY(mhlmoe_forward(p, xd, w, od, saved, workspace, workspace_bytes, nullptr, nullptr, stream));
-  MHL_CUDA(cudaEventRecord(p->ev_fwd, s));
-  MHL_CUDA(cudaStreamWaitEvent(down, p->ev_fwd, 0));
+  MHL_CUDA(cudaEventRecord(p->ev_fwd[sl], s));
+  MHL_CUDA(cudaStreamWaitEvent(down, p->ev_fwd[sl], 0));
   MHL_CUDA(cudaMemcpyAsync(out_host, od, n, cudaMemcpyDeviceToHost, down));
-  MHL_CUDA(cudaEventRecord(p->ev_out, down));
-  MHL_CUDA(cudaStreamWaitEvent(s, p->ev_dout, 0));
-  if (p->io_live) MHL_CUDA(cudaStreamWaitEvent(s, p->ev_dx, 0));    // previous download of gd
+  MHL_CUDA(cudaEventRecord(p->ev_out[sl], down));
+  MHL_CUDA(cudaStreamWaitEvent(s, p->ev_dout[sl], 0));
+  if (live) MHL_CUDA(cudaStreamWaitEvent(s, p->ev_dx[sl], 0));       // slot's previous dx download
   MHL_TRY(mhlmoe_backward(p, xd, w, dd, saved, gd, grads, workspace, workspace_bytes, stream));
-  MHL_CUDA(cudaEventRecord(p->ev_bwd, s));
-  MHL_CUDA(cudaStreamWaitEvent(down, p->ev_bwd, 0));
+  MHL_CUDA(cudaEventRecord(p->ev_bwd[sl], s));
+  MHL_CUDA(cudaStreamWaitEvent(down, p->ev_bwd[sl], 0));
   MHL_CUDA(cudaMemcpyAsync(dx_host, gd, n, cudaMemcpyDeviceToHost, down));
-  MHL_CUDA(cudaEventRecord(p->ev_dx, down));
-  p->io_live = true;
-  // every output of this call is on the host when `stream` completes
-  MHL_CUDA(cudaStreamWaitEvent(s, p->ev_out, 0));
-  MHL_CUDA(cudaStreamWaitEvent(s, p->ev_dx, 0));
+  MHL_CUDA(cudaEventRecord(p->ev_dx[sl], down));
+  p->io_live[sl] = true;
+  p->host_steps++;
+  if (sync_outputs) {
+    MHL_CUDA(cudaStreamWaitEvent(s, p->ev_out[sl], 0));
+    MHL_CUDA(cudaStreamWaitEvent(s, p->ev_dx[sl], 0));
+  }
+  return MHL_OK;
+}
+}  // namespace
+
+mhl_status mhlmoe_train_step_host(mhl_plan p, const void* x_host, const void* dout_host, const mhl_weights* w,
+                                  void* out_host, void* dx_host, const mhl_grads* grads, void* io, void* saved,
+                                  void* workspace, size_t workspace_bytes, void* stream) {
+  return host_step(p, x_host, dout_host, w, out_host, dx_host, grads, io, saved, workspace, workspace_bytes, stream,
+                   true);
+}
+
+mhl_status mhlmoe_train_step_host_pipelined(mhl_plan p, const void* x_host, const void* dout_host,
+                                            const mhl_weights* w, void* out_host, void* dx_host,
+                                            const mhl_grads* grads, void* io, void* saved, void* workspace,
+                                            size_t workspace_bytes, void* stream) {
+  return host_step(p, x_host, dout_host, w, out_host, dx_host, grads, io, saved, workspace, workspace_bytes, stream,
+                   false);
+}
+
+mhl_status mhl_host_drain(mhl_plan p, void* stream) {
+  if (!p) return fail(MHL_ERR_INVALID_ARGUMENT, "NULL plan");
+  if (!p->d2h_stream) return MHL_OK;
+  MHL_CUDA(cudaEventRecord(p->ev_drain, p->d2h_stream));
+  MHL_CUDA(cudaStreamWaitEvent(static_cast<cudaStream_t>(stream), p->ev_drain, 0));
   return MHL_OK;
 }
 

@@ -10,7 +10,7 @@
 // the all-zero sub-token row (token id T) with gate 0 and contribute exactly nothing.
 // Outputs per head (Rp = padded row capacity): perm (row -> replica or -1), tok_s (row -> token
 // or T), gate_s (row -> gate or 0), pos (replica -> row), off, the tile list (L2-friendly
-// (head, part, expert) order, see offsets_kernel) and the list of <= kDwChunk-row chunks used by
+// (head, part, expert) order, see offsets_kernel) and the list of row-part chunks used by
 // the weight-gradient kernel.
 #include "kernels.h"
 
@@ -90,20 +90,19 @@ __device__ int block_exclusive_scan_1024(int v, int* s_warp, int* total) {
 // CTA recomputes itself from `counts` (H*N_e values), so the heads scan in parallel.
 __global__ void __launch_bounds__(1024)
 offsets_kernel(const int32_t* __restrict__ counts, int32_t* __restrict__ off, int32_t* __restrict__ tbase,
-               int32_t* __restrict__ ntiles, int H, int N_e, int max_tiles, int32_t* __restrict__ nchunks,
-               int32_t* __restrict__ cbase, int32_t* __restrict__ ccount, int max_chunks, int seg_align) {
+               int32_t* __restrict__ ntiles, int H, int N_e, int max_tiles, int seg_align) {
   __shared__ int s_warp[64];
   __shared__ int s_tot;
   const int TPS = seg_align / kExpertBM;                                 // tiles per alignment unit
   const int h = blockIdx.x;
-  // tiles and dW chunks of all heads before h (and of all heads, for the totals)
-  int t_before = 0, c_before = 0, t_all = 0, c_all = 0;
+  // tiles of all heads before h (and of all heads, for the total)
+  int t_before = 0, t_all = 0;
   for (int i = threadIdx.x; i < H * N_e; i += blockDim.x) {
     const int c = counts[i];
     const int cp = (c + seg_align - 1) / seg_align * seg_align;
-    const int nt = cp / kExpertBM, nc = (cp + kDwChunk - 1) / kDwChunk;
-    if (i / N_e < h) { t_before += nt; c_before += nc; }
-    t_all += nt; c_all += nc;
+    const int nt = cp / kExpertBM;
+    if (i / N_e < h) t_before += nt;
+    t_all += nt;
   }
   // block reductions (order-independent integer sums)
   auto block_sum = [&](int v) {
@@ -114,8 +113,7 @@ offsets_kernel(const int32_t* __restrict__ counts, int32_t* __restrict__ off, in
     return t;
   };
   int carry_t = block_sum(t_before);
-  int carry_c = block_sum(c_before);
-  const int tot_t = block_sum(t_all), tot_c = block_sum(c_all);
+  const int tot_t = block_sum(t_all);
   int carry_r = 0;
   for (int p = 0; p < kTileParts; ++p) {
     int carry_p = 0;
@@ -139,30 +137,85 @@ offsets_kernel(const int32_t* __restrict__ counts, int32_t* __restrict__ off, in
     const int rx = block_exclusive_scan_1024(cp, s_warp, &s_tot);
     const int rtot = s_tot;
     __syncthreads();
-    const int nc = (cp + kDwChunk - 1) / kDwChunk;
-    const int cx = block_exclusive_scan_1024(nc, s_warp, &s_tot);
-    const int ctot = s_tot;
-    __syncthreads();
-    if (e < N_e) {
-      off[(size_t)h * (N_e + 1) + e] = carry_r + rx;
-      cbase[(size_t)h * N_e + e] = carry_c + cx;
-      ccount[(size_t)h * N_e + e] = nc;
-    }
+    if (e < N_e) off[(size_t)h * (N_e + 1) + e] = carry_r + rx;
     carry_r += rtot;
-    carry_c += ctot;
   }
   if (threadIdx.x == 0) {
     off[(size_t)h * (N_e + 1) + N_e] = carry_r;
-    if (h == 0) { *ntiles = min(tot_t, max_tiles); *nchunks = min(tot_c, max_chunks); }
+    if (h == 0) *ntiles = min(tot_t, max_tiles);
   }
+}
+
+// (2a) dW chunks.  Each head's padded rows [0, R_h) are cut into P equal parts (boundaries rounded
+// down to the dW kernel's 64-row step; P = the dW grid, fixed per plan, independent of G), and a
+// chunk is a part's intersection with one expert segment.  CTA b of the dW kernel takes part b of
+// every head, so every CTA gets the same number of rows; the chunk list is in (head, part,
+// expert) = (head, expert, row) order, so each expert's chunks are consecutive ([cbase, +ccount)),
+// and its partials are summed in that order (deterministic, problem-derived boundaries).
+__device__ __forceinline__ int part_lo(int p, int P, int Rh) {
+  return p >= P ? Rh : (int)(((int64_t)p * Rh / P) & ~(int64_t)(kDwStep - 1));
+}
+
+__global__ void __launch_bounds__(1024)
+dw_parts_kernel(const int32_t* __restrict__ off, int H, int N_e, int P, Tile* __restrict__ chunks, int max_chunks,
+                int32_t* __restrict__ nchunks, int32_t* __restrict__ cbase, int32_t* __restrict__ ccount,
+                int32_t* __restrict__ pbase, int32_t* __restrict__ pcount) {
+  __shared__ int s_warp[64];
+  __shared__ int s_tot;
+  for (int i = threadIdx.x; i < H * N_e; i += blockDim.x) { ccount[i] = 0; cbase[i] = 0; }
+  __syncthreads();
+  int carry = 0;
+  for (int base = 0; base < H * P; base += 1024) {
+    const int i = base + threadIdx.x;
+    int cnt = 0, lo = 0, hi = 0, e0 = 0, h = 0, p = 0;
+    const int32_t* o = off;
+    if (i < H * P) {
+      h = i / P; p = i % P;
+      o = off + (size_t)h * (N_e + 1);
+      const int Rh = o[N_e];
+      lo = part_lo(p, P, Rh); hi = part_lo(p + 1, P, Rh);
+      if (lo < hi) {
+        int a = 0, b = N_e;                  // e0 = last expert with o[e] <= lo (its segment holds lo)
+        while (a < b) { const int mid = (a + b + 1) >> 1; if (o[mid] <= lo) a = mid; else b = mid - 1; }
+        e0 = a;
+        for (int e = e0; e < N_e && o[e] < hi; ++e) cnt += o[e + 1] > o[e];
+      }
+    }
+    const int ex = block_exclusive_scan_1024(cnt, s_warp, &s_tot);
+    const int tot = s_tot;
+    __syncthreads();
+    if (i < H * P) {
+      const int cb = carry + ex;
+      pbase[i] = cb; pcount[i] = cnt;
+      int j = 0;
+      for (int e = e0; cnt > 0 && e < N_e && o[e] < hi; ++e) {
+        if (o[e + 1] <= o[e]) continue;
+        const int r0 = max(lo, o[e]), r1 = min(hi, o[e + 1]), ci = cb + j++;
+        if (ci < max_chunks) {
+          Tile tl;
+          tl.head = h; tl.expert = e; tl.row0 = r0; tl.rows = r1 - r0;
+          chunks[ci] = tl;
+        }
+        if (r0 == o[e]) {                    // the expert's first chunk: count its parts
+          int n = 1;
+          const int Rh = o[N_e];
+          for (int pp = p + 1; pp < P && part_lo(pp, P, Rh) < o[e + 1]; ++pp)
+            n += part_lo(pp, P, Rh) < part_lo(pp + 1, P, Rh);
+          cbase[(size_t)h * N_e + e] = ci;
+          ccount[(size_t)h * N_e + e] = n;
+        }
+      }
+    }
+    carry += tot;
+  }
+  if (threadIdx.x == 0) *nchunks = min(carry, max_chunks);
 }
 
 // (2b) one warp per (h, e): its tiles (at the (h, part, e) positions), its dW chunks and the
 // padding-row fill of its segment, lanes striding over each list.
 __global__ void __launch_bounds__(256)
 tiles_kernel(const int32_t* __restrict__ counts, const int32_t* __restrict__ off, const int32_t* __restrict__ tbase,
-             Tile* __restrict__ tiles, int max_tiles, Tile* __restrict__ chunks, const int32_t* __restrict__ cbase,
-             int max_chunks, int H, int N_e, int64_t Rp, int32_t* __restrict__ perm, int32_t* __restrict__ tok_s,
+             Tile* __restrict__ tiles, int max_tiles, int H, int N_e, int64_t Rp, int32_t* __restrict__ perm, int32_t* __restrict__ tok_s,
              float* __restrict__ gate_s, int tok_zero, int seg_align) {
   const int he = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5), lane = threadIdx.x & 31;
   if (he >= H * N_e) return;
@@ -183,16 +236,6 @@ tiles_kernel(const int32_t* __restrict__ counts, const int32_t* __restrict__ off
         tl.rows = max(0, min(kExpertBM, c - j * kExpertBM));
         tiles[ti] = tl;
       }
-    }
-  }
-  const int nc = (cp + kDwChunk - 1) / kDwChunk;
-  for (int i = lane; i < nc; i += 32) {
-    const int ci = cbase[he] + i;
-    if (ci < max_chunks) {
-      Tile tl;
-      tl.head = h; tl.expert = e; tl.row0 = row_off + i * kDwChunk;
-      tl.rows = min(kDwChunk, cp - i * kDwChunk);
-      chunks[ci] = tl;
     }
   }
   // padding rows of this segment: no replica, zero sub-token, gate 0
@@ -280,15 +323,16 @@ void launch_update_bias(const int32_t* load, int H, int N_e, int64_t total, floa
 void launch_cluster(int H, int64_t T, int k, int N_e, const int32_t* idx, const float* gate, const int32_t* hist,
                     int32_t* tilepref, int32_t* counts, int32_t* off, int32_t* perm, int32_t* pos, int32_t* tok_s,
                     float* gate_s, int64_t Rp, int seg_align, Tile* tiles, int32_t* ntiles, int max_tiles,
-                    Tile* chunks, int32_t* nchunks, int32_t* cbase, int32_t* ccount, int max_chunks, cudaStream_t s) {
+                    Tile* chunks, int32_t* nchunks, int32_t* cbase, int32_t* ccount, int max_chunks, int dw_parts,
+                    int32_t* pbase, int32_t* pcount, cudaStream_t s) {
   const int n_rt = (int)((T + kRouterTile - 1) / kRouterTile);
   tile_prefix_kernel<<<dim3(N_e, H), 256, 0, s>>>(hist, tilepref, counts, n_rt, N_e);
   // tile bases [H][kTileParts][N_e] live in the (otherwise unused here) tail of tilepref's scratch
   int32_t* tbase = tilepref + (size_t)H * n_rt * N_e;
-  offsets_kernel<<<H, 1024, 0, s>>>(counts, off, tbase, ntiles, H, N_e, max_tiles, nchunks, cbase, ccount, max_chunks,
-                                    seg_align);
-  tiles_kernel<<<(H * N_e + 7) / 8, 256, 0, s>>>(counts, off, tbase, tiles, max_tiles, chunks, cbase, max_chunks, H,
-                                                 N_e, Rp, perm, tok_s, gate_s, (int)T, seg_align);
+  offsets_kernel<<<H, 1024, 0, s>>>(counts, off, tbase, ntiles, H, N_e, max_tiles, seg_align);
+  dw_parts_kernel<<<1, 1024, 0, s>>>(off, H, N_e, dw_parts, chunks, max_chunks, nchunks, cbase, ccount, pbase, pcount);
+  tiles_kernel<<<(H * N_e + 7) / 8, 256, 0, s>>>(counts, off, tbase, tiles, max_tiles, H, N_e, Rp, perm, tok_s,
+                                                 gate_s, (int)T, seg_align);
   scatter_kernel<<<dim3(n_rt, H), kScatterWarps * 32, sizeof(int) * kScatterWarps * N_e, s>>>(
       idx, gate, off, tilepref, perm, pos, tok_s, gate_s, T, k, N_e, n_rt, Rp);
 }

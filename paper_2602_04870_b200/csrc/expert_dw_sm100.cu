@@ -3,8 +3,9 @@
 // Chain rule of y_r = g_r * gelu(x W1_e^T) W2_e over the clustered replicas of one expert
 // (Eq. 1): with dH = g dA' gelu'(H) and gA = g gelu(H) from expert_bwd_dx_sm100.cu,
 //   dW1_e^T = X^T dH,   dW2_e^T = dY^T gA        (X, dY = sub-token / dcat rows of the replicas)
-// per chunk of <= kDwChunk sorted rows (tcgen05, both operands MN-major) into fp32 partials; the
-// CTA finishing an expert's last chunk sums its partials in chunk order (deterministic, R21).
+// per chunk (one head's row part intersected with one expert segment, cluster.cu) on tcgen05 (both
+// operands MN-major) into fp32 partials; the CTA finishing an expert's last chunk sums its partials
+// in chunk order (deterministic, R21).  CTA b takes row part b of every head: equal rows per CTA.
 #include <cuda.h>
 
 #include "kernels.h"
@@ -18,7 +19,7 @@ namespace {
 using namespace sm100;
 
 // =============================================================================================
-// dW kernel: per chunk (<= kDwChunk rows of one (head, expert)), accumulate in TMEM
+// dW kernel: per chunk (a row part of one (head, expert)), accumulate in TMEM
 //   dW1^T[c][f] += sum_r X[r][c] dH[r][f]   dW2^T[c][f] += sum_r dY[r][c] gA[r][f]
 // M = c (DH/128 MMAs of M=128), N = f (DE), K = rows (16 per MMA), both operands MN-major.
 // Warp roles: kDwProd producer warps bring X, dY (TMA gather4 for the token-indexed rows, one lane
@@ -26,7 +27,23 @@ using namespace sm100;
 // 64-row steps; 8 warps flush each chunk's fp32 accumulators to its partial slot; the last warp
 // issues the MMAs (+ owns TMEM).  The ring keeps filling while a chunk is flushed.
 // =============================================================================================
-constexpr int kHalf = 64;   // rows per pipeline step
+constexpr int kHalf = kDwStep;   // rows per pipeline step
+static_assert(kHalf == 64, "dW pipeline step");
+
+// The chunks of this CTA: part blockIdx.x of every head (cluster.cu dw_parts_kernel), in order.
+struct MyChunks {
+  const int32_t* pb; const int32_t* pc; int H, P;
+  int h = 0, c = 0, end = 0;
+  __device__ MyChunks(const Routing& rt) : pb(rt.pbase), pc(rt.pcount), H(rt.H), P(rt.dw_parts) {}
+  __device__ int next() {
+    while (c >= end) {
+      if (h >= H) return -1;
+      const int i = h * P + (int)blockIdx.x;
+      c = pb[i]; end = c + pc[i]; ++h;
+    }
+    return c++;
+  }
+};
 constexpr int kDwProd = 8;                     // producer warps 0..kDwProd-1
 constexpr int kDwFlush0 = kDwProd;             // 8 flush warps
 constexpr int kDwMma = kDwProd + 8;
@@ -88,7 +105,8 @@ expert_dw_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant
     for (int p = warp; p < NP; p += kDwProd) mybytes += kHalf * 128;
     for (int t = warp; t < NT; t += kDwProd) mybytes += kHalf * 128;
     int n = 0;                                                // steps of this CTA so far
-    for (int ci = blockIdx.x; ci < nchunks; ci += gridDim.x) {
+    MyChunks it(rt);
+    for (int ci; (ci = it.next()) >= 0 && ci < nchunks;) {
       const Tile ch = chunks[ci];
       const int nsteps = ch.rows / kHalf;
       const int32_t* tk = rt.tok_s + (size_t)ch.head * Rp + ch.row0 + 4 * g;
@@ -125,7 +143,8 @@ expert_dw_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant
     if (lane == 0) {
       constexpr uint32_t IDESC = idesc_bf16(128, DE, 1, 1);
       int n = 0, nc = 0;
-      for (int ci = blockIdx.x; ci < nchunks; ci += gridDim.x, ++nc) {
+      MyChunks it(rt);
+      for (int ci; (ci = it.next()) >= 0 && ci < nchunks; ++nc) {
         const int nsteps = chunks[ci].rows / kHalf;
         if (nc >= 1) mbar_wait(accempty, (nc - 1) & 1);      // previous chunk flushed
         tc_fence_after();
@@ -171,7 +190,8 @@ expert_dw_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant
           if (dW2) dW2[(size_t)he * DEDH + i] = 0.f;
         }
     int nc = 0;
-    for (int ci = blockIdx.x; ci < nchunks; ci += gridDim.x, ++nc) {
+    MyChunks it(rt);
+    for (int ci; (ci = it.next()) >= 0 && ci < nchunks; ++nc) {
       mbar_wait_warp(accfull, nc & 1);
       tc_fence_after();
       const Tile ch = chunks[ci];
@@ -248,7 +268,8 @@ bool launch_dw_t(const Routing& rt, const void* Xs, int64_t ldx, const void* dY,
   auto kern = expert_dw_kernel<DH, DE>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, DwSmem<DH, DE>::BYTES);
   cudaMemsetAsync(done, 0, (size_t)rt.H * rt.N_e * sizeof(int), s);
-  kern<<<num_sms, kDwThreads, DwSmem<DH, DE>::BYTES, s>>>(xm, ym, hm, am, rt, partial, done, dW1, dW2);
+  (void)num_sms;   // one CTA per dW row part (rt.dw_parts = min(#SMs, kMaxDwParts))
+  kern<<<rt.dw_parts, kDwThreads, DwSmem<DH, DE>::BYTES, s>>>(xm, ym, hm, am, rt, partial, done, dW1, dW2);
   return true;
 }
 

@@ -10,7 +10,8 @@ constexpr int kRouterTile = 128;   // tokens per router CTA (= clustering tile o
 constexpr int kExpertBM = 128;     // replica rows per expert tile (tcgen05 M)
 // Expert segments are padded to a multiple of Routing::seg_align rows: one tile (128, default) or a
 // tile pair (256, MHL_FLAG_PAIR), which the cta_group::2 kernels need (tiles 2u, 2u+1 share an expert).
-constexpr int kDwChunk = 4096;     // sorted rows per weight-gradient partial (B5 dW)
+constexpr int kDwStep = 64;        // sorted rows per dW pipeline step (dW chunk boundaries align to it)
+constexpr int kMaxDwParts = 160;   // dW row parts per head (= the dW grid, min(#SMs, this))
 constexpr int kTileGroup = 8;      // consecutive expert tiles a persistent CTA takes at once
 constexpr int kTileParts = 8;      // token-order parts per expert segment in the tile list (cluster.cu)
 
@@ -30,6 +31,7 @@ struct Routing {
   const Tile* tiles; const int32_t* ntiles; int max_tiles;        // 128-row tiles, (h, part, e, row) order
   const Tile* chunks; const int32_t* nchunks; int max_chunks;     // dW chunks
   const int32_t* cbase; const int32_t* ccount;                    // [H][N_e] chunk range per expert
+  const int32_t* pbase; const int32_t* pcount; int dw_parts;       // [H][dw_parts] chunk range per (head, part)
 };
 
 // ---- F3: router + online top-k + gates (SIMT fp32-FMA path). idx/gate [H][T][k];
@@ -59,7 +61,8 @@ bool launch_router_blk_sm100(const void* Xs, int64_t ldx, const void* planes, co
 void launch_cluster(int H, int64_t T, int k, int N_e, const int32_t* idx, const float* gate, const int32_t* hist,
                     int32_t* tilepref, int32_t* counts, int32_t* off, int32_t* perm, int32_t* pos, int32_t* tok_s,
                     float* gate_s, int64_t Rp, int seg_align, Tile* tiles, int32_t* ntiles, int max_tiles,
-                    Tile* chunks, int32_t* nchunks, int32_t* cbase, int32_t* ccount, int max_chunks, cudaStream_t s);
+                    Tile* chunks, int32_t* nchunks, int32_t* cbase, int32_t* ccount, int max_chunks, int dw_parts,
+                    int32_t* pbase, int32_t* pcount, cudaStream_t s);
 
 // ---- F5: Yrep[h][row][c] = gate_s * gelu(X[tok_s] W1_e^T) W2_e for every sorted row (padding rows
 // produce zeros).  Xs holds T+1 rows, row T all-zero.  Yrep is [H][Rp][d_h].

@@ -19,7 +19,8 @@ MHL_FLAG_LOOPBACK, MHL_FLAG_SIMT, MHL_FLAG_PAIR = 1, 2, 4
 STATUS = {0: "MHL_OK", 1: "MHL_ERR_INVALID_ARGUMENT", 2: "MHL_ERR_CONFIG", 3: "MHL_ERR_WORKSPACE_TOO_SMALL",
           4: "MHL_ERR_UNSUPPORTED", 5: "MHL_ERR_CUDA", 6: "MHL_ERR_NCCL", 7: "MHL_ERR_NONFINITE"}
 EXPORTS = ["hp_plan_query", "mhl_get_unique_id", "hp_plan", "hp_plan_info", "hp_plan_destroy", "mhlmoe_forward",
-           "mhlmoe_backward", "mhlmoe_train_step_host", "mhlmoe_update_bias", "mhl_check_device_status",
+           "mhlmoe_backward", "mhlmoe_train_step_host", "mhlmoe_train_step_host_pipelined", "mhl_host_drain",
+           "mhlmoe_update_bias", "mhl_check_device_status",
            "mhl_launch_count",
            "mhl_a2a_bytes_posted", "mhl_set_step_timing", "mhl_step_times", "mhl_status_string",
            "mhl_last_error"]
@@ -72,6 +73,9 @@ def _load():
                                 ctypes.c_size_t, P]),
         "mhlmoe_train_step_host": (I, [P, P, P, ctypes.POINTER(mhl_weights), P, P, ctypes.POINTER(mhl_grads), P,
                                        P, P, ctypes.c_size_t, P]),
+        "mhlmoe_train_step_host_pipelined": (I, [P, P, P, ctypes.POINTER(mhl_weights), P, P,
+                                                 ctypes.POINTER(mhl_grads), P, P, P, ctypes.c_size_t, P]),
+        "mhl_host_drain": (I, [P, P]),
         "mhlmoe_update_bias": (I, [P, P, P, ctypes.c_float, P]),
         "mhl_check_device_status": (I, [P]),
         "mhl_launch_count": (ctypes.c_uint64, [P]),
@@ -185,6 +189,22 @@ def mhlmoe_train_step_host(plan: Plan, x_host, dout_host, W, out_host, dx_host, 
                                        _ptr(dx_host), ctypes.byref(gs), _ptr(io), _ptr(saved), _ptr(workspace),
                                        workspace.numel() * workspace.element_size(), _stream(stream)),
            "mhlmoe_train_step_host")
+
+
+def mhlmoe_train_step_host_pipelined(plan: Plan, x_host, dout_host, W, out_host, dx_host, grads, io, saved,
+                                     workspace, stream=None):
+    """As mhlmoe_train_step_host; host outputs are complete after mhl_host_drain + a stream sync."""
+    ws = weights_struct(W) if isinstance(W, dict) else W
+    gs = grads_struct(grads) if isinstance(grads, dict) else grads
+    _check(_lib.mhlmoe_train_step_host_pipelined(plan.handle, _ptr(x_host), _ptr(dout_host), ctypes.byref(ws),
+                                                 _ptr(out_host), _ptr(dx_host), ctypes.byref(gs), _ptr(io),
+                                                 _ptr(saved), _ptr(workspace),
+                                                 workspace.numel() * workspace.element_size(), _stream(stream)),
+           "mhlmoe_train_step_host_pipelined")
+
+
+def mhl_host_drain(plan: Plan, stream=None):
+    _check(_lib.mhl_host_drain(plan.handle, _stream(stream)), "mhl_host_drain")
 
 
 def mhlmoe_update_bias(plan: Plan, saved, bias, gamma: float, stream=None):

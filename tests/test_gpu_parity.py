@@ -234,10 +234,12 @@ def test_nonfinite_router_score_is_reported():
     assert C.STATUS[ei.value.status] == "MHL_ERR_NONFINITE"
 
 
-def test_train_step_host_matches_device_path():
+@pytest.mark.parametrize("pipelined", [False, True])
+def test_train_step_host_matches_device_path(pipelined):
     """mhlmoe_train_step_host (pinned host buffers, side-stream copies overlapping the forward /
-    backward) gives bit-identical out, dx and gradients to the device-buffer path, for two
-    back-to-back calls with different inputs (checks the cross-call event ordering)."""
+    backward) gives bit-identical out, dx and gradients to the device-buffer path, for three
+    back-to-back calls with different inputs (checks the cross-call event ordering and the two
+    alternating staging slots); the pipelined variant syncs only once, after mhl_host_drain."""
     _need_gpu()
     from paper_2602_04870_b200 import mhlmoe as C
     from paper_2602_04870_b200.layer import MHLatentMoE, torch_dtype, weights_to_device
@@ -248,7 +250,7 @@ def test_train_step_host_matches_device_path():
     Wd = weights_to_device(W, cfg.dtype)
     io = torch.empty(L.info["io_bytes"], dtype=torch.uint8, device="cuda")
     hosts, refs = [], []
-    for seed in (21, 22):
+    for seed in (21, 22, 23):
         _, x, dout = make_problem(cfg, seed, "conf")
         xd, dd = torch.from_numpy(x).to("cuda", td), torch.from_numpy(dout).to("cuda", td)
         g = L.alloc_grads()
@@ -262,8 +264,11 @@ def test_train_step_host_matches_device_path():
         oh = torch.empty_like(xh).pin_memory()
         gh = torch.empty_like(xh).pin_memory()
         g = L.alloc_grads()
-        C.mhlmoe_train_step_host(L.plan, xh, dh, Wd, oh, gh, g, io, L.saved, L.workspace)
+        step = C.mhlmoe_train_step_host_pipelined if pipelined else C.mhlmoe_train_step_host
+        step(L.plan, xh, dh, Wd, oh, gh, g, io, L.saved, L.workspace)
         outs.append((oh, gh, g))
+    if pipelined:
+        C.mhl_host_drain(L.plan)
     torch.cuda.synchronize()
     for (o, d, g), (ro, rd, rg) in zip(outs, refs):
         assert torch.equal(o, ro) and torch.equal(d, rd)

@@ -1,5 +1,8 @@
+#!/usr/bin/env bash
+# Quick GPU pass (under gpurun from the repo root): smoke, GPU tests, bench (no e2e/cpu legs unless FULL=1)
 TAG=$1
 python -c "import __graft_entry__ as g; g.build(); g.smoke()" > gpurun_out/${TAG}_smoke.log 2>&1; echo smoke rc=$?; tail -1 gpurun_out/${TAG}_smoke.log | cut -c1-200
 timeout 900 python -m pytest tests -q -m gpu -x > gpurun_out/${TAG}_gpu_tests.log 2>&1; echo tests rc=$?; tail -15 gpurun_out/${TAG}_gpu_tests.log
-timeout 600 python bench.py --steps 10 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/${TAG}_bench.json 2> gpurun_out/${TAG}_bench.err; echo bench rc=$?
-tail -1 gpurun_out/${TAG}_bench.json | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(d['ms_per_step'], d['step_breakdown_ms'])"
+EXTRA="--no-e2e --no-cpu-baseline"; [ "${FULL:-0}" = 1 ] && EXTRA=""
+timeout 600 python bench.py --steps 10 --warmup 3 $EXTRA > gpurun_out/${TAG}_bench.json 2> gpurun_out/${TAG}_bench.err; echo bench rc=$?
+tail -1 gpurun_out/${TAG}_bench.json | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(d['ms_per_step'], d['value'], d.get('e2e'), d['step_breakdown_ms'])"
