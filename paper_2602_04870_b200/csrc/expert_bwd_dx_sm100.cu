@@ -117,7 +117,8 @@ __global__ void __launch_bounds__(HL<DH, DE>::THREADS, 1)
 expert_bwd_h_kernel(const __grid_constant__ CUtensorMap w1map, const __grid_constant__ CUtensorMap w2map,
                     const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap ymap,
                     const __grid_constant__ CUtensorMap hsmap, const __grid_constant__ CUtensorMap asmap, Routing rt,
-                    float* __restrict__ dg, int dbg) {
+                    float* __restrict__ dg, int dbg, uint8_t* __restrict__ dH_out, uint8_t* __restrict__ gA_out,
+                    int lsu) {
   using L = HL<DH, DE>;
   constexpr int kProdWarps = L::PW, kMmaWarp = L::MMA_WARP, kEpiWarp0 = L::EPI_WARP0, NBUF = L::NBUF;
   TraceBuf trc = g_trace_dx;   // one load; trace_ev then costs a register test
@@ -311,7 +312,27 @@ expert_bwd_h_kernel(const __grid_constant__ CUtensorMap w1map, const __grid_cons
         }
       }
       if (tid == kEpiWarp0 * 32) trace_ev(trc, 52, i);
-      if (!(dbg & 4)) {
+      if (!(dbg & 4) && lsu) {
+        // LSU variant: the box warps copy the staged slot to global with coalesced 16-byte stores
+        // (8 lanes per 128-byte row segment), leaving the TMA unit to the gathers
+        const int bt = (cg % WPB) * 32 + lane;
+        auto copy_out = [&](uint8_t* dst) {
+#pragma unroll
+          for (int c = bt; c < 256; c += 32 * WPB) {
+            const int r = c >> 3, c16 = c & 7;
+            const uint4 v = *reinterpret_cast<const uint4*>(slot + r * 128 + (((c16 ^ (r & 7)) & 7) << 4));
+            *reinterpret_cast<uint4*>(dst + ((size_t)orow + r) * (DE * 2) + box * 128 + c16 * 16) = v;
+          }
+        };
+        box_sync();
+        stage(dhp);
+        box_sync();
+        copy_out(dH_out);
+        box_sync();
+        stage(gap);
+        box_sync();
+        copy_out(gA_out);
+      } else if (!(dbg & 4)) {
         if (leader) bulk_wait_read<0>();          // the previous tile's gA store has read the slot
         box_sync();
         stage(dhp);
@@ -637,7 +658,7 @@ template <int DH, int DE>
 __global__ void __launch_bounds__(kThreads2, 1)
 expert_dx_gemm_kernel(const __grid_constant__ CUtensorMap w1map, const __grid_constant__ CUtensorMap hmap,
                       const __grid_constant__ CUtensorMap xmap, Routing rt, const float* __restrict__ dS,
-                      const float* __restrict__ W_rT) {
+                      const float* __restrict__ W_rT, uint8_t* __restrict__ xout, int lsu) {
   using L = GL<DH, DE>;
   constexpr int AS = L::AS, KB = DH / 64;
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -773,7 +794,7 @@ expert_dx_gemm_kernel(const __grid_constant__ CUtensorMap w1map, const __grid_co
           tc_fence_before();
           mbar_arrive(bar(L::B_DXEMPTY + 8 * b));
         }
-        if (leader) bulk_wait_read<1>();       // the slab store issued from this stage 2 blocks ago has read it
+        if (leader && !lsu) bulk_wait_read<1>();   // the slab store issued from this stage 2 blocks ago has read it
         named_bar_sync(2 + q, 64);
         uint8_t* sp = smem + L::YS + st * kYStage + q * 4096;
 #pragma unroll
@@ -785,11 +806,23 @@ expert_dx_gemm_kernel(const __grid_constant__ CUtensorMap w1map, const __grid_co
           pk.w = pack_bf16x2(__uint_as_float(v[u + 6]), __uint_as_float(v[u + 7]));
           *reinterpret_cast<uint4*>(sp + kmaj_off(lane, half * 32 + u, 32)) = pk;
         }
-        fence_proxy_async();
-        named_bar_sync(2 + q, 64);
-        if (leader) {
-          tma_store_2d(&xmap, sb + L::YS + st * kYStage + q * 4096, cb * 64, (int)((size_t)tl.head * Rp + tl.row0 + q * 32));
-          bulk_commit();
+        if (lsu) {   // coalesced 16-byte stores by the quadrant's two warps (see expert_sm100.cu)
+          named_bar_sync(2 + q, 64);
+          const int bt = half * 32 + lane;
+          uint8_t* dst = xout + ((size_t)tl.head * Rp + tl.row0 + q * 32) * (DH * 2) + cb * 128;
+#pragma unroll
+          for (int c = bt; c < 256; c += 64) {
+            const int r = c >> 3, c16 = c & 7;
+            *reinterpret_cast<uint4*>(dst + (size_t)r * (DH * 2) + c16 * 16) =
+                *reinterpret_cast<const uint4*>(sp + r * 128 + (((c16 ^ (r & 7)) & 7) << 4));
+          }
+        } else {
+          fence_proxy_async();
+          named_bar_sync(2 + q, 64);
+          if (leader) {
+            tma_store_2d(&xmap, sb + L::YS + st * kYStage + q * 4096, cb * 64, (int)((size_t)tl.head * Rp + tl.row0 + q * 32));
+            bulk_commit();
+          }
         }
       }
       ds = ds_n;
@@ -832,7 +865,8 @@ bool launch_t(const Routing& rt, const void* Xs, int64_t ldx, const void* dY, in
     cudaFuncSetAttribute(kp, cudaFuncAttributeMaxDynamicSharedMemorySize, HLP<DH, DE>::BYTES);
     kp<<<(num_sms / 2) * 2, HLP<DH, DE>::THREADS, HLP<DH, DE>::BYTES, s>>>(w1h, w2h, gxm, gym, hsm, asm_, rt, dg);
   } else {
-    k1<<<num_sms, HL<DH, DE>::THREADS, HL<DH, DE>::BYTES, s>>>(w1m, w2m, gxm, gym, hsm, asm_, rt, dg, dbg);
+    k1<<<num_sms, HL<DH, DE>::THREADS, HL<DH, DE>::BYTES, s>>>(w1m, w2m, gxm, gym, hsm, asm_, rt, dg, dbg,
+                                                              (uint8_t*)dH, (uint8_t*)gA, store_lsu(1));
   }
   if (trace_path) {
     TraceBuf tb{nullptr, 0};
@@ -852,7 +886,7 @@ bool launch_gemm_t(const Routing& rt, const void* W1, const void* dH, void* dXre
   if (!make_tmap_2d_bf16(&xm, dXrep, rows, DH, (uint64_t)DH * 2, 32, 64)) return false;
   auto k2 = expert_dx_gemm_kernel<DH, DE>;
   cudaFuncSetAttribute(k2, cudaFuncAttributeMaxDynamicSharedMemorySize, GL<DH, DE>::BYTES);
-  k2<<<num_sms, kThreads2, GL<DH, DE>::BYTES, s>>>(w1m, hm, xm, rt, dS, W_rT);
+  k2<<<num_sms, kThreads2, GL<DH, DE>::BYTES, s>>>(w1m, hm, xm, rt, dS, W_rT, (uint8_t*)dXrep, store_lsu(0));
   return true;
 }
 

@@ -84,7 +84,7 @@ template <int DH, int DE>
 __global__ void __launch_bounds__(kThreads, 1)
 expert_fwd_sm100_kernel(const __grid_constant__ CUtensorMap w1map, const __grid_constant__ CUtensorMap w2map,
                         const __grid_constant__ CUtensorMap ymap, const __grid_constant__ CUtensorMap xmap,
-                        Routing rt) {
+                        Routing rt, uint8_t* __restrict__ yout, int lsu) {
   using L = FwdL<DH, DE>;
   constexpr int XS = L::XS, KB1 = DH / 64;
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -265,7 +265,7 @@ expert_fwd_sm100_kernel(const __grid_constant__ CUtensorMap w1map, const __grid_
           mbar_arrive(bar(L::B_YEMPTY));
           if (et == 0) trace_ev(g_trace_fwd, 24, j);
         }
-        if (leader) bulk_wait_read<1>();       // the slab store issued from this stage 2 blocks ago has read it
+        if (leader && !lsu) bulk_wait_read<1>();   // the slab store issued from this stage 2 blocks ago has read it
         named_bar_sync(2 + q, 64);
         uint8_t* sp = smem + L::YS + st * kYStage + q * 4096;
 #pragma unroll
@@ -277,12 +277,26 @@ expert_fwd_sm100_kernel(const __grid_constant__ CUtensorMap w1map, const __grid_
           pk.w = pack_bf16x2(__uint_as_float(v[u + 6]), __uint_as_float(v[u + 7]));
           *reinterpret_cast<uint4*>(sp + kmaj_off(lane, half * 32 + u, 32)) = pk;
         }
-        fence_proxy_async();
-        named_bar_sync(2 + q, 64);
-        if (leader) {
-          tma_store_2d(&ymap, sb + L::YS + st * kYStage + q * 4096, cb * 64,
-                       (int)((size_t)tl.head * rt.Rp + tl.row0 + q * 32));
-          bulk_commit();
+        if (lsu) {
+          // coalesced 16-byte stores by the quadrant's two warps (8 lanes per 128-byte row segment):
+          // the TMA unit stays with the gathers
+          named_bar_sync(2 + q, 64);
+          const int bt = half * 32 + lane;
+          uint8_t* dst = yout + ((size_t)tl.head * rt.Rp + tl.row0 + q * 32) * (DH * 2) + cb * 128;
+#pragma unroll
+          for (int c = bt; c < 256; c += 64) {
+            const int r = c >> 3, c16 = c & 7;
+            *reinterpret_cast<uint4*>(dst + (size_t)r * (DH * 2) + c16 * 16) =
+                *reinterpret_cast<const uint4*>(sp + r * 128 + (((c16 ^ (r & 7)) & 7) << 4));
+          }
+        } else {
+          fence_proxy_async();
+          named_bar_sync(2 + q, 64);
+          if (leader) {
+            tma_store_2d(&ymap, sb + L::YS + st * kYStage + q * 4096, cb * 64,
+                         (int)((size_t)tl.head * rt.Rp + tl.row0 + q * 32));
+            bulk_commit();
+          }
         }
       }
     };
@@ -382,7 +396,7 @@ bool launch_t(const Routing& rt, const void* Xs, int64_t ldx, const void* W1, co
     TraceBuf tb{tbuf, 0};
     cudaMemcpyToSymbolAsync(g_trace_fwd, &tb, sizeof(tb), 0, cudaMemcpyHostToDevice, s);
   }
-  kern<<<num_sms, kThreads, FwdL<DH, DE>::BYTES, s>>>(w1m, w2m, ym, xm, rt);
+  kern<<<num_sms, kThreads, FwdL<DH, DE>::BYTES, s>>>(w1m, w2m, ym, xm, rt, (uint8_t*)Yrep, store_lsu(0));
   if (trace_path) {
     TraceBuf tb{nullptr, 0};
     cudaMemcpyToSymbolAsync(g_trace_fwd, &tb, sizeof(tb), 0, cudaMemcpyHostToDevice, s);

@@ -50,4 +50,9 @@ void trace_dump(const char* path, cudaStream_t s) {
   free(h);
 }
 
+int store_lsu(int def) {
+  static const char* e = getenv("MHL_STORE_TMA");
+  return e ? (atoi(e) ? 0 : 1) : def;
+}
+
 }  // namespace mhl
