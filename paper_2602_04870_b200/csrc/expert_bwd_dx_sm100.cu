@@ -92,12 +92,17 @@ struct HL {
   static constexpr int W1 = 0, W2 = WB, STG = 2 * WB, RING = STG + STGB;
   static constexpr int CTRL_MAX = 3 * 1024;
   static constexpr int S_RAW = (kMaxSmem - RING - CTRL_MAX) / kChunk;
-  // producer warps (4, or 2 when only a 2-3 stage ring fits, at d_e = 256) and warp roles
-  static constexpr int PW = S_RAW >= 4 ? 4 : 2;
+  // producer warps and warp roles.  With a >= 4-stage ring: 8 warps in 4 pairs, a pair filling a
+  // chunk (each warp 64 of its 128 rows): more warps issuing gathers raise the SM's gather rate
+  // (tools/ring_probe.cu mech 6: 5.8 -> 8.9 TB/s for L2-resident rows).  Otherwise (d_e = 256:
+  // 2-3 stages) 2 warps, each filling whole chunks.
+  static constexpr bool SPLIT = S_RAW >= 4;
+  static constexpr int PW = SPLIT ? 8 : 2;
+  static constexpr int OWNERS = SPLIT ? PW / 2 : PW;        // chunk owners (warp pairs or warps)
   static constexpr int MMA_WARP = PW, EPI_WARP0 = PW + 1, THREADS = (PW + 1 + kEpiWarps) * 32;
-  // a multiple of PW: chunk c -> stage c % S, warp c % PW, so every stage is only ever refilled by
-  // the warp that filled it before (its phase parity can never alias)
-  static constexpr int S = (S_RAW > 12 ? 12 : S_RAW) / PW * PW;
+  // a multiple of OWNERS: chunk c -> stage c % S, owner c % OWNERS, so every stage is only ever
+  // refilled by the owner that filled it before (its phase parity can never alias)
+  static constexpr int S = (S_RAW > 12 ? 12 : S_RAW) / OWNERS * OWNERS;
   // H and dA' accumulators (DE columns each) double-buffered when they fit twice in TMEM
   static constexpr int NBUF = 4 * DE <= 512 ? 2 : 1;
   static constexpr int CTRL = RING + S * kChunk;
@@ -109,7 +114,7 @@ struct HL {
   static constexpr int BYTES = TMEMP + 16;
   static_assert(BYTES - CTRL <= CTRL_MAX, "control block overflow");
   static_assert(BYTES <= kMaxSmem, "K1: shared memory over the per-CTA limit");
-  static_assert(S >= PW, "ring too small");
+  static_assert(S >= OWNERS, "ring too small");
 };
 
 template <int DH, int DE>
@@ -165,11 +170,17 @@ expert_bwd_h_kernel(const __grid_constant__ CUtensorMap w1map, const __grid_cons
     Ph w1e, w2e;
     int cnt = 0;                       // chunks of this CTA's stream so far
     const uint64_t pol_keep = (dbg & 16) ? l2_evict_normal() : l2_evict_last();   // rows reused k times per head
-    int nx[4] = {0, 0, 0, 0};          // token ids of the next tile's rows 4*lane..4*lane+3
+    // SPLIT: warp pair pw/2 owns the chunk, this warp its rows hrow..hrow+63 (lanes 0-15, 4 rows each)
+    constexpr int OWN = L::OWNERS;
+    const int owner = L::SPLIT ? pw >> 1 : pw;
+    const int lrow = L::SPLIT ? (pw & 1) * 64 + 4 * (lane & 15) : 4 * lane;
+    const bool issues = !L::SPLIT || lane < 16;
+    const bool tx_lead = lane == 0 && (!L::SPLIT || (pw & 1) == 0);
+    int nx[4] = {0, 0, 0, 0};          // token ids of the next tile's rows lrow..lrow+3
     auto load_tok = [&](int ti) {
       if (ti < 0) return;
       const Tile t = tiles[ti];
-      const int32_t* tk = rt.tok_s + (size_t)t.head * Rp + t.row0 + 4 * lane;
+      const int32_t* tk = rt.tok_s + (size_t)t.head * Rp + t.row0 + lrow;
       nx[0] = tk[0]; nx[1] = tk[1]; nx[2] = tk[2]; nx[3] = tk[3];
     };
     load_tok(sc.at(0));
@@ -189,17 +200,16 @@ expert_bwd_h_kernel(const __grid_constant__ CUtensorMap w1map, const __grid_cons
       }
       __syncwarp();
       for (int j = 0; j < 2 * KB; ++j, ++cnt) {
-        if (cnt % kProdWarps != pw) continue;
+        if (cnt % OWN != owner) continue;
         const int st = cnt % S;
         uint64_t* full = bar(L::B_FULL + 8 * st);
-        if (lane == 0) {
-          mbar_wait(bar(L::B_EMPTY + 8 * st), ((cnt / S) & 1) ^ 1);
-          mbar_expect_tx(full, kChunk);
-        }
+        if (lane == 0) mbar_wait(bar(L::B_EMPTY + 8 * st), ((cnt / S) & 1) ^ 1);
+        if (tx_lead) mbar_expect_tx(full, kChunk);
         __syncwarp();
         const int kb = j % KB;
-        tma_gather4_hint(sb + L::RING + st * kChunk + lane * 4 * 128, j < KB ? &xmap : &ymap, tl.head * DH + kb * 64,
-                         r0, r1, r2, r3, full, pol_keep);
+        if (issues)
+          tma_gather4_hint(sb + L::RING + st * kChunk + lrow * 128, j < KB ? &xmap : &ymap, tl.head * DH + kb * 64,
+                           r0, r1, r2, r3, full, pol_keep);
       }
     }
   } else if (warp == kMmaWarp) {

@@ -38,7 +38,7 @@ ring(const __grid_constant__ CUtensorMap map, const uint16_t* __restrict__ x, in
   int* stok = reinterpret_cast<int*>(empty + 16);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (tid == 0) {
-    for (int i = 0; i < S; ++i) { mbar_init(&full[i], mech == 5 ? 32 : mech == 4 ? 1 : (mech == 1 || mech == 3) ? PW : 32 * PW); mbar_init(&empty[i], 1); }
+    for (int i = 0; i < S; ++i) { mbar_init(&full[i], mech == 5 ? 32 : (mech == 4 || mech == 6) ? 1 : (mech == 1 || mech == 3) ? PW : 32 * PW); mbar_init(&empty[i], 1); }
     asm volatile("fence.mbarrier_init.release.cluster;");
   }
   __syncthreads();
@@ -68,6 +68,27 @@ ring(const __grid_constant__ CUtensorMap map, const uint16_t* __restrict__ x, in
           gather4(sb + st * kChunk + 4 * lane * 128, &map, h * 256 + kb * 64, r4[0], r4[1], r4[2], r4[3], &full[st]);
           if (lane != 0) mbar_arrive(&full[st]);   // 1 expect_tx + 31 arrivals = the 32 of a cp.async warp
         }
+      }
+    }
+  } else if (mech == 6 && warp < PW) {
+    // chunk c -> stage c % S, filled by the warp pair (c % (PW/2)): each warp of the pair gathers
+    // 64 of its 128 rows with 16 lanes (one gather4 per lane); stage ownership is fixed when S is a
+    // multiple of PW/2, so the EMPTY parity never aliases
+    int cnt = 0;
+    const int pair = warp >> 1, hrow = (warp & 1) * 64;
+    for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+      const int h = t % 8;
+      const int l16 = lane & 15;
+      const int base = (t / 8) * 128 + hrow + 4 * l16;
+      const int r0 = rows[base], r1 = rows[base + 1], r2 = rows[base + 2], r3 = rows[base + 3];
+      for (int kb = 0; kb < 4; ++kb, ++cnt) {
+        if (cnt % (PW / 2) != pair) continue;
+        const int st = cnt % S;
+        if (lane == 0) mbar_wait(&empty[st], ((cnt / S) & 1) ^ 1);
+        __syncwarp();
+        if ((warp & 1) == 0 && lane == 0) mbar_expect_tx(&full[st], kChunk);
+        if (lane < 16)
+          gather4(sb + st * kChunk + (hrow + 4 * l16) * 128, &map, h * 256 + kb * 64, r0, r1, r2, r3, &full[st]);
       }
     }
   } else if (mech == 4 && warp < PW) {
@@ -152,8 +173,13 @@ ring(const __grid_constant__ CUtensorMap map, const uint16_t* __restrict__ x, in
   }
 }
 
-int main() {
+int main(int argc, char** argv) {
   setvbuf(stdout, nullptr, _IONBF, 0);
+  // argv[1]: mechanisms (e.g. "4,5"); argv[2]: source rows (sub-token rows gathered from: 65536 = 256 MB,
+  // mostly DRAM; 8192 = 32 MB, L2-resident)
+  std::vector<int> mechs;
+  { const char* m = argc > 1 ? argv[1] : "4"; for (const char* c = m; *c; ++c) if (*c >= '0' && *c <= '9') mechs.push_back(*c - '0'); }
+  const int Tsrc = argc > 2 ? atoi(argv[2]) : 65536;
   const int T = 65536, k = 8, E = 64;
   const int64_t n = (int64_t)T * k;
   std::mt19937 rng(0);
@@ -162,7 +188,7 @@ int main() {
   for (int t = 0; t < T; ++t) { std::shuffle(perm.begin(), perm.end(), rng); for (int j = 0; j < k; ++j) key.push_back({perm[j], t}); }
   std::sort(key.begin(), key.end());
   std::vector<int> clus(n);
-  for (int64_t i = 0; i < n; ++i) clus[i] = key[i].second;
+  for (int64_t i = 0; i < n; ++i) clus[i] = key[i].second % Tsrc;
   uint16_t* x; int *rows, *sink;
   cudaMalloc(&x, (size_t)T * 4096); cudaMalloc(&rows, n * 4); cudaMalloc(&sink, 4);
   cudaMemset(x, 1, (size_t)T * 4096);
@@ -170,16 +196,16 @@ int main() {
   PFN_cuTensorMapEncodeTiled_v12000 enc; cudaDriverEntryPointQueryResult q;
   cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", (void**)&enc, cudaEnableDefault, &q);
   CUtensorMap map;
-  cuuint64_t dims[2] = {2048, (cuuint64_t)T}; cuuint64_t str[1] = {4096}; cuuint32_t box[2] = {64, 1}, es[2] = {1, 1};
+  cuuint64_t dims[2] = {2048, (cuuint64_t)Tsrc}; cuuint64_t str[1] = {4096}; cuuint32_t box[2] = {64, 1}, es[2] = {1, 1};
   enc(&map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, x, dims, str, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
       CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   const int ntiles = (int)(n / 128) * 8;   // every head of every clustered tile: 2.1 GB gathered
   char* flush; cudaMalloc(&flush, 512 << 20);
   cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
-  for (int mech : {4})
-    for (int PW : {4, 6, 8})
-      for (int S : {4, 6, 8, 12}) {
-        if (S % PW) continue;
+  for (int mech : mechs)
+    for (int PW : {4, 8})
+      for (int S : {4, 8, 12}) {
+        if (mech == 6 ? S % (PW / 2) : S % PW) continue;
         const int smem = S * kChunk + 2048;
         cudaFuncSetAttribute(ring, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         float tot = 0;
