@@ -57,7 +57,9 @@ def _compile(src: str, force: bool) -> str:
     common = ["-O3", "-std=c++17", "-Xcompiler", "-fPIC,-fvisibility=hidden", "-I", CSRC, "-I", os.path.join(ROOT, "include"),
               "-I", _nccl_include()]
     if src.endswith(".cu"):
-        cmd = [NVCC, *ARCH, "-lineinfo", "-Xptxas", "-v", *common, "-c", path, "-o", obj]
+        # MHL_NVCC_DEFS: extra -D flags for A/B builds of kernel variants (rebuild with --force)
+        defs = os.environ.get("MHL_NVCC_DEFS", "").split()
+        cmd = [NVCC, *ARCH, "-lineinfo", "-Xptxas", "-v", *common, *defs, "-c", path, "-o", obj]
     else:
         cmd = ["g++", "-O2", "-std=c++17", "-fPIC", "-fvisibility=hidden", "-I", CSRC, "-I", os.path.join(ROOT, "include"),
                "-I", _nccl_include(), "-I", os.path.join(CUDA, "include"), "-c", path, "-o", obj]

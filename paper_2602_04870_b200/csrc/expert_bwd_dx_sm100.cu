@@ -84,6 +84,10 @@ struct Sched {
 constexpr int kEpiWarps = 16;
 constexpr int kEpiThreads = kEpiWarps * 32;
 
+#ifndef MHL_K1_PW
+#define MHL_K1_PW 8   // producer warps of the backward H kernel (8: in chunk-sharing pairs; 4: whole chunks)
+#endif
+
 template <int DH, int DE>
 struct HL {
   static constexpr int WB = DE * DH * 2;
@@ -96,10 +100,14 @@ struct HL {
   // chunk (each warp 64 of its 128 rows): more warps issuing gathers raise the SM's gather rate
   // (tools/ring_probe.cu mech 6: 5.8 -> 8.9 TB/s for L2-resident rows).  Otherwise (d_e = 256:
   // 2-3 stages) 2 warps, each filling whole chunks.
-  static constexpr bool SPLIT = S_RAW >= 4;
-  static constexpr int PW = SPLIT ? 8 : 2;
+  static constexpr bool SPLIT = S_RAW >= 4 && MHL_K1_PW == 8;
+  static constexpr int PW = S_RAW >= 4 ? MHL_K1_PW : 2;
   static constexpr int OWNERS = SPLIT ? PW / 2 : PW;        // chunk owners (warp pairs or warps)
-  static constexpr int MMA_WARP = PW, EPI_WARP0 = PW + 1, THREADS = (PW + 1 + kEpiWarps) * 32;
+  // warps [0, PW) producers, [PW, PW + 16) epilogue, PW + 16 the MMA issuer.  With 8 producers
+  // the roles are warpgroup-aligned, so producers hand registers to the epilogue (setmaxnreg).
+  static constexpr int EPI_WARP0 = PW, MMA_WARP = PW + kEpiWarps, THREADS = (PW + 1 + kEpiWarps) * 32;
+  static constexpr bool REGS = PW == 8;
+  static constexpr int PROD_REGS = 40, EPI_REGS = 88;   // launch cap 72: 8*32*(72-40) >= 16*32*(88-72)
   // a multiple of OWNERS: chunk c -> stage c % S, owner c % OWNERS, so every stage is only ever
   // refilled by the owner that filled it before (its phase parity can never alias)
   static constexpr int S = (S_RAW > 12 ? 12 : S_RAW) / OWNERS * OWNERS;
@@ -160,6 +168,7 @@ expert_bwd_h_kernel(const __grid_constant__ CUtensorMap w1map, const __grid_cons
   };
 
   if (warp < kProdWarps) {
+    if constexpr (L::REGS) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(L::PROD_REGS));
     // ================================================================ producers
     // A tile is 2*KB chunks (X k-chunks, then dY k-chunks); chunk c of the CTA's stream goes to
     // ring stage c % S and is brought by warp c % kProdWarps, each of its 32 lanes issuing one TMA
@@ -256,6 +265,7 @@ expert_bwd_h_kernel(const __grid_constant__ CUtensorMap w1map, const __grid_cons
       }
     }
   } else {
+    if constexpr (L::REGS) asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(L::EPI_REGS));
     // ================================================================ epilogue (kEpiWarps warps)
     // warp -> (lane quadrant q, column group cg); each thread owns one row and NC columns of H/dA'
     // (TMEM -> gelu/gelu' -> bf16).  dH and gA leave through smem and TMA bulk stores: the warps of
@@ -282,15 +292,28 @@ expert_bwd_h_kernel(const __grid_constant__ CUtensorMap w1map, const __grid_cons
             make_uint4(w[u / 2], w[u / 2 + 1], w[u / 2 + 2], w[u / 2 + 3]);
       fence_proxy_async();
     };
+    // this row's gate and replica id, fetched one tile ahead (their L2 latency was exposed at the
+    // top of every tile, ~15% of the epilogue's period)
+    float g_n = 0.f;
+    int rep_n = -1;
+    Tile tl_n{};
+    auto fetch = [&](int t) {
+      if (t < 0) return;
+      tl_n = tiles[t];
+      const size_t gr = (size_t)tl_n.head * Rp + tl_n.row0 + row;
+      g_n = __ldg(rt.gate_s + gr);
+      rep_n = __ldg(rt.perm + gr);
+    };
+    fetch(sc.at(0));
     for (int i = 0;; ++i) {
       const int ti = sc.at(i);
       if (ti < 0) break;
       const int b = i % NBUF;
-      const Tile tl = tiles[ti];
-      const size_t grow = (size_t)tl.head * Rp + tl.row0 + row;
+      const Tile tl = tl_n;
       const int orow = (int)((size_t)tl.head * Rp + tl.row0 + q * 32);
-      const float g = rt.gate_s[grow];
-      const int rep = rt.perm[grow];
+      const float g = g_n;
+      const int rep = rep_n;
+      fetch(sc.at(i + 1));
       mbar_wait_warp(bar(L::B_HDFULL + 8 * b), hd[b].flip());
       if (tid == kEpiWarp0 * 32) trace_ev(trc, 50, i);
       tc_fence_after();

@@ -300,13 +300,21 @@ expert_fwd_sm100_kernel(const __grid_constant__ CUtensorMap w1map, const __grid_
         }
       }
     };
+    // this row's gate, fetched one tile ahead (its L2 latency would sit at the top of every tile)
+    float g_n = 0.f;
+    auto fetch = [&](int t) {
+      if (t < 0) return;
+      const Tile u = tiles[t];
+      g_n = __ldg(rt.gate_s + (size_t)u.head * rt.Rp + u.row0 + row);
+    };
+    fetch(tile_at(0));
     int i = 0;
     for (;; ++i) {
       const int ti = tile_at(i);
       if (ti < 0) break;
-      const Tile tl = tiles[ti];
       const int b = i % L::NA;
-      const float g = rt.gate_s[(size_t)tl.head * rt.Rp + tl.row0 + row];
+      const float g = g_n;
+      fetch(tile_at(i + 1));
       mbar_wait_warp(bar(L::B_HFULL), hf.flip());
       if (et == 0) trace_ev(g_trace_fwd, 20, i);
       tc_fence_after();
