@@ -349,12 +349,13 @@ expert_bwd_h_kernel(const __grid_constant__ CUtensorMap w1map, const __grid_cons
         // LSU variant: the box warps copy the staged slot to global with coalesced 16-byte stores
         // (8 lanes per 128-byte row segment), leaving the TMA unit to the gathers
         const int bt = (cg % WPB) * 32 + lane;
+        const uint64_t pol_out = l2_evict_first();   // streamed out once; keep L2 for the gathered rows
         auto copy_out = [&](uint8_t* dst) {
 #pragma unroll
           for (int c = bt; c < 256; c += 32 * WPB) {
             const int r = c >> 3, c16 = c & 7;
             const uint4 v = *reinterpret_cast<const uint4*>(slot + r * 128 + (((c16 ^ (r & 7)) & 7) << 4));
-            *reinterpret_cast<uint4*>(dst + ((size_t)orow + r) * (DE * 2) + box * 128 + c16 * 16) = v;
+            st_global_v4_hint(dst + ((size_t)orow + r) * (DE * 2) + box * 128 + c16 * 16, v, pol_out);
           }
         };
         box_sync();

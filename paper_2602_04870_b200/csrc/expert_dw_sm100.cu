@@ -105,6 +105,9 @@ expert_dw_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant
     for (int p = warp; p < NP; p += kDwProd) mybytes += kHalf * 128;
     for (int t = warp; t < NT; t += kDwProd) mybytes += kHalf * 128;
     int n = 0;                                                // steps of this CTA so far
+    // X / dY rows are re-gathered by the head's other experts (keep them in L2); dH / gA stream
+    // through once (evict first), so they do not push the reused rows out
+    const uint64_t pol_keep = l2_evict_last(), pol_stream = l2_evict_first();
     MyChunks it(rt);
     for (int ci; (ci = it.next()) >= 0 && ci < nchunks;) {
       const Tile ch = chunks[ci];
@@ -121,15 +124,15 @@ expert_dw_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant
           mbar_expect_tx(&full[st], mybytes);
           for (int t = warp; t < NT; t += kDwProd) {
             const int kb = t % EK;
-            tma_load_2d(base + (t < EK ? L::DHH : L::GA) + kb * kHalf * 128, t < EK ? &hmap : &amap, kb * 64,
-                        (int)((size_t)ch.head * Rp + ch.row0 + s * kHalf), &full[st]);
+            tma_load_2d_hint(base + (t < EK ? L::DHH : L::GA) + kb * kHalf * 128, t < EK ? &hmap : &amap, kb * 64,
+                             (int)((size_t)ch.head * Rp + ch.row0 + s * kHalf), &full[st], pol_stream);
           }
         }
         __syncwarp();
         for (int u = lane; u < ((NP - warp + kDwProd - 1) / kDwProd) * 16; u += 32) {
           const int p = warp + (u >> 4) * kDwProd, kb = p % XK;
-          tma_gather4(base + (p < XK ? L::X : L::DY) + kb * kHalf * 128 + 4 * g * 128, p < XK ? &xmap : &ymap,
-                      ch.head * DH + kb * 64, r0, r1, r2, r3, &full[st]);
+          tma_gather4_hint(base + (p < XK ? L::X : L::DY) + kb * kHalf * 128 + 4 * g * 128, p < XK ? &xmap : &ymap,
+                           ch.head * DH + kb * 64, r0, r1, r2, r3, &full[st], pol_keep);
         }
         r0 = q0; r1 = q1; r2 = q2; r3 = q3;
         if (s + 2 < nsteps) {

@@ -35,10 +35,13 @@ using namespace sm100;
 __device__ TraceBuf g_trace_fwd;     // profiling aid (MHL_TRACE_FWD=<file>), off by default
 
 constexpr int BM = kExpertBM;        // 128 rows = MMA M
-constexpr int kProdWarps = 4;         // warps 0-3: producers
-constexpr int kMmaWarp = 4;           // warp 4: MMA issuer + TMEM owner
-constexpr int kEpiWarp0 = 5;          // warps 5-12: epilogue
-constexpr int kThreads = 13 * 32;
+// Warp roles, warpgroup-aligned so the producers can hand registers to the epilogue (setmaxnreg):
+constexpr int kProdWarps = 8;         // warps 0-7: producers, in 4 pairs (a pair fills one X chunk)
+constexpr int kOwners = kProdWarps / 2;
+constexpr int kEpiWarp0 = 8;          // warps 8-15: epilogue
+constexpr int kMmaWarp = 16;          // warp 16: MMA issuer + TMEM owner
+constexpr int kThreads = 17 * 32;
+constexpr int kProdRegs = 40, kEpiRegs = 152;   // launch cap 96: 8*32*(96-40) >= 8*32*(152-96)
 constexpr int kEpiThreads = 256;
 constexpr int kXChunk = BM * 128;    // one 64-column K-chunk of the gathered X tile (16 KB)
 constexpr int kYStage = BM * 128;    // one 64-column block of the Y tile (16 KB)
@@ -48,8 +51,8 @@ struct FwdL {
   static constexpr int WB = DE * DH * 2;
   static constexpr int W1 = 0, W2 = WB, YS = 2 * WB, X = YS + 2 * kYStage;
   static constexpr int XS_RAW = (224 * 1024 - X) / kXChunk;
-  static constexpr int XS = (XS_RAW > 12 ? 12 : XS_RAW) / kProdWarps * kProdWarps;   // X ring stages
-  static_assert(XS >= kProdWarps, "X ring too small");
+  static constexpr int XS = (XS_RAW > 12 ? 12 : XS_RAW) / kOwners * kOwners;   // X ring stages
+  static_assert(XS >= kOwners, "X ring too small");
   static constexpr int CTRL = X + XS * kXChunk;
   static constexpr int B_XFULL = CTRL, B_XEMPTY = B_XFULL + 8 * XS;
   static constexpr int B_W1F = B_XEMPTY + 8 * XS, B_W1E = B_W1F + 8, B_W2F = B_W1E + 8, B_W2E = B_W2F + 8;
@@ -131,13 +134,16 @@ expert_fwd_sm100_kernel(const __grid_constant__ CUtensorMap w1map, const __grid_
   };
 
   if (warp < kProdWarps) {
-    // ================================================================ producers (4 warps)
+    // ================================================================ producers (8 warps)
     // Chunk c of this CTA's X stream (tile c / KB1, column block c % KB1) goes to ring stage
-    // c % XS and is brought by warp c % kProdWarps (XS is a multiple of kProdWarps, so a stage is
-    // only ever refilled by the warp that filled it before): each of its 32 lanes issues one TMA
-    // gather4 of 4 sub-token rows (lane l owns tile rows 4l..4l+3).  Warp 0 lane 0 also issues the
-    // weight TMAs.
+    // c % XS and is brought by warp pair c % kOwners (XS is a multiple of kOwners, so a stage is
+    // only ever refilled by the pair that filled it before): lanes 0-15 of each warp of the pair
+    // issue one TMA gather4 of 4 sub-token rows each (warp 2p+h owns tile rows 64h..64h+63).  More
+    // warps issuing gathers raise the SM's gather rate (tools/ring_probe.cu mech 6).  Warp 0 lane 0
+    // also issues the weight TMAs.
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kProdRegs));
     const int pw = warp;
+    const int owner = pw >> 1, lrow = (pw & 1) * 64 + 4 * (lane & 15);
     Ph w1e, w2e;
     int cnt = 0;
     int nx[4] = {0, 0, 0, 0};
@@ -145,7 +151,7 @@ expert_fwd_sm100_kernel(const __grid_constant__ CUtensorMap w1map, const __grid_
       const int t0 = tile_at(0);
       if (t0 >= 0) {
         const Tile tl = tiles[t0];
-        const int32_t* tk = rt.tok_s + (size_t)tl.head * rt.Rp + tl.row0 + 4 * lane;
+        const int32_t* tk = rt.tok_s + (size_t)tl.head * rt.Rp + tl.row0 + lrow;
         nx[0] = tk[0]; nx[1] = tk[1]; nx[2] = tk[2]; nx[3] = tk[3];
       }
     }
@@ -163,7 +169,7 @@ expert_fwd_sm100_kernel(const __grid_constant__ CUtensorMap w1map, const __grid_
       const int tn = tile_at(i + 1);
       if (tn >= 0) {     // next tile's token ids, loaded while this tile's chunks are issued
         const Tile tnl = tiles[tn];
-        const int32_t* tk = rt.tok_s + (size_t)tnl.head * rt.Rp + tnl.row0 + 4 * lane;
+        const int32_t* tk = rt.tok_s + (size_t)tnl.head * rt.Rp + tnl.row0 + lrow;
         nx[0] = tk[0]; nx[1] = tk[1]; nx[2] = tk[2]; nx[3] = tk[3];
       }
       if (pw == 0 && lane == 0 && !same_expert(tile_at(i - 1), ti)) {
@@ -172,16 +178,17 @@ expert_fwd_sm100_kernel(const __grid_constant__ CUtensorMap w1map, const __grid_
       }
       __syncwarp();
       for (int kb = 0; kb < KB1; ++kb, ++cnt) {
-        if (cnt % kProdWarps != pw) continue;
+        if (cnt % kOwners != owner) continue;
         const int xs = cnt % XS;
         uint64_t* full = bar(L::B_XFULL + 8 * xs);
         if (lane == 0) {
           mbar_wait(bar(L::B_XEMPTY + 8 * xs), ((cnt / XS) & 1) ^ 1);
-          mbar_expect_tx(full, kXChunk);
+          if ((pw & 1) == 0) mbar_expect_tx(full, kXChunk);
         }
         __syncwarp();
-        tma_gather4(sb + L::X + xs * kXChunk + lane * 4 * 128, &xmap, (int)tl.head * DH + kb * 64, r0, r1, r2, r3,
-                    full);
+        if (lane < 16)
+          tma_gather4(sb + L::X + xs * kXChunk + lrow * 128, &xmap, (int)tl.head * DH + kb * 64, r0, r1, r2, r3,
+                      full);
       }
       // W2 of the previous tile if it started a new expert run (read by G2(i-1), issued after G1(i))
       if (pw == 0 && lane == 0 && i >= 1 && !same_expert(tile_at(i - 2), tile_at(i - 1))) {
@@ -238,6 +245,7 @@ expert_fwd_sm100_kernel(const __grid_constant__ CUtensorMap w1map, const __grid_
       if (i >= 1) gemm2(i - 1);
     }
   } else {
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kEpiRegs));
     // ================================================================ epilogue (8 warps)
     const int q = warp & 3, half = (warp - kEpiWarp0) >> 2;   // lane quadrant, column half
     const int row = q * 32 + lane;
