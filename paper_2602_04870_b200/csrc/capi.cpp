@@ -554,14 +554,15 @@ mhl_status moe_backward_local(mhl_plan p, const RankPtrs& R, const void* dY, voi
                                         (float*)(R.ws + B.dwr_part),
                                         // token chunks per head from the GLOBAL head count, so the
                                         // partial-sum order (and dW_r bits) do not depend on G
-                                        std::min(m.n_rt, std::max(1, p->num_sms / m.N_h)), R.dW_r, s))
+                                        std::min(m.n_rt, std::max(1, p->num_sms / m.N_h)), R.dW_r, s, rt.pos, m.Rp,
+                                        tc ? (float*)(R.ws + B.dS_s) : nullptr))
         return fail(MHL_ERR_CUDA, "router backward: TMA tensor-map encoding failed");
     } else {
       mhl::launch_router_bwd(m.dtype, Xs, m.HD, idx, gate, dg, m.H, m.T_g, m.k, m.d_h, m.N_e, dS,
                              (float*)(R.ws + B.dwr_part), R.dW_r, s);
+      if (tc) { mhl::launch_sort_ds(rt, dS, (float*)(R.ws + B.dS_s), s); p->launches++; }
     }
     mhl::launch_transpose_wr(R.W_r, W_rT, m.H, m.d_h, m.N_e, s);
-    if (tc) mhl::launch_sort_ds(rt, dS, (float*)(R.ws + B.dS_s), s);
   }
   if (tc) {
     MHL_SPAN("B5_expert_dx_gemm");
@@ -582,8 +583,8 @@ mhl_status moe_backward_local(mhl_plan p, const RankPtrs& R, const void* dY, voi
     MHL_SPAN("B6_combine_bwd");
     combine_bwd(m, rt, dXrep, dS, W_rT, tc, dxout, m.HD, s, 0, -1);
   }
-  // K1 + K2 + dW (+ its in-kernel reduce) + router (2) + transpose + dS sort + combine on the tensor-core path
-  p->launches += (tc ? 8 : (R.dW1 || R.dW2 ? 6 : 5)) - (dxout ? 0 : 1);
+  // K1 + K2 + dW (+ its in-kernel reduce) + router (2) + transpose + combine on the tensor-core path
+  p->launches += (tc ? 7 : (R.dW1 || R.dW2 ? 6 : 5)) - (dxout ? 0 : 1);
   return check_kernels(p);
 }
 

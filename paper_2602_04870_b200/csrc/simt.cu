@@ -321,7 +321,6 @@ sort_ds_kernel(const float* __restrict__ dS, const int32_t* __restrict__ pos, in
 }
 
 void launch_sort_ds(const Routing& rt, const float* dS, float* dS_s, cudaStream_t s) {
-  cudaMemsetAsync(dS_s, 0, (size_t)rt.H * rt.Rp * 4, s);
   const int64_t total = (int64_t)rt.H * rt.T * rt.k;
   if (total <= 0) return;
   const int blocks = (int)std::min<int64_t>((total + 255) / 256, 148 * 8);
