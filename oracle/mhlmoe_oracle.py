@@ -12,6 +12,9 @@ blocking, fusion or reordering beyond what the cited definition states.
 Shapes (global problem, independent of the number of GPUs G):
     x      [T, d]                tokens (B*T flattened b-major, R20)
     W_in   [D, d]   D = N_h*d_h  Eq. 5, P:765  (x_t -> W_in x_t)
+           or [2D, d] with separate routing sub-tokens (ablation, P:1565-P:1570):
+           [x_t1..x_tNh, r_t1..r_tNh] = split(W_in x_t); head i routes on r_ti and
+           computes its experts on x_ti
     W_out  [d, D]                Eq. 6, P:772
     W_r    [N_h, d_h, N_e]       router, fp32 values (Alg. 1 REQUIRE)
     b      [N_h, N_e]            aux-free load-balancing bias
@@ -36,7 +39,7 @@ __all__ = [
     "experts_dense", "experts_sparse_loop", "expert_flex_form",
     "cluster_plan", "layer_forward", "layer_backward", "hp_layer_forward",
     "hp_layer_backward", "hp_a2a_bytes", "layer_flops", "moe_flops_equivalent",
-    "ep_dispatch_rows", "ForwardCache", "expert_loads", "update_bias",
+    "ep_dispatch_rows", "ForwardCache", "expert_loads", "update_bias", "has_routing_tokens",
 ]
 
 
@@ -297,6 +300,16 @@ def _heads(P):
     return N_h, d_h
 
 
+def has_routing_tokens(P) -> bool:
+    """W_in [2D, d]: the separate-routing-token variant of P:1565-P:1570."""
+    N_h, d_h = _heads(P)
+    D = N_h * d_h
+    rows = np.asarray(P["W_in"]).shape[0]
+    if rows not in (D, 2 * D):
+        raise ValueError("W_in must have N_h*d_h rows (or 2*N_h*d_h with routing tokens)")
+    return rows == 2 * D
+
+
 def layer_forward(P: dict, x: np.ndarray, k: int, mode: str = "bf16",
                   forced_idx: dict | None = None) -> ForwardCache:
     """o_t = W_out concat(f_1(x_t1), ..., f_Nh(x_tNh)), [x_t1..x_tNh] = split(W_in x_t).
@@ -308,6 +321,8 @@ def layer_forward(P: dict, x: np.ndarray, k: int, mode: str = "bf16",
     scores at the forced experts.
     """
     N_h, d_h = _heads(P)
+    D = N_h * d_h
+    rtok = has_routing_tokens(P)
     x = np.asarray(x, np.float64)
     Xs_pre = x @ np.asarray(P["W_in"], np.float64).T
     Xs = round_storage(Xs_pre, mode)                                          # O1
@@ -315,7 +330,9 @@ def layer_forward(P: dict, x: np.ndarray, k: int, mode: str = "bf16",
     ys = []
     for h in range(N_h):
         X_h = Xs[:, h * d_h:(h + 1) * d_h]                                   # O2
-        I, S_sel, margin, S, _K = route_topk(X_h, P["W_r"][h], P["b"][h], k)  # O3-O4
+        # routing sub-token: x_th itself, or r_th = columns D + h*d_h.. (P:1568-P:1569)
+        R_h = Xs[:, D + h * d_h:D + (h + 1) * d_h] if rtok else X_h
+        I, S_sel, margin, S, _K = route_topk(R_h, P["W_r"][h], P["b"][h], k)  # O3-O4
         if forced_idx is not None and h in forced_idx:
             I = np.asarray(forced_idx[h], np.int64)
             S_sel = S[np.arange(S.shape[0])[:, None], I]
@@ -336,6 +353,8 @@ def layer_backward(P: dict, x: np.ndarray, dout: np.ndarray, C: ForwardCache) ->
     """
     mode = C.mode
     N_h, d_h = _heads(P)
+    D = N_h * d_h
+    rtok = has_routing_tokens(P)
     x = np.asarray(x, np.float64)
     dout = np.asarray(dout, np.float64)
     W_out = np.asarray(P["W_out"], np.float64)
@@ -344,14 +363,17 @@ def layer_backward(P: dict, x: np.ndarray, dout: np.ndarray, C: ForwardCache) ->
     dW_r = np.zeros(P["W_r"].shape)
     dW1 = np.zeros(P["W1"].shape)
     dW2 = np.zeros(P["W2"].shape)
-    dXs_heads, dgs, dSs = [], [], []
+    dXs_heads, dR_heads, dgs, dSs = [], [], [], []
     for h in range(N_h):
         X_h = C.Xs[:, h * d_h:(h + 1) * d_h]
+        R_h = C.Xs[:, D + h * d_h:D + (h + 1) * d_h] if rtok else None
         dY = dcat[:, h * d_h:(h + 1) * d_h]                                   # O10
-        gh = _head_backward(_head_params(P, h), X_h, dY, C.I[h], C.g[h])      # O10-O11
+        gh = _head_backward(_head_params(P, h), X_h, dY, C.I[h], C.g[h], R_h)  # O10-O11
         dW_r[h], dW1[h], dW2[h] = gh["dW_r"], gh["dW1"], gh["dW2"]
         dXs_heads.append(gh["dXs_h"]); dgs.append(gh["dg"]); dSs.append(gh["dS"])
-    dXs = round_storage(np.concatenate(dXs_heads, axis=1), mode)             # O12
+        if rtok:
+            dR_heads.append(gh["dR_h"])
+    dXs = round_storage(np.concatenate(dXs_heads + dR_heads, axis=1), mode)  # O12
     dx = round_storage(dXs @ np.asarray(P["W_in"], np.float64), mode)
     dW_in = dXs.T @ x
     return dict(dx=dx, dW_in=dW_in, dW_out=dW_out, dW_r=dW_r, dW1=dW1, dW2=dW2,
@@ -383,19 +405,25 @@ def hp_layer_forward(P: dict, x: np.ndarray, k: int, G: int, mode: str = "bf16")
     state list, byte matrix [G,G] summed over both forward all-to-alls)."""
     N_h, d_h = _heads(P)
     _check_hp(N_h, G)
+    D = N_h * d_h
+    rtok = has_routing_tokens(P)
     x = np.asarray(x, np.float64)
     T = x.shape[0]
     if T % G:
         raise ValueError("T must be divisible by G")
     T_loc, H_loc = T // G, N_h // G
+    HD = H_loc * d_h
     el = {"bf16": 2, "fp32": 4, "fp64": 8}[mode]
     nbytes = np.zeros((G, G), np.int64)
-    # rank r: projection of its own tokens (Eq. 5), split into destination blocks
+    # rank r: projection of its own tokens (Eq. 5), split into destination blocks; with routing
+    # sub-tokens the block also carries r_t of the destination's heads (P:1570: twice the bytes)
     send1 = {}
     for r in range(G):
         Xs_r = round_storage(x[r * T_loc:(r + 1) * T_loc] @ np.asarray(P["W_in"], np.float64).T, mode)
         for p in range(G):
-            blk = Xs_r[:, p * H_loc * d_h:(p + 1) * H_loc * d_h].copy()
+            blk = Xs_r[:, p * HD:(p + 1) * HD].copy()
+            if rtok:
+                blk = np.concatenate([blk, Xs_r[:, D + p * HD:D + (p + 1) * HD]], axis=1)
             send1[(r, p)] = blk
             if p != r:
                 nbytes[r, p] += blk.size * el
@@ -407,7 +435,8 @@ def hp_layer_forward(P: dict, x: np.ndarray, k: int, G: int, mode: str = "bf16")
         for hl in range(H_loc):
             h = p * H_loc + hl
             X_h = recv1[:, hl * d_h:(hl + 1) * d_h]
-            I, S_sel, _m, _S, _K = route_topk(X_h, P["W_r"][h], P["b"][h], k)
+            R_h = recv1[:, HD + hl * d_h:HD + (hl + 1) * d_h] if rtok else X_h
+            I, S_sel, _m, _S, _K = route_topk(R_h, P["W_r"][h], P["b"][h], k)
             g = gates_from_scores(S_sel)
             st["I"].append(I); st["g"].append(g)
             st["y"].append(experts_dense(X_h, P["W1"][h], P["W2"][h], I, g))
@@ -433,8 +462,10 @@ def hp_layer_backward(P, x, dout, k, G, mode="bf16"):
     #3 and #4).  dW_in / dW_out are returned summed over ranks (R19)."""
     out, ranks, nb_f = hp_layer_forward(P, x, k, G, mode)
     N_h, d_h = _heads(P)
+    rtok = has_routing_tokens(P)
     T = x.shape[0]
     T_loc, H_loc = T // G, N_h // G
+    HD = H_loc * d_h
     el = {"bf16": 2, "fp32": 4, "fp64": 8}[mode]
     nbytes = np.zeros((G, G), np.int64)
     x = np.asarray(x, np.float64)
@@ -455,15 +486,18 @@ def hp_layer_backward(P, x, dout, k, G, mode="bf16"):
     dXs_blocks = {}
     for p in range(G):
         recv3 = np.concatenate([dcat[(r, p)] for r in range(G)], axis=0)
-        dX_loc = []
+        dX_loc, dR_loc = [], []
         for hl in range(H_loc):
             h = p * H_loc + hl
             X_h = ranks[p]["Xs"][:, hl * d_h:(hl + 1) * d_h]
+            R_h = ranks[p]["Xs"][:, HD + hl * d_h:HD + (hl + 1) * d_h] if rtok else None
             gh = _head_backward(_head_params(P, h), X_h, recv3[:, hl * d_h:(hl + 1) * d_h],
-                                ranks[p]["I"][hl], ranks[p]["g"][hl])
+                                ranks[p]["I"][hl], ranks[p]["g"][hl], R_h)
             dW_r[h] = gh["dW_r"]; dW1[h] = gh["dW1"]; dW2[h] = gh["dW2"]
             dX_loc.append(gh["dXs_h"])
-        dXl = np.concatenate(dX_loc, axis=1)
+            if rtok:
+                dR_loc.append(gh["dR_h"])
+        dXl = np.concatenate(dX_loc + dR_loc, axis=1)   # [T, HD] or [T, 2HD] (dX | dR of local heads)
         for r in range(G):
             blk = round_storage(dXl[r * T_loc:(r + 1) * T_loc], mode)
             dXs_blocks[(p, r)] = blk
@@ -471,7 +505,8 @@ def hp_layer_backward(P, x, dout, k, G, mode="bf16"):
                 nbytes[p, r] += blk.size * el
     dx = np.zeros(x.shape); dW_in = np.zeros(P["W_in"].shape)
     for r in range(G):
-        dXs_r = np.concatenate([dXs_blocks[(p, r)] for p in range(G)], axis=1)
+        dXs_r = np.concatenate([dXs_blocks[(p, r)][:, :HD] for p in range(G)]
+                               + ([dXs_blocks[(p, r)][:, HD:] for p in range(G)] if rtok else []), axis=1)
         dx[r * T_loc:(r + 1) * T_loc] = round_storage(dXs_r @ np.asarray(P["W_in"], np.float64), mode)
         dW_in += dXs_r.T @ x[r * T_loc:(r + 1) * T_loc]
     return dict(out=out, dx=dx, dW_in=dW_in, dW_out=dW_out, dW_r=dW_r, dW1=dW1, dW2=dW2,
@@ -482,12 +517,14 @@ def _head_params(P, h):
     return dict(W_r=P["W_r"][h:h + 1], b=P["b"][h:h + 1], W1=P["W1"][h:h + 1], W2=P["W2"][h:h + 1])
 
 
-def _head_backward(Ph, X_h, dY, I, g):
+def _head_backward(Ph, X_h, dY, I, g, R_h=None):
     """Per-head part of O10-O11: chain rule of Eq. 1 through the dense-masked
     experts (dW2 = A^T (w dY), dH = (w dY W2^T) * gelu'(H), dW1 = dH^T X,
     dX += dH W1, dg_j = <dY, E_{I_j}(x)>), the softmax Jacobian of Eq. 2 over the
     k selected scores (dS = g (dg - sum g dg)), and Alg. 2 (P:846-P:866) in its
-    dense-masked form: dW_r = X^T dS_full, dX += dS_full W_r^T (R13)."""
+    dense-masked form: dW_r = X^T dS_full, dX += dS_full W_r^T (R13).  With a
+    separate routing sub-token R_h (P:1565-P:1570) the router terms use R_h:
+    dW_r = R^T dS_full and dR = dS_full W_r^T is returned apart from dX."""
     N_e = Ph["W1"].shape[1]
     T, k = I.shape
     w = _selection_weights(I, g, N_e)
@@ -511,9 +548,12 @@ def _head_backward(Ph, X_h, dY, I, g):
     dS_full = np.zeros((T, N_e))
     dS_full[np.arange(T)[:, None], I] = dS
     W_r_h = np.asarray(Ph["W_r"][0], np.float64)
-    dW_r = X_h.T @ dS_full
-    dXs_h = dXs_h + dS_full @ W_r_h.T
-    return dict(dXs_h=dXs_h, dW_r=dW_r, dW1=dW1, dW2=dW2, dg=dg, dS=dS)
+    if R_h is None:
+        dW_r = X_h.T @ dS_full
+        dXs_h = dXs_h + dS_full @ W_r_h.T
+        return dict(dXs_h=dXs_h, dW_r=dW_r, dW1=dW1, dW2=dW2, dg=dg, dS=dS)
+    dW_r = R_h.T @ dS_full
+    return dict(dXs_h=dXs_h, dR_h=dS_full @ W_r_h.T, dW_r=dW_r, dW1=dW1, dW2=dW2, dg=dg, dS=dS)
 
 
 # ---------------------------------------------------------------------------

@@ -219,3 +219,91 @@ def test_hp_rejects_bad_degree():
     P, x, _ = _prob(TINY64, 0)
     with pytest.raises(ValueError):
         O.hp_layer_forward(P, x, 2, 2, mode="fp32")    # N_h = 3 not divisible by 2
+
+
+# ---------------------------------------------------------------- separate routing sub-tokens (P:1565-P:1570)
+RT = LayerConfig("rt", T=40, d=10, N_h=2, d_h=4, N_e=6, k=2, d_e=3, dtype="fp32", routing_tokens=True)
+
+
+def test_routing_tokens_with_duplicated_rows_is_the_base_layer():
+    """W_in = [W; W] makes r_t = x_t: forward, routing and every gradient reduce to the base layer
+    (dW_in's two halves summing to the base dW_in), in fp64 storage mode."""
+    cfg = RT.replace(routing_tokens=False)
+    P, x, dout = _prob(cfg, 50)
+    P2 = dict(P, W_in=np.concatenate([P["W_in"], P["W_in"]], axis=0))
+    C = O.layer_forward(P, x, cfg.k, mode="fp64")
+    C2 = O.layer_forward(P2, x, cfg.k, mode="fp64")
+    for h in range(cfg.N_h):
+        np.testing.assert_array_equal(C2.I[h], C.I[h])
+    np.testing.assert_allclose(C2.out, C.out, rtol=1e-12, atol=1e-14)
+    g = O.layer_backward(P, x, dout, C)
+    g2 = O.layer_backward(P2, x, dout, C2)
+    D = cfg.D
+    np.testing.assert_allclose(g2["dW_in"][:D] + g2["dW_in"][D:], g["dW_in"], rtol=1e-12, atol=1e-13)
+    for key in ("dx", "dW_out", "dW_r", "dW1", "dW2"):
+        np.testing.assert_allclose(g2[key], g[key], rtol=1e-12, atol=1e-13)
+    assert g2["dW_in"].shape == (2 * D, cfg.d)
+
+
+def test_routing_tokens_route_on_r_and_compute_on_x():
+    """The selection depends only on the routing rows of W_in, the expert output only (given the
+    selection) on the sub-token rows: perturbing the sub-token half leaves every I unchanged, and
+    perturbing the routing half leaves the selected experts' inputs unchanged."""
+    P, x, _ = _prob(RT, 51)
+    D = RT.D
+    C = O.layer_forward(P, x, RT.k, mode="fp64")
+    Px = dict(P, W_in=P["W_in"].copy())
+    Px["W_in"][:D] *= 1.7
+    Cx = O.layer_forward(Px, x, RT.k, mode="fp64")
+    for h in range(RT.N_h):
+        np.testing.assert_array_equal(Cx.I[h], C.I[h])
+    assert not np.allclose(Cx.out, C.out)
+    Pr = dict(P, W_in=P["W_in"].copy())
+    Pr["W_in"][D:] = np.random.default_rng(3).standard_normal(Pr["W_in"][D:].shape)
+    Cr = O.layer_forward(Pr, x, RT.k, mode="fp64")
+    assert any(not np.array_equal(Cr.I[h], C.I[h]) for h in range(RT.N_h))
+    np.testing.assert_array_equal(Cr.Xs[:, :D], C.Xs[:, :D])
+
+
+@pytest.mark.parametrize("seed", [52, 53])
+def test_routing_tokens_backward_finite_differences(seed):
+    P, x, dout = _prob(RT, seed)
+    C = O.layer_forward(P, x, RT.k, mode="fp64")
+    forced = {h: C.I[h] for h in range(RT.N_h)}
+    grads = O.layer_backward(P, x, dout, C)
+    rng = np.random.default_rng(seed)
+    eps = 1e-6
+    for name, gname in [("W_in", "dW_in"), ("W_r", "dW_r"), ("W1", "dW1"), ("x", "dx")]:
+        for _ in range(3):
+            v = rng.standard_normal(x.shape if name == "x" else P[name].shape)
+            def f(s):
+                Pp = dict(P)
+                xx = x
+                if name == "x":
+                    xx = x + s * v
+                else:
+                    Pp[name] = P[name] + s * v
+                return _loss(Pp, xx, dout, RT.k, forced)
+            fd = (f(eps) - f(-eps)) / (2 * eps)
+            an = float(np.sum(grads[gname] * v))
+            assert abs(fd - an) <= 1e-6 * max(1.0, abs(an)), (name, fd, an)
+    # the routing half of dW_in is the router's alone: zero when every dS vanishes (dout = 0 on gates)
+    assert np.any(grads["dW_in"][RT.D:] != 0)
+    assert min(float(np.min(m)) for m in C.margin) > 1e-5
+
+
+@pytest.mark.parametrize("G", [1, 2])
+def test_routing_tokens_hp_equals_unsharded_and_doubles_scatter_bytes(G):
+    cfg = RT.replace(T=48, N_h=2, dtype="bf16")
+    P, x, dout = _prob(cfg, 54)
+    C = O.layer_forward(P, x, cfg.k, mode="bf16")
+    ref = O.layer_backward(P, x, dout, C)
+    hp = O.hp_layer_backward(P, x, dout, cfg.k, G, mode="bf16")
+    np.testing.assert_array_equal(hp["out"], C.out)
+    np.testing.assert_array_equal(hp["dx"], ref["dx"])
+    for key in ("dW_in", "dW_out", "dW_r", "dW1", "dW2"):
+        np.testing.assert_allclose(hp[key], ref[key], rtol=1e-12, atol=1e-14)
+    per_pair = (cfg.T // G) * (cfg.N_h // G) * cfg.d_h * 2
+    # forward: the scatter carries x and r (2 blocks), the gather the head outputs (1 block)
+    assert np.all(hp["bytes_fwd"][~np.eye(G, dtype=bool)] == 3 * per_pair)
+    assert np.all(hp["bytes_bwd"] == hp["bytes_fwd"])

@@ -37,6 +37,7 @@ class LayerConfig:
     d_e: int
     dtype: str          # "bf16" or "fp32" (storage/compute mode of the CUDA path)
     fwd_only: bool = False
+    routing_tokens: bool = False   # separate routing sub-tokens (P:1565-P:1570): W_in is [2D, d]
 
     @property
     def D(self) -> int:
@@ -94,7 +95,7 @@ def make_weights(cfg: LayerConfig, seed: int = 0, dist: str = "conf", skew: floa
     else:
         raise ValueError(dist)
     W = dict(
-        W_in=_normal(seed, TID["W_in"], (D, d), std["W_in"]),
+        W_in=_normal(seed, TID["W_in"], ((2 if cfg.routing_tokens else 1) * D, d), std["W_in"]),
         W_out=_normal(seed, TID["W_out"], (d, D), std["W_out"]),
         W_r=_normal(seed, TID["W_r"], (N_h, d_h, N_e), std["W_r"]),
         W1=_normal(seed, TID["W1"], (N_h, N_e, d_e, d_h), std["W1"]),
