@@ -56,6 +56,11 @@ typedef enum { MHL_F32 = 0, MHL_BF16 = 1 } mhl_dtype;
                                  tcgen05 kernels (debug/cross-check path; fp32 mode always SIMT). */
 #define MHL_FLAG_PAIR     4u  /* bf16: CTA-pair (tcgen05 cta_group::2) expert kernels; expert
                                  segments are then padded to 256-row tile pairs   */
+#define MHL_FLAG_ROUTING_TOKENS 8u  /* separate routing sub-tokens (ablation, P:1565-P:1570):
+                                 [x_t1..x_tNh, r_t1..r_tNh] = split(W_in x_t), W_in is [2D, d];
+                                 head i routes on r_ti and runs its experts on x_ti.  The HP
+                                 scatter (and its backward mirror) carries both: twice the bytes
+                                 (P:1570); dW_in is [2D, d]. */
 
 /* Layer + HP configuration (the paper's problem statement: P:496). */
 typedef struct {
@@ -77,7 +82,8 @@ typedef struct {
 typedef struct {
   int32_t head_begin, head_end;     /* local heads [head_begin, head_end) of this rank (R12)      */
   int64_t tokens_global;            /* T_glob = G*T_loc                                           */
-  uint64_t a2a_bytes_per_peer;      /* one all-to-all, one (src,dst) pair: T_loc*H_loc*d_h*el     */
+  uint64_t a2a_bytes_per_peer;      /* the scatter all-to-all, one (src,dst) pair: T_loc*H_loc*d_h*el
+                                       (x2 with MHL_FLAG_ROUTING_TOKENS; the gather is always 1x) */
   uint64_t a2a_bytes_per_rank;      /* one all-to-all, sent by one rank: per_peer*(G-1)           */
   uint64_t saved_bytes;             /* forward -> backward state                                  */
   uint64_t workspace_bytes;         /* scratch for forward and for backward                       */
@@ -90,7 +96,7 @@ typedef struct mhl_plan_s* mhl_plan;
 /* Device weights.  Without LOOPBACK the router/expert tensors hold only the
  * rank's LOCAL heads (HP shards experts like EP); with LOOPBACK all N_h. */
 typedef struct {
-  const void*  W_in;   /* [D, d]  E      Eq. 5 (x_t -> W_in x_t)                          */
+  const void*  W_in;   /* [D, d]  E      Eq. 5 (x_t -> W_in x_t), P:765  ([2D, d] with ROUTING_TOKENS) */
   const void*  W_out;  /* [d, D]  E      Eq. 6                                            */
   const float* W_r;    /* [H, d_h, N_e] f32  router (Alg. 1 REQUIRE; FP32 P:521)          */
   const float* bias;   /* [H, N_e] f32   aux-free load-balancing bias, selection only    */
@@ -103,7 +109,7 @@ typedef struct {
  * dW_r/dW1/dW2 are complete for the local heads (each rank owns all tokens of
  * its heads).  There is no bias gradient (R13).  Any pointer may be NULL to skip. */
 typedef struct {
-  float* dW_in;   /* [D, d]            */
+  float* dW_in;   /* [D, d]  ([2D, d] with MHL_FLAG_ROUTING_TOKENS) */
   float* dW_out;  /* [d, D]            */
   float* dW_r;    /* [H, d_h, N_e]     */
   float* dW1;     /* [H, N_e, d_e, d_h]*/
@@ -201,8 +207,10 @@ MHL_API mhl_status mhl_check_device_status(mhl_plan plan);
 MHL_API uint64_t mhl_launch_count(mhl_plan plan);
 
 /* Bytes this plan has posted to other ranks through the HP all-to-alls since creation
- * (self blocks excluded).  Equals calls * a2a_bytes_per_rank: independent of k and of
- * the routing (P:811-P:812).  With LOOPBACK: summed over the virtual ranks. */
+ * (self blocks excluded).  Independent of k and of the routing (P:811-P:812): per
+ * forward (or backward) a2a_bytes_per_rank for the scatter plus T_loc*H_loc*d_h*el*(G-1)
+ * for the gather (the same without routing tokens).  With LOOPBACK: summed over the
+ * virtual ranks. */
 MHL_API uint64_t mhl_a2a_bytes_posted(mhl_plan plan);
 
 /* Per-step timing with CUDA events recorded on the launching stream around each

@@ -106,6 +106,9 @@ struct Dims {
   int64_t T_loc, T_g, R, Rp;   // Rp: padded sorted-row capacity per head (R + N_e*seg_align)
   int d, N_h, d_h, N_e, k, d_e, G, H, HD, D, el, dtype, rank;
   bool loopback, simt, pair;
+  bool rtok;       // MHL_FLAG_ROUTING_TOKENS (P:1565-P:1570): Xs rows carry [x part | r part]
+  int XW;          // Xs row width per rank: HD, or 2*HD with routing tokens (r part at column HD)
+  int Din;         // W_in rows: D, or 2*D with routing tokens
   int n_rt, max_tiles, max_chunks, seg_align;
   int dw_parts = mhl::kMaxDwParts;   // dW row parts per head (= dW grid), set from the SM count by hp_plan
 };
@@ -123,7 +126,7 @@ struct BwdLayout { size_t send3, dY, dXrep, dg, dS, dS_s, dH, gA, dwr_part, W_rT
 
 SavedLayout saved_layout(const Dims& m) {
   Bump b; SavedLayout L;
-  L.Xs = b.take((size_t)(m.T_g + 1) * m.HD * m.el);   // + one zero row: gather target of padding rows
+  L.Xs = b.take((size_t)(m.T_g + 1) * m.XW * m.el);   // + one zero row: gather target of padding rows
   L.idx = b.take((size_t)m.H * m.R * 4);
   L.gate = b.take((size_t)m.H * m.R * 4);
   L.perm = b.take((size_t)m.H * m.Rp * 4);     // padded sorted rows (cluster.cu)
@@ -147,7 +150,7 @@ SavedLayout saved_layout(const Dims& m) {
 
 FwdLayout fwd_layout(const Dims& m) {
   Bump b; FwdLayout L;
-  L.send1 = b.take(m.G > 1 ? (size_t)m.T_loc * m.D * m.el : 0);
+  L.send1 = b.take(m.G > 1 ? (size_t)m.T_loc * m.G * m.XW * m.el : 0);
   L.Yrep = b.take((size_t)m.H * m.Rp * m.d_h * m.el);
   L.send2 = b.take(m.G > 1 ? (size_t)m.T_g * m.HD * m.el : 0);
   L.recv2 = b.take(m.G > 1 ? (size_t)m.T_loc * m.D * m.el : 0);
@@ -170,9 +173,9 @@ BwdLayout bwd_layout(const Dims& m) {
   L.gA = b.take((size_t)m.H * m.Rp * m.d_e * m.el);
   L.dwr_part = b.take((size_t)m.H * m.n_rt * m.N_e * m.d_h * 4);
   L.W_rT = b.take((size_t)m.H * m.N_e * m.d_h * 4);
-  L.send4 = b.take(m.G > 1 ? (size_t)m.T_g * m.HD * m.el : 0);
-  L.recv4 = b.take(m.G > 1 ? (size_t)m.T_loc * m.D * m.el : 0);
-  L.dXs = b.take((size_t)m.T_loc * m.D * m.el);
+  L.send4 = b.take(m.G > 1 ? (size_t)m.T_g * m.XW * m.el : 0);
+  L.recv4 = b.take(m.G > 1 ? (size_t)m.T_loc * m.G * m.XW * m.el : 0);
+  L.dXs = b.take((size_t)m.T_loc * m.Din * m.el);
   L.dw_part = b.take(m.simt ? 0 : (size_t)m.max_chunks * 2 * m.d_e * m.d_h * 4);
   L.dw_done = b.take((size_t)m.H * m.N_e * 4);
   L.total = b.off;
@@ -206,6 +209,9 @@ mhl_status make_dims(const mhl_config* c, Dims* m) {
   if (m->Rp >= (int64_t)1 << 31) return fail(MHL_ERR_UNSUPPORTED, "T_glob * k + N_e * 256 must be < 2^31");
   m->HD = m->H * m->d_h;
   m->D = m->N_h * m->d_h;
+  m->rtok = (c->flags & MHL_FLAG_ROUTING_TOKENS) != 0;
+  m->XW = m->HD * (m->rtok ? 2 : 1);
+  m->Din = m->D * (m->rtok ? 2 : 1);
   m->dtype = c->dtype;
   m->el = c->dtype == MHL_BF16 ? 2 : 4;
   m->loopback = loop;
@@ -230,7 +236,7 @@ void fill_info(const Dims& m, mhl_plan_info* info) {
   info->head_begin = m.loopback ? 0 : m.rank * m.H;
   info->head_end = m.loopback ? m.N_h : (m.rank + 1) * m.H;
   info->tokens_global = m.T_g;
-  info->a2a_bytes_per_peer = (uint64_t)m.T_loc * m.HD * m.el;
+  info->a2a_bytes_per_peer = (uint64_t)m.T_loc * m.XW * m.el;   // the scatter (x and, with routing tokens, r)
   info->a2a_bytes_per_rank = info->a2a_bytes_per_peer * (uint64_t)(m.G - 1);
   info->saved_bytes = (uint64_t)saved_layout(m).total * vr;
   info->workspace_bytes = (uint64_t)std::max(fwd_layout(m).total, bwd_layout(m).total) * vr;
@@ -343,12 +349,16 @@ inline const char* at(const void* base, size_t off) { return static_cast<const c
 //   recv[v]  [G][blk]   incoming blocks (NCCL mode; loopback copies straight to their destination)
 //   place[v] optional: incoming block src is then copied into columns [src*row_bytes, ...) of the
 //            [rows][pitch] matrix place[v] (F7 -> cat, B2 -> dXs), else recv itself is the target
+//   parts    with routing sub-tokens a B2 block row is [dX part | dR part] (parts = 2): part pi of
+//            source src goes to columns [pi*part_dst + src*row_bytes, ...) of place
 struct Xfer {
   std::vector<const char*> send;
   std::vector<char*> recv, place;
   size_t blk = 0;
   int64_t rows = 0;
   size_t row_bytes = 0, pitch = 0;
+  int parts = 1;
+  size_t part_dst = 0;
 };
 
 template <class Produce, class Tail>
@@ -365,12 +375,14 @@ mhl_status hp_exchange(mhl_plan p, const Xfer& X, cudaStream_t s, Produce produc
       for (int v = 0; v < m.G; ++v) {
         const int q = (v + i) % m.G;
         if (!X.place.empty())
-          mhl::launch_copy_rows(X.send[v] + q * blk, (int64_t)X.row_bytes, X.place[q] + v * X.row_bytes,
-                                (int64_t)X.pitch, X.rows, (int64_t)X.row_bytes, cs);
+          for (int pi = 0; pi < X.parts; ++pi)
+            mhl::launch_copy_rows(X.send[v] + q * blk + pi * X.row_bytes, (int64_t)(X.parts * X.row_bytes),
+                                  X.place[q] + pi * X.part_dst + v * X.row_bytes, (int64_t)X.pitch, X.rows,
+                                  (int64_t)X.row_bytes, cs);
         else
           MHL_CUDA(cudaMemcpyAsync(X.recv[q] + v * blk, X.send[v] + q * blk, blk, cudaMemcpyDeviceToDevice, cs));
         p->a2a_bytes_posted += blk;
-        if (!X.place.empty()) p->launches++;
+        if (!X.place.empty()) p->launches += X.parts;
       }
     } else {
       const int r = m.rank, q = (r + i) % m.G, src = (r - i + m.G) % m.G;
@@ -382,9 +394,11 @@ mhl_status hp_exchange(mhl_plan p, const Xfer& X, cudaStream_t s, Produce produc
       p->a2a_bytes_posted += blk;
       p->launches++;
       if (!X.place.empty()) {
-        mhl::launch_copy_rows(X.recv[0] + src * blk, (int64_t)X.row_bytes, X.place[0] + src * X.row_bytes,
-                              (int64_t)X.pitch, X.rows, (int64_t)X.row_bytes, cs);
-        p->launches++;
+        for (int pi = 0; pi < X.parts; ++pi)
+          mhl::launch_copy_rows(X.recv[0] + src * blk + pi * X.row_bytes, (int64_t)(X.parts * X.row_bytes),
+                                X.place[0] + pi * X.part_dst + src * X.row_bytes, (int64_t)X.pitch, X.rows,
+                                (int64_t)X.row_bytes, cs);
+        p->launches += X.parts;
       }
     }
   }
@@ -443,13 +457,19 @@ mhl_status check_kernels(mhl_plan p) {
 }
 
 // B6 for tokens [t0, t0 + nT): on the tensor-core path K2 already added the router term to each
-// replica row, so B6 is the plain k-row sum (the F6 kernel); the SIMT path adds it here
+// replica row, so B6 is the plain k-row sum (the F6 kernel); the SIMT path adds it here.  With
+// routing sub-tokens (P:1565-P:1570) the router term is the gradient of r, not of x: dX gets the
+// plain sum (out_x) and dR the router term alone (out_r).
 void combine_bwd(const Dims& m, const mhl::Routing& rt, const void* dXrep, const float* dS, const float* W_rT, bool tc,
-                 void* out, int64_t ldo, cudaStream_t s, int64_t t0, int64_t nT) {
-  if (tc)
-    mhl::launch_combine_fwd(m.dtype, rt, dXrep, m.d_h, out, ldo, s, t0, nT);
-  else
-    mhl::launch_combine_bwd(m.dtype, rt, dXrep, dS, W_rT, m.d_h, out, ldo, s, t0, nT);
+                 void* out_x, int64_t ld_x, void* out_r, int64_t ld_r, cudaStream_t s, int64_t t0, int64_t nT) {
+  if (m.rtok) {
+    mhl::launch_combine_fwd(m.dtype, rt, dXrep, m.d_h, out_x, ld_x, s, t0, nT);
+    mhl::launch_combine_bwd(m.dtype, rt, nullptr, dS, W_rT, m.d_h, out_r, ld_r, s, t0, nT);
+  } else if (tc) {
+    mhl::launch_combine_fwd(m.dtype, rt, dXrep, m.d_h, out_x, ld_x, s, t0, nT);
+  } else {
+    mhl::launch_combine_bwd(m.dtype, rt, dXrep, dS, W_rT, m.d_h, out_x, ld_x, s, t0, nT);
+  }
 }
 
 // F3-F6 for one rank's local heads; input recv1 (= saved Xs), output rows into `yout` [T_g][HD]
@@ -459,6 +479,8 @@ mhl_status moe_forward_local(mhl_plan p, const RankPtrs& R, void* yout, cudaStre
   const SavedLayout S = saved_layout(m);
   const FwdLayout F = fwd_layout(m);
   const void* Xs = R.saved + S.Xs;
+  // routing sub-tokens: Xs itself, or its r part at column HD (MHL_FLAG_ROUTING_TOKENS)
+  const void* Xr = R.saved + S.Xs + (m.rtok ? (size_t)m.HD * m.el : 0);
   int32_t* idx = (int32_t*)(R.saved + S.idx);
   float* gate = (float*)(R.saved + S.gate);
   int32_t* perm = (int32_t*)(R.saved + S.perm);
@@ -470,16 +492,16 @@ mhl_status moe_forward_local(mhl_plan p, const RankPtrs& R, void* yout, cudaStre
   {
     MHL_SPAN("F3_router_topk");
     if (!m.simt && mhl::router_sm100_supported(m.d_h, m.N_e)) {
-      if (!mhl::launch_router_sm100(Xs, m.HD, R.W_r, R.bias, m.H, m.T_g, m.d_h, m.N_e, m.k, R.ws + F.planes, idx, gate,
+      if (!mhl::launch_router_sm100(Xr, m.XW, R.W_r, R.bias, m.H, m.T_g, m.d_h, m.N_e, m.k, R.ws + F.planes, idx, gate,
                                     hist, p->dflag, p->num_sms, s))
         return fail(MHL_ERR_CUDA, "router: TMA tensor-map encoding failed");
     } else if (!m.simt && mhl::router_blk_supported(m.d_h, m.N_e, m.k)) {
       mhl::launch_router_split(R.W_r, R.ws + F.planes, m.H, m.d_h, m.N_e, s);
-      if (!mhl::launch_router_blk_sm100(Xs, m.HD, R.ws + F.planes, R.bias, m.H, m.T_g, m.d_h, m.N_e, m.k, idx, gate,
+      if (!mhl::launch_router_blk_sm100(Xr, m.XW, R.ws + F.planes, R.bias, m.H, m.T_g, m.d_h, m.N_e, m.k, idx, gate,
                                         hist, p->dflag, p->num_sms, s))
         return fail(MHL_ERR_CUDA, "router (blocked): TMA tensor-map encoding failed");
     } else {
-      mhl::launch_router_topk(m.dtype, Xs, m.HD, R.W_r, R.bias, m.H, m.T_g, m.d_h, m.N_e, m.k, idx, gate, hist,
+      mhl::launch_router_topk(m.dtype, Xr, m.XW, R.W_r, R.bias, m.H, m.T_g, m.d_h, m.N_e, m.k, idx, gate, hist,
                               p->dflag, s);
     }
   }
@@ -497,14 +519,14 @@ mhl_status moe_forward_local(mhl_plan p, const RankPtrs& R, void* yout, cudaStre
   {
     MHL_SPAN("F5_expert_fwd");
     // the all-zero sub-token row T: target of the padding rows of every expert tile
-    MHL_CUDA(cudaMemsetAsync(R.saved + S.Xs + (size_t)m.T_g * m.HD * m.el, 0, (size_t)m.HD * m.el, s));
+    MHL_CUDA(cudaMemsetAsync(R.saved + S.Xs + (size_t)m.T_g * m.XW * m.el, 0, (size_t)m.XW * m.el, s));
     // CTA-pair (cta_group::2) kernels with MHL_FLAG_PAIR (segments padded to tile pairs)
     if (m.simt || !mhl::expert_fwd_sm100_supported(m.d_h, m.d_e)) {
-      mhl::launch_expert_fwd_simt(m.dtype, rt, Xs, m.HD, R.W1, R.W2, m.d_h, m.d_e, Yrep, s);
+      mhl::launch_expert_fwd_simt(m.dtype, rt, Xs, m.XW, R.W1, R.W2, m.d_h, m.d_e, Yrep, s);
     } else if (m.pair && mhl::expert_fwd_pair_supported(m.d_h, m.d_e) && p->num_sms >= 2) {
-      if (!mhl::launch_expert_fwd_pair_sm100(rt, Xs, m.HD, R.W1, R.W2, m.d_h, m.d_e, Yrep, p->num_sms, s))
+      if (!mhl::launch_expert_fwd_pair_sm100(rt, Xs, m.XW, R.W1, R.W2, m.d_h, m.d_e, Yrep, p->num_sms, s))
         return fail(MHL_ERR_CUDA, "expert_fwd (pair): TMA tensor-map encoding failed");
-    } else if (!mhl::launch_expert_fwd_sm100(rt, Xs, m.HD, R.W1, R.W2, m.d_h, m.d_e, Yrep, p->num_sms, s)) {
+    } else if (!mhl::launch_expert_fwd_sm100(rt, Xs, m.XW, R.W1, R.W2, m.d_h, m.d_e, Yrep, p->num_sms, s)) {
       return fail(MHL_ERR_CUDA, "expert_fwd: TMA tensor-map encoding failed");
     }
   }
@@ -520,11 +542,13 @@ mhl_status moe_forward_local(mhl_plan p, const RankPtrs& R, void* yout, cudaStre
 
 // B5, B3, B6 for one rank's local heads; input dY [T_g][HD], output dXs rows into `dxout` [T_g][HD]
 // (dxout == nullptr: B6 is left to the caller, which runs it per HP destination block)
-mhl_status moe_backward_local(mhl_plan p, const RankPtrs& R, const void* dY, void* dxout, cudaStream_t s) {
+mhl_status moe_backward_local(mhl_plan p, const RankPtrs& R, const void* dY, void* dxout, cudaStream_t s,
+                              void* dxout_r = nullptr) {
   const Dims& m = p->m;
   const SavedLayout S = saved_layout(m);
   const BwdLayout B = bwd_layout(m);
   const void* Xs = R.saved + S.Xs;
+  const void* Xr = R.saved + S.Xs + (m.rtok ? (size_t)m.HD * m.el : 0);   // routing sub-tokens
   const int32_t* idx = (const int32_t*)(R.saved + S.idx);
   const float* gate = (const float*)(R.saved + S.gate);
   const mhl::Routing rt = routing_view(m, R.saved);
@@ -540,48 +564,50 @@ mhl_status moe_backward_local(mhl_plan p, const RankPtrs& R, const void* dY, voi
   {
     MHL_SPAN("B5_expert_bwd_dx");
     if (tc)
-      mhl::launch_expert_bwd_sm100(rt, Xs, m.HD, dY, m.HD, R.W1, R.W2, m.d_h, m.d_e, dXrep, dg, dH, gA, nullptr,
+      mhl::launch_expert_bwd_sm100(rt, Xs, m.XW, dY, m.HD, R.W1, R.W2, m.d_h, m.d_e, dXrep, dg, dH, gA, nullptr,
                                    nullptr, nullptr, nullptr, p->num_sms, s, true, false);
     else
-      mhl::launch_expert_bwd_simt(m.dtype, rt, Xs, m.HD, dY, m.HD, R.W1, R.W2, m.d_h, m.d_e, dXrep, dg, dH, gA, s);
+      mhl::launch_expert_bwd_simt(m.dtype, rt, Xs, m.XW, dY, m.HD, R.W1, R.W2, m.d_h, m.d_e, dXrep, dg, dH, gA, s);
   }
   // B3 (needs only K1's dg) runs before K2, which folds the router term dS W_r^T into dXrep
   float* W_rT = (float*)(R.ws + B.W_rT);
   {
     MHL_SPAN("B3_router_bwd");
     if (!m.simt && m.T_g > 0 && mhl::router_bwd_sm100_supported(m.d_h, m.N_e, m.k)) {
-      if (!mhl::launch_router_bwd_sm100(Xs, m.HD, idx, gate, dg, m.H, m.T_g, m.k, m.d_h, m.N_e, dS,
+      if (!mhl::launch_router_bwd_sm100(Xr, m.XW, idx, gate, dg, m.H, m.T_g, m.k, m.d_h, m.N_e, dS,
                                         (float*)(R.ws + B.dwr_part),
                                         // token chunks per head from the GLOBAL head count, so the
                                         // partial-sum order (and dW_r bits) do not depend on G
-                                        std::min(m.n_rt, std::max(1, p->num_sms / m.N_h)), R.dW_r, s, rt.pos, m.Rp,
-                                        tc ? (float*)(R.ws + B.dS_s) : nullptr))
+                                        std::min(m.n_rt, std::max(1, p->num_sms / m.N_h)), R.dW_r, s))
         return fail(MHL_ERR_CUDA, "router backward: TMA tensor-map encoding failed");
     } else {
-      mhl::launch_router_bwd(m.dtype, Xs, m.HD, idx, gate, dg, m.H, m.T_g, m.k, m.d_h, m.N_e, dS,
+      mhl::launch_router_bwd(m.dtype, Xr, m.XW, idx, gate, dg, m.H, m.T_g, m.k, m.d_h, m.N_e, dS,
                              (float*)(R.ws + B.dwr_part), R.dW_r, s);
-      if (tc) { mhl::launch_sort_ds(rt, dS, (float*)(R.ws + B.dS_s), s); p->launches++; }
     }
+    // dS in clustered-row order for K2's router term: a separate scatter kernel (20 us faster than
+    // scattering from inside the router backward, r1e)
+    if (tc && !m.rtok) { mhl::launch_sort_ds(rt, dS, (float*)(R.ws + B.dS_s), s); p->launches++; }
     mhl::launch_transpose_wr(R.W_r, W_rT, m.H, m.d_h, m.N_e, s);
   }
   if (tc) {
     MHL_SPAN("B5_expert_dx_gemm");
-    if (!mhl::launch_expert_dx_gemm_sm100(rt, R.W1, m.d_h, m.d_e, dH, dXrep, (const float*)(R.ws + B.dS_s), W_rT,
+    if (!mhl::launch_expert_dx_gemm_sm100(rt, R.W1, m.d_h, m.d_e, dH, dXrep,
+                                          m.rtok ? nullptr : (const float*)(R.ws + B.dS_s), W_rT,
                                           p->num_sms, s))
       return fail(MHL_ERR_CUDA, "expert dX GEMM: TMA tensor-map encoding failed");
   }
   if (R.dW1 || R.dW2) {
     MHL_SPAN("B5_expert_bwd_dw");
     if (tc)
-      mhl::launch_expert_bwd_sm100(rt, Xs, m.HD, dY, m.HD, R.W1, R.W2, m.d_h, m.d_e, dXrep, dg, dH, gA,
+      mhl::launch_expert_bwd_sm100(rt, Xs, m.XW, dY, m.HD, R.W1, R.W2, m.d_h, m.d_e, dXrep, dg, dH, gA,
                                    (float*)(R.ws + B.dw_part), (int*)(R.ws + B.dw_done), R.dW1, R.dW2,
                                    p->num_sms, s, false, true);
     else
-      mhl::launch_expert_dw_simt(m.dtype, rt, Xs, m.HD, dY, m.HD, dH, gA, m.d_h, m.d_e, R.dW1, R.dW2, s);
+      mhl::launch_expert_dw_simt(m.dtype, rt, Xs, m.XW, dY, m.HD, dH, gA, m.d_h, m.d_e, R.dW1, R.dW2, s);
   }
   if (dxout) {
     MHL_SPAN("B6_combine_bwd");
-    combine_bwd(m, rt, dXrep, dS, W_rT, tc, dxout, m.HD, s, 0, -1);
+    combine_bwd(m, rt, dXrep, dS, W_rT, tc, dxout, m.Din, dxout_r, m.Din, s, 0, -1);
   }
   // K1 + K2 + dW (+ its in-kernel reduce) + router (2) + transpose + combine on the tensor-core path
   p->launches += (tc ? 7 : (R.dW1 || R.dW2 ? 6 : 5)) - (dxout ? 0 : 1);
@@ -733,12 +759,13 @@ mhl_status mhlmoe_forward(mhl_plan p, const void* x, const mhl_weights* w, void*
   std::vector<RankPtrs> ranks;
   for (int r = 0; r < VR; ++r)
     ranks.push_back(rank_view(p, r, saved, workspace, x, out, nullptr, w, nullptr, topk_idx, gates));
-  const size_t blk = (size_t)m.T_loc * m.HD * m.el;
+  const size_t blk = (size_t)m.T_loc * m.HD * m.el;     // gather block (head outputs)
+  const size_t blk_s = (size_t)m.T_loc * m.XW * m.el;  // scatter block (sub-tokens [+ routing sub-tokens])
   if (m.G == 1) {
     const RankPtrs& R = ranks[0];
     {
-      MHL_SPAN("F1_proj_in");   // F1: Xs = x W_in^T (Eq. 5)
-      MHL_TRY(gemm(false, true, m.T_loc, m.D, m.d, R.x, m.d, w->W_in, m.d, R.saved + S.Xs, m.D, false, 0.0f));
+      MHL_SPAN("F1_proj_in");   // F1: Xs = x W_in^T (Eq. 5; [x | r] parts with routing tokens)
+      MHL_TRY(gemm(false, true, m.T_loc, m.Din, m.d, R.x, m.d, w->W_in, m.d, R.saved + S.Xs, m.Din, false, 0.0f));
     }
     MHL_TRY(moe_forward_local(p, R, R.saved + S.cat, s));   // F3-F6
     MHL_SPAN("F8_proj_out");     // F8: out = cat W_out^T (Eq. 6)
@@ -750,15 +777,19 @@ mhl_status mhlmoe_forward(mhl_plan p, const void* x, const mhl_weights* w, void*
   {
     MHL_SPAN("F1F2_proj_in_a2a");
     Xfer X;
-    X.blk = blk;
+    X.blk = blk_s;
     for (auto& R : ranks) { X.send.push_back(R.ws + F.send1); X.recv.push_back(R.saved + S.Xs); }
     MHL_TRY(hp_exchange(p, X, s, [&](int i) -> mhl_status {
       for (int v = 0; v < VR; ++v) {
         const RankPtrs& R = ranks[v];
         const int rk = rank_of(v), q = (rk + i) % m.G;
-        char* dst = i == 0 ? R.saved + S.Xs + rk * blk : R.ws + F.send1 + q * blk;
+        char* dst = i == 0 ? R.saved + S.Xs + rk * blk_s : R.ws + F.send1 + q * blk_s;
         MHL_TRY(gemm(false, true, m.T_loc, m.HD, m.d, R.x, m.d, at(w->W_in, (size_t)q * m.HD * m.d * m.el), m.d,
-                     dst, m.HD, false, 0.0f));
+                     dst, m.XW, false, 0.0f));
+        if (m.rtok)   // routing sub-tokens of q's heads: W_in rows D + q*HD.., same block
+          MHL_TRY(gemm(false, true, m.T_loc, m.HD, m.d, R.x, m.d,
+                       at(w->W_in, ((size_t)m.D + (size_t)q * m.HD) * m.d * m.el), m.d,
+                       dst + (size_t)m.HD * m.el, m.XW, false, 0.0f));
       }
       return MHL_OK;
     }, [] { return MHL_OK; }));
@@ -820,11 +851,12 @@ mhl_status mhlmoe_backward(mhl_plan p, const void* x, const mhl_weights* w, cons
       if (grads->dW_out)
         MHL_TRY(gemm(true, false, m.d, m.D, m.T_loc, R.dout, m.d, R.saved + S.cat, m.D, grads->dW_out, m.D, true, 0.0f));
     }
-    MHL_TRY(moe_backward_local(p, R, R.ws + B.dY, R.ws + B.dXs, s));   // B5, B3, B6
-    MHL_SPAN("B1_proj_in_bwd");      // B1: dx = dXs W_in, dW_in = dXs^T x
-    MHL_TRY(gemm(false, false, m.T_loc, m.d, m.D, R.ws + B.dXs, m.D, w->W_in, m.d, R.out, m.d, false, 0.0f));
+    MHL_TRY(moe_backward_local(p, R, R.ws + B.dY, R.ws + B.dXs, s,
+                               m.rtok ? R.ws + B.dXs + (size_t)m.D * m.el : nullptr));   // B5, B3, B6
+    MHL_SPAN("B1_proj_in_bwd");      // B1: dx = dXs W_in, dW_in = dXs^T x  (dXs = [dX | dR] with routing tokens)
+    MHL_TRY(gemm(false, false, m.T_loc, m.d, m.Din, R.ws + B.dXs, m.Din, w->W_in, m.d, R.out, m.d, false, 0.0f));
     if (grads->dW_in)
-      MHL_TRY(gemm(true, false, m.D, m.d, m.T_loc, R.ws + B.dXs, m.D, R.x, m.d, grads->dW_in, m.d, true, 0.0f));
+      MHL_TRY(gemm(true, false, m.Din, m.d, m.T_loc, R.ws + B.dXs, m.Din, R.x, m.d, grads->dW_in, m.d, true, 0.0f));
     return check_kernels(p);
   }
   auto rank_of = [&](int v) { return m.loopback ? v : m.rank; };
@@ -859,7 +891,9 @@ mhl_status mhlmoe_backward(mhl_plan p, const void* x, const mhl_weights* w, cons
   {
     MHL_SPAN("B6B2_combine_bwd_a2a");
     Xfer X;
-    X.blk = blk; X.rows = m.T_loc; X.row_bytes = (size_t)m.HD * m.el; X.pitch = (size_t)m.D * m.el;
+    const size_t blk4 = (size_t)m.T_loc * m.XW * m.el;   // [dX | dR] rows with routing tokens
+    X.blk = blk4; X.rows = m.T_loc; X.row_bytes = (size_t)m.HD * m.el; X.pitch = (size_t)m.Din * m.el;
+    X.parts = m.rtok ? 2 : 1; X.part_dst = (size_t)m.D * m.el;
     for (auto& R : ranks) {
       X.send.push_back(R.ws + B.send4); X.recv.push_back(R.ws + B.recv4); X.place.push_back(R.ws + B.dXs);
     }
@@ -868,11 +902,12 @@ mhl_status mhlmoe_backward(mhl_plan p, const void* x, const mhl_weights* w, cons
         const RankPtrs& R = ranks[v];
         const int rk = rank_of(v), q = (rk + i) % m.G;
         const mhl::Routing rt = routing_view(m, R.saved);
-        void* dst = i == 0 ? (void*)(R.ws + B.dXs + rk * X.row_bytes) : (void*)(R.ws + B.send4 + q * blk);
+        char* dst = i == 0 ? R.ws + B.dXs + rk * X.row_bytes : R.ws + B.send4 + q * blk4;
+        char* dst_r = i == 0 ? dst + X.part_dst : dst + X.row_bytes;
         combine_bwd(m, rt, R.ws + B.dXrep, (const float*)(R.ws + B.dS), (const float*)(R.ws + B.W_rT),
-                    !m.simt && mhl::expert_bwd_sm100_supported(m.d_h, m.d_e), dst, i == 0 ? m.D : m.HD, s,
-                    (int64_t)q * m.T_loc, m.T_loc);
-        p->launches++;
+                    !m.simt && mhl::expert_bwd_sm100_supported(m.d_h, m.d_e), dst, i == 0 ? m.Din : m.XW,
+                    dst_r, i == 0 ? m.Din : m.XW, s, (int64_t)q * m.T_loc, m.T_loc);
+        p->launches += m.rtok ? 2 : 1;
       }
       return MHL_OK;
     }, [] { return MHL_OK; }));
@@ -881,9 +916,9 @@ mhl_status mhlmoe_backward(mhl_plan p, const void* x, const mhl_weights* w, cons
   for (int v = 0; v < VR; ++v) {
     MHL_SPAN("B1_proj_in_bwd");
     const RankPtrs& R = ranks[v];
-    MHL_TRY(gemm(false, false, m.T_loc, m.d, m.D, R.ws + B.dXs, m.D, w->W_in, m.d, R.out, m.d, false, 0.0f));
+    MHL_TRY(gemm(false, false, m.T_loc, m.d, m.Din, R.ws + B.dXs, m.Din, w->W_in, m.d, R.out, m.d, false, 0.0f));
     if (grads->dW_in)
-      MHL_TRY(gemm(true, false, m.D, m.d, m.T_loc, R.ws + B.dXs, m.D, R.x, m.d, grads->dW_in, m.d, true,
+      MHL_TRY(gemm(true, false, m.Din, m.d, m.T_loc, R.ws + B.dXs, m.Din, R.x, m.d, grads->dW_in, m.d, true,
                    v == 0 ? 0.0f : 1.0f));
   }
   return check_kernels(p);

@@ -2,6 +2,7 @@
 //
 // F6: y[t][h*d_h + c] = sum_{j=0..k-1} Yrep[h][pos(t,j)][c]          (gates already applied in F5)
 // B6: dXs[t][h*d_h + c] = sum_j dXrep[h][pos(t,j)][c] + sum_j dS[t][j] W_r[h][c][e_j]   (Alg. 2 l.9)
+//     (dXrep == nullptr: the router term alone, the routing sub-token's gradient of P:1565-P:1570)
 // Lane l owns 16-byte column chunks l, l+32, ... of a (token, head) row.  Sums run in fixed j
 // order in fp32 (deterministic), rounded once to the storage type.  Rows are written straight
 // into the all-to-all send buffer (row = global token, column block = local head).
@@ -79,10 +80,10 @@ combine_kernel(const E* __restrict__ rep, const int32_t* __restrict__ pos, const
         uint4 v[KMAX];
 #pragma unroll
         for (int j = 0; j < KMAX; ++j)
-          if (j < k) v[j] = __ldg(reinterpret_cast<const uint4*>(rep + ((size_t)h * Rp + p[j]) * d_h + ch * V));
+          if (j < k && rep) v[j] = __ldg(reinterpret_cast<const uint4*>(rep + ((size_t)h * Rp + p[j]) * d_h + ch * V));
 #pragma unroll
         for (int j = 0; j < KMAX; ++j) {
-          if (j < k) {
+          if (j < k && rep) {
             float f[8];
             unpack(v[j], f);
 #pragma unroll
@@ -93,10 +94,10 @@ combine_kernel(const E* __restrict__ rep, const int32_t* __restrict__ pos, const
         float4 v[KMAX];
 #pragma unroll
         for (int j = 0; j < KMAX; ++j)
-          if (j < k) v[j] = __ldg(reinterpret_cast<const float4*>(rep + ((size_t)h * Rp + p[j]) * d_h + ch * V));
+          if (j < k && rep) v[j] = __ldg(reinterpret_cast<const float4*>(rep + ((size_t)h * Rp + p[j]) * d_h + ch * V));
 #pragma unroll
         for (int j = 0; j < KMAX; ++j)
-          if (j < k) { acc[0] += v[j].x; acc[1] += v[j].y; acc[2] += v[j].z; acc[3] += v[j].w; }
+          if (j < k && rep) { acc[0] += v[j].x; acc[1] += v[j].y; acc[2] += v[j].z; acc[3] += v[j].w; }
       }
       if constexpr (BWD) {
         float racc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};

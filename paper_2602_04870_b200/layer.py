@@ -21,9 +21,10 @@ class MHLatentMoE:
     """
 
     def __init__(self, T_loc, d, N_h, d_h, N_e, k, d_e, dtype="bf16", world_size=1, rank=0, loopback=False,
-                 simt=False, nccl_id=None, device="cuda", pair=False):
+                 simt=False, nccl_id=None, device="cuda", pair=False, routing_tokens=False):
         flags = ((C.MHL_FLAG_LOOPBACK if loopback else 0) | (C.MHL_FLAG_SIMT if simt else 0)
-                 | (C.MHL_FLAG_PAIR if pair else 0))
+                 | (C.MHL_FLAG_PAIR if pair else 0) | (C.MHL_FLAG_ROUTING_TOKENS if routing_tokens else 0))
+        self.routing_tokens = routing_tokens
         self.cfg = C.make_config(T_loc, d, N_h, d_h, N_e, k, d_e, dtype, world_size, rank, flags)
         self.plan = C.hp_plan(self.cfg, nccl_id)
         self.info = self.plan.info
@@ -41,7 +42,8 @@ class MHLatentMoE:
     def alloc_grads(self):
         f32 = dict(dtype=torch.float32, device=self.device)
         D = self.N_h * self.d_h
-        return dict(dW_in=torch.empty(D, self.d, **f32), dW_out=torch.empty(self.d, D, **f32),
+        D_in = D * (2 if self.routing_tokens else 1)   # [2D, d] with separate routing sub-tokens
+        return dict(dW_in=torch.empty(D_in, self.d, **f32), dW_out=torch.empty(self.d, D, **f32),
                     dW_r=torch.empty(self.H_loc, self.d_h, self.N_e, **f32),
                     dW1=torch.empty(self.H_loc, self.N_e, self.d_e, self.d_h, **f32),
                     dW2=torch.empty(self.H_loc, self.N_e, self.d_e, self.d_h, **f32))

@@ -39,6 +39,14 @@ def boundary_flip_budget(Xs_pre: np.ndarray, W_r_h: np.ndarray, mode: str) -> np
     return np.max((amb * ulp) @ np.abs(W_r_h), axis=1)
 
 
+def routing_slice(P, h):
+    """Columns of Xs that head h routes on: its sub-token, or with separate routing sub-tokens
+    (W_in [2D, d], P:1565-P:1570) the r part at column D + h*d_h."""
+    N_h, d_h = P["W_r"].shape[0], P["W_r"].shape[1]
+    off = N_h * d_h if O.has_routing_tokens(P) else 0
+    return slice(off + h * d_h, off + (h + 1) * d_h)
+
+
 def check_routing(P, C, gpu_idx, k, margin_thr=MARGIN):
     """R8 (+R22): a sub-token is *clean* if its oracle margin minus twice its Xs
     boundary-flip budget is >= 1e-3.  On clean sub-tokens the GPU's index SET must equal
@@ -50,7 +58,7 @@ def check_routing(P, C, gpu_idx, k, margin_thr=MARGIN):
     forced = {}
     n_clean = n_excl = 0
     for h in range(N_h):
-        sl = slice(h * d_h, (h + 1) * d_h)
+        sl = routing_slice(P, h)
         X_h = C.Xs[:, sl]
         I, _S_sel, margin, _S, K = O.route_topk(X_h, P["W_r"][h], P["b"][h], k)
         budget = boundary_flip_budget(C.Xs_pre[:, sl], P["W_r"][h], C.mode)

@@ -9,7 +9,7 @@ torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
 
 import oracle as O  # noqa: E402
-from parity_util import GATE_TOL, TOL, boundary_flip_budget, check_routing, rel_err  # noqa: E402
+from parity_util import GATE_TOL, TOL, boundary_flip_budget, check_routing, rel_err, routing_slice  # noqa: E402
 from workloads import PRESETS, LayerConfig, make_problem  # noqa: E402
 
 
@@ -23,7 +23,7 @@ def _run_gpu(cfg: LayerConfig, W, x, dout, G=1, simt=False, backward=True, pair=
     td = torch_dtype(cfg.dtype)
     loop = G > 1
     L = MHLatentMoE(cfg.T // G, cfg.d, cfg.N_h, cfg.d_h, cfg.N_e, cfg.k, cfg.d_e, cfg.dtype, world_size=G,
-                    loopback=loop, simt=simt, pair=pair)
+                    loopback=loop, simt=simt, pair=pair, routing_tokens=cfg.routing_tokens)
     Wd = weights_to_device(W, cfg.dtype)
     xd = torch.from_numpy(x).to("cuda", td)
     out, idx, gates = L.forward(xd, Wd, want_routing=True)
@@ -51,7 +51,7 @@ def _compare(cfg, W, x, dout, g, backward=True):
     for h in range(cfg.N_h):
         # gates: fp32 softmax of fp32 scores, |dg| <= 1e-5 plus the Lipschitz bound (1/2 per
         # unit score change) of the Xs boundary-flip budget (R22; zero in fp32 mode)
-        sl = slice(h * cfg.d_h, (h + 1) * cfg.d_h)
+        sl = routing_slice(P, h)
         budget = boundary_flip_budget(C.Xs_pre[:, sl], P["W_r"][h], mode)
         err = np.abs(g["gates"][h] - C.g[h])
         assert np.all(err <= GATE_TOL + 0.5 * budget[:, None]), f"gates head {h}: {err.max():.2e}"
@@ -299,3 +299,33 @@ def test_update_bias_matches_oracle(G):
         load = O.expert_loads(idx[h], cfg.N_e)
         want = O.update_bias(b0[h].cpu().numpy(), load, 1e-3)
         np.testing.assert_array_equal(got[h], want)
+
+
+@pytest.mark.parametrize("simt,G", [(False, 1), (True, 1), (False, 2)])
+def test_routing_tokens_match_oracle(simt, G):
+    """Separate routing sub-tokens (MHL_FLAG_ROUTING_TOKENS, P:1565-P:1570): the router runs on the r
+    part of each projected token, the experts on the x part; dX and dR both reach dx through
+    W_in [2D, d].  Against the oracle on the tensor-core and SIMT paths, and under loopback HP
+    (G = 2) where the scatter carries twice the bytes of the gather."""
+    _need_gpu()
+    from paper_2602_04870_b200 import mhlmoe as C
+    cfg = LayerConfig("rtok", T=1000, d=256, N_h=2, d_h=128, N_e=16, k=4, d_e=64, dtype="bf16", routing_tokens=True)
+    W, x, dout = make_problem(cfg, 15, "conf")
+    assert W["W_in"].shape == (2 * cfg.D, cfg.d)
+    g = _run_gpu(cfg, W, x, dout, G=G, simt=simt)
+    _compare(cfg, W, x, dout, g)
+    if G == 1 and not simt:
+        # the bits must not depend on G (HP carries r next to x, R12)
+        g2 = _run_gpu(cfg, W, x, dout, G=2)
+        for key in ("out", "dx", "dW_r", "dW1", "dW2", "idx"):
+            np.testing.assert_array_equal(g2[key], g[key], err_msg=key)
+
+
+def test_routing_tokens_scatter_bytes_double():
+    _need_gpu()
+    from paper_2602_04870_b200 import mhlmoe as C
+    from paper_2602_04870_b200.layer import MHLatentMoE
+    base = dict(T_loc=512, d=256, N_h=4, d_h=64, N_e=8, k=2, d_e=64, dtype="bf16", world_size=2, loopback=True)
+    info0 = MHLatentMoE(**base).info
+    info1 = MHLatentMoE(**base, routing_tokens=True).info
+    assert info1["a2a_bytes_per_peer"] == 2 * info0["a2a_bytes_per_peer"]
