@@ -251,7 +251,7 @@ def main():
         nccl_id = obj[0]
 
     L = MHLatentMoE(T_loc, cfg.d, cfg.N_h, cfg.d_h, cfg.N_e, cfg.k, cfg.d_e, cfg.dtype, world_size=G, rank=rank,
-                    simt=args.simt, nccl_id=nccl_id, device=dev)
+                    simt=args.simt, nccl_id=nccl_id, device=dev, routing_tokens=cfg.routing_tokens)
     td = torch_dtype(cfg.dtype)
     W = make_weights(cfg, 0, "paper")
     Wd = weights_to_device(W, cfg.dtype, dev, heads=(L.info["head_begin"], L.info["head_end"]))

@@ -59,6 +59,8 @@ PRESETS = {
 }
 for _k in (2, 4, 16):
     PRESETS[f"paper_k{_k}"] = PRESETS["paper"].replace(name=f"paper_k{_k}", k=_k)
+# separate routing sub-tokens (ablation P:1565-P:1570), supplementary: W_in [2D, d], the HP scatter doubles
+PRESETS["paper_rtok"] = PRESETS["paper"].replace(name="paper_rtok", routing_tokens=True)
 # paper's own Table-5 shape (P:2070-P:2080), supplementary (multi-block online top-k, N_e > 256)
 PRESETS["table5"] = LayerConfig("table5", T=16384, d=1024, N_h=8, d_h=128, N_e=768, k=4, d_e=256, dtype="bf16")
 
