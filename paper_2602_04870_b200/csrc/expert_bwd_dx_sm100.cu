@@ -92,27 +92,36 @@ template <int DH, int DE>
 struct HL {
   static constexpr int WB = DE * DH * 2;
   static constexpr int BOXES = DE / 64;                    // 64-column output boxes per row
+  // H and dA' accumulators (DE columns each) double-buffered when they fit twice in TMEM
+  static constexpr int NBUF = 4 * DE <= 512 ? 2 : 1;
+  // With double-buffered accumulators the 16 epilogue warps form two groups of 8 that take
+  // alternate tiles (group g = buffer g): one group's MUFU-bound GELU math overlaps the other's
+  // stores instead of every warp doing math, then stores, in lock step.  That epilogue stores
+  // dH/gA straight from registers; giving its smem staging to the gather ring (6 stages instead
+  // of 4) measured SLOWER (K1 1.10 -> 1.50 ms, r1e), so the layout keeps the 4-stage ring.
+  static constexpr bool GROUPED = NBUF == 2 && kEpiWarps == 16;
   static constexpr int STGB = 4 * BOXES * 4096;             // dH/gA staging: [quadrant][box] 32 x 64 bf16
   static constexpr int W1 = 0, W2 = WB, STG = 2 * WB, RING = STG + STGB;
   static constexpr int CTRL_MAX = 3 * 1024;
   static constexpr int S_RAW = (kMaxSmem - RING - CTRL_MAX) / kChunk;
-  // producer warps and warp roles.  With a >= 4-stage ring: 8 warps in 4 pairs, a pair filling a
-  // chunk (each warp 64 of its 128 rows): more warps issuing gathers raise the SM's gather rate
+  // producer warps and warp roles.  With a >= 4-stage ring: 8 warps, WPC of them filling each
+  // chunk (128/WPC rows each): more warps issuing gathers raise the SM's gather rate
   // (tools/ring_probe.cu mech 6: 5.8 -> 8.9 TB/s for L2-resident rows).  Otherwise (d_e = 256:
   // 2-3 stages) 2 warps, each filling whole chunks.
   static constexpr bool SPLIT = S_RAW >= 4 && MHL_K1_PW == 8;
   static constexpr int PW = S_RAW >= 4 ? MHL_K1_PW : 2;
-  static constexpr int OWNERS = SPLIT ? PW / 2 : PW;        // chunk owners (warp pairs or warps)
+  static constexpr int WPC = SPLIT ? 2 : 1;                 // warps per chunk
+  static constexpr int OWNERS = PW / WPC;                   // chunk owners (warp pairs or warps)
   // warps [0, PW) producers, [PW, PW + 16) epilogue, PW + 16 the MMA issuer.  With 8 producers
   // the roles are warpgroup-aligned, so producers hand registers to the epilogue (setmaxnreg).
   static constexpr int EPI_WARP0 = PW, MMA_WARP = PW + kEpiWarps, THREADS = (PW + 1 + kEpiWarps) * 32;
   static constexpr bool REGS = PW == 8;
   static constexpr int PROD_REGS = 40, EPI_REGS = 88;   // launch cap 72: 8*32*(72-40) >= 16*32*(88-72)
   // a multiple of OWNERS: chunk c -> stage c % S, owner c % OWNERS, so every stage is only ever
-  // refilled by the owner that filled it before (its phase parity can never alias)
+  // refilled by the owner that filled it before.  (S >= OWNERS alone would keep the EMPTY parity
+  // exact too — the owner's previous chunk waited for the in-order consumption of chunk
+  // c - OWNERS - S >= c - 2S — but the 6-stage ring it allows measured slower, see above.)
   static constexpr int S = (S_RAW > 12 ? 12 : S_RAW) / OWNERS * OWNERS;
-  // H and dA' accumulators (DE columns each) double-buffered when they fit twice in TMEM
-  static constexpr int NBUF = 4 * DE <= 512 ? 2 : 1;
   static constexpr int CTRL = RING + S * kChunk;
   static constexpr int B_FULL = CTRL, B_EMPTY = B_FULL + 8 * S;
   static constexpr int B_W1F = B_EMPTY + 8 * S, B_W1E = B_W1F + 8, B_W2F = B_W1E + 8, B_W2E = B_W2F + 8;
@@ -150,7 +159,10 @@ expert_bwd_h_kernel(const __grid_constant__ CUtensorMap w1map, const __grid_cons
   if (tid == 0) {
     for (int i = 0; i < S; ++i) { mbar_init(bar(L::B_FULL + 8 * i), 1); mbar_init(bar(L::B_EMPTY + 8 * i), 1); }
     mbar_init(bar(L::B_W1F), 1); mbar_init(bar(L::B_W1E), 1); mbar_init(bar(L::B_W2F), 1); mbar_init(bar(L::B_W2E), 1);
-    for (int b = 0; b < 2; ++b) { mbar_init(bar(L::B_HDFULL + 8 * b), 1); mbar_init(bar(L::B_HDFREE + 8 * b), kEpiThreads); }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(bar(L::B_HDFULL + 8 * b), 1);
+      mbar_init(bar(L::B_HDFREE + 8 * b), L::GROUPED ? kEpiThreads / 2 : kEpiThreads);
+    }
     fence_mbar_init();
     tma_prefetch_desc(&w1map); tma_prefetch_desc(&w2map); tma_prefetch_desc(&xmap); tma_prefetch_desc(&ymap);
     tma_prefetch_desc(&hsmap); tma_prefetch_desc(&asmap);
@@ -179,12 +191,12 @@ expert_bwd_h_kernel(const __grid_constant__ CUtensorMap w1map, const __grid_cons
     Ph w1e, w2e;
     int cnt = 0;                       // chunks of this CTA's stream so far
     const uint64_t pol_keep = (dbg & 16) ? l2_evict_normal() : l2_evict_last();   // rows reused k times per head
-    // SPLIT: warp pair pw/2 owns the chunk, this warp its rows hrow..hrow+63 (lanes 0-15, 4 rows each)
-    constexpr int OWN = L::OWNERS;
-    const int owner = L::SPLIT ? pw >> 1 : pw;
-    const int lrow = L::SPLIT ? (pw & 1) * 64 + 4 * (lane & 15) : 4 * lane;
-    const bool issues = !L::SPLIT || lane < 16;
-    const bool tx_lead = lane == 0 && (!L::SPLIT || (pw & 1) == 0);
+    // owner pw/WPC fills the chunk, this warp its rows lrow.. (lanes 0..LPW-1, 4 rows each)
+    constexpr int OWN = L::OWNERS, WPC = L::WPC, LPW = 32 / WPC;   // lanes issuing per warp
+    const int owner = pw / WPC;
+    const int lrow = (pw % WPC) * (BM / WPC) + 4 * (lane % LPW);
+    const bool issues = lane < LPW;
+    const bool tx_lead = lane == 0 && pw % WPC == 0;
     int nx[4] = {0, 0, 0, 0};          // token ids of the next tile's rows lrow..lrow+3
     auto load_tok = [&](int ti) {
       if (ti < 0) return;
@@ -266,6 +278,86 @@ expert_bwd_h_kernel(const __grid_constant__ CUtensorMap w1map, const __grid_cons
     }
   } else {
     if constexpr (L::REGS) asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(L::EPI_REGS));
+    if constexpr (L::GROUPED) {
+      // ============================================================ epilogue: two groups of 8 warps
+      // group grp takes tiles i = grp, grp + 2, ... (TMEM buffer grp); in a group, warp -> (lane
+      // quadrant q, column half hc): one row and DE/2 columns per thread, 16 at a time: TMEM ->
+      // gelu/gelu' -> bf16 -> dH, gA straight to global (32-byte st.global.v8 per lane, L2
+      // evict-first; every 128-byte row segment is written whole by one thread).  dg keeps the
+      // summation order of the single-group epilogue (32-column partials, added in column order).
+      constexpr int NC = DE / 2;
+      static_assert(NC % 32 == 0, "grouped K1 epilogue: d_e = 64 or 128");
+      const int ew = warp - kEpiWarp0, grp = ew >> 3, q = warp & 3, hc = (ew >> 2) & 1;
+      const int row = q * 32 + lane;
+      const uint32_t lane_off = (uint32_t)(q * 32) << 16;
+      const int bar_dg = 2 + grp * 4 + q;                   // the two warps of (group, quadrant)
+      const uint64_t pol_out = l2_evict_first();
+      float* s_x = s_dg + grp * 2 * BM;                     // [parity][BM]: s0 + s1 of each row
+      Ph hd;
+      float g_n = 0.f;
+      int rep_n = -1;
+      Tile tl_n{};
+      auto fetch = [&](int t) {
+        if (t < 0) return;
+        tl_n = tiles[t];
+        const size_t gr = (size_t)tl_n.head * Rp + tl_n.row0 + row;
+        g_n = __ldg(rt.gate_s + gr);
+        rep_n = __ldg(rt.perm + gr);
+      };
+      fetch(sc.at(grp));
+      for (int i = grp;; i += 2) {
+        const int ti = sc.at(i);
+        if (ti < 0) break;
+        const int b = grp;
+        const Tile tl = tl_n;
+        const float g = g_n;
+        const int rep = rep_n;
+        fetch(sc.at(i + 2));
+        const size_t grow = (size_t)tl.head * Rp + tl.row0 + row;
+        uint8_t* dh_row = dH_out + grow * (DE * 2) + hc * NC * 2;
+        uint8_t* ga_row = gA_out + grow * (DE * 2) + hc * NC * 2;
+        mbar_wait_warp(bar(L::B_HDFULL + 8 * b), hd.flip());
+        if (tid == kEpiWarp0 * 32) trace_ev(trc, 50, i);
+        tc_fence_after();
+        float sp[2] = {0.f, 0.f};                           // this thread's two DE/4-column dg partials
+#pragma unroll
+        for (int c = 0; c < NC; c += 16) {
+          uint32_t hv[16], dv[16], wh[8], wa[8];
+          const uint32_t col = lane_off + hc * NC + c;
+          tmem_ld16(tmem + 2 * DE * b + col, hv);
+          tmem_ld16(tmem + 2 * DE * b + DE + col, dv);
+          tmem_ld_wait();
+          if (c + 16 >= NC) {
+            tc_fence_before();
+            mbar_arrive(bar(L::B_HDFREE + 8 * b));
+          }
+          float dgp = sp[c / (NC / 2)];
+#pragma unroll
+          for (int u = 0; u < 16; u += 2) {
+            const float2 h2 = make_float2(__uint_as_float(hv[u]), __uint_as_float(hv[u + 1]));
+            const float2 d2 = make_float2(__uint_as_float(dv[u]), __uint_as_float(dv[u + 1]));
+            float2 gp;
+            const float2 a = gelu2(h2, &gp);
+            dgp = fmaf(a.x, d2.x, dgp);
+            dgp = fmaf(a.y, d2.y, dgp);
+            const float2 dh = __fmul2_rn(__fmul2_rn(d2, gp), make_float2(g, g));
+            const float2 ga = __fmul2_rn(a, make_float2(g, g));
+            wh[u / 2] = pack_bf16x2(dh.x, dh.y);
+            wa[u / 2] = pack_bf16x2(ga.x, ga.y);
+          }
+          sp[c / (NC / 2)] = dgp;
+          st_global_v8_hint(dh_row + c * 2, wh[0], wh[1], wh[2], wh[3], wh[4], wh[5], wh[6], wh[7], pol_out);
+          st_global_v8_hint(ga_row + c * 2, wa[0], wa[1], wa[2], wa[3], wa[4], wa[5], wa[6], wa[7], pol_out);
+        }
+        if (tid == kEpiWarp0 * 32) trace_ev(trc, 52, i);
+        // dg = ((s0 + s1) + s2) + s3 over the four DE/4-column partials, as the single-group epilogue
+        float* sx = s_x + ((i >> 1) & 1) * BM;              // parity slot: no second barrier needed
+        if (hc == 0) sx[row] = sp[0] + sp[1];
+        named_bar_sync(bar_dg, 64);
+        if (hc == 1 && rep >= 0) dg[(size_t)tl.head * R + rep] = (sx[row] + sp[0]) + sp[1];
+        if (tid == kEpiWarp0 * 32) trace_ev(trc, 55, i);
+      }
+    } else {
     // ================================================================ epilogue (kEpiWarps warps)
     // warp -> (lane quadrant q, column group cg); each thread owns one row and NC columns of H/dA'
     // (TMEM -> gelu/gelu' -> bf16).  dH and gA leave through smem and TMA bulk stores: the warps of
@@ -390,6 +482,7 @@ expert_bwd_h_kernel(const __grid_constant__ CUtensorMap w1map, const __grid_cons
       if (tid == kEpiWarp0 * 32) trace_ev(trc, 55, i);
     }
     if (leader) bulk_wait_all();
+    }
   }
   tc_fence_before();
   __syncthreads();
