@@ -46,12 +46,24 @@ constexpr int kEpiThreads = 256;
 constexpr int kXChunk = BM * 128;    // one 64-column K-chunk of the gathered X tile (16 KB)
 constexpr int kYStage = BM * 128;    // one 64-column block of the Y tile (16 KB)
 
+// Y store path: 0 = smem staging + TMA bulk stores, 2 = straight from registers (32-byte
+// st.global.v8 per lane, no staging smem, so the X ring can take its 32 KB).  X ring depth cap.
+#ifndef MHL_F5_YSTORE
+#define MHL_F5_YSTORE 0
+#endif
+#ifndef MHL_F5_XS
+#define MHL_F5_XS 4
+#endif
+
 template <int DH, int DE>
 struct FwdL {
   static constexpr int WB = DE * DH * 2;
-  static constexpr int W1 = 0, W2 = WB, YS = 2 * WB, X = YS + 2 * kYStage;
+  static constexpr bool YDIRECT = MHL_F5_YSTORE == 2;
+  static constexpr int W1 = 0, W2 = WB, YS = 2 * WB, X = YS + (YDIRECT ? 0 : 2 * kYStage);
   static constexpr int XS_RAW = (224 * 1024 - X) / kXChunk;
-  static constexpr int XS = (XS_RAW > 12 ? 12 : XS_RAW) / kOwners * kOwners;   // X ring stages
+  // chunk c -> stage c % XS, pair c % kOwners; XS >= kOwners keeps the EMPTY parity exact (a
+  // pair's previous chunk waited for the in-order consumption of chunk c - kOwners - XS >= c - 2 XS)
+  static constexpr int XS = XS_RAW > MHL_F5_XS ? MHL_F5_XS : XS_RAW;   // X ring stages
   static_assert(XS >= kOwners, "X ring too small");
   static constexpr int CTRL = X + XS * kXChunk;
   static constexpr int B_XFULL = CTRL, B_XEMPTY = B_XFULL + 8 * XS;
@@ -262,6 +274,28 @@ expert_fwd_sm100_kernel(const __grid_constant__ CUtensorMap w1map, const __grid_
       // 64-column blocks: TMEM -> regs -> bf16 -> smem stage (SW128) -> TMA bulk store.  The two
       // warps of a lane quadrant own a 32-row slab and synchronise only with each other.
       const bool leader = (half == 0 && lane == 0);
+      if constexpr (L::YDIRECT) {
+        // this thread's row, 32 columns per block: 2 x 32-byte stores (whole sectors), evict-first
+        uint8_t* yrow = yout + ((size_t)tl.head * rt.Rp + tl.row0 + row) * (DH * 2) + half * 64;
+        const uint64_t pol = l2_evict_first();
+#pragma unroll 1
+        for (int cb = 0; cb < DH / 64; ++cb) {
+          uint32_t v[32];
+          tmem_ld32(tmem + L::T_Y + lane_off + cb * 64 + half * 32, v);
+          tmem_ld_wait();
+          if (cb == DH / 64 - 1) {
+            tc_fence_before();
+            mbar_arrive(bar(L::B_YEMPTY));
+            if (et == 0) trace_ev(g_trace_fwd, 24, j);
+          }
+          uint32_t w[16];
+#pragma unroll
+          for (int u = 0; u < 16; ++u) w[u] = pack_bf16x2(__uint_as_float(v[2 * u]), __uint_as_float(v[2 * u + 1]));
+          st_global_v8_hint(yrow + cb * 128, w[0], w[1], w[2], w[3], w[4], w[5], w[6], w[7], pol);
+          st_global_v8_hint(yrow + cb * 128 + 32, w[8], w[9], w[10], w[11], w[12], w[13], w[14], w[15], pol);
+        }
+        return;
+      }
 #pragma unroll 1
       for (int cb = 0; cb < DH / 64; ++cb, ++ys) {
         const int st = ys & 1;
