@@ -151,7 +151,8 @@ offsets_kernel(const int32_t* __restrict__ counts, int32_t* __restrict__ off, in
 // chunk is a part's intersection with one expert segment.  CTA b of the dW kernel takes part b of
 // every head, so every CTA gets the same number of rows; the chunk list is in (head, part,
 // expert) = (head, expert, row) order, so each expert's chunks are consecutive ([cbase, +ccount)),
-// and its partials are summed in that order (deterministic, problem-derived boundaries).
+// and its partials are summed in that order (deterministic, problem-derived boundaries).  Chunk
+// ids are per-head blocks of P + N_e (the list has gaps between heads).
 __device__ __forceinline__ int part_lo(int p, int P, int Rh) {
   return p >= P ? Rh : (int)(((int64_t)p * Rh / P) & ~(int64_t)(kDwStep - 1));
 }
@@ -160,19 +161,20 @@ __global__ void __launch_bounds__(1024)
 dw_parts_kernel(const int32_t* __restrict__ off, int H, int N_e, int P, Tile* __restrict__ chunks, int max_chunks,
                 int32_t* __restrict__ nchunks, int32_t* __restrict__ cbase, int32_t* __restrict__ ccount,
                 int32_t* __restrict__ pbase, int32_t* __restrict__ pcount) {
+  // one CTA per head; head h's chunks live at [h*(P+N_e), ...) (a part adds one chunk per expert
+  // segment it touches: at most P + N_e per head), so the heads need no cross-head scan
   __shared__ int s_warp[64];
   __shared__ int s_tot;
-  for (int i = threadIdx.x; i < H * N_e; i += blockDim.x) { ccount[i] = 0; cbase[i] = 0; }
+  const int h = blockIdx.x;
+  const int32_t* o = off + (size_t)h * (N_e + 1);
+  const int Rh = o[N_e];
+  for (int e = threadIdx.x; e < N_e; e += blockDim.x) { ccount[(size_t)h * N_e + e] = 0; cbase[(size_t)h * N_e + e] = 0; }
   __syncthreads();
-  int carry = 0;
-  for (int base = 0; base < H * P; base += 1024) {
-    const int i = base + threadIdx.x;
-    int cnt = 0, lo = 0, hi = 0, e0 = 0, h = 0, p = 0;
-    const int32_t* o = off;
-    if (i < H * P) {
-      h = i / P; p = i % P;
-      o = off + (size_t)h * (N_e + 1);
-      const int Rh = o[N_e];
+  int carry = h * (P + N_e);
+  for (int base = 0; base < P; base += 1024) {
+    const int p = base + threadIdx.x;
+    int cnt = 0, lo = 0, hi = 0, e0 = 0;
+    if (p < P) {
       lo = part_lo(p, P, Rh); hi = part_lo(p + 1, P, Rh);
       if (lo < hi) {
         int a = 0, b = N_e;                  // e0 = last expert with o[e] <= lo (its segment holds lo)
@@ -184,9 +186,9 @@ dw_parts_kernel(const int32_t* __restrict__ off, int H, int N_e, int P, Tile* __
     const int ex = block_exclusive_scan_1024(cnt, s_warp, &s_tot);
     const int tot = s_tot;
     __syncthreads();
-    if (i < H * P) {
+    if (p < P) {
       const int cb = carry + ex;
-      pbase[i] = cb; pcount[i] = cnt;
+      pbase[(size_t)h * P + p] = cb; pcount[(size_t)h * P + p] = cnt;
       int j = 0;
       for (int e = e0; cnt > 0 && e < N_e && o[e] < hi; ++e) {
         if (o[e + 1] <= o[e]) continue;
@@ -198,7 +200,6 @@ dw_parts_kernel(const int32_t* __restrict__ off, int H, int N_e, int P, Tile* __
         }
         if (r0 == o[e]) {                    // the expert's first chunk: count its parts
           int n = 1;
-          const int Rh = o[N_e];
           for (int pp = p + 1; pp < P && part_lo(pp, P, Rh) < o[e + 1]; ++pp)
             n += part_lo(pp, P, Rh) < part_lo(pp + 1, P, Rh);
           cbase[(size_t)h * N_e + e] = ci;
@@ -208,7 +209,7 @@ dw_parts_kernel(const int32_t* __restrict__ off, int H, int N_e, int P, Tile* __
     }
     carry += tot;
   }
-  if (threadIdx.x == 0) *nchunks = min(carry, max_chunks);
+  if (h == 0 && threadIdx.x == 0) *nchunks = min(H * (P + N_e), max_chunks);   // index bound
 }
 
 // (2b) one warp per (h, e): its tiles (at the (h, part, e) positions), its dW chunks and the
@@ -330,7 +331,7 @@ void launch_cluster(int H, int64_t T, int k, int N_e, const int32_t* idx, const 
   // tile bases [H][kTileParts][N_e] live in the (otherwise unused here) tail of tilepref's scratch
   int32_t* tbase = tilepref + (size_t)H * n_rt * N_e;
   offsets_kernel<<<H, 1024, 0, s>>>(counts, off, tbase, ntiles, H, N_e, max_tiles, seg_align);
-  dw_parts_kernel<<<1, 1024, 0, s>>>(off, H, N_e, dw_parts, chunks, max_chunks, nchunks, cbase, ccount, pbase, pcount);
+  dw_parts_kernel<<<H, 1024, 0, s>>>(off, H, N_e, dw_parts, chunks, max_chunks, nchunks, cbase, ccount, pbase, pcount);
   tiles_kernel<<<(H * N_e + 7) / 8, 256, 0, s>>>(counts, off, tbase, tiles, max_tiles, H, N_e, Rp, perm, tok_s,
                                                  gate_s, (int)T, seg_align);
   scatter_kernel<<<dim3(n_rt, H), kScatterWarps * 32, sizeof(int) * kScatterWarps * N_e, s>>>(
