@@ -61,6 +61,8 @@ typedef enum { MHL_F32 = 0, MHL_BF16 = 1 } mhl_dtype;
                                  head i routes on r_ti and runs its experts on x_ti.  The HP
                                  scatter (and its backward mirror) carries both: twice the bytes
                                  (P:1570); dW_in is [2D, d]. */
+#define MHL_FLAG_FUSED_COMBINE 16u  /* G = 1, bf16: run the forward combine (F6) inside the expert
+                                 kernel, window by window (NEXT-1 experiment; same bits, opt-in) */
 
 /* Layer + HP configuration (the paper's problem statement: P:496). */
 typedef struct {

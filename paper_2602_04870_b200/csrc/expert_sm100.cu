@@ -40,7 +40,8 @@ constexpr int kProdWarps = 8;         // warps 0-7: producers, in 4 pairs (a pai
 constexpr int kOwners = kProdWarps / 2;
 constexpr int kEpiWarp0 = 8;          // warps 8-15: epilogue
 constexpr int kMmaWarp = 16;          // warp 16: MMA issuer + TMEM owner
-constexpr int kThreads = 17 * 32;
+constexpr int kCombWarp0 = 17;        // warps 17-19: fused combine (FwdCombine), idle without it
+constexpr int kThreads = 20 * 32;
 constexpr int kProdRegs = 40, kEpiRegs = 152;   // launch cap 96: 8*32*(96-40) >= 8*32*(152-96)
 constexpr int kEpiThreads = 256;
 constexpr int kXChunk = BM * 128;    // one 64-column K-chunk of the gathered X tile (16 KB)
@@ -54,6 +55,7 @@ constexpr int kYStage = BM * 128;    // one 64-column block of the Y tile (16 KB
 #ifndef MHL_F5_XS
 #define MHL_F5_XS 4
 #endif
+#define L_YDIRECT (MHL_F5_YSTORE == 2)
 
 template <int DH, int DE>
 struct FwdL {
@@ -99,7 +101,7 @@ template <int DH, int DE>
 __global__ void __launch_bounds__(kThreads, 1)
 expert_fwd_sm100_kernel(const __grid_constant__ CUtensorMap w1map, const __grid_constant__ CUtensorMap w2map,
                         const __grid_constant__ CUtensorMap ymap, const __grid_constant__ CUtensorMap xmap,
-                        Routing rt, uint8_t* __restrict__ yout, int lsu) {
+                        Routing rt, uint8_t* __restrict__ yout, int lsu, FwdCombine fc) {
   using L = FwdL<DH, DE>;
   constexpr int XS = L::XS, KB1 = DH / 64;
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -256,7 +258,7 @@ expert_fwd_sm100_kernel(const __grid_constant__ CUtensorMap w1map, const __grid_
       }
       if (i >= 1) gemm2(i - 1);
     }
-  } else {
+  } else if (warp >= kEpiWarp0 && warp < kMmaWarp) {
     asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kEpiRegs));
     // ================================================================ epilogue (8 warps)
     const int q = warp & 3, half = (warp - kEpiWarp0) >> 2;   // lane quadrant, column half
@@ -265,6 +267,12 @@ expert_fwd_sm100_kernel(const __grid_constant__ CUtensorMap w1map, const __grid_
     const uint32_t lane_off = (uint32_t)(q * 32) << 16;
     Ph hf, gd[2];
     int ys = 0;   // running count of Y blocks stored (selects the smem stage)
+    auto signal = [&](int t) {
+      if (t < 0) return;
+      asm volatile("fence.proxy.async.global;" ::: "memory");
+      __threadfence();
+      atomicAdd(fc.wdone + fc.tilewin[t], 1);
+    };
     auto epi2 = [&](int j, bool waited) {
       const int b = j % L::NA;
       const Tile tl = tiles[tile_at(j)];
@@ -341,7 +349,16 @@ expert_fwd_sm100_kernel(const __grid_constant__ CUtensorMap w1map, const __grid_
           }
         }
       }
+      // fused combine: once the previous tile's slab stores have completed (all bulk groups but this
+      // tile's DH/64), publish them to the combine warps of every CTA
+      if (fc.out && leader && !lsu) {
+        asm volatile("cp.async.bulk.wait_group %0;" ::"n"(DH / 64) : "memory");
+        if (j >= 1) signal(tile_at(j - 1));
+      }
     };
+    // (the fused combine's completion signal of one tile's 32-row slab: async-proxy writes complete,
+    // then made visible to other CTAs' generic loads before the counter is released)
+    (void)0;
     // this row's gate, fetched one tile ahead (its L2 latency would sit at the top of every tile)
     float g_n = 0.f;
     auto fetch = [&](int t) {
@@ -420,6 +437,82 @@ expert_fwd_sm100_kernel(const __grid_constant__ CUtensorMap w1map, const __grid_
     }
     if (i >= 1) epi2(i - 1, false);
     if (half == 0 && lane == 0) bulk_wait_all();
+    if (fc.out && half == 0 && lane == 0 && !lsu && i >= 1) signal(tile_at(i - 1));
+  } else if (warp >= kCombWarp0 && fc.out) {
+    // ================================================================ fused combine (3 warps)
+    // Windows (head h, part p) in order: wait until every tile of the window has been stored by all
+    // CTAs (4 slab signals per tile), then combine this CTA's slice of the window's tokens
+    // [wtok[h][p-1], wtok[h][p]): y[t][h*d_h + c] = sum_j Yrep[h][pos(t,j)][c] in j order, fp32,
+    // rounded once — the arithmetic of combine_kernel (bit-identical).  The window's Yrep rows were
+    // written moments ago and are read back from L2.  All CTAs are co-resident (one per SM), so the
+    // spin cannot deadlock; a bounded spin traps instead of hanging on a bookkeeping error.
+    const int cw = warp - kCombWarp0, NCW = kThreads / 32 - kCombWarp0;
+    const int nwin = rt.H * kTileParts;
+    const int64_t R = rt.T * rt.k;
+    for (int w = 0; w < nwin; ++w) {
+      const int h = w / kTileParts, p = w % kTileParts;
+      if (lane == 0) {
+        const int need = 4 * fc.wtiles[w];
+        long long spins = 0;
+        while (true) {
+          int v;
+          asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(fc.wdone + w) : "memory");
+          if (v >= need) break;
+          __nanosleep(100);
+          if (++spins > (1ll << 24)) {
+            printf("[mhl fused combine] CTA %d warp %d: window %d stuck at %d of %d tile-slab signals\n",
+                   (int)blockIdx.x, warp, w, v, need);
+            __trap();
+          }
+        }
+      }
+      __syncwarp();
+      const int lo = p == 0 ? 0 : fc.wtok[w - 1], hi = fc.wtok[w];
+      const int n = hi - lo;
+      const int b0 = lo + (int)((int64_t)n * blockIdx.x / gridDim.x), b1 = lo + (int)((int64_t)n * (blockIdx.x + 1) / gridDim.x);
+      const bf16* rep = reinterpret_cast<const bf16*>(yout) + (size_t)h * rt.Rp * DH;
+      // two tokens per warp iteration (16 lanes x 32-byte loads per token row when d_h = 256) for
+      // twice the loads in flight; every lane takes part in the position broadcasts
+      for (int t0 = b0 + 2 * cw; t0 < b1; t0 += 2 * NCW) {
+        const int sub = lane >> 4, l16 = lane & 15;            // token t0 + sub, lane l16 of its half-warp
+        const int t = t0 + sub;
+        const bool tok = t < b1;
+        const int64_t rb = (size_t)h * R + (int64_t)t * rt.k;
+        const int my_pos = (tok && l16 < rt.k) ? rt.pos[rb + l16] : 0;
+        int pj[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) pj[j] = __shfl_sync(0xffffffffu, my_pos, (lane & 16) | j);
+        if (tok) {
+          for (int ch = l16; ch < DH / 8; ch += 16) {
+            float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+            for (int j0 = 0; j0 < 16; j0 += 8) {
+              if (j0 >= rt.k) break;
+              uint4 v[8];
+#pragma unroll
+              for (int j = 0; j < 8; ++j)
+                if (j0 + j < rt.k) v[j] = __ldcg(reinterpret_cast<const uint4*>(rep + (size_t)pj[j0 + j] * DH + ch * 8));
+#pragma unroll
+              for (int j = 0; j < 8; ++j) {
+                if (j0 + j < rt.k) {
+                  const __nv_bfloat162* pv = reinterpret_cast<const __nv_bfloat162*>(&v[j]);
+#pragma unroll
+                  for (int u = 0; u < 4; ++u) {
+                    const float2 f = __bfloat1622float2(pv[u]);
+                    acc[2 * u] += f.x;
+                    acc[2 * u + 1] += f.y;
+                  }
+                }
+              }
+            }
+            uint4 o;
+            o.x = pack_bf16x2(acc[0], acc[1]); o.y = pack_bf16x2(acc[2], acc[3]);
+            o.z = pack_bf16x2(acc[4], acc[5]); o.w = pack_bf16x2(acc[6], acc[7]);
+            *reinterpret_cast<uint4*>(reinterpret_cast<bf16*>(fc.out) + (size_t)t * fc.ldo + (size_t)h * DH + ch * 8) = o;
+          }
+        }
+      }
+    }
   }
   tc_fence_before();
   __syncthreads();
@@ -428,7 +521,7 @@ expert_fwd_sm100_kernel(const __grid_constant__ CUtensorMap w1map, const __grid_
 
 template <int DH, int DE>
 bool launch_t(const Routing& rt, const void* Xs, int64_t ldx, const void* W1, const void* W2, void* Yrep, int num_sms,
-              cudaStream_t s) {
+              cudaStream_t s, const FwdCombine& fc) {
   CUtensorMap w1m, w2m, ym, xm;
   // sub-token gather map: T+1 rows (row T all-zero), box = 64 columns x 1 row (TMA gather4)
   if (!make_tmap_2d_bf16(&xm, Xs, (uint64_t)rt.T + 1, (uint64_t)rt.H * DH, (uint64_t)ldx * 2, 1, 64)) return false;
@@ -446,7 +539,9 @@ bool launch_t(const Routing& rt, const void* Xs, int64_t ldx, const void* W1, co
     TraceBuf tb{tbuf, 0};
     cudaMemcpyToSymbolAsync(g_trace_fwd, &tb, sizeof(tb), 0, cudaMemcpyHostToDevice, s);
   }
-  kern<<<num_sms, kThreads, FwdL<DH, DE>::BYTES, s>>>(w1m, w2m, ym, xm, rt, (uint8_t*)Yrep, store_lsu(0));
+  const int lsu = store_lsu(0);
+  if (fc.out && (lsu || L_YDIRECT)) return false;   // the fused combine needs the TMA-store path's signals
+  kern<<<num_sms, kThreads, FwdL<DH, DE>::BYTES, s>>>(w1m, w2m, ym, xm, rt, (uint8_t*)Yrep, lsu, fc);
   if (trace_path) {
     TraceBuf tb{nullptr, 0};
     cudaMemcpyToSymbolAsync(g_trace_fwd, &tb, sizeof(tb), 0, cudaMemcpyHostToDevice, s);
@@ -473,9 +568,9 @@ bool expert_fwd_sm100_supported(int d_h, int d_e) {
 }
 
 bool launch_expert_fwd_sm100(const Routing& rt, const void* Xs, int64_t ldx, const void* W1, const void* W2, int d_h,
-                             int d_e, void* Yrep, int num_sms, cudaStream_t s) {
+                             int d_e, void* Yrep, int num_sms, cudaStream_t s, const FwdCombine& fc) {
 #define MHL_F(A, B) \
-  if (d_h == A && d_e == B) return launch_t<A, B>(rt, Xs, ldx, W1, W2, Yrep, num_sms, s);
+  if (d_h == A && d_e == B) return launch_t<A, B>(rt, Xs, ldx, W1, W2, Yrep, num_sms, s, fc);
   MHL_F(256, 128) MHL_F(256, 64) MHL_F(192, 64) MHL_F(128, 128) MHL_F(128, 64) MHL_F(64, 64) MHL_F(128, 256)
 #undef MHL_F
   return false;
