@@ -112,3 +112,50 @@ def test_bench_reference_arm_json():
     line = json.loads(out.stdout.strip().splitlines()[-1])
     assert line["impl"] == "reference" and line["value"] > 0
     assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["cpu_baseline"]["kind"] == "oracle"
+
+
+def _sched_worker(rank, world, port, result_q):
+    """The pipelined exchange schedule of hp_exchange (capi.cpp): at step i rank r sends the block
+    addressed to q = (r+i) mod G and receives the block of src = (r-i) mod G.  Over gloo it must
+    deliver exactly what an all-to-all delivers (block s of rank r = rank s's block for r), and
+    the block sizes come from the plan (x2 for the scatter with separate routing sub-tokens).
+    A step's send and receive are posted together (NCCL group there, isend + recv here)."""
+    import sys
+    sys.path.insert(0, ROOT)
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2602_04870_b200 import mhlmoe as C
+        ok = True
+        for flags in (0, C.MHL_FLAG_ROUTING_TOKENS):
+            cfg = C.make_config(64, 32, 4, 8, 8, 2, 8, "bf16", world, rank, flags)
+            info = C.hp_plan_query(cfg)
+            n = info["a2a_bytes_per_peer"] // 2                     # bf16 elements per block
+            base = 64 * 8 * (4 // world)                            # T_loc * H_loc * d_h
+            ok &= n == (2 if flags else 1) * base
+            send = [torch.full((n,), float(100 * rank + q)) for q in range(world)]
+            recv = [torch.empty(n) for _ in range(world)]
+            recv[rank].copy_(send[rank])                            # step 0: the self block
+            for i in range(1, world):                               # one grouped send/recv pair per step
+                q, src = (rank + i) % world, (rank - i) % world
+                w = dist.isend(send[q], q)
+                dist.recv(recv[src], src)
+                w.wait()
+            ok &= all(torch.equal(recv[s], torch.full((n,), float(100 * s + rank))) for s in range(world))
+        result_q.put((rank, bool(ok)))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_pipelined_exchange_schedule_gloo(world):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_sched_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=180) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+    assert all(res[r] for r in range(world)), res
