@@ -40,11 +40,24 @@ __device__ __forceinline__ float fast_ex2(float x) {
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
   return r;
 }
+// 1/x on the FMA pipe (x >= 1 here): magic-constant seed (|rel err| <= 1/8) and three Newton steps
+// (1/8 -> 1.6e-2 -> 2.4e-4 -> 6e-8), so half of the GELU reciprocals leave the MUFU (the epilogues
+// are MUFU-bound at 2 MUFU ops per element).
+__device__ __forceinline__ float nr_rcp(float x) {
+  float r = __int_as_float(0x7EF311C7 - __float_as_int(x));
+#pragma unroll
+  for (int i = 0; i < 3; ++i) r = fmaf(r, fmaf(-x, r, 1.0f), r);
+  return r;
+}
 __device__ __forceinline__ float2 gelu2(float2 h, float2* dgelu) {
   const float2 hh = __fmul2_rn(h, h);
   const float2 z = make_float2(fabsf(h.x) * 0.70710678118654752f, fabsf(h.y) * 0.70710678118654752f);
   const float2 d = __ffma2_rn(make_float2(0.3275911f, 0.3275911f), z, make_float2(1.f, 1.f));
+#ifdef MHL_GELU_NR
+  const float2 t = make_float2(fast_rcp(d.x), nr_rcp(d.y));
+#else
   const float2 t = make_float2(fast_rcp(d.x), fast_rcp(d.y));
+#endif
   float2 q = __ffma2_rn(make_float2(1.061405429f, 1.061405429f), t, make_float2(-1.453152027f, -1.453152027f));
   q = __ffma2_rn(q, t, make_float2(1.421413741f, 1.421413741f));
   q = __ffma2_rn(q, t, make_float2(-0.284496736f, -0.284496736f));
