@@ -204,8 +204,8 @@ int main(int argc, char** argv) {
   cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
   for (int mech : mechs)
     for (int PW : {4, 8})
-      for (int S : {4, 8, 12}) {
-        if (mech == 6 ? S % (PW / 2) : S % PW) continue;
+      for (int S : {4, 6, 8, 12}) {
+        if (mech == 6 ? S < PW / 2 : S % PW) continue;   // mech 6: any S >= owners (parity argument)
         const int smem = S * kChunk + 2048;
         cudaFuncSetAttribute(ring, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         float tot = 0;
