@@ -100,7 +100,11 @@ struct HL {
   // dH/gA straight from registers; giving its smem staging to the gather ring (6 stages instead
   // of 4) measured SLOWER (K1 1.10 -> 1.50 ms, r1e), so the layout keeps the 4-stage ring.
   static constexpr bool GROUPED = NBUF == 2 && kEpiWarps == 16;
+#ifdef MHL_K1_RING6
+  static constexpr int STGB = GROUPED ? 0 : 4 * BOXES * 4096;   // experiment: staging smem -> ring
+#else
   static constexpr int STGB = 4 * BOXES * 4096;             // dH/gA staging: [quadrant][box] 32 x 64 bf16
+#endif
   static constexpr int W1 = 0, W2 = WB, STG = 2 * WB, RING = STG + STGB;
   static constexpr int CTRL_MAX = 3 * 1024;
   static constexpr int S_RAW = (kMaxSmem - RING - CTRL_MAX) / kChunk;
@@ -121,7 +125,11 @@ struct HL {
   // refilled by the owner that filled it before.  (S >= OWNERS alone would keep the EMPTY parity
   // exact too — the owner's previous chunk waited for the in-order consumption of chunk
   // c - OWNERS - S >= c - 2S — but the 6-stage ring it allows measured slower, see above.)
+#ifdef MHL_K1_RING6
+  static constexpr int S = S_RAW > 12 ? 12 : S_RAW;
+#else
   static constexpr int S = (S_RAW > 12 ? 12 : S_RAW) / OWNERS * OWNERS;
+#endif
   static constexpr int CTRL = RING + S * kChunk;
   static constexpr int B_FULL = CTRL, B_EMPTY = B_FULL + 8 * S;
   static constexpr int B_W1F = B_EMPTY + 8 * S, B_W1E = B_W1F + 8, B_W2F = B_W1E + 8, B_W2E = B_W2F + 8;
@@ -144,6 +152,7 @@ expert_bwd_h_kernel(const __grid_constant__ CUtensorMap w1map, const __grid_cons
   using L = HL<DH, DE>;
   constexpr int kProdWarps = L::PW, kMmaWarp = L::MMA_WARP, kEpiWarp0 = L::EPI_WARP0, NBUF = L::NBUF;
   TraceBuf trc = g_trace_dx;   // one load; trace_ev then costs a register test
+  if (threadIdx.x == 0) trace_cta(trc, 60);
   constexpr int S = L::S, KB = DH / 64;
   extern __shared__ __align__(1024) uint8_t smem[];
   if ((smem_u32(smem) & 1023u) != 0u) __trap();
@@ -486,6 +495,7 @@ expert_bwd_h_kernel(const __grid_constant__ CUtensorMap w1map, const __grid_cons
   }
   tc_fence_before();
   __syncthreads();
+  if (threadIdx.x == 0) trace_cta(trc, 61);
   if (warp == kMmaWarp) tmem_dealloc<512>(tmem);
 }
 

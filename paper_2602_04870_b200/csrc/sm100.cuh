@@ -319,6 +319,15 @@ struct TraceBuf { unsigned long long* p; unsigned int cap; };
 __device__ __forceinline__ void trace_ev(TraceBuf& tb, int ev, int tile) {
   if (tb.p != nullptr && blockIdx.x == 0 && tile >= 0 && tile < 4096) tb.p[ev * 4096 + tile] = clock64();
 }
+// per-CTA event (slot = CTA index): start / end stamps of every CTA, for load-balance traces.
+// globaltimer (ns, common to all SMs) rather than the per-SM clock.
+__device__ __forceinline__ void trace_cta(TraceBuf& tb, int ev) {
+  if (tb.p != nullptr && blockIdx.x < 4096) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    tb.p[ev * 4096 + blockIdx.x] = t;
+  }
+}
 
 __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
   uint32_t r;
