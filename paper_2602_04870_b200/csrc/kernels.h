@@ -13,7 +13,10 @@ constexpr int kExpertBM = 128;     // replica rows per expert tile (tcgen05 M)
 constexpr int kDwStep = 64;        // sorted rows per dW pipeline step (dW chunk boundaries align to it)
 constexpr int kMaxDwParts = 160;   // dW row parts per head (= the dW grid, min(#SMs, this))
 constexpr int kTileGroup = 8;      // consecutive expert tiles a persistent CTA takes at once
-constexpr int kTileParts = 8;      // token-order parts per expert segment in the tile list (cluster.cu)
+#ifndef MHL_TILE_PARTS
+#define MHL_TILE_PARTS 8
+#endif
+constexpr int kTileParts = MHL_TILE_PARTS;   // token-order parts per expert segment in the tile list (cluster.cu)
 
 // Clustered routing of one rank's local heads (F3/F4 outputs, device pointers).
 // Sorted-row arrays have a fixed per-head capacity Rp = T*k + N_e*seg_align (expert segments are
