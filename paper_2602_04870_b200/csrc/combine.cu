@@ -41,10 +41,11 @@ template <typename E, bool BWD, int KMAX, bool SMEM_W>
 __global__ void __launch_bounds__(SMEM_W ? 512 : 256)
 combine_kernel(const E* __restrict__ rep, const int32_t* __restrict__ pos, const int32_t* __restrict__ idx,
                const float* __restrict__ dS, const float* __restrict__ W_rT, int H, int64_t T, int k, int d_h,
-               int N_e, int64_t Rp, int64_t t0, int64_t nT, E* __restrict__ out, int64_t ldo) {
+               int N_e, int64_t Rp, int64_t t0, int64_t nT, E* __restrict__ out, int64_t ldo, int tok_rt) {
   constexpr int V = Vec<E>::N;
   extern __shared__ __align__(16) float s_w[];           // [N_e][d_h] when SMEM_W
-  constexpr int NT = SMEM_W ? 512 : 256, NW = NT / 32, TOK = SMEM_W ? kCombTokW : kCombTok;
+  constexpr int NT = SMEM_W ? 512 : 256, NW = NT / 32;
+  const int TOK = SMEM_W ? kCombTokW : tok_rt;   // tokens per CTA (smaller for small T: more CTAs in flight)
   const int h = blockIdx.y, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t R = T * k;
   const float* wt_h = W_rT + (size_t)h * N_e * d_h;
@@ -134,14 +135,16 @@ combine_kernel(const E* __restrict__ rep, const int32_t* __restrict__ pos, const
 template <typename E, bool BWD, bool SMEM_W>
 void launch_kw(const Routing& rt, const E* rep, const float* dS, const float* W_rT, int d_h, E* out, int64_t ldo,
                int64_t t0, int64_t nT, cudaStream_t s) {
-  const int tok = SMEM_W ? kCombTokW : kCombTok;
+  // tokens per CTA: kCombTok, halved down to 16 until the grid has >= 8 CTAs per SM (148 SMs)
+  int tok = SMEM_W ? kCombTokW : kCombTok;
+  while (!SMEM_W && tok > 16 && ((nT + tok - 1) / tok) * rt.H < 8 * 148) tok /= 2;
   const dim3 grid((unsigned)((nT + tok - 1) / tok), (unsigned)rt.H);
   const size_t smem = SMEM_W ? (size_t)rt.N_e * d_h * 4 : 0;
 #define MHL_CK(KM)                                                                                          \
   {                                                                                                         \
     auto f = combine_kernel<E, BWD, KM, SMEM_W>;                                                            \
     if (smem > 48 * 1024) cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);  \
-    f<<<grid, SMEM_W ? 512 : 256, smem, s>>>(rep, rt.pos, rt.idx, dS, W_rT, rt.H, rt.T, rt.k, d_h, rt.N_e, rt.Rp, t0, nT, out, ldo); \
+    f<<<grid, SMEM_W ? 512 : 256, smem, s>>>(rep, rt.pos, rt.idx, dS, W_rT, rt.H, rt.T, rt.k, d_h, rt.N_e, rt.Rp, t0, nT, out, ldo, tok); \
   }
   if (rt.k <= 2) MHL_CK(2) else if (rt.k <= 4) MHL_CK(4) else if (rt.k <= 8) MHL_CK(8) else MHL_CK(16)
 #undef MHL_CK
