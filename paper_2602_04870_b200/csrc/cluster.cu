@@ -258,7 +258,11 @@ scatter_kernel(const int32_t* __restrict__ idx, const float* __restrict__ gate, 
                const int32_t* __restrict__ tilepref, int32_t* __restrict__ perm, int32_t* __restrict__ pos,
                int32_t* __restrict__ tok_s, float* __restrict__ gate_s, int64_t T, int k, int N_e, int n_rt,
                int64_t Rp) {
-  extern __shared__ int wcnt[];                       // [kScatterWarps][N_e]
+  extern __shared__ int sm[];
+  int* wcnt = sm;                                     // [kScatterWarps][N_e]
+  int* lbase = wcnt + kScatterWarps * N_e;            // [N_e] the tile's expert runs in local sorted order
+  int* s_r = lbase + N_e;                             // [kRouterTile * k] replicas in local sorted order
+  int* s_e = s_r + kRouterTile * k;                   // [kRouterTile * k] their experts
   const int tt = blockIdx.x, h = blockIdx.y, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   for (int i = threadIdx.x; i < kScatterWarps * N_e; i += blockDim.x) wcnt[i] = 0;
   __syncthreads();
@@ -280,10 +284,28 @@ scatter_kernel(const int32_t* __restrict__ idx, const float* __restrict__ gate, 
   for (int e = threadIdx.x; e < N_e; e += blockDim.x) {
     int run = 0;
     for (int w = 0; w < kScatterWarps; ++w) { const int c = wcnt[w * N_e + e]; wcnt[w * N_e + e] = run; run += c; }
+    lbase[e] = run;                                   // the tile's count of expert e (scanned below)
+  }
+  __syncthreads();
+  if (warp == 0) {                                    // exclusive scan of the counts over experts
+    int carry = 0;
+    for (int b = 0; b < N_e; b += 32) {
+      const int e = b + lane;
+      const int v = e < N_e ? lbase[e] : 0;
+      int incl = v;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const int n = __shfl_up_sync(0xffffffffu, incl, d);
+        if (lane >= d) incl += n;
+      }
+      if (e < N_e) lbase[e] = carry + incl - v;
+      carry += __shfl_sync(0xffffffffu, incl, 31);
+    }
   }
   __syncthreads();
   const int32_t* offh = off + (size_t)h * (N_e + 1);
   const int32_t* pre = tilepref + ((size_t)h * n_rt + tt) * N_e;
+  // pass 2: stable ranks -> pos (coalesced, replica order) and the tile's replicas sorted by expert in smem
   for (int64_t base = w0; base < w1; base += 32) {
     const int64_t r = base + lane;
     const bool act = r < w1;
@@ -291,16 +313,25 @@ scatter_kernel(const int32_t* __restrict__ idx, const float* __restrict__ gate, 
     const unsigned mask = __match_any_sync(0xffffffffu, e);
     const int rank = __popc(mask & ((1u << lane) - 1u));
     if (act) {
-      const int p = offh[e] + pre[e] + my[e] + rank;
-      const size_t q = (size_t)h * Rp + p;
-      perm[q] = (int32_t)r;
-      tok_s[q] = (int32_t)(r / k);
-      gate_s[q] = gate_h[r];
-      pos[(size_t)h * T * k + r] = p;
+      const int li = lbase[e] + my[e] + rank;
+      s_r[li] = (int)(r - r0);
+      s_e[li] = e;
+      pos[(size_t)h * T * k + r] = offh[e] + pre[e] + my[e] + rank;
     }
     __syncwarp();
     if (act && rank == 0) my[e] += __popc(mask);
     __syncwarp();
+  }
+  __syncthreads();
+  // pass 3: each expert's run of this tile is contiguous in the clustered rows -> coalesced stores
+  const int n = (int)(r1 - r0);
+  for (int li = threadIdx.x; li < n; li += blockDim.x) {
+    const int e = s_e[li];
+    const int64_t r = r0 + s_r[li];
+    const size_t q = (size_t)h * Rp + offh[e] + pre[e] + (li - lbase[e]);
+    perm[q] = (int32_t)r;
+    tok_s[q] = (int32_t)(r / k);
+    gate_s[q] = gate_h[r];
   }
 }
 
@@ -376,8 +407,10 @@ void launch_cluster(int H, int64_t T, int k, int N_e, const int32_t* idx, const 
   dw_parts_kernel<<<H, 1024, 0, s>>>(off, H, N_e, dw_parts, chunks, max_chunks, nchunks, cbase, ccount, pbase, pcount);
   tiles_kernel<<<(H * N_e + 7) / 8, 256, 0, s>>>(counts, off, tbase, tiles, max_tiles, H, N_e, Rp, perm, tok_s,
                                                  gate_s, (int)T, seg_align, tilewin);
-  scatter_kernel<<<dim3(n_rt, H), kScatterWarps * 32, sizeof(int) * kScatterWarps * N_e, s>>>(
-      idx, gate, off, tilepref, perm, pos, tok_s, gate_s, T, k, N_e, n_rt, Rp);
+  const size_t ssm = sizeof(int) * ((size_t)(kScatterWarps + 1) * N_e + 2 * (size_t)kRouterTile * k);
+  if (ssm > 48 * 1024) cudaFuncSetAttribute(scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ssm);
+  scatter_kernel<<<dim3(n_rt, H), kScatterWarps * 32, ssm, s>>>(idx, gate, off, tilepref, perm, pos, tok_s, gate_s,
+                                                                T, k, N_e, n_rt, Rp);
 }
 
 }  // namespace mhl
