@@ -157,7 +157,10 @@ MHL_API mhl_status mhlmoe_forward(mhl_plan plan, const void* x, const mhl_weight
 /* Backward (chain rule of Eq. 1-6; router part = Alg. 2, P:846-P:866, done
  * deterministically without atomics, R21).  Same plan, x and weights as the forward
  * that filled `saved`.  d_out: [T_loc, d] E; dx: [T_loc, d] E (LOOPBACK: global).
- * Gradients: see mhl_grads.  Errors as mhlmoe_forward. */
+ * Gradients: see mhl_grads.  Errors as mhlmoe_forward.  The forward's state in `saved`
+ * is only read; the backward does (re)derive the weight-gradient chunk lists, a pure
+ * function of that state, into scratch inside `saved`, so calls on one `saved` must not
+ * run concurrently (as for any use of one plan). */
 MHL_API mhl_status mhlmoe_backward(mhl_plan plan, const void* x, const mhl_weights* w, const void* d_out,
                            const void* saved, void* dx, const mhl_grads* grads,
                            void* workspace, size_t workspace_bytes, void* stream);

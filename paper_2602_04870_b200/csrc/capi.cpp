@@ -523,7 +523,7 @@ mhl_status moe_forward_local(mhl_plan p, const RankPtrs& R, void* yout, cudaStre
                         (float*)(R.saved + S.gate_s), m.Rp, m.seg_align, tiles, ntiles, m.max_tiles,
                         (mhl::Tile*)(R.saved + S.chunks),
                         (int32_t*)(R.saved + S.nchunks), (int32_t*)(R.saved + S.cbase), (int32_t*)(R.saved + S.ccount),
-                        m.max_chunks, m.dw_parts, (int32_t*)(R.saved + S.pbase), (int32_t*)(R.saved + S.pcount), s,
+                        m.max_chunks, 0, (int32_t*)(R.saved + S.pbase), (int32_t*)(R.saved + S.pcount), s,
                         fuse ? (int32_t*)(R.saved + S.tilewin) : nullptr);
     if (fuse) {
       mhl::launch_windows(routing_view(m, R.saved), (const int32_t*)(R.saved + S.load), (int32_t*)(R.saved + S.wtiles),
@@ -625,6 +625,12 @@ mhl_status moe_backward_local(mhl_plan p, const RankPtrs& R, const void* dY, voi
   }
   if (R.dW1 || R.dW2) {
     MHL_SPAN("B5_expert_bwd_dw");
+    if (tc) {
+      mhl::launch_dw_parts(rt, (mhl::Tile*)(R.saved + S.chunks), (int32_t*)(R.saved + S.nchunks),
+                           (int32_t*)(R.saved + S.cbase), (int32_t*)(R.saved + S.ccount),
+                           (int32_t*)(R.saved + S.pbase), (int32_t*)(R.saved + S.pcount), s);
+      p->launches++;
+    }
     if (tc)
       mhl::launch_expert_bwd_sm100(rt, Xs, m.XW, dY, m.HD, R.W1, R.W2, m.d_h, m.d_e, dXrep, dg, dH, gA,
                                    (float*)(R.ws + B.dw_part), (int*)(R.ws + B.dw_done), R.dW1, R.dW2,

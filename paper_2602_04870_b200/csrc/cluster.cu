@@ -384,6 +384,12 @@ __global__ void update_bias_kernel(const int32_t* __restrict__ load, int n, int 
 
 }  // namespace
 
+void launch_dw_parts(const Routing& rt, Tile* chunks, int32_t* nchunks, int32_t* cbase, int32_t* ccount,
+                     int32_t* pbase, int32_t* pcount, cudaStream_t s) {
+  dw_parts_kernel<<<rt.H, 1024, 0, s>>>(rt.off, rt.H, rt.N_e, rt.dw_parts, chunks, rt.max_chunks, nchunks, cbase,
+                                         ccount, pbase, pcount);
+}
+
 void launch_windows(const Routing& rt, const int32_t* counts, int32_t* wtiles, int32_t* wtok, cudaStream_t s) {
   window_kernel<<<rt.H, 256, 0, s>>>(counts, rt.off, rt.tok_s, rt.Rp, rt.N_e, rt.seg_align, (int)rt.T, wtiles, wtok);
 }
@@ -404,7 +410,8 @@ void launch_cluster(int H, int64_t T, int k, int N_e, const int32_t* idx, const 
   // tile bases [H][kTileParts][N_e] live in the (otherwise unused here) tail of tilepref's scratch
   int32_t* tbase = tilepref + (size_t)H * n_rt * N_e;
   offsets_kernel<<<H, 1024, 0, s>>>(counts, off, tbase, ntiles, H, N_e, max_tiles, seg_align);
-  dw_parts_kernel<<<H, 1024, 0, s>>>(off, H, N_e, dw_parts, chunks, max_chunks, nchunks, cbase, ccount, pbase, pcount);
+  if (dw_parts > 0)
+    dw_parts_kernel<<<H, 1024, 0, s>>>(off, H, N_e, dw_parts, chunks, max_chunks, nchunks, cbase, ccount, pbase, pcount);
   tiles_kernel<<<(H * N_e + 7) / 8, 256, 0, s>>>(counts, off, tbase, tiles, max_tiles, H, N_e, Rp, perm, tok_s,
                                                  gate_s, (int)T, seg_align, tilewin);
   const size_t ssm = sizeof(int) * ((size_t)(kScatterWarps + 1) * N_e + 2 * (size_t)kRouterTile * k);

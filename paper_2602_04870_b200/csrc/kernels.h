@@ -85,6 +85,10 @@ struct FwdCombine {
   const int32_t* tilewin = nullptr;  // [ntiles] window of each tile
 };
 void launch_windows(const Routing& rt, const int32_t* counts, int32_t* wtiles, int32_t* wtok, cudaStream_t s);
+// the dW kernel's row-part chunks of a clustered routing (launch_cluster with dw_parts = 0 leaves
+// them to this call, which the backward makes: a forward-only step does not pay for them)
+void launch_dw_parts(const Routing& rt, Tile* chunks, int32_t* nchunks, int32_t* cbase, int32_t* ccount,
+                     int32_t* pbase, int32_t* pcount, cudaStream_t s);
 
 bool launch_expert_fwd_sm100(const Routing& rt, const void* Xs, int64_t ldx, const void* W1, const void* W2, int d_h,
                              int d_e, void* Yrep, int num_sms, cudaStream_t s, const FwdCombine& fc = FwdCombine());
