@@ -110,7 +110,7 @@ struct Dims {
   bool rtok;       // MHL_FLAG_ROUTING_TOKENS (P:1565-P:1570): Xs rows carry [x part | r part]
   int XW;          // Xs row width per rank: HD, or 2*HD with routing tokens (r part at column HD)
   int Din;         // W_in rows: D, or 2*D with routing tokens
-  int n_rt, max_tiles, max_chunks, seg_align;
+  int n_rt, max_tiles, max_chunks, seg_align, n_rbwd;
   int dw_parts = mhl::kMaxDwParts;   // dW row parts per head (= dW grid), set from the SM count by hp_plan
 };
 
@@ -176,7 +176,7 @@ BwdLayout bwd_layout(const Dims& m) {
   L.dS_s = b.take((size_t)m.H * m.Rp * 4);   // dS in sorted-row order (K2's router term)
   L.dH = b.take((size_t)m.H * m.Rp * m.d_e * m.el);
   L.gA = b.take((size_t)m.H * m.Rp * m.d_e * m.el);
-  L.dwr_part = b.take((size_t)m.H * m.n_rt * m.N_e * m.d_h * 4);
+  L.dwr_part = b.take((size_t)m.H * m.n_rbwd * m.N_e * m.d_h * 4);
   L.W_rT = b.take((size_t)m.H * m.N_e * m.d_h * 4);
   L.send4 = b.take(m.G > 1 ? (size_t)m.T_g * m.XW * m.el : 0);
   L.recv4 = b.take(m.G > 1 ? (size_t)m.T_loc * m.G * m.XW * m.el : 0);
@@ -210,8 +210,6 @@ mhl_status make_dims(const mhl_config* c, Dims* m) {
   if (m->R >= (int64_t)1 << 31) return fail(MHL_ERR_UNSUPPORTED, "T_glob * k must be < 2^31");
   m->d = c->d_model; m->N_h = c->n_heads; m->d_h = c->d_head; m->N_e = c->n_experts; m->d_e = c->d_expert;
   m->H = m->N_h / m->G;
-  m->Rp = m->R + (int64_t)m->N_e * 2 * mhl::kExpertBM;   // capacity for either segment alignment
-  if (m->Rp >= (int64_t)1 << 31) return fail(MHL_ERR_UNSUPPORTED, "T_glob * k + N_e * 256 must be < 2^31");
   m->HD = m->H * m->d_h;
   m->D = m->N_h * m->d_h;
   m->rtok = (c->flags & MHL_FLAG_ROUTING_TOKENS) != 0;
@@ -223,8 +221,14 @@ mhl_status make_dims(const mhl_config* c, Dims* m) {
   m->simt = (c->flags & MHL_FLAG_SIMT) != 0 || c->dtype == MHL_F32;
   m->pair = !m->simt && (c->flags & MHL_FLAG_PAIR) != 0;
   m->seg_align = m->pair ? 2 * mhl::kExpertBM : mhl::kExpertBM;
+  m->Rp = m->R + (int64_t)m->N_e * m->seg_align;   // each expert segment padded by < seg_align rows
+  if (m->Rp >= (int64_t)1 << 31) return fail(MHL_ERR_UNSUPPORTED, "T_glob * k + N_e * seg_align must be < 2^31");
   m->rank = loop ? 0 : c->rank;
   m->n_rt = (int)((m->T_g + mhl::kRouterTile - 1) / mhl::kRouterTile);
+  // router-backward partials: one per router tile on the SIMT path, at most one per (SM / N_h) on
+  // the tcgen05 path (launch: min(n_rt, #SMs / N_h) chunks per head)
+  m->n_rbwd = (!m->simt && mhl::router_bwd_sm100_supported(m->d_h, m->N_e, m->k))
+                  ? std::min(m->n_rt, std::max(1, mhl::kMaxDwParts / m->N_h)) : m->n_rt;
   const int64_t mt = (int64_t)m->H * ((m->R + mhl::kExpertBM - 1) / mhl::kExpertBM + 2 * m->N_e);
   if (mt >= (int64_t)1 << 31) return fail(MHL_ERR_UNSUPPORTED, "too many tiles");
   m->max_tiles = (int)mt;
@@ -605,7 +609,8 @@ mhl_status moe_backward_local(mhl_plan p, const RankPtrs& R, const void* dY, voi
                                         (float*)(R.ws + B.dwr_part),
                                         // token chunks per head from the GLOBAL head count, so the
                                         // partial-sum order (and dW_r bits) do not depend on G
-                                        std::min(m.n_rt, std::max(1, p->num_sms / m.N_h)), R.dW_r, s))
+                                        std::min(m.n_rbwd, std::max(1, std::min(p->num_sms, mhl::kMaxDwParts) / m.N_h)),
+                                        R.dW_r, s))
         return fail(MHL_ERR_CUDA, "router backward: TMA tensor-map encoding failed");
     } else {
       mhl::launch_router_bwd(m.dtype, Xr, m.XW, idx, gate, dg, m.H, m.T_g, m.k, m.d_h, m.N_e, dS,

@@ -87,3 +87,28 @@ def test_oracle_is_not_imported_by_the_product():
             if f.endswith((".py", ".cpp", ".cu", ".h", ".cuh")):
                 src = open(os.path.join(dirpath, f), errors="ignore").read()
                 assert "oracle" not in re.sub(r"#.*|//.*", "", src).lower().replace("oracle/", ""), f
+
+
+def test_score_matrix_never_materialised_memory_flat_in_N_e():
+    """Fig. 4 / P:1277 and north_star: the fused router never writes the T x N_e score matrix.  The
+    plan's device memory (saved + workspace) has per-expert tables and per-replica buffers, but no
+    T*N_e term of score size: doubling T adds far less than the naive router's extra score bytes
+    for N_e = 1536 vs 64 experts."""
+    def mem(T, N_e):
+        i = _q(T_loc=T, d=1024, N_h=8, d_h=128, N_e=N_e, k=4, d_e=128, dtype="bf16")
+        return i["saved_bytes"] + i["workspace_bytes"]
+    cross = (mem(32768, 1536) - mem(32768, 64)) - (mem(16384, 1536) - mem(16384, 64))
+    naive = 8 * 16384 * (1536 - 64) * 4          # fp32 scores of 16384 more tokens x 1472 more experts
+    assert cross < 0.1 * naive, (cross, naive)
+
+
+def test_routing_tokens_plan_doubles_the_scatter_only():
+    """separate routing sub-tokens double the HP scatter volume; the plan's byte counts say
+    so (the gather of head outputs is unchanged, see mhl_a2a_bytes_posted)."""
+    from paper_2602_04870_b200 import mhlmoe as C
+    for G in (2, 4, 8):
+        a = _q(T_loc=4096, d=2048, N_h=8, d_h=256, N_e=64, k=8, d_e=128, dtype="bf16", world_size=G, rank=0)
+        b = _q(T_loc=4096, d=2048, N_h=8, d_h=256, N_e=64, k=8, d_e=128, dtype="bf16", world_size=G, rank=0,
+               flags=C.MHL_FLAG_ROUTING_TOKENS)
+        assert b["a2a_bytes_per_peer"] == 2 * a["a2a_bytes_per_peer"]
+        assert b["a2a_bytes_per_rank"] == 2 * a["a2a_bytes_per_rank"]
