@@ -146,8 +146,7 @@ void launch_router_bwd(int dtype, const void* Xs, int64_t ldx, const int32_t* id
 bool router_bwd_sm100_supported(int d_h, int N_e, int k);
 bool launch_router_bwd_sm100(const void* Xs, int64_t ldx, const int32_t* idx, const float* gate, const float* dg,
                              int H, int64_t T, int k, int d_h, int N_e, float* dS, float* partial, int nc_target,
-                             float* dW_r, cudaStream_t s, const int32_t* pos = nullptr, int64_t Rp = 0,
-                             float* dS_s = nullptr);   // dS_s: dS also scattered to sorted-row order
+                             float* dW_r, cudaStream_t s);
 
 // ---- dS_s[h][pos(t,j)] = dS[h][t][j] (padding rows untouched: their dXrep rows are never read)
 void launch_sort_ds(const Routing& rt, const float* dS, float* dS_s, cudaStream_t s);

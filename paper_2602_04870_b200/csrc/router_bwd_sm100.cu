@@ -54,8 +54,7 @@ template <int DH, int NE, int KMAX>
 __global__ void __launch_bounds__(kThreads, 1)
 router_bwd_sm100_kernel(const __grid_constant__ CUtensorMap xmap, const int32_t* __restrict__ idx,
                         const float* __restrict__ gate, const float* __restrict__ dg, int64_t T, int k, int nc,
-                        int N_e, float* __restrict__ dS, float* __restrict__ partial, const int32_t* __restrict__ pos,
-                        int64_t Rp, float* __restrict__ dS_s) {
+                        int N_e, float* __restrict__ dS, float* __restrict__ partial) {
   // blockIdx.z = expert block [e0, e0 + NE) of N_e (the paper's own N_e = 384-1536 per head)
   const int e0 = blockIdx.z * NE;
   using L = RbL<DH, NE>;
@@ -163,11 +162,7 @@ router_bwd_sm100_kernel(const __grid_constant__ CUtensorMap xmap, const int32_t*
         for (int j = 0; j < KMAX; ++j) {
           if (j < k) {
             const float v = gv[j] * (dv[j] - sum);
-            if (blockIdx.z == 0) {
-              dso[j] = v;
-              // dS in sorted-row order for the router term the dX GEMM folds in (expert_bwd_dx_sm100.cu)
-              if (dS_s) dS_s[(size_t)h * Rp + pos[((size_t)h * T + t) * k + j]] = v;
-            }
+            if (blockIdx.z == 0) dso[j] = v;
             const int el = ev[j] - e0;
             if (el >= 0 && el < NE) {
               const bf16 hi = __float2bfloat16_rn(v);
@@ -220,8 +215,7 @@ router_bwd_sum_kernel(const float* __restrict__ partial, int nc, int64_t n, floa
 
 template <int DH, int NE, int KMAX>
 bool launch_t(const void* Xs, int64_t ldx, const int32_t* idx, const float* gate, const float* dg, int H, int64_t T,
-              int k, int N_e, float* dS, float* partial, int nc_target, float* dW_r, cudaStream_t s, const int32_t* pos,
-              int64_t Rp, float* dS_s) {
+              int k, int N_e, float* dS, float* partial, int nc_target, float* dW_r, cudaStream_t s) {
   using L = RbL<DH, NE>;
   CUtensorMap xm;
   if (!make_tmap_2d_bf16(&xm, Xs, (uint64_t)T, (uint64_t)H * DH, (uint64_t)ldx * 2, kStep, 64)) return false;
@@ -229,8 +223,7 @@ bool launch_t(const void* Xs, int64_t ldx, const int32_t* idx, const float* gate
   const int nc = (int)std::max<int64_t>(1, std::min<int64_t>(nc_target, nst));
   auto kern = router_bwd_sm100_kernel<DH, NE, KMAX>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::BYTES);
-  kern<<<dim3(nc, H, N_e / NE), kThreads, L::BYTES, s>>>(xm, idx, gate, dg, T, k, nc, N_e, dS, partial, pos, Rp,
-                                                             dS_s);
+  kern<<<dim3(nc, H, N_e / NE), kThreads, L::BYTES, s>>>(xm, idx, gate, dg, T, k, nc, N_e, dS, partial);
   if (dW_r) {
     const int64_t n = (int64_t)DH * N_e;
     router_bwd_sum_kernel<<<dim3((unsigned)std::max<int64_t>(1, (n + 255) / 256), H), 256, 0, s>>>(partial, nc, n, dW_r);
@@ -240,9 +233,8 @@ bool launch_t(const void* Xs, int64_t ldx, const int32_t* idx, const float* gate
 
 template <int DH, int NE>
 bool launch_k(const void* Xs, int64_t ldx, const int32_t* idx, const float* gate, const float* dg, int H, int64_t T,
-              int k, int N_e, float* dS, float* partial, int nc_target, float* dW_r, cudaStream_t s, const int32_t* pos,
-              int64_t Rp, float* dS_s) {
-#define MHL_RBK(KM) return launch_t<DH, NE, KM>(Xs, ldx, idx, gate, dg, H, T, k, N_e, dS, partial, nc_target, dW_r, s, pos, Rp, dS_s);
+              int k, int N_e, float* dS, float* partial, int nc_target, float* dW_r, cudaStream_t s) {
+#define MHL_RBK(KM) return launch_t<DH, NE, KM>(Xs, ldx, idx, gate, dg, H, T, k, N_e, dS, partial, nc_target, dW_r, s);
   if (k <= 2) MHL_RBK(2)
   if (k <= 4) MHL_RBK(4)
   if (k <= 8) MHL_RBK(8)
@@ -260,12 +252,12 @@ bool router_bwd_sm100_supported(int d_h, int N_e, int k) {
 
 bool launch_router_bwd_sm100(const void* Xs, int64_t ldx, const int32_t* idx, const float* gate, const float* dg,
                              int H, int64_t T, int k, int d_h, int N_e, float* dS, float* partial, int nc_target,
-                             float* dW_r, cudaStream_t s, const int32_t* pos, int64_t Rp, float* dS_s) {
+                             float* dW_r, cudaStream_t s) {
   if (T <= 0) return false;
   const int NEB = N_e > 256 ? 256 : N_e;                      // experts per CTA block
 #define MHL_RB(A, B)        \
   if (d_h == A && NEB == B) \
-    return launch_k<A, B>(Xs, ldx, idx, gate, dg, H, T, k, N_e, dS, partial, nc_target, dW_r, s, pos, Rp, dS_s);
+    return launch_k<A, B>(Xs, ldx, idx, gate, dg, H, T, k, N_e, dS, partial, nc_target, dW_r, s);
   MHL_RB(256, 32) MHL_RB(256, 64) MHL_RB(256, 128) MHL_RB(256, 256)
   MHL_RB(128, 32) MHL_RB(128, 64) MHL_RB(128, 128) MHL_RB(128, 256)
 #undef MHL_RB
