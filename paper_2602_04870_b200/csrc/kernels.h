@@ -12,7 +12,10 @@ constexpr int kExpertBM = 128;     // replica rows per expert tile (tcgen05 M)
 // tile pair (256, MHL_FLAG_PAIR), which the cta_group::2 kernels need (tiles 2u, 2u+1 share an expert).
 constexpr int kDwStep = 64;        // sorted rows per dW pipeline step (dW chunk boundaries align to it)
 constexpr int kMaxDwParts = 160;   // dW row parts per head (= the dW grid, min(#SMs, this))
-constexpr int kTileGroup = 8;      // consecutive expert tiles a persistent CTA takes at once
+#ifndef MHL_TILE_GROUP
+#define MHL_TILE_GROUP 8
+#endif
+constexpr int kTileGroup = MHL_TILE_GROUP;   // consecutive expert tiles a persistent CTA takes at once
 #ifndef MHL_TILE_PARTS
 #define MHL_TILE_PARTS 8
 #endif
