@@ -92,7 +92,18 @@ __device__ __forceinline__ void tma_store_2d(const void* tmap, uint32_t src, int
                "r"(c0), "r"(c1)
                : "memory");
 }
+__device__ __forceinline__ void tma_store_2d_hint(const void* tmap, uint32_t src, int c0, int c1, uint64_t pol) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group.L2::cache_hint [%0, {%2, %3}], [%1], %4;"
+               ::"l"(tmap), "r"(src), "r"(c0), "r"(c1), "l"(pol)
+               : "memory");
+}
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+// L2 policies of the forward kernel (MHL_F5_L2HINT, off: measured F5 0.87 -> 0.91 ms with them):
+// sub-token rows gathered evict_last (each is
+// re-read by its other top-k experts), Y tiles stored evict_first (streamed out once)
+#ifndef MHL_F5_L2HINT
+#define MHL_F5_L2HINT 0
+#endif
 template <int N>
 __device__ __forceinline__ void bulk_wait_read() { asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory"); }
 __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
@@ -158,6 +169,7 @@ expert_fwd_sm100_kernel(const __grid_constant__ CUtensorMap w1map, const __grid_
     asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kProdRegs));
     const int pw = warp;
     const int owner = pw >> 1, lrow = (pw & 1) * 64 + 4 * (lane & 15);
+    const uint64_t pol_keep = l2_evict_last();
     Ph w1e, w2e;
     int cnt = 0;
     int nx[4] = {0, 0, 0, 0};
@@ -201,6 +213,10 @@ expert_fwd_sm100_kernel(const __grid_constant__ CUtensorMap w1map, const __grid_
         }
         __syncwarp();
         if (lane < 16)
+          if (MHL_F5_L2HINT)
+            tma_gather4_hint(sb + L::X + xs * kXChunk + lrow * 128, &xmap, (int)tl.head * DH + kb * 64, r0, r1, r2,
+                             r3, full, pol_keep);
+          else
           tma_gather4(sb + L::X + xs * kXChunk + lrow * 128, &xmap, (int)tl.head * DH + kb * 64, r0, r1, r2, r3,
                       full);
       }
@@ -267,6 +283,7 @@ expert_fwd_sm100_kernel(const __grid_constant__ CUtensorMap w1map, const __grid_
     const uint32_t lane_off = (uint32_t)(q * 32) << 16;
     Ph hf, gd[2];
     int ys = 0;   // running count of Y blocks stored (selects the smem stage)
+    const uint64_t pol_stream = l2_evict_first();
     auto signal = [&](int t) {
       if (t < 0) return;
       asm volatile("fence.proxy.async.global;" ::: "memory");
@@ -343,6 +360,10 @@ expert_fwd_sm100_kernel(const __grid_constant__ CUtensorMap w1map, const __grid_
           fence_proxy_async();
           named_bar_sync(2 + q, 64);
           if (leader) {
+            if (MHL_F5_L2HINT)
+              tma_store_2d_hint(&ymap, sb + L::YS + st * kYStage + q * 4096, cb * 64,
+                                (int)((size_t)tl.head * rt.Rp + tl.row0 + q * 32), pol_stream);
+            else
             tma_store_2d(&ymap, sb + L::YS + st * kYStage + q * 4096, cb * 64,
                          (int)((size_t)tl.head * rt.Rp + tl.row0 + q * 32));
             bulk_commit();
