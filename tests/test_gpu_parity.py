@@ -351,3 +351,44 @@ def test_fused_combine_bitwise_equals_separate_kernel(d_h, d_e, N_e, k, T):
     np.testing.assert_array_equal(outs[0], outs[1])
     g = _run_gpu(cfg, W, x, dout, backward=False)
     _compare(cfg, W, x, dout, g, backward=False)
+
+
+@pytest.mark.parametrize("name", ["paper", "g2x", "table5", "paper_rtok"])
+def test_full_size_sampled_rows_match_oracle(name):
+    """BASELINE's full-size configs (paper-scale T = 65536, d = 2048, N_h = 8, d_h = 256, N_e = 64,
+    k = 8, d_e = 128; its doubled-granularity variant; the paper's Table-5 shape; separate routing
+    tokens), bf16, the paper init, the bench's launch configuration, checked on sampled tokens:
+    every per-token quantity of the layer (sub-tokens, routing, gates, expert outputs, out, and dx
+    through the backward) is a function of that token alone, so the oracle run on the sampled rows
+    gives exactly their values.  Routing: indices bit-exact on clean sub-tokens (R8/R22)."""
+    _need_gpu()
+    from paper_2602_04870_b200.layer import MHLatentMoE, torch_dtype, weights_to_device
+    cfg = PRESETS[name]
+    W, x, dout = make_problem(cfg, 0, "paper")
+    td = torch_dtype(cfg.dtype)
+    L = MHLatentMoE(cfg.T, cfg.d, cfg.N_h, cfg.d_h, cfg.N_e, cfg.k, cfg.d_e, cfg.dtype,
+                    routing_tokens=cfg.routing_tokens)
+    Wd = weights_to_device(W, cfg.dtype)
+    xd = torch.from_numpy(x).to("cuda", td)
+    out, idx, gates = L.forward(xd, Wd, want_routing=True)
+    grads = L.alloc_grads()
+    dx = L.backward(xd, Wd, torch.from_numpy(dout).to("cuda", td), grads)
+    torch.cuda.synchronize()
+    L.check_status()
+    rng = np.random.default_rng(7)
+    S = np.sort(np.concatenate([rng.choice(cfg.T, 60, replace=False), [0, cfg.T - 1]]))
+    g = dict(out=out.float().cpu().numpy()[S], dx=dx.float().cpu().numpy()[S],
+             idx=idx.cpu().numpy()[:, S], gates=gates.cpu().numpy()[:, S])
+    P = {k: v.astype(np.float64) for k, v in W.items()}
+    xs, ds = x[S].astype(np.float64), dout[S].astype(np.float64)
+    C0 = O.layer_forward(P, xs, cfg.k, mode="bf16")
+    forced, n_clean, n_excl = check_routing(P, C0, g["idx"], cfg.k)
+    assert n_clean > 0.8 * (n_clean + n_excl)
+    C = O.layer_forward(P, xs, cfg.k, mode="bf16", forced_idx=forced)
+    for h in range(cfg.N_h):
+        sl = routing_slice(P, h)
+        budget = boundary_flip_budget(C.Xs_pre[:, sl], P["W_r"][h], "bf16")
+        assert np.all(np.abs(g["gates"][h] - C.g[h]) <= GATE_TOL + 0.5 * budget[:, None]), h
+    gr = O.layer_backward(P, xs, ds, C)
+    assert rel_err(g["out"], C.out) <= TOL["bf16"]
+    assert rel_err(g["dx"], gr["dx"]) <= TOL["bf16"]
