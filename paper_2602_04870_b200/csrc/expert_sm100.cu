@@ -98,7 +98,8 @@ __device__ __forceinline__ void tma_store_2d_hint(const void* tmap, uint32_t src
                : "memory");
 }
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
-// L2 policies of the forward kernel (MHL_F5_L2HINT, off: measured F5 0.87 -> 0.91 ms with them):
+// L2 policies of the forward kernel (MHL_F5_L2HINT: 0 none (default), 1 both, 2 stores only; 1 and 2
+// measured F5 0.87 -> 0.92-0.93 ms):
 // sub-token rows gathered evict_last (each is
 // re-read by its other top-k experts), Y tiles stored evict_first (streamed out once)
 #ifndef MHL_F5_L2HINT
@@ -213,7 +214,7 @@ expert_fwd_sm100_kernel(const __grid_constant__ CUtensorMap w1map, const __grid_
         }
         __syncwarp();
         if (lane < 16)
-          if (MHL_F5_L2HINT)
+          if (MHL_F5_L2HINT == 1)
             tma_gather4_hint(sb + L::X + xs * kXChunk + lrow * 128, &xmap, (int)tl.head * DH + kb * 64, r0, r1, r2,
                              r3, full, pol_keep);
           else
