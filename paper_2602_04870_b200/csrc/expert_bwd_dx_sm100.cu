@@ -84,6 +84,9 @@ struct Sched {
 constexpr int kEpiWarps = 16;
 constexpr int kEpiThreads = kEpiWarps * 32;
 
+#ifndef MHL_K1_STOREHINT
+#define MHL_K1_STOREHINT 1   // dH / gA stores evict_first (1) or normal (0)
+#endif
 #ifndef MHL_K1_PW
 #define MHL_K1_PW 8   // producer warps of the backward H kernel (8: in chunk-sharing pairs; 4: whole chunks)
 #endif
@@ -300,7 +303,7 @@ expert_bwd_h_kernel(const __grid_constant__ CUtensorMap w1map, const __grid_cons
       const int row = q * 32 + lane;
       const uint32_t lane_off = (uint32_t)(q * 32) << 16;
       const int bar_dg = 2 + grp * 4 + q;                   // the two warps of (group, quadrant)
-      const uint64_t pol_out = l2_evict_first();
+      const uint64_t pol_out = MHL_K1_STOREHINT ? l2_evict_first() : l2_evict_normal();
       float* s_x = s_dg + grp * 2 * BM;                     // [parity][BM]: s0 + s1 of each row
       Ph hd;
       float g_n = 0.f;
