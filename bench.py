@@ -392,6 +392,10 @@ def main():
                        "parallelism": f"hp{G}", "l2": "inputs larger than L2 (per-step working set >> 126 MB)",
                        "kernels": "simt-reference" if args.simt else "default"},
             "layer_tflops": layer_tflops,
+            # the metric's "% tcgen05 peak": whole-layer algorithmic FLOPs / step time vs the measured
+            # burst bf16 matmul peak and vs the 2.25 PF/s nominal dense bf16 figure
+            "layer_pct_tcgen05_peak": {"measured_burst": 100.0 * layer_tflops / tf_peak,
+                                       "nominal_2250": 100.0 * layer_tflops / 2250.0},
             "roofline": roof, "step_breakdown_ms": breakdown, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": int(launches), "clocks": clk}
     print(json.dumps(line), flush=True)
