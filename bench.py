@@ -130,11 +130,17 @@ class ClockSampler:
 
 # ----------------------------------------------------------------------------- algorithmic work
 def step_work(cfg, T_loc, G):
-    """Algorithmic work per step on one GPU, per timed span: FLOPs of the
-    contraction and the MINIMAL HBM bytes — every tensor the span must read or write, each unique
-    row once (gathered sub-token / dcat rows count once per head, not once per replica: their
-    k-fold re-reads are L2 traffic, not algorithmic HBM traffic).  The roofline time of a span is
-    max(flops / tensor peak, bytes / HBM peak)."""
+    """Algorithmic work per step on one GPU, per timed span, in SURVEY.md §8(d)'s units
+    (DESIGN.md §6): `flops` = the span's contraction FLOPs (the expert backward includes the
+    recompute of H that the IO-aware design implies, P:916-P:978: 5 GEMM units, §8(d) "1.37 TFLOP
+    implemented"); `bytes` = the MINIMAL HBM bytes the method requires of the span — its inputs and
+    outputs, each unique row once (a gathered sub-token / dcat row counts once per head: its k-fold
+    re-reads are L2 traffic).  Intermediates this implementation chooses to write and read back —
+    the per-replica Yrep / dXrep (v1 combine) inside the expert kernels, and dH / gA
+    between the backward expert kernels (SURVEY A.5 option c) — are NOT algorithmic bytes: they are
+    counted in `impl_bytes`, and the ncu-measured DRAM bytes are reported as `traffic`.  The
+    combine spans exist because of v1; their roofline is §8(d)'s v1 combine_pack bytes.  A span's
+    roofline time is max(flops / tensor peak, bytes / HBM peak)."""
     d, N_h, d_h, N_e, k, d_e = cfg.d, cfg.N_h, cfg.d_h, cfg.N_e, cfg.k, cfg.d_e
     D, el = N_h * d_h, (2 if cfg.dtype == "bf16" else 4)
     Din = D * (2 if cfg.routing_tokens else 1)
@@ -143,29 +149,34 @@ def step_work(cfg, T_loc, G):
     H = N_h // G
     wexp = H * N_e * d_e * d_h * el                        # one of W1 / W2 (local heads)
     row, erow = d_h * el, d_e * el
-    return {
+    unit = 2 * rep * d_h * d_e                             # one expert GEMM over every replica
+    w = {
         "F1_proj_in": dict(flops=2 * T_loc * d * Din, bytes=T_loc * d * el + Din * d * el + T_loc * Din * el),
         "F3_router_topk": dict(flops=2 * subtok * d_h * N_e, bytes=subtok * row + H * d_h * N_e * 4 + rep * 8),
         "F4_cluster": dict(flops=0, bytes=rep * 24),
-        # X rows once + W1, W2 + sorted token ids / gates; Yrep written
-        "F5_expert_fwd": dict(flops=4 * rep * d_h * d_e, bytes=subtok * row + 2 * wexp + rep * 8 + rep * row),
+        # X rows once + W1, W2 + sorted token ids / gates (Yrep, the v1 per-replica output: impl)
+        "F5_expert_fwd": dict(flops=2 * unit, bytes=subtok * row + 2 * wexp + rep * 8,
+                              impl_bytes=rep * row),
         "F6_combine": dict(flops=0, bytes=rep * row + rep * 4 + subtok * row),
         "F8_proj_out": dict(flops=2 * T_loc * D * d, bytes=T_loc * D * el + d * D * el + T_loc * d * el),
         "B8_proj_out_bwd": dict(flops=4 * T_loc * d * D,
                                 bytes=2 * T_loc * d * el + T_loc * D * el + d * D * el + T_loc * D * el + d * D * 4),
-        # X, dY rows once + W1, W2 + row metadata; dH, gA, dg written
-        "B5_expert_bwd_dx": dict(flops=4 * rep * d_h * d_e,
-                                 bytes=2 * subtok * row + 2 * wexp + rep * 12 + 2 * rep * erow + rep * 4),
-        # dH + W1 + dS read; dXrep written
-        "B5_expert_dx_gemm": dict(flops=2 * rep * d_h * d_e, bytes=rep * erow + wexp + rep * 4 + rep * row),
-        # X, dY rows once, dH, gA, token ids read; dW1, dW2 (fp32) written
-        "B5_expert_bwd_dw": dict(flops=4 * rep * d_h * d_e,
-                                 bytes=2 * subtok * row + 2 * rep * erow + rep * 4 + 2 * H * N_e * d_e * d_h * 4),
+        # H recompute + dA' (2 units); X, dY rows once + W1, W2 + row metadata; dg written (dH, gA: impl)
+        "B5_expert_bwd_dx": dict(flops=2 * unit, bytes=2 * subtok * row + 2 * wexp + rep * 12 + rep * 4,
+                                 impl_bytes=2 * rep * erow),
+        # dXrep = dH W1 (1 unit); W1 + dS read (dH read, dXrep written: impl)
+        "B5_expert_dx_gemm": dict(flops=unit, bytes=wexp + rep * 4, impl_bytes=rep * erow + rep * row),
+        # dW1, dW2 (2 units); X, dY rows once, token ids; dW1, dW2 (fp32) written (dH, gA read: impl)
+        "B5_expert_bwd_dw": dict(flops=2 * unit, bytes=2 * subtok * row + rep * 4 + 2 * H * N_e * d_e * d_h * 4,
+                                 impl_bytes=2 * rep * erow),
         "B3_router_bwd": dict(flops=2 * rep * d_h, bytes=subtok * row + rep * 12 + rep * 8 + H * d_h * N_e * 4),
         "B6_combine_bwd": dict(flops=0, bytes=rep * row + rep * 4 + subtok * row * (Din // D)),
         "B1_proj_in_bwd": dict(flops=4 * T_loc * d * Din,
                                bytes=T_loc * Din * el + Din * d * el + 2 * T_loc * d * el + Din * d * 4),
     }
+    for v in w.values():
+        v["impl_bytes"] = v["bytes"] + v.get("impl_bytes", 0)
+    return w
 
 
 def span_roofline(w, dur_s, tf_peak, hbm_peak):
@@ -204,6 +215,36 @@ def oracle_tokens_per_s(cfg, sample_tokens, seed=0, budget_s=20.0):
     return done / el, el, done
 
 
+def torchrun_argv(argv, n):
+    """The command that runs this bench with one process per GPU (the driver's own launch form)."""
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    return [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+            "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *argv]
+
+
+def nvlink_bytes(dev_index):
+    """(tx, rx) NVLink data bytes of this GPU so far, summed over its links (NVML field counters,
+    KiB), or None where NVML / NVLink is unavailable."""
+    try:
+        import pynvml
+        pynvml.nvmlInit()
+        h = pynvml.nvmlDeviceGetHandleByIndex(dev_index)
+        tx = rx = 0
+        for link in range(18):
+            vals = pynvml.nvmlDeviceGetFieldValues(h, [(pynvml.NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_TX, link),
+                                                       (pynvml.NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_RX, link)])
+            if vals[0].nvmlReturn != 0 or vals[1].nvmlReturn != 0:
+                continue
+            tx += vals[0].value.ullVal
+            rx += vals[1].value.ullVal
+        return tx * 1024, rx * 1024
+    except Exception:
+        return None
+
+
 def blas_threads():
     try:
         from threadpoolctl import threadpool_info
@@ -211,6 +252,49 @@ def blas_threads():
         return max((i.get("num_threads", 1) for i in info), default=1)
     except Exception:
         return os.cpu_count() or 1
+
+
+def run_reference(args, cfg, T_loc):
+    """The reference arm of this tier: the CPU oracle as it stands, on the host cores, each step one
+    fwd+bwd of a bounded token sample of the workload (full weights).  W untimed warm-up steps,
+    then exactly K timed steps; the sample is shrunk (by halving) when the warm-up says K steps of
+    it would not fit in ~3 minutes."""
+    import oracle as O
+    try:   # torchrun pins OMP/BLAS to 1 thread per process; the reference arm is rank 0 alone
+        from threadpoolctl import threadpool_limits
+        threadpool_limits(len(os.sched_getaffinity(0)))
+    except Exception:
+        pass
+    W = make_weights(cfg, 0, "paper")
+    P = {k: v.astype(np.float64) for k, v in W.items()}
+    S = max(8, args.cpu_sample)
+
+    def one(S):
+        x = make_tokens(cfg, 0, S, which="x").astype(np.float64)
+        dout = make_tokens(cfg, 0, S, which="dout").astype(np.float64)
+        t0 = time.perf_counter()
+        C = O.layer_forward(P, x, cfg.k, mode=cfg.dtype)
+        O.layer_backward(P, x, dout, C)
+        return time.perf_counter() - t0
+
+    for i in range(args.warmup):
+        dt = one(S)
+        while i == 0 and S > 8 and dt * args.steps > 180.0:
+            S //= 2
+            dt = one(S)
+    times = [one(S) for _ in range(args.steps)]
+    el = float(sum(times))
+    tps = S * args.steps / el
+    cores = blas_threads()
+    sample = f"{S} tokens of the {cfg.name} workload (full weights) per step, fwd+bwd fp64, {args.steps} steps in {el:.1f} s"
+    line = {"metric": METRIC, "value": tps, "unit": "tokens/s", "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1e3 * el / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, paper init)",
+            "impl": "reference",
+            "config": {"workload": workload_desc(cfg, T_loc), "sample_tokens_per_step": S},
+            "cpu_baseline": {"value": tps, "unit": "tokens/s", "cores": cores, "kind": "oracle", "sample": sample},
+            "e2e": {"value": tps, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
 
 
 # ----------------------------------------------------------------------------- main
@@ -231,26 +315,22 @@ def main():
 
     cfg = PRESETS[args.config]
     T_loc = args.tokens or cfg.T
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        # --gpus N without a launcher: re-run under torch.distributed.run, one process per GPU
+        argv = torchrun_argv(sys.argv[1:], args.gpus)
+        sys.stdout.flush()
+        os.execv(argv[0], argv)
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     G = max(world, 1)
+    if G != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
 
     if args.impl == "reference":
         if rank != 0:
             return
-        tps, el, done = oracle_tokens_per_s(cfg, args.cpu_sample, budget_s=20.0)
-        # each "step" is the bounded sample; report the oracle's throughput on it
-        line = {"metric": METRIC, "value": tps, "unit": "tokens/s", "n_gpus": args.gpus, "steps": args.steps,
-                "warmup": args.warmup, "ms_per_step": 1e3 * args.cpu_sample / tps, "higher_is_better": True,
-                "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-                "impl": "reference",
-                "config": {"workload": workload_desc(cfg, T_loc), "sample_tokens": args.cpu_sample},
-                "cpu_baseline": {"value": tps, "unit": "tokens/s", "cores": blas_threads(), "kind": "oracle",
-                                 "sample": f"{done} tokens of the {cfg.name} workload (full weights) fwd+bwd, "
-                                           f"{el:.1f} s"},
-                "e2e": {"value": tps, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-        print(json.dumps(line), flush=True)
+        run_reference(args, cfg, T_loc)
         return
 
     import torch
@@ -298,6 +378,8 @@ def main():
     time.sleep(0.3)
     C.mhl_set_step_timing(L.plan, True)
     launches0 = L.launches()
+    a2a0 = C.mhl_a2a_bytes_posted(L.plan)
+    nvl0 = nvlink_bytes(local_rank) if G > 1 else None
     if G > 1:
         dist.barrier()
     torch.cuda.synchronize(dev)
@@ -311,6 +393,16 @@ def main():
         dist.barrier()
     ms = ev0.elapsed_time(ev1)
     launches = L.launches() - launches0
+    a2a = (C.mhl_a2a_bytes_posted(L.plan) - a2a0) / args.steps
+    nvl1 = nvlink_bytes(local_rank) if G > 1 else None
+    nvlink = None
+    if G > 1:
+        nvlink = {"a2a_bytes_posted_per_step": a2a, "a2a_bytes_per_step_closed_form": 4 * L.info["a2a_bytes_per_rank"]
+                  if not cfg.routing_tokens else None}
+        if nvl0 and nvl1:
+            nvlink.update(tx_bytes_per_step=(nvl1[0] - nvl0[0]) / args.steps,
+                          rx_bytes_per_step=(nvl1[1] - nvl0[1]) / args.steps,
+                          tx_gbs=(nvl1[0] - nvl0[0]) / (ms / 1e3) / 1e9, source="NVML NVLINK_THROUGHPUT_DATA")
     steps_t = C.mhl_step_times(L.plan)
     C.mhl_set_step_timing(L.plan, False)
     clk = clocks.stop()
@@ -371,11 +463,24 @@ def main():
         tr = traffic.get(dom, {}).get("dram_bytes_per_launch") if cfg.name == traffic.get("_workload") else None
         bound, achieved, peak, unit, frac = span_roofline(w, dur_s, tf_peak, hbm_peak)
         roof = {"bound": bound, "achieved": achieved, "peak": peak, "unit": unit, "frac": frac, "traffic": tr,
+                "traffic_over_algorithmic": (tr / (w["bytes"] / max(calls, 1))) if tr else None,
+                "impl_bytes_per_launch": w["impl_bytes"] / max(calls, 1),
                 "algorithmic_bytes_per_launch": w["bytes"] / max(calls, 1),
                 "algorithmic_flops_per_launch": w["flops"] / max(calls, 1), "kernel": dom,
                 "launches_per_step": calls, "peak_source": tf_src if bound == "tensor" else hbm_src}
         roof["per_span_frac"] = {k: round(span_roofline(work[k], per_step[k] / 1e3, tf_peak, hbm_peak)[4], 3)
                                  for k in per_step if k in work and per_step[k] > 0}
+        roof["per_span_bound"] = {k: span_roofline(work[k], per_step[k] / 1e3, tf_peak, hbm_peak)[0]
+                                  for k in per_step if k in work and per_step[k] > 0}
+        # the expert contractions as one unit (F5 + the three B5 kernels): §8(d)'s expert_fwd +
+        # expert_bwd, 2 + 5 GEMM units, tensor-bound; north_star's ">= 60 % of tcgen05 peak" target
+        ek = [k for k in ("F5_expert_fwd", "B5_expert_bwd_dx", "B5_expert_dx_gemm", "B5_expert_bwd_dw")
+              if k in per_step]
+        if ek:
+            ef = sum(work[k]["flops"] for k in ek)
+            et = sum(per_step[k] for k in ek) / 1e3
+            roof["expert_kernels"] = {"flops": ef, "ms": et * 1e3, "tflops": ef / et / 1e12,
+                                      "frac_of_peak": ef / et / 1e12 / tf_peak}
     breakdown = {k: round(v, 4) for k, v in sorted(per_step.items(), key=lambda kv: -kv[1])}
     layer_tflops = total_flops(cfg, T_loc) / (ms_per_step / 1e3) / 1e12
 
@@ -397,7 +502,7 @@ def main():
             "layer_pct_tcgen05_peak": {"measured_burst": 100.0 * layer_tflops / tf_peak,
                                        "nominal_2250": 100.0 * layer_tflops / 2250.0},
             "roofline": roof, "step_breakdown_ms": breakdown, "cpu_baseline": cpu, "e2e": e2e,
-            "gpu_launches": int(launches), "clocks": clk}
+            "gpu_launches": int(launches), "clocks": clk, "nvlink": nvlink}
     print(json.dumps(line), flush=True)
     if G > 1:
         dist.destroy_process_group()

@@ -144,7 +144,9 @@ MHL_API mhl_status hp_plan_destroy(mhl_plan plan);
  *   F6 combine sum_j (Eq. 1) -> F7 all-to-all #2 -> F8 out = W_out concat  Eq. 6
  * x:   [T_loc, d] E  (LOOPBACK: [G*T_loc, d], the global batch, rank-major)
  * out: [T_loc, d] E  (LOOPBACK: [G*T_loc, d])
- * saved: saved_bytes, written here, read by mhlmoe_backward.
+ * saved: saved_bytes, written here, read by mhlmoe_backward.  It begins with Xs
+ *        [T_glob][H_loc*d_h] E (x2 columns with routing sub-tokens), the all-to-all #1
+ *        receive buffer (R12 layout), which callers may read (e.g. conformance tests).
  * topk_idx (nullable): [H_loc, T_glob, k] int32 expert ids, slot order = descending biased key.
  * gates    (nullable): [H_loc, T_glob, k] f32.  (LOOPBACK: [N_h, T_glob, k].)
  * Token order of T_glob is global: source rank-major (R12).
@@ -230,6 +232,26 @@ MHL_API mhl_status mhl_set_step_timing(mhl_plan plan, int enable);
  * a NULL plan. */
 MHL_API int32_t mhl_step_times(mhl_plan plan, char* names, size_t names_cap, double* ms, int32_t* calls,
                                int32_t max_steps);
+
+/* Which kernel implementation ran each step (bits OR-ed in at launch since the plan was
+ * created or last reset): lets callers and tests assert that a shape took the tcgen05
+ * path instead of the SIMT reference kernels, which shapes outside the tensor-core kernels'
+ * support (d_h, d_e, N_e) fall back to.  reset != 0 clears the bits after reading. */
+#define MHL_PATH_ROUTER_TC        (1u << 0)   /* F3 on tcgen05, N_e <= 128 (router_sm100.cu)       */
+#define MHL_PATH_ROUTER_BLK       (1u << 1)   /* F3 Alg. 1 multi-block on tcgen05 (router_blk)     */
+#define MHL_PATH_ROUTER_SIMT      (1u << 2)   /* F3 fp32 FMA reference kernel                      */
+#define MHL_PATH_EXPERT_FWD_TC    (1u << 3)   /* F5 tcgen05, one CTA per tile                      */
+#define MHL_PATH_EXPERT_FWD_PAIR  (1u << 4)   /* F5 tcgen05 cta_group::2                           */
+#define MHL_PATH_EXPERT_FWD_SIMT  (1u << 5)
+#define MHL_PATH_EXPERT_BWD_TC    (1u << 6)   /* B5 tcgen05 kernels                                */
+#define MHL_PATH_EXPERT_BWD_SIMT  (1u << 7)
+#define MHL_PATH_ROUTER_BWD_TC    (1u << 8)   /* B3 dW_r on tcgen05                                */
+#define MHL_PATH_ROUTER_BWD_SIMT  (1u << 9)
+#define MHL_PATH_PROJ_PINNED      (1u << 10)  /* F1/F8/B8/B1 on the plan's pinned GEMM algorithm   */
+#define MHL_PATH_FUSED_COMBINE    (1u << 11)  /* F6 inside the forward expert kernel               */
+#define MHL_PATH_A2A_NCCL         (1u << 12)  /* HP exchanges through NCCL send/recv               */
+#define MHL_PATH_A2A_LOOPBACK     (1u << 13)  /* HP exchanges as device copies (MHL_FLAG_LOOPBACK) */
+MHL_API uint32_t mhl_kernel_paths(mhl_plan plan, int reset);
 
 MHL_API const char* mhl_status_string(mhl_status s);
 MHL_API const char* mhl_last_error(void);

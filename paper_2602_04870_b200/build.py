@@ -76,7 +76,7 @@ def build(force: bool = False, verbose: bool = True) -> str:
     with cf.ThreadPoolExecutor(max_workers=max(1, min(8, os.cpu_count() or 1))) as ex:
         objs = list(ex.map(lambda s: _compile(s, force), CU_SOURCES + CXX_SOURCES))
     if force or not os.path.exists(LIB) or any(os.path.getmtime(o) > os.path.getmtime(LIB) for o in objs):
-        cmd = [NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-lcublas", "-ldl",
+        cmd = [NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-lcublasLt", "-ldl",
                "-Xlinker", f"-rpath={os.path.join(CUDA, 'lib64')}", "-cudart", "static"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:

@@ -10,6 +10,7 @@
 //   idx, gate   [H_loc][T_glob][k];  perm/pos [H_loc][T_glob*k];  Yrep/dXrep [H_loc][T_glob*k][d_h]
 #include "../../include/mhlmoe.h"
 
+#include <cublasLt.h>
 #include <cublas_v2.h>
 #include <cuda_runtime.h>
 #include <dlfcn.h>
@@ -40,13 +41,6 @@ mhl_status fail(mhl_status s, const std::string& msg) {
     cudaError_t e_ = (expr);                                                                      \
     if (e_ != cudaSuccess)                                                                        \
       return fail(MHL_ERR_CUDA, std::string(#expr) + ": " + cudaGetErrorString(e_));             \
-  } while (0)
-
-#define MHL_CUBLAS(expr)                                                                          \
-  do {                                                                                            \
-    cublasStatus_t e_ = (expr);                                                                   \
-    if (e_ != CUBLAS_STATUS_SUCCESS)                                                              \
-      return fail(MHL_ERR_CUDA, std::string(#expr) + ": cublas status " + std::to_string((int)e_)); \
   } while (0)
 
 #define MHL_TRY(expr)                 \
@@ -111,7 +105,6 @@ struct Dims {
   int XW;          // Xs row width per rank: HD, or 2*HD with routing tokens (r part at column HD)
   int Din;         // W_in rows: D, or 2*D with routing tokens
   int n_rt, max_tiles, max_chunks, seg_align, n_rbwd;
-  int dw_parts = mhl::kMaxDwParts;   // dW row parts per head (= dW grid), set from the SM count by hp_plan
 };
 
 struct Bump {
@@ -141,8 +134,8 @@ SavedLayout saved_layout(const Dims& m) {
   L.nchunks = b.take(16);
   L.cbase = b.take((size_t)m.H * m.N_e * 4);
   L.ccount = b.take((size_t)m.H * m.N_e * 4);
-  L.pbase = b.take((size_t)m.H * mhl::kMaxDwParts * 4);
-  L.pcount = b.take((size_t)m.H * mhl::kMaxDwParts * 4);
+  L.pbase = b.take((size_t)m.H * mhl::kDwParts * 4);
+  L.pcount = b.take((size_t)m.H * mhl::kDwParts * 4);
   L.load = b.take((size_t)m.H * m.N_e * 4);             // per-head expert loads of the step (F4)
   L.tilewin = b.take((size_t)m.max_tiles * 4);          // fused combine: window of each tile
   L.wtiles = b.take((size_t)m.H * mhl::kTileParts * 4); //   tiles per (head, part) window
@@ -228,11 +221,11 @@ mhl_status make_dims(const mhl_config* c, Dims* m) {
   // router-backward partials: one per router tile on the SIMT path, at most one per (SM / N_h) on
   // the tcgen05 path (launch: min(n_rt, #SMs / N_h) chunks per head)
   m->n_rbwd = (!m->simt && mhl::router_bwd_sm100_supported(m->d_h, m->N_e, m->k))
-                  ? std::min(m->n_rt, std::max(1, mhl::kMaxDwParts / m->N_h)) : m->n_rt;
+                  ? std::min(m->n_rt, std::max(1, mhl::kDwParts / m->N_h)) : m->n_rt;
   const int64_t mt = (int64_t)m->H * ((m->R + mhl::kExpertBM - 1) / mhl::kExpertBM + 2 * m->N_e);
   if (mt >= (int64_t)1 << 31) return fail(MHL_ERR_UNSUPPORTED, "too many tiles");
   m->max_tiles = (int)mt;
-  m->max_chunks = (int)((int64_t)m->H * (mhl::kMaxDwParts + m->N_e));   // <= parts + expert boundaries
+  m->max_chunks = (int)((int64_t)m->H * (mhl::kDwParts + m->N_e));   // <= parts + expert boundaries
   const size_t router_smem = (size_t)m->el * m->d_h * mhl::kRouterTile + 4ull * m->d_h * 32 + 4ull * m->N_e;
   const size_t rbwd_smem = 4ull * std::min<int64_t>((int64_t)m->N_e * m->d_h, 32768) + 8ull * mhl::kRouterTile * m->k;
   if (router_smem > 200 * 1024 || rbwd_smem > 200 * 1024)
@@ -253,6 +246,14 @@ void fill_info(const Dims& m, mhl_plan_info* info) {
   info->max_tiles = m.max_tiles;
 }
 
+struct LtKey {
+  bool ta, tb, c_f32, bf; int64_t N, K, Mkey;
+  bool operator==(const LtKey& o) const {
+    return ta == o.ta && tb == o.tb && c_f32 == o.c_f32 && bf == o.bf && N == o.N && K == o.K && Mkey == o.Mkey;
+  }
+};
+struct LtEntry { LtKey key; cublasLtMatmulAlgo_t algo; };
+
 }  // namespace
 
 // ------------------------------------------------------------------------------------------
@@ -262,9 +263,10 @@ struct mhl_plan_s {
   mhl_config cfg;
   Dims m;
   mhl_plan_info info;
-  cublasHandle_t blas = nullptr;
+  cublasLtHandle_t lt = nullptr;
   void* blas_ws = nullptr;
   size_t blas_ws_bytes = 32u << 20;
+  std::vector<LtEntry> lt_algos;   // pinned projection-GEMM algorithms (Gemm)
   ncclComm_t comm = nullptr;
   int32_t* dflag = nullptr;   // device non-finite flag
   cudaError_t launch_err = cudaSuccess;   // first launch error harvested by a StepSpan
@@ -281,6 +283,7 @@ struct mhl_plan_s {
   cudaStream_t comm_stream = nullptr;
   cudaEvent_t ev_prod = nullptr, ev_comm = nullptr;
   std::atomic<uint64_t> launches{0};
+  std::atomic<uint32_t> paths{0};     // MHL_PATH_* bits of the kernels launched (mhl_kernel_paths)
   uint64_t a2a_bytes_posted = 0;
   // optional per-step CUDA-event timing (mhl_set_step_timing)
   bool timing = false;
@@ -322,29 +325,104 @@ struct StepSpan {
 };
 #define MHL_SPAN(name) StepSpan span_##__LINE__(p, name, s)
 
+// Projection GEMMs (F1, F8, B8, B1: Eq. 5, Eq. 6 P:772 and their chain rule) on cuBLASLt
+// with a PINNED algorithm: for each (op, N, K, types) the algorithm is chosen once,
+// from the heuristic at a fixed reference M (kRefM, independent of the plan's T_loc and of G), with
+// split-K disabled (one sequential K loop per output tile), and then reused for every M.  Every
+// output row is therefore computed by the same tile program with the same K order whatever M is,
+// which is what makes out / dx bitwise independent of T_loc and so of the HP degree (§8(e)); the
+// weight-gradient GEMMs (K = tokens) are pinned per shape, so they are run-to-run deterministic.
+constexpr int64_t kRefM = 65536;
+
+// cuBLASLt is column-major: row-major C[M,N] = op(A) op(B) is computed as C^T[N,M] = op(B)^T op(A)^T.
+struct LtShape {
+  cublasLtMatmulDesc_t op = nullptr;
+  cublasLtMatrixLayout_t a = nullptr, b = nullptr, c = nullptr;
+  ~LtShape() {
+    if (op) cublasLtMatmulDescDestroy(op);
+    if (a) cublasLtMatrixLayoutDestroy(a);
+    if (b) cublasLtMatrixLayoutDestroy(b);
+    if (c) cublasLtMatrixLayoutDestroy(c);
+  }
+  bool make(bool ta, bool tb, int64_t M, int64_t N, int64_t K, int64_t lda, int64_t ldb, int64_t ldc, bool c_f32,
+            bool bf) {
+    const cudaDataType_t ab = bf ? CUDA_R_16BF : CUDA_R_32F;
+    const cudaDataType_t ct = c_f32 ? CUDA_R_32F : ab;
+    const cublasComputeType_t comp = bf ? CUBLAS_COMPUTE_32F : CUBLAS_COMPUTE_32F_PEDANTIC;
+    if (cublasLtMatmulDescCreate(&op, comp, CUDA_R_32F) != CUBLAS_STATUS_SUCCESS) return false;
+    const cublasOperation_t opB = tb ? CUBLAS_OP_T : CUBLAS_OP_N, opA = ta ? CUBLAS_OP_T : CUBLAS_OP_N;
+    // column-major "A" operand of cuBLAS = our B (N x K view), "B" operand = our A
+    cublasLtMatmulDescSetAttribute(op, CUBLASLT_MATMUL_DESC_TRANSA, &opB, sizeof(opB));
+    cublasLtMatmulDescSetAttribute(op, CUBLASLT_MATMUL_DESC_TRANSB, &opA, sizeof(opA));
+    // stored shapes (column-major rows x cols): B^T-view is (tb ? K x N : N x K), A-view (ta ? M x K : K x M)
+    if (cublasLtMatrixLayoutCreate(&a, ab, tb ? K : N, tb ? N : K, ldb) != CUBLAS_STATUS_SUCCESS) return false;
+    if (cublasLtMatrixLayoutCreate(&b, ab, ta ? M : K, ta ? K : M, lda) != CUBLAS_STATUS_SUCCESS) return false;
+    if (cublasLtMatrixLayoutCreate(&c, ct, N, M, ldc) != CUBLAS_STATUS_SUCCESS) return false;
+    return true;
+  }
+};
+
 struct Gemm {
   mhl_plan p;
   cudaStream_t s;
   // Row-major C[M,N] = alpha * op(A) op(B) + beta C; A is [M,K] (ta: stored [K,M]),
-  // B is [K,N] (tb: stored [N,K]).  Column-major cuBLAS computes C^T = op(B)^T op(A)^T.
+  // B is [K,N] (tb: stored [N,K]).
   mhl_status operator()(bool ta, bool tb, int64_t M, int64_t N, int64_t K, const void* A, int64_t lda,
-                        const void* B, int64_t ldb, void* C, int64_t ldc, bool c_f32, float beta) const {
-    const float alpha = 1.0f;
-    const bool bf = p->m.dtype == MHL_BF16;
-    const cudaDataType_t ab = bf ? CUDA_R_16BF : CUDA_R_32F;
-    const cudaDataType_t ct = c_f32 ? CUDA_R_32F : ab;
-    const cublasComputeType_t comp = bf ? CUBLAS_COMPUTE_32F : CUBLAS_COMPUTE_32F_PEDANTIC;
-    MHL_CUBLAS(cublasSetStream(p->blas, s));
-    MHL_CUBLAS(cublasGemmEx(p->blas, tb ? CUBLAS_OP_T : CUBLAS_OP_N, ta ? CUBLAS_OP_T : CUBLAS_OP_N, (int)N,
-                            (int)M, (int)K, &alpha, B, ab, (int)ldb, A, ab, (int)lda, &beta, C, ct, (int)ldc, comp,
-                            CUBLAS_GEMM_DEFAULT));
-    p->launches++;
-    return MHL_OK;
-  }
+                        const void* B, int64_t ldb, void* C, int64_t ldc, bool c_f32, float beta) const;
 };
 
 inline char* at(void* base, size_t off) { return static_cast<char*>(base) + off; }
 inline const char* at(const void* base, size_t off) { return static_cast<const char*>(base) + off; }
+
+mhl_status Gemm::operator()(bool ta, bool tb, int64_t M, int64_t N, int64_t K, const void* A, int64_t lda,
+                            const void* B, int64_t ldb, void* C, int64_t ldc, bool c_f32, float beta) const {
+  if (M == 0 || N == 0) return MHL_OK;
+  const bool bf = p->m.dtype == MHL_BF16;
+  // per-row GEMMs (fprop / dgrad: K fixed by the weights) are pinned at the reference M, the
+  // weight-gradient GEMMs (ta: M, N fixed by the weights, K = tokens) per actual shape
+  const LtKey key{ta, tb, c_f32, bf, N, K, ta ? M : kRefM};
+  const cublasLtMatmulAlgo_t* algo = nullptr;
+  for (const LtEntry& e : p->lt_algos)
+    if (e.key == key) { algo = &e.algo; break; }
+  if (!algo) {
+    const int64_t Mh = key.Mkey;
+    LtShape h;
+    if (!h.make(ta, tb, Mh, N, K, ta ? Mh : K, tb ? K : N, N, c_f32, bf))
+      return fail(MHL_ERR_CUDA, "cublasLt descriptor creation failed");
+    cublasLtMatmulPreference_t pref;
+    if (cublasLtMatmulPreferenceCreate(&pref) != CUBLAS_STATUS_SUCCESS) return fail(MHL_ERR_CUDA, "cublasLt preference");
+    size_t wsb = p->blas_ws_bytes;
+    cublasLtMatmulPreferenceSetAttribute(pref, CUBLASLT_MATMUL_PREF_MAX_WORKSPACE_BYTES, &wsb, sizeof(wsb));
+    // per-row GEMMs: no split-K at all (one sequential K loop per output tile); wgrad: any
+    // reduction scheme cuBLASLt runs deterministically (fixed partition, no atomics)
+    const uint32_t mask = ta ? (uint32_t)CUBLASLT_REDUCTION_SCHEME_MASK : (uint32_t)CUBLASLT_REDUCTION_SCHEME_NONE;
+    cublasLtMatmulPreferenceSetAttribute(pref, CUBLASLT_MATMUL_PREF_REDUCTION_SCHEME_MASK, &mask, sizeof(mask));
+    cublasLtMatmulHeuristicResult_t res[8];
+    int n = 0;
+    const cublasStatus_t st = cublasLtMatmulAlgoGetHeuristic(p->lt, h.op, h.a, h.b, h.c, h.c, pref, 8, res, &n);
+    cublasLtMatmulPreferenceDestroy(pref);
+    if (st != CUBLAS_STATUS_SUCCESS || n == 0) return fail(MHL_ERR_CUDA, "cublasLt: no algorithm for a projection GEMM");
+    LtEntry e{key, res[0].algo};
+    if (!ta) {
+      const int32_t one = 1;
+      const uint32_t none = CUBLASLT_REDUCTION_SCHEME_NONE;
+      cublasLtMatmulAlgoConfigSetAttribute(&e.algo, CUBLASLT_ALGO_CONFIG_SPLITK_NUM, &one, sizeof(one));
+      cublasLtMatmulAlgoConfigSetAttribute(&e.algo, CUBLASLT_ALGO_CONFIG_REDUCTION_SCHEME, &none, sizeof(none));
+    }
+    p->lt_algos.push_back(e);
+    algo = &p->lt_algos.back().algo;
+  }
+  LtShape sh;
+  if (!sh.make(ta, tb, M, N, K, lda, ldb, ldc, c_f32, bf)) return fail(MHL_ERR_CUDA, "cublasLt descriptor creation failed");
+  const float alpha = 1.0f;
+  const cublasStatus_t st = cublasLtMatmul(p->lt, sh.op, &alpha, B, sh.a, A, sh.b, &beta, C, sh.c, C, sh.c, algo,
+                                           p->blas_ws, p->blas_ws_bytes, s);
+  if (st != CUBLAS_STATUS_SUCCESS)
+    return fail(MHL_ERR_CUDA, "cublasLtMatmul (pinned algorithm) status " + std::to_string((int)st));
+  p->launches++;
+  p->paths |= MHL_PATH_PROJ_PINNED;
+  return MHL_OK;
+}
 
 // Equal-split all-to-all (P:805-P:806), pipelined with its producer.  Step
 // i = 0..G-1 sends the block rank r addresses to q = (r+i) mod G and receives the block of
@@ -391,6 +469,7 @@ mhl_status hp_exchange(mhl_plan p, const Xfer& X, cudaStream_t s, Produce produc
         else
           MHL_CUDA(cudaMemcpyAsync(X.recv[q] + v * blk, X.send[v] + q * blk, blk, cudaMemcpyDeviceToDevice, cs));
         p->a2a_bytes_posted += blk;
+        p->paths |= MHL_PATH_A2A_LOOPBACK;
         if (!X.place.empty()) p->launches += X.parts;
       }
     } else {
@@ -401,6 +480,7 @@ mhl_status hp_exchange(mhl_plan p, const Xfer& X, cudaStream_t s, Produce produc
       MHL_NCCL(api.Recv(X.recv[0] + src * blk, blk, ncclUint8, src, p->comm, cs));
       MHL_NCCL(api.GroupEnd());
       p->a2a_bytes_posted += blk;
+      p->paths |= MHL_PATH_A2A_NCCL;
       p->launches++;
       if (!X.place.empty()) {
         for (int pi = 0; pi < X.parts; ++pi)
@@ -450,7 +530,7 @@ mhl::Routing routing_view(const Dims& m, const char* saved) {
   rt.ccount = (const int32_t*)(saved + S.ccount);
   rt.pbase = (const int32_t*)(saved + S.pbase);
   rt.pcount = (const int32_t*)(saved + S.pcount);
-  rt.dw_parts = m.dw_parts;
+  rt.dw_parts = mhl::kDwParts;
   return rt;
 }
 
@@ -510,14 +590,17 @@ mhl_status moe_forward_local(mhl_plan p, const RankPtrs& R, void* yout, cudaStre
       if (!mhl::launch_router_sm100(Xr, m.XW, R.W_r, R.bias, m.H, m.T_g, m.d_h, m.N_e, m.k, R.ws + F.planes, idx, gate,
                                     hist, p->dflag, p->num_sms, s))
         return fail(MHL_ERR_CUDA, "router: TMA tensor-map encoding failed");
+      p->paths |= MHL_PATH_ROUTER_TC;
     } else if (!m.simt && mhl::router_blk_supported(m.d_h, m.N_e, m.k)) {
       mhl::launch_router_split(R.W_r, R.ws + F.planes, m.H, m.d_h, m.N_e, s);
       if (!mhl::launch_router_blk_sm100(Xr, m.XW, R.ws + F.planes, R.bias, m.H, m.T_g, m.d_h, m.N_e, m.k, idx, gate,
                                         hist, p->dflag, p->num_sms, s))
         return fail(MHL_ERR_CUDA, "router (blocked): TMA tensor-map encoding failed");
+      p->paths |= MHL_PATH_ROUTER_BLK;
     } else {
       mhl::launch_router_topk(m.dtype, Xr, m.XW, R.W_r, R.bias, m.H, m.T_g, m.d_h, m.N_e, m.k, idx, gate, hist,
                               p->dflag, s);
+      p->paths |= MHL_PATH_ROUTER_SIMT;
     }
   }
   {
@@ -545,9 +628,11 @@ mhl_status moe_forward_local(mhl_plan p, const RankPtrs& R, void* yout, cudaStre
     // CTA-pair (cta_group::2) kernels with MHL_FLAG_PAIR (segments padded to tile pairs)
     if (m.simt || !mhl::expert_fwd_sm100_supported(m.d_h, m.d_e)) {
       mhl::launch_expert_fwd_simt(m.dtype, rt, Xs, m.XW, R.W1, R.W2, m.d_h, m.d_e, Yrep, s);
+      p->paths |= MHL_PATH_EXPERT_FWD_SIMT;
     } else if (m.pair && mhl::expert_fwd_pair_supported(m.d_h, m.d_e) && p->num_sms >= 2) {
       if (!mhl::launch_expert_fwd_pair_sm100(rt, Xs, m.XW, R.W1, R.W2, m.d_h, m.d_e, Yrep, p->num_sms, s))
         return fail(MHL_ERR_CUDA, "expert_fwd (pair): TMA tensor-map encoding failed");
+      p->paths |= MHL_PATH_EXPERT_FWD_PAIR;
     } else {
       mhl::FwdCombine fc;
       if (fuse) {
@@ -559,6 +644,7 @@ mhl_status moe_forward_local(mhl_plan p, const RankPtrs& R, void* yout, cudaStre
       }
       if (!mhl::launch_expert_fwd_sm100(rt, Xs, m.XW, R.W1, R.W2, m.d_h, m.d_e, Yrep, p->num_sms, s, fc))
         return fail(MHL_ERR_CUDA, "expert_fwd: TMA tensor-map encoding failed");
+      p->paths |= MHL_PATH_EXPERT_FWD_TC | (fuse ? MHL_PATH_FUSED_COMBINE : 0u);
     }
   }
   if (yout && !fuse) {
@@ -589,6 +675,7 @@ mhl_status moe_backward_local(mhl_plan p, const RankPtrs& R, const void* dY, voi
   void* dH = R.ws + B.dH;
   void* gA = R.ws + B.gA;
   const bool tc = !m.simt && mhl::expert_bwd_sm100_supported(m.d_h, m.d_e);
+  p->paths |= tc ? MHL_PATH_EXPERT_BWD_TC : MHL_PATH_EXPERT_BWD_SIMT;
   // the all-zero row T of dY (padding rows of every expert tile gather it)
   MHL_CUDA(cudaMemsetAsync(static_cast<char*>(const_cast<void*>(dY)) + (size_t)m.T_g * m.HD * m.el, 0,
                            (size_t)m.HD * m.el, s));
@@ -607,12 +694,15 @@ mhl_status moe_backward_local(mhl_plan p, const RankPtrs& R, const void* dY, voi
     if (!m.simt && m.T_g > 0 && mhl::router_bwd_sm100_supported(m.d_h, m.N_e, m.k)) {
       if (!mhl::launch_router_bwd_sm100(Xr, m.XW, idx, gate, dg, m.H, m.T_g, m.k, m.d_h, m.N_e, dS,
                                         (float*)(R.ws + B.dwr_part),
-                                        // token chunks per head from the GLOBAL head count, so the
-                                        // partial-sum order (and dW_r bits) do not depend on G
-                                        std::min(m.n_rbwd, std::max(1, std::min(p->num_sms, mhl::kMaxDwParts) / m.N_h)),
+                                        // token chunks per head from T and the GLOBAL head count only,
+                                        // so the partial-sum order (dW_r bits) depends neither on G
+                                        // nor on the device's SM count
+                                        m.n_rbwd,
                                         R.dW_r, s))
         return fail(MHL_ERR_CUDA, "router backward: TMA tensor-map encoding failed");
+      p->paths |= MHL_PATH_ROUTER_BWD_TC;
     } else {
+      p->paths |= MHL_PATH_ROUTER_BWD_SIMT;
       mhl::launch_router_bwd(m.dtype, Xr, m.XW, idx, gate, dg, m.H, m.T_g, m.k, m.d_h, m.N_e, dS,
                              (float*)(R.ws + B.dwr_part), R.dW_r, s);
     }
@@ -732,11 +822,8 @@ mhl_status hp_plan(const mhl_config* cfg, const uint8_t* nccl_id, mhl_plan* out)
   if (cudaGetDeviceProperties(&prop, dev) != cudaSuccess) return cleanup(fail(MHL_ERR_CUDA, "cudaGetDeviceProperties"));
   if (prop.major != 10) return cleanup(fail(MHL_ERR_UNSUPPORTED, "this library is built for sm_100a (B200)"));
   p->num_sms = prop.multiProcessorCount;
-  p->m.dw_parts = std::max(1, std::min(p->num_sms, mhl::kMaxDwParts));
-  if (cublasCreate(&p->blas) != CUBLAS_STATUS_SUCCESS) return cleanup(fail(MHL_ERR_CUDA, "cublasCreate"));
+  if (cublasLtCreate(&p->lt) != CUBLAS_STATUS_SUCCESS) return cleanup(fail(MHL_ERR_CUDA, "cublasLtCreate"));
   if (cudaMalloc(&p->blas_ws, p->blas_ws_bytes) != cudaSuccess) return cleanup(fail(MHL_ERR_CUDA, "cudaMalloc"));
-  if (cublasSetWorkspace(p->blas, p->blas_ws, p->blas_ws_bytes) != CUBLAS_STATUS_SUCCESS)
-    return cleanup(fail(MHL_ERR_CUDA, "cublasSetWorkspace"));
   if (cudaMalloc(&p->dflag, 16) != cudaSuccess || cudaMemset(p->dflag, 0, 16) != cudaSuccess)
     return cleanup(fail(MHL_ERR_CUDA, "cudaMalloc flag"));
   if (m.G > 1) {
@@ -766,7 +853,7 @@ mhl_status hp_plan_info(mhl_plan p, mhl_plan_info* info) {
 mhl_status hp_plan_destroy(mhl_plan p) {
   if (!p) return MHL_OK;
   if (p->comm && nccl().CommDestroy) nccl().CommDestroy(p->comm);
-  if (p->blas) cublasDestroy(p->blas);
+  if (p->lt) cublasLtDestroy(p->lt);
   if (p->blas_ws) cudaFree(p->blas_ws);
   if (p->dflag) cudaFree(p->dflag);
   for (int i = 0; i < 2; ++i)
@@ -1110,6 +1197,11 @@ int32_t mhl_step_times(mhl_plan p, char* names, size_t names_cap, double* ms, in
 }
 
 uint64_t mhl_a2a_bytes_posted(mhl_plan p) { return p ? p->a2a_bytes_posted : 0; }
+
+uint32_t mhl_kernel_paths(mhl_plan p, int reset) {
+  if (!p) return 0;
+  return reset ? p->paths.exchange(0u) : p->paths.load();
+}
 
 const char* mhl_status_string(mhl_status s) {
   switch (s) {

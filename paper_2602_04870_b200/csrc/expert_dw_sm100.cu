@@ -271,7 +271,7 @@ bool launch_dw_t(const Routing& rt, const void* Xs, int64_t ldx, const void* dY,
   auto kern = expert_dw_kernel<DH, DE>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, DwSmem<DH, DE>::BYTES);
   cudaMemsetAsync(done, 0, (size_t)rt.H * rt.N_e * sizeof(int), s);
-  (void)num_sms;   // one CTA per dW row part (rt.dw_parts = min(#SMs, kMaxDwParts))
+  (void)num_sms;   // one CTA per dW row part (rt.dw_parts = kDwParts, a constant: bits independent of the device)
   kern<<<rt.dw_parts, kDwThreads, DwSmem<DH, DE>::BYTES, s>>>(xm, ym, hm, am, rt, partial, done, dW1, dW2);
   return true;
 }

@@ -11,7 +11,10 @@ constexpr int kExpertBM = 128;     // replica rows per expert tile (tcgen05 M)
 // Expert segments are padded to a multiple of Routing::seg_align rows: one tile (128, default) or a
 // tile pair (256, MHL_FLAG_PAIR), which the cta_group::2 kernels need (tiles 2u, 2u+1 share an expert).
 constexpr int kDwStep = 64;        // sorted rows per dW pipeline step (dW chunk boundaries align to it)
-constexpr int kMaxDwParts = 160;   // dW row parts per head (= the dW grid, min(#SMs, this))
+// dW row parts per head (= the dW grid).  A constant of the decomposition, NOT the device's SM count:
+// part boundaries fix the order of the dW partial sums, so dW1/dW2 bits must not depend on the device
+// (§8(e)).  148 = one part per B200 SM; a device with fewer SMs runs the grid in waves, same bits.
+constexpr int kDwParts = 148;
 #ifndef MHL_TILE_GROUP
 #define MHL_TILE_GROUP 8
 #endif

@@ -65,11 +65,24 @@ class MHLatentMoE:
         C.mhlmoe_backward(self.plan, x, W, d_out, self.saved, dx, grads, self.workspace, stream)
         return dx
 
+    def saved_xs(self):
+        """The forward's sub-tokens as the GPU stored them: `saved` begins with Xs [T_glob][XW] E
+        (the all-to-all #1 receive buffer, include/mhlmoe.h), XW = H_loc*d_h (x2 with routing
+        sub-tokens).  Test access, G = 1 or one rank."""
+        XW = self.H_loc * self.d_h * (2 if self.routing_tokens else 1)
+        td = torch_dtype(self.dtype)
+        n = self.T_glob * XW
+        return self.saved[: n * torch.tensor([], dtype=td).element_size()].view(td).view(self.T_glob, XW)
+
     def check_status(self):
         C.mhl_check_device_status(self.plan)
 
     def launches(self):
         return C.mhl_launch_count(self.plan)
+
+    def paths(self, reset=False):
+        """Kernel implementations that ran (mhl_kernel_paths)."""
+        return C.mhl_kernel_paths(self.plan, reset)
 
 
 def weights_to_device(W: dict, dtype: str, device="cuda", heads=None) -> dict:

@@ -22,8 +22,13 @@ EXPORTS = ["hp_plan_query", "mhl_get_unique_id", "hp_plan", "hp_plan_info", "hp_
            "mhlmoe_backward", "mhlmoe_train_step_host", "mhlmoe_train_step_host_pipelined", "mhl_host_drain",
            "mhlmoe_update_bias", "mhl_check_device_status",
            "mhl_launch_count",
-           "mhl_a2a_bytes_posted", "mhl_set_step_timing", "mhl_step_times", "mhl_status_string",
-           "mhl_last_error"]
+           "mhl_a2a_bytes_posted", "mhl_set_step_timing", "mhl_step_times", "mhl_kernel_paths",
+           "mhl_status_string", "mhl_last_error"]
+# mhl_kernel_paths bits (include/mhlmoe.h MHL_PATH_*)
+PATHS = {"router_tc": 1 << 0, "router_blk": 1 << 1, "router_simt": 1 << 2, "expert_fwd_tc": 1 << 3,
+         "expert_fwd_pair": 1 << 4, "expert_fwd_simt": 1 << 5, "expert_bwd_tc": 1 << 6, "expert_bwd_simt": 1 << 7,
+         "router_bwd_tc": 1 << 8, "router_bwd_simt": 1 << 9, "proj_pinned": 1 << 10, "fused_combine": 1 << 11,
+         "a2a_nccl": 1 << 12, "a2a_loopback": 1 << 13}
 
 
 class MhlError(RuntimeError):
@@ -83,6 +88,7 @@ def _load():
         "mhl_set_step_timing": (I, [P, I]),
         "mhl_step_times": (ctypes.c_int32, [P, ctypes.c_char_p, ctypes.c_size_t, ctypes.POINTER(ctypes.c_double),
                                             ctypes.POINTER(ctypes.c_int32), ctypes.c_int32]),
+        "mhl_kernel_paths": (ctypes.c_uint32, [P, I]),
         "mhl_status_string": (ctypes.c_char_p, [I]),
         "mhl_last_error": (ctypes.c_char_p, []),
     }
@@ -239,6 +245,13 @@ def mhl_step_times(plan: Plan) -> dict:
         raise MhlError(1, "mhl_step_times", "NULL plan")
     keys = [k for k in names.value.decode().split(",") if k]
     return {k: (ms[i], calls[i]) for i, k in enumerate(keys)}
+
+
+def mhl_kernel_paths(plan: Plan, reset: bool = False) -> set:
+    """Names (PATHS keys) of the kernel implementations launched since the plan was created or
+    last reset."""
+    bits = int(_lib.mhl_kernel_paths(plan.handle, int(bool(reset))))
+    return {k for k, b in PATHS.items() if bits & b}
 
 
 def mhl_status_string(s: int) -> str:

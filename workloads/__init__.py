@@ -13,6 +13,14 @@ Value distributions:
   paper  the paper's init (P:1995-P:1996): all weights N(0, 0.02^2), output
          projections (W_out, W2) further x 1/sqrt(2L), L = 12 (R18); b = 0
   skew   as paper, plus b[h,e] = -s * sigma_S * ln(1+e)   (expert-load imbalance)
+  exact  as conf, but every sub-token is EXACT in fp32 whatever the summation order: W_in has
+         EXACT_NNZ = 8 nonzeros per row, each +-2^-j (j in {1,2,3}), and x is bf16 with
+         |x| >= 2^-6 (smaller values flushed to 0).  Every product is then a multiple of 2^-16
+         below 2^3 in magnitude and every partial sum of a row a multiple of 2^-16 below 2^7,
+         i.e. representable in fp32's 24-bit significand, so the GPU's fp32-accumulated Xs is the
+         exact value and rounds to bf16 exactly as the oracle's fp64 value does (no R22 budget:
+         the router sees identical sub-tokens on both sides and north_star's margin rule applies
+         as stated).
 """
 from __future__ import annotations
 
@@ -85,19 +93,46 @@ def _normal(seed, tid, shape, std, extra=()):
     return a
 
 
+EXACT_NNZ = 8
+
+
+def _sparse_pow2(seed, tid, shape):
+    """EXACT_NNZ nonzeros per row at distinct random columns, values +-2^-j, j uniform in {1,2,3}."""
+    rng = _rng(seed, tid)
+    rows, cols = shape
+    nnz = min(EXACT_NNZ, cols)
+    a = np.zeros(shape, np.float32)
+    for r in range(rows):
+        c = rng.choice(cols, nnz, replace=False)
+        a[r, c] = rng.choice([-1.0, 1.0], nnz) * np.exp2(-rng.integers(1, 4, nnz).astype(np.float32))
+    return a
+
+
+def quantize_exact_tokens(a: np.ndarray) -> np.ndarray:
+    """bf16 values with |x| >= 2^-6 (smaller ones flushed to 0): the token side of `exact`."""
+    q = to_bf16_exact(a)
+    q[np.abs(q) < 2.0 ** -6] = 0.0
+    return q
+
+
 def make_weights(cfg: LayerConfig, seed: int = 0, dist: str = "conf", skew: float = 0.0) -> dict:
     """Layer parameters as float32 arrays (bf16-exact where stored in bf16)."""
     d, D, N_h, d_h, N_e, d_e = cfg.d, cfg.D, cfg.N_h, cfg.d_h, cfg.N_e, cfg.d_e
     if dist == "conf":
         std = dict(W_in=1 / math.sqrt(d), W_r=1 / math.sqrt(d_h), W1=1 / math.sqrt(d_h),
                    W2=1 / math.sqrt(d_e), W_out=1 / math.sqrt(D), b=0.1)
+    elif dist == "exact":
+        std = dict(W_in=None, W_r=1 / math.sqrt(d_h), W1=1 / math.sqrt(d_h),
+                   W2=1 / math.sqrt(d_e), W_out=1 / math.sqrt(D), b=0.1)
     elif dist in ("paper", "skew"):
         o = 0.02 / math.sqrt(2 * 12)
         std = dict(W_in=0.02, W_r=0.02, W1=0.02, W2=o, W_out=o, b=0.0)
     else:
         raise ValueError(dist)
+    rows_in = (2 if cfg.routing_tokens else 1) * D
     W = dict(
-        W_in=_normal(seed, TID["W_in"], ((2 if cfg.routing_tokens else 1) * D, d), std["W_in"]),
+        W_in=(_sparse_pow2(seed, TID["W_in"], (rows_in, d)) if dist == "exact"
+              else _normal(seed, TID["W_in"], (rows_in, d), std["W_in"])),
         W_out=_normal(seed, TID["W_out"], (d, D), std["W_out"]),
         W_r=_normal(seed, TID["W_r"], (N_h, d_h, N_e), std["W_r"]),
         W1=_normal(seed, TID["W1"], (N_h, N_e, d_e, d_h), std["W1"]),
@@ -127,5 +162,7 @@ def make_problem(cfg: LayerConfig, seed: int = 0, dist: str = "conf", T: int | N
     """(weights, x, dout) of the global problem."""
     W = make_weights(cfg, seed, dist, skew)
     x = make_tokens(cfg, seed, T, which="x")
+    if dist == "exact":
+        x = quantize_exact_tokens(x)
     dout = make_tokens(cfg, seed, T, which="dout")
     return W, x, dout
