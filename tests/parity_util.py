@@ -14,11 +14,12 @@ TOL = {"bf16": 2e-2, "fp32": 1e-4}
 GATE_TOL = 1e-5
 # R22: bound on |fp32-accumulated GEMM element - exact value|, as a multiple of
 # 2^-24 * sqrt(K) * ||x_t o W_in[i]||_2 (the rounding-error scale of a K-term fp32 sum whose
-# rounding points see partial sums of size ~sqrt(m) * rms(product)): about 10 standard
-# deviations of the error of a tensor-core accumulation in K-blocks of 16, 2.5 of a purely
-# sequential one.  test_gpu_parity.test_xs_rounding_within_r22_bound checks on the GPU that
-# every element outside this band rounds exactly as the oracle's.
-FP32_ACC_SCALE = 1.0
+# rounding points see partial sums of size ~sqrt(m) * rms(product)).  Calibrated on the B200
+# (test_gpu_parity.test_xs_rounding_within_r22_bound, K = 2048, 1M elements): the pinned F1 GEMM's
+# sub-tokens that round differently from the oracle's all lie within 2.74 units of a midpoint
+# (99 % within 1.15); the band takes 4 units.  That test checks on every GPU run that every
+# element outside the band rounds exactly as the oracle's.
+FP32_ACC_SCALE = 4.0
 
 
 def rel_err(gpu, ref) -> float:
@@ -51,21 +52,24 @@ def rel_err_slices(gpu, ref, keep_axes) -> float:
 SLICES = {"out": (0,), "dx": (0,), "dW1": (0, 1), "dW2": (0, 1), "dW_r": (0, 2), "dW_in": (0,), "dW_out": (0,)}
 
 
+def xs_band_ratio(x, W_in, Xs_pre) -> np.ndarray:
+    """Per element: distance of the exact value to the nearest bf16 rounding midpoint, in units of
+    2^-24 * sqrt(K) * ||x_t o W_in[i]||_2 (an element is ambiguous iff this is <= FP32_ACC_SCALE)."""
+    x = np.asarray(x, np.float64)
+    W = np.asarray(W_in, np.float64)
+    unit = 2.0 ** -24 * np.sqrt(x.shape[1]) * np.sqrt((x * x) @ (W * W).T)
+    m, e = np.frexp(Xs_pre)
+    ulp = np.ldexp(1.0, e - 8)
+    q = m * 256.0
+    return np.abs((q - np.floor(q)) - 0.5) * ulp / unit
+
+
 def xs_ambiguous(x, W_in, Xs_pre, mode) -> np.ndarray:
     """R22: boolean mask of the Xs elements whose exact value lies within the fp32-accumulation
     error bound of a bf16 rounding midpoint (the GPU may legitimately round them the other way)."""
     if mode != "bf16":
         return np.zeros(Xs_pre.shape, bool)
-    x = np.asarray(x, np.float64)
-    W = np.asarray(W_in, np.float64)
-    K = x.shape[1]
-    scale = np.sqrt((x * x) @ (W * W).T)                          # ||x_t o W_in[i]||_2
-    delta = FP32_ACC_SCALE * 2.0 ** -24 * np.sqrt(K) * scale
-    m, e = np.frexp(Xs_pre)
-    ulp = np.ldexp(1.0, e - 8)
-    q = m * 256.0
-    dist = np.abs((q - np.floor(q)) - 0.5) * ulp                   # distance to the nearest rounding midpoint
-    return dist <= delta
+    return xs_band_ratio(x, W_in, Xs_pre) <= FP32_ACC_SCALE
 
 
 def boundary_flip_budget(amb: np.ndarray, Xs_pre: np.ndarray, W_r_h: np.ndarray) -> np.ndarray:
@@ -140,8 +144,11 @@ def check_routing(P, C, gpu_idx, k, x=None, margin_thr=MARGIN, exact=False) -> R
         in_tie = K[rows, gi] >= (kth - max(margin_thr, MARGIN) - 2 * budget)[:, None]
         assert np.all(in_tie), f"head {h}: a GPU selection is outside the oracle's near-tie set"
         out.forced[h] = gi
-    assert out.n_excl <= max(2 * out.n_margin, out.n_margin + 0.005 * out.n), \
-        f"R22 budget excludes too many sub-tokens: {out.n_excl} vs {out.n_margin} by the margin rule alone of {out.n}"
+    if exact:
+        assert out.n_excl == out.n_margin
+    else:   # R22 widens the exclusion; bound it (SURVEY 8(d) expects 0.3-4.5 % by the margin rule alone)
+        assert out.n_excl <= max(4 * out.n_margin, out.n_margin + 0.02 * out.n), \
+            f"R22 budget excludes too many sub-tokens: {out.n_excl} vs {out.n_margin} by the margin rule alone of {out.n}"
     return out
 
 

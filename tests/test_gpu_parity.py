@@ -9,6 +9,7 @@ torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
 
 import oracle as O  # noqa: E402
+import oracle.mhlmoe_oracle as OM  # noqa: E402  (per-head backward, for sampled full-size dW slices)
 from parity_util import (SLICES, TOL, check_gates, check_routing, rel_err, rel_err_slices,  # noqa: E402
                          routing_slice, xs_ambiguous)
 from workloads import PRESETS, LayerConfig, make_problem  # noqa: E402
@@ -86,12 +87,13 @@ def test_tiny_fp32_fwd_bwd_matches_oracle():
     assert n_excl <= 0.01 * n, f"tiny: {n_excl} of {n} sub-tokens excluded (survey expects ~0.3 %)"
 
 
+@pytest.mark.parametrize("simt", [False, True])
 def test_small_bf16_forward_matches_oracle(simt):
     _need_gpu()
     cfg = PRESETS["small"].replace(T=2048)
-    W, x, dout = make_problem(cfg, 1, "conf")
+    W, x, dout = make_problem(cfg, 1, "exact")
     g = _run_gpu(cfg, W, x, dout, simt=simt, backward=False)
-    _compare(cfg, W, x, dout, g, backward=False)
+    _compare(cfg, W, x, dout, g, backward=False, dist="exact")
 
 
 @pytest.mark.parametrize("d_h,d_e", [(256, 128), (256, 64), (128, 128), (192, 64), (128, 256)])
@@ -100,9 +102,12 @@ def test_expert_tcgen05_matches_oracle_and_simt(d_h, d_e):
     paper's per-head shapes, ragged T; and vs the SIMT reference kernel."""
     _need_gpu()
     cfg = LayerConfig("tc", T=1500, d=2 * d_h, N_h=2, d_h=d_h, N_e=16, k=4, d_e=d_e, dtype="bf16")
-    W, x, dout = make_problem(cfg, 8, "conf")
+    W, x, dout = make_problem(cfg, 8, "exact")
     g = _run_gpu(cfg, W, x, dout)
-    _compare(cfg, W, x, dout, g, expect=TC_FWD | TC_BWD)
+    # N_e = 16 is outside the tcgen05 routers' shapes (SIMT router); d_h = 192 has no tcgen05 backward
+    bwd_tc = (d_h, d_e) != (192, 64)
+    _compare(cfg, W, x, dout, g, dist="exact",
+             expect={"expert_fwd_tc", "proj_pinned", "expert_bwd_tc" if bwd_tc else "expert_bwd_simt"})
     s = _run_gpu(cfg, W, x, dout, simt=True)
     assert {"expert_fwd_simt", "expert_bwd_simt", "router_simt"} <= s["paths"]
     np.testing.assert_array_equal(g["idx"], s["idx"])
@@ -116,9 +121,9 @@ def test_router_bwd_tcgen05_matches_oracle_and_simt(d_h, N_e, k):
     2^-17 relative bound (ragged T: the last 64-token step is partial)."""
     _need_gpu()
     cfg = LayerConfig("rb", T=1000, d=2 * d_h, N_h=2, d_h=d_h, N_e=N_e, k=k, d_e=64, dtype="bf16")
-    W, x, dout = make_problem(cfg, 11, "conf")
+    W, x, dout = make_problem(cfg, 11, "exact")
     g = _run_gpu(cfg, W, x, dout)
-    _compare(cfg, W, x, dout, g, expect={"router_bwd_tc", "expert_bwd_tc"})
+    _compare(cfg, W, x, dout, g, dist="exact", expect={"router_bwd_tc", "expert_bwd_tc"})
     s = _run_gpu(cfg, W, x, dout, simt=True)
     if np.array_equal(g["idx"], s["idx"]):
         assert rel_err(g["dW_r"], s["dW_r"]) < 1e-4
@@ -130,9 +135,9 @@ def test_paper_head_shapes_match_oracle(N_e, k, d_e):
     expert settings, every kernel on its tensor-core path, ragged T."""
     _need_gpu()
     cfg = LayerConfig("g2x", T=1000, d=512, N_h=2, d_h=256, N_e=N_e, k=k, d_e=d_e, dtype="bf16")
-    W, x, dout = make_problem(cfg, 12, "conf")
+    W, x, dout = make_problem(cfg, 12, "exact")
     g = _run_gpu(cfg, W, x, dout)
-    _compare(cfg, W, x, dout, g, expect=TC_FWD | TC_BWD)
+    _compare(cfg, W, x, dout, g, dist="exact", expect=TC_FWD | TC_BWD)
 
 
 @pytest.mark.parametrize("N_e,k,d_e", [(384, 4, 256), (1536, 8, 128)])
@@ -142,9 +147,11 @@ def test_paper_own_shapes_match_oracle(N_e, k, d_e):
     router backward tiles the experts; kernels outside the tcgen05 shapes take the SIMT path."""
     _need_gpu()
     cfg = LayerConfig("t5", T=384, d=256, N_h=2, d_h=128, N_e=N_e, k=k, d_e=d_e, dtype="bf16")
-    W, x, dout = make_problem(cfg, 14, "conf")
+    W, x, dout = make_problem(cfg, 14, "exact")
     g = _run_gpu(cfg, W, x, dout)
-    _compare(cfg, W, x, dout, g, expect={"router_blk", "router_bwd_tc", "expert_fwd_tc", "expert_bwd_tc"})
+    # the tcgen05 router backward takes N_e in whole 256-expert blocks (1536), else the SIMT one (384)
+    _compare(cfg, W, x, dout, g, dist="exact", expect={"router_blk", "expert_fwd_tc", "expert_bwd_tc",
+                                         "router_bwd_tc" if N_e % 256 == 0 else "router_bwd_simt"})
 
 
 @pytest.mark.parametrize("d_h,d_e,G", [(256, 128, 1), (128, 64, 1), (256, 128, 2)])
@@ -154,9 +161,9 @@ def test_pair_kernels_match_oracle_and_single_cta(d_h, d_e, G):
     per-row arithmetic: outputs and input gradients identical; weight gradients to 1e-6)."""
     _need_gpu()
     cfg = LayerConfig("pair", T=1500, d=2 * d_h, N_h=2, d_h=d_h, N_e=16, k=4, d_e=d_e, dtype="bf16")
-    W, x, dout = make_problem(cfg, 15, "conf")
+    W, x, dout = make_problem(cfg, 15, "exact")
     g = _run_gpu(cfg, W, x, dout, G=G, pair=True)
-    _compare(cfg, W, x, dout, g, expect={"expert_fwd_pair", "expert_bwd_tc"})
+    _compare(cfg, W, x, dout, g, dist="exact", expect={"expert_fwd_pair", "expert_bwd_tc"})
     s = _run_gpu(cfg, W, x, dout, G=G)
     for key in ("out", "dx", "idx", "gates"):
         np.testing.assert_array_equal(g[key], s[key], err_msg=key)
@@ -326,10 +333,10 @@ def test_routing_tokens_match_oracle(simt, G):
     _need_gpu()
     from paper_2602_04870_b200 import mhlmoe as C
     cfg = LayerConfig("rtok", T=1000, d=256, N_h=2, d_h=128, N_e=16, k=4, d_e=64, dtype="bf16", routing_tokens=True)
-    W, x, dout = make_problem(cfg, 15, "conf")
+    W, x, dout = make_problem(cfg, 15, "exact")
     assert W["W_in"].shape == (2 * cfg.D, cfg.d)
     g = _run_gpu(cfg, W, x, dout, G=G, simt=simt)
-    _compare(cfg, W, x, dout, g)
+    _compare(cfg, W, x, dout, g, dist="exact")
     if G == 1 and not simt:
         # the bits must not depend on G (HP carries r next to x, R12)
         g2 = _run_gpu(cfg, W, x, dout, G=2)
@@ -354,7 +361,7 @@ def test_fused_combine_bitwise_equals_separate_kernel(d_h, d_e, N_e, k, T):
     _need_gpu()
     from paper_2602_04870_b200.layer import MHLatentMoE, torch_dtype, weights_to_device
     cfg = LayerConfig("fc", T=T, d=2 * d_h, N_h=2, d_h=d_h, N_e=N_e, k=k, d_e=d_e, dtype="bf16")
-    W, x, dout = make_problem(cfg, 16, "conf")
+    W, x, dout = make_problem(cfg, 16, "exact")
     Wd = weights_to_device(W, cfg.dtype)
     xd = torch.from_numpy(x).to("cuda", torch_dtype(cfg.dtype))
     outs = []
@@ -366,7 +373,7 @@ def test_fused_combine_bitwise_equals_separate_kernel(d_h, d_e, N_e, k, T):
         outs.append(out.float().cpu().numpy())
     np.testing.assert_array_equal(outs[0], outs[1])
     g = _run_gpu(cfg, W, x, dout, backward=False)
-    _compare(cfg, W, x, dout, g, backward=False)
+    _compare(cfg, W, x, dout, g, backward=False, dist="exact")
 
 
 def _full_size_run(cfg, dist="paper"):
@@ -385,17 +392,19 @@ def _full_size_run(cfg, dist="paper"):
     return W, x, dout, L, dict(out=out, idx=idx, gates=gates, dx=dx, **grads)
 
 
-@pytest.mark.parametrize("name", ["paper", "g2x", "table5", "paper_rtok"])
-def test_full_size_sampled_rows_match_oracle(name):
+@pytest.mark.parametrize("name,dist", [("paper", "paper"), ("paper", "exact"), ("g2x", "paper"), ("table5", "paper"),
+                                       ("paper_rtok", "paper")])
+def test_full_size_sampled_rows_match_oracle(name, dist):
     """BASELINE's full-size configs (paper-scale T = 65536, d = 2048, N_h = 8, d_h = 256, N_e = 64,
     k = 8, d_e = 128; its doubled-granularity variant; the paper's Table-5 shape; separate routing
     tokens), bf16, the paper init, the bench's launch configuration, checked on sampled tokens:
     every per-token quantity of the layer (sub-tokens, routing, gates, expert outputs, out, and dx
     through the backward) is a function of that token alone, so the oracle run on the sampled rows
-    gives exactly their values.  Routing: indices bit-exact on clean sub-tokens (R8/R22)."""
+    gives exactly their values.  Routing: indices bit-exact on clean sub-tokens (R8; R22 with the
+    paper init, north_star's rule literally with the exact-sub-token recipe)."""
     _need_gpu()
     cfg = PRESETS[name]
-    W, x, dout, L, r = _full_size_run(cfg)
+    W, x, dout, L, r = _full_size_run(cfg, dist)
     assert TC_FWD | TC_BWD <= L.paths() or name == "table5"
     rng = np.random.default_rng(7)
     S = np.sort(np.concatenate([rng.choice(cfg.T, 60, replace=False), [0, cfg.T - 1]]))
@@ -404,7 +413,8 @@ def test_full_size_sampled_rows_match_oracle(name):
     P = {k: v.astype(np.float64) for k, v in W.items()}
     xs, ds = x[S].astype(np.float64), dout[S].astype(np.float64)
     C0 = O.layer_forward(P, xs, cfg.k, mode="bf16")
-    rt = check_routing(P, C0, g["idx"], cfg.k, x=xs)
+    rt = check_routing(P, C0, g["idx"], cfg.k, x=xs, exact=dist == "exact")
+    print(f"[{name}/{dist}] excluded {rt.n_excl} of {rt.n} sub-tokens ({rt.n_margin} by the margin rule alone)")
     C = O.layer_forward(P, xs, cfg.k, mode="bf16", forced_idx=rt.forced)
     check_gates(P, C, g["gates"], rt)
     gr = O.layer_backward(P, xs, ds, C)
@@ -448,7 +458,7 @@ def test_full_size_weight_gradients_match_oracle(h, experts):
         Ie = gi[T_e]
         ge = O.gates_from_scores(S[T_e][np.arange(T_e.size)[:, None], Ie])
         dY = O.round_storage(dout[T_e].astype(np.float64) @ W_out_h, "bf16")       # dcat block of head h (R9)
-        gh = O._head_backward(O._head_params(P, h), X_h[T_e], dY, Ie, ge)
+        gh = OM._head_backward(OM._head_params(P, h), X_h[T_e], dY, Ie, ge)
         e1 = rel_err(dW1[e], gh["dW1"][e]); e2 = rel_err(dW2[e], gh["dW2"][e]); er = rel_err(dW_r[:, e], gh["dW_r"][:, e])
         assert max(e1, e2, er) <= TOL["bf16"], f"h={h} e={e}: dW1 {e1:.2e} dW2 {e2:.2e} dW_r {er:.2e}"
 
@@ -516,9 +526,14 @@ def test_xs_rounding_within_r22_bound():
     P = {k: v.astype(np.float64) for k, v in W.items()}
     xs = x.astype(np.float64)
     C0 = O.layer_forward(P, xs, cfg.k, mode="bf16")
+    from parity_util import FP32_ACC_SCALE, xs_band_ratio
     amb = xs_ambiguous(xs, P["W_in"], C0.Xs_pre, "bf16")
     diff = g["Xs"] != C0.Xs
-    assert not np.any(diff & ~amb), f"{int(np.sum(diff & ~amb))} Xs elements outside the R22 band round differently"
+    need = xs_band_ratio(xs, P["W_in"], C0.Xs_pre)[diff]      # band width (in FP32_ACC_SCALE units) each flip needs
+    print(f"[R22] flips {int(diff.sum())} of {diff.size}; band {100 * amb.mean():.3f} % of elements; "
+          f"needed scale max {need.max() if need.size else 0:.2f}, p99 {np.percentile(need, 99) if need.size else 0:.2f}")
+    assert not np.any(diff & ~amb), (f"{int(np.sum(diff & ~amb))} Xs elements outside the R22 band round differently "
+                                     f"(need scale {need.max():.2f} > {FP32_ACC_SCALE})")
     assert amb.mean() < 0.01, f"R22 band covers {100 * amb.mean():.2f} % of the elements"
     # and the flips inside the band are single-ulp moves to the neighbouring bf16 value
     if np.any(diff):
