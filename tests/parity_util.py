@@ -30,7 +30,7 @@ def rel_err(gpu, ref) -> float:
     return float(np.max(np.abs(gpu - ref)) / den) if den > 0 else float(np.max(np.abs(gpu)))
 
 
-def rel_err_slices(gpu, ref, keep_axes) -> float:
+def rel_err_slices(gpu, ref, keep_axes, scale=None) -> float:
     """R10 per slice: the tensor is cut into slices indexed by `keep_axes` (e.g. one token row of
     out / dx, one (head, expert) block of dW1, one expert column of dW_r); each slice's error is
     max|gpu - ref| / max|ref| over that slice, and the worst slice is returned.  An error confined
@@ -40,11 +40,29 @@ def rel_err_slices(gpu, ref, keep_axes) -> float:
     ref = np.asarray(ref, np.float64)
     red = tuple(a for a in range(ref.ndim) if a not in keep_axes)
     num = np.max(np.abs(gpu - ref), axis=red)
-    den = np.max(np.abs(ref), axis=red)
+    den = np.max(np.abs(ref if scale is None else np.asarray(scale, np.float64)), axis=red)
     zero = den == 0
     if np.any(zero & (num > 0)):
         return float("inf")
     return float(np.max(num[~zero] / den[~zero])) if np.any(~zero) else 0.0
+
+
+def dW_r_scale(P, C, gr):
+    """Per-element magnitude scale of dW_r before cancellation: dW_r[h] = X_h^T dS_full with
+    dS = g (dg - sum_i g_i dg_i) (Alg. 2); a column with few replicas whose dS cancels would make the
+    plain relative error measure the conditioning of that subtraction, not the kernel.  Scale =
+    |X_h|^T (g (|dg| + sum_i g_i |dg_i|)) scattered to the selected experts (the componentwise
+    bound of the same expression); max |ref| <= max scale.  Test-side tolerance scale only."""
+    N_h, d_h, N_e = P["W_r"].shape
+    out = np.zeros((N_h, d_h, N_e))
+    for h in range(N_h):
+        sl = routing_slice(P, h)
+        g = C.g[h]; adg = np.abs(gr["dg"][h]); I = C.I[h]
+        dsa = g * (adg + np.sum(g * adg, axis=1, keepdims=True))
+        full = np.zeros((I.shape[0], N_e))
+        np.add.at(full, (np.arange(I.shape[0])[:, None].repeat(I.shape[1], 1), I), dsa)
+        out[h] = np.abs(C.Xs[:, sl]).T @ full
+    return out
 
 
 # per-tensor slicing for rel_err_slices: out/dx per token row, dW1/dW2 per (head, expert), dW_r per
