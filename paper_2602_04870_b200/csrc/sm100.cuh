@@ -22,13 +22,29 @@ __device__ __forceinline__ void fence_mbar_init() {
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.shared::cta.b64 st, [%0];\n\t}" ::"r"(smem_u32(bar)) : "memory");
 }
+// try_wait suspends the warp until the phase completes or a time limit elapses; with the
+// system-default limit idle role warps re-poll so often that their YIELD / SYNCS / BRA spin took
+// about half of the issued instructions of the expert kernels (ncu r2c), and the MMA warp (highest
+// warp id, first in the issue arbiter) competed with the epilogue for issue slots.  The hint only
+// lengthens the sleep: completion of the phase still wakes the warp.
+#ifndef MHL_WAIT_HINT_NS
+#define MHL_WAIT_HINT_NS 20000
+#endif
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
   const uint32_t a = smem_u32(bar);
+#if MHL_WAIT_HINT_NS > 0
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
+      "@!p bra WAIT_%=;\n\t}" ::"r"(a), "r"(phase), "n"(MHL_WAIT_HINT_NS) : "memory");
+#else
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
       "WAIT_%=:\n\t"
       "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
       "@!p bra WAIT_%=;\n\t}" ::"r"(a), "r"(phase) : "memory");
+#endif
 }
 
 // one lane polls, the rest of the warp parks at __syncwarp (32x fewer try_wait issues)

@@ -13,13 +13,15 @@ from collections import defaultdict
 
 KEYS = [
     "gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
+    "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed",
     "TPC.TriageCompute.sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed",
     "sm__throughput.avg.pct_of_peak_sustained_elapsed", "dram__throughput.avg.pct_of_peak_sustained_elapsed",
     "lts__t_sector_hit_rate.pct", "lts__throughput.avg.pct_of_peak_sustained_elapsed",
+    "l1tex__throughput.avg.pct_of_peak_sustained_elapsed", "smsp__issue_active.avg.pct_of_peak_sustained_active",
     "launch__registers_per_thread", "launch__grid_size", "launch__block_size",
     "sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active",
     "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active",
-    "SM_A.TriageCompute.sm__inst_executed_pipe_xu_realtime.avg.pct_of_peak_sustained_elapsed",
+    "sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active",
     "sm__warps_active.avg.pct_of_peak_sustained_active",
 ]
 
@@ -49,27 +51,32 @@ def launches(path):
     print(f"{'total':70s} {sum(cnt.values()):8d} {s:10.1f}")
 
 
-def report(path, flops=None, nbytes=None):
+def _rows(path):
     out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
-    hdr, units, vals = rows[0], rows[1], rows[2]
-    d = {h: (vals[i], units[i]) for i, h in enumerate(hdr)}
-    print("kernel:", d.get("Kernel Name", ("?",))[0][:160])
-    for k in KEYS:
-        if k in d:
-            print(f"  {k} = {d[k][0]} {d[k][1]}")
-    t = float(d["gpu__time_duration.sum"][0]) * {"ms": 1e-3, "us": 1e-6, "ns": 1e-9}.get(d["gpu__time_duration.sum"][1], 1)
-    if flops:
-        print(f"  algorithmic {float(flops) / 1e9:.1f} GFLOP -> {float(flops) / t / 1e12:.1f} TFLOP/s (cold, serialised)")
-    if nbytes:
-        print(f"  algorithmic {float(nbytes) / 1e6:.1f} MB -> {float(nbytes) / t / 1e9:.1f} GB/s")
-    rb = float(d.get("dram__bytes_read.sum", ("0",))[0] or 0)
-    print(f"  dram traffic (read+write): {d.get('dram__bytes_read.sum')} + {d.get('dram__bytes_write.sum')}")
+    hdr, units = rows[0], rows[1]
+    return [{h: (vals[i], units[i]) for i, h in enumerate(hdr)} for vals in rows[2:] if len(vals) == len(hdr)]
+
+
+def report(path, flops=None, nbytes=None):
+    """Key metrics of every kernel launch captured in one report."""
+    for d in _rows(path):
+        print("kernel:", d.get("Kernel Name", ("?",))[0][:160])
+        for k in KEYS:
+            if k in d:
+                print(f"  {k} = {d[k][0]} {d[k][1]}")
+        t = float(d["gpu__time_duration.sum"][0]) * {"ms": 1e-3, "us": 1e-6, "ns": 1e-9}.get(d["gpu__time_duration.sum"][1], 1)
+        if flops:
+            print(f"  algorithmic {float(flops) / 1e9:.1f} GFLOP -> {float(flops) / t / 1e12:.1f} TFLOP/s (cold, serialised)")
+        if nbytes:
+            print(f"  algorithmic {float(nbytes) / 1e6:.1f} MB -> {float(nbytes) / t / 1e9:.1f} GB/s")
 
 
 SPAN_OF = {"expert_bwd_h": "B5_expert_bwd_dx", "expert_dw_kernel": "B5_expert_bwd_dw",
            "expert_fwd_sm100": "F5_expert_fwd", "expert_dx_gemm": "B5_expert_dx_gemm",
-           "combine_bwd": "B6_combine_bwd", "combine_fwd": "F6_combine", "router_sm100": "F3_router_topk"}
+           "router_sm100": "F3_router_topk", "router_bwd_sm100": "B3_router_bwd", "scatter_kernel": "F4_cluster",
+           # the same combine kernel serves F6 and then B6 within one step (capture order)
+           "combine_kernel": ("F6_combine", "B6_combine_bwd")}
 
 
 def traffic(workload, paths):
@@ -78,18 +85,22 @@ def traffic(workload, paths):
     import json
     import os
     out = {"_workload": workload, "_source": "ncu --set full --clock-control none, one launch each"}
+    seen = {}
     for path in paths:
-        csvout = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
-        rows = list(csv.reader(io.StringIO(csvout)))
-        hdr, units, vals = rows[0], rows[1], rows[2]
-        d = {h: (vals[i], units[i]) for i, h in enumerate(hdr)}
         scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
-        b = sum(float(d[k][0].replace(",", "")) * scale.get(d[k][1], 1) for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"))
-        name = d["Kernel Name"][0]
-        span = next((v for k, v in SPAN_OF.items() if k in name), None)
-        if span:
-            out[span] = {"kernel": name.split("(")[0][:120], "dram_bytes_per_launch": b,
-                         "report": os.path.basename(path)}
+        for d in _rows(path):
+            b = sum(float(d[k][0].replace(",", "")) * scale.get(d[k][1], 1) for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"))
+            name = d["Kernel Name"][0]
+            key = next((k for k in SPAN_OF if k in name), None)
+            if key is None:
+                continue
+            span = SPAN_OF[key]
+            if isinstance(span, tuple):
+                span = span[min(seen.get(key, 0), len(span) - 1)]
+            seen[key] = seen.get(key, 0) + 1
+            if span not in out:
+                out[span] = {"kernel": name.split("(")[0][:120], "dram_bytes_per_launch": b,
+                             "report": os.path.basename(path)}
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     json.dump(out, open(os.path.join(root, "profiles", "ncu_traffic.json"), "w"), indent=1)
     print(json.dumps(out, indent=1))
