@@ -61,8 +61,9 @@ typedef enum { MHL_F32 = 0, MHL_BF16 = 1 } mhl_dtype;
                                  head i routes on r_ti and runs its experts on x_ti.  The HP
                                  scatter (and its backward mirror) carries both: twice the bytes
                                  (P:1570); dW_in is [2D, d]. */
-#define MHL_FLAG_FUSED_COMBINE 16u  /* G = 1, bf16: run the forward combine (F6) inside the expert
-                                 kernel, window by window (NEXT-1 experiment; same bits, opt-in) */
+#define MHL_FLAG_FUSED_COMBINE 16u  /* REMOVED (round 2): the in-kernel forward combine experiment
+                                 measured slower than the separate pass; hp_plan / hp_plan_query
+                                 return MHL_ERR_UNSUPPORTED for it. */
 
 /* Layer + HP configuration (the paper's problem statement: P:496). */
 typedef struct {
@@ -248,7 +249,7 @@ MHL_API int32_t mhl_step_times(mhl_plan plan, char* names, size_t names_cap, dou
 #define MHL_PATH_ROUTER_BWD_TC    (1u << 8)   /* B3 dW_r on tcgen05                                */
 #define MHL_PATH_ROUTER_BWD_SIMT  (1u << 9)
 #define MHL_PATH_PROJ_PINNED      (1u << 10)  /* F1/F8/B8/B1 on the plan's pinned GEMM algorithm   */
-#define MHL_PATH_FUSED_COMBINE    (1u << 11)  /* F6 inside the forward expert kernel               */
+#define MHL_PATH_FUSED_COMBINE    (1u << 11)  /* (reserved: the removed in-kernel combine)         */
 #define MHL_PATH_A2A_NCCL         (1u << 12)  /* HP exchanges through NCCL send/recv               */
 #define MHL_PATH_A2A_LOOPBACK     (1u << 13)  /* HP exchanges as device copies (MHL_FLAG_LOOPBACK) */
 MHL_API uint32_t mhl_kernel_paths(mhl_plan plan, int reset);

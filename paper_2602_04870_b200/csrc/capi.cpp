@@ -113,7 +113,7 @@ struct Bump {
 };
 
 // offsets inside one rank's saved region
-struct SavedLayout { size_t Xs, idx, gate, perm, tok_s, gate_s, pos, off, tiles, ntiles, chunks, nchunks, cbase, ccount, pbase, pcount, load, tilewin, wtiles, wtok, wdone, cat, total; };
+struct SavedLayout { size_t Xs, idx, gate, perm, tok_s, gate_s, pos, off, tiles, ntiles, chunks, nchunks, cbase, ccount, pbase, pcount, load, cat, total; };
 // offsets inside one rank's workspace region (forward and backward alias each other)
 struct FwdLayout { size_t send1, Yrep, send2, recv2, hist, tilepref, planes, total; };
 struct BwdLayout { size_t send3, dY, dXrep, dg, dS, dS_s, dH, gA, dwr_part, W_rT, send4, recv4, dXs, dw_part, dw_done, total; };
@@ -137,10 +137,6 @@ SavedLayout saved_layout(const Dims& m) {
   L.pbase = b.take((size_t)m.H * mhl::kDwParts * 4);
   L.pcount = b.take((size_t)m.H * mhl::kDwParts * 4);
   L.load = b.take((size_t)m.H * m.N_e * 4);             // per-head expert loads of the step (F4)
-  L.tilewin = b.take((size_t)m.max_tiles * 4);          // fused combine: window of each tile
-  L.wtiles = b.take((size_t)m.H * mhl::kTileParts * 4); //   tiles per (head, part) window
-  L.wtok = b.take((size_t)m.H * mhl::kTileParts * 4);   //   token bound per window
-  L.wdone = b.take((size_t)m.H * mhl::kTileParts * 4);  //   completed tile-slab stores per window
   L.cat = b.take((size_t)m.T_loc * m.D * m.el);
   L.total = b.off;
   return L;
@@ -192,6 +188,9 @@ mhl_status make_dims(const mhl_config* c, Dims* m) {
   if (!loop && (c->rank < 0 || c->rank >= c->world_size)) return fail(MHL_ERR_CONFIG, "rank out of range");
   if (c->dtype != MHL_F32 && c->dtype != MHL_BF16) return fail(MHL_ERR_CONFIG, "dtype must be MHL_F32 or MHL_BF16");
   if (c->top_k > 16) return fail(MHL_ERR_UNSUPPORTED, "top_k > 16 is not supported by the router kernel");
+  if (c->flags & MHL_FLAG_FUSED_COMBINE)
+    return fail(MHL_ERR_UNSUPPORTED, "MHL_FLAG_FUSED_COMBINE was removed: the in-kernel combine measured slower than "
+                                     "the separate pass (DESIGN.md §7)");
   if (c->d_head % 8 != 0 || c->d_expert % 8 != 0 || c->d_model % 8 != 0)
     return fail(MHL_ERR_UNSUPPORTED, "d_model, d_head and d_expert must be multiples of 8");
   if (c->d_head > 512 || c->d_expert > 512) return fail(MHL_ERR_UNSUPPORTED, "d_head, d_expert <= 512");
@@ -578,12 +577,6 @@ mhl_status moe_forward_local(mhl_plan p, const RankPtrs& R, void* yout, cudaStre
   mhl::Tile* tiles = (mhl::Tile*)(R.saved + S.tiles);
   int32_t* ntiles = (int32_t*)(R.saved + S.ntiles);
   int32_t* hist = (int32_t*)(R.ws + F.hist);
-  // NEXT-1 (G = 1): F6 runs inside the forward expert kernel, window by window, while the window's
-  // Yrep rows are still in L2 (FwdCombine, expert_sm100.cu).  Opt-in (MHL_FLAG_FUSED_COMBINE, or
-  // MHL_FUSED_COMBINE=1 for the process): measured slower than the separate kernel.
-  static const bool fuse_env = getenv("MHL_FUSED_COMBINE") && atoi(getenv("MHL_FUSED_COMBINE")) != 0;
-  const bool fuse = (fuse_env || (p->cfg.flags & MHL_FLAG_FUSED_COMBINE)) && yout != nullptr && m.G == 1 && !m.simt && !m.pair &&
-                    mhl::expert_fwd_sm100_supported(m.d_h, m.d_e) && mhl::store_lsu_default_fwd() == 0;
   {
     MHL_SPAN("F3_router_topk");
     if (!m.simt && mhl::router_sm100_supported(m.d_h, m.N_e)) {
@@ -610,14 +603,7 @@ mhl_status moe_forward_local(mhl_plan p, const RankPtrs& R, void* yout, cudaStre
                         (float*)(R.saved + S.gate_s), m.Rp, m.seg_align, tiles, ntiles, m.max_tiles,
                         (mhl::Tile*)(R.saved + S.chunks),
                         (int32_t*)(R.saved + S.nchunks), (int32_t*)(R.saved + S.cbase), (int32_t*)(R.saved + S.ccount),
-                        m.max_chunks, 0, (int32_t*)(R.saved + S.pbase), (int32_t*)(R.saved + S.pcount), s,
-                        fuse ? (int32_t*)(R.saved + S.tilewin) : nullptr);
-    if (fuse) {
-      mhl::launch_windows(routing_view(m, R.saved), (const int32_t*)(R.saved + S.load), (int32_t*)(R.saved + S.wtiles),
-                          (int32_t*)(R.saved + S.wtok), s);
-      MHL_CUDA(cudaMemsetAsync(R.saved + S.wdone, 0, (size_t)m.H * mhl::kTileParts * 4, s));
-      p->launches++;
-    }
+                        m.max_chunks, 0, (int32_t*)(R.saved + S.pbase), (int32_t*)(R.saved + S.pcount), s);
   }
   const mhl::Routing rt = routing_view(m, R.saved);
   void* Yrep = R.ws + F.Yrep;
@@ -634,24 +620,16 @@ mhl_status moe_forward_local(mhl_plan p, const RankPtrs& R, void* yout, cudaStre
         return fail(MHL_ERR_CUDA, "expert_fwd (pair): TMA tensor-map encoding failed");
       p->paths |= MHL_PATH_EXPERT_FWD_PAIR;
     } else {
-      mhl::FwdCombine fc;
-      if (fuse) {
-        fc.out = yout; fc.ldo = m.HD;
-        fc.wdone = (int32_t*)(R.saved + S.wdone);
-        fc.wtiles = (const int32_t*)(R.saved + S.wtiles);
-        fc.wtok = (const int32_t*)(R.saved + S.wtok);
-        fc.tilewin = (const int32_t*)(R.saved + S.tilewin);
-      }
-      if (!mhl::launch_expert_fwd_sm100(rt, Xs, m.XW, R.W1, R.W2, m.d_h, m.d_e, Yrep, p->num_sms, s, fc))
+      if (!mhl::launch_expert_fwd_sm100(rt, Xs, m.XW, R.W1, R.W2, m.d_h, m.d_e, Yrep, p->num_sms, s))
         return fail(MHL_ERR_CUDA, "expert_fwd: TMA tensor-map encoding failed");
-      p->paths |= MHL_PATH_EXPERT_FWD_TC | (fuse ? MHL_PATH_FUSED_COMBINE : 0u);
+      p->paths |= MHL_PATH_EXPERT_FWD_TC;
     }
   }
-  if (yout && !fuse) {
+  if (yout) {
     MHL_SPAN("F6_combine");
     mhl::launch_combine_fwd(m.dtype, rt, Yrep, m.d_h, yout, m.HD, s);
   }
-  p->launches += (yout && !fuse) ? 7 : 6;
+  p->launches += yout ? 7 : 6;
   if (R.topk_idx) MHL_CUDA(cudaMemcpyAsync(R.topk_idx, idx, (size_t)m.H * m.R * 4, cudaMemcpyDeviceToDevice, s));
   if (R.gates) MHL_CUDA(cudaMemcpyAsync(R.gates, gate, (size_t)m.H * m.R * 4, cudaMemcpyDeviceToDevice, s));
   return check_kernels(p);

@@ -217,7 +217,7 @@ dw_parts_kernel(const int32_t* __restrict__ off, int H, int N_e, int P, Tile* __
 __global__ void __launch_bounds__(256)
 tiles_kernel(const int32_t* __restrict__ counts, const int32_t* __restrict__ off, const int32_t* __restrict__ tbase,
              Tile* __restrict__ tiles, int max_tiles, int H, int N_e, int64_t Rp, int32_t* __restrict__ perm, int32_t* __restrict__ tok_s,
-             float* __restrict__ gate_s, int tok_zero, int seg_align, int32_t* __restrict__ tilewin) {
+             float* __restrict__ gate_s, int tok_zero, int seg_align) {
   const int he = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5), lane = threadIdx.x & 31;
   if (he >= H * N_e) return;
   const int h = he / N_e, e = he % N_e;
@@ -236,7 +236,6 @@ tiles_kernel(const int32_t* __restrict__ counts, const int32_t* __restrict__ off
         tl.head = h; tl.expert = e; tl.row0 = row_off + j * kExpertBM;
         tl.rows = max(0, min(kExpertBM, c - j * kExpertBM));
         tiles[ti] = tl;
-        if (tilewin) tilewin[ti] = h * kTileParts + p;
       }
     }
   }
@@ -335,42 +334,6 @@ scatter_kernel(const int32_t* __restrict__ idx, const float* __restrict__ gate, 
   }
 }
 
-// (4) token windows of the fused combine (FwdCombine, expert_sm100.cu): per (head h, part p)
-// the number of expert tiles in part p, and wtok[h][p] = the first token of part p+1 over all
-// experts (rows within an expert are in token order, so every token below it has all k replicas
-// in parts <= p); the last part's bound is T.
-__global__ void __launch_bounds__(256)
-window_kernel(const int32_t* __restrict__ counts, const int32_t* __restrict__ off, const int32_t* __restrict__ tok_s,
-              int64_t Rp, int N_e, int seg_align, int T, int32_t* __restrict__ wtiles, int32_t* __restrict__ wtok) {
-  __shared__ int s_t[8], s_m[8];
-  const int h = blockIdx.x, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int TPS = seg_align / kExpertBM;
-  for (int p = 0; p < kTileParts; ++p) {
-    int nt = 0, mn = T;
-    for (int e = threadIdx.x; e < N_e; e += blockDim.x) {
-      const int c = counts[(size_t)h * N_e + e];
-      const int nu = (c + seg_align - 1) / seg_align;
-      nt += TPS * ((p + 1) * nu / kTileParts - p * nu / kTileParts);
-      if (p + 1 < kTileParts) {
-        const int r = TPS * ((p + 1) * nu / kTileParts) * kExpertBM;     // first row of part p+1
-        if (r < c) mn = min(mn, tok_s[(size_t)h * Rp + off[(size_t)h * (N_e + 1) + e] + r]);
-      }
-    }
-    for (int o = 16; o > 0; o >>= 1) {
-      nt += __shfl_xor_sync(0xffffffffu, nt, o);
-      mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, o));
-    }
-    if (lane == 0) { s_t[warp] = nt; s_m[warp] = mn; }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      int a = 0, b = T;
-      for (int w = 0; w < 8; ++w) { a += s_t[w]; b = min(b, s_m[w]); }
-      wtiles[h * kTileParts + p] = a;
-      wtok[h * kTileParts + p] = b;
-    }
-    __syncthreads();
-  }
-}
 
 // aux-free bias update (R24): one thread per (h, e); sign of load - mean as an exact integer test
 __global__ void update_bias_kernel(const int32_t* __restrict__ load, int n, int N_e, int64_t total, float gamma,
@@ -390,9 +353,6 @@ void launch_dw_parts(const Routing& rt, Tile* chunks, int32_t* nchunks, int32_t*
                                          ccount, pbase, pcount);
 }
 
-void launch_windows(const Routing& rt, const int32_t* counts, int32_t* wtiles, int32_t* wtok, cudaStream_t s) {
-  window_kernel<<<rt.H, 256, 0, s>>>(counts, rt.off, rt.tok_s, rt.Rp, rt.N_e, rt.seg_align, (int)rt.T, wtiles, wtok);
-}
 
 void launch_update_bias(const int32_t* load, int H, int N_e, int64_t total, float gamma, float* bias,
                         cudaStream_t s) {
@@ -404,7 +364,7 @@ void launch_cluster(int H, int64_t T, int k, int N_e, const int32_t* idx, const 
                     int32_t* tilepref, int32_t* counts, int32_t* off, int32_t* perm, int32_t* pos, int32_t* tok_s,
                     float* gate_s, int64_t Rp, int seg_align, Tile* tiles, int32_t* ntiles, int max_tiles,
                     Tile* chunks, int32_t* nchunks, int32_t* cbase, int32_t* ccount, int max_chunks, int dw_parts,
-                    int32_t* pbase, int32_t* pcount, cudaStream_t s, int32_t* tilewin) {
+                    int32_t* pbase, int32_t* pcount, cudaStream_t s) {
   const int n_rt = (int)((T + kRouterTile - 1) / kRouterTile);
   tile_prefix_kernel<<<dim3(N_e, H), 256, 0, s>>>(hist, tilepref, counts, n_rt, N_e);
   // tile bases [H][kTileParts][N_e] live in the (otherwise unused here) tail of tilepref's scratch
@@ -413,7 +373,7 @@ void launch_cluster(int H, int64_t T, int k, int N_e, const int32_t* idx, const 
   if (dw_parts > 0)
     dw_parts_kernel<<<H, 1024, 0, s>>>(off, H, N_e, dw_parts, chunks, max_chunks, nchunks, cbase, ccount, pbase, pcount);
   tiles_kernel<<<(H * N_e + 7) / 8, 256, 0, s>>>(counts, off, tbase, tiles, max_tiles, H, N_e, Rp, perm, tok_s,
-                                                 gate_s, (int)T, seg_align, tilewin);
+                                                 gate_s, (int)T, seg_align);
   const size_t ssm = sizeof(int) * ((size_t)(kScatterWarps + 1) * N_e + 2 * (size_t)kRouterTile * k);
   if (ssm > 48 * 1024) cudaFuncSetAttribute(scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ssm);
   scatter_kernel<<<dim3(n_rt, H), kScatterWarps * 32, ssm, s>>>(idx, gate, off, tilepref, perm, pos, tok_s, gate_s,

@@ -71,33 +71,20 @@ void launch_cluster(int H, int64_t T, int k, int N_e, const int32_t* idx, const 
                     int32_t* tilepref, int32_t* counts, int32_t* off, int32_t* perm, int32_t* pos, int32_t* tok_s,
                     float* gate_s, int64_t Rp, int seg_align, Tile* tiles, int32_t* ntiles, int max_tiles,
                     Tile* chunks, int32_t* nchunks, int32_t* cbase, int32_t* ccount, int max_chunks, int dw_parts,
-                    int32_t* pbase, int32_t* pcount, cudaStream_t s, int32_t* tilewin = nullptr);
+                    int32_t* pbase, int32_t* pcount, cudaStream_t s);
 
 // ---- F5: Yrep[h][row][c] = gate_s * gelu(X[tok_s] W1_e^T) W2_e for every sorted row (padding rows
 // produce zeros).  Xs holds T+1 rows, row T all-zero.  Yrep is [H][Rp][d_h].
 void launch_expert_fwd_simt(int dtype, const Routing& rt, const void* Xs, int64_t ldx, const void* W1, const void* W2,
                             int d_h, int d_e, void* Yrep, cudaStream_t s);
 bool expert_fwd_sm100_supported(int d_h, int d_e);
-// In-kernel F6 of the forward expert kernel (NEXT-1, G = 1): spare warps of every CTA combine a
-// token window of a head as soon as all expert tiles of the window's parts have been stored, so the
-// window's Yrep rows are read back while still in L2.  Windows = (head, part) of the tile list;
-// wtok[h][p] = tokens whose replicas all lie in parts <= p (cluster.cu window_kernel).
-struct FwdCombine {
-  void* out = nullptr;             // cat [T][ldo] (head h at column h*d_h); nullptr: no fused combine
-  int64_t ldo = 0;
-  int32_t* wdone = nullptr;        // [H*kTileParts] tile-slab stores completed (4 per tile), zeroed per call
-  const int32_t* wtiles = nullptr; // [H*kTileParts] tiles per window
-  const int32_t* wtok = nullptr;   // [H*kTileParts] token bound per window (non-decreasing in p, last = T)
-  const int32_t* tilewin = nullptr;  // [ntiles] window of each tile
-};
-void launch_windows(const Routing& rt, const int32_t* counts, int32_t* wtiles, int32_t* wtok, cudaStream_t s);
 // the dW kernel's row-part chunks of a clustered routing (launch_cluster with dw_parts = 0 leaves
 // them to this call, which the backward makes: a forward-only step does not pay for them)
 void launch_dw_parts(const Routing& rt, Tile* chunks, int32_t* nchunks, int32_t* cbase, int32_t* ccount,
                      int32_t* pbase, int32_t* pcount, cudaStream_t s);
 
 bool launch_expert_fwd_sm100(const Routing& rt, const void* Xs, int64_t ldx, const void* W1, const void* W2, int d_h,
-                             int d_e, void* Yrep, int num_sms, cudaStream_t s, const FwdCombine& fc = FwdCombine());
+                             int d_e, void* Yrep, int num_sms, cudaStream_t s);
 // the same on CTA pairs (tcgen05 cta_group::2, half of each weight matrix per CTA)
 bool expert_fwd_pair_supported(int d_h, int d_e);
 bool launch_expert_fwd_pair_sm100(const Routing& rt, const void* Xs, int64_t ldx, const void* W1, const void* W2,

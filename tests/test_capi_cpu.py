@@ -112,3 +112,16 @@ def test_routing_tokens_plan_doubles_the_scatter_only():
                flags=C.MHL_FLAG_ROUTING_TOKENS)
         assert b["a2a_bytes_per_peer"] == 2 * a["a2a_bytes_per_peer"]
         assert b["a2a_bytes_per_rank"] == 2 * a["a2a_bytes_per_rank"]
+
+
+def test_fused_combine_flag_is_rejected():
+    """The in-kernel combine experiment (MHL_FLAG_FUSED_COMBINE) was removed (measured slower, and it
+    needed every CTA resident for its cross-CTA spin); the flag is refused before any launch."""
+    from paper_2602_04870_b200 import mhlmoe as C
+    cfg = C.make_config(1024, 256, 2, 128, 64, 8, 64, "bf16", 1, 0, C.MHL_FLAG_FUSED_COMBINE)
+    try:
+        C.hp_plan_query(cfg)
+    except C.MhlError as e:
+        assert C.STATUS[e.status] == "MHL_ERR_UNSUPPORTED"
+    else:
+        raise AssertionError("MHL_FLAG_FUSED_COMBINE accepted")

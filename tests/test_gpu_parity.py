@@ -355,28 +355,6 @@ def test_routing_tokens_scatter_bytes_double():
     assert info1["a2a_bytes_per_peer"] == 2 * info0["a2a_bytes_per_peer"]
 
 
-@pytest.mark.parametrize("d_h,d_e,N_e,k,T", [(256, 128, 64, 8, 4000), (128, 64, 16, 4, 1500), (256, 64, 128, 16, 1000)])
-def test_fused_combine_bitwise_equals_separate_kernel(d_h, d_e, N_e, k, T):
-    """NEXT-1 (G = 1): the combine running inside the forward expert kernel, window by window, gives
-    the same bits as the separate combine kernel (same j order, fp32 sums), and matches the oracle."""
-    _need_gpu()
-    from paper_2602_04870_b200.layer import MHLatentMoE, torch_dtype, weights_to_device
-    cfg = LayerConfig("fc", T=T, d=2 * d_h, N_h=2, d_h=d_h, N_e=N_e, k=k, d_e=d_e, dtype="bf16")
-    W, x, dout = make_problem(cfg, 16, "exact")
-    Wd = weights_to_device(W, cfg.dtype)
-    xd = torch.from_numpy(x).to("cuda", torch_dtype(cfg.dtype))
-    outs = []
-    for fused in (True, False):
-        L = MHLatentMoE(cfg.T, cfg.d, cfg.N_h, cfg.d_h, cfg.N_e, cfg.k, cfg.d_e, cfg.dtype, fused_combine=fused)
-        out, _, _ = L.forward(xd, Wd)
-        torch.cuda.synchronize()
-        L.check_status()
-        outs.append(out.float().cpu().numpy())
-    np.testing.assert_array_equal(outs[0], outs[1])
-    g = _run_gpu(cfg, W, x, dout, backward=False)
-    _compare(cfg, W, x, dout, g, backward=False, dist="exact")
-
-
 def _full_size_run(cfg, dist="paper"):
     from paper_2602_04870_b200.layer import MHLatentMoE, torch_dtype, weights_to_device
     W, x, dout = make_problem(cfg, 0, dist)
