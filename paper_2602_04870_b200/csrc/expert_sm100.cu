@@ -44,14 +44,13 @@ constexpr int kGeluWarp0 = 8;         // warps 8-15: GELU epilogue (2 per lane q
 constexpr int kYWarp0 = 16;           // warps 16-19: Y epilogue (one per lane quadrant)
 constexpr int kMmaWarp = 20;          // warp 20: MMA issuer + TMEM owner
 constexpr int kThreads = 21 * 32;
-// Registers: setmaxnreg moves registers between warps of one SM sub-partition (warps w with the
-// same w % 4 share a 16384-register file).  Sub-partition 0 holds warps 0, 4 (producers), 8, 12
-// (GELU), 16 (Y) and 20 (MMA): six warps, so the launch count is 80 (ptxas), and after the
-// producers' decrease the GELU warps' increase must still fit that file: 2*32*40 + 2*32*136 +
-// 2*32*80 = 16384.  (An increase the file cannot cover blocks setmaxnreg.inc forever.)
-constexpr int kLaunchRegs = 80, kProdRegs = 40, kGeluRegs = 136;
-static_assert(2 * 32 * kProdRegs + 2 * 32 * kGeluRegs + 2 * 32 * kLaunchRegs <= 16384,
-              "expert fwd: register budget of sub-partition 0 exceeded");
+// Registers: setmaxnreg.inc draws only on registers the CTA's own warps released with
+// setmaxnreg.dec (an increase nothing covers blocks forever).  With 21 warps ptxas sets the launch
+// count to 80 (sub-partition 0 holds six of them in its 16384-register file); the 8 producer warps
+// release 8*32*(80-40), exactly what the 8 GELU warps take to reach 120.
+constexpr int kLaunchRegs = 80, kProdRegs = 40, kGeluRegs = 120;
+static_assert(8 * (kLaunchRegs - kProdRegs) >= 8 * (kGeluRegs - kLaunchRegs),
+              "expert fwd: the GELU warps' register increase exceeds the producers' release");
 static_assert(6 * 32 * kLaunchRegs <= 16384, "expert fwd: launch register count does not fit sub-partition 0");
 constexpr int kGeluThreads = 256, kYThreads = 128;
 constexpr int kXChunk = BM * 128;    // one 64-column K-chunk of the gathered X tile (16 KB)
