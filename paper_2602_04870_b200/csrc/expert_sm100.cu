@@ -220,12 +220,26 @@ expert_fwd_sm100_kernel(const __grid_constant__ CUtensorMap w1map, const __grid_
       constexpr uint32_t ID2 = idesc_bf16(BM, DH, 0, 1);
       Ph xf[12], w1f, w2f, hfr, af[2], ye;
       int xs = 0;
-      auto gemm2 = [&](int j) {
-        const int b = j % L::NA;
+      // G2(j) is issued as soon as its A buffer, Y and W2 are ready, between the K-chunks of the next
+      // tile's G1 (whose gathered chunks usually arrive later): with G2(i-1) strictly after all of
+      // G1(i), the tensor pipe and the Y read-out waited on the next tile's gathers (~1.5 k cycles
+      // per tile, trace r2d).
+      int pend = -1;   // tile whose G2 is not issued yet
+      auto gemm2 = [&](bool block) {
+        if (pend < 0) return;
+        const int j = pend, b = j % L::NA;
         const int tj = tile_at(j);
-        if (!same_expert(tile_at(j - 1), tj)) mbar_wait(bar(L::B_W2F), w2f.flip());
-        mbar_wait(bar(L::B_AFULL + 8 * b), af[b].flip());   // (NA = 1: b = 0 throughout)
-        mbar_wait(bar(L::B_YEMPTY), ye.flip() ^ 1);
+        const bool neww = !same_expert(tile_at(j - 1), tj);
+        if (block) {
+          if (neww) mbar_wait(bar(L::B_W2F), w2f.v);
+          mbar_wait(bar(L::B_AFULL + 8 * b), af[b].v);   // (NA = 1: b = 0 throughout)
+          mbar_wait(bar(L::B_YEMPTY), ye.v ^ 1);
+        } else if ((neww && !mbar_try(bar(L::B_W2F), w2f.v)) || !mbar_try(bar(L::B_AFULL + 8 * b), af[b].v) ||
+                   !mbar_try(bar(L::B_YEMPTY), ye.v ^ 1)) {
+          return;
+        }
+        if (neww) w2f.flip();
+        af[b].flip(); ye.flip();
         trace_ev(g_trace_fwd, 13, j);
         tc_fence_after();
 #pragma unroll
@@ -235,6 +249,7 @@ expert_fwd_sm100_kernel(const __grid_constant__ CUtensorMap w1map, const __grid_
         mma_commit(bar(L::B_G2DONE + 8 * b));
         trace_ev(g_trace_fwd, 14, j);
         if (!same_expert(tj, tile_at(j + 1))) mma_commit(bar(L::B_W2E));
+        pend = -1;
       };
       int i = 0;
       for (;; ++i) {
@@ -245,7 +260,8 @@ expert_fwd_sm100_kernel(const __grid_constant__ CUtensorMap w1map, const __grid_
         trace_ev(g_trace_fwd, 10, i);
         tc_fence_after();
         for (int kb = 0; kb < KB1; ++kb) {
-          mbar_wait(bar(L::B_XFULL + 8 * xs), xf[xs].flip());
+          while (!mbar_try(bar(L::B_XFULL + 8 * xs), xf[xs].v)) gemm2(false);
+          xf[xs].flip();
           trace_ev(g_trace_fwd, 11, i * 16 + kb);
           tc_fence_after();
 #pragma unroll
@@ -257,9 +273,10 @@ expert_fwd_sm100_kernel(const __grid_constant__ CUtensorMap w1map, const __grid_
         }
         mma_commit(bar(L::B_HFULL));
         if (!same_expert(ti, tile_at(i + 1))) mma_commit(bar(L::B_W1E));
-        if (i >= 1) gemm2(i - 1);
+        gemm2(true);      // G2(i-1), if the chunks of G1(i) all arrived before its A buffer
+        pend = i;
       }
-      if (i >= 1) gemm2(i - 1);
+      gemm2(true);
     }
   } else if (warp >= kGeluWarp0 && warp < kYWarp0) {
     asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kGeluRegs));

@@ -47,6 +47,17 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
 #endif
 }
 
+// one bounded try_wait: true once the phase with parity `phase` has completed; suspends for at most
+// about hint_ns otherwise (lets a single issuing thread interleave several waits)
+__device__ __forceinline__ bool mbar_try(uint64_t* bar, uint32_t phase) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, 256;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}" : "=r"(ok) : "r"(smem_u32(bar)), "r"(phase) : "memory");
+  return ok != 0;
+}
+
 // one lane polls, the rest of the warp parks at __syncwarp (32x fewer try_wait issues)
 __device__ __forceinline__ void mbar_wait_warp(uint64_t* bar, uint32_t phase) {
   if ((threadIdx.x & 31) == 0) mbar_wait(bar, phase);
