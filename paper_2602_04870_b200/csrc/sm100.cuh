@@ -58,6 +58,16 @@ __device__ __forceinline__ bool mbar_try(uint64_t* bar, uint32_t phase) {
   return ok != 0;
 }
 
+// non-blocking probe of a phase
+__device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t phase) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}" : "=r"(ok) : "r"(smem_u32(bar)), "r"(phase) : "memory");
+  return ok != 0;
+}
+
 // one lane polls, the rest of the warp parks at __syncwarp (32x fewer try_wait issues)
 __device__ __forceinline__ void mbar_wait_warp(uint64_t* bar, uint32_t phase) {
   if ((threadIdx.x & 31) == 0) mbar_wait(bar, phase);
