@@ -38,9 +38,8 @@ __device__ TraceBuf g_trace_fwd;     // profiling aid (MHL_TRACE_FWD=<file>), of
 
 constexpr int BM = kExpertBM;        // 128 rows = MMA M
 // Warp roles, warpgroup-aligned so the producers can hand registers to the GELU epilogue (setmaxnreg):
-constexpr int kProdWarps = 8;         // warps 0-7: producers (warpgroups 0-1, for setmaxnreg)
-constexpr int kOwners = 6;            // warps 0-5 each own one X ring stage (a whole 16 KB chunk)
-constexpr int kWLoadWarp = 7;         // warp 7 loads W1_e / W2_e (warp 6 only donates registers)
+constexpr int kProdWarps = 8;         // warps 0-7: producers, in 4 pairs (a pair fills one X chunk)
+constexpr int kOwners = kProdWarps / 2;
 constexpr int kGeluWarp0 = 8;         // warps 8-15: GELU epilogue (2 per lane quadrant, column halves)
 constexpr int kYWarp0 = 16;           // warps 16-19: Y epilogue (one per lane quadrant)
 constexpr int kMmaWarp = 20;          // warp 20: MMA issuer + TMEM owner
@@ -55,14 +54,17 @@ static_assert(8 * (kLaunchRegs - kProdRegs) >= 8 * (kGeluRegs - kLaunchRegs),
 static_assert(6 * 32 * kLaunchRegs <= 16384, "expert fwd: launch register count does not fit sub-partition 0");
 constexpr int kGeluThreads = 256, kYThreads = 128;
 constexpr int kXChunk = BM * 128;    // one 64-column K-chunk of the gathered X tile (16 KB)
+constexpr int kYStage = BM * 128;    // one 64-column block of the Y tile (16 KB)
 
 template <int DH, int DE>
 struct FwdL {
   static constexpr int WB = DE * DH * 2;
-  static constexpr int W1 = 0, W2 = WB, X = 2 * WB;
-  // chunk c -> stage c % XS = owner warp c % kOwners: a stage is only ever refilled by its owner
-  static constexpr int XS = kOwners;
-  static_assert(X + XS * kXChunk <= 224 * 1024, "X ring does not fit");
+  static constexpr int W1 = 0, W2 = WB, YS = 2 * WB, X = YS + 2 * kYStage;
+  static constexpr int XS_RAW = (224 * 1024 - X) / kXChunk;
+  // chunk c -> stage c % XS, pair c % kOwners; XS >= kOwners keeps the EMPTY parity exact (a
+  // pair's previous chunk waited for the in-order consumption of chunk c - kOwners - XS >= c - 2 XS)
+  static constexpr int XS = XS_RAW > 4 ? 4 : XS_RAW;   // X ring stages (deeper rings measured slower)
+  static_assert(XS >= kOwners, "X ring too small");
   static constexpr int CTRL = X + XS * kXChunk;
   static constexpr int B_XFULL = CTRL, B_XEMPTY = B_XFULL + 8 * XS;
   static constexpr int B_W1F = B_XEMPTY + 8 * XS, B_W1E = B_W1F + 8, B_W2F = B_W1E + 8, B_W2E = B_W2F + 8;
@@ -83,10 +85,26 @@ struct Ph {   // mbarrier phase bit
   __device__ uint32_t flip() { uint32_t o = v; v ^= 1u; return o; }
 };
 
+__device__ __forceinline__ void tma_store_2d(const void* tmap, uint32_t src, int c0, int c1) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(tmap), "r"(src),
+               "r"(c0), "r"(c1)
+               : "memory");
+}
+__device__ __forceinline__ void tma_store_2d_hint(const void* tmap, uint32_t src, int c0, int c1, uint64_t pol) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group.L2::cache_hint [%0, {%2, %3}], [%1], %4;"
+               ::"l"(tmap), "r"(src), "r"(c0), "r"(c1), "l"(pol)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() { asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory"); }
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+
 template <int DH, int DE>
 __global__ void __launch_bounds__(kThreads, 1)
 expert_fwd_sm100_kernel(const __grid_constant__ CUtensorMap w1map, const __grid_constant__ CUtensorMap w2map,
-                        const __grid_constant__ CUtensorMap xmap, Routing rt, uint8_t* __restrict__ yout) {
+                        const __grid_constant__ CUtensorMap ymap, const __grid_constant__ CUtensorMap xmap,
+                        Routing rt) {
   using L = FwdL<DH, DE>;
   constexpr int XS = L::XS, KB1 = DH / 64;
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -106,7 +124,7 @@ expert_fwd_sm100_kernel(const __grid_constant__ CUtensorMap w1map, const __grid_
     for (int b = 0; b < 2; ++b) { mbar_init(bar(L::B_AFULL + 8 * b), kGeluThreads); mbar_init(bar(L::B_G2DONE + 8 * b), 1); }
     mbar_init(bar(L::B_YEMPTY), kYThreads);
     fence_mbar_init();
-    tma_prefetch_desc(&w1map); tma_prefetch_desc(&w2map); tma_prefetch_desc(&xmap);
+    tma_prefetch_desc(&w1map); tma_prefetch_desc(&w2map); tma_prefetch_desc(&ymap); tma_prefetch_desc(&xmap);
   }
   if (warp == kMmaWarp) tmem_alloc<512>(s_tmem);
   tc_fence_before();
@@ -134,61 +152,65 @@ expert_fwd_sm100_kernel(const __grid_constant__ CUtensorMap w1map, const __grid_
 
   if (warp < kProdWarps) {
     // ================================================================ producers (8 warps)
-    // Chunk c of this CTA's X stream (tile c / KB1, column block c % KB1) goes to ring stage c % XS,
-    // brought by its owner warp c % kOwners (= the stage): 32 lanes x one TMA gather4 of 4 sub-token
-    // rows each.  The six-stage ring holds 1.5 tiles, so the next tile's gathers are in flight while
-    // G1 of this one runs (a one-tile ring left G1 waiting ~1.8 k cycles per tile on gathers, trace
-    // r2e).  Warp 7 loads the weights, so no gather waits behind a weight-buffer release.
+    // Chunk c of this CTA's X stream (tile c / KB1, column block c % KB1) goes to ring stage
+    // c % XS and is brought by warp pair c % kOwners (XS is a multiple of kOwners, so a stage is
+    // only ever refilled by the pair that filled it before): lanes 0-15 of each warp of the pair
+    // issue one TMA gather4 of 4 sub-token rows each (warp 2p+h owns tile rows 64h..64h+63).  More
+    // warps issuing gathers raise the SM's gather rate (tools/ring_probe.cu mech 6).  Warp 0 lane 0
+    // also issues the weight TMAs.
     asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kProdRegs));
-    if (warp == kWLoadWarp) {
-      if (lane == 0) {
-        Ph w1e, w2e;
-        for (int i = 0;; ++i) {
-          const int ti = tile_at(i);
-          if (ti < 0) break;
-          if (same_expert(tile_at(i - 1), ti)) continue;
-          const Tile tl = tiles[ti];
-          mbar_wait(bar(L::B_W1E), w1e.flip() ^ 1);   // the previous run's last G1 has read W1
-          load_w(&w1map, L::W1, bar(L::B_W1F), tl);
-          mbar_wait(bar(L::B_W2E), w2e.flip() ^ 1);   // the previous run's last G2 has read W2
-          load_w(&w2map, L::W2, bar(L::B_W2F), tl);
-        }
+    const int pw = warp;
+    const int owner = pw >> 1, lrow = (pw & 1) * 64 + 4 * (lane & 15);
+    Ph w1e, w2e;
+    int cnt = 0;
+    int nx[4] = {0, 0, 0, 0};
+    {
+      const int t0 = tile_at(0);
+      if (t0 >= 0) {
+        const Tile tl = tiles[t0];
+        const int32_t* tk = rt.tok_s + (size_t)tl.head * rt.Rp + tl.row0 + lrow;
+        nx[0] = tk[0]; nx[1] = tk[1]; nx[2] = tk[2]; nx[3] = tk[3];
       }
-    } else if (warp < kOwners) {
-      const int owner = warp, lrow = 4 * lane;
-      int cnt = 0;
-      int nx[4] = {0, 0, 0, 0};
-      {
-        const int t0 = tile_at(0);
-        if (t0 >= 0) {
-          const Tile tl = tiles[t0];
-          const int32_t* tk = rt.tok_s + (size_t)tl.head * rt.Rp + tl.row0 + lrow;
-          nx[0] = tk[0]; nx[1] = tk[1]; nx[2] = tk[2]; nx[3] = tk[3];
+    }
+    for (int i = 0;; ++i) {
+      const int ti = tile_at(i);
+      if (ti < 0) {
+        if (pw == 0 && i >= 1 && lane == 0 && !same_expert(tile_at(i - 2), tile_at(i - 1))) {
+          mbar_wait(bar(L::B_W2E), w2e.flip() ^ 1);
+          load_w(&w2map, L::W2, bar(L::B_W2F), tiles[tile_at(i - 1)]);
         }
+        break;
       }
-      for (int i = 0;; ++i) {
-        const int ti = tile_at(i);
-        if (ti < 0) break;
-        const Tile tl = tiles[ti];
-        const int r0 = nx[0], r1 = nx[1], r2 = nx[2], r3 = nx[3];
-        const int tn = tile_at(i + 1);
-        if (tn >= 0) {     // next tile's token ids, loaded while this tile's chunks are issued
-          const Tile tnl = tiles[tn];
-          const int32_t* tk = rt.tok_s + (size_t)tnl.head * rt.Rp + tnl.row0 + lrow;
-          nx[0] = tk[0]; nx[1] = tk[1]; nx[2] = tk[2]; nx[3] = tk[3];
+      const Tile tl = tiles[ti];
+      const int r0 = nx[0], r1 = nx[1], r2 = nx[2], r3 = nx[3];
+      const int tn = tile_at(i + 1);
+      if (tn >= 0) {     // next tile's token ids, loaded while this tile's chunks are issued
+        const Tile tnl = tiles[tn];
+        const int32_t* tk = rt.tok_s + (size_t)tnl.head * rt.Rp + tnl.row0 + lrow;
+        nx[0] = tk[0]; nx[1] = tk[1]; nx[2] = tk[2]; nx[3] = tk[3];
+      }
+      if (pw == 0 && lane == 0 && !same_expert(tile_at(i - 1), ti)) {
+        mbar_wait(bar(L::B_W1E), w1e.flip() ^ 1);
+        load_w(&w1map, L::W1, bar(L::B_W1F), tl);
+      }
+      __syncwarp();
+      for (int kb = 0; kb < KB1; ++kb, ++cnt) {
+        if (cnt % kOwners != owner) continue;
+        const int xs = cnt % XS;
+        uint64_t* full = bar(L::B_XFULL + 8 * xs);
+        if (lane == 0) {
+          mbar_wait(bar(L::B_XEMPTY + 8 * xs), ((cnt / XS) & 1) ^ 1);
+          if ((pw & 1) == 0) mbar_expect_tx(full, kXChunk);
         }
-        for (int kb = 0; kb < KB1; ++kb, ++cnt) {
-          if (cnt % kOwners != owner) continue;
-          const int xs = owner;
-          uint64_t* full = bar(L::B_XFULL + 8 * xs);
-          if (lane == 0) {
-            mbar_wait(bar(L::B_XEMPTY + 8 * xs), ((cnt / XS) & 1) ^ 1);
-            mbar_expect_tx(full, kXChunk);
-          }
-          __syncwarp();
+        __syncwarp();
+        if (lane < 16)
           tma_gather4(sb + L::X + xs * kXChunk + lrow * 128, &xmap, (int)tl.head * DH + kb * 64, r0, r1, r2, r3,
                       full);
-        }
+      }
+      // W2 of the previous tile if it started a new expert run (read by G2(i-1), issued after G1(i))
+      if (pw == 0 && lane == 0 && i >= 1 && !same_expert(tile_at(i - 2), tile_at(i - 1))) {
+        mbar_wait(bar(L::B_W2E), w2e.flip() ^ 1);
+        load_w(&w2map, L::W2, bar(L::B_W2F), tiles[tile_at(i - 1)]);
       }
     }
   } else if (warp == kMmaWarp) {
@@ -196,28 +218,14 @@ expert_fwd_sm100_kernel(const __grid_constant__ CUtensorMap w1map, const __grid_
     if (lane == 0) {
       constexpr uint32_t ID1 = idesc_bf16(BM, DE, 0, 0);
       constexpr uint32_t ID2 = idesc_bf16(BM, DH, 0, 1);
-      Ph w1f, w2f, hfr, af[2], ye;
-      int xs = 0, xc = 0;   // ring stage, chunk count (phase of chunk c: (c / XS) & 1)
-      // G2(j) is issued as soon as its A buffer, Y and W2 are ready, between the K-chunks of the next
-      // tile's G1 (whose gathered chunks usually arrive later): with G2(i-1) strictly after all of
-      // G1(i), the tensor pipe and the Y read-out waited on the next tile's gathers (~1.5 k cycles
-      // per tile, trace r2d).
-      int pend = -1;   // tile whose G2 is not issued yet
-      auto gemm2 = [&](bool block) {
-        if (pend < 0) return;
-        const int j = pend, b = j % L::NA;
+      Ph xf[12], w1f, w2f, hfr, af[2], ye;
+      int xs = 0;
+      auto gemm2 = [&](int j) {
+        const int b = j % L::NA;
         const int tj = tile_at(j);
-        const bool neww = !same_expert(tile_at(j - 1), tj);
-        if (block) {
-          if (neww) mbar_wait(bar(L::B_W2F), w2f.v);
-          mbar_wait(bar(L::B_AFULL + 8 * b), af[b].v);   // (NA = 1: b = 0 throughout)
-          mbar_wait(bar(L::B_YEMPTY), ye.v ^ 1);
-        } else if ((neww && !mbar_test(bar(L::B_W2F), w2f.v)) || !mbar_test(bar(L::B_AFULL + 8 * b), af[b].v) ||
-                   !mbar_test(bar(L::B_YEMPTY), ye.v ^ 1)) {
-          return;
-        }
-        if (neww) w2f.flip();
-        af[b].flip(); ye.flip();
+        if (!same_expert(tile_at(j - 1), tj)) mbar_wait(bar(L::B_W2F), w2f.flip());
+        mbar_wait(bar(L::B_AFULL + 8 * b), af[b].flip());   // (NA = 1: b = 0 throughout)
+        mbar_wait(bar(L::B_YEMPTY), ye.flip() ^ 1);
         trace_ev(g_trace_fwd, 13, j);
         tc_fence_after();
 #pragma unroll
@@ -227,7 +235,6 @@ expert_fwd_sm100_kernel(const __grid_constant__ CUtensorMap w1map, const __grid_
         mma_commit(bar(L::B_G2DONE + 8 * b));
         trace_ev(g_trace_fwd, 14, j);
         if (!same_expert(tj, tile_at(j + 1))) mma_commit(bar(L::B_W2E));
-        pend = -1;
       };
       int i = 0;
       for (;; ++i) {
@@ -238,8 +245,7 @@ expert_fwd_sm100_kernel(const __grid_constant__ CUtensorMap w1map, const __grid_
         trace_ev(g_trace_fwd, 10, i);
         tc_fence_after();
         for (int kb = 0; kb < KB1; ++kb) {
-          const uint32_t xph = (uint32_t)(xc / XS) & 1u;
-          while (!mbar_try(bar(L::B_XFULL + 8 * xs), xph)) gemm2(false);
+          mbar_wait(bar(L::B_XFULL + 8 * xs), xf[xs].flip());
           trace_ev(g_trace_fwd, 11, i * 16 + kb);
           tc_fence_after();
 #pragma unroll
@@ -248,14 +254,12 @@ expert_fwd_sm100_kernel(const __grid_constant__ CUtensorMap w1map, const __grid_
                      sdesc_sw128(sb + L::W1 + kb * DE * 128 + ks * 32, 16, 1024), ID1, (kb | ks) ? 1u : 0u);
           mma_commit(bar(L::B_XEMPTY + 8 * xs));
           if (++xs == XS) xs = 0;
-          ++xc;
         }
         mma_commit(bar(L::B_HFULL));
         if (!same_expert(ti, tile_at(i + 1))) mma_commit(bar(L::B_W1E));
-        gemm2(true);      // G2(i-1), if the chunks of G1(i) all arrived before its A buffer
-        pend = i;
+        if (i >= 1) gemm2(i - 1);
       }
-      gemm2(true);
+      if (i >= 1) gemm2(i - 1);
     }
   } else if (warp >= kGeluWarp0 && warp < kYWarp0) {
     asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kGeluRegs));
@@ -343,37 +347,54 @@ expert_fwd_sm100_kernel(const __grid_constant__ CUtensorMap w1map, const __grid_
     }
   } else if (warp >= kYWarp0 && warp < kMmaWarp) {
     // ================================================================ Y epilogue (4 warps)
-    // tile j: this warp's lane quadrant of Y (32 rows x DH columns) -> bf16 -> Yrep, each lane its
-    // own row straight from registers (32-byte st.global.v8 = whole sectors; no staging smem, which
-    // the X ring takes instead).
+    // tile j: Y rows of this warp's lane quadrant (32 rows x DH columns) -> bf16 -> SW128 smem
+    // stage (64-column blocks, two stages) -> TMA bulk store of the 32-row slab.
     const int q = warp & 3;
     const uint32_t lane_off = (uint32_t)(q * 32) << 16;
     Ph gd[2];
+    int ys = 0;   // running count of Y blocks stored by this warp (selects the smem stage)
     for (int j = 0;; ++j) {
       const int tj = tile_at(j);
       if (tj < 0) break;
       const int b = j % L::NA;
       const Tile tl = tiles[tj];
-      uint8_t* yrow = yout + ((size_t)tl.head * rt.Rp + tl.row0 + q * 32 + lane) * (DH * 2);
       mbar_wait_warp(bar(L::B_G2DONE + 8 * b), gd[b].flip());
       if (q == 0 && lane == 0) trace_ev(g_trace_fwd, 23, j);
       tc_fence_after();
 #pragma unroll 1
-      for (int cb = 0; cb < DH / 32; ++cb) {
-        uint32_t v[32], w[16];
-        tmem_ld32(tmem + L::T_Y + lane_off + cb * 32, v);
+      for (int cb = 0; cb < DH / 64; ++cb, ++ys) {
+        const int st = ys & 1;
+        uint32_t v[32], w[32];
+        tmem_ld32(tmem + L::T_Y + lane_off + cb * 64, v);
         tmem_ld_wait();
-        if (cb == DH / 32 - 1) {
+#pragma unroll
+        for (int u = 0; u < 16; ++u) w[u] = pack_bf16x2(__uint_as_float(v[2 * u]), __uint_as_float(v[2 * u + 1]));
+        tmem_ld32(tmem + L::T_Y + lane_off + cb * 64 + 32, v);
+        tmem_ld_wait();
+        if (cb == DH / 64 - 1) {
           tc_fence_before();
           mbar_arrive(bar(L::B_YEMPTY));
           if (q == 0 && lane == 0) trace_ev(g_trace_fwd, 24, j);
         }
 #pragma unroll
-        for (int u = 0; u < 16; ++u) w[u] = pack_bf16x2(__uint_as_float(v[2 * u]), __uint_as_float(v[2 * u + 1]));
-        st_global_v8(yrow + cb * 64, w[0], w[1], w[2], w[3], w[4], w[5], w[6], w[7]);
-        st_global_v8(yrow + cb * 64 + 32, w[8], w[9], w[10], w[11], w[12], w[13], w[14], w[15]);
+        for (int u = 0; u < 16; ++u) w[16 + u] = pack_bf16x2(__uint_as_float(v[2 * u]), __uint_as_float(v[2 * u + 1]));
+        // the slab store issued from this stage two blocks ago must have read it
+        if (lane == 0) bulk_wait_read<1>();
+        __syncwarp();
+        uint8_t* sp = smem + L::YS + st * kYStage + q * 4096;
+#pragma unroll
+        for (int u = 0; u < 32; u += 4)
+          *reinterpret_cast<uint4*>(sp + kmaj_off(lane, 2 * u, 32)) = make_uint4(w[u], w[u + 1], w[u + 2], w[u + 3]);
+        fence_proxy_async();
+        __syncwarp();
+        if (lane == 0) {
+          tma_store_2d(&ymap, sb + L::YS + st * kYStage + q * 4096, cb * 64,
+                       (int)((size_t)tl.head * rt.Rp + tl.row0 + q * 32));
+          bulk_commit();
+        }
       }
     }
+    if (lane == 0) bulk_wait_all();
   }
   tc_fence_before();
   __syncthreads();
@@ -383,11 +404,12 @@ expert_fwd_sm100_kernel(const __grid_constant__ CUtensorMap w1map, const __grid_
 template <int DH, int DE>
 bool launch_t(const Routing& rt, const void* Xs, int64_t ldx, const void* W1, const void* W2, void* Yrep, int num_sms,
               cudaStream_t s) {
-  CUtensorMap w1m, w2m, xm;
+  CUtensorMap w1m, w2m, ym, xm;
   // sub-token gather map: T+1 rows (row T all-zero), box = 64 columns x 1 row (TMA gather4)
   if (!make_tmap_2d_bf16(&xm, Xs, (uint64_t)rt.T + 1, (uint64_t)rt.H * DH, (uint64_t)ldx * 2, 1, 64)) return false;
   if (!make_tmap_2d_bf16(&w1m, W1, (uint64_t)rt.H * rt.N_e * DE, DH, (uint64_t)DH * 2, DE, 64)) return false;
   if (!make_tmap_2d_bf16(&w2m, W2, (uint64_t)rt.H * rt.N_e * DE, DH, (uint64_t)DH * 2, DE, 64)) return false;
+  if (!make_tmap_2d_bf16(&ym, Yrep, (uint64_t)rt.H * rt.Rp, DH, (uint64_t)DH * 2, 32, 64)) return false;
   auto kern = expert_fwd_sm100_kernel<DH, DE>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, FwdL<DH, DE>::BYTES);
   static const char* trace_path = getenv("MHL_TRACE_FWD");
@@ -399,7 +421,7 @@ bool launch_t(const Routing& rt, const void* Xs, int64_t ldx, const void* W1, co
     TraceBuf tb{tbuf, 0};
     cudaMemcpyToSymbolAsync(g_trace_fwd, &tb, sizeof(tb), 0, cudaMemcpyHostToDevice, s);
   }
-  kern<<<num_sms, kThreads, FwdL<DH, DE>::BYTES, s>>>(w1m, w2m, xm, rt, (uint8_t*)Yrep);
+  kern<<<num_sms, kThreads, FwdL<DH, DE>::BYTES, s>>>(w1m, w2m, ym, xm, rt);
   if (trace_path) {
     TraceBuf tb{nullptr, 0};
     cudaMemcpyToSymbolAsync(g_trace_fwd, &tb, sizeof(tb), 0, cudaMemcpyHostToDevice, s);
