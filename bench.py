@@ -310,6 +310,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample", type=int, default=256)
+    ap.add_argument("--graph", action="store_true", help="replay the step as one CUDA graph (default for fwd-only configs)")
+    ap.add_argument("--no-graph", action="store_true")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
 
@@ -362,21 +364,44 @@ def main():
     dx = torch.empty(T_loc, cfg.d, dtype=td, device=dev)
     stream = torch.cuda.current_stream(dev)
 
-    def step():
-        L.forward(x, Wd, out=out, stream=stream)
+    def step(st=stream):
+        L.forward(x, Wd, out=out, stream=st)
         if not cfg.fwd_only:      # BASELINE's "small" config is forward only
-            L.backward(x, Wd, dout, grads, dx=dx, stream=stream)
+            L.backward(x, Wd, dout, grads, dx=dx, stream=st)
 
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize(dev)
     L.check_status()
+    n0 = L.launches()
+    step()
+    torch.cuda.synchronize(dev)
+    launches_per_step = L.launches() - n0
+
+    # the forward-only small config is launch-bound unless graphed: capture one step
+    # (every launch of the library, cuBLASLt included, on one stream) and replay it
+    use_graph = G == 1 and not args.no_graph and (args.graph or cfg.fwd_only)
+    graph = None
+    if use_graph:
+        gs = torch.cuda.Stream(dev)
+        gs.wait_stream(stream)
+        with torch.cuda.stream(gs):
+            step(gs)
+        torch.cuda.synchronize(dev)
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph, stream=gs):
+            step(torch.cuda.current_stream(dev))
+        torch.cuda.synchronize(dev)
+        for _ in range(3):
+            graph.replay()
+        torch.cuda.synchronize(dev)
 
     # ---- timed region (device-resident inputs)
     clocks = ClockSampler(local_rank)
     clocks.start()
     time.sleep(0.3)
-    C.mhl_set_step_timing(L.plan, True)
+    if graph is None:
+        C.mhl_set_step_timing(L.plan, True)
     launches0 = L.launches()
     a2a0 = C.mhl_a2a_bytes_posted(L.plan)
     nvl0 = nvlink_bytes(local_rank) if G > 1 else None
@@ -386,13 +411,16 @@ def main():
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     ev0.record(stream)
     for _ in range(args.steps):
-        step()
+        if graph is not None:
+            graph.replay()
+        else:
+            step()
     ev1.record(stream)
     torch.cuda.synchronize(dev)
     if G > 1:
         dist.barrier()
     ms = ev0.elapsed_time(ev1)
-    launches = L.launches() - launches0
+    launches = (L.launches() - launches0) if graph is None else launches_per_step * args.steps
     a2a = (C.mhl_a2a_bytes_posted(L.plan) - a2a0) / args.steps
     nvl1 = nvlink_bytes(local_rank) if G > 1 else None
     nvlink = None
@@ -403,9 +431,15 @@ def main():
             nvlink.update(tx_bytes_per_step=(nvl1[0] - nvl0[0]) / args.steps,
                           rx_bytes_per_step=(nvl1[1] - nvl0[1]) / args.steps,
                           tx_gbs=(nvl1[0] - nvl0[0]) / (ms / 1e3) / 1e9, source="NVML NVLINK_THROUGHPUT_DATA")
+    clk = clocks.stop()
+    if graph is not None:
+        # per-span breakdown from an eager pass (span events cannot sit inside the replayed graph)
+        C.mhl_set_step_timing(L.plan, True)
+        for _ in range(args.steps):
+            step()
+        torch.cuda.synchronize(dev)
     steps_t = C.mhl_step_times(L.plan)
     C.mhl_set_step_timing(L.plan, False)
-    clk = clocks.stop()
     if G > 1:
         t = torch.tensor([ms], device=dev, dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -495,7 +529,9 @@ def main():
             "vs_baseline": None, "dtype": cfg.dtype, "data": "synthetic (seeded, paper init P:1995-P:1996)",
             "config": {"workload": workload_desc(cfg, T_loc), "T_loc": T_loc, "global_tokens": G * T_loc,
                        "parallelism": f"hp{G}", "l2": "inputs larger than L2 (per-step working set >> 126 MB)",
-                       "kernels": "simt-reference" if args.simt else "default"},
+                       "kernels": "simt-reference" if args.simt else "default",
+                       "cuda_graph": bool(graph is not None),
+                       "span_times": "eager pass after the graph-timed region" if graph is not None else "timed region"},
             "layer_tflops": layer_tflops,
             # the metric's "% tcgen05 peak": whole-layer algorithmic FLOPs / step time vs the measured
             # burst bf16 matmul peak and vs the 2.25 PF/s nominal dense bf16 figure

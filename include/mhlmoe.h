@@ -234,6 +234,11 @@ MHL_API mhl_status mhl_set_step_timing(mhl_plan plan, int enable);
 MHL_API int32_t mhl_step_times(mhl_plan plan, char* names, size_t names_cap, double* ms, int32_t* calls,
                                int32_t max_steps);
 
+/* Fault injection (test-suite sensitivity): if the environment variable
+ * MHL_FAULT_INJECT is set when hp_plan runs, that plan perturbs one step's output by a factor
+ * (1 + 1e-3): "gates" (after F3), "out" (after F8), "dx" (after B1) or "dW1" (after B5); any other
+ * non-empty value makes hp_plan fail with MHL_ERR_INVALID_ARGUMENT.  Never set in production. */
+
 /* Which kernel implementation ran each step (bits OR-ed in at launch since the plan was
  * created or last reset): lets callers and tests assert that a shape took the tcgen05
  * path instead of the SIMT reference kernels, which shapes outside the tensor-core kernels'

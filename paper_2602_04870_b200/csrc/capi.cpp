@@ -283,6 +283,9 @@ struct mhl_plan_s {
   cudaEvent_t ev_prod = nullptr, ev_comm = nullptr;
   std::atomic<uint64_t> launches{0};
   std::atomic<uint32_t> paths{0};     // MHL_PATH_* bits of the kernels launched (mhl_kernel_paths)
+  // fault injection: MHL_FAULT_INJECT=gates|out|dx|dW1 at plan creation scales that
+  // output by (1 + 1e-3) so the conformance suite can be shown to fail
+  int fault = 0;   // 0 none, 1 gates (after F3), 2 out (after F8), 3 dx (after B1), 4 dW1 (after B5)
   uint64_t a2a_bytes_posted = 0;
   // optional per-step CUDA-event timing (mhl_set_step_timing)
   bool timing = false;
@@ -596,6 +599,7 @@ mhl_status moe_forward_local(mhl_plan p, const RankPtrs& R, void* yout, cudaStre
       p->paths |= MHL_PATH_ROUTER_SIMT;
     }
   }
+  if (p->fault == 1) mhl::launch_scale(0, gate, (int64_t)m.H * m.R, 1.001f, s);
   {
     MHL_SPAN("F4_cluster");
     mhl::launch_cluster(m.H, m.T_g, m.k, m.N_e, idx, gate, hist, (int32_t*)(R.ws + F.tilepref),
@@ -800,6 +804,11 @@ mhl_status hp_plan(const mhl_config* cfg, const uint8_t* nccl_id, mhl_plan* out)
   if (cudaGetDeviceProperties(&prop, dev) != cudaSuccess) return cleanup(fail(MHL_ERR_CUDA, "cudaGetDeviceProperties"));
   if (prop.major != 10) return cleanup(fail(MHL_ERR_UNSUPPORTED, "this library is built for sm_100a (B200)"));
   p->num_sms = prop.multiProcessorCount;
+  if (const char* f = getenv("MHL_FAULT_INJECT")) {
+    const std::string v(f);
+    p->fault = v == "gates" ? 1 : v == "out" ? 2 : v == "dx" ? 3 : v == "dW1" ? 4 : 0;
+    if (p->fault == 0 && !v.empty()) return cleanup(fail(MHL_ERR_INVALID_ARGUMENT, "MHL_FAULT_INJECT: gates|out|dx|dW1"));
+  }
   if (cublasLtCreate(&p->lt) != CUBLAS_STATUS_SUCCESS) return cleanup(fail(MHL_ERR_CUDA, "cublasLtCreate"));
   if (cudaMalloc(&p->blas_ws, p->blas_ws_bytes) != cudaSuccess) return cleanup(fail(MHL_ERR_CUDA, "cudaMalloc"));
   if (cudaMalloc(&p->dflag, 16) != cudaSuccess || cudaMemset(p->dflag, 0, 16) != cudaSuccess)
@@ -848,8 +857,9 @@ mhl_status hp_plan_destroy(mhl_plan p) {
   return MHL_OK;
 }
 
-mhl_status mhlmoe_forward(mhl_plan p, const void* x, const mhl_weights* w, void* out, void* saved, void* workspace,
-                          size_t workspace_bytes, int32_t* topk_idx, float* gates, void* stream) {
+namespace {
+mhl_status forward_impl(mhl_plan p, const void* x, const mhl_weights* w, void* out, void* saved, void* workspace,
+                        size_t workspace_bytes, int32_t* topk_idx, float* gates, void* stream) {
   MHL_TRY(check_ws(p, saved, workspace, workspace_bytes));
   if (!x || !w || !out || !w->W_in || !w->W_out || !w->W_r || !w->bias || !w->W1 || !w->W2)
     return fail(MHL_ERR_INVALID_ARGUMENT, "NULL tensor");
@@ -932,8 +942,8 @@ mhl_status mhlmoe_forward(mhl_plan p, const void* x, const mhl_weights* w, void*
   return check_kernels(p);
 }
 
-mhl_status mhlmoe_backward(mhl_plan p, const void* x, const mhl_weights* w, const void* d_out, const void* saved,
-                           void* dx, const mhl_grads* grads, void* workspace, size_t workspace_bytes, void* stream) {
+mhl_status backward_impl(mhl_plan p, const void* x, const mhl_weights* w, const void* d_out, const void* saved,
+                         void* dx, const mhl_grads* grads, void* workspace, size_t workspace_bytes, void* stream) {
   MHL_TRY(check_ws(p, saved, workspace, workspace_bytes));
   if (!x || !w || !d_out || !dx || !grads) return fail(MHL_ERR_INVALID_ARGUMENT, "NULL tensor");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
@@ -1024,6 +1034,28 @@ mhl_status mhlmoe_backward(mhl_plan p, const void* x, const mhl_weights* w, cons
       MHL_TRY(gemm(true, false, m.Din, m.d, m.T_loc, R.ws + B.dXs, m.Din, R.x, m.d, grads->dW_in, m.d, true,
                    v == 0 ? 0.0f : 1.0f));
   }
+  return check_kernels(p);
+}
+
+}  // namespace
+
+mhl_status mhlmoe_forward(mhl_plan p, const void* x, const mhl_weights* w, void* out, void* saved, void* workspace,
+                          size_t workspace_bytes, int32_t* topk_idx, float* gates, void* stream) {
+  MHL_TRY(forward_impl(p, x, w, out, saved, workspace, workspace_bytes, topk_idx, gates, stream));
+  if (p->fault == 2)
+    mhl::launch_scale(p->m.dtype, out, p->m.T_loc * (p->m.loopback ? p->m.G : 1) * p->m.d, 1.001f,
+                      static_cast<cudaStream_t>(stream));
+  return check_kernels(p);
+}
+
+mhl_status mhlmoe_backward(mhl_plan p, const void* x, const mhl_weights* w, const void* d_out, const void* saved,
+                           void* dx, const mhl_grads* grads, void* workspace, size_t workspace_bytes, void* stream) {
+  MHL_TRY(backward_impl(p, x, w, d_out, saved, dx, grads, workspace, workspace_bytes, stream));
+  const Dims& m = p->m;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (p->fault == 3) mhl::launch_scale(m.dtype, dx, m.T_loc * (m.loopback ? m.G : 1) * m.d, 1.001f, s);
+  if (p->fault == 4 && grads->dW1)
+    mhl::launch_scale(0, grads->dW1, (int64_t)(m.loopback ? m.N_h : m.H) * m.N_e * m.d_e * m.d_h, 1.001f, s);
   return check_kernels(p);
 }
 

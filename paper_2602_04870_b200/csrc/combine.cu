@@ -176,4 +176,19 @@ void launch_combine_bwd(int dtype, const Routing& rt, const void* dXrep, const f
   }
 }
 
+// Fault injection ("injected fault mode perturbs one kernel by 1e-3 -> suite fails"):
+// scales a step's output tensor by f, in place.  Only launched when MHL_FAULT_INJECT names a site.
+template <typename E>
+__global__ void scale_kernel(E* __restrict__ p, int64_t n, float f) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    p[i] = from_f<E>(to_f(p[i]) * f);
+}
+
+void launch_scale(int dtype, void* p, int64_t n, float f, cudaStream_t s) {
+  if (n <= 0) return;
+  const unsigned g = (unsigned)std::min<int64_t>((n + 255) / 256, 4096);
+  if (dtype == 1) scale_kernel<bf16><<<g, 256, 0, s>>>((bf16*)p, n, f);
+  else scale_kernel<float><<<g, 256, 0, s>>>((float*)p, n, f);
+}
+
 }  // namespace mhl

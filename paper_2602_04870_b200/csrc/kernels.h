@@ -100,6 +100,9 @@ void launch_update_bias(const int32_t* load, int H, int N_e, int64_t total, floa
 void launch_combine_fwd(int dtype, const Routing& rt, const void* Yrep, int d_h, void* out, int64_t ldo,
                         cudaStream_t s, int64_t t0 = 0, int64_t nT = -1);
 
+// ---- fault injection: p[i] *= f (dtype 1 = bf16, else fp32)
+void launch_scale(int dtype, void* p, int64_t n, float f, cudaStream_t s);
+
 // ---- [G][T_loc][HD] -> [T_loc][G*HD]
 void launch_permute_blocks(int dtype, const void* src, void* dst, int G, int64_t T_loc, int64_t HD, cudaStream_t s);
 // ---- rows x row_bytes from src (pitch sp) to dst (pitch dp); 16-byte aligned (HP block placement)

@@ -520,3 +520,20 @@ def test_xs_rounding_within_r22_bound():
             u = (np.asarray(v, np.float32).view(np.uint32) >> 16).astype(np.int64)
             return np.where(u & 0x8000, -(u & 0x7FFF), u)
         assert np.all(np.abs(ordbits(g["Xs"][diff]) - ordbits(C0.Xs[diff])) == 1)
+
+
+@pytest.mark.parametrize("site,cfgname,dist", [("gates", "exact_small", "exact"), ("out", "tiny", "conf"),
+                                               ("dx", "tiny", "conf"), ("dW1", "tiny", "conf")])
+def test_fault_injection_makes_conformance_fail(site, cfgname, dist, monkeypatch):
+    """perturbing one step's output by 1e-3 (MHL_FAULT_INJECT) must make the conformance
+    check fail — gates against their 1e-5 bar, outputs / gradients against fp32's 1e-4."""
+    _need_gpu()
+    cfg = (PRESETS["tiny"] if cfgname == "tiny" else
+           LayerConfig("fi", T=512, d=256, N_h=2, d_h=128, N_e=64, k=8, d_e=64, dtype="bf16"))
+    W, x, dout = make_problem(cfg, 50, dist)
+    g = _run_gpu(cfg, W, x, dout)
+    _compare(cfg, W, x, dout, g, dist=dist)                   # unperturbed: passes
+    monkeypatch.setenv("MHL_FAULT_INJECT", site)
+    gf = _run_gpu(cfg, W, x, dout)
+    with pytest.raises(AssertionError):
+        _compare(cfg, W, x, dout, gf, dist=dist)
