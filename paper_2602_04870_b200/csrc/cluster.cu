@@ -278,6 +278,7 @@ scatter_kernel(const int32_t* __restrict__ idx, const float* __restrict__ gate, 
     const int e = act ? idx_h[r] : -1 - lane;   // unique dummy per inactive lane
     const unsigned mask = __match_any_sync(0xffffffffu, e);
     if (act && __popc(mask & ((1u << lane) - 1u)) == 0) my[e] += __popc(mask);
+    __syncwarp();   // orders this iteration's my[] updates before the next one's (racecheck-clean)
   }
   __syncthreads();
   for (int e = threadIdx.x; e < N_e; e += blockDim.x) {

@@ -83,6 +83,48 @@ __device__ __forceinline__ uint32_t ord32(float v) {
 __device__ __forceinline__ unsigned long long pack_key(float v, int idx) {
   return ((unsigned long long)ord32(v) << 32) | (unsigned long long)(~(uint32_t)idx);
 }
+// inverse of ord32 (for a canonical key: -0.0 never occurs)
+__device__ __forceinline__ float unord32(uint32_t o) {
+  return __uint_as_float((o & 0x80000000u) ? (o & 0x7FFFFFFFu) : ~o);
+}
+
+// Sorting networks on packed u64 keys held in registers (fully unrolled, N a power of two):
+// bitonic sort into descending order, and the top-N merge of two descending lists (a <- top N of
+// a and b): c_i = max(a_i, b_{N-1-i}) is bitonic, one bitonic merge sorts it.
+template <int N>
+__device__ __forceinline__ void bitonic_sort_desc(unsigned long long (&a)[N]) {
+#pragma unroll
+  for (int k = 2; k <= N; k <<= 1)
+#pragma unroll
+    for (int j = k >> 1; j > 0; j >>= 1)
+#pragma unroll
+      for (int i = 0; i < N; ++i) {
+        const int l = i ^ j;
+        if (l > i) {
+          const unsigned long long x = a[i], y = a[l];
+          const bool desc = (i & k) == 0;
+          const unsigned long long hi = x > y ? x : y, lo = x > y ? y : x;
+          a[i] = desc ? hi : lo;
+          a[l] = desc ? lo : hi;
+        }
+      }
+}
+template <int N>
+__device__ __forceinline__ void merge_top_desc(unsigned long long (&a)[N], const unsigned long long (&b)[N]) {
+#pragma unroll
+  for (int i = 0; i < N; ++i) a[i] = a[i] > b[N - 1 - i] ? a[i] : b[N - 1 - i];
+#pragma unroll
+  for (int j = N >> 1; j > 0; j >>= 1)
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      const int l = i ^ j;
+      if (l > i) {
+        const unsigned long long x = a[i], y = a[l];
+        a[i] = x > y ? x : y;
+        a[l] = x > y ? y : x;
+      }
+    }
+}
 
 #endif  // __CUDACC__
 

@@ -145,10 +145,9 @@ router_blk_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constan
         named_bar_sync(1, 128);
         cur_h = h;
       }
-      float key[KMAX], sraw[KMAX];
-      int kid[KMAX];
-#pragma unroll
-      for (int j = 0; j < KMAX; ++j) { key[j] = -INFINITY; sraw[j] = 0.f; kid[j] = 0; }   // line 4 (R17)
+      // running top-KMAX as packed u64 keys: each KMAX-wide group of a block's scores is
+      // bitonic-sorted and merged (branch-free; see router_sm100.cu)
+      unsigned long long top[KMAX];
       float chk = 0.f;
       for (int b = 0; b < nblk; ++b, ++q) {              // line 5: expert blocks in index order
         const int tbuf = q % kNB;
@@ -161,25 +160,31 @@ router_blk_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constan
           tmem_ld_wait();
           if (c0 + 32 >= EB) { tc_fence_before(); mbar_arrive(&tempty[tbuf]); }
 #pragma unroll
-          for (int j = 0; j < 32; ++j) {
-            const float s = __uint_as_float(v[j]);
-            const int e = b * EB + c0 + j;
-            float kf = s + s_bias[e];
-            chk = fmaf(kf, 0.f, chk);
-            if (kf > key[KMAX - 1]) {                    // lines 8-10: merge into the running top-k
-              float sv = s;
-              int ki = e;
+          for (int g0 = 0; g0 < 32; g0 += KMAX) {
+            unsigned long long blk[KMAX];
 #pragma unroll
-              for (int u = 0; u < KMAX; ++u) {
-                const bool sw = kf > key[u];
-                const float tk = key[u], ts = sraw[u];
-                const int ti2 = kid[u];
-                key[u] = sw ? kf : tk; sraw[u] = sw ? sv : ts; kid[u] = sw ? ki : ti2;
-                kf = sw ? tk : kf;     sv = sw ? ts : sv;     ki = sw ? ti2 : ki;
-              }
+            for (int u = 0; u < KMAX; ++u) {
+              const int e = b * EB + c0 + g0 + u;
+              const float kf = __uint_as_float(v[g0 + u]) + s_bias[e];   // line 7
+              chk = fmaf(kf, 0.f, chk);
+              blk[u] = pack_key(kf, e);                                  // line 8
+            }
+            bitonic_sort_desc<KMAX>(blk);                                // line 9
+            if (b == 0 && c0 == 0 && g0 == 0) {
+#pragma unroll
+              for (int u = 0; u < KMAX; ++u) top[u] = blk[u];
+            } else {
+              merge_top_desc<KMAX>(top, blk);                            // line 10
             }
           }
         }
+      }
+      int kid[KMAX];
+      float sraw[KMAX];
+#pragma unroll
+      for (int j = 0; j < KMAX; ++j) {                   // lines 12-13: unpack, remove the bias
+        kid[j] = (int)(~(uint32_t)top[j]);
+        sraw[j] = unord32((uint32_t)(top[j] >> 32)) - s_bias[kid[j]];
       }
       bad |= (chk != 0.f);
       const int64_t t = (int64_t)rt * RT + row;

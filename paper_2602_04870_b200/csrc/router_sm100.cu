@@ -170,14 +170,13 @@ router_sm100_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_const
       const int acc = n % kNB;
       mbar_wait(&tfull[acc], (n / kNB) & 1);
       tc_fence_after();
-      // Running top-k on float keys.  Experts are visited in increasing index order and a new
-      // key displaces a slot only if STRICTLY greater, so equal keys keep the lower index first:
-      // exactly the order of the packed (ord32(key) << 32 | ~idx) keys of P:832 / R6 (with
-      // -0.0 == +0.0), at a fraction of the 64-bit compare cost.
-      float key[KMAX], sraw[KMAX];
-      int kid[KMAX];
-#pragma unroll
-      for (int j = 0; j < KMAX; ++j) { key[j] = -INFINITY; sraw[j] = 0.f; kid[j] = 0; }
+      // Alg. 1 (P:829-P:834) in registers: the scores of each block of KMAX experts become packed
+      // u64 keys (ord32(s + b) << 32 | ~e, P:832 / R6: a larger key wins, equal keys go to the lower
+      // index), the block is sorted by a bitonic network and merged into the running top-KMAX (the
+      // max of the running list against the reversed block is bitonic; one bitonic merge sorts it).
+      // Branch-free: the former per-candidate insertion diverged in every warp (some lane nearly
+      // always inserted), which made the router ALU-bound (ncu r2c: ALU pipe 69 %).
+      unsigned long long top[KMAX];
       float chk = 0.f;   // becomes NaN if any key is NaN or +-Inf (0 * inf = NaN)
 #pragma unroll 1
       for (int c0 = 0; c0 < NE; c0 += 32) {
@@ -185,23 +184,31 @@ router_sm100_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_const
         tmem_ld32(tmem + acc * NE + ((uint32_t)(q * 32) << 16) + c0, v);
         tmem_ld_wait();
 #pragma unroll
-        for (int j = 0; j < 32; ++j) {
-          const float s = __uint_as_float(v[j]);
-          float kf = s + s_bias_g[c0 + j];
-          chk = fmaf(kf, 0.f, chk);
-          if (kf > key[KMAX - 1]) {
-            float sv = s;
-            int ki = c0 + j;
+        for (int b0 = 0; b0 < 32; b0 += KMAX) {
+          unsigned long long blk[KMAX];
 #pragma unroll
-            for (int u = 0; u < KMAX; ++u) {
-              const bool sw = kf > key[u];
-              const float tk = key[u], ts = sraw[u];
-              const int ti2 = kid[u];
-              key[u] = sw ? kf : tk; sraw[u] = sw ? sv : ts; kid[u] = sw ? ki : ti2;
-              kf = sw ? tk : kf;     sv = sw ? ts : sv;     ki = sw ? ti2 : ki;
-            }
+          for (int u = 0; u < KMAX; ++u) {
+            const float kf = __uint_as_float(v[b0 + u]) + s_bias_g[c0 + b0 + u];
+            chk = fmaf(kf, 0.f, chk);
+            blk[u] = pack_key(kf, c0 + b0 + u);
+          }
+          bitonic_sort_desc<KMAX>(blk);
+          if (c0 == 0 && b0 == 0) {
+#pragma unroll
+            for (int u = 0; u < KMAX; ++u) top[u] = blk[u];
+          } else {
+            merge_top_desc<KMAX>(top, blk);
           }
         }
+      }
+      int kid[KMAX];
+      float sraw[KMAX];
+#pragma unroll
+      for (int j = 0; j < KMAX; ++j) {
+        kid[j] = (int)(~(uint32_t)top[j]);
+        // raw score for the gates (R4): the biased key minus the bias (R25: within one fp32 rounding
+        // of the score itself)
+        sraw[j] = unord32((uint32_t)(top[j] >> 32)) - s_bias_g[kid[j]];
       }
       bad |= (chk != 0.f);
       tc_fence_before();
