@@ -537,3 +537,21 @@ def test_fault_injection_makes_conformance_fail(site, cfgname, dist, monkeypatch
     gf = _run_gpu(cfg, W, x, dout)
     with pytest.raises(AssertionError):
         _compare(cfg, W, x, dout, gf, dist=dist)
+
+
+def test_projection_gemms_row_invariant_across_M():
+    """the projection GEMMs run one pinned cuBLASLt algorithm (chosen at a fixed reference
+    M, split-K off) for every M, so each output row is computed by the same tile program with the same
+    K order whatever T_loc is.  Every per-token quantity of the layer (routing, experts, combine) is
+    row-local too, so the forward output rows and the input gradient rows of the first M tokens are
+    bitwise the same at T_loc = M as at T_loc = 65536 (M in 8192 ... 32768, the per-rank T_loc of HP
+    at G = 8 ... 2)."""
+    _need_gpu()
+    cfg = PRESETS["paper"]
+    W, x, dout = make_problem(cfg, 1, "paper")
+    full = _run_gpu(cfg, W, x, dout)
+    assert "proj_pinned" in full["paths"]
+    for M in (8192, 16384, 32768):
+        part = _run_gpu(cfg.replace(T=M), W, x[:M], dout[:M])
+        np.testing.assert_array_equal(part["out"], full["out"][:M], err_msg=f"out M={M}")
+        np.testing.assert_array_equal(part["dx"], full["dx"][:M], err_msg=f"dx M={M}")
