@@ -307,6 +307,7 @@ def main():
     ap.add_argument("--tokens", type=int, default=None, help="override T_loc (tokens per GPU)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--simt", action="store_true", help="use the SIMT reference kernels (debug)")
+    ap.add_argument("--pair", action="store_true", help="CTA-pair expert kernels (MHL_FLAG_PAIR)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample", type=int, default=256)
@@ -352,7 +353,7 @@ def main():
         nccl_id = obj[0]
 
     L = MHLatentMoE(T_loc, cfg.d, cfg.N_h, cfg.d_h, cfg.N_e, cfg.k, cfg.d_e, cfg.dtype, world_size=G, rank=rank,
-                    simt=args.simt, nccl_id=nccl_id, device=dev, routing_tokens=cfg.routing_tokens)
+                    simt=args.simt, nccl_id=nccl_id, device=dev, routing_tokens=cfg.routing_tokens, pair=args.pair)
     td = torch_dtype(cfg.dtype)
     W = make_weights(cfg, 0, "paper")
     Wd = weights_to_device(W, cfg.dtype, dev, heads=(L.info["head_begin"], L.info["head_end"]))
@@ -529,7 +530,7 @@ def main():
             "vs_baseline": None, "dtype": cfg.dtype, "data": "synthetic (seeded, paper init P:1995-P:1996)",
             "config": {"workload": workload_desc(cfg, T_loc), "T_loc": T_loc, "global_tokens": G * T_loc,
                        "parallelism": f"hp{G}", "l2": "inputs larger than L2 (per-step working set >> 126 MB)",
-                       "kernels": "simt-reference" if args.simt else "default",
+                       "kernels": "simt-reference" if args.simt else ("cta-pair" if args.pair else "default"),
                        "cuda_graph": bool(graph is not None),
                        "span_times": "eager pass after the graph-timed region" if graph is not None else "timed region"},
             "layer_tflops": layer_tflops,

@@ -619,7 +619,7 @@ mhl_status moe_forward_local(mhl_plan p, const RankPtrs& R, void* yout, cudaStre
     if (m.simt || !mhl::expert_fwd_sm100_supported(m.d_h, m.d_e)) {
       mhl::launch_expert_fwd_simt(m.dtype, rt, Xs, m.XW, R.W1, R.W2, m.d_h, m.d_e, Yrep, s);
       p->paths |= MHL_PATH_EXPERT_FWD_SIMT;
-    } else if (m.pair && mhl::expert_fwd_pair_supported(m.d_h, m.d_e) && p->num_sms >= 2) {
+    } else if (m.pair && mhl::expert_fwd_pair_supported(m.d_h, m.d_e) && p->num_sms >= 2 && !getenv("MHL_F5_SINGLE")) {
       if (!mhl::launch_expert_fwd_pair_sm100(rt, Xs, m.XW, R.W1, R.W2, m.d_h, m.d_e, Yrep, p->num_sms, s))
         return fail(MHL_ERR_CUDA, "expert_fwd (pair): TMA tensor-map encoding failed");
       p->paths |= MHL_PATH_EXPERT_FWD_PAIR;

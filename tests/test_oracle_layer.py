@@ -93,14 +93,54 @@ def test_per_head_decomposition_and_head_independence():
     assert not np.array_equal(C2.cat[:, d_h:2 * d_h], C.cat[:, d_h:2 * d_h])
 
 
+def _counted_scalar_forward(P, x, k):
+    """An independent scalar-loop forward of the layer (Eq. 1-6, fp64, no storage rounding) that
+    counts every multiply-add it performs: the pin of layer_flops / moe_flops_equivalent."""
+    import math
+    N_h, d_h, N_e = P["W_r"].shape
+    d_e = P["W1"].shape[2]
+    T, d = x.shape
+    D = N_h * d_h
+    macs = dict(w_in=0, router=0, experts=0, w_out=0)
+    out = np.zeros((T, P["W_out"].shape[0]))
+    for t in range(T):
+        xs = [sum(P["W_in"][i][c] * x[t][c] for c in range(d)) for i in range(D)]
+        macs["w_in"] += D * d
+        cat = []
+        for h in range(N_h):
+            sub = xs[h * d_h:(h + 1) * d_h]
+            s = [sum(sub[i] * P["W_r"][h][i][e] for i in range(d_h)) for e in range(N_e)]
+            macs["router"] += d_h * N_e
+            order = sorted(range(N_e), key=lambda e: (-(s[e] + P["b"][h][e]), e))[:k]
+            m = max(s[e] for e in order)
+            z = sum(math.exp(s[e] - m) for e in order)
+            y = [0.0] * d_h
+            for e in order:
+                g = math.exp(s[e] - m) / z
+                hid = [sum(sub[i] * P["W1"][h][e][j][i] for i in range(d_h)) for j in range(d_e)]
+                a = [v * 0.5 * (1.0 + math.erf(v / math.sqrt(2.0))) for v in hid]
+                for c in range(d_h):
+                    y[c] += g * sum(a[j] * P["W2"][h][e][j][c] for j in range(d_e))
+                macs["experts"] += 2 * d_h * d_e
+            cat.extend(y)
+        for o in range(out.shape[1]):
+            out[t][o] = sum(cat[c] * P["W_out"][o][c] for c in range(D))
+        macs["w_out"] += out.shape[1] * D
+    return out, macs
+
+
 def test_flop_parity_p777():
-    for (T, d, N_h, d_h, N_e, k, d_e) in [(256, 64, 4, 16, 8, 2, 16), (65536, 2048, 8, 256, 64, 8, 128)]:
-        f = O.layer_flops(T, d, N_h, d_h, N_e, k, d_e)
-        assert f["router"] + f["experts"] == O.moe_flops_equivalent(T, N_h, d_h, N_e, k, d_e)
-    # count multiply-adds of the dense oracle directly on a tiny case: experts touched k per sub-token
-    T, N_h, d_h, N_e, k, d_e = 10, 2, 4, 5, 2, 3
-    per_replica = 2 * d_h * d_e * 2       # gelu(x W1^T) then W2: two d_h x d_e products
-    assert O.layer_flops(T, 8, N_h, d_h, N_e, k, d_e)["experts"] == T * N_h * k * per_replica
+    """layer_flops / moe_flops_equivalent against the multiply-adds an independent scalar-loop forward
+    actually performs (its output checked against the oracle's), and P:777's parity: router +
+    experts of the layer = one MoE over N_h*T sub-tokens."""
+    cfg = TINY64.replace(T=6, d=16, N_h=2, d_h=8, N_e=6, k=2, d_e=5, dtype="fp64")
+    P, x, _ = _prob(cfg, 9)
+    out, macs = _counted_scalar_forward(P, x, cfg.k)
+    C = O.layer_forward(P, x, cfg.k, mode="fp64")
+    np.testing.assert_allclose(out, C.out, rtol=1e-10, atol=1e-12)
+    f = O.layer_flops(cfg.T, cfg.d, cfg.N_h, cfg.d_h, cfg.N_e, cfg.k, cfg.d_e)
+    assert f == {kk: 2 * v for kk, v in macs.items()}
+    assert f["router"] + f["experts"] == O.moe_flops_equivalent(cfg.T, cfg.N_h, cfg.d_h, cfg.N_e, cfg.k, cfg.d_e)
 
 
 def test_bf16_rounding_points():
