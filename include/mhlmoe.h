@@ -255,6 +255,9 @@ MHL_API int32_t mhl_step_times(mhl_plan plan, char* names, size_t names_cap, dou
 #define MHL_PATH_ROUTER_BWD_SIMT  (1u << 9)
 #define MHL_PATH_PROJ_PINNED      (1u << 10)  /* F1/F8/B8/B1 on the plan's pinned GEMM algorithm   */
 #define MHL_PATH_FUSED_COMBINE    (1u << 11)  /* (reserved: the removed in-kernel combine)         */
+#define MHL_PATH_WINDOWED_COMBINE (1u << 14)  /* F5/F6 and K2/B6 alternate per token window, the
+                                                 per-replica rows combined from L2 and discarded
+                                                 (NEXT-1; G = 1, bf16 tensor-core path)         */
 #define MHL_PATH_A2A_NCCL         (1u << 12)  /* HP exchanges through NCCL send/recv               */
 #define MHL_PATH_A2A_LOOPBACK     (1u << 13)  /* HP exchanges as device copies (MHL_FLAG_LOOPBACK) */
 MHL_API uint32_t mhl_kernel_paths(mhl_plan plan, int reset);

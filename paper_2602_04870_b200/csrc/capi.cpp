@@ -113,7 +113,7 @@ struct Bump {
 };
 
 // offsets inside one rank's saved region
-struct SavedLayout { size_t Xs, idx, gate, perm, tok_s, gate_s, pos, off, tiles, ntiles, chunks, nchunks, cbase, ccount, pbase, pcount, load, cat, total; };
+struct SavedLayout { size_t Xs, idx, gate, perm, tok_s, gate_s, pos, off, tiles, ntiles, chunks, nchunks, cbase, ccount, pbase, pcount, load, win, cat, total; };
 // offsets inside one rank's workspace region (forward and backward alias each other)
 struct FwdLayout { size_t send1, Yrep, send2, recv2, hist, tilepref, planes, total; };
 struct BwdLayout { size_t send3, dY, dXrep, dg, dS, dS_s, dH, gA, dwr_part, W_rT, send4, recv4, dXs, dw_part, dw_done, total; };
@@ -137,6 +137,7 @@ SavedLayout saved_layout(const Dims& m) {
   L.pbase = b.take((size_t)m.H * mhl::kDwParts * 4);
   L.pcount = b.take((size_t)m.H * mhl::kDwParts * 4);
   L.load = b.take((size_t)m.H * m.N_e * 4);             // per-head expert loads of the step (F4)
+  L.win = b.take((size_t)m.H * mhl::kWindows * 4 * 4);  // windowed combine: tile / token range per window
   L.cat = b.take((size_t)m.T_loc * m.D * m.el);
   L.total = b.off;
   return L;
@@ -536,6 +537,17 @@ mhl::Routing routing_view(const Dims& m, const char* saved) {
   return rt;
 }
 
+// NEXT-1 (windowed, L2-resident combine): at G = 1 on the tensor-core path the expert kernel and
+// the combine alternate window by window (kWinParts token-order parts of one head): each window's
+// per-replica rows (Yrep forward, dXrep backward; ~67 MB at paper scale) are combined while still
+// in L2 and then discarded from it, so they are never written back to HBM.  MHL_WINDOWS=0 restores
+// one expert launch + one combine launch.
+bool windowed(const Dims& m) {
+  static const bool off = getenv("MHL_WINDOWS") && atoi(getenv("MHL_WINDOWS")) == 0;
+  return !off && m.G == 1 && !m.simt && !m.pair && !m.rtok && m.dtype == MHL_BF16 && m.d_h % 64 == 0 &&
+         mhl::expert_fwd_sm100_supported(m.d_h, m.d_e) && mhl::expert_bwd_sm100_supported(m.d_h, m.d_e);
+}
+
 mhl_status check_kernels(mhl_plan p) {
   if (p->launch_err != cudaSuccess) {
     const cudaError_t e = p->launch_err;
@@ -608,9 +620,37 @@ mhl_status moe_forward_local(mhl_plan p, const RankPtrs& R, void* yout, cudaStre
                         (mhl::Tile*)(R.saved + S.chunks),
                         (int32_t*)(R.saved + S.nchunks), (int32_t*)(R.saved + S.cbase), (int32_t*)(R.saved + S.ccount),
                         m.max_chunks, 0, (int32_t*)(R.saved + S.pbase), (int32_t*)(R.saved + S.pcount), s);
+    if (windowed(m)) {
+      mhl::launch_windows(m.H, m.N_e, m.T_g, m.Rp, m.seg_align, (const int32_t*)(R.saved + S.load), off,
+                          (const int32_t*)(R.ws + F.tilepref), m.n_rt, ntiles, (const int32_t*)(R.saved + S.tok_s),
+                          (int32_t*)(R.saved + S.win), s);
+      p->launches++;
+    }
   }
   const mhl::Routing rt = routing_view(m, R.saved);
   void* Yrep = R.ws + F.Yrep;
+  if (yout && windowed(m)) {
+    MHL_CUDA(cudaMemsetAsync(R.saved + S.Xs + (size_t)m.T_g * m.XW * m.el, 0, (size_t)m.XW * m.el, s));
+    const int32_t* win = (const int32_t*)(R.saved + S.win);
+    for (int h = 0; h < m.H; ++h)
+      for (int w = 0; w < mhl::kWindows; ++w) {
+        mhl::Routing rw = rt;
+        rw.trange = win + ((size_t)h * mhl::kWindows + w) * 4;
+        {
+          MHL_SPAN("F5_expert_fwd");
+          if (!mhl::launch_expert_fwd_sm100(rw, Xs, m.XW, R.W1, R.W2, m.d_h, m.d_e, Yrep, p->num_sms, s))
+            return fail(MHL_ERR_CUDA, "expert_fwd: TMA tensor-map encoding failed");
+        }
+        MHL_SPAN("F6_combine");
+        mhl::launch_combine_window(m.dtype, rt, Yrep, m.d_h, yout, m.HD, h, rw.trange + 2, m.T_g / mhl::kWindows, true,
+                                   s);
+      }
+    p->paths |= MHL_PATH_EXPERT_FWD_TC | MHL_PATH_WINDOWED_COMBINE;
+    p->launches += 5 + 2 * m.H * mhl::kWindows;
+    if (R.topk_idx) MHL_CUDA(cudaMemcpyAsync(R.topk_idx, idx, (size_t)m.H * m.R * 4, cudaMemcpyDeviceToDevice, s));
+    if (R.gates) MHL_CUDA(cudaMemcpyAsync(R.gates, gate, (size_t)m.H * m.R * 4, cudaMemcpyDeviceToDevice, s));
+    return check_kernels(p);
+  }
   {
     MHL_SPAN("F5_expert_fwd");
     // the all-zero sub-token row T: target of the padding rows of every expert tile
@@ -693,7 +733,9 @@ mhl_status moe_backward_local(mhl_plan p, const RankPtrs& R, const void* dY, voi
     if (tc && !m.rtok) { mhl::launch_sort_ds(rt, dS, (float*)(R.ws + B.dS_s), s); p->launches++; }
     mhl::launch_transpose_wr(R.W_r, W_rT, m.H, m.d_h, m.N_e, s);
   }
-  if (tc) {
+  // windowed (NEXT-1): the dX GEMM and B6 alternate window by window after the dW kernel
+  const bool win_b = tc && dxout && windowed(m);
+  if (tc && !win_b) {
     MHL_SPAN("B5_expert_dx_gemm");
     if (!mhl::launch_expert_dx_gemm_sm100(rt, R.W1, m.d_h, m.d_e, dH, dXrep,
                                           m.rtok ? nullptr : (const float*)(R.ws + B.dS_s), W_rT,
@@ -715,7 +757,25 @@ mhl_status moe_backward_local(mhl_plan p, const RankPtrs& R, const void* dY, voi
     else
       mhl::launch_expert_dw_simt(m.dtype, rt, Xs, m.XW, dY, m.HD, dH, gA, m.d_h, m.d_e, R.dW1, R.dW2, s);
   }
-  if (dxout) {
+  if (win_b) {
+    const int32_t* win = (const int32_t*)(R.saved + S.win);
+    for (int h = 0; h < m.H; ++h)
+      for (int w = 0; w < mhl::kWindows; ++w) {
+        mhl::Routing rw = rt;
+        rw.trange = win + ((size_t)h * mhl::kWindows + w) * 4;
+        {
+          MHL_SPAN("B5_expert_dx_gemm");
+          if (!mhl::launch_expert_dx_gemm_sm100(rw, R.W1, m.d_h, m.d_e, dH, dXrep, (const float*)(R.ws + B.dS_s),
+                                                W_rT, p->num_sms, s))
+            return fail(MHL_ERR_CUDA, "expert dX GEMM: TMA tensor-map encoding failed");
+        }
+        MHL_SPAN("B6_combine_bwd");
+        mhl::launch_combine_window(m.dtype, rt, dXrep, m.d_h, dxout, m.Din, h, rw.trange + 2, m.T_g / mhl::kWindows,
+                                   true, s);
+      }
+    p->paths |= MHL_PATH_WINDOWED_COMBINE;
+    p->launches += 2 * m.H * mhl::kWindows - 2;
+  } else if (dxout) {
     MHL_SPAN("B6_combine_bwd");
     combine_bwd(m, rt, dXrep, dS, W_rT, tc, dxout, m.Din, dxout_r, m.Din, s, 0, -1);
   }

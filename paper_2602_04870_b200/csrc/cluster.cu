@@ -361,6 +361,54 @@ void launch_update_bias(const int32_t* load, int H, int N_e, int64_t total, floa
   if (n > 0) update_bias_kernel<<<(n + 255) / 256, 256, 0, s>>>(load, n, N_e, total, gamma, bias);
 }
 
+// (4) windows of the windowed combine (kernels.h kWinParts): one block per head.  Tile range of
+// window w: the first tile of its first part to the first tile of the next window (the next head's
+// first tile, or the end of the list); token range: tokens below the first token of the next
+// window's first part in every expert segment (rows within a segment are in token order).
+__global__ void __launch_bounds__(256)
+windows_kernel(const int32_t* __restrict__ counts, const int32_t* __restrict__ off, const int32_t* __restrict__ tbase,
+               const int32_t* __restrict__ ntiles, const int32_t* __restrict__ tok_s, int H, int N_e, int64_t T,
+               int64_t Rp, int seg_align, int32_t* __restrict__ win) {
+  __shared__ int s_m[8];
+  const int h = blockIdx.x, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int TPS = seg_align / kExpertBM;
+  int tok_lo = 0;
+  for (int w = 0; w < kWindows; ++w) {
+    const int p1 = (w + 1) * kWinParts;
+    int mn = (int)T;
+    if (p1 < kTileParts) {
+      for (int e = threadIdx.x; e < N_e; e += blockDim.x) {
+        const int c = counts[(size_t)h * N_e + e];
+        const int nu = (c + seg_align - 1) / seg_align;
+        const int r = TPS * (p1 * nu / kTileParts) * kExpertBM;        // first row of part p1
+        if (r < c) mn = min(mn, tok_s[(size_t)h * Rp + off[(size_t)h * (N_e + 1) + e] + r]);
+      }
+    }
+    for (int o = 16; o > 0; o >>= 1) mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+    if (lane == 0) s_m[warp] = mn;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int b = (int)T;
+      for (int i = 0; i < (int)(blockDim.x / 32); ++i) b = min(b, s_m[i]);
+      int32_t* o = win + ((size_t)h * kWindows + w) * 4;
+      o[0] = tbase[((size_t)h * kTileParts + w * kWinParts) * N_e];
+      o[1] = p1 < kTileParts ? tbase[((size_t)h * kTileParts + p1) * N_e]
+                             : (h + 1 < H ? tbase[(size_t)(h + 1) * kTileParts * N_e] : *ntiles);
+      o[2] = tok_lo;
+      o[3] = b;
+      tok_lo = b;
+    }
+    __syncthreads();
+  }
+}
+
+void launch_windows(int H, int N_e, int64_t T, int64_t Rp, int seg_align, const int32_t* counts, const int32_t* off,
+                    const int32_t* tilepref, int n_rt, const int32_t* ntiles, const int32_t* tok_s, int32_t* win,
+                    cudaStream_t s) {
+  const int32_t* tbase = tilepref + (size_t)H * n_rt * N_e;
+  windows_kernel<<<H, 256, 0, s>>>(counts, off, tbase, ntiles, tok_s, H, N_e, T, Rp, seg_align, win);
+}
+
 void launch_cluster(int H, int64_t T, int k, int N_e, const int32_t* idx, const float* gate, const int32_t* hist,
                     int32_t* tilepref, int32_t* counts, int32_t* off, int32_t* perm, int32_t* pos, int32_t* tok_s,
                     float* gate_s, int64_t Rp, int seg_align, Tile* tiles, int32_t* ntiles, int max_tiles,

@@ -41,12 +41,19 @@ template <typename E, bool BWD, int KMAX, bool SMEM_W>
 __global__ void __launch_bounds__(SMEM_W ? 512 : 256)
 combine_kernel(const E* __restrict__ rep, const int32_t* __restrict__ pos, const int32_t* __restrict__ idx,
                const float* __restrict__ dS, const float* __restrict__ W_rT, int H, int64_t T, int k, int d_h,
-               int N_e, int64_t Rp, int64_t t0, int64_t nT, E* __restrict__ out, int64_t ldo, int tok_rt) {
+               int N_e, int64_t Rp, int64_t t0, int64_t nT, E* __restrict__ out, int64_t ldo, int tok_rt,
+               int h0, const int32_t* __restrict__ tr, int discard) {
   constexpr int V = Vec<E>::N;
   extern __shared__ __align__(16) float s_w[];           // [N_e][d_h] when SMEM_W
   constexpr int NT = SMEM_W ? 512 : 256, NW = NT / 32;
   const int TOK = SMEM_W ? kCombTokW : tok_rt;   // tokens per CTA (smaller for small T: more CTAs in flight)
-  const int h = blockIdx.y, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int h = h0 + (int)blockIdx.y, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int64_t tout = t0;               // output row = t - tout
+  if (tr != nullptr) {             // windowed combine: head h0's tokens [tr[0], tr[1]), rows absolute
+    t0 = tr[0];
+    nT = tr[1] - t0;
+    tout = 0;
+  }
   const int64_t R = T * k;
   const float* wt_h = W_rT + (size_t)h * N_e * d_h;
   if constexpr (BWD && SMEM_W) {
@@ -56,7 +63,8 @@ combine_kernel(const E* __restrict__ rep, const int32_t* __restrict__ pos, const
   }
   const int nchunk = d_h / V;
   // tokens [t0, t0 + nT) of the head (one HP destination block, or all T); output row = t - t0
-  const int64_t tb = (int64_t)blockIdx.x * TOK;
+  // token blocks of TOK, grid-stride (the windowed combine's grid does not know its range's size)
+  for (int64_t tb = (int64_t)blockIdx.x * TOK; tb < nT; tb += (int64_t)gridDim.x * TOK)
   for (int tt = warp; tt < TOK; tt += NW) {
     if (tb + tt >= nT) break;
     const int64_t t = t0 + tb + tt;
@@ -91,6 +99,7 @@ combine_kernel(const E* __restrict__ rep, const int32_t* __restrict__ pos, const
             for (int i = 0; i < 8; ++i) acc[i] += f[i];
           }
         }
+
       } else {
         float4 v[KMAX];
 #pragma unroll
@@ -122,12 +131,24 @@ combine_kernel(const E* __restrict__ rep, const int32_t* __restrict__ pos, const
 #pragma unroll
         for (int i = 0; i < V; ++i) acc[i] += racc[i];
       }
-      E* dst = out + (t - t0) * ldo + (int64_t)h * d_h + ch * V;
+      E* dst = out + (t - tout) * ldo + (int64_t)h * d_h + ch * V;
       if constexpr (V == 8) {
         *reinterpret_cast<uint4*>(dst) = pack(acc);
       } else {
         *reinterpret_cast<float4*>(dst) = make_float4(acc[0], acc[1], acc[2], acc[3]);
       }
+    }
+    // every replica row is read exactly once: once all lanes have consumed their loads, drop the
+    // rows' lines from L2 without a write-back (one lane per 128-byte line; rows are line-aligned)
+    if (discard && rep) {
+      __syncwarp();
+      for (int ch = lane; ch < nchunk; ch += 32)
+        if ((ch & 7) == 0)
+#pragma unroll
+          for (int j = 0; j < KMAX; ++j)
+            if (j < k)
+              asm volatile("discard.global.L2 [%0], 128;" ::"l"(rep + ((size_t)h * Rp + p[j]) * d_h + ch * V)
+                           : "memory");
     }
   }
 }
@@ -144,13 +165,35 @@ void launch_kw(const Routing& rt, const E* rep, const float* dS, const float* W_
   {                                                                                                         \
     auto f = combine_kernel<E, BWD, KM, SMEM_W>;                                                            \
     if (smem > 48 * 1024) cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);  \
-    f<<<grid, SMEM_W ? 512 : 256, smem, s>>>(rep, rt.pos, rt.idx, dS, W_rT, rt.H, rt.T, rt.k, d_h, rt.N_e, rt.Rp, t0, nT, out, ldo, tok); \
+    f<<<grid, SMEM_W ? 512 : 256, smem, s>>>(rep, rt.pos, rt.idx, dS, W_rT, rt.H, rt.T, rt.k, d_h, rt.N_e, rt.Rp, t0, nT, out, ldo, tok, 0, nullptr, 0); \
   }
   if (rt.k <= 2) MHL_CK(2) else if (rt.k <= 4) MHL_CK(4) else if (rt.k <= 8) MHL_CK(8) else MHL_CK(16)
 #undef MHL_CK
 }
 
 }  // namespace
+
+void launch_combine_window(int dtype, const Routing& rt, const void* rep, int d_h, void* out, int64_t ldo, int h,
+                           const int32_t* tr, int64_t max_tokens, bool discard, cudaStream_t s) {
+  if (max_tokens <= 0) return;
+  // max_tokens sizes the grid (the range itself is read on the device; the token loop is
+  // grid-stride, so any grid covers it)
+  int tok = kCombTok;
+  while (tok > 16 && (max_tokens + tok - 1) / tok < 8 * 148) tok /= 2;
+  const dim3 grid((unsigned)std::min<int64_t>((max_tokens + tok - 1) / tok, 16 * 148), 1u);
+#define MHL_CW(E, KM)                                                                                        \
+  combine_kernel<E, false, KM, false><<<grid, 256, 0, s>>>((const E*)rep, rt.pos, rt.idx, nullptr, nullptr, rt.H, rt.T, \
+                                                           rt.k, d_h, rt.N_e, rt.Rp, 0, 0, (E*)out, ldo, tok, h, tr,     \
+                                                           discard ? 1 : 0)
+  if (dtype == 1) {
+    if (rt.k <= 2) MHL_CW(bf16, 2); else if (rt.k <= 4) MHL_CW(bf16, 4); else if (rt.k <= 8) MHL_CW(bf16, 8);
+    else MHL_CW(bf16, 16);
+  } else {
+    if (rt.k <= 2) MHL_CW(float, 2); else if (rt.k <= 4) MHL_CW(float, 4); else if (rt.k <= 8) MHL_CW(float, 8);
+    else MHL_CW(float, 16);
+  }
+#undef MHL_CW
+}
 
 void launch_combine_fwd(int dtype, const Routing& rt, const void* Yrep, int d_h, void* out, int64_t ldo,
                         cudaStream_t s, int64_t t0, int64_t nT) {

@@ -164,7 +164,8 @@ expert_bwd_h_kernel(const __grid_constant__ CUtensorMap w1map, const __grid_cons
   float* s_dg = reinterpret_cast<float*>(smem + L::DG);
   uint32_t* s_tmem = reinterpret_cast<uint32_t*>(smem + L::TMEMP);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const Tile* tiles = rt.tiles;
+  const int t_lo = rt.trange ? rt.trange[0] : 0;   // tile window (NEXT-1) or every tile
+  const Tile* tiles = rt.tiles + t_lo;
   const int N_e = rt.N_e;
   const int64_t Rp = rt.Rp, R = rt.T * rt.k;
 
@@ -184,7 +185,7 @@ expert_bwd_h_kernel(const __grid_constant__ CUtensorMap w1map, const __grid_cons
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *s_tmem;
-  const Sched sc(tiles, *rt.ntiles);
+  const Sched sc(tiles, (rt.trange ? rt.trange[1] : *rt.ntiles) - t_lo);
 
   auto load_w = [&](const CUtensorMap* map, int off, uint64_t* full, const Tile& t) {
     mbar_expect_tx(full, L::WB);
@@ -551,7 +552,8 @@ expert_bwd_h_pair_kernel(const __grid_constant__ CUtensorMap w1map, const __grid
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const uint32_t rank = cta_rank();
   const bool leader = rank == 0;
-  const Tile* tiles = rt.tiles;
+  const int t_lo = rt.trange ? rt.trange[0] : 0;   // tile window (NEXT-1) or every tile
+  const Tile* tiles = rt.tiles + t_lo;
   const int N_e = rt.N_e;
   const int64_t Rp = rt.Rp, R = rt.T * rt.k;
 
@@ -807,7 +809,8 @@ expert_dx_gemm_kernel(const __grid_constant__ CUtensorMap w1map, const __grid_co
   auto bar = [&](int off) { return reinterpret_cast<uint64_t*>(smem + off); };
   uint32_t* s_tmem = reinterpret_cast<uint32_t*>(smem + L::TMEMP);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const Tile* tiles = rt.tiles;
+  const int t_lo = rt.trange ? rt.trange[0] : 0;   // tile window (NEXT-1) or every tile
+  const Tile* tiles = rt.tiles + t_lo;
   const int N_e = rt.N_e;
   const int64_t Rp = rt.Rp;
 
@@ -823,7 +826,7 @@ expert_dx_gemm_kernel(const __grid_constant__ CUtensorMap w1map, const __grid_co
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *s_tmem;
-  const Sched sc(tiles, *rt.ntiles);
+  const Sched sc(tiles, (rt.trange ? rt.trange[1] : *rt.ntiles) - t_lo);
 
   if (warp == 0) {
     // ================================================================ TMA producer

@@ -113,7 +113,9 @@ expert_fwd_sm100_kernel(const __grid_constant__ CUtensorMap w1map, const __grid_
   auto bar = [&](int off) { return reinterpret_cast<uint64_t*>(smem + off); };
   uint32_t* s_tmem = reinterpret_cast<uint32_t*>(smem + L::TMEMP);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const Tile* tiles = rt.tiles;
+  // tile window (NEXT-1 windowed combine) or every tile
+  const int t_lo = rt.trange ? rt.trange[0] : 0;
+  const Tile* tiles = rt.tiles + t_lo;
   const int N_e = rt.N_e;
 
   if (tid == 0) {
@@ -132,7 +134,7 @@ expert_fwd_sm100_kernel(const __grid_constant__ CUtensorMap w1map, const __grid_
   tc_fence_after();
   const uint32_t tmem = *s_tmem;
 
-  const int nt = *rt.ntiles;
+  const int nt = (rt.trange ? rt.trange[1] : *rt.ntiles) - t_lo;
   const int ngroups = (nt + kTileGroup - 1) / kTileGroup;
   const int my_groups = ngroups > (int)blockIdx.x ? (ngroups - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
   auto tile_at = [&](int i) -> int {   // the i-th tile of this CTA, or -1

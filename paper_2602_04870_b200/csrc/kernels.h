@@ -41,7 +41,25 @@ struct Routing {
   const Tile* chunks; const int32_t* nchunks; int max_chunks;     // dW chunks
   const int32_t* cbase; const int32_t* ccount;                    // [H][N_e] chunk range per expert
   const int32_t* pbase; const int32_t* pcount; int dw_parts;       // [H][dw_parts] chunk range per (head, part)
+  // optional tile window: the expert kernels then take only tiles [trange[0], trange[1]) (device
+  // pointer; nullptr = every tile).  Used by the L2-resident windowed combine (NEXT-1, capi.cpp).
+  const int32_t* trange = nullptr;
 };
+
+// Token windows of the windowed combine (NEXT-1): each head's tile list is cut into kWinParts
+// consecutive token-order parts per window; win[(h * kWindows + w) * 4 + {0,1,2,3}] = tile range
+// [lo, hi) and token range [lo, hi) of window w of head h (every replica of a token in the token
+// range lies in the window's tiles or earlier ones of the same head).
+constexpr int kWinParts = 2;
+constexpr int kWindows = MHL_TILE_PARTS / kWinParts;
+void launch_windows(int H, int N_e, int64_t T, int64_t Rp, int seg_align, const int32_t* counts, const int32_t* off,
+                    const int32_t* tilepref, int n_rt, const int32_t* ntiles, const int32_t* tok_s, int32_t* win,
+                    cudaStream_t s);
+// F6 / B6 of one window: the k-row sum for head h's tokens [tr[0], tr[1]) (device pointer), written
+// to output row t (absolute); with `discard` every replica row read is dropped from L2 afterwards
+// (discard.global.L2: it is never read again, so it need not be written back to HBM).
+void launch_combine_window(int dtype, const Routing& rt, const void* rep, int d_h, void* out, int64_t ldo, int h,
+                           const int32_t* tr, int64_t max_tokens, bool discard, cudaStream_t s);
 
 // ---- F3: router + online top-k + gates (SIMT fp32-FMA path). idx/gate [H][T][k];
 // hist [H][ceil(T/128)][N_e]; flag set to 1 on a non-finite key.

@@ -28,7 +28,7 @@ EXPORTS = ["hp_plan_query", "mhl_get_unique_id", "hp_plan", "hp_plan_info", "hp_
 PATHS = {"router_tc": 1 << 0, "router_blk": 1 << 1, "router_simt": 1 << 2, "expert_fwd_tc": 1 << 3,
          "expert_fwd_pair": 1 << 4, "expert_fwd_simt": 1 << 5, "expert_bwd_tc": 1 << 6, "expert_bwd_simt": 1 << 7,
          "router_bwd_tc": 1 << 8, "router_bwd_simt": 1 << 9, "proj_pinned": 1 << 10, "fused_combine": 1 << 11,
-         "a2a_nccl": 1 << 12, "a2a_loopback": 1 << 13}
+         "a2a_nccl": 1 << 12, "a2a_loopback": 1 << 13, "windowed_combine": 1 << 14}
 
 
 class MhlError(RuntimeError):
