@@ -65,6 +65,13 @@ typedef enum { MHL_F32 = 0, MHL_BF16 = 1 } mhl_dtype;
                                  measured slower than the separate pass; hp_plan / hp_plan_query
                                  return MHL_ERR_UNSUPPORTED for it. */
 
+#define MHL_FLAG_WINDOWED_COMBINE 32u  /* G = 1, bf16 tensor-core path (NEXT-1 experiment, opt-in): the
+                                 expert kernel and the combine alternate per token window (2 of
+                                 the 8 token-order parts of one head), each window's per-replica
+                                 rows (Yrep, dXrep) combined while L2-resident and then discarded
+                                 from L2.  Same bits as the default; measured slower (the extra
+                                 launches cost more than the HBM round trip they save). */
+
 /* Layer + HP configuration (the paper's problem statement: P:496). */
 typedef struct {
   int64_t tokens;        /* T_loc: tokens on this rank (B*T of P:804)                             */

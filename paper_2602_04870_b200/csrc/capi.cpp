@@ -102,6 +102,7 @@ struct Dims {
   int d, N_h, d_h, N_e, k, d_e, G, H, HD, D, el, dtype, rank;
   bool loopback, simt, pair;
   bool rtok;       // MHL_FLAG_ROUTING_TOKENS (P:1565-P:1570): Xs rows carry [x part | r part]
+  bool win;        // MHL_FLAG_WINDOWED_COMBINE (or MHL_WINDOWS=1)
   int XW;          // Xs row width per rank: HD, or 2*HD with routing tokens (r part at column HD)
   int Din;         // W_in rows: D, or 2*D with routing tokens
   int n_rt, max_tiles, max_chunks, seg_align, n_rbwd;
@@ -206,6 +207,7 @@ mhl_status make_dims(const mhl_config* c, Dims* m) {
   m->HD = m->H * m->d_h;
   m->D = m->N_h * m->d_h;
   m->rtok = (c->flags & MHL_FLAG_ROUTING_TOKENS) != 0;
+  m->win = (c->flags & MHL_FLAG_WINDOWED_COMBINE) != 0 || (getenv("MHL_WINDOWS") && atoi(getenv("MHL_WINDOWS")) != 0);
   m->XW = m->HD * (m->rtok ? 2 : 1);
   m->Din = m->D * (m->rtok ? 2 : 1);
   m->dtype = c->dtype;
@@ -540,11 +542,13 @@ mhl::Routing routing_view(const Dims& m, const char* saved) {
 // NEXT-1 (windowed, L2-resident combine): at G = 1 on the tensor-core path the expert kernel and
 // the combine alternate window by window (kWinParts token-order parts of one head): each window's
 // per-replica rows (Yrep forward, dXrep backward; ~67 MB at paper scale) are combined while still
-// in L2 and then discarded from it, so they are never written back to HBM.  MHL_WINDOWS=0 restores
-// one expert launch + one combine launch.
+// in L2 and then discarded from it, so they are never written back to HBM.  Opt-in
+// (MHL_FLAG_WINDOWED_COMBINE, or MHL_WINDOWS=1 for the process):
+// the 32 extra launch pairs per direction cost more than the L2 residency saves (F5 + F6 1.97 ms
+// vs 1.27, K2 + B6 1.64 vs 1.08 at paper scale, tools/ab_windows.sh), so the default is one expert
+// launch + one combine launch.
 bool windowed(const Dims& m) {
-  static const bool off = getenv("MHL_WINDOWS") && atoi(getenv("MHL_WINDOWS")) == 0;
-  return !off && m.G == 1 && !m.simt && !m.pair && !m.rtok && m.dtype == MHL_BF16 && m.d_h % 64 == 0 &&
+  return m.win && m.G == 1 && !m.simt && !m.pair && !m.rtok && m.dtype == MHL_BF16 && m.d_h % 64 == 0 &&
          mhl::expert_fwd_sm100_supported(m.d_h, m.d_e) && mhl::expert_bwd_sm100_supported(m.d_h, m.d_e);
 }
 

@@ -37,7 +37,7 @@ constexpr int kCombTokW = 512;   // B6 with W_r^T staged in smem: 16 warps x 32 
 // every lane then has all k 16-byte row loads of its column chunk in flight at once (KMAX-unrolled).
 // B6 keeps W_r^T of the head in shared memory when it fits (SMEM_W), so the router term reads
 // smem instead of re-fetching k rows of W_r^T from L2 per token.
-template <typename E, bool BWD, int KMAX, bool SMEM_W>
+template <typename E, bool BWD, int KMAX, bool SMEM_W, bool WIN = false>
 __global__ void __launch_bounds__(SMEM_W ? 512 : 256)
 combine_kernel(const E* __restrict__ rep, const int32_t* __restrict__ pos, const int32_t* __restrict__ idx,
                const float* __restrict__ dS, const float* __restrict__ W_rT, int H, int64_t T, int k, int d_h,
@@ -49,7 +49,7 @@ combine_kernel(const E* __restrict__ rep, const int32_t* __restrict__ pos, const
   const int TOK = SMEM_W ? kCombTokW : tok_rt;   // tokens per CTA (smaller for small T: more CTAs in flight)
   const int h = h0 + (int)blockIdx.y, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   int64_t tout = t0;               // output row = t - tout
-  if (tr != nullptr) {             // windowed combine: head h0's tokens [tr[0], tr[1]), rows absolute
+  if constexpr (WIN) {             // windowed combine: head h0's tokens [tr[0], tr[1]), rows absolute
     t0 = tr[0];
     nT = tr[1] - t0;
     tout = 0;
@@ -63,8 +63,9 @@ combine_kernel(const E* __restrict__ rep, const int32_t* __restrict__ pos, const
   }
   const int nchunk = d_h / V;
   // tokens [t0, t0 + nT) of the head (one HP destination block, or all T); output row = t - t0
-  // token blocks of TOK, grid-stride (the windowed combine's grid does not know its range's size)
-  for (int64_t tb = (int64_t)blockIdx.x * TOK; tb < nT; tb += (int64_t)gridDim.x * TOK)
+  // token blocks of TOK (grid-stride only for the windowed combine, whose grid does not know its
+  // range's size; a plain launch has one block per CTA)
+  for (int64_t tb = (int64_t)blockIdx.x * TOK; tb < nT; tb += WIN ? (int64_t)gridDim.x * TOK : nT)
   for (int tt = warp; tt < TOK; tt += NW) {
     if (tb + tt >= nT) break;
     const int64_t t = t0 + tb + tt;
@@ -140,7 +141,7 @@ combine_kernel(const E* __restrict__ rep, const int32_t* __restrict__ pos, const
     }
     // every replica row is read exactly once: once all lanes have consumed their loads, drop the
     // rows' lines from L2 without a write-back (one lane per 128-byte line; rows are line-aligned)
-    if (discard && rep) {
+    if (WIN && discard && rep) {
       __syncwarp();
       for (int ch = lane; ch < nchunk; ch += 32)
         if ((ch & 7) == 0)
@@ -182,7 +183,7 @@ void launch_combine_window(int dtype, const Routing& rt, const void* rep, int d_
   while (tok > 16 && (max_tokens + tok - 1) / tok < 8 * 148) tok /= 2;
   const dim3 grid((unsigned)std::min<int64_t>((max_tokens + tok - 1) / tok, 16 * 148), 1u);
 #define MHL_CW(E, KM)                                                                                        \
-  combine_kernel<E, false, KM, false><<<grid, 256, 0, s>>>((const E*)rep, rt.pos, rt.idx, nullptr, nullptr, rt.H, rt.T, \
+  combine_kernel<E, false, KM, false, true><<<grid, 256, 0, s>>>((const E*)rep, rt.pos, rt.idx, nullptr, nullptr, rt.H, rt.T, \
                                                            rt.k, d_h, rt.N_e, rt.Rp, 0, 0, (E*)out, ldo, tok, h, tr,     \
                                                            discard ? 1 : 0)
   if (dtype == 1) {

@@ -555,3 +555,32 @@ def test_projection_gemms_row_invariant_across_M():
         part = _run_gpu(cfg.replace(T=M), W, x[:M], dout[:M])
         np.testing.assert_array_equal(part["out"], full["out"][:M], err_msg=f"out M={M}")
         np.testing.assert_array_equal(part["dx"], full["dx"][:M], err_msg=f"dx M={M}")
+
+
+@pytest.mark.parametrize("d_h,d_e,N_e,k,T", [(256, 128, 64, 8, 4000), (128, 64, 32, 4, 3000)])
+def test_windowed_combine_bitwise_equals_default(d_h, d_e, N_e, k, T):
+    """NEXT-1 experiment (MHL_FLAG_WINDOWED_COMBINE): the expert kernels and the combines alternating
+    per token window (replica rows discarded from L2 after their one read) give the same bits as one
+    expert launch + one combine launch, forward and backward, and match the oracle."""
+    _need_gpu()
+    from paper_2602_04870_b200.layer import MHLatentMoE, torch_dtype, weights_to_device
+    cfg = LayerConfig("win", T=T, d=2 * d_h, N_h=2, d_h=d_h, N_e=N_e, k=k, d_e=d_e, dtype="bf16")
+    W, x, dout = make_problem(cfg, 17, "exact")
+    Wd = weights_to_device(W, cfg.dtype)
+    td = torch_dtype(cfg.dtype)
+    xd = torch.from_numpy(x).to("cuda", td)
+    dd = torch.from_numpy(dout).to("cuda", td)
+    res = []
+    for win in (True, False):
+        L = MHLatentMoE(cfg.T, cfg.d, cfg.N_h, cfg.d_h, cfg.N_e, cfg.k, cfg.d_e, cfg.dtype, windowed=win)
+        out, _, _ = L.forward(xd, Wd)
+        g = L.alloc_grads()
+        dx = L.backward(xd, Wd, dd, g)
+        torch.cuda.synchronize()
+        L.check_status()
+        assert ("windowed_combine" in L.paths()) == win
+        res.append({"out": out.cpu(), "dx": dx.cpu(), **{kk: v.cpu() for kk, v in g.items()}})
+    for key in res[0]:
+        assert torch.equal(res[0][key], res[1][key]), key
+    g = _run_gpu(cfg, W, x, dout)
+    _compare(cfg, W, x, dout, g, dist="exact")
