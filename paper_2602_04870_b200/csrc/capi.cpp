@@ -95,6 +95,7 @@ NcclApi& nccl() {
 // Config validation and buffer layout (pure host)
 // ------------------------------------------------------------------------------------------
 constexpr size_t kAlign = 256;
+constexpr int kMaxA2aChunks = 8;   // token chunks of one HP exchange (hp_exchange)
 inline size_t align_up(size_t v) { return (v + kAlign - 1) / kAlign * kAlign; }
 
 struct Dims {
@@ -284,6 +285,7 @@ struct mhl_plan_s {
   // HP exchanges (G > 1): comm stream pipelined against the producers on the compute stream
   cudaStream_t comm_stream = nullptr;
   cudaEvent_t ev_prod = nullptr, ev_comm = nullptr;
+  cudaEvent_t ev_chunk[kMaxA2aChunks] = {};   // chunk c of an exchange has landed (hp_exchange)
   std::atomic<uint64_t> launches{0};
   std::atomic<uint32_t> paths{0};     // MHL_PATH_* bits of the kernels launched (mhl_kernel_paths)
   // fault injection: MHL_FAULT_INJECT=gates|out|dx|dW1 at plan creation scales that
@@ -429,15 +431,20 @@ mhl_status Gemm::operator()(bool ta, bool tb, int64_t M, int64_t N, int64_t K, c
   return MHL_OK;
 }
 
-// Equal-split all-to-all (P:805-P:806), pipelined with its producer.  Step
-// i = 0..G-1 sends the block rank r addresses to q = (r+i) mod G and receives the block of
-// src = (r-i) mod G, so at every step each rank's send meets its peer's receive.  produce(i)
-// enqueues on the compute stream `s` whatever writes step i's outgoing block (step 0 is the self
-// block, which its producer writes straight into place); step i's exchange waits only for that
-// producer and runs on the plan's comm stream while produce(i+1) runs on `s`.  tail() enqueues
-// more independent work on `s` (the dW_out GEMM) that overlaps the last exchanges; `s` then waits
-// for the comm stream.  Bytes are k-independent and counted per posted send.
-//   send[v]  [G][blk]   outgoing blocks of (virtual) rank v
+// Equal-split all-to-all (P:805-P:806), pipelined with its producer and its consumer (SURVEY
+// §8(e)).  The T_loc rows of every block are cut into C token chunks (chunk boundaries c*T_loc/C,
+// MHL_A2A_CHUNKS, default 4).  For chunk c, step i = 0..G-1 sends the chunk of the block rank r
+// addresses to q = (r+i) mod G and receives that of src = (r-i) mod G, so at every step each rank's
+// send meets its peer's receive.  produce(c, i) enqueues on the compute stream `s` whatever writes
+// step i's outgoing chunk (step 0, the self block, is written straight into place); each step's
+// exchange waits only for its producer and runs on the plan's comm stream while the compute stream
+// produces the next one.  consume(c) — the row-chunk GEMM that needs every source's chunk c (F8,
+// B1's dgrad) — is enqueued on `s` after chunk c+1 has been produced, waiting only for chunk c's
+// exchange, so it overlaps chunk c+1's.  Row chunks keep the per-row GEMM programs (pinned
+// algorithm, no split-K), so every output row has the same bits whatever C and G are.  tail()
+// enqueues more independent work on `s`; `s` then waits for the comm stream.  Bytes are
+// k-independent and counted per posted send.
+//   send[v]  [G][blk]   outgoing blocks of (virtual) rank v, blk = rows * (parts * row_bytes)
 //   recv[v]  [G][blk]   incoming blocks (NCCL mode; loopback copies straight to their destination)
 //   place[v] optional: incoming block src is then copied into columns [src*row_bytes, ...) of the
 //            [rows][pitch] matrix place[v] (F7 -> cat, B2 -> dXs), else recv itself is the target
@@ -453,49 +460,69 @@ struct Xfer {
   size_t part_dst = 0;
 };
 
-template <class Produce, class Tail>
-mhl_status hp_exchange(mhl_plan p, const Xfer& X, cudaStream_t s, Produce produce, Tail tail) {
+int a2a_chunks(int64_t rows) {
+  static const int env = getenv("MHL_A2A_CHUNKS") ? atoi(getenv("MHL_A2A_CHUNKS")) : 4;
+  return (int)std::max<int64_t>(1, std::min<int64_t>({(int64_t)env, (int64_t)kMaxA2aChunks, rows}));
+}
+inline int64_t chunk_row(int64_t rows, int C, int c) { return rows * c / C; }
+
+template <class Produce, class Consume, class Tail>
+mhl_status hp_exchange(mhl_plan p, const Xfer& X, cudaStream_t s, Produce produce, Consume consume, Tail tail) {
   const Dims& m = p->m;
   cudaStream_t cs = p->comm_stream;
   const size_t blk = X.blk;
-  for (int i = 0; i < m.G; ++i) {
-    MHL_TRY(produce(i));
-    if (i == 0) continue;
-    MHL_CUDA(cudaEventRecord(p->ev_prod, s));
-    MHL_CUDA(cudaStreamWaitEvent(cs, p->ev_prod, 0));
-    if (m.loopback) {
-      for (int v = 0; v < m.G; ++v) {
-        const int q = (v + i) % m.G;
-        if (!X.place.empty())
+  const int64_t rows = X.rows;
+  const size_t rb = blk / (size_t)rows;   // bytes of one block row
+  const int C = a2a_chunks(rows);
+  for (int c = 0; c < C; ++c) {
+    const int64_t r0 = chunk_row(rows, C, c), nr = chunk_row(rows, C, c + 1) - r0;
+    for (int i = 0; i < m.G; ++i) {
+      MHL_TRY(produce(c, i));
+      if (i == 0) continue;
+      MHL_CUDA(cudaEventRecord(p->ev_prod, s));
+      MHL_CUDA(cudaStreamWaitEvent(cs, p->ev_prod, 0));
+      if (m.loopback) {
+        for (int v = 0; v < m.G; ++v) {
+          const int q = (v + i) % m.G;
+          const char* src = X.send[v] + q * blk + r0 * rb;
+          if (!X.place.empty())
+            for (int pi = 0; pi < X.parts; ++pi)
+              mhl::launch_copy_rows(src + pi * X.row_bytes, (int64_t)(X.parts * X.row_bytes),
+                                    X.place[q] + r0 * X.pitch + pi * X.part_dst + v * X.row_bytes, (int64_t)X.pitch,
+                                    nr, (int64_t)X.row_bytes, cs);
+          else
+            MHL_CUDA(cudaMemcpyAsync(X.recv[q] + v * blk + r0 * rb, src, nr * rb, cudaMemcpyDeviceToDevice, cs));
+          p->a2a_bytes_posted += nr * rb;
+          p->paths |= MHL_PATH_A2A_LOOPBACK;
+          if (!X.place.empty()) p->launches += X.parts;
+        }
+      } else {
+        const int r = m.rank, q = (r + i) % m.G, src = (r - i + m.G) % m.G;
+        NcclApi& api = nccl();
+        MHL_NCCL(api.GroupStart());
+        MHL_NCCL(api.Send(X.send[0] + q * blk + r0 * rb, nr * rb, ncclUint8, q, p->comm, cs));
+        MHL_NCCL(api.Recv(X.recv[0] + src * blk + r0 * rb, nr * rb, ncclUint8, src, p->comm, cs));
+        MHL_NCCL(api.GroupEnd());
+        p->a2a_bytes_posted += nr * rb;
+        p->paths |= MHL_PATH_A2A_NCCL;
+        p->launches++;
+        if (!X.place.empty()) {
           for (int pi = 0; pi < X.parts; ++pi)
-            mhl::launch_copy_rows(X.send[v] + q * blk + pi * X.row_bytes, (int64_t)(X.parts * X.row_bytes),
-                                  X.place[q] + pi * X.part_dst + v * X.row_bytes, (int64_t)X.pitch, X.rows,
-                                  (int64_t)X.row_bytes, cs);
-        else
-          MHL_CUDA(cudaMemcpyAsync(X.recv[q] + v * blk, X.send[v] + q * blk, blk, cudaMemcpyDeviceToDevice, cs));
-        p->a2a_bytes_posted += blk;
-        p->paths |= MHL_PATH_A2A_LOOPBACK;
-        if (!X.place.empty()) p->launches += X.parts;
-      }
-    } else {
-      const int r = m.rank, q = (r + i) % m.G, src = (r - i + m.G) % m.G;
-      NcclApi& api = nccl();
-      MHL_NCCL(api.GroupStart());
-      MHL_NCCL(api.Send(X.send[0] + q * blk, blk, ncclUint8, q, p->comm, cs));
-      MHL_NCCL(api.Recv(X.recv[0] + src * blk, blk, ncclUint8, src, p->comm, cs));
-      MHL_NCCL(api.GroupEnd());
-      p->a2a_bytes_posted += blk;
-      p->paths |= MHL_PATH_A2A_NCCL;
-      p->launches++;
-      if (!X.place.empty()) {
-        for (int pi = 0; pi < X.parts; ++pi)
-          mhl::launch_copy_rows(X.recv[0] + src * blk + pi * X.row_bytes, (int64_t)(X.parts * X.row_bytes),
-                                X.place[0] + pi * X.part_dst + src * X.row_bytes, (int64_t)X.pitch, X.rows,
-                                (int64_t)X.row_bytes, cs);
-        p->launches += X.parts;
+            mhl::launch_copy_rows(X.recv[0] + src * blk + r0 * rb + pi * X.row_bytes, (int64_t)(X.parts * X.row_bytes),
+                                  X.place[0] + r0 * X.pitch + pi * X.part_dst + src * X.row_bytes, (int64_t)X.pitch,
+                                  nr, (int64_t)X.row_bytes, cs);
+          p->launches += X.parts;
+        }
       }
     }
+    MHL_CUDA(cudaEventRecord(p->ev_chunk[c], cs));
+    if (c >= 1) {   // chunk c-1 is complete on every rank once its exchange is: consume it now
+      MHL_CUDA(cudaStreamWaitEvent(s, p->ev_chunk[c - 1], 0));
+      MHL_TRY(consume(c - 1, chunk_row(rows, C, c - 1), chunk_row(rows, C, c) - chunk_row(rows, C, c - 1)));
+    }
   }
+  MHL_CUDA(cudaStreamWaitEvent(s, p->ev_chunk[C - 1], 0));
+  MHL_TRY(consume(C - 1, chunk_row(rows, C, C - 1), rows - chunk_row(rows, C, C - 1)));
   MHL_TRY(tail());
   MHL_CUDA(cudaEventRecord(p->ev_comm, cs));
   MHL_CUDA(cudaStreamWaitEvent(s, p->ev_comm, 0));
@@ -882,6 +909,9 @@ mhl_status hp_plan(const mhl_config* cfg, const uint8_t* nccl_id, mhl_plan* out)
         cudaEventCreateWithFlags(&p->ev_prod, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&p->ev_comm, cudaEventDisableTiming) != cudaSuccess)
       return cleanup(fail(MHL_ERR_CUDA, "comm stream / events"));
+    for (auto& e : p->ev_chunk)
+      if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess)
+      return cleanup(fail(MHL_ERR_CUDA, "comm stream / events"));
   }
   if (need_nccl) {
     NcclApi& api = nccl();
@@ -914,6 +944,8 @@ mhl_status hp_plan_destroy(mhl_plan p) {
   if (p->h2d_stream) cudaStreamDestroy(p->h2d_stream);
   if (p->comm_stream) cudaStreamDestroy(p->comm_stream);
   for (cudaEvent_t e : {p->ev_prod, p->ev_comm})
+    if (e) cudaEventDestroy(e);
+  for (cudaEvent_t e : p->ev_chunk)
     if (e) cudaEventDestroy(e);
   if (p->d2h_stream) cudaStreamDestroy(p->d2h_stream);
   for (auto e : p->pool) cudaEventDestroy(e);
@@ -954,22 +986,25 @@ mhl_status forward_impl(mhl_plan p, const void* x, const mhl_weights* w, void* o
   {
     MHL_SPAN("F1F2_proj_in_a2a");
     Xfer X;
-    X.blk = blk_s;
+    X.blk = blk_s; X.rows = m.T_loc;
     for (auto& R : ranks) { X.send.push_back(R.ws + F.send1); X.recv.push_back(R.saved + S.Xs); }
-    MHL_TRY(hp_exchange(p, X, s, [&](int i) -> mhl_status {
+    const int C = a2a_chunks(m.T_loc);
+    MHL_TRY(hp_exchange(p, X, s, [&](int c, int i) -> mhl_status {
+      const int64_t r0 = chunk_row(m.T_loc, C, c), nr = chunk_row(m.T_loc, C, c + 1) - r0;
       for (int v = 0; v < VR; ++v) {
         const RankPtrs& R = ranks[v];
         const int rk = rank_of(v), q = (rk + i) % m.G;
-        char* dst = i == 0 ? R.saved + S.Xs + rk * blk_s : R.ws + F.send1 + q * blk_s;
-        MHL_TRY(gemm(false, true, m.T_loc, m.HD, m.d, R.x, m.d, at(w->W_in, (size_t)q * m.HD * m.d * m.el), m.d,
+        char* dst = (i == 0 ? R.saved + S.Xs + rk * blk_s : R.ws + F.send1 + q * blk_s) + r0 * m.XW * m.el;
+        const char* xr = at(R.x, (size_t)r0 * m.d * m.el);
+        MHL_TRY(gemm(false, true, nr, m.HD, m.d, xr, m.d, at(w->W_in, (size_t)q * m.HD * m.d * m.el), m.d,
                      dst, m.XW, false, 0.0f));
         if (m.rtok)   // routing sub-tokens of q's heads: W_in rows D + q*HD.., same block
-          MHL_TRY(gemm(false, true, m.T_loc, m.HD, m.d, R.x, m.d,
+          MHL_TRY(gemm(false, true, nr, m.HD, m.d, xr, m.d,
                        at(w->W_in, ((size_t)m.D + (size_t)q * m.HD) * m.d * m.el), m.d,
                        dst + (size_t)m.HD * m.el, m.XW, false, 0.0f));
       }
       return MHL_OK;
-    }, [] { return MHL_OK; }));
+    }, [](int, int64_t, int64_t) { return MHL_OK; }, [] { return MHL_OK; }));
   }
   // F3-F5 per rank
   for (int v = 0; v < VR; ++v) MHL_TRY(moe_forward_local(p, ranks[v], nullptr, s));
@@ -982,26 +1017,32 @@ mhl_status forward_impl(mhl_plan p, const void* x, const mhl_weights* w, void* o
     for (auto& R : ranks) {
       X.send.push_back(R.ws + F.send2); X.recv.push_back(R.ws + F.recv2); X.place.push_back(R.saved + S.cat);
     }
-    MHL_TRY(hp_exchange(p, X, s, [&](int i) -> mhl_status {
+    const int C = a2a_chunks(m.T_loc);
+    MHL_TRY(hp_exchange(p, X, s, [&](int c, int i) -> mhl_status {
+      const int64_t r0 = chunk_row(m.T_loc, C, c), nr = chunk_row(m.T_loc, C, c + 1) - r0;
       for (int v = 0; v < VR; ++v) {
         const RankPtrs& R = ranks[v];
         const int rk = rank_of(v), q = (rk + i) % m.G;
         const mhl::Routing rt = routing_view(m, R.saved);
         if (i == 0)
-          mhl::launch_combine_fwd(m.dtype, rt, R.ws + F.Yrep, m.d_h, R.saved + S.cat + rk * X.row_bytes, m.D, s,
-                                  (int64_t)q * m.T_loc, m.T_loc);
+          mhl::launch_combine_fwd(m.dtype, rt, R.ws + F.Yrep, m.d_h,
+                                  R.saved + S.cat + r0 * X.pitch + rk * X.row_bytes, m.D, s, (int64_t)q * m.T_loc + r0,
+                                  nr);
         else
-          mhl::launch_combine_fwd(m.dtype, rt, R.ws + F.Yrep, m.d_h, R.ws + F.send2 + q * blk, m.HD, s,
-                                  (int64_t)q * m.T_loc, m.T_loc);
+          mhl::launch_combine_fwd(m.dtype, rt, R.ws + F.Yrep, m.d_h, R.ws + F.send2 + q * blk + r0 * X.row_bytes, m.HD,
+                                  s, (int64_t)q * m.T_loc + r0, nr);
         p->launches++;
       }
       return MHL_OK;
+    }, [&](int, int64_t r0, int64_t nr) -> mhl_status {
+      // F8 on the token chunk whose head outputs have all arrived: out = cat W_out^T (Eq. 6)
+      for (auto& R : ranks) {
+        MHL_SPAN("F8_proj_out");
+        MHL_TRY(gemm(false, true, nr, m.d, m.D, R.saved + S.cat + r0 * X.pitch, m.D, w->W_out, m.D,
+                     at(R.out, (size_t)r0 * m.d * m.el), m.d, false, 0.0f));
+      }
+      return MHL_OK;
     }, [] { return MHL_OK; }));
-  }
-  // F8: out = cat W_out^T (Eq. 6)
-  for (auto& R : ranks) {
-    MHL_SPAN("F8_proj_out");
-    MHL_TRY(gemm(false, true, m.T_loc, m.d, m.D, R.saved + S.cat, m.D, w->W_out, m.D, R.out, m.d, false, 0.0f));
   }
   return check_kernels(p);
 }
@@ -1042,18 +1083,20 @@ mhl_status backward_impl(mhl_plan p, const void* x, const mhl_weights* w, const 
   {
     MHL_SPAN("B8B7_proj_out_bwd_a2a");
     Xfer X;
-    X.blk = blk;
+    X.blk = blk; X.rows = m.T_loc;
     for (auto& R : ranks) { X.send.push_back(R.ws + B.send3); X.recv.push_back(R.ws + B.dY); }
-    MHL_TRY(hp_exchange(p, X, s, [&](int i) -> mhl_status {
+    const int C = a2a_chunks(m.T_loc);
+    MHL_TRY(hp_exchange(p, X, s, [&](int c, int i) -> mhl_status {
+      const int64_t r0 = chunk_row(m.T_loc, C, c), nr = chunk_row(m.T_loc, C, c + 1) - r0;
       for (int v = 0; v < VR; ++v) {
         const RankPtrs& R = ranks[v];
         const int rk = rank_of(v), q = (rk + i) % m.G;
-        char* dst = i == 0 ? R.ws + B.dY + rk * blk : R.ws + B.send3 + q * blk;
-        MHL_TRY(gemm(false, false, m.T_loc, m.HD, m.d, R.dout, m.d, at(w->W_out, (size_t)q * m.HD * m.el), m.D,
-                     dst, m.HD, false, 0.0f));
+        char* dst = (i == 0 ? R.ws + B.dY + rk * blk : R.ws + B.send3 + q * blk) + r0 * m.HD * m.el;
+        MHL_TRY(gemm(false, false, nr, m.HD, m.d, at(R.dout, (size_t)r0 * m.d * m.el), m.d,
+                     at(w->W_out, (size_t)q * m.HD * m.el), m.D, dst, m.HD, false, 0.0f));
       }
       return MHL_OK;
-    }, [&]() -> mhl_status {
+    }, [](int, int64_t, int64_t) { return MHL_OK; }, [&]() -> mhl_status {
       if (grads->dW_out)
         for (int v = 0; v < VR; ++v)
           MHL_TRY(gemm(true, false, m.d, m.D, m.T_loc, ranks[v].dout, m.d, ranks[v].saved + S.cat, m.D,
@@ -1074,30 +1117,41 @@ mhl_status backward_impl(mhl_plan p, const void* x, const mhl_weights* w, const 
     for (auto& R : ranks) {
       X.send.push_back(R.ws + B.send4); X.recv.push_back(R.ws + B.recv4); X.place.push_back(R.ws + B.dXs);
     }
-    MHL_TRY(hp_exchange(p, X, s, [&](int i) -> mhl_status {
+    const int C = a2a_chunks(m.T_loc);
+    MHL_TRY(hp_exchange(p, X, s, [&](int c, int i) -> mhl_status {
+      const int64_t r0 = chunk_row(m.T_loc, C, c), nr = chunk_row(m.T_loc, C, c + 1) - r0;
       for (int v = 0; v < VR; ++v) {
         const RankPtrs& R = ranks[v];
         const int rk = rank_of(v), q = (rk + i) % m.G;
         const mhl::Routing rt = routing_view(m, R.saved);
-        char* dst = i == 0 ? R.ws + B.dXs + rk * X.row_bytes : R.ws + B.send4 + q * blk4;
+        char* dst = i == 0 ? R.ws + B.dXs + r0 * X.pitch + rk * X.row_bytes
+                           : R.ws + B.send4 + q * blk4 + r0 * (size_t)m.XW * m.el;
         char* dst_r = i == 0 ? dst + X.part_dst : dst + X.row_bytes;
         combine_bwd(m, rt, R.ws + B.dXrep, (const float*)(R.ws + B.dS), (const float*)(R.ws + B.W_rT),
                     !m.simt && mhl::expert_bwd_sm100_supported(m.d_h, m.d_e), dst, i == 0 ? m.Din : m.XW,
-                    dst_r, i == 0 ? m.Din : m.XW, s, (int64_t)q * m.T_loc, m.T_loc);
+                    dst_r, i == 0 ? m.Din : m.XW, s, (int64_t)q * m.T_loc + r0, nr);
         p->launches += m.rtok ? 2 : 1;
+      }
+      return MHL_OK;
+    }, [&](int, int64_t r0, int64_t nr) -> mhl_status {
+      // B1's dgrad on the token chunk whose dXs blocks have all arrived: dx = dXs W_in
+      for (int v = 0; v < VR; ++v) {
+        MHL_SPAN("B1_proj_in_bwd");
+        const RankPtrs& R = ranks[v];
+        MHL_TRY(gemm(false, false, nr, m.d, m.Din, R.ws + B.dXs + r0 * X.pitch, m.Din, w->W_in, m.d,
+                     at(R.out, (size_t)r0 * m.d * m.el), m.d, false, 0.0f));
       }
       return MHL_OK;
     }, [] { return MHL_OK; }));
   }
-  // B1: dx = dXs W_in; dW_in = dXs^T x (rank partial; loopback: summed)
-  for (int v = 0; v < VR; ++v) {
-    MHL_SPAN("B1_proj_in_bwd");
-    const RankPtrs& R = ranks[v];
-    MHL_TRY(gemm(false, false, m.T_loc, m.d, m.Din, R.ws + B.dXs, m.Din, w->W_in, m.d, R.out, m.d, false, 0.0f));
-    if (grads->dW_in)
+  // B1's wgrad: dW_in = dXs^T x (rank partial; loopback: summed in rank order)
+  if (grads->dW_in)
+    for (int v = 0; v < VR; ++v) {
+      MHL_SPAN("B1_proj_in_bwd");
+      const RankPtrs& R = ranks[v];
       MHL_TRY(gemm(true, false, m.Din, m.d, m.T_loc, R.ws + B.dXs, m.Din, R.x, m.d, grads->dW_in, m.d, true,
                    v == 0 ? 0.0f : 1.0f));
-  }
+    }
   return check_kernels(p);
 }
 
