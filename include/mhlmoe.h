@@ -72,6 +72,14 @@ typedef enum { MHL_F32 = 0, MHL_BF16 = 1 } mhl_dtype;
                                  from L2.  Same bits as the default; measured slower (the extra
                                  launches cost more than the HBM round trip they save). */
 
+#define MHL_FLAG_DET_DP   64u  /* deterministic data-parallel weight gradients: dW_in and
+                                 dW_out are formed from fixed 8192-token chunk partials (global
+                                 token order) summed by a fixed pairwise tree, so with
+                                 mhl_dp_reduce they are bitwise identical at every G (T_loc a
+                                 multiple of 8192 with a power-of-two chunk count, G a power of
+                                 two; else MHL_ERR_UNSUPPORTED).  Without LOOPBACK the backward
+                                 returns the rank's subtree; mhl_dp_reduce finishes the tree. */
+
 /* Layer + HP configuration (the paper's problem statement: P:496). */
 typedef struct {
   int64_t tokens;        /* T_loc: tokens on this rank (B*T of P:804)                             */
@@ -240,6 +248,16 @@ MHL_API mhl_status mhl_set_step_timing(mhl_plan plan, int enable);
  * a NULL plan. */
 MHL_API int32_t mhl_step_times(mhl_plan plan, char* names, size_t names_cap, double* ms, int32_t* calls,
                                int32_t max_steps);
+
+/* Deterministic DP reduction of the rank-partial dW_in / dW_out (MHL_FLAG_DET_DP plans, G > 1
+ * without LOOPBACK): all-gathers every rank's subtree result over NCCL into `workspace`
+ * (>= hp_plan_info().workspace_bytes) and sums them in the fixed tree order, in place, on every
+ * rank — the caller's DP all-reduce of R19, bitwise equal to the single-GPU result.  A no-op for
+ * G == 1 or LOOPBACK (the backward already returns the finished tree).  dW_in / dW_out: the same
+ * device tensors the backward wrote.  Errors: MHL_ERR_INVALID_ARGUMENT (NULL, plan without
+ * MHL_FLAG_DET_DP), MHL_ERR_NCCL, MHL_ERR_CUDA. */
+MHL_API mhl_status mhl_dp_reduce(mhl_plan plan, float* dW_in, float* dW_out, void* workspace, size_t workspace_bytes,
+                                 void* stream);
 
 /* Fault injection (test-suite sensitivity): if the environment variable
  * MHL_FAULT_INJECT is set when hp_plan runs, that plan perturbs one step's output by a factor

@@ -59,6 +59,7 @@ struct NcclApi {
   ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
   ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*GroupStart)() = nullptr;
   ncclResult_t (*GroupEnd)() = nullptr;
   const char* (*GetErrorString)(ncclResult_t) = nullptr;
@@ -77,7 +78,7 @@ NcclApi& nccl() {
   if (!h) return api;
 #define LOAD(name) api.name = reinterpret_cast<decltype(api.name)>(dlsym(h, "nccl" #name))
   LOAD(GetUniqueId); LOAD(CommInitRank); LOAD(CommDestroy); LOAD(Send); LOAD(Recv);
-  LOAD(GroupStart); LOAD(GroupEnd); LOAD(GetErrorString);
+  LOAD(GroupStart); LOAD(GroupEnd); LOAD(GetErrorString); LOAD(AllGather);
 #undef LOAD
   api.loaded = api.GetUniqueId && api.CommInitRank && api.Send && api.Recv && api.GroupStart && api.GroupEnd;
   return api;
@@ -96,6 +97,7 @@ NcclApi& nccl() {
 // ------------------------------------------------------------------------------------------
 constexpr size_t kAlign = 256;
 constexpr int kMaxA2aChunks = 8;   // token chunks of one HP exchange (hp_exchange)
+constexpr int64_t kDpChunk = 8192;   // tokens per deterministic-DP weight-gradient partial
 inline size_t align_up(size_t v) { return (v + kAlign - 1) / kAlign * kAlign; }
 
 struct Dims {
@@ -104,6 +106,8 @@ struct Dims {
   bool loopback, simt, pair;
   bool rtok;       // MHL_FLAG_ROUTING_TOKENS (P:1565-P:1570): Xs rows carry [x part | r part]
   bool win;        // MHL_FLAG_WINDOWED_COMBINE (or MHL_WINDOWS=1)
+  bool det_dp;     // MHL_FLAG_DET_DP: dW_in / dW_out from kDpChunk-token chunk partials, fixed tree
+  int dp_nc = 0;   //   chunks per rank
   int XW;          // Xs row width per rank: HD, or 2*HD with routing tokens (r part at column HD)
   int Din;         // W_in rows: D, or 2*D with routing tokens
   int n_rt, max_tiles, max_chunks, seg_align, n_rbwd;
@@ -118,7 +122,7 @@ struct Bump {
 struct SavedLayout { size_t Xs, idx, gate, perm, tok_s, gate_s, pos, off, tiles, ntiles, chunks, nchunks, cbase, ccount, pbase, pcount, load, win, cat, total; };
 // offsets inside one rank's workspace region (forward and backward alias each other)
 struct FwdLayout { size_t send1, Yrep, send2, recv2, hist, tilepref, planes, total; };
-struct BwdLayout { size_t send3, dY, dXrep, dg, dS, dS_s, dH, gA, dwr_part, W_rT, send4, recv4, dXs, dw_part, dw_done, total; };
+struct BwdLayout { size_t send3, dY, dXrep, dg, dS, dS_s, dH, gA, dwr_part, W_rT, send4, recv4, dXs, dw_part, dw_done, dp_part, total; };
 
 SavedLayout saved_layout(const Dims& m) {
   Bump b; SavedLayout L;
@@ -175,6 +179,8 @@ BwdLayout bwd_layout(const Dims& m) {
   L.dXs = b.take((size_t)m.T_loc * m.Din * m.el);
   L.dw_part = b.take(m.simt ? 0 : (size_t)m.max_chunks * 2 * m.d_e * m.d_h * 4);
   L.dw_done = b.take((size_t)m.H * m.N_e * 4);
+  // MHL_FLAG_DET_DP: one fp32 weight-gradient partial per 8192-token chunk of this rank
+  L.dp_part = b.take(m.det_dp ? (size_t)m.dp_nc * std::max((size_t)m.Din * m.d, (size_t)m.d * m.D) * 4 : 0);
   L.total = b.off;
   return L;
 }
@@ -209,6 +215,13 @@ mhl_status make_dims(const mhl_config* c, Dims* m) {
   m->D = m->N_h * m->d_h;
   m->rtok = (c->flags & MHL_FLAG_ROUTING_TOKENS) != 0;
   m->win = (c->flags & MHL_FLAG_WINDOWED_COMBINE) != 0 || (getenv("MHL_WINDOWS") && atoi(getenv("MHL_WINDOWS")) != 0);
+  m->det_dp = (c->flags & MHL_FLAG_DET_DP) != 0;
+  if (m->det_dp) {
+    auto pow2 = [](int64_t v) { return v > 0 && (v & (v - 1)) == 0; };
+    m->dp_nc = (int)(m->T_loc / kDpChunk);
+    if (m->T_loc % kDpChunk != 0 || !pow2(m->dp_nc) || !pow2(m->G))
+      return fail(MHL_ERR_UNSUPPORTED, "MHL_FLAG_DET_DP needs T_loc a power-of-two multiple of 8192 and G a power of two");
+  }
   m->XW = m->HD * (m->rtok ? 2 : 1);
   m->Din = m->D * (m->rtok ? 2 : 1);
   m->dtype = c->dtype;
@@ -526,6 +539,34 @@ mhl_status hp_exchange(mhl_plan p, const Xfer& X, cudaStream_t s, Produce produc
   MHL_TRY(tail());
   MHL_CUDA(cudaEventRecord(p->ev_comm, cs));
   MHL_CUDA(cudaStreamWaitEvent(s, p->ev_comm, 0));
+  return MHL_OK;
+}
+
+// MHL_FLAG_DET_DP: a weight gradient W = Σ_tokens a_tᵀ b_t (dW_out = doᵀ cat, dW_in =
+// dXsᵀ x) as kDpChunk-token chunk partials in global token order (virtual rank v's chunks follow
+// v-1's: R12), summed by a fixed pairwise tree ((P0+P1)+(P2+P3))+...  The same tree at every G
+// (chunk counts are powers of two): with LOOPBACK all ranks' chunks are here and the tree is
+// finished; otherwise the rank's subtree is returned and mhl_dp_reduce completes it.
+template <class AB>
+mhl_status det_wgrad(mhl_plan p, const Gemm& gemm, int VR, AB ab, int64_t M, int64_t N, int64_t lda, int64_t ldb,
+                     const std::vector<char*>& part, float* out, cudaStream_t s) {
+  const Dims& m = p->m;
+  std::vector<float*> slot;
+  for (int v = 0; v < VR; ++v) {
+    const auto op = ab(v);   // (A [tokens][lda], B [tokens][ldb]) of rank v
+    for (int c = 0; c < m.dp_nc; ++c) {
+      float* sl = reinterpret_cast<float*>(part[v]) + (size_t)c * M * N;
+      MHL_TRY(gemm(true, false, M, N, kDpChunk, at(op.first, (size_t)c * kDpChunk * lda * m.el), lda,
+                   at(op.second, (size_t)c * kDpChunk * ldb * m.el), ldb, sl, N, true, 0.0f));
+      slot.push_back(sl);
+    }
+  }
+  for (size_t st = 1; st < slot.size(); st *= 2)
+    for (size_t i = 0; i + st < slot.size(); i += 2 * st) {
+      mhl::launch_add_inplace(slot[i], slot[i + st], M * N, s);
+      p->launches++;
+    }
+  MHL_CUDA(cudaMemcpyAsync(out, slot[0], (size_t)M * N * 4, cudaMemcpyDeviceToDevice, s));
   return MHL_OK;
 }
 
@@ -1061,20 +1102,42 @@ mhl_status backward_impl(mhl_plan p, const void* x, const mhl_weights* w, const 
   for (int r = 0; r < VR; ++r)
     ranks.push_back(rank_view(p, r, const_cast<void*>(saved), workspace, x, dx, d_out, w, grads, nullptr, nullptr));
   const size_t blk = (size_t)m.T_loc * m.HD * m.el;
+  // the two projection weight gradients (rank partials, R19; loopback: all virtual ranks), plain or
+  // as the deterministic chunk tree (MHL_FLAG_DET_DP)
+  std::vector<char*> dp_part;
+  for (auto& R : ranks) dp_part.push_back(R.ws + B.dp_part);
+  auto dW_out_grad = [&]() -> mhl_status {
+    if (!grads->dW_out) return MHL_OK;
+    if (m.det_dp)
+      return det_wgrad(p, gemm, VR, [&](int v) { return std::make_pair(ranks[v].dout, (const void*)(ranks[v].saved + S.cat)); },
+                       m.d, m.D, m.d, m.D, dp_part, grads->dW_out, s);
+    for (int v = 0; v < VR; ++v)
+      MHL_TRY(gemm(true, false, m.d, m.D, m.T_loc, ranks[v].dout, m.d, ranks[v].saved + S.cat, m.D, grads->dW_out, m.D,
+                   true, v == 0 ? 0.0f : 1.0f));
+    return MHL_OK;
+  };
+  auto dW_in_grad = [&]() -> mhl_status {
+    if (!grads->dW_in) return MHL_OK;
+    if (m.det_dp)
+      return det_wgrad(p, gemm, VR, [&](int v) { return std::make_pair((const void*)(ranks[v].ws + B.dXs), ranks[v].x); },
+                       m.Din, m.d, m.Din, m.d, dp_part, grads->dW_in, s);
+    for (int v = 0; v < VR; ++v)
+      MHL_TRY(gemm(true, false, m.Din, m.d, m.T_loc, ranks[v].ws + B.dXs, m.Din, ranks[v].x, m.d, grads->dW_in, m.d,
+                   true, v == 0 ? 0.0f : 1.0f));
+    return MHL_OK;
+  };
   if (m.G == 1) {
     const RankPtrs& R = ranks[0];
     {
       MHL_SPAN("B8_proj_out_bwd");   // B8: dcat = dout W_out, dW_out = dout^T cat
       MHL_TRY(gemm(false, false, m.T_loc, m.D, m.d, R.dout, m.d, w->W_out, m.D, R.ws + B.dY, m.D, false, 0.0f));
-      if (grads->dW_out)
-        MHL_TRY(gemm(true, false, m.d, m.D, m.T_loc, R.dout, m.d, R.saved + S.cat, m.D, grads->dW_out, m.D, true, 0.0f));
+      MHL_TRY(dW_out_grad());
     }
     MHL_TRY(moe_backward_local(p, R, R.ws + B.dY, R.ws + B.dXs, s,
                                m.rtok ? R.ws + B.dXs + (size_t)m.D * m.el : nullptr));   // B5, B3, B6
     MHL_SPAN("B1_proj_in_bwd");      // B1: dx = dXs W_in, dW_in = dXs^T x  (dXs = [dX | dR] with routing tokens)
     MHL_TRY(gemm(false, false, m.T_loc, m.d, m.Din, R.ws + B.dXs, m.Din, w->W_in, m.d, R.out, m.d, false, 0.0f));
-    if (grads->dW_in)
-      MHL_TRY(gemm(true, false, m.Din, m.d, m.T_loc, R.ws + B.dXs, m.Din, R.x, m.d, grads->dW_in, m.d, true, 0.0f));
+    MHL_TRY(dW_in_grad());
     return check_kernels(p);
   }
   auto rank_of = [&](int v) { return m.loopback ? v : m.rank; };
@@ -1096,13 +1159,7 @@ mhl_status backward_impl(mhl_plan p, const void* x, const mhl_weights* w, const 
                      at(w->W_out, (size_t)q * m.HD * m.el), m.D, dst, m.HD, false, 0.0f));
       }
       return MHL_OK;
-    }, [](int, int64_t, int64_t) { return MHL_OK; }, [&]() -> mhl_status {
-      if (grads->dW_out)
-        for (int v = 0; v < VR; ++v)
-          MHL_TRY(gemm(true, false, m.d, m.D, m.T_loc, ranks[v].dout, m.d, ranks[v].saved + S.cat, m.D,
-                       grads->dW_out, m.D, true, v == 0 ? 0.0f : 1.0f));
-      return MHL_OK;
-    }));
+    }, [](int, int64_t, int64_t) { return MHL_OK; }, [&]() -> mhl_status { return dW_out_grad(); }));
   }
   // B5, B3 per rank
   for (int v = 0; v < VR; ++v) MHL_TRY(moe_backward_local(p, ranks[v], ranks[v].ws + B.dY, nullptr, s));
@@ -1145,13 +1202,10 @@ mhl_status backward_impl(mhl_plan p, const void* x, const mhl_weights* w, const 
     }, [] { return MHL_OK; }));
   }
   // B1's wgrad: dW_in = dXs^T x (rank partial; loopback: summed in rank order)
-  if (grads->dW_in)
-    for (int v = 0; v < VR; ++v) {
-      MHL_SPAN("B1_proj_in_bwd");
-      const RankPtrs& R = ranks[v];
-      MHL_TRY(gemm(true, false, m.Din, m.d, m.T_loc, R.ws + B.dXs, m.Din, R.x, m.d, grads->dW_in, m.d, true,
-                   v == 0 ? 0.0f : 1.0f));
-    }
+  {
+    MHL_SPAN("B1_proj_in_bwd");
+    MHL_TRY(dW_in_grad());
+  }
   return check_kernels(p);
 }
 
@@ -1325,6 +1379,31 @@ int32_t mhl_step_times(mhl_plan p, char* names, size_t names_cap, double* ms, in
 }
 
 uint64_t mhl_a2a_bytes_posted(mhl_plan p) { return p ? p->a2a_bytes_posted : 0; }
+
+mhl_status mhl_dp_reduce(mhl_plan p, float* dW_in, float* dW_out, void* workspace, size_t workspace_bytes,
+                         void* stream) {
+  if (!p || !workspace) return fail(MHL_ERR_INVALID_ARGUMENT, "NULL argument");
+  const Dims& m = p->m;
+  if (!m.det_dp) return fail(MHL_ERR_INVALID_ARGUMENT, "mhl_dp_reduce needs a MHL_FLAG_DET_DP plan");
+  if (m.G == 1 || m.loopback) return MHL_OK;   // the backward returned the finished tree
+  if (workspace_bytes < p->info.workspace_bytes)
+    return fail(MHL_ERR_WORKSPACE_TOO_SMALL, "workspace_bytes < hp_plan_info().workspace_bytes");
+  NcclApi& api = nccl();
+  if (!api.AllGather) return fail(MHL_ERR_NCCL, "ncclAllGather not available");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  for (int wgt = 0; wgt < 2; ++wgt) {
+    float* g = wgt == 0 ? dW_in : dW_out;
+    if (!g) continue;
+    const size_t n = wgt == 0 ? (size_t)m.Din * m.d : (size_t)m.d * m.D;
+    if (workspace_bytes < (size_t)m.G * n * 4) return fail(MHL_ERR_WORKSPACE_TOO_SMALL, "mhl_dp_reduce: G x dW bytes");
+    float* all = static_cast<float*>(workspace);   // [G][n]: every rank's subtree, rank order = token order
+    MHL_NCCL(api.AllGather(g, all, n, ncclFloat32, p->comm, s));
+    for (int st = 1; st < m.G; st *= 2)
+      for (int i = 0; i + st < m.G; i += 2 * st) mhl::launch_add_inplace(all + (size_t)i * n, all + (size_t)(i + st) * n, n, s);
+    MHL_CUDA(cudaMemcpyAsync(g, all, n * 4, cudaMemcpyDeviceToDevice, s));
+  }
+  return check_kernels(p);
+}
 
 uint32_t mhl_kernel_paths(mhl_plan p, int reset) {
   if (!p) return 0;

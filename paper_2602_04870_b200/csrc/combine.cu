@@ -235,4 +235,21 @@ void launch_scale(int dtype, void* p, int64_t n, float f, cudaStream_t s) {
   else scale_kernel<float><<<g, 256, 0, s>>>((float*)p, n, f);
 }
 
+// dst[i] += src[i] (fp32): one pairwise step of the deterministic DP tree (MHL_FLAG_DET_DP)
+__global__ void add_inplace_kernel(float4* __restrict__ dst, const float4* __restrict__ src, int64_t n4) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x) {
+    float4 a = dst[i];
+    const float4 b = src[i];
+    a.x += b.x; a.y += b.y; a.z += b.z; a.w += b.w;
+    dst[i] = a;
+  }
+}
+
+void launch_add_inplace(float* dst, const float* src, int64_t n, cudaStream_t s) {
+  if (n <= 0) return;
+  const int64_t n4 = n / 4;   // n is a multiple of 4 (weight matrices with d % 8 == 0)
+  add_inplace_kernel<<<(unsigned)std::min<int64_t>((n4 + 255) / 256, 4 * 148), 256, 0, s>>>((float4*)dst,
+                                                                                          (const float4*)src, n4);
+}
+
 }  // namespace mhl

@@ -118,6 +118,9 @@ void launch_update_bias(const int32_t* load, int H, int N_e, int64_t total, floa
 void launch_combine_fwd(int dtype, const Routing& rt, const void* Yrep, int d_h, void* out, int64_t ldo,
                         cudaStream_t s, int64_t t0 = 0, int64_t nT = -1);
 
+// ---- deterministic DP tree step: dst[i] += src[i], n floats (a multiple of 4)
+void launch_add_inplace(float* dst, const float* src, int64_t n, cudaStream_t s);
+
 // ---- fault injection: p[i] *= f (dtype 1 = bf16, else fp32)
 void launch_scale(int dtype, void* p, int64_t n, float f, cudaStream_t s);
 

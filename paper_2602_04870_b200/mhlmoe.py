@@ -16,14 +16,14 @@ LIB_PATH = os.path.join(_HERE, "libmhlmoe.so")
 
 MHL_F32, MHL_BF16 = 0, 1
 MHL_FLAG_LOOPBACK, MHL_FLAG_SIMT, MHL_FLAG_PAIR, MHL_FLAG_ROUTING_TOKENS, MHL_FLAG_FUSED_COMBINE = 1, 2, 4, 8, 16
-MHL_FLAG_WINDOWED_COMBINE = 32
+MHL_FLAG_WINDOWED_COMBINE, MHL_FLAG_DET_DP = 32, 64
 STATUS = {0: "MHL_OK", 1: "MHL_ERR_INVALID_ARGUMENT", 2: "MHL_ERR_CONFIG", 3: "MHL_ERR_WORKSPACE_TOO_SMALL",
           4: "MHL_ERR_UNSUPPORTED", 5: "MHL_ERR_CUDA", 6: "MHL_ERR_NCCL", 7: "MHL_ERR_NONFINITE"}
 EXPORTS = ["hp_plan_query", "mhl_get_unique_id", "hp_plan", "hp_plan_info", "hp_plan_destroy", "mhlmoe_forward",
            "mhlmoe_backward", "mhlmoe_train_step_host", "mhlmoe_train_step_host_pipelined", "mhl_host_drain",
            "mhlmoe_update_bias", "mhl_check_device_status",
            "mhl_launch_count",
-           "mhl_a2a_bytes_posted", "mhl_set_step_timing", "mhl_step_times", "mhl_kernel_paths",
+           "mhl_a2a_bytes_posted", "mhl_set_step_timing", "mhl_step_times", "mhl_kernel_paths", "mhl_dp_reduce",
            "mhl_status_string", "mhl_last_error"]
 # mhl_kernel_paths bits (include/mhlmoe.h MHL_PATH_*)
 PATHS = {"router_tc": 1 << 0, "router_blk": 1 << 1, "router_simt": 1 << 2, "expert_fwd_tc": 1 << 3,
@@ -90,6 +90,7 @@ def _load():
         "mhl_step_times": (ctypes.c_int32, [P, ctypes.c_char_p, ctypes.c_size_t, ctypes.POINTER(ctypes.c_double),
                                             ctypes.POINTER(ctypes.c_int32), ctypes.c_int32]),
         "mhl_kernel_paths": (ctypes.c_uint32, [P, I]),
+        "mhl_dp_reduce": (I, [P, P, P, P, ctypes.c_size_t, P]),
         "mhl_status_string": (ctypes.c_char_p, [I]),
         "mhl_last_error": (ctypes.c_char_p, []),
     }
@@ -246,6 +247,11 @@ def mhl_step_times(plan: Plan) -> dict:
         raise MhlError(1, "mhl_step_times", "NULL plan")
     keys = [k for k in names.value.decode().split(",") if k]
     return {k: (ms[i], calls[i]) for i, k in enumerate(keys)}
+
+
+def mhl_dp_reduce(plan: Plan, dW_in, dW_out, workspace, stream=None):
+    _check(_lib.mhl_dp_reduce(plan.handle, _ptr(dW_in), _ptr(dW_out), _ptr(workspace), workspace.numel(),
+                              _stream(stream)), "mhl_dp_reduce")
 
 
 def mhl_kernel_paths(plan: Plan, reset: bool = False) -> set:

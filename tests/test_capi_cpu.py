@@ -125,3 +125,18 @@ def test_fused_combine_flag_is_rejected():
         assert C.STATUS[e.status] == "MHL_ERR_UNSUPPORTED"
     else:
         raise AssertionError("MHL_FLAG_FUSED_COMBINE accepted")
+
+
+def test_det_dp_flag_validation():
+    """MHL_FLAG_DET_DP needs T_loc a power-of-two multiple of 8192 and G a power of two."""
+    from paper_2602_04870_b200 import mhlmoe as C
+    ok = C.make_config(16384, 256, 4, 64, 16, 4, 64, "bf16", 2, 0, C.MHL_FLAG_DET_DP)
+    C.hp_plan_query(ok)
+    for T_loc, G in ((12288, 1), (24576, 1), (8192, 3)):
+        cfg = C.make_config(T_loc, 256, 6 if G == 3 else 4, 64, 16, 4, 64, "bf16", G, 0, C.MHL_FLAG_DET_DP)
+        try:
+            C.hp_plan_query(cfg)
+        except C.MhlError as e:
+            assert C.STATUS[e.status] == "MHL_ERR_UNSUPPORTED"
+        else:
+            raise AssertionError((T_loc, G))

@@ -584,3 +584,52 @@ def test_windowed_combine_bitwise_equals_default(d_h, d_e, N_e, k, T):
         assert torch.equal(res[0][key], res[1][key]), key
     g = _run_gpu(cfg, W, x, dout)
     _compare(cfg, W, x, dout, g, dist="exact")
+
+
+def _det_dp_run(cfg, W, x, dout, G):
+    from paper_2602_04870_b200.layer import MHLatentMoE, torch_dtype, weights_to_device
+    td = torch_dtype(cfg.dtype)
+    L = MHLatentMoE(cfg.T // G, cfg.d, cfg.N_h, cfg.d_h, cfg.N_e, cfg.k, cfg.d_e, cfg.dtype, world_size=G,
+                    loopback=G > 1, det_dp=True)
+    Wd = weights_to_device(W, cfg.dtype)
+    xd = torch.from_numpy(x).to("cuda", td)
+    L.forward(xd, Wd)
+    g = L.alloc_grads()
+    L.backward(xd, Wd, torch.from_numpy(dout).to("cuda", td), g)
+    torch.cuda.synchronize()
+    L.check_status()
+    return {k: v.cpu().numpy() for k, v in g.items()}
+
+
+def test_det_dp_weight_gradients_bitwise_equal_across_G():
+    """MHL_FLAG_DET_DP: dW_in and dW_out as 8192-token chunk partials summed by one fixed
+    pairwise tree are bitwise identical at G = 1, 2, 4, 8 (strong scaling, global T = 65536, loopback
+    ranks) — unlike the default rank partials (R19), which agree only to ~1e-4 — and equal the default
+    single-GPU GEMM to fp32 summation-order accuracy."""
+    _need_gpu()
+    cfg = PRESETS["paper"]
+    W, x, dout = make_problem(cfg, 2, "paper")
+    g1 = _det_dp_run(cfg, W, x, dout, 1)
+    for G in (2, 4, 8):
+        gG = _det_dp_run(cfg, W, x, dout, G)
+        for key in ("dW_in", "dW_out", "dW_r", "dW1", "dW2"):
+            np.testing.assert_array_equal(gG[key], g1[key], err_msg=f"{key} G={G}")
+    ref = _run_gpu(cfg, W, x, dout)
+    for key in ("dW_in", "dW_out"):
+        assert rel_err_slices(g1[key], ref[key], SLICES[key]) < 1e-4, key
+
+
+def test_det_dp_matches_oracle():
+    _need_gpu()
+    cfg = LayerConfig("dp", T=16384, d=256, N_h=2, d_h=128, N_e=16, k=4, d_e=64, dtype="bf16")
+    W, x, dout = make_problem(cfg, 21, "exact")
+    g = _det_dp_run(cfg, W, x, dout, 1)
+    P = {k: v.astype(np.float64) for k, v in W.items()}
+    xs = x.astype(np.float64)
+    ref = _run_gpu(cfg, W, x, dout)
+    C0 = O.layer_forward(P, xs, cfg.k, mode="bf16")
+    rt = check_routing(P, C0, ref["idx"], cfg.k, exact=True)
+    C = O.layer_forward(P, xs, cfg.k, mode="bf16", forced_idx=rt.forced)
+    gr = O.layer_backward(P, xs, dout.astype(np.float64), C)
+    for key in ("dW_in", "dW_out"):
+        assert rel_err_slices(g[key], gr[key], SLICES[key]) <= TOL["bf16"], key
