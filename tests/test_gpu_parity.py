@@ -616,7 +616,7 @@ def test_det_dp_weight_gradients_bitwise_equal_across_G():
             np.testing.assert_array_equal(gG[key], g1[key], err_msg=f"{key} G={G}")
     ref = _run_gpu(cfg, W, x, dout)
     for key in ("dW_in", "dW_out"):
-        assert rel_err_slices(g1[key], ref[key], SLICES[key]) < 1e-4, key
+        assert rel_err_slices(g1[key], ref[key], SLICES[key]) < 5e-4, key   # fp32 sums over 65536 tokens, two orders
 
 
 def test_det_dp_matches_oracle():
