@@ -514,12 +514,15 @@ def test_xs_rounding_within_r22_bound():
     assert not np.any(diff & ~amb), (f"{int(np.sum(diff & ~amb))} Xs elements outside the R22 band round differently "
                                      f"(need scale {need.max():.2f} > {FP32_ACC_SCALE})")
     assert amb.mean() < 0.03, f"R22 band covers {100 * amb.mean():.2f} % of the elements"
-    # and the flips inside the band are single-ulp moves to the neighbouring bf16 value
-    if np.any(diff):   # adjacent bf16 values: their bit patterns, as ordered integers, differ by one
-        def ordbits(v):
-            u = (np.asarray(v, np.float32).view(np.uint32) >> 16).astype(np.int64)
-            return np.where(u & 0x8000, -(u & 0x7FFF), u)
-        assert np.all(np.abs(ordbits(g["Xs"][diff]) - ordbits(C0.Xs[diff])) == 1)
+    # and every flipped element is the bf16 rounding of a value within the band of the exact one:
+    # |gpu - exact| <= delta + ulp(gpu) / 2 (small elements whose band spans several ulps may move by
+    # more than one ulp)
+    if np.any(diff):
+        unit = 2.0 ** -24 * np.sqrt(xs.shape[1]) * np.sqrt((xs * xs) @ (P["W_in"] ** 2).T)
+        gv = g["Xs"][diff].astype(np.float64)
+        _m, e = np.frexp(gv)
+        bound = FP32_ACC_SCALE * unit[diff] + np.ldexp(1.0, e - 9)
+        assert np.all(np.abs(gv - C0.Xs_pre[diff]) <= bound * (1 + 1e-9))
 
 
 @pytest.mark.parametrize("site,cfgname,dist", [("gates", "exact_small", "exact"), ("out", "tiny", "conf"),
