@@ -311,7 +311,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample", type=int, default=256)
-    ap.add_argument("--graph", action="store_true", help="replay the step as one CUDA graph (default for fwd-only configs)")
+    ap.add_argument("--graph", action="store_true", help="(default at G = 1) replay the step as one CUDA graph")
     ap.add_argument("--no-graph", action="store_true")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
@@ -379,9 +379,11 @@ def main():
     torch.cuda.synchronize(dev)
     launches_per_step = L.launches() - n0
 
-    # the forward-only small config is launch-bound unless graphed: capture one step
-    # (every launch of the library, cuBLASLt included, on one stream) and replay it
-    use_graph = G == 1 and not args.no_graph and (args.graph or cfg.fwd_only)
+    # CUDA graph: capture one step (every launch of the library, cuBLASLt included, on one stream)
+    # and replay it — SURVEY 8(d) asks for it on the launch-bound forward-only small config; at
+    # paper scale it removes the ~0.1 ms of launch gaps between the ~25 kernels of a step.  G = 1
+    # only (the multi-rank step keeps its NCCL exchanges eager).
+    use_graph = G == 1 and not args.no_graph
     graph = None
     if use_graph:
         gs = torch.cuda.Stream(dev)
