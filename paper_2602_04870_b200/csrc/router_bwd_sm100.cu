@@ -132,21 +132,22 @@ router_bwd_sm100_kernel(const __grid_constant__ CUtensorMap xmap, const int32_t*
     // ============================ dS builders (thread tt < 64 = token of the step), then epilogue
     const int tt = tid - 64;
     uint32_t eph[2] = {0, 0};
-    float gv[KMAX], dv[KMAX];
-    int ev[KMAX];
-    auto load = [&](int s) {
+    // the step's gates / dg / expert ids are prefetched two steps ahead (two register sets, the
+    // step loop unrolled by two): their global-load latency stalled the builders (ncu r2c: long
+    // scoreboard + the builders' barrier held 40 % of the kernel's samples with one step of lookahead)
+    struct Rt { float g[KMAX], d[KMAX]; int e[KMAX]; };
+    auto load = [&](Rt& r, int s) {
       const int64_t t = (s0 + s) * kStep + tt;
 #pragma unroll
-      for (int j = 0; j < KMAX; ++j) { gv[j] = 0.f; dv[j] = 0.f; ev[j] = -1; }
+      for (int j = 0; j < KMAX; ++j) { r.g[j] = 0.f; r.d[j] = 0.f; r.e[j] = -1; }
       if (s < ns && tt < kStep && t < T) {
         const size_t base = ((size_t)h * T + t) * k;
 #pragma unroll
         for (int j = 0; j < KMAX; ++j)
-          if (j < k) { gv[j] = __ldg(gate + base + j); dv[j] = __ldg(dg + base + j); ev[j] = __ldg(idx + base + j); }
+          if (j < k) { r.g[j] = __ldg(gate + base + j); r.d[j] = __ldg(dg + base + j); r.e[j] = __ldg(idx + base + j); }
       }
     };
-    load(0);
-    for (int s = 0; s < ns; ++s) {
+    auto build = [&](const Rt& r, int s) {
       const int bs = s & 1;
       mbar_wait(&bempty[bs], eph[bs] ^ 1); eph[bs] ^= 1;
       uint8_t* bt = smem + L::B + bs * L::BBUF;
@@ -156,14 +157,14 @@ router_bwd_sm100_kernel(const __grid_constant__ CUtensorMap xmap, const int32_t*
       if (tt < kStep && t < T) {
         float sum = 0.f;
 #pragma unroll
-        for (int j = 0; j < KMAX; ++j) if (j < k) sum = fmaf(gv[j], dv[j], sum);
+        for (int j = 0; j < KMAX; ++j) if (j < k) sum = fmaf(r.g[j], r.d[j], sum);
         float* dso = dS + ((size_t)h * T + t) * k;
 #pragma unroll
         for (int j = 0; j < KMAX; ++j) {
           if (j < k) {
-            const float v = gv[j] * (dv[j] - sum);
+            const float v = r.g[j] * (r.d[j] - sum);
             if (blockIdx.z == 0) dso[j] = v;
-            const int el = ev[j] - e0;
+            const int el = r.e[j] - e0;
             if (el >= 0 && el < NE) {
               const bf16 hi = __float2bfloat16_rn(v);
               const bf16 lo = __float2bfloat16_rn(v - __bfloat162float(hi));
@@ -176,7 +177,17 @@ router_bwd_sm100_kernel(const __grid_constant__ CUtensorMap xmap, const int32_t*
       }
       fence_proxy_async();
       mbar_arrive(&bfull[bs]);
-      load(s + 1);
+    };
+    Rt ra, rb;
+    load(ra, 0);
+    load(rb, 1);
+    for (int s = 0; s < ns; s += 2) {
+      build(ra, s);
+      load(ra, s + 2);
+      if (s + 1 < ns) {
+        build(rb, s + 1);
+        load(rb, s + 3);
+      }
     }
     // epilogue: features (TMEM lanes) x experts (columns) -> partial[h][c][i][e]
     mbar_wait(accf, 0);
