@@ -6,6 +6,8 @@
 // Lane l owns 16-byte column chunks l, l+32, ... of a (token, head) row.  Sums run in fixed j
 // order in fp32 (deterministic), rounded once to the storage type.  Rows are written straight
 // into the all-to-all send buffer (row = global token, column block = local head).
+#include <cstdlib>
+
 #include "kernels.h"
 
 namespace mhl {
@@ -177,6 +179,8 @@ void launch_kw(const Routing& rt, const E* rep, const float* dS, const float* W_
 void launch_combine_window(int dtype, const Routing& rt, const void* rep, int d_h, void* out, int64_t ldo, int h,
                            const int32_t* tr, int64_t max_tokens, bool discard, cudaStream_t s) {
   if (max_tokens <= 0) return;
+  static const bool no_discard = getenv("MHL_WIN_DISCARD") && atoi(getenv("MHL_WIN_DISCARD")) == 0;   // A/B
+  if (no_discard) discard = false;
   // max_tokens sizes the grid (the range itself is read on the device; the token loop is
   // grid-stride, so any grid covers it)
   int tok = kCombTok;
