@@ -80,6 +80,12 @@ typedef enum { MHL_F32 = 0, MHL_BF16 = 1 } mhl_dtype;
                                  two; else MHL_ERR_UNSUPPORTED).  Without LOOPBACK the backward
                                  returns the rank's subtree; mhl_dp_reduce finishes the tree. */
 
+#define MHL_FLAG_REQUIRE_TC 128u  /* bf16: refuse (MHL_ERR_UNSUPPORTED at hp_plan / hp_plan_query) any
+                                 shape for which a step would fall back from its tcgen05 kernel to
+                                 the SIMT reference kernel (router, router backward, expert forward
+                                 or backward); without it such shapes run, and mhl_kernel_paths
+                                 tells which path ran. */
+
 /* Layer + HP configuration (the paper's problem statement: P:496). */
 typedef struct {
   int64_t tokens;        /* T_loc: tokens on this rank (B*T of P:804)                             */

@@ -229,6 +229,16 @@ mhl_status make_dims(const mhl_config* c, Dims* m) {
   m->loopback = loop;
   m->simt = (c->flags & MHL_FLAG_SIMT) != 0 || c->dtype == MHL_F32;
   m->pair = !m->simt && (c->flags & MHL_FLAG_PAIR) != 0;
+  if ((c->flags & MHL_FLAG_REQUIRE_TC) && !m->simt) {
+    std::string miss;
+    if (!mhl::router_sm100_supported(m->d_h, m->N_e) && !mhl::router_blk_supported(m->d_h, m->N_e, m->k)) miss += " router";
+    if (!mhl::router_bwd_sm100_supported(m->d_h, m->N_e, m->k)) miss += " router-backward";
+    if (!mhl::expert_fwd_sm100_supported(m->d_h, m->d_e)) miss += " expert-forward";
+    if (!mhl::expert_bwd_sm100_supported(m->d_h, m->d_e)) miss += " expert-backward";
+    if (!miss.empty()) return fail(MHL_ERR_UNSUPPORTED, "MHL_FLAG_REQUIRE_TC: no tcgen05 kernel for this shape:" + miss);
+  }
+  if ((c->flags & MHL_FLAG_REQUIRE_TC) && m->simt)
+    return fail(MHL_ERR_UNSUPPORTED, "MHL_FLAG_REQUIRE_TC with the SIMT path (fp32 or MHL_FLAG_SIMT)");
   m->seg_align = m->pair ? 2 * mhl::kExpertBM : mhl::kExpertBM;
   m->Rp = m->R + (int64_t)m->N_e * m->seg_align;   // each expert segment padded by < seg_align rows
   if (m->Rp >= (int64_t)1 << 31) return fail(MHL_ERR_UNSUPPORTED, "T_glob * k + N_e * seg_align must be < 2^31");

@@ -140,3 +140,19 @@ def test_det_dp_flag_validation():
             assert C.STATUS[e.status] == "MHL_ERR_UNSUPPORTED"
         else:
             raise AssertionError((T_loc, G))
+
+
+def test_require_tc_flag_refuses_simt_fallback_shapes():
+    """MHL_FLAG_REQUIRE_TC: a shape some step has no tcgen05 kernel for is refused up front (pure host),
+    a fully supported one (the paper head) is accepted."""
+    from paper_2602_04870_b200 import mhlmoe as C
+    C.hp_plan_query(C.make_config(1024, 512, 2, 256, 64, 8, 128, "bf16", 1, 0, C.MHL_FLAG_REQUIRE_TC))
+    for (d_h, N_e, k, d_e, dt) in ((256, 16, 4, 128, "bf16"), (192, 64, 8, 64, "bf16"), (32, 16, 4, 32, "bf16"),
+                                   (256, 64, 8, 128, "fp32")):
+        cfg = C.make_config(1024, 2 * d_h, 2, d_h, N_e, k, d_e, dt, 1, 0, C.MHL_FLAG_REQUIRE_TC)
+        try:
+            C.hp_plan_query(cfg)
+        except C.MhlError as e:
+            assert C.STATUS[e.status] == "MHL_ERR_UNSUPPORTED"
+        else:
+            raise AssertionError((d_h, N_e, k, d_e, dt))
