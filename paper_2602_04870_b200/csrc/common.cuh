@@ -75,6 +75,25 @@ __device__ __forceinline__ float2 gelu2(float2 h, float2* dgelu) {
   return __fmul2_rn(h, phi);
 }
 
+// g * gelu(x) for a pair, forward only, with the fewest issued instructions: gelu(x) = x Phi(x) =
+// (x + |x| erf(|x|/sqrt2)) / 2, so with hg = g / 2:  hg * (x + |x| * erfa).  erf from the same
+// Abramowitz-Stegun 7.1.26 form as gelu2 (t = 1 / (1 + p |x| / sqrt2), one rcp + one ex2 per element,
+// |error| <= 1.5e-7), the |x| folded into FFMA operands (18 instructions per pair instead of 23).
+__device__ __forceinline__ float2 gelu2_scaled(float2 h, float hg) {
+  const float2 ea = __fmul2_rn(__fmul2_rn(h, make_float2(-0.72134752044448170f, -0.72134752044448170f)), h);
+  const float dx = fmaf(fabsf(h.x), 0.23164188f, 1.f), dy = fmaf(fabsf(h.y), 0.23164188f, 1.f);
+  const float2 t = make_float2(fast_rcp(dx), fast_rcp(dy));
+  float2 q = __ffma2_rn(make_float2(1.061405429f, 1.061405429f), t, make_float2(-1.453152027f, -1.453152027f));
+  q = __ffma2_rn(q, t, make_float2(1.421413741f, 1.421413741f));
+  q = __ffma2_rn(q, t, make_float2(-0.284496736f, -0.284496736f));
+  q = __ffma2_rn(q, t, make_float2(0.254829592f, 0.254829592f));
+  q = __fmul2_rn(q, t);
+  const float2 e = make_float2(fast_ex2(ea.x), fast_ex2(ea.y));                                  // exp(-x^2/2)
+  const float2 erfa = __ffma2_rn(make_float2(-q.x, -q.y), e, make_float2(1.f, 1.f));             // erf(|x|/sqrt2)
+  const float2 s2 = make_float2(fmaf(fabsf(h.x), erfa.x, h.x), fmaf(fabsf(h.y), erfa.y, h.y));   // 2 gelu(x)
+  return __fmul2_rn(s2, make_float2(hg, hg));
+}
+
 // Order-preserving float -> uint32 (R6): flip sign bit of non-negatives, all bits of negatives.
 __device__ __forceinline__ uint32_t ord32(float v) {
   uint32_t u = __float_as_uint(v == 0.0f ? 0.0f : v);   // canonicalise -0.0

@@ -40,19 +40,22 @@ constexpr int BM = kExpertBM;        // 128 rows = MMA M
 // Warp roles, warpgroup-aligned so the producers can hand registers to the GELU epilogue (setmaxnreg):
 constexpr int kProdWarps = 8;         // warps 0-7: producers, in 4 pairs (a pair fills one X chunk)
 constexpr int kOwners = kProdWarps / 2;
-constexpr int kGeluWarp0 = 8;         // warps 8-15: GELU epilogue (2 per lane quadrant, column halves)
-constexpr int kYWarp0 = 16;           // warps 16-19: Y epilogue (one per lane quadrant)
-constexpr int kMmaWarp = 20;          // warp 20: MMA issuer + TMEM owner
-constexpr int kThreads = 21 * 32;
+constexpr int kGeluWarp0 = 8;         // warps 8-23: GELU epilogue (4 per lane quadrant, column quarters)
+constexpr int kGeluWarps = 16;
+constexpr int kYWarp0 = 24;           // warps 24-27: Y epilogue (one per lane quadrant)
+constexpr int kMmaWarp = 28;          // warp 28: MMA issuer + TMEM owner
+constexpr int kThreads = 29 * 32;
 // Registers: setmaxnreg.inc draws only on registers the CTA's own warps released with
-// setmaxnreg.dec (an increase nothing covers blocks forever).  With 21 warps ptxas sets the launch
-// count to 80 (sub-partition 0 holds six of them in its 16384-register file); the 8 producer warps
-// release 8*32*(80-40), exactly what the 8 GELU warps take to reach 120.
-constexpr int kLaunchRegs = 80, kProdRegs = 40, kGeluRegs = 120;
-static_assert(8 * (kLaunchRegs - kProdRegs) >= 8 * (kGeluRegs - kLaunchRegs),
+// setmaxnreg.dec (an increase nothing covers blocks forever).  With 29 warps ptxas launches at 64
+// registers (sub-partition 0 holds eight of them in its 16384-register file); the 8 producer
+// warps' release (8*32*24) covers the 16 GELU warps' raise to 72.  Four GELU warps per
+// sub-partition (instead of two with twice the columns) hide the MUFU / FMA latency of the
+// GELU chain (3.7 k cycles per tile with two, trace r2e).
+constexpr int kLaunchRegs = 64, kProdRegs = 40, kGeluRegs = 72;
+static_assert(8 * (kLaunchRegs - kProdRegs) >= kGeluWarps * (kGeluRegs - kLaunchRegs),
               "expert fwd: the GELU warps' register increase exceeds the producers' release");
-static_assert(6 * 32 * kLaunchRegs <= 16384, "expert fwd: launch register count does not fit sub-partition 0");
-constexpr int kGeluThreads = 256, kYThreads = 128;
+static_assert(8 * 32 * kLaunchRegs <= 16384, "expert fwd: launch register count does not fit sub-partition 0");
+constexpr int kGeluThreads = kGeluWarps * 32, kYThreads = 128;
 constexpr int kXChunk = BM * 128;    // one 64-column K-chunk of the gathered X tile (16 KB)
 constexpr int kYStage = BM * 128;    // one 64-column block of the Y tile (16 KB)
 
@@ -268,7 +271,7 @@ expert_fwd_sm100_kernel(const __grid_constant__ CUtensorMap w1map, const __grid_
     // ================================================================ GELU epilogue (8 warps)
     // tile i: H (this warp's quadrant rows, DE/2 columns) -> registers, release H, A = bf16(g *
     // gelu(H)) -> TMEM A buffer i % NA once G2(i - NA) has read that buffer.
-    const int q = warp & 3, half = (warp - kGeluWarp0) >> 2;   // lane quadrant, column half
+    const int q = warp & 3, sl = (warp - kGeluWarp0) >> 2;   // lane quadrant, column quarter
     const int row = q * 32 + lane;
     const int et = tid - kGeluWarp0 * 32;
     const uint32_t lane_off = (uint32_t)(q * 32) << 16;
@@ -281,33 +284,41 @@ expert_fwd_sm100_kernel(const __grid_constant__ CUtensorMap w1map, const __grid_
       g_n = __ldg(rt.gate_s + (size_t)u.head * rt.Rp + u.row0 + row);
     };
     fetch(tile_at(0));
+    constexpr int NC = DE / 4;               // H columns of this warp
+    constexpr int CW = NC < 32 ? NC : 32;    // columns per TMEM load
+    auto ld = [&](uint32_t addr, uint32_t* v) {
+      if constexpr (CW == 32) tmem_ld32(addr, *reinterpret_cast<uint32_t(*)[32]>(v));
+      else tmem_ld16(addr, *reinterpret_cast<uint32_t(*)[16]>(v));
+    };
+    auto st = [&](uint32_t addr, const uint32_t* w) {
+      if constexpr (CW == 32) tmem_st16(addr, *reinterpret_cast<const uint32_t(*)[16]>(w));
+      else tmem_st8(addr, *reinterpret_cast<const uint32_t(*)[8]>(w));
+    };
     for (int i = 0;; ++i) {
       const int ti = tile_at(i);
       if (ti < 0) break;
       const int b = i % L::NA;
-      const float g = g_n;
+      const float hg = 0.5f * g_n;
       fetch(tile_at(i + 1));
       mbar_wait_warp(bar(L::B_HFULL), hf.flip());
       if (et == 0) trace_ev(g_trace_fwd, 20, i);
       tc_fence_after();
-      constexpr int NC = DE / 2;
       if constexpr (L::NA == 1) {
-        // single A buffer: G2(i-1) must have read it; stream H 32 columns at a time (NC = 128 values
-        // would not fit in registers), release H after the last load
+        // single A buffer: G2(i-1) must have read it; stream H CW columns at a time, release H after
+        // the last load
         if (i >= 1) { mbar_wait_warp(bar(L::B_G2DONE), gd[0].flip()); tc_fence_after(); }
 #pragma unroll 1
-        for (int c = 0; c < NC; c += 32) {
-          uint32_t v[32], w[16];
-          tmem_ld32(tmem + L::T_H + lane_off + half * NC + c, v);
+        for (int c = 0; c < NC; c += CW) {
+          uint32_t v[CW], w[CW / 2];
+          ld(tmem + L::T_H + lane_off + sl * NC + c, v);
           tmem_ld_wait();
-          if (c + 32 >= NC) { tc_fence_before(); mbar_arrive(bar(L::B_HFREE)); }
+          if (c + CW >= NC) { tc_fence_before(); mbar_arrive(bar(L::B_HFREE)); }
 #pragma unroll
-          for (int u = 0; u < 32; u += 2) {
-            const float2 a = __fmul2_rn(gelu2(make_float2(__uint_as_float(v[u]), __uint_as_float(v[u + 1])), nullptr),
-                                        make_float2(g, g));
+          for (int u = 0; u < CW; u += 2) {
+            const float2 a = gelu2_scaled(make_float2(__uint_as_float(v[u]), __uint_as_float(v[u + 1])), hg);
             w[u / 2] = pack_bf16x2(a.x, a.y);
           }
-          tmem_st16(tmem + L::T_A + lane_off + half * (NC / 2) + c / 2, w);
+          st(tmem + L::T_A + lane_off + sl * (NC / 2) + c / 2, w);
         }
         tmem_st_wait();
         tc_fence_before();
@@ -316,12 +327,7 @@ expert_fwd_sm100_kernel(const __grid_constant__ CUtensorMap w1map, const __grid_
       }
       uint32_t hv[NC];
 #pragma unroll
-      for (int c = 0; c < NC; c += 32) {
-        uint32_t v[32];
-        tmem_ld32(tmem + L::T_H + lane_off + half * NC + c, v);
-#pragma unroll
-        for (int u = 0; u < 32; ++u) hv[c + u] = v[u];
-      }
+      for (int c = 0; c < NC; c += CW) ld(tmem + L::T_H + lane_off + sl * NC + c, hv + c);
       tmem_ld_wait();
       tc_fence_before();
       mbar_arrive(bar(L::B_HFREE));
@@ -329,19 +335,13 @@ expert_fwd_sm100_kernel(const __grid_constant__ CUtensorMap w1map, const __grid_
       uint32_t pa[NC / 2];
 #pragma unroll
       for (int u = 0; u < NC; u += 2) {
-        const float2 a = __fmul2_rn(gelu2(make_float2(__uint_as_float(hv[u]), __uint_as_float(hv[u + 1])), nullptr),
-                                    make_float2(g, g));
+        const float2 a = gelu2_scaled(make_float2(__uint_as_float(hv[u]), __uint_as_float(hv[u + 1])), hg);
         pa[u / 2] = pack_bf16x2(a.x, a.y);
       }
       // A buffer b was last read by G2(i - 2)
       if (i >= L::NA) { mbar_wait_warp(bar(L::B_G2DONE + 8 * b), gd[b].flip()); tc_fence_after(); }
 #pragma unroll
-      for (int c = 0; c < NC / 2; c += 16) {
-        uint32_t w[16];
-#pragma unroll
-        for (int u = 0; u < 16; ++u) w[u] = pa[c + u];
-        tmem_st16(tmem + L::T_A + b * (DE / 2) + lane_off + half * (NC / 2) + c, w);
-      }
+      for (int c = 0; c < NC / 2; c += CW / 2) st(tmem + L::T_A + b * (DE / 2) + lane_off + sl * (NC / 2) + c, pa + c);
       tmem_st_wait();
       tc_fence_before();
       mbar_arrive(bar(L::B_AFULL + 8 * b));
