@@ -318,8 +318,8 @@ expert_fwd_pair_kernel(const __grid_constant__ CUtensorMap w1map, const __grid_c
       uint32_t pa[NC / 2];
 #pragma unroll
       for (int w = 0; w < NC; w += 2) {
-        const float2 a = __fmul2_rn(gelu2(make_float2(__uint_as_float(hv[w]), __uint_as_float(hv[w + 1])), nullptr),
-                                    make_float2(g, g));
+        // the single-CTA kernel's arithmetic (same bits, tested)
+        const float2 a = gelu2_scaled(make_float2(__uint_as_float(hv[w]), __uint_as_float(hv[w + 1])), 0.5f * g);
         pa[w / 2] = pack_bf16x2(a.x, a.y);
       }
 #pragma unroll
