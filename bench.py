@@ -129,7 +129,7 @@ class ClockSampler:
 
 
 # ----------------------------------------------------------------------------- algorithmic work
-def step_work(cfg, T_loc, G):
+def step_work(cfg, T_loc, G, fused_bwd=False):
     """Algorithmic work per step on one GPU, per timed span, in SURVEY.md §8(d)'s units
     (DESIGN.md §6): `flops` = the span's contraction FLOPs (the expert backward includes the
     recompute of H that the IO-aware design implies, P:916-P:978: 5 GEMM units, §8(d) "1.37 TFLOP
@@ -140,7 +140,9 @@ def step_work(cfg, T_loc, G):
     between the backward expert kernels (SURVEY A.5 option c) — are NOT algorithmic bytes: they are
     counted in `impl_bytes`, and the ncu-measured DRAM bytes are reported as `traffic`.  The
     combine spans exist because of v1; their roofline is §8(d)'s v1 combine_pack bytes.  A span's
-    roofline time is max(flops / tensor peak, bytes / HBM peak)."""
+    roofline time is max(flops / tensor peak, bytes / HBM peak).  `fused_bwd`: the B5 input side
+    ran as one kernel (expert_bwd_fused_sm100.cu: span B5_expert_bwd_dx = H, dA' and dX, 3 units;
+    no B5_expert_dx_gemm span; B6 adds the router term, reading dS and the expert ids)."""
     d, N_h, d_h, N_e, k, d_e = cfg.d, cfg.N_h, cfg.d_h, cfg.N_e, cfg.k, cfg.d_e
     D, el = N_h * d_h, (2 if cfg.dtype == "bf16" else 4)
     Din = D * (2 if cfg.routing_tokens else 1)
@@ -174,6 +176,12 @@ def step_work(cfg, T_loc, G):
         "B1_proj_in_bwd": dict(flops=4 * T_loc * d * Din,
                                bytes=T_loc * Din * el + Din * d * el + 2 * T_loc * d * el + Din * d * 4),
     }
+    if fused_bwd:
+        # H, dA' and dXrep = dH W1 (3 units); dH, gA and the per-replica dXrep written: impl
+        w["B5_expert_bwd_dx"] = dict(flops=3 * unit, bytes=2 * subtok * row + 2 * wexp + rep * 12 + rep * 4,
+                                     impl_bytes=2 * rep * erow + rep * row)
+        del w["B5_expert_dx_gemm"]
+        w["B6_combine_bwd"]["bytes"] += rep * 8 + H * N_e * d_h * 4   # dS, expert ids, W_r^T
     for v in w.values():
         v["impl_bytes"] = v["bytes"] + v.get("impl_bytes", 0)
     return w
@@ -489,8 +497,8 @@ def main():
     # ---- roofline of the dominant kernel (largest share of the step)
     (hbm_peak, hbm_src), (tf_peak, tf_src) = load_peaks()
     traffic = load_traffic()
-    work = step_work(cfg, T_loc, G)
     per_step = {k: v[0] / args.steps for k, v in steps_t.items()}
+    work = step_work(cfg, T_loc, G, fused_bwd="B5_expert_bwd_dx" in per_step and "B5_expert_dx_gemm" not in per_step)
     dom = max(per_step, key=per_step.get) if per_step else None
     roof = None
     if dom is not None:

@@ -85,6 +85,11 @@ typedef enum { MHL_F32 = 0, MHL_BF16 = 1 } mhl_dtype;
                                  the SIMT reference kernel (router, router backward, expert forward
                                  or backward); without it such shapes run, and mhl_kernel_paths
                                  tells which path ran. */
+#define MHL_FLAG_BWD_FUSED 256u  /* bf16: run B5's input side (H, dA' -> dg, dH, gA; dX = dH W1) as ONE
+                                 tcgen05 kernel (expert_bwd_fused_sm100.cu) with the router term of
+                                 dX added by B6, instead of the default two kernels (shapes with
+                                 2 d_expert + d_head <= 512; same dg, dH, gA, dW bits; measured
+                                 equal step time at paper scale). */
 
 /* Layer + HP configuration (the paper's problem statement: P:496). */
 typedef struct {
@@ -291,6 +296,8 @@ MHL_API mhl_status mhl_dp_reduce(mhl_plan plan, float* dW_in, float* dW_out, voi
                                                  (NEXT-1; G = 1, bf16 tensor-core path)         */
 #define MHL_PATH_A2A_NCCL         (1u << 12)  /* HP exchanges through NCCL send/recv               */
 #define MHL_PATH_A2A_LOOPBACK     (1u << 13)  /* HP exchanges as device copies (MHL_FLAG_LOOPBACK) */
+#define MHL_PATH_EXPERT_BWD_FUSED (1u << 15)  /* B5 input side (H, dA', dH, gA, dX) in ONE tcgen05
+                                                 kernel; the router term of dX moves to B6      */
 MHL_API uint32_t mhl_kernel_paths(mhl_plan plan, int reset);
 
 MHL_API const char* mhl_status_string(mhl_status s);

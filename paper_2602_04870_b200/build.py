@@ -18,7 +18,7 @@ CUDA = os.environ.get("CUDA_HOME", "/usr/local/cuda")
 NVCC = os.path.join(CUDA, "bin", "nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 CU_SOURCES = ["router.cu", "router_sm100.cu", "tma_host.cu", "cluster.cu", "simt.cu", "combine.cu",
-              "expert_sm100.cu", "expert_bwd_dx_sm100.cu", "expert_dw_sm100.cu",
+              "expert_sm100.cu", "expert_bwd_dx_sm100.cu", "expert_bwd_fused_sm100.cu", "expert_dw_sm100.cu",
               "router_bwd_sm100.cu", "expert_fwd_pair_sm100.cu",
               "router_blk_sm100.cu"]
 CXX_SOURCES = ["capi.cpp"]

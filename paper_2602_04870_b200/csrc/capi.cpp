@@ -106,6 +106,7 @@ struct Dims {
   bool loopback, simt, pair;
   bool rtok;       // MHL_FLAG_ROUTING_TOKENS (P:1565-P:1570): Xs rows carry [x part | r part]
   bool win;        // MHL_FLAG_WINDOWED_COMBINE (or MHL_WINDOWS=1)
+  bool bwd_fused;  // MHL_FLAG_BWD_FUSED (or MHL_BWD_FUSED=1): B5 input side as one kernel
   bool det_dp;     // MHL_FLAG_DET_DP: dW_in / dW_out from kDpChunk-token chunk partials, fixed tree
   int dp_nc = 0;   //   chunks per rank
   int XW;          // Xs row width per rank: HD, or 2*HD with routing tokens (r part at column HD)
@@ -215,6 +216,7 @@ mhl_status make_dims(const mhl_config* c, Dims* m) {
   m->D = m->N_h * m->d_h;
   m->rtok = (c->flags & MHL_FLAG_ROUTING_TOKENS) != 0;
   m->win = (c->flags & MHL_FLAG_WINDOWED_COMBINE) != 0 || (getenv("MHL_WINDOWS") && atoi(getenv("MHL_WINDOWS")) != 0);
+  m->bwd_fused = (c->flags & MHL_FLAG_BWD_FUSED) != 0 || (getenv("MHL_BWD_FUSED") && atoi(getenv("MHL_BWD_FUSED")) != 0);
   m->det_dp = (c->flags & MHL_FLAG_DET_DP) != 0;
   if (m->det_dp) {
     auto pow2 = [](int64_t v) { return v > 0 && (v & (v - 1)) == 0; };
@@ -630,6 +632,14 @@ bool windowed(const Dims& m) {
          mhl::expert_fwd_sm100_supported(m.d_h, m.d_e) && mhl::expert_bwd_sm100_supported(m.d_h, m.d_e);
 }
 
+// B5's input side as ONE kernel (MHL_FLAG_BWD_FUSED, opt-in; expert_bwd_fused_sm100.cu, the router
+// term of dX then moves to B6) where its TMEM budget holds; the default is the K1 + K2 pair, which
+// measured the same step time (the fused kernel's gain went to B6's router term).
+bool bwd_fused(const Dims& m) {
+  return m.bwd_fused && !m.simt && !m.pair && !windowed(m) && m.dtype == MHL_BF16 &&
+         mhl::expert_bwd_sm100_supported(m.d_h, m.d_e) && mhl::expert_bwd_fused_supported(m.d_h, m.d_e);
+}
+
 mhl_status check_kernels(mhl_plan p) {
   if (p->launch_err != cudaSuccess) {
     const cudaError_t e = p->launch_err;
@@ -641,16 +651,17 @@ mhl_status check_kernels(mhl_plan p) {
   return MHL_OK;
 }
 
-// B6 for tokens [t0, t0 + nT): on the tensor-core path K2 already added the router term to each
-// replica row, so B6 is the plain k-row sum (the F6 kernel); the SIMT path adds it here.  With
+// B6 for tokens [t0, t0 + nT): on the split tensor-core path K2 already added the router term to
+// each replica row (rterm_in_rep), so B6 is the plain k-row sum (the F6 kernel); the fused and SIMT
+// paths add it here.  With
 // routing sub-tokens (P:1565-P:1570) the router term is the gradient of r, not of x: dX gets the
 // plain sum (out_x) and dR the router term alone (out_r).
-void combine_bwd(const Dims& m, const mhl::Routing& rt, const void* dXrep, const float* dS, const float* W_rT, bool tc,
+void combine_bwd(const Dims& m, const mhl::Routing& rt, const void* dXrep, const float* dS, const float* W_rT, bool rterm_in_rep,
                  void* out_x, int64_t ld_x, void* out_r, int64_t ld_r, cudaStream_t s, int64_t t0, int64_t nT) {
   if (m.rtok) {
     mhl::launch_combine_fwd(m.dtype, rt, dXrep, m.d_h, out_x, ld_x, s, t0, nT);
     mhl::launch_combine_bwd(m.dtype, rt, nullptr, dS, W_rT, m.d_h, out_r, ld_r, s, t0, nT);
-  } else if (tc) {
+  } else if (rterm_in_rep) {
     mhl::launch_combine_fwd(m.dtype, rt, dXrep, m.d_h, out_x, ld_x, s, t0, nT);
   } else {
     mhl::launch_combine_bwd(m.dtype, rt, dXrep, dS, W_rT, m.d_h, out_x, ld_x, s, t0, nT);
@@ -779,13 +790,19 @@ mhl_status moe_backward_local(mhl_plan p, const RankPtrs& R, const void* dY, voi
   void* dH = R.ws + B.dH;
   void* gA = R.ws + B.gA;
   const bool tc = !m.simt && mhl::expert_bwd_sm100_supported(m.d_h, m.d_e);
+  const bool fused = bwd_fused(m);
   p->paths |= tc ? MHL_PATH_EXPERT_BWD_TC : MHL_PATH_EXPERT_BWD_SIMT;
+  if (fused) p->paths |= MHL_PATH_EXPERT_BWD_FUSED;
   // the all-zero row T of dY (padding rows of every expert tile gather it)
   MHL_CUDA(cudaMemsetAsync(static_cast<char*>(const_cast<void*>(dY)) + (size_t)m.T_g * m.HD * m.el, 0,
                            (size_t)m.HD * m.el, s));
   {
     MHL_SPAN("B5_expert_bwd_dx");
-    if (tc)
+    if (fused) {
+      if (!mhl::launch_expert_bwd_fused_sm100(rt, Xs, m.XW, dY, m.HD, R.W1, R.W2, m.d_h, m.d_e, dXrep, dg, dH, gA,
+                                              p->num_sms, s))
+        return fail(MHL_ERR_CUDA, "fused expert backward: TMA tensor-map encoding failed");
+    } else if (tc)
       mhl::launch_expert_bwd_sm100(rt, Xs, m.XW, dY, m.HD, R.W1, R.W2, m.d_h, m.d_e, dXrep, dg, dH, gA, nullptr,
                                    nullptr, nullptr, nullptr, p->num_sms, s, true, false);
     else
@@ -812,12 +829,12 @@ mhl_status moe_backward_local(mhl_plan p, const RankPtrs& R, const void* dY, voi
     }
     // dS in clustered-row order for K2's router term: a separate scatter kernel (20 us faster than
     // scattering from inside the router backward, r1e)
-    if (tc && !m.rtok) { mhl::launch_sort_ds(rt, dS, (float*)(R.ws + B.dS_s), s); p->launches++; }
+    if (tc && !fused && !m.rtok) { mhl::launch_sort_ds(rt, dS, (float*)(R.ws + B.dS_s), s); p->launches++; }
     mhl::launch_transpose_wr(R.W_r, W_rT, m.H, m.d_h, m.N_e, s);
   }
   // windowed (NEXT-1): the dX GEMM and B6 alternate window by window after the dW kernel
   const bool win_b = tc && dxout && windowed(m);
-  if (tc && !win_b) {
+  if (tc && !fused && !win_b) {
     MHL_SPAN("B5_expert_dx_gemm");
     if (!mhl::launch_expert_dx_gemm_sm100(rt, R.W1, m.d_h, m.d_e, dH, dXrep,
                                           m.rtok ? nullptr : (const float*)(R.ws + B.dS_s), W_rT,
@@ -859,10 +876,11 @@ mhl_status moe_backward_local(mhl_plan p, const RankPtrs& R, const void* dY, voi
     p->launches += 2 * m.H * mhl::kWindows - 2;
   } else if (dxout) {
     MHL_SPAN("B6_combine_bwd");
-    combine_bwd(m, rt, dXrep, dS, W_rT, tc, dxout, m.Din, dxout_r, m.Din, s, 0, -1);
+    combine_bwd(m, rt, dXrep, dS, W_rT, tc && !fused, dxout, m.Din, dxout_r, m.Din, s, 0, -1);
   }
   // K1 + K2 + dW (+ its in-kernel reduce) + router (2) + transpose + combine on the tensor-core path
-  p->launches += (tc ? 7 : (R.dW1 || R.dW2 ? 6 : 5)) - (dxout ? 0 : 1);
+  // (the fused kernel replaces K1 + K2)
+  p->launches += (tc ? (fused ? 6 : 7) : (R.dW1 || R.dW2 ? 6 : 5)) - (dxout ? 0 : 1);
   return check_kernels(p);
 }
 
@@ -1195,7 +1213,8 @@ mhl_status backward_impl(mhl_plan p, const void* x, const mhl_weights* w, const 
                            : R.ws + B.send4 + q * blk4 + r0 * (size_t)m.XW * m.el;
         char* dst_r = i == 0 ? dst + X.part_dst : dst + X.row_bytes;
         combine_bwd(m, rt, R.ws + B.dXrep, (const float*)(R.ws + B.dS), (const float*)(R.ws + B.W_rT),
-                    !m.simt && mhl::expert_bwd_sm100_supported(m.d_h, m.d_e), dst, i == 0 ? m.Din : m.XW,
+                    !m.simt && mhl::expert_bwd_sm100_supported(m.d_h, m.d_e) && !bwd_fused(m), dst,
+                    i == 0 ? m.Din : m.XW,
                     dst_r, i == 0 ? m.Din : m.XW, s, (int64_t)q * m.T_loc + r0, nr);
         p->launches += m.rtok ? 2 : 1;
       }

@@ -214,7 +214,7 @@ void launch_combine_bwd(int dtype, const Routing& rt, const void* dXrep, const f
                         void* out, int64_t ldo, cudaStream_t s, int64_t t0, int64_t nT) {
   if (nT < 0) nT = rt.T - t0;
   if (nT <= 0) return;
-  const bool smem_w = (size_t)rt.N_e * d_h * 4 <= 96 * 1024;
+  const bool smem_w = (size_t)rt.N_e * d_h * 4 <= 160 * 1024;   // W_r^T of the head in smem (1 CTA/SM above 96 KB)
   if (dtype == 1) {
     if (smem_w) launch_kw<bf16, true, true>(rt, (const bf16*)dXrep, dS, W_rT, d_h, (bf16*)out, ldo, t0, nT, s);
     else launch_kw<bf16, true, false>(rt, (const bf16*)dXrep, dS, W_rT, d_h, (bf16*)out, ldo, t0, nT, s);

@@ -145,6 +145,13 @@ bool launch_expert_bwd_dx_sm100(const Routing& rt, const void* Xs, int64_t ldx, 
 // dS_s = dS in sorted-row order [H][Rp], see launch_sort_ds) per expert tile (expert_bwd_dx_sm100.cu)
 bool launch_expert_dx_gemm_sm100(const Routing& rt, const void* W1, int d_h, int d_e, const void* dH, void* dXrep,
                                  const float* dS, const float* W_rT, int num_sms, cudaStream_t s);
+// ONE tcgen05 kernel for the input side of B5 (expert_bwd_fused_sm100.cu): H, dA' recomputed,
+// dg, dH / gA (the dW kernel's inputs) and dXrep = dH W1_e WITHOUT the router term (B6 adds it,
+// launch_combine_bwd).  Shapes with 2 d_e + d_h <= 512 TMEM columns.
+bool expert_bwd_fused_supported(int d_h, int d_e);
+bool launch_expert_bwd_fused_sm100(const Routing& rt, const void* Xs, int64_t ldx, const void* dY, int64_t ldy,
+                                   const void* W1, const void* W2, int d_h, int d_e, void* dXrep, float* dg, void* dH,
+                                   void* gA, int num_sms, cudaStream_t s);
 // tcgen05 dX kernel (dXrep, dg, dH, gA) and/or dW kernel (chunk partials + in-kernel ordered
 // reduce; `done` = H*N_e int counters, zeroed by the launch)
 bool launch_expert_bwd_sm100(const Routing& rt, const void* Xs, int64_t ldx, const void* dY, int64_t ldy,

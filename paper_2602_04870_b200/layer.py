@@ -22,10 +22,11 @@ class MHLatentMoE:
 
     def __init__(self, T_loc, d, N_h, d_h, N_e, k, d_e, dtype="bf16", world_size=1, rank=0, loopback=False,
                  simt=False, nccl_id=None, device="cuda", pair=False, routing_tokens=False, windowed=False,
-                 det_dp=False):
+                 det_dp=False, bwd_fused=False):
         flags = ((C.MHL_FLAG_LOOPBACK if loopback else 0) | (C.MHL_FLAG_SIMT if simt else 0)
                  | (C.MHL_FLAG_PAIR if pair else 0) | (C.MHL_FLAG_ROUTING_TOKENS if routing_tokens else 0)
-                 | (C.MHL_FLAG_WINDOWED_COMBINE if windowed else 0) | (C.MHL_FLAG_DET_DP if det_dp else 0))
+                 | (C.MHL_FLAG_WINDOWED_COMBINE if windowed else 0) | (C.MHL_FLAG_DET_DP if det_dp else 0)
+                 | (C.MHL_FLAG_BWD_FUSED if bwd_fused else 0))
         self.routing_tokens = routing_tokens
         self.cfg = C.make_config(T_loc, d, N_h, d_h, N_e, k, d_e, dtype, world_size, rank, flags)
         self.plan = C.hp_plan(self.cfg, nccl_id)

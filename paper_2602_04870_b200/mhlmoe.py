@@ -16,7 +16,7 @@ LIB_PATH = os.path.join(_HERE, "libmhlmoe.so")
 
 MHL_F32, MHL_BF16 = 0, 1
 MHL_FLAG_LOOPBACK, MHL_FLAG_SIMT, MHL_FLAG_PAIR, MHL_FLAG_ROUTING_TOKENS, MHL_FLAG_FUSED_COMBINE = 1, 2, 4, 8, 16
-MHL_FLAG_WINDOWED_COMBINE, MHL_FLAG_DET_DP, MHL_FLAG_REQUIRE_TC = 32, 64, 128
+MHL_FLAG_WINDOWED_COMBINE, MHL_FLAG_DET_DP, MHL_FLAG_REQUIRE_TC, MHL_FLAG_BWD_FUSED = 32, 64, 128, 256
 STATUS = {0: "MHL_OK", 1: "MHL_ERR_INVALID_ARGUMENT", 2: "MHL_ERR_CONFIG", 3: "MHL_ERR_WORKSPACE_TOO_SMALL",
           4: "MHL_ERR_UNSUPPORTED", 5: "MHL_ERR_CUDA", 6: "MHL_ERR_NCCL", 7: "MHL_ERR_NONFINITE"}
 EXPORTS = ["hp_plan_query", "mhl_get_unique_id", "hp_plan", "hp_plan_info", "hp_plan_destroy", "mhlmoe_forward",
@@ -29,7 +29,8 @@ EXPORTS = ["hp_plan_query", "mhl_get_unique_id", "hp_plan", "hp_plan_info", "hp_
 PATHS = {"router_tc": 1 << 0, "router_blk": 1 << 1, "router_simt": 1 << 2, "expert_fwd_tc": 1 << 3,
          "expert_fwd_pair": 1 << 4, "expert_fwd_simt": 1 << 5, "expert_bwd_tc": 1 << 6, "expert_bwd_simt": 1 << 7,
          "router_bwd_tc": 1 << 8, "router_bwd_simt": 1 << 9, "proj_pinned": 1 << 10, "fused_combine": 1 << 11,
-         "a2a_nccl": 1 << 12, "a2a_loopback": 1 << 13, "windowed_combine": 1 << 14}
+         "a2a_nccl": 1 << 12, "a2a_loopback": 1 << 13, "windowed_combine": 1 << 14,
+         "expert_bwd_fused": 1 << 15}
 
 
 class MhlError(RuntimeError):

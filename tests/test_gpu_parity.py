@@ -23,12 +23,12 @@ def _need_gpu():
         pytest.skip("no GPU")
 
 
-def _run_gpu(cfg: LayerConfig, W, x, dout, G=1, simt=False, backward=True, pair=False):
+def _run_gpu(cfg: LayerConfig, W, x, dout, G=1, simt=False, backward=True, pair=False, bwd_fused=False):
     from paper_2602_04870_b200.layer import MHLatentMoE, torch_dtype, weights_to_device
     td = torch_dtype(cfg.dtype)
     loop = G > 1
     L = MHLatentMoE(cfg.T // G, cfg.d, cfg.N_h, cfg.d_h, cfg.N_e, cfg.k, cfg.d_e, cfg.dtype, world_size=G,
-                    loopback=loop, simt=simt, pair=pair, routing_tokens=cfg.routing_tokens)
+                    loopback=loop, simt=simt, pair=pair, routing_tokens=cfg.routing_tokens, bwd_fused=bwd_fused)
     Wd = weights_to_device(W, cfg.dtype)
     xd = torch.from_numpy(x).to("cuda", td)
     out, idx, gates = L.forward(xd, Wd, want_routing=True)
@@ -113,6 +113,26 @@ def test_expert_tcgen05_matches_oracle_and_simt(d_h, d_e):
     assert {"expert_fwd_simt", "expert_bwd_simt", "router_simt"} <= s["paths"]
     np.testing.assert_array_equal(g["idx"], s["idx"])
     assert rel_err(g["out"], s["out"]) < 1e-2
+
+
+@pytest.mark.parametrize("d_h,d_e,k", [(256, 128, 8), (256, 64, 16), (128, 128, 4), (128, 64, 2)])
+def test_fused_expert_bwd_matches_oracle_and_split(d_h, d_e, k):
+    """B5's input side as ONE kernel (expert_bwd_fused_sm100.cu, MHL_FLAG_BWD_FUSED) vs the oracle,
+    and vs the default K1 + K2 pair on the same inputs: dH, gA and dg are the same arithmetic in
+    both, so dW1 / dW2 / dW_r agree bit for bit; dx differs only in where the router term is added
+    (B6 after the k-row sum instead of K2 per replica row, both fp32) — a few bf16 roundings.
+    Ragged T: the last tile of each expert is partial."""
+    _need_gpu()
+    cfg = LayerConfig("fb", T=1300, d=2 * d_h, N_h=2, d_h=d_h, N_e=64, k=k, d_e=d_e, dtype="bf16")
+    W, x, dout = make_problem(cfg, 21, "exact")
+    g = _run_gpu(cfg, W, x, dout, bwd_fused=True)
+    _compare(cfg, W, x, dout, g, dist="exact", expect={"expert_bwd_tc", "expert_bwd_fused", "router_bwd_tc"})
+    s = _run_gpu(cfg, W, x, dout)
+    assert "expert_bwd_fused" not in s["paths"] and "expert_bwd_tc" in s["paths"]
+    np.testing.assert_array_equal(g["idx"], s["idx"])
+    for key in ("out", "dW1", "dW2", "dW_r"):
+        np.testing.assert_array_equal(g[key], s[key], err_msg=key)
+    assert rel_err(g["dx"], s["dx"]) < 1e-2
 
 
 @pytest.mark.parametrize("d_h,N_e,k", [(256, 64, 8), (128, 32, 4), (128, 128, 8), (128, 256, 16)])
