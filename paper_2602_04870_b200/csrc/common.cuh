@@ -107,41 +107,63 @@ __device__ __forceinline__ float unord32(uint32_t o) {
   return __uint_as_float((o & 0x80000000u) ? (o & 0x7FFFFFFFu) : ~o);
 }
 
-// Sorting networks on packed u64 keys held in registers (fully unrolled, N a power of two):
-// bitonic sort into descending order, and the top-N merge of two descending lists (a <- top N of
-// a and b): c_i = max(a_i, b_{N-1-i}) is bitonic, one bitonic merge sorts it.
+// Sorting networks on packed u64 keys held in registers (fully unrolled, N a power of two): block
+// sort into descending order, and the top-N merge of two descending lists (a <- top N of a and b):
+// c_i = max(a_i, b_{N-1-i}) is bitonic, one bitonic merge sorts it.  A compare-exchange is one
+// 64-bit compare (2 ISETP) and four selects on ONE predicate: the plain C++ form (x > y ? x : y,
+// x > y ? y : x) compiled to separate GT and LT compares, 8 instructions per exchange, and it is
+// the router's ALU-bound inner loop (ncu: ALU pipe 76 %).  Keys of one token are distinct (the
+// index is in the low word), so every network gives the same sorted list.
+__device__ __forceinline__ void ce_desc(unsigned long long& a, unsigned long long& b) {   // a <- max, b <- min
+  asm("{\n\t.reg .pred p;\n\t.reg .b64 t;\n\t"
+      "setp.gt.u64 p, %0, %1;\n\t"
+      "selp.b64 t, %0, %1, p;\n\t"
+      "selp.b64 %1, %1, %0, p;\n\t"
+      "mov.b64 %0, t;\n\t}"
+      : "+l"(a), "+l"(b));
+}
+__device__ __forceinline__ unsigned long long max_u64(unsigned long long a, unsigned long long b) {
+  unsigned long long r;
+  asm("{\n\t.reg .pred p;\n\tsetp.gt.u64 p, %1, %2;\n\tselp.b64 %0, %1, %2, p;\n\t}" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
 template <int N>
 __device__ __forceinline__ void bitonic_sort_desc(unsigned long long (&a)[N]) {
+  if constexpr (N == 8) {
+    // Batcher's odd-even merge sort: 19 exchanges (bitonic: 24), checked on all 2^8 0/1 inputs
+    constexpr int net[19][2] = {{0, 1}, {2, 3}, {4, 5}, {6, 7}, {0, 2}, {1, 3}, {4, 6}, {5, 7}, {1, 2}, {5, 6},
+                                {0, 4}, {1, 5}, {2, 6}, {3, 7}, {2, 4}, {3, 5}, {1, 2}, {3, 4}, {5, 6}};
 #pragma unroll
-  for (int k = 2; k <= N; k <<= 1)
+    for (int c = 0; c < 19; ++c) ce_desc(a[net[c][0]], a[net[c][1]]);
+  } else if constexpr (N == 4) {
+    constexpr int net[5][2] = {{0, 1}, {2, 3}, {0, 2}, {1, 3}, {1, 2}};
 #pragma unroll
-    for (int j = k >> 1; j > 0; j >>= 1)
+    for (int c = 0; c < 5; ++c) ce_desc(a[net[c][0]], a[net[c][1]]);
+  } else {
 #pragma unroll
-      for (int i = 0; i < N; ++i) {
-        const int l = i ^ j;
-        if (l > i) {
-          const unsigned long long x = a[i], y = a[l];
-          const bool desc = (i & k) == 0;
-          const unsigned long long hi = x > y ? x : y, lo = x > y ? y : x;
-          a[i] = desc ? hi : lo;
-          a[l] = desc ? lo : hi;
+    for (int k = 2; k <= N; k <<= 1)
+#pragma unroll
+      for (int j = k >> 1; j > 0; j >>= 1)
+#pragma unroll
+        for (int i = 0; i < N; ++i) {
+          const int l = i ^ j;
+          if (l > i) {
+            if ((i & k) == 0) ce_desc(a[i], a[l]);
+            else ce_desc(a[l], a[i]);
+          }
         }
-      }
+  }
 }
 template <int N>
 __device__ __forceinline__ void merge_top_desc(unsigned long long (&a)[N], const unsigned long long (&b)[N]) {
 #pragma unroll
-  for (int i = 0; i < N; ++i) a[i] = a[i] > b[N - 1 - i] ? a[i] : b[N - 1 - i];
+  for (int i = 0; i < N; ++i) a[i] = max_u64(a[i], b[N - 1 - i]);
 #pragma unroll
   for (int j = N >> 1; j > 0; j >>= 1)
 #pragma unroll
     for (int i = 0; i < N; ++i) {
       const int l = i ^ j;
-      if (l > i) {
-        const unsigned long long x = a[i], y = a[l];
-        a[i] = x > y ? x : y;
-        a[l] = x > y ? y : x;
-      }
+      if (l > i) ce_desc(a[i], a[l]);
     }
 }
 
