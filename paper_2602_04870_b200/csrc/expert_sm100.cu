@@ -10,14 +10,15 @@
 //   epi 1  A = bf16(g * gelu(H)) -> TMEM          (exact-erf GELU, R1; A never touches smem)
 //   GEMM2  Y[128 x d_h] = A W2_e                 A read from TMEM; B = W2_e read MN-major
 //   epi 2  Yrep rows = bf16(Y)                   TMEM -> registers -> smem -> TMA bulk store
-// Warp roles (672 threads): warps 0-7 = producers (TMA gather4 of the sub-tokens through an smem
+// Warp roles (960 threads): warps 0-7 = producers (TMA gather4 of the sub-tokens through an smem
 // ring, W1/W2 by TMA when the expert changes, each as soon as the previous expert's last GEMM
-// reading it has completed), warps 8-15 = GELU epilogue (H -> A), warps 16-19 = Y epilogue (Y ->
-// Yrep, one warp per TMEM lane quadrant), warp 20 = MMA issuer (+ TMEM owner).  TMEM: H [0,128),
-// A double buffer [128,256), Y [256,512).  The two epilogue groups run concurrently: the GELU of
-// tile i overlaps the Y read-out of tile i-1 and the MMAs of tiles i+1 / i-1 (with one group doing
-// both, GELU + read-out set the tile period: 6.6 k cycles, ncu r2c).  Persistent CTAs take groups
-// of kTileGroup consecutive tiles round-robin (weights reused within a group; the tiles in flight
+// reading it has completed), warps 8-23 = GELU epilogue (H -> A), warps 24-27 = Y epilogue (Y ->
+// Yrep, one warp per TMEM lane quadrant), warp 28 = G1 issuer (+ TMEM owner), warp 29 = G2 issuer.
+// TMEM: H [0,128), A double buffer [128,256), Y [256,512) in two 128-column halves.  The epilogue
+// groups and the two issuers run concurrently: the GELU of tile i overlaps the Y read-out of tile
+// i-1, G2 of tile i's first Y half overlaps the read-out of tile i-1's second half, and G1 never
+// waits behind G2's barriers (nor G2 behind G1's gathers).  Persistent CTAs take groups of
+// kTileGroup consecutive tiles round-robin (weights reused within a group; the tiles in flight
 // stay inside one head, whose sub-tokens then stay L2-resident for their k gathers).
 #include <cuda.h>
 
@@ -43,10 +44,11 @@ constexpr int kOwners = kProdWarps / 2;
 constexpr int kGeluWarp0 = 8;         // warps 8-23: GELU epilogue (4 per lane quadrant, column quarters)
 constexpr int kGeluWarps = 16;
 constexpr int kYWarp0 = 24;           // warps 24-27: Y epilogue (one per lane quadrant)
-constexpr int kMmaWarp = 28;          // warp 28: MMA issuer + TMEM owner
-constexpr int kThreads = 29 * 32;
+constexpr int kMmaWarp = 28;          // warp 28: G1 issuer + TMEM owner
+constexpr int kMma2Warp = 29;         // warp 29: G2 issuer
+constexpr int kThreads = 30 * 32;
 // Registers: setmaxnreg.inc draws only on registers the CTA's own warps released with
-// setmaxnreg.dec (an increase nothing covers blocks forever).  With 29 warps ptxas launches at 64
+// setmaxnreg.dec (an increase nothing covers blocks forever).  With 30 warps ptxas launches at 64
 // registers (sub-partition 0 holds eight of them in its 16384-register file); the 8 producer
 // warps' release (8*32*24) covers the 16 GELU warps' raise to 72.  Four GELU warps per
 // sub-partition (instead of two with twice the columns) hide the MUFU / FMA latency of the
@@ -58,22 +60,31 @@ static_assert(8 * 32 * kLaunchRegs <= 16384, "expert fwd: launch register count 
 constexpr int kGeluThreads = kGeluWarps * 32, kYThreads = 128;
 constexpr int kXChunk = BM * 128;    // one 64-column K-chunk of the gathered X tile (16 KB)
 constexpr int kYStage = BM * 128;    // one 64-column block of the Y tile (16 KB)
+// Y staging stages: each Y warp's 4 KB slot is reused once its slab store issued kYStages blocks
+// earlier has read it; one stage leaves room for a 5th X ring stage
+#ifndef MHL_F5_YSTAGES
+#define MHL_F5_YSTAGES 1
+#endif
+constexpr int kYStages = MHL_F5_YSTAGES;
 
 template <int DH, int DE>
 struct FwdL {
   static constexpr int WB = DE * DH * 2;
-  static constexpr int W1 = 0, W2 = WB, YS = 2 * WB, X = YS + 2 * kYStage;
+  static constexpr int W1 = 0, W2 = WB, YS = 2 * WB, X = YS + kYStages * kYStage;
   static constexpr int XS_RAW = (224 * 1024 - X) / kXChunk;
   // chunk c -> stage c % XS, pair c % kOwners; XS >= kOwners keeps the EMPTY parity exact (a
   // pair's previous chunk waited for the in-order consumption of chunk c - kOwners - XS >= c - 2 XS)
-  static constexpr int XS = XS_RAW > 4 ? 4 : XS_RAW;   // X ring stages (deeper rings measured slower)
+  static constexpr int XS = XS_RAW > 6 ? 6 : XS_RAW;   // X ring stages
   static_assert(XS >= kOwners, "X ring too small");
   static constexpr int CTRL = X + XS * kXChunk;
   static constexpr int B_XFULL = CTRL, B_XEMPTY = B_XFULL + 8 * XS;
   static constexpr int B_W1F = B_XEMPTY + 8 * XS, B_W1E = B_W1F + 8, B_W2F = B_W1E + 8, B_W2E = B_W2F + 8;
   static constexpr int B_HFULL = B_W2E + 8, B_HFREE = B_HFULL + 8, B_AFULL = B_HFREE + 8, B_G2DONE = B_AFULL + 16;
-  static constexpr int B_YEMPTY = B_G2DONE + 16;
-  static constexpr int TMEMP = B_YEMPTY + 8;
+  // Y in column halves (DH % 128 == 0): G2 of tile j+1's first half overwrites Y half 0 while the
+  // Y warps still read half 1 of tile j, so the read-out (TMEM-read bound) overlaps the next G2
+  static constexpr int YH = DH % 128 == 0 ? 2 : 1, YHC = DH / YH;
+  static constexpr int B_YFULL = B_G2DONE + 16, B_YEMPTY = B_YFULL + 16;
+  static constexpr int TMEMP = B_YEMPTY + 16;
   static constexpr int BYTES = TMEMP + 16;
   static_assert(BYTES <= 227 * 1024, "expert fwd: shared memory over the per-CTA limit");
   // TMEM columns: H [0, DE), A (bf16 pairs, DE/2 columns) x NA buffers, Y [T_Y, T_Y + DH).  At
@@ -107,7 +118,7 @@ template <int DH, int DE>
 __global__ void __launch_bounds__(kThreads, 1)
 expert_fwd_sm100_kernel(const __grid_constant__ CUtensorMap w1map, const __grid_constant__ CUtensorMap w2map,
                         const __grid_constant__ CUtensorMap ymap, const __grid_constant__ CUtensorMap xmap,
-                        Routing rt) {
+                        Routing rt, int xdbg) {
   using L = FwdL<DH, DE>;
   constexpr int XS = L::XS, KB1 = DH / 64;
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -127,7 +138,7 @@ expert_fwd_sm100_kernel(const __grid_constant__ CUtensorMap w1map, const __grid_
     mbar_init(bar(L::B_HFULL), 1);
     mbar_init(bar(L::B_HFREE), kGeluThreads);
     for (int b = 0; b < 2; ++b) { mbar_init(bar(L::B_AFULL + 8 * b), kGeluThreads); mbar_init(bar(L::B_G2DONE + 8 * b), 1); }
-    mbar_init(bar(L::B_YEMPTY), kYThreads);
+    for (int h = 0; h < 2; ++h) { mbar_init(bar(L::B_YFULL + 8 * h), 1); mbar_init(bar(L::B_YEMPTY + 8 * h), kYThreads); }
     fence_mbar_init();
     tma_prefetch_desc(&w1map); tma_prefetch_desc(&w2map); tma_prefetch_desc(&ymap); tma_prefetch_desc(&xmap);
   }
@@ -205,12 +216,22 @@ expert_fwd_sm100_kernel(const __grid_constant__ CUtensorMap w1map, const __grid_
         uint64_t* full = bar(L::B_XFULL + 8 * xs);
         if (lane == 0) {
           mbar_wait(bar(L::B_XEMPTY + 8 * xs), ((cnt / XS) & 1) ^ 1);
-          if ((pw & 1) == 0) mbar_expect_tx(full, kXChunk);
+          if ((pw & 1) == 0) {
+            if (xdbg & 2) mbar_arrive(full);   // A/B only: no gathers (garbage X)
+            else mbar_expect_tx(full, kXChunk);
+          }
         }
         __syncwarp();
-        if (lane < 16)
-          tma_gather4(sb + L::X + xs * kXChunk + lrow * 128, &xmap, (int)tl.head * DH + kb * 64, r0, r1, r2, r3,
-                      full);
+        if (lane < 16 && !(xdbg & 2)) {
+          if (xdbg & 1) {   // A/B only: the same gather4 stream over consecutive rows
+            const int c0 = (int)((tl.row0 + lrow) % rt.T);
+            tma_gather4(sb + L::X + xs * kXChunk + lrow * 128, &xmap, (int)tl.head * DH + kb * 64, c0,
+                        (c0 + 1) % (int)rt.T, (c0 + 2) % (int)rt.T, (c0 + 3) % (int)rt.T, full);
+          } else {
+            tma_gather4(sb + L::X + xs * kXChunk + lrow * 128, &xmap, (int)tl.head * DH + kb * 64, r0, r1, r2, r3,
+                        full);
+          }
+        }
       }
       // W2 of the previous tile if it started a new expert run (read by G2(i-1), issued after G1(i))
       if (pw == 0 && lane == 0 && i >= 1 && !same_expert(tile_at(i - 2), tile_at(i - 1))) {
@@ -219,30 +240,16 @@ expert_fwd_sm100_kernel(const __grid_constant__ CUtensorMap w1map, const __grid_
       }
     }
   } else if (warp == kMmaWarp) {
-    // ================================================================ MMA issuer
+    // ================================================================ G1 issuer
+    // Two issuing threads: G1 (this warp) waits for gathered chunks, G2 (warp kMma2Warp) for the
+    // GELU's A and the Y read-out; in one thread each waited behind the other's barriers (a G2
+    // behind the next tile's gathers, a G1 behind the Y read-out).  They touch disjoint TMEM
+    // columns and smem operands; every cross dependency goes through an mbarrier.
     if (lane == 0) {
       constexpr uint32_t ID1 = idesc_bf16(BM, DE, 0, 0);
-      constexpr uint32_t ID2 = idesc_bf16(BM, DH, 0, 1);
-      Ph xf[12], w1f, w2f, hfr, af[2], ye;
+      Ph xf[12], w1f, hfr;
       int xs = 0;
-      auto gemm2 = [&](int j) {
-        const int b = j % L::NA;
-        const int tj = tile_at(j);
-        if (!same_expert(tile_at(j - 1), tj)) mbar_wait(bar(L::B_W2F), w2f.flip());
-        mbar_wait(bar(L::B_AFULL + 8 * b), af[b].flip());   // (NA = 1: b = 0 throughout)
-        mbar_wait(bar(L::B_YEMPTY), ye.flip() ^ 1);
-        trace_ev(g_trace_fwd, 13, j);
-        tc_fence_after();
-#pragma unroll
-        for (int ks = 0; ks < DE / 16; ++ks)
-          mma_bf16_ts(tmem + L::T_Y, tmem + L::T_A + b * (DE / 2) + ks * 8,
-                      sdesc_sw128(sb + L::W2 + ks * 2 * 1024, DE * 128, 1024), ID2, ks > 0);
-        mma_commit(bar(L::B_G2DONE + 8 * b));
-        trace_ev(g_trace_fwd, 14, j);
-        if (!same_expert(tj, tile_at(j + 1))) mma_commit(bar(L::B_W2E));
-      };
-      int i = 0;
-      for (;; ++i) {
+      for (int i = 0;; ++i) {
         const int ti = tile_at(i);
         if (ti < 0) break;
         if (!same_expert(tile_at(i - 1), ti)) mbar_wait(bar(L::B_W1F), w1f.flip());
@@ -262,9 +269,36 @@ expert_fwd_sm100_kernel(const __grid_constant__ CUtensorMap w1map, const __grid_
         }
         mma_commit(bar(L::B_HFULL));
         if (!same_expert(ti, tile_at(i + 1))) mma_commit(bar(L::B_W1E));
-        if (i >= 1) gemm2(i - 1);
       }
-      if (i >= 1) gemm2(i - 1);
+    }
+  } else if (warp == kMma2Warp) {
+    // ================================================================ G2 issuer
+    if (lane == 0) {
+      constexpr uint32_t ID2 = idesc_bf16(BM, L::YHC, 0, 1);
+      Ph w2f, af[2], ye[2];
+      for (int j = 0;; ++j) {
+        const int tj = tile_at(j);
+        if (tj < 0) break;
+        const int b = j % L::NA;
+        if (!same_expert(tile_at(j - 1), tj)) mbar_wait(bar(L::B_W2F), w2f.flip());
+        mbar_wait(bar(L::B_AFULL + 8 * b), af[b].flip());   // (NA = 1: b = 0 throughout)
+#pragma unroll
+        for (int hh = 0; hh < L::YH; ++hh) {
+          mbar_wait(bar(L::B_YEMPTY + 8 * hh), ye[hh].flip() ^ 1);   // the Y warps read this half of Y(j-1)
+          if (hh == 0) trace_ev(g_trace_fwd, 13, j);
+          tc_fence_after();
+          // B = W2_e's columns [hh*YHC, (hh+1)*YHC): MN-major 64-column atoms at DE*128 bytes
+#pragma unroll
+          for (int ks = 0; ks < DE / 16; ++ks)
+            mma_bf16_ts(tmem + L::T_Y + hh * L::YHC, tmem + L::T_A + b * (DE / 2) + ks * 8,
+                        sdesc_sw128(sb + L::W2 + hh * (L::YHC / 64) * DE * 128 + ks * 2 * 1024, DE * 128, 1024), ID2,
+                        ks > 0);
+          mma_commit(bar(L::B_YFULL + 8 * hh));
+        }
+        mma_commit(bar(L::B_G2DONE + 8 * b));
+        trace_ev(g_trace_fwd, 14, j);
+        if (!same_expert(tj, tile_at(j + 1))) mma_commit(bar(L::B_W2E));
+      }
     }
   } else if (warp >= kGeluWarp0 && warp < kYWarp0) {
     asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kGeluRegs));
@@ -353,19 +387,21 @@ expert_fwd_sm100_kernel(const __grid_constant__ CUtensorMap w1map, const __grid_
     // stage (64-column blocks, two stages) -> TMA bulk store of the 32-row slab.
     const int q = warp & 3;
     const uint32_t lane_off = (uint32_t)(q * 32) << 16;
-    Ph gd[2];
+    Ph yf[2];
     int ys = 0;   // running count of Y blocks stored by this warp (selects the smem stage)
     for (int j = 0;; ++j) {
       const int tj = tile_at(j);
       if (tj < 0) break;
-      const int b = j % L::NA;
       const Tile tl = tiles[tj];
-      mbar_wait_warp(bar(L::B_G2DONE + 8 * b), gd[b].flip());
-      if (q == 0 && lane == 0) trace_ev(g_trace_fwd, 23, j);
-      tc_fence_after();
 #pragma unroll 1
       for (int cb = 0; cb < DH / 64; ++cb, ++ys) {
-        const int st = ys & 1;
+        const int hh = cb / (L::YHC / 64);
+        if (cb % (L::YHC / 64) == 0) {          // first block of a Y half: wait for its G2
+          mbar_wait_warp(bar(L::B_YFULL + 8 * hh), yf[hh].flip());
+          if (q == 0 && lane == 0 && hh == 0) trace_ev(g_trace_fwd, 23, j);
+          tc_fence_after();
+        }
+        const int st = ys % kYStages;
         uint32_t v[32], w[32];
         tmem_ld32(tmem + L::T_Y + lane_off + cb * 64, v);
         tmem_ld_wait();
@@ -373,15 +409,15 @@ expert_fwd_sm100_kernel(const __grid_constant__ CUtensorMap w1map, const __grid_
         for (int u = 0; u < 16; ++u) w[u] = pack_bf16x2(__uint_as_float(v[2 * u]), __uint_as_float(v[2 * u + 1]));
         tmem_ld32(tmem + L::T_Y + lane_off + cb * 64 + 32, v);
         tmem_ld_wait();
-        if (cb == DH / 64 - 1) {
+        if (cb % (L::YHC / 64) == L::YHC / 64 - 1) {   // last block of the half read: release it
           tc_fence_before();
-          mbar_arrive(bar(L::B_YEMPTY));
-          if (q == 0 && lane == 0) trace_ev(g_trace_fwd, 24, j);
+          mbar_arrive(bar(L::B_YEMPTY + 8 * hh));
+          if (q == 0 && lane == 0 && hh == L::YH - 1) trace_ev(g_trace_fwd, 24, j);
         }
 #pragma unroll
         for (int u = 0; u < 16; ++u) w[16 + u] = pack_bf16x2(__uint_as_float(v[2 * u]), __uint_as_float(v[2 * u + 1]));
         // the slab store issued from this stage two blocks ago must have read it
-        if (lane == 0) bulk_wait_read<1>();
+        if (lane == 0) bulk_wait_read<kYStages - 1>();
         __syncwarp();
         uint8_t* sp = smem + L::YS + st * kYStage + q * 4096;
 #pragma unroll
@@ -423,7 +459,8 @@ bool launch_t(const Routing& rt, const void* Xs, int64_t ldx, const void* W1, co
     TraceBuf tb{tbuf, 0};
     cudaMemcpyToSymbolAsync(g_trace_fwd, &tb, sizeof(tb), 0, cudaMemcpyHostToDevice, s);
   }
-  kern<<<num_sms, kThreads, FwdL<DH, DE>::BYTES, s>>>(w1m, w2m, ym, xm, rt);
+  static const int xdbg = getenv("MHL_F5_XDBG") ? atoi(getenv("MHL_F5_XDBG")) : 0;   // A/B only (wrong results)
+  kern<<<num_sms, kThreads, FwdL<DH, DE>::BYTES, s>>>(w1m, w2m, ym, xm, rt, xdbg);
   if (trace_path) {
     TraceBuf tb{nullptr, 0};
     cudaMemcpyToSymbolAsync(g_trace_fwd, &tb, sizeof(tb), 0, cudaMemcpyHostToDevice, s);
