@@ -135,6 +135,22 @@ def test_fused_expert_bwd_matches_oracle_and_split(d_h, d_e, k):
     assert rel_err(g["dx"], s["dx"]) < 1e-2
 
 
+@pytest.mark.parametrize("G", [2, 4])
+def test_fused_expert_bwd_hp_bitwise_equals_single_rank(G):
+    """The opt-in fused backward under HP (loopback): bit-identical to its own G = 1 run on the paper
+    head shape (the router term added by B6 per destination block, the fused kernel per rank)."""
+    _need_gpu()
+    cfg = LayerConfig("fb_hp", T=2048, d=512, N_h=8, d_h=256, N_e=64, k=8, d_e=128, dtype="bf16")
+    W, x, dout = make_problem(cfg, 50 + G, "conf")
+    g1 = _run_gpu(cfg, W, x, dout, G=1, bwd_fused=True)
+    gG = _run_gpu(cfg, W, x, dout, G=G, bwd_fused=True)
+    assert "expert_bwd_fused" in g1["paths"] and "expert_bwd_fused" in gG["paths"]
+    for key in ("out", "dx", "idx", "gates", "dW_r", "dW1", "dW2"):
+        np.testing.assert_array_equal(gG[key], g1[key], err_msg=key)
+    for key in ("dW_in", "dW_out"):     # rank-partial sums, summed in rank order (R19)
+        assert rel_err(gG[key], g1[key]) < 1e-5
+
+
 @pytest.mark.parametrize("d_h,N_e,k", [(256, 64, 8), (128, 32, 4), (128, 128, 8), (128, 256, 16)])
 def test_router_bwd_tcgen05_matches_oracle_and_simt(d_h, N_e, k):
     """B3 on the tensor cores (dW_r = X^T dS_dense, dS as hi+lo bf16 planes, P:846-P:866) vs the
