@@ -14,3 +14,11 @@ for tool in memcheck racecheck synccheck; do
   timeout 900 compute-sanitizer --tool $tool --error-exitcode 9 python -c "import __graft_entry__ as g; g.smoke()" > $OUT/${TAG}_${tool}_smoke.log 2>&1
   echo "$tool rc=$? $(grep -E 'ERROR SUMMARY|RACECHECK SUMMARY' $OUT/${TAG}_${tool}_smoke.log | tail -1)"
 done
+# the opt-in fused backward (MHL_FLAG_BWD_FUSED): a bench line, one --set full capture of its kernel,
+# and memcheck / racecheck of smoke() on that path
+MHL_BWD_FUSED=1 timeout 300 python bench.py --steps 20 --warmup 5 --no-cpu-baseline > $OUT/${TAG}_bench_paper_fused.json 2> $OUT/${TAG}_bench_paper_fused.err; echo "paper fused rc=$?"
+MHL_BWD_FUSED=1 KREGEX=expert_bwd_fused bash tools/ncu_one.sh ${TAG}_prof_fused > /dev/null 2>&1; echo "ncu fused rc=$?"
+for tool in memcheck racecheck; do
+  MHL_BWD_FUSED=1 timeout 900 compute-sanitizer --tool $tool --error-exitcode 9 python -c "import __graft_entry__ as g; g.smoke()" > $OUT/${TAG}_${tool}_smoke_fused.log 2>&1
+  echo "fused $tool rc=$? $(grep -E 'ERROR SUMMARY|RACECHECK SUMMARY' $OUT/${TAG}_${tool}_smoke_fused.log | tail -1)"
+done
