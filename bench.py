@@ -505,7 +505,9 @@ def main():
         calls = steps_t[dom][1] / args.steps
         dur_s = per_step[dom] / 1e3
         w = work.get(dom, {})
-        tr = traffic.get(dom, {}).get("dram_bytes_per_launch") if cfg.name == traffic.get("_workload") else None
+        fused_bwd = "B5_expert_bwd_dx" in per_step and "B5_expert_dx_gemm" not in per_step
+        tkey = dom + "@fused" if fused_bwd and dom == "B5_expert_bwd_dx" else dom
+        tr = traffic.get(tkey, {}).get("dram_bytes_per_launch") if cfg.name == traffic.get("_workload") else None
         bound, achieved, peak, unit, frac = span_roofline(w, dur_s, tf_peak, hbm_peak)
         roof = {"bound": bound, "achieved": achieved, "peak": peak, "unit": unit, "frac": frac, "traffic": tr,
                 "traffic_over_algorithmic": (tr / (w["bytes"] / max(calls, 1))) if tr else None,

@@ -73,6 +73,9 @@ def report(path, flops=None, nbytes=None):
 
 
 SPAN_OF = {"expert_bwd_h": "B5_expert_bwd_dx", "expert_dw_kernel": "B5_expert_bwd_dw",
+           # the opt-in fused backward (MHL_FLAG_BWD_FUSED) runs under the same span name; its traffic
+           # is keyed separately and bench.py picks it when the dX GEMM span is absent
+           "expert_bwd_fused": "B5_expert_bwd_dx@fused",
            "expert_fwd_sm100": "F5_expert_fwd", "expert_dx_gemm": "B5_expert_dx_gemm",
            "router_sm100": "F3_router_topk", "router_bwd_sm100": "B3_router_bwd", "scatter_kernel": "F4_cluster",
            # the same combine kernel serves F6 and then B6 within one step (capture order)
