@@ -143,6 +143,7 @@ expert_fwd_sm100_kernel(const __grid_constant__ CUtensorMap w1map, const __grid_
     tma_prefetch_desc(&w1map); tma_prefetch_desc(&w2map); tma_prefetch_desc(&ymap); tma_prefetch_desc(&xmap);
   }
   if (warp == kMmaWarp) tmem_alloc<512>(s_tmem);
+  if (tid == 0) { TraceBuf tb = g_trace_fwd; trace_cta(tb, 60); }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -436,6 +437,7 @@ expert_fwd_sm100_kernel(const __grid_constant__ CUtensorMap w1map, const __grid_
   }
   tc_fence_before();
   __syncthreads();
+  if (tid == 0) { TraceBuf tb = g_trace_fwd; trace_cta(tb, 61); }
   if (warp == kMmaWarp) tmem_dealloc<512>(tmem);
 }
 
@@ -452,7 +454,7 @@ bool launch_t(const Routing& rt, const void* Xs, int64_t ldx, const void* W1, co
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, FwdL<DH, DE>::BYTES);
   static const char* trace_path = getenv("MHL_TRACE_FWD");
   static unsigned long long* tbuf = nullptr;
-  const size_t nslot = 32 * 4096;
+  const size_t nslot = 64 * 4096;   // events < 64 (60 / 61: per-CTA start / end)
   if (trace_path) {
     if (!tbuf) cudaMalloc(&tbuf, nslot * sizeof(unsigned long long));
     cudaMemsetAsync(tbuf, 0, nslot * sizeof(unsigned long long), s);
