@@ -39,27 +39,44 @@ __device__ TraceBuf g_trace_fwd;     // profiling aid (MHL_TRACE_FWD=<file>), of
 
 constexpr int BM = kExpertBM;        // 128 rows = MMA M
 // Warp roles, warpgroup-aligned so the producers can hand registers to the GELU epilogue (setmaxnreg):
-constexpr int kProdWarps = 8;         // warps 0-7: producers, in 4 pairs (a pair fills one X chunk)
-constexpr int kOwners = kProdWarps / 2;
-constexpr int kGeluWarp0 = 8;         // warps 8-23: GELU epilogue (4 per lane quadrant, column quarters)
+// MHL_F5_PROD_WARPS = 8 (default): producers in pairs, four Y warps; 4: four producer warps own
+// whole X chunks and eight Y warps (two per lane quadrant, one per Y column half) read Y out.  The
+// Y read-out is per-warp bound (one warp per quadrant moves ~50 B/clk of TMEM; the 16 GELU warps
+// read H at ~190 B/clk), and two Y warps per quadrant do shorten it (3.7 k -> 2.5 k cycles per
+// tile), but with four producer warps G1 waits 5.8 k instead of 3.9 k cycles for its gathers:
+// F5 0.85-0.86 vs 0.77-0.78 ms (tools/ab_f5prod.sh).
+#ifndef MHL_F5_PROD_WARPS
+#define MHL_F5_PROD_WARPS 8
+#endif
+constexpr int kProdWarps = MHL_F5_PROD_WARPS;   // warps [0, kProdWarps): producers
+constexpr int kOwners = 4;                      // chunk owners: whole warps (4) or warp pairs (8)
+constexpr int kWpc = kProdWarps / kOwners;      // producer warps per chunk
+constexpr int kGeluWarp0 = kProdWarps;          // 16 GELU warps (4 per lane quadrant, column quarters)
 constexpr int kGeluWarps = 16;
-constexpr int kYWarp0 = 24;           // warps 24-27: Y epilogue (one per lane quadrant)
-constexpr int kMmaWarp = 28;          // warp 28: G1 issuer + TMEM owner
-constexpr int kMma2Warp = 29;         // warp 29: G2 issuer
-constexpr int kThreads = 30 * 32;
+constexpr int kYWarp0 = kGeluWarp0 + kGeluWarps;
+constexpr int kYWarps = kProdWarps == 4 ? 8 : 4;   // Y epilogue: 1 or 2 per lane quadrant
+constexpr int kYGroups = kYWarps / 4;
+constexpr int kMmaWarp = kYWarp0 + kYWarps;     // G1 issuer + TMEM owner
+constexpr int kMma2Warp = kMmaWarp + 1;         // G2 issuer
+constexpr int kThreads = (kMma2Warp + 1) * 32;
+static_assert(kThreads == 30 * 32 && (kProdWarps == 4 || kProdWarps == 8), "expert fwd: warp roles");
 // Registers: setmaxnreg.inc draws only on registers the CTA's own warps released with
 // setmaxnreg.dec (an increase nothing covers blocks forever).  With 30 warps ptxas launches at 64
-// registers (sub-partition 0 holds eight of them in its 16384-register file); the 8 producer
-// warps' release (8*32*24) covers the 16 GELU warps' raise to 72.  Four GELU warps per
-// sub-partition (instead of two with twice the columns) hide the MUFU / FMA latency of the
-// GELU chain (3.7 k cycles per tile with two, trace r2e).
-constexpr int kLaunchRegs = 64, kProdRegs = 40, kGeluRegs = 72;
-static_assert(8 * (kLaunchRegs - kProdRegs) >= kGeluWarps * (kGeluRegs - kLaunchRegs),
-              "expert fwd: the GELU warps' register increase exceeds the producers' release");
+// registers (sub-partitions 0 and 1 hold eight of them in their 16384-register files); the
+// producers' release (and with eight Y warps theirs, to 56) covers the 16 GELU warps' raise to 72,
+// pool-wide and on every sub-partition.  Four GELU warps per sub-partition (instead of two with
+// twice the columns) hide the MUFU / FMA latency of the GELU chain (3.7 k cycles per tile with
+// two, trace r2e).
+constexpr int kLaunchRegs = 64, kProdRegs = 40, kGeluRegs = 72, kYRegs = kYWarps == 8 ? 56 : 64;
+static_assert(kProdWarps * (kLaunchRegs - kProdRegs) + kYWarps * (kLaunchRegs - kYRegs) >=
+                  kGeluWarps * (kGeluRegs - kLaunchRegs),
+              "expert fwd: the GELU warps' register increase exceeds the release");
+static_assert(kProdWarps / 4 * kProdRegs + 4 * kGeluRegs + kYGroups * kYRegs + kLaunchRegs <= 512,
+              "expert fwd: sub-partition 0 register file");
 static_assert(8 * 32 * kLaunchRegs <= 16384, "expert fwd: launch register count does not fit sub-partition 0");
-constexpr int kGeluThreads = kGeluWarps * 32, kYThreads = 128;
+constexpr int kGeluThreads = kGeluWarps * 32, kYThreads = kYWarps * 32;
 constexpr int kXChunk = BM * 128;    // one 64-column K-chunk of the gathered X tile (16 KB)
-constexpr int kYStage = BM * 128;    // one 64-column block of the Y tile (16 KB)
+constexpr int kYStage = kYWarps * 4096;   // one 4 KB slot (32 rows x 64 columns) per Y warp
 // Y staging stages: each Y warp's 4 KB slot is reused once its slab store issued kYStages blocks
 // earlier has read it; one stage leaves room for a 5th X ring stage
 #ifndef MHL_F5_YSTAGES
@@ -72,8 +89,8 @@ struct FwdL {
   static constexpr int WB = DE * DH * 2;
   static constexpr int W1 = 0, W2 = WB, YS = 2 * WB, X = YS + kYStages * kYStage;
   static constexpr int XS_RAW = (224 * 1024 - X) / kXChunk;
-  // chunk c -> stage c % XS, pair c % kOwners; XS >= kOwners keeps the EMPTY parity exact (a
-  // pair's previous chunk waited for the in-order consumption of chunk c - kOwners - XS >= c - 2 XS)
+  // chunk c -> stage c % XS, owner c % kOwners; XS >= kOwners keeps the EMPTY parity exact (an
+  // owner's previous chunk waited for the in-order consumption of chunk c - kOwners - XS >= c - 2 XS)
   static constexpr int XS = XS_RAW > 6 ? 6 : XS_RAW;   // X ring stages
   static_assert(XS >= kOwners, "X ring too small");
   static constexpr int CTRL = X + XS * kXChunk;
@@ -138,7 +155,12 @@ expert_fwd_sm100_kernel(const __grid_constant__ CUtensorMap w1map, const __grid_
     mbar_init(bar(L::B_HFULL), 1);
     mbar_init(bar(L::B_HFREE), kGeluThreads);
     for (int b = 0; b < 2; ++b) { mbar_init(bar(L::B_AFULL + 8 * b), kGeluThreads); mbar_init(bar(L::B_G2DONE + 8 * b), 1); }
-    for (int h = 0; h < 2; ++h) { mbar_init(bar(L::B_YFULL + 8 * h), 1); mbar_init(bar(L::B_YEMPTY + 8 * h), kYThreads); }
+    // a Y half is released by the Y warps that read it: one group per half with two groups and
+    // two halves, every Y warp otherwise
+    for (int h = 0; h < 2; ++h) {
+      mbar_init(bar(L::B_YFULL + 8 * h), 1);
+      mbar_init(bar(L::B_YEMPTY + 8 * h), (kYGroups == 2 && L::YH == 2) ? 128 : kYThreads);
+    }
     fence_mbar_init();
     tma_prefetch_desc(&w1map); tma_prefetch_desc(&w2map); tma_prefetch_desc(&ymap); tma_prefetch_desc(&xmap);
   }
@@ -168,16 +190,15 @@ expert_fwd_sm100_kernel(const __grid_constant__ CUtensorMap w1map, const __grid_
   };
 
   if (warp < kProdWarps) {
-    // ================================================================ producers (8 warps)
+    // ================================================================ producers (4 or 8 warps)
     // Chunk c of this CTA's X stream (tile c / KB1, column block c % KB1) goes to ring stage
-    // c % XS and is brought by warp pair c % kOwners (XS is a multiple of kOwners, so a stage is
-    // only ever refilled by the pair that filled it before): lanes 0-15 of each warp of the pair
-    // issue one TMA gather4 of 4 sub-token rows each (warp 2p+h owns tile rows 64h..64h+63).  More
-    // warps issuing gathers raise the SM's gather rate (tools/ring_probe.cu mech 6).  Warp 0 lane 0
-    // also issues the weight TMAs.
+    // c % XS and is brought by owner c % kOwners (a warp, or a warp pair with 8 producers): each
+    // issuing lane brings 4 sub-token rows with one TMA gather4 (warp w of an owner holds tile rows
+    // [w*128/kWpc, (w+1)*128/kWpc)).  Warp 0 lane 0 also issues the weight TMAs.
     asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kProdRegs));
     const int pw = warp;
-    const int owner = pw >> 1, lrow = (pw & 1) * 64 + 4 * (lane & 15);
+    constexpr int LPW = 32 / kWpc;   // issuing lanes per warp
+    const int owner = pw / kWpc, lrow = (pw % kWpc) * (BM / kWpc) + 4 * (lane % LPW);
     Ph w1e, w2e;
     int cnt = 0;
     int nx[4] = {0, 0, 0, 0};
@@ -217,13 +238,13 @@ expert_fwd_sm100_kernel(const __grid_constant__ CUtensorMap w1map, const __grid_
         uint64_t* full = bar(L::B_XFULL + 8 * xs);
         if (lane == 0) {
           mbar_wait(bar(L::B_XEMPTY + 8 * xs), ((cnt / XS) & 1) ^ 1);
-          if ((pw & 1) == 0) {
+          if (pw % kWpc == 0) {
             if (xdbg & 2) mbar_arrive(full);   // A/B only: no gathers (garbage X)
             else mbar_expect_tx(full, kXChunk);
           }
         }
         __syncwarp();
-        if (lane < 16 && !(xdbg & 2)) {
+        if (lane < LPW && !(xdbg & 2)) {
           if (xdbg & 1) {   // A/B only: the same gather4 stream over consecutive rows
             const int c0 = (int)((tl.row0 + lrow) % rt.T);
             tma_gather4(sb + L::X + xs * kXChunk + lrow * 128, &xmap, (int)tl.head * DH + kb * 64, c0,
@@ -383,52 +404,61 @@ expert_fwd_sm100_kernel(const __grid_constant__ CUtensorMap w1map, const __grid_
       if (et == 0) trace_ev(g_trace_fwd, 22, i);
     }
   } else if (warp >= kYWarp0 && warp < kMmaWarp) {
-    // ================================================================ Y epilogue (4 warps)
-    // tile j: Y rows of this warp's lane quadrant (32 rows x DH columns) -> bf16 -> SW128 smem
-    // stage (64-column blocks, two stages) -> TMA bulk store of the 32-row slab.
-    const int q = warp & 3;
+    if constexpr (kYRegs < kLaunchRegs) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kYRegs));
+    // ================================================================ Y epilogue (kYWarps warps)
+    // tile j: Y rows of this warp's lane quadrant (32 rows) -> bf16 -> SW128 smem slot (64-column
+    // blocks) -> TMA bulk store of the 32-row slab.  With two warps per quadrant, group g reads Y
+    // half g (or the blocks of its parity when Y is one half); each half is released to G2 by the
+    // warps that read it, after their last TMEM load of it.
+    const int q = warp & 3, yg = (warp - kYWarp0) >> 2;
     const uint32_t lane_off = (uint32_t)(q * 32) << 16;
+    constexpr int NB = DH / 64, BPH = L::YHC / 64;   // 64-column blocks: per tile, per Y half
+    auto mine = [&](int cb) { return kYGroups == 1 ? true : (L::YH == 2 ? cb / BPH == yg : cb % 2 == yg); };
     Ph yf[2];
     int ys = 0;   // running count of Y blocks stored by this warp (selects the smem stage)
+    const uint32_t slot = (uint32_t)(warp - kYWarp0) * 4096;
     for (int j = 0;; ++j) {
       const int tj = tile_at(j);
       if (tj < 0) break;
       const Tile tl = tiles[tj];
 #pragma unroll 1
-      for (int cb = 0; cb < DH / 64; ++cb, ++ys) {
-        const int hh = cb / (L::YHC / 64);
-        if (cb % (L::YHC / 64) == 0) {          // first block of a Y half: wait for its G2
+      for (int cb = 0; cb < NB; ++cb) {
+        if (!mine(cb)) continue;
+        const int hh = cb / BPH;
+        int first = hh * BPH, last = hh * BPH + BPH - 1;   // this warp's first / last block of half hh
+        while (!mine(first)) ++first;
+        while (!mine(last)) --last;
+        if (cb == first) {          // wait for this Y half's G2
           mbar_wait_warp(bar(L::B_YFULL + 8 * hh), yf[hh].flip());
           if (q == 0 && lane == 0 && hh == 0) trace_ev(g_trace_fwd, 23, j);
           tc_fence_after();
         }
         const int st = ys % kYStages;
-        uint32_t v[32], w[32];
-        tmem_ld32(tmem + L::T_Y + lane_off + cb * 64, v);
-        tmem_ld_wait();
-#pragma unroll
-        for (int u = 0; u < 16; ++u) w[u] = pack_bf16x2(__uint_as_float(v[2 * u]), __uint_as_float(v[2 * u + 1]));
-        tmem_ld32(tmem + L::T_Y + lane_off + cb * 64 + 32, v);
-        tmem_ld_wait();
-        if (cb % (L::YHC / 64) == L::YHC / 64 - 1) {   // last block of the half read: release it
-          tc_fence_before();
-          mbar_arrive(bar(L::B_YEMPTY + 8 * hh));
-          if (q == 0 && lane == 0 && hh == L::YH - 1) trace_ev(g_trace_fwd, 24, j);
-        }
-#pragma unroll
-        for (int u = 0; u < 16; ++u) w[16 + u] = pack_bf16x2(__uint_as_float(v[2 * u]), __uint_as_float(v[2 * u + 1]));
-        // the slab store issued from this stage two blocks ago must have read it
+        ++ys;
+        // the slab store issued from this stage kYStages blocks ago must have read the slot
         if (lane == 0) bulk_wait_read<kYStages - 1>();
         __syncwarp();
-        uint8_t* sp = smem + L::YS + st * kYStage + q * 4096;
+        uint8_t* sp = smem + L::YS + st * kYStage + slot;
 #pragma unroll
-        for (int u = 0; u < 32; u += 4)
-          *reinterpret_cast<uint4*>(sp + kmaj_off(lane, 2 * u, 32)) = make_uint4(w[u], w[u + 1], w[u + 2], w[u + 3]);
+        for (int hc = 0; hc < 2; ++hc) {      // two 32-column loads, each packed and staged at once
+          uint32_t v[32], w[16];
+          tmem_ld32(tmem + L::T_Y + lane_off + cb * 64 + hc * 32, v);
+          tmem_ld_wait();
+          if (hc == 1 && cb == last) {   // this warp's last read of the half: release it
+            tc_fence_before();
+            mbar_arrive(bar(L::B_YEMPTY + 8 * hh));
+            if (q == 0 && lane == 0 && hh == L::YH - 1 && yg == kYGroups - 1) trace_ev(g_trace_fwd, 24, j);
+          }
+#pragma unroll
+          for (int u = 0; u < 16; ++u) w[u] = pack_bf16x2(__uint_as_float(v[2 * u]), __uint_as_float(v[2 * u + 1]));
+#pragma unroll
+          for (int u = 0; u < 16; u += 4)
+            *reinterpret_cast<uint4*>(sp + kmaj_off(lane, hc * 32 + 2 * u, 32)) = make_uint4(w[u], w[u + 1], w[u + 2], w[u + 3]);
+        }
         fence_proxy_async();
         __syncwarp();
         if (lane == 0) {
-          tma_store_2d(&ymap, sb + L::YS + st * kYStage + q * 4096, cb * 64,
-                       (int)((size_t)tl.head * rt.Rp + tl.row0 + q * 32));
+          tma_store_2d(&ymap, sb + L::YS + st * kYStage + slot, cb * 64, (int)((size_t)tl.head * rt.Rp + tl.row0 + q * 32));
           bulk_commit();
         }
       }
