@@ -88,7 +88,7 @@ constexpr int kEpiThreads = kEpiWarps * 32;
 #define MHL_K1_STOREHINT 1   // dH / gA stores evict_first (1) or normal (0)
 #endif
 #ifndef MHL_K1_PW
-#define MHL_K1_PW 8   // producer warps of the backward H kernel (8: in chunk-sharing pairs; 4: whole chunks)
+#define MHL_K1_PW 8   // producer warps of the backward H kernel (8: pairs, 12: triples per chunk; 4: whole chunks)
 #endif
 
 template <int DH, int DE>
@@ -115,15 +115,18 @@ struct HL {
   // chunk (128/WPC rows each): more warps issuing gathers raise the SM's gather rate
   // (tools/ring_probe.cu mech 6: 5.8 -> 8.9 TB/s for L2-resident rows).  Otherwise (d_e = 256:
   // 2-3 stages) 2 warps, each filling whole chunks.
-  static constexpr bool SPLIT = S_RAW >= 4 && MHL_K1_PW == 8;
+  static constexpr bool SPLIT = S_RAW >= 4 && (MHL_K1_PW == 8 || MHL_K1_PW == 12);
   static constexpr int PW = S_RAW >= 4 ? MHL_K1_PW : 2;
-  static constexpr int WPC = SPLIT ? 2 : 1;                 // warps per chunk
+  static constexpr int WPC = SPLIT ? PW / 4 : 1;            // warps per chunk (lanes split as evenly as possible)
   static constexpr int OWNERS = PW / WPC;                   // chunk owners (warp pairs or warps)
   // warps [0, PW) producers, [PW, PW + 16) epilogue, PW + 16 the MMA issuer.  With 8 producers
   // the roles are warpgroup-aligned, so producers hand registers to the epilogue (setmaxnreg).
   static constexpr int EPI_WARP0 = PW, MMA_WARP = PW + kEpiWarps, THREADS = (PW + 1 + kEpiWarps) * 32;
-  static constexpr bool REGS = PW == 8;
-  static constexpr int PROD_REGS = 40, EPI_REGS = 88;   // launch cap 72: 8*32*(72-40) >= 16*32*(88-72)
+  static constexpr bool REGS = PW == 8 || PW == 12;
+  // launch cap 72 with 25 warps (8 producers): 8*32*(72-40) >= 16*32*(88-72); 64 with 29 warps
+  // (12 producers): 12*32*(64-40) >= 16*32*(80-64), and sub-partition 0 (3 producers, 4 epilogue
+  // warps, the MMA warp) holds 3*40 + 4*80 + 64 <= 512
+  static constexpr int PROD_REGS = 40, EPI_REGS = PW == 12 ? 80 : 88;
   // a multiple of OWNERS: chunk c -> stage c % S, owner c % OWNERS, so every stage is only ever
   // refilled by the owner that filled it before.  (S >= OWNERS alone would keep the EMPTY parity
   // exact too — the owner's previous chunk waited for the in-order consumption of chunk
@@ -205,11 +208,13 @@ expert_bwd_h_kernel(const __grid_constant__ CUtensorMap w1map, const __grid_cons
     int cnt = 0;                       // chunks of this CTA's stream so far
     const uint64_t pol_keep = (dbg & 16) ? l2_evict_normal() : l2_evict_last();   // rows reused k times per head
     // owner pw/WPC fills the chunk, this warp its rows lrow.. (lanes 0..LPW-1, 4 rows each)
-    constexpr int OWN = L::OWNERS, WPC = L::WPC, LPW = 32 / WPC;   // lanes issuing per warp
-    const int owner = pw / WPC;
-    const int lrow = (pw % WPC) * (BM / WPC) + 4 * (lane % LPW);
-    const bool issues = lane < LPW;
-    const bool tx_lead = lane == 0 && pw % WPC == 0;
+    // the 32 gather4 lanes of a chunk split over its WPC warps (11/11/10 with three)
+    constexpr int OWN = L::OWNERS, WPC = L::WPC, LB = 32 / WPC, LX = 32 % WPC;
+    const int owner = pw / WPC, wi = pw % WPC;
+    const int lpw = LB + (wi < LX ? 1 : 0), lane0 = wi * LB + (wi < LX ? wi : LX);   // this warp's lanes of the chunk
+    const bool issues = lane < lpw;
+    const int lrow = 4 * (lane0 + (issues ? lane : 0));
+    const bool tx_lead = lane == 0 && wi == 0;
     int nx[4] = {0, 0, 0, 0};          // token ids of the next tile's rows lrow..lrow+3
     auto load_tok = [&](int ti) {
       if (ti < 0) return;
