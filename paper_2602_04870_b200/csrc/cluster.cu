@@ -87,62 +87,78 @@ __device__ int block_exclusive_scan_1024(int v, int* s_warp, int* total) {
 // token window of the head across many experts: every sub-token row gathered for them is re-read
 // by its other top-k experts while it is still in L2.
 // One CTA per head: the global tile / chunk bases of head h are the totals of heads < h, which the
-// CTA recomputes itself from `counts` (H*N_e values), so the heads scan in parallel.
-__global__ void __launch_bounds__(1024)
+// CTA recomputes itself from `counts` (H*N_e values), so the heads scan in parallel.  Warp p scans
+// tile part p over the experts (32 experts per step, carry in a register) and warp 0 the padded
+// segment lengths: one barrier in all (the former 1024-thread block scans, one per part and 32
+// experts, took 10 us at paper scale, most of it in __syncthreads).
+__device__ __forceinline__ int warp_incl_scan(int v) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const int n = __shfl_up_sync(0xffffffffu, v, d);
+    if (lane >= d) v += n;
+  }
+  return v;
+}
+
+constexpr int kOffsetsThreads = 32 * kTileParts;
+__global__ void __launch_bounds__(kOffsetsThreads)
 offsets_kernel(const int32_t* __restrict__ counts, int32_t* __restrict__ off, int32_t* __restrict__ tbase,
                int32_t* __restrict__ ntiles, int H, int N_e, int max_tiles, int seg_align) {
-  __shared__ int s_warp[64];
-  __shared__ int s_tot;
+  __shared__ int s_red[2][kOffsetsThreads / 32];
+  __shared__ int s_ptot[kTileParts];
   const int TPS = seg_align / kExpertBM;                                 // tiles per alignment unit
-  const int h = blockIdx.x;
-  // tiles of all heads before h (and of all heads, for the total)
+  const int h = blockIdx.x, lane = threadIdx.x & 31, p = threadIdx.x >> 5;
+  auto units = [&](int c) { return (c + seg_align - 1) / seg_align; };  // alignment units of a segment
+  // tiles of all heads before h, and of all heads (order-independent integer sums)
   int t_before = 0, t_all = 0;
-  for (int i = threadIdx.x; i < H * N_e; i += blockDim.x) {
-    const int c = counts[i];
-    const int cp = (c + seg_align - 1) / seg_align * seg_align;
-    const int nt = cp / kExpertBM;
+  for (int i = threadIdx.x; i < H * N_e; i += kOffsetsThreads) {
+    const int nt = units(counts[i]) * TPS;
     if (i / N_e < h) t_before += nt;
     t_all += nt;
   }
-  // block reductions (order-independent integer sums)
-  auto block_sum = [&](int v) {
-    const int ex = block_exclusive_scan_1024(v, s_warp, &s_tot);
-    (void)ex;
-    const int t = s_tot;
-    __syncthreads();
-    return t;
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) {
+    t_before += __shfl_xor_sync(0xffffffffu, t_before, d);
+    t_all += __shfl_xor_sync(0xffffffffu, t_all, d);
+  }
+  if (lane == 0) { s_red[0][p] = t_before; s_red[1][p] = t_all; }
+  // part p's tile count over the experts
+  const int32_t* ch = counts + (size_t)h * N_e;
+  auto part_tiles = [&](int e) {
+    const int nu = units(ch[e]);
+    return TPS * ((p + 1) * nu / kTileParts - p * nu / kTileParts);
   };
-  int carry_t = block_sum(t_before);
-  const int tot_t = block_sum(t_all);
-  int carry_r = 0;
-  for (int p = 0; p < kTileParts; ++p) {
-    int carry_p = 0;
-    for (int base = 0; base < N_e; base += 1024) {
-      const int e = base + threadIdx.x;
-      const int c = (e < N_e) ? counts[(size_t)h * N_e + e] : 0;
-      const int nu = (c + seg_align - 1) / seg_align;                   // alignment units of e
-      const int np = TPS * ((p + 1) * nu / kTileParts - p * nu / kTileParts);   // tiles in part p
-      const int px = block_exclusive_scan_1024(np, s_warp, &s_tot);
-      const int ptot = s_tot;
-      __syncthreads();
-      if (e < N_e) tbase[((size_t)h * kTileParts + p) * N_e + e] = carry_t + carry_p + px;
-      carry_p += ptot;
+  int ptot = 0;
+  for (int e = lane; e < N_e; e += 32) ptot += part_tiles(e);
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) ptot += __shfl_xor_sync(0xffffffffu, ptot, d);
+  if (lane == 0) s_ptot[p] = ptot;
+  __syncthreads();
+  int carry = 0, tot_t = 0;
+  for (int w = 0; w < kOffsetsThreads / 32; ++w) { carry += s_red[0][w]; tot_t += s_red[1][w]; }
+  for (int q = 0; q < p; ++q) carry += s_ptot[q];
+  // tbase[h][p][e] = tiles of earlier heads + earlier parts of this head + this part's earlier experts
+  for (int b = 0; b < N_e; b += 32) {
+    const int e = b + lane;
+    const int v = e < N_e ? part_tiles(e) : 0;
+    const int incl = warp_incl_scan(v);
+    if (e < N_e) tbase[((size_t)h * kTileParts + p) * N_e + e] = carry + incl - v;
+    carry += __shfl_sync(0xffffffffu, incl, 31);
+  }
+  if (p == 0) {   // padded segment offsets of this head
+    int carry_r = 0;
+    for (int b = 0; b < N_e; b += 32) {
+      const int e = b + lane;
+      const int cp = e < N_e ? units(ch[e]) * seg_align : 0;
+      const int incl = warp_incl_scan(cp);
+      if (e < N_e) off[(size_t)h * (N_e + 1) + e] = carry_r + incl - cp;
+      carry_r += __shfl_sync(0xffffffffu, incl, 31);
     }
-    carry_t += carry_p;
-  }
-  for (int base = 0; base < N_e; base += 1024) {
-    const int e = base + threadIdx.x;
-    const int c = (e < N_e) ? counts[(size_t)h * N_e + e] : 0;
-    const int cp = (c + seg_align - 1) / seg_align * seg_align;         // padded segment length
-    const int rx = block_exclusive_scan_1024(cp, s_warp, &s_tot);
-    const int rtot = s_tot;
-    __syncthreads();
-    if (e < N_e) off[(size_t)h * (N_e + 1) + e] = carry_r + rx;
-    carry_r += rtot;
-  }
-  if (threadIdx.x == 0) {
-    off[(size_t)h * (N_e + 1) + N_e] = carry_r;
-    if (h == 0) *ntiles = min(tot_t, max_tiles);
+    if (lane == 0) {
+      off[(size_t)h * (N_e + 1) + N_e] = carry_r;
+      if (h == 0) *ntiles = min(tot_t, max_tiles);
+    }
   }
 }
 
@@ -418,7 +434,7 @@ void launch_cluster(int H, int64_t T, int k, int N_e, const int32_t* idx, const 
   tile_prefix_kernel<<<dim3(N_e, H), 256, 0, s>>>(hist, tilepref, counts, n_rt, N_e);
   // tile bases [H][kTileParts][N_e] live in the (otherwise unused here) tail of tilepref's scratch
   int32_t* tbase = tilepref + (size_t)H * n_rt * N_e;
-  offsets_kernel<<<H, 1024, 0, s>>>(counts, off, tbase, ntiles, H, N_e, max_tiles, seg_align);
+  offsets_kernel<<<H, kOffsetsThreads, 0, s>>>(counts, off, tbase, ntiles, H, N_e, max_tiles, seg_align);
   if (dw_parts > 0)
     dw_parts_kernel<<<H, 1024, 0, s>>>(off, H, N_e, dw_parts, chunks, max_chunks, nchunks, cbase, ccount, pbase, pcount);
   tiles_kernel<<<(H * N_e + 7) / 8, 256, 0, s>>>(counts, off, tbase, tiles, max_tiles, H, N_e, Rp, perm, tok_s,
