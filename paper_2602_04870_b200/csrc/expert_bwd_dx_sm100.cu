@@ -1002,7 +1002,7 @@ bool launch_t(const Routing& rt, const void* Xs, int64_t ldx, const void* dY, in
     TraceBuf tb{trace_buffer(s), 0};
     cudaMemcpyToSymbolAsync(g_trace_dx, &tb, sizeof(tb), 0, cudaMemcpyHostToDevice, s);
   }
-  static const int dbg = getenv("MHL_DX_DBG") ? atoi(getenv("MHL_DX_DBG")) : 0;
+  static const int dbg = timing_only_switch("MHL_DX_DBG");
   if (rt.seg_align % (2 * kExpertBM) == 0 && num_sms >= 2) {   // MHL_FLAG_PAIR: CTA-pair variant
     // CTA-pair variant: W maps with half-height boxes (each CTA loads its d_e/2 rows)
     CUtensorMap w1h, w2h;

@@ -470,7 +470,7 @@ bool launch_t(const Routing& rt, const void* Xs, int64_t ldx, const void* dY, in
     TraceBuf tb{trace_buffer(s), 0};
     cudaMemcpyToSymbolAsync(g_trace_fb, &tb, sizeof(tb), 0, cudaMemcpyHostToDevice, s);
   }
-  static const int dbg = getenv("MHL_FB_DBG") ? atoi(getenv("MHL_FB_DBG")) : 0;   // A/B: 1 no dH/gA, 2 no dX stores
+  static const int dbg = timing_only_switch("MHL_FB_DBG");   // A/B: 1 no dH/gA, 2 no dX stores
   k<<<num_sms, FL<DH, DE>::THREADS, FL<DH, DE>::BYTES, s>>>(w1m, w2m, gxm, gym, hsm, rt, dg, (uint8_t*)dH, (uint8_t*)gA,
                                                            (uint8_t*)dXrep, dbg);
   if (trace_path) {

@@ -491,7 +491,7 @@ bool launch_t(const Routing& rt, const void* Xs, int64_t ldx, const void* W1, co
     TraceBuf tb{tbuf, 0};
     cudaMemcpyToSymbolAsync(g_trace_fwd, &tb, sizeof(tb), 0, cudaMemcpyHostToDevice, s);
   }
-  static const int xdbg = getenv("MHL_F5_XDBG") ? atoi(getenv("MHL_F5_XDBG")) : 0;   // A/B only (wrong results)
+  static const int xdbg = timing_only_switch("MHL_F5_XDBG");   // A/B only (wrong results)
   kern<<<num_sms, kThreads, FwdL<DH, DE>::BYTES, s>>>(w1m, w2m, ym, xm, rt, xdbg);
   if (trace_path) {
     TraceBuf tb{nullptr, 0};

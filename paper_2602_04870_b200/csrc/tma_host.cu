@@ -50,6 +50,13 @@ void trace_dump(const char* path, cudaStream_t s) {
   free(h);
 }
 
+int timing_only_switch(const char* name) {
+  const char* e = getenv(name);
+  const int v = e ? atoi(e) : 0;
+  if (v != 0) fprintf(stderr, "[mhlmoe] timing-only A/B switch %s=%d is set: kernel results are NOT valid\n", name, v);
+  return v;
+}
+
 int store_lsu(int def) {
   static const char* e = getenv("MHL_STORE_TMA");
   return e ? (atoi(e) ? 0 : 1) : def;

@@ -16,6 +16,9 @@ bool make_tmap_2d_bf16(CUtensorMap* map, const void* base, uint64_t rows, uint64
 // with st.global (1.39 -> 1.30 ms); the GELU-heavy forward and the dX GEMM lose (0.87 -> 1.00,
 // 0.59 -> 0.65 ms).  `def` is the kernel's default; MHL_STORE_TMA=0/1 overrides all kernels.
 int store_lsu(int def);
+// value of a timing-only A/B environment switch (0 when unset); a nonzero value, which makes a
+// kernel skip work and so produce invalid results, is reported on stderr
+int timing_only_switch(const char* name);
 
 // Event-trace profiling aid (see sm100.cuh trace_ev): a zeroed device buffer of kTraceSlots
 // slots, and a dump of the non-zero slots "event tile clock" to a text file.
