@@ -44,7 +44,10 @@ struct MyChunks {
     return c++;
   }
 };
-constexpr int kDwProd = 8;                     // producer warps 0..kDwProd-1
+#ifndef MHL_DW_PROD
+#define MHL_DW_PROD 16
+#endif
+constexpr int kDwProd = MHL_DW_PROD;           // producer warps 0..kDwProd-1 (8, or 16: half chunks)
 constexpr int kDwFlush0 = kDwProd;             // 8 flush warps
 constexpr int kDwMma = kDwProd + 8;
 constexpr int kDwThreads = (kDwMma + 1) * 32;
@@ -94,15 +97,23 @@ expert_dw_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant
   const uint32_t tmem = *s_tmem;
   const int nchunks = *rt.nchunks;
 
+  // 16 producers: the launch cap falls to 72 registers; producers hand registers to the flush warps
+  // (warpgroup-aligned roles: producers 0-15, flush 16-23): 16*(72-40) >= 8*(88-72)
+  constexpr bool kRegs = kDwProd == 16;
   if (warp < kDwProd) {
+    if constexpr (kRegs) asm volatile("setmaxnreg.dec.sync.aligned.u32 40;");
     // ================================================================ producers
     // A step needs 2*XK gathered 64-column chunks (X, dY: pair p -> operand p / XK, column block
     // p % XK) and 2*EK contiguous chunks (dH, gA).  Warp w takes pairs w, w + kDwProd, ...; in a
     // pair, lane g (mod 16) issues one gather4 for rows 4g..4g+3.
     constexpr int NP = 2 * XK, NT = 2 * EK;
-    const int g = lane & 15;
+    // more producer warps than chunks: WPCH warps share a chunk, warp w its rows [sub*RW, (sub+1)*RW)
+    constexpr int WPCH = kDwProd > NP ? kDwProd / NP : 1, RW = kHalf / WPCH;
+    const int sub = warp % WPCH;
+    const int g = WPCH > 1 ? (sub * RW) / 4 + (lane & (RW / 4 - 1)) : (lane & 15);   // this lane's row group
     int mybytes = 0;
-    for (int p = warp; p < NP; p += kDwProd) mybytes += kHalf * 128;
+    if constexpr (WPCH > 1) mybytes += RW * 128;
+    else for (int p = warp; p < NP; p += kDwProd) mybytes += kHalf * 128;
     for (int t = warp; t < NT; t += kDwProd) mybytes += kHalf * 128;
     int n = 0;                                                // steps of this CTA so far
     // X / dY rows are re-gathered by the head's other experts (keep them in L2); dH / gA stream
@@ -129,10 +140,17 @@ expert_dw_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant
           }
         }
         __syncwarp();
-        for (int u = lane; u < ((NP - warp + kDwProd - 1) / kDwProd) * 16; u += 32) {
-          const int p = warp + (u >> 4) * kDwProd, kb = p % XK;
-          tma_gather4_hint(base + (p < XK ? L::X : L::DY) + kb * kHalf * 128 + 4 * g * 128, p < XK ? &xmap : &ymap,
-                           ch.head * DH + kb * 64, r0, r1, r2, r3, &full[st], pol_keep);
+        if constexpr (WPCH > 1) {
+          const int p = warp / WPCH, kb = p % XK;
+          if (lane < RW / 4)
+            tma_gather4_hint(base + (p < XK ? L::X : L::DY) + kb * kHalf * 128 + 4 * g * 128, p < XK ? &xmap : &ymap,
+                             ch.head * DH + kb * 64, r0, r1, r2, r3, &full[st], pol_keep);
+        } else {
+          for (int u = lane; u < ((NP - warp + kDwProd - 1) / kDwProd) * 16; u += 32) {
+            const int p = warp + (u >> 4) * kDwProd, kb = p % XK;
+            tma_gather4_hint(base + (p < XK ? L::X : L::DY) + kb * kHalf * 128 + 4 * g * 128, p < XK ? &xmap : &ymap,
+                             ch.head * DH + kb * 64, r0, r1, r2, r3, &full[st], pol_keep);
+          }
         }
         r0 = q0; r1 = q1; r2 = q2; r3 = q3;
         if (s + 2 < nsteps) {
@@ -175,6 +193,7 @@ expert_dw_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant
       }
     }
   } else if (warp >= kDwFlush0 && warp < kDwFlush0 + 8) {
+    if constexpr (kRegs) asm volatile("setmaxnreg.inc.sync.aligned.u32 88;");
     // ================================================================ flush: partial[ci][mat][f][c]
     // Each chunk's accumulators go to its partial slot; the CTA that flushes an expert's LAST chunk
     // (counted with one atomic per chunk) then sums that expert's partials in chunk order and
