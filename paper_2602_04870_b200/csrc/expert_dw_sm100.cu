@@ -27,8 +27,11 @@ using namespace sm100;
 // 64-row steps; 8 warps flush each chunk's fp32 accumulators to its partial slot; the last warp
 // issues the MMAs (+ owns TMEM).  The ring keeps filling while a chunk is flushed.
 // =============================================================================================
-constexpr int kHalf = kDwStep;   // rows per pipeline step
-static_assert(kHalf == 64, "dW pipeline step");
+#ifndef MHL_DW_STEP
+#define MHL_DW_STEP 32
+#endif
+constexpr int kHalf = MHL_DW_STEP;   // rows per pipeline step (chunk boundaries stay kDwStep-aligned)
+static_assert((kHalf == 64 || kHalf == 32 || kHalf == 16) && kDwStep % kHalf == 0, "dW pipeline step");
 
 // The chunks of this CTA: part blockIdx.x of every head (cluster.cu dw_parts_kernel), in order.
 struct MyChunks {
@@ -57,7 +60,7 @@ struct DwSmem {
   static constexpr int XB = kHalf * DH * 2, EB = kHalf * DE * 2;
   static constexpr int STAGE = 2 * XB + 2 * EB;                      // X, dY, dH, gA
   static constexpr int X = 0, DY = XB, DHH = 2 * XB, GA = 2 * XB + EB;
-  static constexpr int S = 2;
+  static constexpr int S = 2 * (64 / kHalf);      // 192 KB of stages either way
   static constexpr int BAR = S * STAGE;            // full[S], empty[S], accfull, accempty
   static constexpr int LAST = BAR + 8 * (2 * S + 2);            // int: "this CTA reduces the expert"
   static constexpr int TMEM = LAST + 16;
