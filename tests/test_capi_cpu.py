@@ -156,3 +156,17 @@ def test_require_tc_flag_refuses_simt_fallback_shapes():
             assert C.STATUS[e.status] == "MHL_ERR_UNSUPPORTED"
         else:
             raise AssertionError((d_h, N_e, k, d_e, dt))
+
+
+def test_bwd_fused_flag_matches_header_and_is_accepted():
+    """MHL_FLAG_BWD_FUSED (the one-kernel expert backward input side) is the header's value and a
+    plan query accepts it on a supported and on an unsupported shape (the latter falls back to the
+    two-kernel path, which mhl_kernel_paths reports on the GPU)."""
+    import re
+    from paper_2602_04870_b200 import mhlmoe as C
+    hdr = open(os.path.join(ROOT, "include", "mhlmoe.h")).read()
+    m = re.search(r"#define MHL_FLAG_BWD_FUSED (\d+)u", hdr)
+    assert m and int(m.group(1)) == C.MHL_FLAG_BWD_FUSED
+    assert C.PATHS["expert_bwd_fused"] == 1 << 15 and "MHL_PATH_EXPERT_BWD_FUSED (1u << 15)" in hdr
+    for d_e in (128, 256):   # 2 d_e + d_h <= 512 only for d_e = 128
+        C.hp_plan_query(C.make_config(1024, 512, 2, 256, 64, 8, d_e, "bf16", 1, 0, C.MHL_FLAG_BWD_FUSED))
