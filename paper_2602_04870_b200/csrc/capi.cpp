@@ -246,10 +246,10 @@ mhl_status make_dims(const mhl_config* c, Dims* m) {
   if (m->Rp >= (int64_t)1 << 31) return fail(MHL_ERR_UNSUPPORTED, "T_glob * k + N_e * seg_align must be < 2^31");
   m->rank = loop ? 0 : c->rank;
   m->n_rt = (int)((m->T_g + mhl::kRouterTile - 1) / mhl::kRouterTile);
-  // router-backward partials: one per router tile on the SIMT path, at most one per (SM / N_h) on
-  // the tcgen05 path (launch: min(n_rt, #SMs / N_h) chunks per head)
+  // router-backward partials: one per router tile on the SIMT path, at most 2 * 148 / N_h per head on
+  // the tcgen05 path (two CTAs per SM; a constant, not the device's SM count: dW_r bits stay fixed)
   m->n_rbwd = (!m->simt && mhl::router_bwd_sm100_supported(m->d_h, m->N_e, m->k))
-                  ? std::min(m->n_rt, std::max(1, mhl::kDwParts / m->N_h)) : m->n_rt;
+                  ? std::min(m->n_rt, std::max(1, 2 * mhl::kDwParts / m->N_h)) : m->n_rt;
   const int64_t mt = (int64_t)m->H * ((m->R + mhl::kExpertBM - 1) / mhl::kExpertBM + 2 * m->N_e);
   if (mt >= (int64_t)1 << 31) return fail(MHL_ERR_UNSUPPORTED, "too many tiles");
   m->max_tiles = (int)mt;

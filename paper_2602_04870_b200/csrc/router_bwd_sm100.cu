@@ -38,7 +38,9 @@ struct RbL {
   static constexpr int BT = NE * 128;                        // one K-major bf16 plane: NE rows x 64 tokens
   static constexpr int BBUF = 2 * BT;                        // hi + lo
   static constexpr int XS_RAW = (220 * 1024 - 2 * BBUF) / XSTAGE;
-  static constexpr int XS = XS_RAW > 6 ? 6 : XS_RAW;
+  // two X stages: ~97 KB of smem at d_h = 256, N_e = 64, so two CTAs share an SM (the builders'
+  // per-step chain is latency-bound; one 6-warp CTA per SM left 91 % of the warp slots empty)
+  static constexpr int XS = XS_RAW > 2 ? 2 : XS_RAW;
   static constexpr int X = 0, B = XS * XSTAGE, BAR = B + 2 * BBUF;
   static constexpr int NBAR = 2 * XS + 5;                    // xfull[XS], xempty[XS], bfull[2], bempty[2], acc
   static constexpr int TMEMP = BAR + NBAR * 8;
@@ -51,7 +53,7 @@ struct RbL {
 };
 
 template <int DH, int NE, int KMAX>
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(kThreads, 2)
 router_bwd_sm100_kernel(const __grid_constant__ CUtensorMap xmap, const int32_t* __restrict__ idx,
                         const float* __restrict__ gate, const float* __restrict__ dg, int64_t T, int k, int nc,
                         int N_e, float* __restrict__ dS, float* __restrict__ partial) {
