@@ -30,7 +30,10 @@ constexpr int kChunkBytes = RT * 128;   // one 64-column K-chunk of the X tile
 template <int DH, int NE>
 struct RSmem {
   // epilogue warpgroups (each owns every kEG-th tile of the CTA); fewer when the W planes fill smem
-  static constexpr int kEG = NE <= 64 ? 3 : 2;
+#ifndef MHL_ROUTER_EG
+#define MHL_ROUTER_EG 3
+#endif
+  static constexpr int kEG = NE <= 64 ? MHL_ROUTER_EG : 2;
   static constexpr int THREADS = (2 + 4 * kEG) * 32;
   static constexpr int kNB = (2 * kEG * NE <= 512) ? 2 * kEG : 512 / NE;   // TMEM accumulator buffers
   static_assert(kNB >= kEG, "router: fewer TMEM buffers than epilogue warpgroups");
