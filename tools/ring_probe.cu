@@ -4,6 +4,8 @@
 //   mech 0: cp.async 16 B per lane + cp.async.mbarrier.arrive.noinc
 //   mech 1: TMA tile::gather4 issued by lane 0 of each producer warp
 //   mech 2: plain 16 B loads to registers, st.shared, mbarrier arrive (2-chunk software pipeline)
+//   mech 7: mech 6's gathers, and the consumer writes every chunk back out with a 16 KB bulk store
+//           (equal bytes in and out per tile, F5's traffic shape); TB/s counts in + out
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <cuda_runtime.h>
@@ -31,14 +33,14 @@ __device__ __forceinline__ uint32_t kmaj(int r, int c) { return r * 128 + ((((c 
 constexpr int kChunk = 16384;
 __global__ void __launch_bounds__(1024, 1)
 ring(const __grid_constant__ CUtensorMap map, const uint16_t* __restrict__ x, int ld, const int* __restrict__ rows,
-     int ntiles, int S, int PW, int mech, int* sink) {
+     int ntiles, int S, int PW, int mech, int* sink, char* out) {
   extern __shared__ __align__(1024) uint8_t smem[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + S * kChunk);
   uint64_t* empty = full + 16;
   int* stok = reinterpret_cast<int*>(empty + 16);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (tid == 0) {
-    for (int i = 0; i < S; ++i) { mbar_init(&full[i], mech == 5 ? 32 : (mech == 4 || mech == 6) ? 1 : (mech == 1 || mech == 3) ? PW : 32 * PW); mbar_init(&empty[i], 1); }
+    for (int i = 0; i < S; ++i) { mbar_init(&full[i], mech == 5 ? 32 : (mech == 4 || mech == 6 || mech == 7) ? 1 : (mech == 1 || mech == 3) ? PW : 32 * PW); mbar_init(&empty[i], 1); }
     asm volatile("fence.mbarrier_init.release.cluster;");
   }
   __syncthreads();
@@ -70,7 +72,7 @@ ring(const __grid_constant__ CUtensorMap map, const uint16_t* __restrict__ x, in
         }
       }
     }
-  } else if (mech == 6 && warp < PW) {
+  } else if ((mech == 6 || mech == 7) && warp < PW) {
     // chunk c -> stage c % S, filled by the warp pair (c % (PW/2)): each warp of the pair gathers
     // 64 of its 128 rows with 16 lanes (one gather4 per lane); stage ownership is fixed when S is a
     // multiple of PW/2, so the EMPTY parity never aliases
@@ -166,9 +168,17 @@ ring(const __grid_constant__ CUtensorMap map, const uint16_t* __restrict__ x, in
       for (int kb = 0; kb < 4; ++kb) {
         mbar_wait(&full[st], fph[st]); fph[st] ^= 1;
         acc += smem[st * kChunk + 5];
+        if (mech == 7) {   // write the chunk out (contiguous, like Yrep), release the stage once read
+          char* dst = out + ((size_t)t * 4 + kb) * kChunk;
+          asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst),
+                       "r"(sb + st * kChunk), "r"(kChunk) : "memory");
+          asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+          asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+        }
         mbar_arrive(&empty[st]);
         if (++st == S) st = 0;
       }
+    if (mech == 7) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
     if (acc == 123456789) *sink = acc;
   }
 }
@@ -201,23 +211,25 @@ int main(int argc, char** argv) {
       CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   const int ntiles = (int)(n / 128) * 8;   // every head of every clustered tile: 2.1 GB gathered
   char* flush; cudaMalloc(&flush, 512 << 20);
+  char* out; cudaMalloc(&out, (size_t)ntiles * 4 * 16384);
   cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
   for (int mech : mechs)
     for (int PW : {4, 8})
       for (int S : {4, 6, 8, 12}) {
-        if (mech == 6 ? S < PW / 2 : S % PW) continue;   // mech 6: any S >= owners (parity argument)
+        if ((mech == 6 || mech == 7) ? S < PW / 2 : S % PW) continue;   // mech 6/7: any S >= owners
         const int smem = S * kChunk + 2048;
         cudaFuncSetAttribute(ring, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         float tot = 0;
         for (int it = 0; it < 3; ++it) {
           cudaMemset(flush, it, 512 << 20);
           cudaEventRecord(a);
-          ring<<<148, 32 * (PW + 1), smem>>>(map, x, 2048, rows, ntiles, S, PW, mech, sink);
+          ring<<<148, 32 * (PW + 1), smem>>>(map, x, 2048, rows, ntiles, S, PW, mech, sink, out);
           cudaEventRecord(b); cudaEventSynchronize(b);
           float ms; cudaEventElapsedTime(&ms, a, b); if (it) tot += ms;
         }
         cudaError_t e = cudaGetLastError();
-        printf("mech %d PW %2d S %2d: %.3f ms  %.2f TB/s  %s\n", mech, PW, S, tot / 2, ntiles * 65536.0 / (tot / 2) / 1e9,
+        const double bytes = ntiles * 65536.0 * (mech == 7 ? 2 : 1);   // gathered (+ stored)
+        printf("mech %d PW %2d S %2d: %.3f ms  %.2f TB/s  %s\n", mech, PW, S, tot / 2, bytes / (tot / 2) / 1e9,
                e == cudaSuccess ? "" : cudaGetErrorString(e));
       }
   return 0;
