@@ -69,6 +69,15 @@ def load_peaks():
     return (hbm or FALLBACK_PEAKS["hbm_gbs"], hbm_src), (tf or FALLBACK_PEAKS["bf16_tflops"], tf_src)
 
 
+def load_probe_ceiling():
+    """The SM data-movement ceiling for the expert kernels' traffic mix (gathered rows in, rows out),
+    measured without compute by tools/ring_probe.cu (profiles/probe_ceilings.json), or None."""
+    try:
+        return json.load(open(os.path.join(ROOT, "profiles", "probe_ceilings.json")))
+    except Exception:
+        return None
+
+
 def load_traffic():
     """Per-launch DRAM bytes (read + write) of each span's kernel from the committed ncu --set full
     captures (profiles/ncu_traffic.json, written by tools/ncu_summary.py), or {}."""
@@ -176,10 +185,17 @@ def step_work(cfg, T_loc, G, fused_bwd=False):
         "B1_proj_in_bwd": dict(flops=4 * T_loc * d * Din,
                                bytes=T_loc * Din * el + Din * d * el + 2 * T_loc * d * el + Din * d * 4),
     }
+    # bytes each expert kernel moves between L2 and the SMs (gathered rows once per replica, tiles
+    # loaded, rows stored): the "data movement" the ring probe's ceiling is measured for
+    w["F5_expert_fwd"]["sm_bytes"] = 2 * rep * row
+    w["B5_expert_bwd_dx"]["sm_bytes"] = 2 * rep * row + 2 * rep * erow
+    w["B5_expert_dx_gemm"]["sm_bytes"] = rep * erow + rep * row
+    w["B5_expert_bwd_dw"]["sm_bytes"] = 2 * rep * row + 2 * rep * erow
     if fused_bwd:
         # H, dA' and dXrep = dH W1 (3 units); dH, gA and the per-replica dXrep written: impl
         w["B5_expert_bwd_dx"] = dict(flops=3 * unit, bytes=2 * subtok * row + 2 * wexp + rep * 12 + rep * 4,
-                                     impl_bytes=2 * rep * erow + rep * row)
+                                     impl_bytes=2 * rep * erow + rep * row,
+                                     sm_bytes=2 * rep * row + 2 * rep * erow + rep * row)
         del w["B5_expert_dx_gemm"]
         w["B6_combine_bwd"]["bytes"] += rep * 8 + H * N_e * d_h * 4   # dS, expert ids, W_r^T
     for v in w.values():
@@ -528,6 +544,13 @@ def main():
             et = sum(per_step[k] for k in ek) / 1e3
             roof["expert_kernels"] = {"flops": ef, "ms": et * 1e3, "tflops": ef / et / 1e12,
                                       "frac_of_peak": ef / et / 1e12 / tf_peak}
+            probe = load_probe_ceiling()
+            sb = sum(work[k].get("sm_bytes", 0) for k in ek)
+            if probe and sb:
+                ceil = probe["gather_store_TBps"]
+                roof["expert_kernels"]["data_movement"] = {
+                    "sm_bytes": sb, "achieved_TBps": sb / et / 1e12, "ceiling_TBps": ceil,
+                    "frac": sb / et / 1e12 / ceil, "ceiling_source": probe["source"]}
     breakdown = {k: round(v, 4) for k, v in sorted(per_step.items(), key=lambda kv: -kv[1])}
     layer_tflops = total_flops(cfg, T_loc) / (ms_per_step / 1e3) / 1e12
 
