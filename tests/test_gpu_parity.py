@@ -407,6 +407,30 @@ def test_routing_tokens_match_oracle(simt, G):
             np.testing.assert_array_equal(g2[key], g[key], err_msg=key)
 
 
+@pytest.mark.parametrize("G", [1, 2])
+def test_fused_bwd_with_routing_tokens_and_fallback_shapes(G):
+    """MHL_FLAG_BWD_FUSED with separate routing sub-tokens: the fused kernel's dXrep rows carry no
+    router term, and B6 writes dX (plain k-row sum) and dR (router term alone) exactly as on the
+    default path — so dX, dR and every weight gradient equal the default path's bits (dx too: with
+    routing tokens the router term never enters the replica rows).  A d_e = 256 shape (2 d_e + d_h
+    > 512 TMEM columns) keeps the two-kernel path under the flag."""
+    _need_gpu()
+    cfg = LayerConfig("rtok_f", T=1000, d=256, N_h=2, d_h=128, N_e=64, k=4, d_e=64, dtype="bf16", routing_tokens=True)
+    W, x, dout = make_problem(cfg, 16, "exact")
+    g = _run_gpu(cfg, W, x, dout, G=G, bwd_fused=True)
+    assert "expert_bwd_fused" in g["paths"]
+    _compare(cfg, W, x, dout, g, dist="exact")
+    d = _run_gpu(cfg, W, x, dout, G=G)
+    for key in ("out", "dx", "dW_r", "dW1", "dW2", "dW_in", "idx"):
+        np.testing.assert_array_equal(g[key], d[key], err_msg=key)
+    if G == 1:
+        cfg2 = LayerConfig("de256", T=600, d=256, N_h=2, d_h=128, N_e=64, k=4, d_e=256, dtype="bf16")
+        W2, x2, dout2 = make_problem(cfg2, 17, "exact")
+        g2 = _run_gpu(cfg2, W2, x2, dout2, bwd_fused=True)
+        assert "expert_bwd_fused" not in g2["paths"] and "expert_bwd_tc" in g2["paths"]
+        _compare(cfg2, W2, x2, dout2, g2, dist="exact")
+
+
 def test_routing_tokens_scatter_bytes_double():
     _need_gpu()
     from paper_2602_04870_b200 import mhlmoe as C
