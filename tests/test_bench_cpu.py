@@ -46,3 +46,28 @@ def test_expert_spans_are_tensor_bound_and_intermediates_are_not_algorithmic():
         assert w[k]["impl_bytes"] > w[k]["bytes"]          # Yrep / dH / gA / dXrep counted apart
     # §8(d): expert_bwd 1.37 TFLOP implemented
     assert abs(5 * unit / 1e12 - 1.374) < 0.01
+
+
+def test_expert_data_movement_bytes_and_fused_accounting():
+    """`sm_bytes` (L2 <-> SM bytes of each expert kernel, the ring probe's unit): per replica row F5
+    moves X in and Yrep out, K1 X and dY in and dH, gA out, K2 dH in and dXrep out, dW X, dY, dH, gA
+    in; the fused input side replaces K1 + K2 (3 units, no dH re-read) and B6 gains the router
+    term's inputs."""
+    cfg = PRESETS["paper"]
+    rep = cfg.T * cfg.N_h * cfg.k
+    row, erow = cfg.d_h * 2, cfg.d_e * 2
+    w = bench.step_work(cfg, cfg.T, 1)
+    assert w["F5_expert_fwd"]["sm_bytes"] == 2 * rep * row
+    assert w["B5_expert_bwd_dx"]["sm_bytes"] == 2 * rep * (row + erow)
+    assert w["B5_expert_dx_gemm"]["sm_bytes"] == rep * (row + erow)
+    assert w["B5_expert_bwd_dw"]["sm_bytes"] == 2 * rep * (row + erow)
+    total = sum(w[k]["sm_bytes"] for k in ("F5_expert_fwd", "B5_expert_bwd_dx", "B5_expert_dx_gemm", "B5_expert_bwd_dw"))
+    assert abs(total / 1e9 - 20.4) < 0.1                       # 608 KB per 128-row tile
+    f = bench.step_work(cfg, cfg.T, 1, fused_bwd=True)
+    assert "B5_expert_dx_gemm" not in f
+    unit = 2 * rep * cfg.d_h * cfg.d_e
+    assert f["B5_expert_bwd_dx"]["flops"] == 3 * unit
+    assert f["B5_expert_bwd_dx"]["sm_bytes"] == 3 * rep * row + 2 * rep * erow
+    assert f["B6_combine_bwd"]["bytes"] > w["B6_combine_bwd"]["bytes"]
+    probe = bench.load_probe_ceiling()
+    assert probe is not None and 5.0 < probe["gather_store_TBps"] < 10.0
