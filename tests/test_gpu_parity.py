@@ -262,6 +262,22 @@ def test_all_tokens_to_one_expert():
     _compare(cfg, W, x, dout, g)
 
 
+@pytest.mark.parametrize("d_h,N_e,k,d_e", [(256, 64, 8, 128), (128, 64, 4, 64)])
+def test_tcgen05_seed_sweep_strict_rule(d_h, N_e, k, d_e):
+    """24 seeds per shape on the tensor-core path with the exact recipe (north_star's rule as stated:
+    indices bit-exact on every sub-token with margin >= 1e-3, gates within 1e-5, every output and
+    gradient slice within 2e-2), so a rare-input failure of any kernel has a chance to show."""
+    _need_gpu()
+    n_excl = n = 0
+    for seed in range(24):
+        cfg = LayerConfig("sweep", T=384 + 37 * seed, d=2 * d_h, N_h=2, d_h=d_h, N_e=N_e, k=k, d_e=d_e, dtype="bf16")
+        W, x, dout = make_problem(cfg, 1000 + seed, "exact")
+        g = _run_gpu(cfg, W, x, dout)
+        _, rt = _compare(cfg, W, x, dout, g, dist="exact", expect=TC_FWD | TC_BWD)
+        n_excl += rt.n_excl; n += rt.n
+    assert n_excl <= 0.05 * n, f"{n_excl} of {n} sub-tokens excluded by the margin rule"
+
+
 @pytest.mark.parametrize("T,k,skew,fused", [(1, 8, False, False), (127, 8, False, False), (129, 1, False, True),
                                              (700, 16, False, False), (600, 4, True, False), (600, 4, True, True)])
 def test_tcgen05_edge_cases_match_oracle(T, k, skew, fused):
