@@ -457,12 +457,12 @@ def test_routing_tokens_scatter_bytes_double():
     assert info1["a2a_bytes_per_peer"] == 2 * info0["a2a_bytes_per_peer"]
 
 
-def _full_size_run(cfg, dist="paper"):
+def _full_size_run(cfg, dist="paper", bwd_fused=False):
     from paper_2602_04870_b200.layer import MHLatentMoE, torch_dtype, weights_to_device
     W, x, dout = make_problem(cfg, 0, dist)
     td = torch_dtype(cfg.dtype)
     L = MHLatentMoE(cfg.T, cfg.d, cfg.N_h, cfg.d_h, cfg.N_e, cfg.k, cfg.d_e, cfg.dtype,
-                    routing_tokens=cfg.routing_tokens)
+                    routing_tokens=cfg.routing_tokens, bwd_fused=bwd_fused)
     Wd = weights_to_device(W, cfg.dtype)
     xd = torch.from_numpy(x).to("cuda", td)
     out, idx, gates = L.forward(xd, Wd, want_routing=True)
@@ -501,6 +501,31 @@ def test_full_size_sampled_rows_match_oracle(name, dist):
     gr = O.layer_backward(P, xs, ds, C)
     assert rel_err_slices(g["out"], C.out, SLICES["out"]) <= TOL["bf16"]
     assert rel_err_slices(g["dx"], gr["dx"], SLICES["dx"]) <= TOL["bf16"]
+
+
+def test_full_size_fused_backward_matches_oracle_and_default():
+    """The opt-in one-kernel expert backward at BASELINE's full paper-scale config: dx on sampled
+    tokens against the oracle, and dW1 / dW2 / dW_r bit-identical to the default two-kernel path
+    over all 65536 tokens (same dH, gA, dg arithmetic and the same dW kernel)."""
+    _need_gpu()
+    cfg = PRESETS["paper"]
+    W, x, dout, L, r = _full_size_run(cfg, "paper", bwd_fused=True)
+    assert "expert_bwd_fused" in L.paths()
+    rng = np.random.default_rng(8)
+    S = np.sort(np.concatenate([rng.choice(cfg.T, 40, replace=False), [0, cfg.T - 1]]))
+    P = {k: v.astype(np.float64) for k, v in W.items()}
+    xs, ds = x[S].astype(np.float64), dout[S].astype(np.float64)
+    C0 = O.layer_forward(P, xs, cfg.k, mode="bf16")
+    rt = check_routing(P, C0, r["idx"].cpu().numpy()[:, S], cfg.k, x=xs)
+    C = O.layer_forward(P, xs, cfg.k, mode="bf16", forced_idx=rt.forced)
+    gr = O.layer_backward(P, xs, ds, C)
+    assert rel_err_slices(r["dx"].float().cpu().numpy()[S], gr["dx"], SLICES["dx"]) <= TOL["bf16"]
+    fused = {k: r[k].float().cpu().numpy() for k in ("dW1", "dW2", "dW_r")}
+    del r, L
+    torch.cuda.empty_cache()
+    _, _, _, _, d = _full_size_run(cfg, "paper")
+    for k in ("dW1", "dW2", "dW_r"):
+        np.testing.assert_array_equal(fused[k], d[k].float().cpu().numpy(), err_msg=k)
 
 
 @pytest.mark.parametrize("h,experts", [(0, (3, 41)), (5, (0, 63))])
